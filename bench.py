@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the B200-native HH hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1, one rank per GPU)
+
+Metric (BASELINE.json): HH neuron-steps/s.  Workload at N = 1 is BASELINE
+config 2: a 10,000,000-neuron population with the custom Na / K_dr / leak /
+Ca_L / K_Ca channel set (6 gates, 5 channels, dt = 0.01 ms) driven by
+I = 2 * Poisson(2) for 10,000 steps, fp32.  One "step" of this benchmark is
+that whole simulation (1e11 neuron-steps): the device generates each
+100-step chunk of stimulus (Philox) and the fused forward kernel advances the
+population through it, writing the V trace and spike bitmap of the chunk
+(4.0 GB + 125 MB per chunk, far above L2, so no flush is needed).  Weak
+scaling: every rank owns its own 10M-neuron population (no collective on the
+data path; independent neurons).
+
+Extra keys: roofline (forward kernel vs the MUFU pipe peak measured live on
+this GPU by hhb_pipe_probe), cpu_baseline (reference algorithm on the host
+cores), e2e (the reference-facing `simulate` call with host numpy buffers),
+fwd_bwd (forward + BPTT throughput on the config-3 shaped layer), clocks,
+gpu_launches.  Only stdlib imports at module level: the CPU-baseline workers
+are spawned processes that re-import this file.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+METRIC = "HH neuron-steps/sec (fwd; fwd+bwd) at 1/2/4/8 B200 vs CPU ref, % roofline"
+UNIT = "neuron-steps/s"
+# MUFU (transcendental) operations per neuron-step of the config-2 channel set:
+# per gate 2 (1/(a+b), exp decay) + 1 per exp-form rate + 2 per linoid/sigmoid
+# rate; SURVEY.md §8 tau = 31.  Algorithmic HBM bytes per neuron-step of the
+# forward kernel: I read 4 + V write 4 + spike bit 1/8.
+TAU_C2 = 31
+BYTES_PER_NS = 8.125
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--neurons", type=int, default=10_000_000)
+    ap.add_argument("--sim-steps", type=int, default=10_000)
+    ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / fwd_bwd / cpu legs")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def c2_params(dtype):
+    sys.path.insert(0, ROOT)
+    from paper_2601_21407_b200.defaults import na_kdr_cal_kca_params
+    return na_kdr_cal_kca_params(dt=0.01).with_(dtype=dtype)
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_leg(seconds, n_total, dtype="float32"):
+    sys.path.insert(0, ROOT)
+    from oracle import cpu_baseline
+    from paper_2601_21407_b200.defaults import na_kdr_cal_kca_params
+    pdict = na_kdr_cal_kca_params(dt=0.01).to_dict()
+    return cpu_baseline.run(pdict, dtype=dtype, n_total=n_total, seconds=seconds)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    secs = max(2.0, args.cpu_seconds / 2)
+    for _ in range(args.warmup):
+        cpu_leg(min(secs, 2.0), 1 << 21)
+    tot_ns, tot_s, last = 0, 0.0, None
+    for _ in range(args.steps):
+        r = cpu_leg(secs, 1 << 21)
+        tot_ns += r["neuron_steps"]
+        tot_s += r["seconds"]
+        last = r
+    value = tot_ns / tot_s
+    sample = (f"reference hh_step loop (oracle port, fp32 mode) on {last['cores']} processes x "
+              f"{last['n_local']} neurons of the config-2 population, ~{secs:.0f} s per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_dict(args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args):
+    return {"workload": "BASELINE config 2: HH population, custom Na/K_dr/leak/Ca_L/K_Ca channels "
+                        "(6 gates), I = 2*Poisson(2), fp32 forward, V + spike trace recorded",
+            "neurons_per_gpu": args.neurons, "sim_steps": args.sim_steps, "dt_ms": 0.01,
+            "chunk_steps": args.chunk, "parallelism": f"neuron-shard x{args.gpus} (weak, no collective)",
+            "l2": "inputs/outputs per chunk (4 GB) exceed the 126 MB L2; no flush needed"}
+
+
+# --------------------------------------------------------------------------- GPU legs
+def probe_mufu_peak(torch, nat, dev):
+    """MUFU ex2 throughput of this GPU, ops/s (live roofline denominator)."""
+    import ctypes as C
+    sink = torch.zeros(1, device=dev)
+    ops = C.c_int64(0)
+    lib = nat.load()
+    for _ in range(2):
+        nat.check(lib.hhb_pipe_probe(0, 2000, sink.data_ptr(), C.byref(ops), None), "probe")
+    torch.cuda.synchronize()
+    best = 0.0
+    for which in (0, 2):
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nat.check(lib.hhb_pipe_probe(which, 20000, sink.data_ptr(), C.byref(ops),
+                                         torch.cuda.current_stream().cuda_stream), "probe")
+            e1.record()
+            e1.synchronize()
+            best = max(best, ops.value / (e0.elapsed_time(e1) * 1e-3)) if which == 0 else best
+    return best
+
+
+def e2e_leg(torch, args, params, rank):
+    """Reference-facing call with host buffers: dynamics.simulate(numpy) on the
+    full population for a bounded number of steps (H2D of I, D2H of the
+    float64 V trace and bool spikes inside the timed region)."""
+    import numpy as np
+    from paper_2601_21407_b200 import dynamics as Dy
+    n, T = args.neurons, args.e2e_steps
+    rng = np.random.default_rng(rank)
+    i_host = (2.0 * rng.poisson(2.0, size=(T, n))).astype(np.float32)
+    Dy.simulate(params, i_host[:2])            # warm-up (allocator, module)
+    torch.cuda.synchronize()
+    reps = 2
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        tr = Dy.simulate(params, i_host)
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / reps
+    h2d = i_host.nbytes
+    d2h = tr.v_series.nbytes + tr.spike_series.nbytes
+    return {"value": n * T / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "seconds_per_step": el,
+            "sample": f"simulate(numpy float32 I[{T}, {n}]) -> Trace(float64 V, bool spikes)"}
+
+
+def fwd_bwd_leg(torch, dev):
+    """Forward + BPTT (backward_through_time, full storage) on the config-3
+    shaped HH layer: RS neurons, 256 x 1024, 100 steps, fp32, device tensors."""
+    import numpy as np
+    from paper_2601_21407_b200 import adjoint as A
+    from paper_2601_21407_b200 import defaults as DF
+    from paper_2601_21407_b200 import dynamics as Dy
+    p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
+    B, N, T = 256, 1024, 100
+    g = torch.Generator(device=dev).manual_seed(0)
+    i = 7.8 + 3.0 * torch.randn((T, B, N), device=dev, generator=g)
+    sv = torch.randn((T, B, N), device=dev, generator=g) * 1e-4
+    s0 = Dy.init_state(p, (B, N), device=dev)
+    for _ in range(2):
+        A.backward_through_time(p, s0, i, sv)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        A.backward_through_time(p, s0, i, sv)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "config": "RS layer 256x1024 neurons, 100 steps, fp32, forward + full-storage BPTT "
+                      "(one unit = one neuron-step through forward and backward)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_2601_21407_b200 import _native as nat
+    from paper_2601_21407_b200.population import Population, PoissonCurrent
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    nat.load()
+
+    params = c2_params(np.float32)
+    pop = Population(params, args.neurons, chunk=args.chunk, device=dev, neuron_base=rank * args.neurons)
+    stim = PoissonCurrent(2.0, 2.0, seed=1234)
+
+    # warm-up: W full passes
+    for _ in range(args.warmup):
+        pop.reset()
+        pop.advance(stim, args.sim_steps)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    events = []
+    step_ev = []
+    launches0 = pop.launches
+    for _ in range(args.steps):
+        pop.reset()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        pop.advance(stim, args.sim_steps, events=events)
+        s1.record()
+        step_ev.append((s0, s1))
+    torch.cuda.synchronize()
+    launches = pop.launches - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    from paper_2601_21407_b200.dynamics import _raise_if_bad
+    _raise_if_bad(pop.first_bad)
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    total_ms = sum(step_ms)
+    fwd_ms = sum(e1.elapsed_time(e2) for _, e1, e2 in events)
+    stim_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in events)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+
+    ns_per_rank = args.neurons * args.sim_steps * args.steps
+    value = ns_per_rank * world / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (hhb_forward), from its own events
+    n_fwd = len(events)
+    fwd_avg_s = fwd_ms * 1e-3 / n_fwd
+    ns_per_launch = args.neurons * args.chunk
+    mufu_peak = probe_mufu_peak(torch, nat, dev)
+    achieved = TAU_C2 * ns_per_launch / fwd_avg_s
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k_forward_dram.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9, "unit": "Gop/s",
+            "frac": achieved / mufu_peak, "traffic": traffic,
+            "kernel": "k_forward<float,6,4> (hhb_forward)",
+            "algorithmic": f"{TAU_C2} MUFU ops per neuron-step x {ns_per_launch} neuron-steps per launch",
+            "peak_source": "measured live: hhb_pipe_probe MUFU.EX2 throughput on this GPU",
+            "avg_launch_ms": fwd_avg_s * 1e3, "share_of_step": fwd_ms / sum(step_ms),
+            "hbm": {"achieved_gbs": BYTES_PER_NS * ns_per_launch / fwd_avg_s / 1e9,
+                    "peak_gbs": hbm_peak, "frac": BYTES_PER_NS * ns_per_launch / fwd_avg_s / 1e9 / hbm_peak,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}}
+
+    extras = {}
+    if not args.no_extras:
+        extras["e2e"] = e2e_leg(torch, args, params, rank)
+        ev = torch.tensor([extras["e2e"]["seconds_per_step"]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ev, op=dist.ReduceOp.MAX)
+        extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
+        extras["fwd_bwd"] = fwd_bwd_leg(torch, dev)
+        if world > 1:
+            fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(fb, op=dist.ReduceOp.MAX)
+            extras["fwd_bwd"]["value"] = 256 * 1024 * 100 * world / (float(fb.item()) * 1e-3)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.no_extras:
+        r = cpu_leg(args.cpu_seconds, 1 << 21)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": f"reference hh_step loop (oracle port of dynamics.py:443-529, fp32 mode) "
+                         f"on {r['cores']} processes x {r['n_local']} neurons of the config-2 "
+                         f"population for ~{args.cpu_seconds:.0f} s"}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
+                "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
+                "gpu_launches": launches, "clocks": clk,
+                "stimulus_ms_share": stim_ms / sum(step_ms)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

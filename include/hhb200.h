@@ -1,0 +1,208 @@
+/*
+ * hhb200.h -- C ABI of the B200-native Hodgkin-Huxley hot path.
+ *
+ * The reference (arXiv 2601.21407 desk-scale package `hhengine`) has no native
+ * code and no FFI: its boundary is the Python module API of
+ * hhengine.dynamics / hhengine.adjoint.  This header is the library that a
+ * drop-in for that API binds (through ctypes); each entry
+ * point names the reference function it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch / C++ types.
+ *   - Array pointers are DEVICE pointers unless a comment says "host".
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  No call allocates device memory: the
+ *     caller pre-allocates every buffer (the Workspace idea of
+ *     dynamics.py:388-406).
+ *   - Return value: HHB_OK (0) or an error code; hhb_last_error() returns a
+ *     thread-local message.  No C++ exception crosses the ABI.
+ *   - dtype selects the arithmetic: HHB_F32 (MUFU fast path, the throughput
+ *     build) or HHB_F64 (reference-order arithmetic, the parity build).  All
+ *     floating arrays of one call share that dtype.
+ *   - Layouts are the reference's own: time-major series [T][ld] (Trace,
+ *     dynamics.py:269-270) and gate-major state [n_gates][ld]
+ *     (NeuronState, dynamics.py:254-256).  Spikes are bitmaps, one uint32
+ *     word per 32 neurons, bit i of word w = neuron 32*w + i.
+ */
+#ifndef HHB200_H
+#define HHB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HHB_ABI_VERSION 1
+#define HHB_MAX_GATES 8
+#define HHB_MAX_CHANNELS 8
+
+enum hhb_status {
+  HHB_OK = 0,
+  HHB_EINVAL = 22,   /* bad shape / argument / parameter table */
+  HHB_ENOTSUP = 95,  /* combination not compiled in */
+  HHB_ECUDA = 1000   /* CUDA launch or runtime error */
+};
+
+enum hhb_dtype { HHB_F32 = 0, HHB_F64 = 1 };
+
+/* RateFn.kind (dynamics.py:36-38) */
+enum hhb_rate_kind { HHB_RATE_LINOID = 0, HHB_RATE_EXP = 1, HHB_RATE_SIGMOID = 2 };
+
+/* SurrogateSpec.kind (adjoint.py:37-46) */
+enum hhb_surrogate_kind { HHB_SUR_SIGMOID_DERIV = 0, HHB_SUR_RECTANGULAR = 1 };
+
+/* RateFn(kind, a, v0, b)                                 dynamics.py:32-54 */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  double a, v0, b;
+} hhb_rate_t;
+
+/* GateSpec(name, alpha, beta, exponent), plus its owning channel index
+ * (HHParams.gate_layout, dynamics.py:190-193)            dynamics.py:96-108 */
+typedef struct {
+  hhb_rate_t alpha, beta;
+  int32_t exponent;
+  int32_t channel;
+} hhb_gate_t;
+
+/* ChannelSpec(name, g_max, e_rev, gates): its gates are the contiguous run
+ * gates[gate_begin .. gate_begin+gate_count) of hhb_params_t  dynamics.py:128-142 */
+typedef struct {
+  double g_max, e_rev;
+  int32_t gate_begin, gate_count;
+} hhb_channel_t;
+
+/* HHParams (dynamics.py:162-188), flattened. Host pointer at every call. */
+typedef struct {
+  int32_t n_gates, n_channels;
+  double c_m, dt, v_theta, v_rest, rate_scale;
+  hhb_gate_t gates[HHB_MAX_GATES];
+  hhb_channel_t channels[HHB_MAX_CHANNELS];
+} hhb_params_t;
+
+/* SurrogateSpec(kind, width)                             adjoint.py:33-48 */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  double width;
+} hhb_surrogate_t;
+
+int hhb_abi_version(void);
+const char* hhb_last_error(void);
+/* Validate a parameter table (the ConfigurationError checks of
+ * dynamics.py:50-54, :106-108, :140-142, :178-188).  Host-only. */
+int hhb_check_params(const hhb_params_t* params);
+
+/*
+ * hhb_forward -- replaces simulate() (dynamics.py:541-586) and hh_step()
+ * (dynamics.py:443-529): runs n_steps fused HH steps for n neurons in one
+ * launch with the state in registers.
+ *
+ *   v_in [n], g_in [n_gates][g_ld]          state before step 0
+ *   v_fin, g_fin (same layout)              state after the last step; may
+ *                                           alias v_in / g_in (in place)
+ *   i_ext + (i_st, i_sn)                    current of neuron j at step t is
+ *                                           i_ext[t*i_st + j*i_sn]; (ld,1) dense,
+ *                                           (0,1) per-neuron constant, (1,0) per
+ *                                           step scalar, (0,0) one scalar
+ *   v_out [n_steps][v_ld]      or NULL      Trace.v_series (potential after step t)
+ *   spk_out [n_steps][spk_ld]  or NULL      Trace.spike_series as bitmap words
+ *   ckpt [ceil(T/K)][1+n_gates][ckpt_ld]    state BEFORE steps 0, K, 2K, ...
+ *        or NULL, K = ckpt_every            (adjoint.py:330-336 stored states)
+ *   first_bad (device int64)                atomicMin(step_base + t) over the
+ *                                           first non-finite V' of every neuron;
+ *                                           caller initialises it to INT64_MAX
+ *                                           (NumericalOverflowError, dynamics.py:526-527)
+ */
+int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                const void* v_in, const void* g_in, int64_t g_ld,
+                void* v_fin, void* g_fin,
+                const void* i_ext, int64_t i_st, int64_t i_sn,
+                void* v_out, int64_t v_ld,
+                uint32_t* spk_out, int64_t spk_ld,
+                void* ckpt, int64_t ckpt_every, int64_t ckpt_ld,
+                int64_t step_base, int64_t* first_bad, void* stream);
+
+/*
+ * hhb_backward -- replaces backward_through_time() (adjoint.py:281-365) and
+ * hh_step_backward() (adjoint.py:102-194).  One launch runs the whole reverse
+ * sweep: for each checkpoint segment, newest first, it recomputes the segment
+ * states into seg_buf (skipped when ckpt_every == 1: full storage) and then
+ * applies the exact adjoint step by step.
+ *
+ *   ckpt, ckpt_every, ckpt_ld           as written by hhb_forward
+ *   seg_buf [ckpt_every][1+n_gates][ckpt_ld] scratch, may be NULL if ckpt_every == 1
+ *   seed_v  [T][seed_v_ld]   or NULL    dL/dV of trace row t (added before step t)
+ *   seed_spk[T][seed_spk_ld] or NULL    dL/dspike of trace row t
+ *   adj_v [n], adj_g [n_gates][adj_g_ld] in: adjoint after the last step;
+ *                                        out: adjoint of the state before step 0
+ *   d_i [T][d_i_ld]          or NULL    dL/di_ext per neuron and step
+ *   d_params [1+n_channels]  (double)   += {d_c_m, d_g_max[0..]}: deterministic
+ *                                       two-pass reduction through `partials`
+ *   partials  (double) hhb_backward_partials(n, dtype) doubles of scratch
+ *   first_bad (device int64)            atomicMax(step_base + t) of the first
+ *                                       non-finite adjoint in processing order;
+ *                                       caller initialises it to -1
+ *                                       (GradientOverflowError, adjoint.py:190-191)
+ */
+int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
+                 int64_t n, int64_t n_steps,
+                 const void* i_ext, int64_t i_st, int64_t i_sn,
+                 const void* ckpt, int64_t ckpt_every, int64_t ckpt_ld, void* seg_buf,
+                 const void* seed_v, int64_t seed_v_ld,
+                 const void* seed_spk, int64_t seed_spk_ld,
+                 void* adj_v, void* adj_g, int64_t adj_g_ld,
+                 void* d_i, int64_t d_i_ld,
+                 double* d_params, double* partials,
+                 int64_t step_base, int64_t* first_bad, void* stream);
+/* doubles of `partials` scratch hhb_backward needs for n neurons */
+int64_t hhb_backward_partials(int64_t n, int32_t dtype);
+
+/* ---- elementary ops (dynamics.py:324-381, adjoint.py:60-66) ------------ */
+
+/* gate_rates(): alpha, beta of one gate at n potentials, times rate_scale */
+int hhb_gate_rates(const hhb_gate_t* gate, double rate_scale, int32_t dtype, int64_t n,
+                   const void* v, void* alpha, void* beta, void* stream);
+/* RateFn.__call__ (with_slope=0) or RateFn.deriv (with_slope=1) of one rate */
+int hhb_rate_eval(const hhb_rate_t* rate, int32_t with_slope, int32_t dtype, int64_t n,
+                  const void* v, void* out, void* stream);
+/* gate_step(): exponential Euler p_inf + (p - p_inf) exp(-dt (alpha+beta)) */
+int hhb_gate_step(int32_t dtype, int64_t n, const void* p, const void* alpha, const void* beta,
+                  double dt, void* out, void* stream);
+/* ionic_current(): sum_X g_X prod p^k (V - E_X) */
+int hhb_ionic_current(const hhb_params_t* params, int32_t dtype, int64_t n, const void* v,
+                      const void* g, int64_t g_ld, void* out, void* stream);
+/* spike_detect(): v_prev < theta <= v_new, one byte per neuron */
+int hhb_spike_detect(int32_t dtype, int64_t n, const void* v_prev, const void* v_new,
+                     double theta, uint8_t* out, void* stream);
+/* surrogate_grad() at threshold offsets u */
+int hhb_surrogate_grad(const hhb_surrogate_t* surrogate, int32_t dtype, int64_t n,
+                       const void* u, void* out, void* stream);
+
+/* ---- data formats either side of the step ------------------------------ */
+
+/* bitmap [T][words] -> bool bytes [T][n] (Trace.spike_series) */
+int hhb_unpack_spikes(const uint32_t* bits, int64_t words_ld, int64_t n_steps, int64_t n,
+                      uint8_t* out, int64_t out_ld, void* stream);
+/* Synthetic stimulus (BASELINE config 2): out[t][j] = amp * Poisson(lam), Philox-4x32-10
+ * keyed by (seed, global neuron j + neuron_base, global step t + step_base) so a
+ * sharded population draws the same numbers as an unsharded one. */
+int hhb_poisson_current(int32_t dtype, int64_t n, int64_t n_steps, uint64_t seed,
+                        int64_t neuron_base, int64_t step_base, double lam, double amp,
+                        void* out, int64_t ld, void* stream);
+
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Pipe-throughput probe used by bench.py to measure the roofline denominator
+ * of the SFU-bound kernels on the box itself: which = 0 runs independent
+ * MUFU ex2 chains, which = 1 FFMA chains, which = 2 MUFU rcp chains, on
+ * 148 * 8 blocks x 256 threads, `iters` iterations of 8 ops per thread.
+ * Returns the number of operations issued in *ops (host). */
+int hhb_pipe_probe(int32_t which, int64_t iters, float* sink, int64_t* ops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HHB200_H */

@@ -1,0 +1,166 @@
+"""ctypes binding of the C-ABI library (include/hhb200.h).
+
+This is the only place Python touches native code.  The library is loaded from
+the package directory (built in-tree by `_build.py`); if it is missing or the
+ABI version differs, every compute entry point raises NativeLibraryError --
+there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import ConfigurationError, NativeLibraryError, UsageError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhhb200.so")
+ABI_VERSION = 1
+MAX_GATES = 8
+MAX_CHANNELS = 8
+
+F32, F64 = 0, 1
+RATE_KIND = {"linoid": 0, "exp": 1, "sigmoid": 2}
+SUR_KIND = {"sigmoid-derivative": 0, "rectangular": 1}
+
+OK, EINVAL, ENOTSUP, ECUDA = 0, 22, 95, 1000
+
+
+class Rate(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32),
+                ("a", C.c_double), ("v0", C.c_double), ("b", C.c_double)]
+
+
+class Gate(C.Structure):
+    _fields_ = [("alpha", Rate), ("beta", Rate), ("exponent", C.c_int32), ("channel", C.c_int32)]
+
+
+class Channel(C.Structure):
+    _fields_ = [("g_max", C.c_double), ("e_rev", C.c_double),
+                ("gate_begin", C.c_int32), ("gate_count", C.c_int32)]
+
+
+class Params(C.Structure):
+    _fields_ = [("n_gates", C.c_int32), ("n_channels", C.c_int32),
+                ("c_m", C.c_double), ("dt", C.c_double), ("v_theta", C.c_double),
+                ("v_rest", C.c_double), ("rate_scale", C.c_double),
+                ("gates", Gate * MAX_GATES), ("channels", Channel * MAX_CHANNELS)]
+
+
+class Surrogate(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("width", C.c_double)]
+
+
+_vp, _i64, _i32, _dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+
+# name -> (restype, argtypes); mirrors include/hhb200.h one to one
+SIGNATURES = {
+    "hhb_abi_version": (_i32, []),
+    "hhb_last_error": (C.c_char_p, []),
+    "hhb_check_params": (_i32, [C.POINTER(Params)]),
+    "hhb_forward": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
+                           _vp, _vp, _i64, _vp, _vp,
+                           _vp, _i64, _i64,
+                           _vp, _i64,
+                           _vp, _i64,
+                           _vp, _i64, _i64,
+                           _i64, _vp, _vp]),
+    "hhb_backward": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
+                            _vp, _i64, _i64,
+                            _vp, _i64, _i64, _vp,
+                            _vp, _i64, _vp, _i64,
+                            _vp, _vp, _i64,
+                            _vp, _i64,
+                            _vp, _vp,
+                            _i64, _vp, _vp]),
+    "hhb_backward_partials": (_i64, [_i64, _i32]),
+    "hhb_gate_rates": (_i32, [C.POINTER(Gate), _dbl, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "hhb_rate_eval": (_i32, [C.POINTER(Rate), _i32, _i32, _i64, _vp, _vp, _vp]),
+    "hhb_gate_step": (_i32, [_i32, _i64, _vp, _vp, _vp, _dbl, _vp, _vp]),
+    "hhb_ionic_current": (_i32, [C.POINTER(Params), _i32, _i64, _vp, _vp, _i64, _vp, _vp]),
+    "hhb_spike_detect": (_i32, [_i32, _i64, _vp, _vp, _dbl, _vp, _vp]),
+    "hhb_surrogate_grad": (_i32, [C.POINTER(Surrogate), _i32, _i64, _vp, _vp, _vp]),
+    "hhb_unpack_spikes": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "hhb_poisson_current": (_i32, [_i32, _i64, _i64, C.c_uint64, _i64, _i64, _dbl, _dbl,
+                                   _vp, _i64, _vp]),
+    "hhb_pipe_probe": (_i32, [_i32, _i64, _vp, C.POINTER(C.c_int64), _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_load_error: str | None = None
+
+
+def load():
+    """Load and type the library once; raise NativeLibraryError if unusable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            _load_error = (f"{LIB_PATH} not built; run `python -m paper_2601_21407_b200._build` "
+                           "(there is no CPU fallback)")
+            raise NativeLibraryError(_load_error)
+        try:
+            lib = C.CDLL(LIB_PATH)
+        except OSError as e:
+            raise NativeLibraryError(f"cannot load {LIB_PATH}: {e}") from None
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.hhb_abi_version() != ABI_VERSION:
+            raise NativeLibraryError("libhhb200.so ABI version mismatch; rebuild")
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str):
+    if rc == OK:
+        return
+    msg = load().hhb_last_error().decode(errors="replace")
+    if rc == EINVAL:
+        raise UsageError(f"{what}: {msg}")
+    raise NativeLibraryError(f"{what} failed (code {rc}): {msg}")
+
+
+def pack_rate(fn) -> Rate:
+    return Rate(RATE_KIND[fn.kind], 0, float(fn.a), float(fn.v0), float(fn.b))
+
+
+def pack_gate(gate, channel: int = 0) -> Gate:
+    return Gate(pack_rate(gate.alpha), pack_rate(gate.beta), int(gate.exponent), channel)
+
+
+def pack_params(channels, c_m=1.0, dt=1.0, v_theta=0.0, v_rest=-65.0, rate_scale=1.0) -> Params:
+    """Flatten a channel list (HHParams.channels) into the C table."""
+    P = Params()
+    gi = 0
+    if len(channels) > MAX_CHANNELS:
+        raise ConfigurationError(f"at most {MAX_CHANNELS} channels are supported, got {len(channels)}")
+    for ci, ch in enumerate(channels):
+        P.channels[ci] = Channel(float(ch.g_max), float(ch.e_rev), gi, len(ch.gates))
+        for g in ch.gates:
+            if gi >= MAX_GATES:
+                raise ConfigurationError(f"at most {MAX_GATES} gates are supported")
+            P.gates[gi] = pack_gate(g, ci)
+            gi += 1
+    P.n_gates = gi
+    P.n_channels = len(channels)
+    P.c_m, P.dt, P.v_theta, P.v_rest, P.rate_scale = (float(c_m), float(dt), float(v_theta),
+                                                        float(v_rest), float(rate_scale))
+    lib = load()
+    if lib.hhb_check_params(C.byref(P)) != OK:
+        raise ConfigurationError(lib.hhb_last_error().decode(errors="replace"))
+    return P
+
+
+def pack_hh(params) -> Params:
+    return pack_params(params.channels, params.c_m, params.dt, params.v_theta, params.v_rest,
+                       params.rate_scale)
+
+
+def pack_surrogate(spec) -> Surrogate:
+    return Surrogate(SUR_KIND[spec.kind], 0, float(spec.width))

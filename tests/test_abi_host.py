@@ -1,0 +1,156 @@
+"""CPU tests of the boundary: the C-ABI library loads and exports every symbol
+include/hhb200.h declares, the ctypes structs match the C layout, and the
+host-side logic (parameter validation, plans, stats) mirrors the reference.
+No kernel is launched here."""
+
+import ctypes as C
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT, golden
+from paper_2601_21407_b200 import _native as nat
+from paper_2601_21407_b200 import adjoint as A
+from paper_2601_21407_b200 import defaults as DF
+from paper_2601_21407_b200 import dynamics as Dy
+from paper_2601_21407_b200.errors import (ConfigurationError, NativeLibraryError,
+                                          NumericalOverflowError, UsageError)
+
+HEADER = os.path.join(ROOT, "include", "hhb200.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hhb_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.load()
+    names = _declared()
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(lib, name), f"{name} not exported"
+        assert name in nat.SIGNATURES, f"{name} not typed in _native.SIGNATURES"
+    assert lib.hhb_abi_version() == nat.ABI_VERSION
+
+
+def test_symbol_visibility_with_nm():
+    out = subprocess.run(["nm", "-D", "--defined-only", nat.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (hhb_[a-z0-9_]+)", out))
+    assert set(_declared()) <= exported
+
+
+def test_struct_layout_matches_c_header():
+    src = r"""
+    #include <stdio.h>
+    #include <stddef.h>
+    #include "hhb200.h"
+    int main(void) {
+      printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(hhb_rate_t), sizeof(hhb_gate_t),
+             sizeof(hhb_channel_t), sizeof(hhb_params_t), sizeof(hhb_surrogate_t),
+             offsetof(hhb_params_t, gates), offsetof(hhb_params_t, channels),
+             offsetof(hhb_gate_t, exponent));
+      return 0;
+    }
+    """
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "l.c")
+        open(c, "w").write(src)
+        exe = os.path.join(d, "l")
+        subprocess.run(["gcc", "-I", os.path.dirname(HEADER), c, "-o", exe], check=True)
+        vals = list(map(int, subprocess.run([exe], capture_output=True, text=True).stdout.split()))
+    mine = [C.sizeof(nat.Rate), C.sizeof(nat.Gate), C.sizeof(nat.Channel), C.sizeof(nat.Params),
+            C.sizeof(nat.Surrogate), nat.Params.gates.offset, nat.Params.channels.offset,
+            nat.Gate.exponent.offset]
+    assert vals == mine
+
+
+def test_param_table_validation_matches_reference_errors():
+    p = DF.na_kdr_cal_kca_params()
+    P = nat.pack_hh(p)
+    assert (P.n_gates, P.n_channels) == (6, 5)
+    assert [P.gates[g].channel for g in range(6)] == [0, 0, 1, 3, 3, 4]
+    assert (P.channels[2].gate_begin, P.channels[2].gate_count) == (3, 0)
+    with pytest.raises(ConfigurationError):
+        Dy.RateFn("tanh", 1.0, 0.0, 1.0)
+    with pytest.raises(ConfigurationError):
+        Dy.RateFn("exp", 1.0, 0.0, 0.0)
+    with pytest.raises(ConfigurationError):
+        Dy.GateSpec("g", Dy.RateFn("exp", 1, 0, 1), Dy.RateFn("exp", 1, 0, 1), -1)
+    with pytest.raises(ConfigurationError):
+        Dy.ChannelSpec("c", -1.0, 0.0)
+    with pytest.raises(ConfigurationError):
+        p.with_(c_m=0.0)
+    with pytest.raises(ConfigurationError):
+        p.with_(dt=-1.0)
+    with pytest.raises(ConfigurationError):
+        p.with_(channels=p.channels + (p.channels[0],))
+    # C-side check (the same table, corrupted)
+    P.channels[1].gate_begin = 5
+    assert nat.load().hhb_check_params(C.byref(P)) == nat.EINVAL
+    # more gates than the kernels carry in registers
+    g = p.channels[0].gates[0]
+    big = Dy.HHParams(1.0, (Dy.ChannelSpec("x", 1.0, 0.0, (g,) * 9),), -65.0, 0.0, 0.01)
+    with pytest.raises(ConfigurationError):
+        nat.pack_hh(big)
+
+
+def test_dict_round_trip():
+    p = DF.na_kdr_cal_kca_params(dt=0.02, rate_scale=1.5)
+    q = Dy.HHParams.from_dict(p.to_dict())
+    assert q == p.with_(dtype=np.float64)
+    assert q.gate_layout == p.gate_layout and q.n_gates == 6
+    with pytest.raises(ConfigurationError):
+        Dy.HHParams.from_dict({"c_m": 1.0})
+
+
+def test_plans_and_stats_match_reference_counts():
+    ka = golden("known_answers")
+    for (T, b), seg, cnt in zip(ka["plan_in"], ka["plan_seg"], ka["plan_count"]):
+        pl = A.make_plan(int(T), int(b))
+        assert pl.segment_length == seg and len(pl.stored_indices) == cnt
+    with pytest.raises(UsageError):
+        A.make_plan(0, 3)
+    with pytest.raises(UsageError):
+        A.CheckpointPlan(10, 2, (1, 3))
+    with pytest.raises(UsageError):
+        A.CheckpointPlan(10, 2, (0, 5))
+    for case in ("bptt_rs", "bptt_squid_rect", "bptt_c2"):
+        g = golden(case)
+        T = g["i"].shape[0]
+        seg = A.make_plan(T, int(g["budget"])).segment_length
+        st = A._plan_stats(T, seg, False)
+        assert (st.forward_calls, st.peak_stored_states) == (int(g["plan_calls"]), int(g["plan_peak"]))
+        st = A._plan_stats(T, 1, True)
+        assert (st.forward_calls, st.peak_stored_states) == (int(g["full_calls"]), int(g["full_peak"]))
+    # T=400, budget 20 -> peak <= 40, forward calls <= 2T + budget
+    st = A._plan_stats(400, A.make_plan(400, 20).segment_length, False)
+    assert st.peak_stored_states <= 40 and st.forward_calls <= 2 * 400 + 20
+
+
+def test_surrogate_spec_validation():
+    assert A.default_surrogate(DF.squid_axon_params()).width == 16.25
+    with pytest.raises(UsageError):
+        A.SurrogateSpec("tanh", 1.0)
+    with pytest.raises(UsageError):
+        A.SurrogateSpec("rectangular", 0.0)
+
+
+def test_errors_carry_step_index():
+    e = NumericalOverflowError("membrane potential became non-finite", 12)
+    assert e.step_index == 12 and "(step 12)" in str(e)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_product_path_fails_loudly_without_gpu():
+    p = DF.squid_axon_params()
+    with pytest.raises(NativeLibraryError):
+        Dy.simulate(p, np.zeros((3, 2)), state0=Dy.NeuronState(np.full(2, -65.0), np.zeros((3, 2))))
+    with pytest.raises(NativeLibraryError):
+        Dy.gate_rates(p.channels[0].gates[0], np.zeros(3))

@@ -1,0 +1,280 @@
+"""GPU parity of the forward path (hhb_forward and the elementary-op kernels)
+against the reference's golden vectors and the CPU oracle.
+
+Tolerances:
+  float64 build: V within 1e-9 relative (+1e-9 mV) of the reference over the
+                 whole horizon, spikes identical.
+  float32 build: V within 1e-4*|V_ref| + 0.02 mV up to each neuron's first
+                 spike (and over the whole horizon for subthreshold neurons),
+                 per-neuron spike counts equal, every spike within +-1 step.
+  spike bitmaps: bit-exact against spike_detect on the kernel's own V trace.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle import hh_oracle as O
+from paper_2601_21407_b200 import adjoint as A
+from paper_2601_21407_b200 import defaults as DF
+from paper_2601_21407_b200 import dynamics as Dy
+from paper_2601_21407_b200.errors import ConfigurationError, NumericalOverflowError
+
+pytestmark = pytest.mark.gpu
+
+
+def _close64(v, ref, rtol=1e-9, atol=1e-9):
+    return np.all(np.abs(v - ref) <= rtol * np.abs(ref) + atol), float(np.max(np.abs(v - ref)))
+
+
+def check_fp32_contract(v, s, v_ref, s_ref):
+    """The float32 contract above; returns a dict of the measured quantities."""
+    v = np.asarray(v, dtype=np.float64)
+    T, n = v.shape
+    counts_ok = np.array_equal(s.sum(0), s_ref.sum(0))
+    assert counts_ok, f"spike counts differ: {s.sum(0)} vs {s_ref.sum(0)}"
+    for j in range(n):
+        a, b = np.flatnonzero(s[:, j]), np.flatnonzero(s_ref[:, j])
+        assert np.all(np.abs(a - b) <= 1), f"neuron {j}: spike steps {a} vs {b}"
+    tol = 1e-4 * np.abs(v_ref) + 0.02
+    ok = np.abs(v - v_ref) <= tol
+    full_pass = 0
+    for j in range(n):
+        first = np.flatnonzero(s_ref[:, j])
+        horizon = T if first.size == 0 else first[0]
+        assert ok[:horizon, j].all(), f"neuron {j}: V outside tolerance before its first spike"
+        full_pass += ok[:, j].all()
+    return {"full_horizon_pass_fraction": full_pass / n}
+
+
+# ------------------------------------------------------------------ float64 build
+
+def test_fp64_squid_ramp_matches_reference(cuda):
+    g = golden("fwd_squid_ramp")
+    p = DF.squid_axon_params(dt=0.01)
+    i = np.tile(g["i"], (int(g["T"]), 1))
+    tr, fin = Dy.simulate(p, i, record_state=True)
+    ok, err = _close64(tr.v_series, g["v"])
+    assert ok, err
+    assert np.array_equal(tr.spike_series, g["spikes"])
+    assert _close64(fin.v, g["v_fin"])[0] and _close64(fin.gates, g["g_fin"])[0]
+
+
+def test_fp64_config1_full_10000_steps(cuda):
+    g = golden("fwd_c1_one")
+    p = DF.squid_axon_params(dt=0.01)
+    tr = Dy.simulate(p, np.full((10000, 1024), 10.0))
+    assert np.array_equal(tr.spike_series, np.repeat(g["spikes"][:, None], 1024, 1))
+    ok, err = _close64(tr.v_series[:, 7], g["v"])
+    assert ok, err
+    assert np.all(tr.v_series == tr.v_series[:, :1])  # identical neurons stay identical
+
+
+@pytest.mark.parametrize("case,mk", [("fwd_rs", lambda: DF.cortical_rs_params(dt=0.1)),
+                                     ("fwd_c2", lambda: DF.na_kdr_cal_kca_params(dt=0.01))])
+def test_fp64_random_inputs(cuda, case, mk):
+    g = golden(case)
+    tr = Dy.simulate(mk(), g["i"])
+    ok, err = _close64(tr.v_series, g["v"])
+    assert ok, err
+    assert np.array_equal(tr.spike_series, g["spikes"])
+
+
+def test_fp64_hh_step_scalar_current_and_rate_scale(cuda):
+    g = golden("fwd_scaled_scalar")
+    p = DF.squid_axon_params(dt=0.025, rate_scale=1.7)
+    st = Dy.NeuronState(g["v0"].copy(), g["g0"].copy())
+    ws = Dy.Workspace((8,), np.float64)
+    for t in range(g["v"].shape[0]):
+        st, sp = Dy.hh_step(st, 14.0, p, workspace=ws, step_index=t)
+        assert _close64(st.v, g["v"][t])[0]
+        assert np.array_equal(sp, g["spikes"][t])
+
+
+def test_fp64_device_tensors_equal_numpy_path(cuda):
+    g = golden("fwd_c2")
+    p = DF.na_kdr_cal_kca_params(dt=0.01)
+    tr_np = Dy.simulate(p, g["i"])
+    tr_dev, fin = Dy.simulate(p, torch.from_numpy(g["i"]).to(cuda), record_state=True)
+    assert isinstance(tr_dev.v_series, torch.Tensor) and tr_dev.v_series.is_cuda
+    assert np.array_equal(tr_dev.v_series.cpu().numpy(), tr_np.v_series)
+    assert np.array_equal(tr_dev.spike_series.cpu().numpy(), tr_np.spike_series)
+
+
+def test_chunked_simulation_equals_one_shot(cuda):
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    rng = np.random.default_rng(5)
+    i = 2.0 * rng.poisson(2.0, size=(700, 300)).astype(np.float32)
+    full = Dy.simulate(p, i)
+    a, st = Dy.simulate(p, i[:333], record_state=True)
+    b = Dy.simulate(p, i[333:], state0=st)
+    assert np.array_equal(np.concatenate([a.v_series, b.v_series]), full.v_series)
+    assert np.array_equal(np.concatenate([a.spike_series, b.spike_series]), full.spike_series)
+
+
+def test_determinism_and_empty(cuda):
+    p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
+    i = np.random.default_rng(1).normal(8, 3, size=(200, 77))
+    a, b = Dy.simulate(p, i), Dy.simulate(p, i)
+    assert np.array_equal(a.v_series, b.v_series) and np.array_equal(a.spike_series, b.spike_series)
+    e = Dy.simulate(p, np.zeros((0, 5)))
+    assert e.v_series.shape == (0, 5) and e.spike_series.shape == (0, 5)
+
+
+def test_overflow_raises_with_step_index(cuda):
+    p = DF.squid_axon_params(dt=0.01)
+    i = np.full((20, 40), 5.0)
+    i[7, 33] = 1e308
+    with pytest.raises(NumericalOverflowError) as e:
+        Dy.simulate(p, i * 1e10)
+    assert e.value.step_index == 7
+    with pytest.raises(O.Overflow) as eo:
+        O.simulate(p, i * 1e10)
+    assert eo.value.step == 7
+
+
+# ------------------------------------------------------------------ float32 build
+
+def test_fp32_config1_contract(cuda):
+    g = golden("fwd_c1_one")
+    p = DF.squid_axon_params(dt=0.01).with_(dtype=np.float32)
+    tr = Dy.simulate(p, np.full((10000, 1024), 10.0))
+    v = tr.v_series[:, :1]
+    check_fp32_contract(v, tr.spike_series[:, :1], g["v"][:, None], g["spikes"][:, None])
+    assert int(tr.spike_series[:, 0].sum()) == 7
+
+
+@pytest.mark.parametrize("case,mk", [("fwd_squid_ramp", lambda: DF.squid_axon_params(dt=0.01)),
+                                     ("fwd_rs", lambda: DF.cortical_rs_params(dt=0.1)),
+                                     ("fwd_c2", lambda: DF.na_kdr_cal_kca_params(dt=0.01))])
+def test_fp32_contract_against_reference(cuda, case, mk):
+    g = golden(case)
+    i = g["i"] if g["i"].ndim == 2 else np.tile(g["i"], (int(g["T"]), 1))
+    tr = Dy.simulate(mk().with_(dtype=np.float32), i)
+    check_fp32_contract(tr.v_series, tr.spike_series, g["v"], g["spikes"])
+
+
+def test_fp32_vector_and_scalar_kernels_agree_bitwise(cuda):
+    """n >= 148*32*4 takes the float4 (4 neurons/thread) kernel; a small batch the
+    1 neuron/thread kernel.  Same math => identical bits per neuron."""
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    n_big = 148 * 32 * 4 + 64
+    rng = np.random.default_rng(3)
+    i = (2.0 * rng.poisson(2.0, size=(300, n_big))).astype(np.float32)
+    big = Dy.simulate(p, torch.from_numpy(i).to(cuda))
+    small = Dy.simulate(p, torch.from_numpy(i[:, :1000].copy()).to(cuda))
+    assert torch.equal(big.v_series[:, :1000], small.v_series)
+    assert torch.equal(big.spike_series[:, :1000], small.spike_series)
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 129, 148 * 128 + 4])
+def test_fp32_bitmap_exact_and_ragged_sizes(cuda, n):
+    p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
+    i = np.random.default_rng(n).normal(9.0, 4.0, size=(150, n)).astype(np.float32)
+    tr, _ = Dy.simulate(p, torch.from_numpy(i).to(cuda), record_state=True)
+    v = tr.v_series.cpu().numpy()
+    st0 = Dy.init_state(p, (n,))
+    vprev = np.concatenate([st0.v[None, :].astype(np.float32), v[:-1]])
+    expect = (vprev < p.v_theta) & (v >= p.v_theta)
+    assert np.array_equal(tr.spike_series.cpu().numpy(), expect)
+    # same neurons against the float64 oracle under the fp32 contract
+    vo, so = O.simulate(p, i.astype(np.float64))
+    if n <= 200:
+        check_fp32_contract(v, tr.spike_series.cpu().numpy(), vo, so)
+
+
+# ------------------------------------------------------------------ elementary ops
+
+@pytest.mark.parametrize("name,mk", [("squid", lambda: DF.squid_axon_params(dt=0.01)),
+                                     ("rs", lambda: DF.cortical_rs_params(dt=0.1)),
+                                     ("c2", lambda: DF.na_kdr_cal_kca_params(dt=0.01))])
+def test_rates_slopes_init_state(cuda, name, mk):
+    ka = golden("known_answers")
+    p = mk()
+    vg = ka[f"{name}_vgrid"]
+    rows, slopes = [], []
+    for _, g in p.gate_layout:
+        a, b = Dy.gate_rates(g, vg, p.rate_scale)
+        rows += [a, b]
+        slopes += [g.alpha.deriv(vg), g.beta.deriv(vg)]
+    assert np.allclose(np.array(rows), ka[f"{name}_rates"], rtol=1e-13, atol=1e-300)
+    assert np.allclose(np.array(slopes), ka[f"{name}_slopes"], rtol=1e-12, atol=1e-300)
+    st = Dy.init_state(p, (3,))
+    assert np.allclose(st.gates[:, 0], ka[f"{name}_init_gates"], rtol=1e-14, atol=0)
+    st = Dy.init_state(p, (2,), v0=-55.0)
+    assert np.allclose(st.gates[:, 1], ka[f"{name}_init_gates_m55"], rtol=1e-14, atol=0)
+    # float32 rate kernel: series branch near the singularity keeps full accuracy
+    for k, (_, g) in enumerate(p.gate_layout):
+        a32 = g.alpha(torch.tensor(vg, dtype=torch.float32, device=cuda)).cpu().numpy()
+        ref = ka[f"{name}_rates"][2 * k] / p.rate_scale
+        assert np.allclose(a32, ref, rtol=2e-6, atol=1e-30)
+
+
+def test_known_answers_elementwise(cuda):
+    ka = golden("known_answers")
+    assert abs(float(Dy.gate_step(0.2, 0.5, 1.5, 0.1)) - float(ka["gate_step"])) < 1e-15
+    assert float(Dy.gate_step(0.25, 0.5, 1.5, 0.1)) == pytest.approx(0.25, abs=1e-15)
+    assert abs(float(Dy.gate_step(0.3, 0.5, 1.5, 1e-12)) - 0.3) <= 1e-12
+    st = Dy.NeuronState(np.array([-65.0]), np.zeros((0, 1)))
+    assert np.allclose(Dy.ionic_current(st, (Dy.ChannelSpec("leak", 0.3, -54.4),)), -3.18, atol=1e-12)
+    with pytest.raises(ConfigurationError):
+        Dy.ionic_current(st, DF.squid_axon_params().channels)
+    pairs = ka["spike_pairs"]
+    got = [bool(Dy.spike_detect(a, b, c)) for a, b, c in pairs]
+    assert got == [bool(x) for x in ka["spike_out"]]
+    u = ka["sur_u"]
+    assert np.allclose(A.surrogate_grad(u, A.SurrogateSpec("sigmoid-derivative", 2.5)), ka["sur_sig"],
+                       rtol=1e-14, atol=1e-300)
+    assert np.array_equal(A.surrogate_grad(u, A.SurrogateSpec("rectangular", 2.5)), ka["sur_rect"])
+    # peak at 0, tail <= 1e-6 at 20 w, integrates to 1
+    w = 3.0
+    uu = np.linspace(-200 * w, 200 * w, 400001)
+    s = A.surrogate_grad(uu, A.SurrogateSpec("sigmoid-derivative", w))
+    assert np.argmax(s) == len(uu) // 2 and A.surrogate_grad(20 * w, A.SurrogateSpec(width=w)) <= 1e-6
+    assert abs(np.trapezoid(s, uu) - 1.0) < 1e-3
+
+
+def test_ionic_current_matches_oracle(cuda):
+    p = DF.na_kdr_cal_kca_params()
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-90, 40, 257)
+    gt = rng.uniform(0, 1, (6, 257))
+    got = Dy.ionic_current(Dy.NeuronState(v, gt), p.channels)
+    _, _, _ = O.step(p, v, gt, 0.0)
+    ref = np.zeros_like(v)
+    row = 0
+    for ch in p.channels:
+        eta = 1.0
+        for g in ch.gates:
+            eta = eta * O._ipow(gt[row], g.exponent)
+            row += 1
+        ref = ref + ch.g_max * eta * (v - ch.e_rev)
+    assert np.allclose(got, ref, rtol=1e-14, atol=1e-12)
+
+
+def test_invariants_zero_conductance_and_cm_scaling(cuda):
+    """zero conductances and zero input leave V unchanged;
+    doubling c_m halves dV exactly (float64 build)."""
+    p = DF.squid_axon_params(g_na=0.0, g_k=0.0, g_leak=0.0)
+    st = Dy.init_state(p, (4,))
+    new, sp = Dy.hh_step(st, 0.0, p)
+    assert np.array_equal(new.v, st.v) and not sp.any()
+    q = DF.squid_axon_params(dt=0.01)
+    s0 = Dy.init_state(q, (5,))
+    i = np.array([0.0, 3.0, 10.0, -4.0, 25.0])
+    a, _ = Dy.hh_step(s0, i, q)
+    b, _ = Dy.hh_step(s0, i, q.with_(c_m=2.0))
+    assert np.array_equal(b.v - s0.v, (a.v - s0.v) / 2.0)
+
+
+def test_gate_boundedness_and_rest_stability(cuda):
+    p = DF.cortical_rs_params(dt=0.1)
+    rng = np.random.default_rng(9)
+    i = rng.normal(0, 30, size=(500, 64))
+    st0 = Dy.init_state(p, (64,))
+    st0.gates = rng.uniform(0, 1, st0.gates.shape)
+    _, fin = Dy.simulate(p, i, state0=st0, record_state=True)
+    assert np.all((fin.gates >= 0) & (fin.gates <= 1))
+    rest = Dy.simulate(p, np.zeros((1000, 3)))   # 100 ms at rest
+    assert np.all(np.abs(rest.v_series - p.v_rest) < 1.0) and not rest.spike_series.any()
