@@ -193,6 +193,18 @@ int hhb_poisson_current(int32_t dtype, int64_t n, int64_t n_steps, uint64_t seed
                         int64_t neuron_base, int64_t step_base, double lam, double amp,
                         void* out, int64_t ld, void* stream);
 
+/* ---- runtime specialisation ----------------------------------------------- */
+
+/* The float (HHB_F32) forward/backward kernels are generated per parameter
+ * table (constants as immediates, rate kinds and exponents resolved) and
+ * compiled with NVRTC for sm_100a on first use; the generic table-driven
+ * kernels run when NVRTC is unavailable or HHB_NO_JIT=1.
+ * hhb_jit_status: "ok", "not initialised" or the reason the JIT is off.
+ * hhb_jit_source: writes the generated CUDA source for `params` into buf
+ * (NUL-terminated, truncated to cap) and returns the full size + 1, or -1. */
+const char* hhb_jit_status(void);
+int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap);
+
 /* ---- measurement ---------------------------------------------------------- */
 
 /* Pipe-throughput probe used by bench.py to measure the roofline denominator

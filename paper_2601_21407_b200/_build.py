@@ -28,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 # per-source extra flags: the double flavour must not contract into FMA (NumPy parity)
 EXTRA = {"hh_f64.cu": ["-fmad=false"]}
-LINK_LIBS: list[str] = []
+LINK_LIBS: list[str] = ["-ldl"]
 
 
 def nvcc() -> str:

@@ -50,8 +50,10 @@ def to_dev(x, dtype, dev=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=td)
     else:
-        a = np.asarray(x)
-        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np_dtype(dtype)))
+        a = np.asarray(x, dtype=np_dtype(dtype))
+        if not a.flags.c_contiguous:
+            a = np.array(a, order="C")  # (np.ascontiguousarray would turn 0-d into 1-d)
+        t = torch.from_numpy(a)
         t = t.to(dev, non_blocking=False)
     return t.contiguous()
 

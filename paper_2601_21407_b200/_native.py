@@ -84,6 +84,8 @@ SIGNATURES = {
     "hhb_poisson_current": (_i32, [_i32, _i64, _i64, C.c_uint64, _i64, _i64, _dbl, _dbl,
                                    _vp, _i64, _vp]),
     "hhb_pipe_probe": (_i32, [_i32, _i64, _vp, C.POINTER(C.c_int64), _vp]),
+    "hhb_jit_status": (C.c_char_p, []),
+    "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }
 
 _lock = threading.Lock()
@@ -164,3 +166,17 @@ def pack_hh(params) -> Params:
 
 def pack_surrogate(spec) -> Surrogate:
     return Surrogate(SUR_KIND[spec.kind], 0, float(spec.width))
+
+
+def jit_source(params) -> str:
+    """CUDA source the library generates for `params` (float kernels)."""
+    P = pack_hh(params)
+    lib = load()
+    n = int(lib.hhb_jit_source(C.byref(P), None, 0))
+    buf = C.create_string_buffer(n)
+    lib.hhb_jit_source(C.byref(P), buf, n)
+    return buf.value.decode()
+
+
+def jit_status() -> str:
+    return load().hhb_jit_status().decode()

@@ -282,6 +282,19 @@ int hhb_poisson_current(int32_t dtype, int64_t n, int64_t n_steps, uint64_t seed
                                   ld, ST(stream));
 }
 
+const char* hhb_jit_status(void) { return jit_status(); }
+
+int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap) {
+  if (check_params(params)) return -1;
+  const std::string src = jit_source(params);
+  if (buf && cap > 0) {
+    const int64_t n = int64_t(src.size()) < cap - 1 ? int64_t(src.size()) : cap - 1;
+    memcpy(buf, src.data(), size_t(n));
+    buf[n] = '\0';
+  }
+  return int64_t(src.size()) + 1;
+}
+
 int hhb_pipe_probe(int32_t which, int64_t iters, float* sink, int64_t* ops, void* stream) {
   if (which < 0 || which > 2 || iters < 1 || !sink || !ops) return fail(HHB_EINVAL, "bad probe args");
   const int blocks = kNumSMs * 8, threads = 256;

@@ -149,6 +149,22 @@ inline DevSur<T> pack_sur(const hhb_surrogate_t* s) {
   return d;
 }
 
+template <typename T>
+inline PoissonTab<T> poisson_table(double lam, double amp) {
+  PoissonTab<T> tb{};
+  tb.amp = T(amp);
+  double pk = std::exp(-lam), cdf = pk;
+  int k = 0;
+  for (; k < 48; ++k) {
+    tb.cdf[k] = T(cdf);
+    if (cdf >= 1.0 - 1.16e-10) break;
+    pk *= lam / double(k + 1);
+    cdf += pk;
+  }
+  tb.size = k < 48 ? k + 1 : 48;
+  return tb;
+}
+
 inline int fwd_block(int64_t threads) {
   if (threads >= int64_t(kNumSMs) * kFwdThreads) return kFwdThreads;
   int64_t per = (threads + kNumSMs - 1) / kNumSMs;
@@ -228,6 +244,32 @@ int launch_ionic(const DevTable<T>& tb, int64_t n, const T* v, const T* g, int64
   return cuda_check("k_ionic launch");
 }
 
+// Runtime-specialised float kernels (jit.cu).  Return false when the JIT is
+// unavailable or disabled; the generic kernels then run.
+bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, bool vec4, cudaStream_t st, int& rc);
+bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs<float>& a, cudaStream_t st,
+                  int& rc);
+const char* jit_status();
+std::string jit_source(const hhb_params_t* P);
+
+template <typename T>
+inline bool try_jit_fwd(const hhb_params_t* P, const FwdArgs<T>& a, bool vec4, cudaStream_t st, int& rc) {
+  if constexpr (sizeof(T) == 4) {
+    return jit_forward(P, a, vec4, st, rc);
+  } else {
+    return false;
+  }
+}
+template <typename T>
+inline bool try_jit_bwd(const hhb_params_t* P, const DevSur<T>& s, const BwdArgs<T>& a, cudaStream_t st,
+                        int& rc) {
+  if constexpr (sizeof(T) == 4) {
+    return jit_backward(P, s, a, st, rc);
+  } else {
+    return false;
+  }
+}
+
 // Flavour entry points (one definition per TU: hh_f32.cu / hh_f64.cu).
 template <typename T>
 struct Flavour {
@@ -261,14 +303,24 @@ struct Flavour {
          (a.v_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.v_out) % (sizeof(T) * (VECW)) == 0)) && \
         (a.ckpt == nullptr ||                                                                    \
          (a.ck_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.ckpt) % (sizeof(T) * (VECW)) == 0)); \
-    if (vec_ok && a.n >= int64_t(kNumSMs) * 32 * (VECW))                                          \
-      return launch_forward_vec<T, VECW>(tb, a, st);                                             \
+    const bool wide = vec_ok && a.n >= int64_t(kNumSMs) * 32 * (VECW);                            \
+    int jrc = HHB_OK;                                                                            \
+    if (try_jit_fwd<T>(P, a, wide && (VECW) == 4, st, jrc)) return jrc;                          \
+    if (wide) return launch_forward_vec<T, VECW>(tb, a, st);                                     \
     return launch_forward_vec<T, 1>(tb, a, st);                                                  \
   }                                                                                              \
   template <>                                                                                    \
   int Flavour<T>::backward(const hhb_params_t* P, const hhb_surrogate_t* S,                      \
                            const BwdArgs<T>& a, double* d_params, cudaStream_t st) {             \
-    return launch_backward<T>(pack_table<T>(P), pack_sur<T>(S), a, d_params, st);                \
+    const DevTable<T> tb = pack_table<T>(P);                                                     \
+    const DevSur<T> sur = pack_sur<T>(S);                                                        \
+    int jrc = HHB_OK;                                                                            \
+    if (try_jit_bwd<T>(P, sur, a, st, jrc)) {                                                    \
+      if (jrc) return jrc;                                                                       \
+      k_reduce<T><<<kSlots, 256, 0, st>>>(tb, a.partials, bwd_blocks(a.n), d_params);            \
+      return cuda_check("k_reduce launch");                                                      \
+    }                                                                                            \
+    return launch_backward<T>(tb, sur, a, d_params, st);                                         \
   }                                                                                              \
   template <>                                                                                    \
   int Flavour<T>::gate_rates(const hhb_gate_t* G, double scale, int64_t n, const T* v, T* al,    \
@@ -321,7 +373,8 @@ struct Flavour {
     if (n <= 0 || steps <= 0) return HHB_OK;                                                     \
     const int64_t groups = ((tbase + steps - 1) >> 2) - (tbase >> 2) + 1;                        \
     dim3 grid(unsigned((n + 255) / 256), unsigned(groups < 65535 ? groups : 65535));             \
-    k_poisson<T><<<grid, 256, 0, st>>>(n, steps, seed, nbase, tbase, T(lam), T(amp), out, ld);  \
+    k_poisson<T><<<grid, 256, 0, st>>>(n, steps, seed, nbase, tbase, poisson_table<T>(lam, amp),  \
+                                       out, ld);                                                 \
     return cuda_check("k_poisson launch");                                                       \
   }
 

@@ -432,15 +432,23 @@ struct Philox {
   }
 };
 
+// inverse-CDF table of Poisson(lam), built on the host in fp64
 template <typename T>
-__global__ void k_poisson(int64_t n, int64_t steps, uint64_t seed, int64_t nbase, int64_t tbase,
-                          T lam, T amp, T* out, int64_t ld) {
+struct PoissonTab {
+  int size;      // entries used; cdf[size-1] >= 1 - 2^-33
+  T amp;
+  T cdf[48];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint64_t seed,
+                                                 int64_t nbase, int64_t tbase,
+                                                 const PoissonTab<T> tab, T* out, int64_t ld) {
   // one thread = one neuron x 4 consecutive global steps (one Philox block)
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t gj = j + nbase;
-  const T p0 = exp(-lam);
-  const int64_t g_first = (tbase) >> 2, g_last = (tbase + steps - 1) >> 2;
+  const int64_t g_first = tbase >> 2, g_last = (tbase + steps - 1) >> 2;
   for (int64_t gq = g_first + int64_t(blockIdx.y); gq <= g_last; gq += gridDim.y) {
     const uint4 r = Philox::run(make_uint4(uint32_t(gj), uint32_t(uint64_t(gj) >> 32), uint32_t(gq),
                                            uint32_t(uint64_t(gq) >> 32)),
@@ -448,18 +456,12 @@ __global__ void k_poisson(int64_t n, int64_t steps, uint64_t seed, int64_t nbase
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int64_t gt = gq * 4 + q;
-      const int64_t t = gt - tbase;
+      const int64_t t = gq * 4 + q - tbase;
       if (t < 0 || t >= steps) continue;
       const T u = (T(w[q]) + T(0.5)) * T(2.3283064365386963e-10);
-      T pk = p0, cdf = p0;
       int k = 0;
-      while (u > cdf && k < 64) {
-        ++k;
-        pk = pk * lam / T(k);
-        cdf = cdf + pk;
-      }
-      out[t * ld + j] = amp * T(k);
+      while (k < tab.size - 1 && u > tab.cdf[k]) ++k;
+      out[t * ld + j] = tab.amp * T(k);
     }
   }
 }

@@ -1,0 +1,636 @@
+// jit.cu -- runtime specialisation of the float kernels per channel table.
+//
+// The generic kernels in hh_kernels.cuh read the channel table from the
+// kernel-parameter bank and branch on every rate kind and exponent at run
+// time.  ncu on B200 (profiles/round1_fwd_generic.md) showed that this costs
+// ~430 issued instructions per neuron-step for config 2 against 31 MUFU ops,
+// plus instruction-cache misses from the 3-way unrolled code.  Here the same
+// step is generated as CUDA source with every constant an immediate, every
+// kind resolved and every power unrolled, compiled by NVRTC for sm_100a on
+// first use of a table, and cached per (table, device) for the process.
+//
+// The generated module holds the forward kernel (1 and 4 neurons per thread)
+// and the backward kernel; both call the same generated step function, so
+// the backward's segment recompute reproduces the forward's checkpoints bit
+// for bit.  NVRTC is loaded with dlopen and the driver API through
+// cudaGetDriverEntryPoint, so the library still loads on hosts without a GPU.
+// HHB_NO_JIT=1 forces the generic kernels.
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hh_host.cuh"
+
+namespace hhb {
+namespace jit {
+
+// ------------------------------------------------------------ loaders
+struct Nvrtc {
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+struct Driver {
+  decltype(&cuModuleLoadData) load = nullptr;
+  decltype(&cuModuleGetFunction) get = nullptr;
+  decltype(&cuLaunchKernel) launch = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+static std::mutex g_mu;
+static Nvrtc g_nv;
+static Driver g_drv;
+static bool g_loaded = false;
+static std::string g_status = "not initialised";
+
+template <typename F>
+static bool sym(void* h, const char* name, F& out) {
+  out = reinterpret_cast<F>(dlsym(h, name));
+  return out != nullptr;
+}
+
+static void load_libs() {
+  if (g_loaded) return;
+  g_loaded = true;
+  const char* cands[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                         "/usr/local/cuda/lib64/libnvrtc.so", "libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* c : cands) {
+    h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+    if (h) break;
+  }
+  if (!h) {
+    g_nv.why = "libnvrtc.so.12 not found";
+  } else {
+    g_nv.ok = sym(h, "nvrtcCreateProgram", g_nv.create) && sym(h, "nvrtcCompileProgram", g_nv.compile) &&
+              sym(h, "nvrtcGetCUBINSize", g_nv.cubin_size) && sym(h, "nvrtcGetCUBIN", g_nv.cubin) &&
+              sym(h, "nvrtcGetProgramLogSize", g_nv.log_size) && sym(h, "nvrtcGetProgramLog", g_nv.log) &&
+              sym(h, "nvrtcDestroyProgram", g_nv.destroy);
+    if (!g_nv.ok) g_nv.why = "libnvrtc symbols missing";
+  }
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  bool ok = true;
+  ok = ok && cudaGetDriverEntryPoint("cuModuleLoadData", &p, cudaEnableDefault, &q) == cudaSuccess && p;
+  g_drv.load = reinterpret_cast<decltype(g_drv.load)>(p);
+  ok = ok && cudaGetDriverEntryPoint("cuModuleGetFunction", &p, cudaEnableDefault, &q) == cudaSuccess && p;
+  g_drv.get = reinterpret_cast<decltype(g_drv.get)>(p);
+  ok = ok && cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess && p;
+  g_drv.launch = reinterpret_cast<decltype(g_drv.launch)>(p);
+  g_drv.ok = ok;
+  if (!ok) g_drv.why = "driver entry points unavailable";
+}
+
+// ------------------------------------------------------------ codegen
+static std::string fmt(const char* f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+// exact float literal (hex) of a double constant rounded to float
+static std::string F(double x) {
+  const float f = float(x);
+  if (!std::isfinite(f)) return f > 0 ? "__int_as_float(0x7f800000)" : "__int_as_float(0xff800000)";
+  char buf[64];
+  snprintf(buf, sizeof buf, "%af", double(f));
+  return std::string("(") + buf + ")";
+}
+
+// One rate: value (and slope) of kind(a, v0, b) * scale at `v`.
+static void emit_rate(std::string& o, const hhb_rate_t& r, double scale, const std::string& val,
+                      const std::string* slope) {
+  const double A = r.a * scale, K2 = -kLog2e / r.b;
+  o += "  {\n";
+  if (r.kind == HHB_RATE_EXP || r.kind == HHB_RATE_SIGMOID) {
+    o += fmt("    const float e = ex2f_(__fmaf_rn(v, %s, %s));\n", F(K2).c_str(), F(-r.v0 * K2).c_str());
+    if (r.kind == HHB_RATE_EXP) {
+      o += fmt("    %s = __fmul_rn(%s, e);\n", val.c_str(), F(A).c_str());
+      if (slope) o += fmt("    %s = __fmul_rn(%s, %s);\n", slope->c_str(), F(-1.0 / r.b).c_str(), val.c_str());
+    } else {
+      o += "    const float q = rcpf_(__fadd_rn(1.0f, e));\n";
+      o += fmt("    %s = __fmul_rn(%s, q);\n", val.c_str(), F(A).c_str());
+      if (slope)
+        o += fmt("    %s = __fmul_rn(__fmul_rn(%s, %s), __fsub_rn(1.0f, q));\n", slope->c_str(), val.c_str(),
+                 F(1.0 / r.b).c_str());
+    }
+  } else {
+    // linoid a*x/(1-exp(-x/b)); its Bernoulli series where |x/b| < 1/2
+    o += fmt("    const float x = __fsub_rn(v, %s);\n", F(r.v0).c_str());
+    o += fmt("    const float e = ex2f_(__fmul_rn(x, %s));\n", F(K2).c_str());
+    o += "    const float den = __fsub_rn(1.0f, e);\n";
+    o += "    const float rd = rcpf_(den);\n";
+    o += fmt("    %s = __fmul_rn(__fmul_rn(%s, x), rd);\n", val.c_str(), F(A).c_str());
+    if (slope)
+      o += fmt("    %s = __fmul_rn(__fmul_rn(%s, __fsub_rn(den, __fmul_rn(__fmul_rn(x, %s), e))), "
+               "__fmul_rn(rd, rd));\n",
+               slope->c_str(), F(A).c_str(), F(1.0 / r.b).c_str());
+    o += fmt("    const bool sm = fabsf(x) < %s;\n", F(0.5 * std::fabs(r.b)).c_str());
+    o += "    if (__any_sync(0xffffffffu, sm)) {\n";
+    o += fmt("      const float u = __fmul_rn(x, %s);\n", F(1.0 / r.b).c_str());
+    o += "      const float w = __fmul_rn(u, u);\n";
+    o += "      float f = __fmaf_rn(w, -8.267195767195767e-07f, 3.3068783068783070e-05f);\n";
+    o += "      f = __fmaf_rn(w, f, -1.3888888888888889e-03f);\n";
+    o += "      f = __fmaf_rn(w, f, 8.3333333333333333e-02f);\n";
+    o += "      f = __fmaf_rn(w, f, __fmaf_rn(u, 0.5f, 1.0f));\n";
+    o += fmt("      %s = sm ? __fmul_rn(%s, f) : %s;\n", val.c_str(), F(r.a * r.b * scale).c_str(), val.c_str());
+    if (slope) {
+      o += "      float d = __fmaf_rn(w, 2.0876756987868099e-07f, -6.6137566137566138e-06f);\n";
+      o += "      d = __fmaf_rn(w, d, 1.9841269841269841e-04f);\n";
+      o += "      d = __fmaf_rn(w, d, -5.5555555555555556e-03f);\n";
+      o += "      d = __fmaf_rn(w, d, 1.6666666666666667e-01f);\n";
+      o += "      d = __fmaf_rn(u, d, 0.5f);\n";
+      o += fmt("      %s = sm ? __fmul_rn(%s, d) : %s;\n", slope->c_str(), F(A).c_str(), slope->c_str());
+    }
+    o += "    }\n";
+  }
+  o += "  }\n";
+}
+
+static std::string pow_expr(const std::string& p, int k) {
+  if (k == 0) return "1.0f";
+  std::string e = p;
+  for (int i = 1; i < k; ++i) e = "__fmul_rn(" + e + ", " + p + ")";
+  return e;
+}
+
+struct Layout {
+  int ng = 0;
+  std::vector<int> first, last, chan;
+  std::vector<int> leak_ch;
+  double gl = 0, gle = 0;
+};
+
+static Layout layout_of(const hhb_params_t* P) {
+  Layout L;
+  L.ng = P->n_gates;
+  L.first.assign(L.ng, 0);
+  L.last.assign(L.ng, 0);
+  L.chan.assign(L.ng, 0);
+  for (int c = 0; c < P->n_channels; ++c) {
+    const hhb_channel_t& C = P->channels[c];
+    if (C.gate_count == 0) {
+      L.leak_ch.push_back(c);
+      L.gl += C.g_max;
+      L.gle += C.g_max * C.e_rev;
+      continue;
+    }
+    for (int g = C.gate_begin; g < C.gate_begin + C.gate_count; ++g) {
+      L.first[g] = g == C.gate_begin;
+      L.last[g] = g == C.gate_begin + C.gate_count - 1;
+      L.chan[g] = c;
+    }
+  }
+  return L;
+}
+
+// step_fwd(v, p[], cur) -> v' ; p[] updated in place (hh_step, dynamics.py:472-528)
+static std::string emit_forward_step(const hhb_params_t* P, const Layout& L) {
+  std::string o;
+  const int NG = L.ng;
+  o += fmt("__device__ __forceinline__ float step_fwd(const float v, float (&p)[%d], const float cur) {\n",
+           NG > 0 ? NG : 1);
+  o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
+                         : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
+  o += "  float eta = 1.0f;\n";
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  // gate %d (channel %d), exponent %d\n  {\n", g, L.chan[g], G.exponent);
+    const std::string pg = fmt("p[%d]", g);
+    o += "  const float pk = " + pow_expr(pg, G.exponent) + ";\n";
+    o += L.first[g] ? "  eta = pk;\n" : "  eta = __fmul_rn(eta, pk);\n";
+    o += "  float a, b;\n";
+    emit_rate(o, G.alpha, P->rate_scale, "a", nullptr);
+    emit_rate(o, G.beta, P->rate_scale, "b", nullptr);
+    o += "  const float s = __fadd_rn(a, b);\n";
+    o += "  const float pinf = __fmul_rn(a, rcpf_(s));\n";
+    o += fmt("  const float dec = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
+    o += fmt("  const float pn = __fmaf_rn(__fsub_rn(%s, pinf), dec, pinf);\n", pg.c_str());
+    o += fmt("  %s = (s == 0.0f) ? %s : pn;\n", pg.c_str(), pg.c_str());
+    if (L.last[g])
+      o += fmt("  ion = __fmaf_rn(__fmul_rn(eta, %s), __fsub_rn(v, %s), ion);\n", F(C.g_max).c_str(),
+               F(C.e_rev).c_str());
+    o += "  }\n";
+  }
+  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n}\n", F(P->dt / P->c_m).c_str());
+  return o;
+}
+
+// adjoint of step_fwd (hh_step_backward, adjoint.py:116-188)
+static std::string emit_backward_step(const hhb_params_t* P, const Layout& L) {
+  std::string o;
+  const int NG = L.ng, NGX = NG > 0 ? NG : 1;
+  const double dtcm = P->dt / P->c_m;
+  o += fmt(
+      "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[%d], "
+      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
+      "double (&acc)[%d]) {\n",
+      NGX, NGX, kSlots);
+  o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
+                         : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
+  o += fmt("  float gsum = %s;\n", F(L.gl).c_str());
+  o += fmt("  float pk[%d], eta_c[%d];\n", NGX, NGX);
+  o += "  float eta = 1.0f;\n";
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  pk[%d] = %s;\n", g, pow_expr(fmt("p[%d]", g), G.exponent).c_str());
+    o += L.first[g] ? fmt("  eta = pk[%d];\n", g) : fmt("  eta = __fmul_rn(eta, pk[%d]);\n", g);
+    o += fmt("  eta_c[%d] = eta;\n", g);
+    if (L.last[g]) {
+      o += fmt("  ion = __fmaf_rn(__fmul_rn(eta, %s), __fsub_rn(v, %s), ion);\n", F(C.g_max).c_str(),
+               F(C.e_rev).c_str());
+      o += fmt("  gsum = __fmaf_rn(%s, eta, gsum);\n", F(C.g_max).c_str());
+    }
+  }
+  o += fmt("  const float vn = __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n", F(dtcm).c_str());
+  o += "  float g_vp = d_v;\n";
+  o += fmt("  if (has_s) g_vp = __fmaf_rn(d_spike, surrogate(sur, __fsub_rn(vn, %s)), g_vp);\n",
+           F(P->v_theta).c_str());
+  o += "  acc[0] += double(__fmul_rn(g_vp, __fsub_rn(cur, ion)));\n";
+  for (int g = 0; g < NG; ++g) {
+    if (!L.last[g]) continue;
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  acc[%d] += double(__fmul_rn(__fmul_rn(g_vp, eta_c[%d]), __fsub_rn(v, %s)));\n", 1 + g, g,
+             F(C.e_rev).c_str());
+  }
+  for (size_t j = 0; j < L.leak_ch.size(); ++j)
+    o += fmt("  acc[%d] += double(__fmul_rn(g_vp, __fsub_rn(v, %s)));\n", 1 + kMaxGates + int(j),
+             F(P->channels[L.leak_ch[j]].e_rev).c_str());
+  o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  // gate %d\n  {\n  float a, b, da, db;\n", g);
+    std::string sa = "da", sb = "db";
+    emit_rate(o, G.alpha, P->rate_scale, "a", &sa);
+    emit_rate(o, G.beta, P->rate_scale, "b", &sb);
+    o += "  const float s = __fadd_rn(a, b);\n";
+    o += "  const float rs = rcpf_(s);\n";
+    o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
+    o += "  const float pinf = __fmul_rn(a, rs);\n";
+    o += "  const float dpinf = __fmul_rn(__fsub_rn(__fmul_rn(da, b), __fmul_rn(a, db)), __fmul_rn(rs, rs));\n";
+    o += fmt("  const float term = __fmaf_rn(dpinf, __fsub_rn(1.0f, e), __fmul_rn(__fsub_rn(p[%d], pinf), "
+             "__fmul_rn(__fmul_rn(%s, __fadd_rn(da, db)), e)));\n",
+             g, F(-P->dt).c_str());
+    o += "  const bool pos = s > 0.0f;\n";
+    o += fmt("  const float up = d_p[%d];\n", g);
+    o += "  dv_in = pos ? __fmaf_rn(up, term, dv_in) : dv_in;\n";
+    o += "  float dp = pos ? __fmul_rn(up, e) : up;\n";
+    if (G.exponent > 0) {
+      // d eta / d p = k p^(k-1) prod(other gates of the channel)
+      std::string der = fmt("__fmul_rn(%s, %s)", F(double(G.exponent)).c_str(),
+                            pow_expr(fmt("p[%d]", g), G.exponent - 1).c_str());
+      const hhb_channel_t& CC = P->channels[L.chan[g]];
+      for (int o2 = CC.gate_begin; o2 < CC.gate_begin + CC.gate_count; ++o2)
+        if (o2 != g) der = fmt("__fmul_rn(%s, pk[%d])", der.c_str(), o2);
+      o += fmt("  dp = __fmaf_rn(__fmul_rn(__fmul_rn(g_vp, %s), __fsub_rn(v, %s)), %s, dp);\n",
+               F(-dtcm * C.g_max).c_str(), F(C.e_rev).c_str(), der.c_str());
+    }
+    o += fmt("  d_p[%d] = dp;\n  }\n", g);
+  }
+  o += "  d_v = dv_in;\n";
+  o += fmt("  return __fmul_rn(g_vp, %s);\n}\n", F(dtcm).c_str());
+  return o;
+}
+
+// Kernel bodies (parameterised by NG through the generated step functions).
+static const char* kPrelude = R"(
+typedef long long i64;
+typedef unsigned int u32;
+struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
+  const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
+  i64 ck_every, ck_ld; i64 step_base; i64* first_bad; };
+struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
+  float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
+  i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad; };
+struct Sur { int kind; float w, inv_w, k2, half_inv_w; };
+#define LLMAX 0x7fffffffffffffffLL
+__device__ __forceinline__ float ex2f_(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rcpf_(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ bool finitef_(float x) { return fabsf(x) < __int_as_float(0x7f800000); }
+__device__ __forceinline__ float surrogate(const Sur& s, float u) {
+  if (s.kind == 1) return (fabsf(u) <= s.w) ? s.half_inv_w : 0.0f;
+  const float q = rcpf_(__fadd_rn(1.0f, ex2f_(__fmul_rn(u, s.k2))));
+  return __fmul_rn(__fmul_rn(q, __fsub_rn(1.0f, q)), s.inv_w);
+}
+)";
+
+static const char* kForwardBody = R"(
+template <int VEC>
+__device__ __forceinline__ void load_cur(const FwdArgs& a, i64 t, i64 n0, bool full, float (&c)[VEC]) {
+  if (VEC == 4 && full && a.i_sn == 1) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(a.i_ext + t * a.i_st + n0));
+    c[0] = q.x; c[1] = q.y; c[2] = q.z; c[3] = q.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) c[j] = (n0 + j < a.n) ? __ldg(a.i_ext + t * a.i_st + (n0 + j) * a.i_sn) : 0.0f;
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* p, const float (&x)[VEC], bool full, i64 n0, i64 n) {
+  if (VEC == 4 && full) { *reinterpret_cast<float4*>(p + n0) = make_float4(x[0], x[1], x[2], x[3]); }
+  else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) if (n0 + j < n) p[n0 + j] = x[j];
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void fwd_body(const FwdArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 n0 = tid * VEC;
+  const bool full = n0 + VEC <= a.n;
+  float v[VEC];
+  float p[VEC][NGX];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const bool on = n0 + j < a.n;
+    v[j] = on ? a.v_in[n0 + j] : -65.0f;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) p[j][g] = on ? a.g_in[g * a.g_ld + n0 + j] : 0.5f;
+  }
+  i64 bad = LLMAX, ck_slot = 0, ck_count = 0;
+  float cur[VEC];
+  if (a.steps > 0) load_cur<VEC>(a, 0, n0, full, cur);
+  for (i64 t = 0; t < a.steps; ++t) {
+    float nxt[VEC];
+    if (t + 1 < a.steps) load_cur<VEC>(a, t + 1, n0, full, nxt);
+    if (a.ckpt != nullptr && ck_count == 0) {
+      float* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
+      store_vec<VEC>(base, v, full, n0, a.n);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        float q[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) q[j] = p[j][g];
+        store_vec<VEC>(base + (1 + g) * a.ck_ld, q, full, n0, a.n);
+      }
+      ++ck_slot;
+      ck_count = a.ck_every;
+    }
+    --ck_count;
+    u32 nib = 0;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const float vn = step_fwd(v[j], p[j], cur[j]);
+      nib |= u32((v[j] < THETA) && (vn >= THETA) && (n0 + j < a.n)) << j;
+      if (!finitef_(vn) && bad == LLMAX && n0 + j < a.n) bad = a.step_base + t;
+      v[j] = vn;
+    }
+    if (a.v_out != nullptr) store_vec<VEC>(a.v_out + t * a.v_ld, v, full, n0, a.n);
+    if (a.spk != nullptr) {
+      u32 w;
+      if (VEC == 1) {
+        w = __ballot_sync(0xffffffffu, nib != 0);
+      } else {
+        w = nib << (VEC * (lane % (32 / VEC)));
+#pragma unroll
+        for (int o = 1; o < 32 / VEC; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
+      }
+      if (lane % (32 / VEC) == 0 && n0 < a.n) a.spk[t * a.spk_ld + n0 / 32] = w;
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
+  }
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    if (n0 + j < a.n) {
+      a.v_fin[n0 + j] = v[j];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) a.g_fin[g * a.g_ld + n0 + j] = p[j][g];
+    }
+  }
+  if (bad != LLMAX) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
+}
+extern "C" __global__ void __launch_bounds__(256) hh_fwd_v1(const FwdArgs a) { fwd_body<1>(a); }
+extern "C" __global__ void __launch_bounds__(256) hh_fwd_v4(const FwdArgs a) { fwd_body<4>(a); }
+
+__device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
+  v = base[i];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) p[g] = base[(1 + g) * ld + i];
+}
+__device__ __forceinline__ void store_state(float* base, i64 ld, i64 i, float v, const float (&p)[NGX]) {
+  base[i] = v;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) base[(1 + g) * ld + i] = p[g];
+}
+extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, const BwdArgs a) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool on = i < a.n;
+  const i64 ii = on ? i : 0;
+  double acc[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) acc[s] = 0.0;
+  i64 bad = -1;
+  float d_v = on ? a.adj_v[ii] : 0.0f;
+  float d_p[NGX];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) d_p[g] = on ? a.adj_g[g * a.ag_ld + ii] : 0.0f;
+  const i64 K = a.ck_every;
+  const i64 nseg = (a.steps + K - 1) / K;
+  const i64 sstride = (1 + NG) * a.ck_ld;
+  const bool has_s = a.seed_s != nullptr;
+  for (i64 seg = nseg - 1; seg >= 0; --seg) {
+    const i64 lo = seg * K;
+    const i64 hi = (lo + K < a.steps) ? lo + K : a.steps;
+    const float* ck = a.ckpt + seg * sstride;
+    float v, p[NGX];
+    load_state(ck, a.ck_ld, ii, v, p);
+    if (K > 1) {
+      for (i64 t = lo; t < hi - 1; ++t) {
+        const float cur = __ldg(a.i_ext + t * a.i_st + ii * a.i_sn);
+        v = step_fwd(v, p, cur);
+        if (on) store_state(a.seg + (t + 1 - lo) * sstride, a.ck_ld, ii, v, p);
+      }
+    }
+    for (i64 t = hi - 1; t >= lo; --t) {
+      if (t != hi - 1 || K == 1) {
+        const float* src = (K == 1) ? a.ckpt + t * sstride : (t == lo ? ck : a.seg + (t - lo) * sstride);
+        load_state(src, a.ck_ld, ii, v, p);
+      }
+      const float cur = __ldg(a.i_ext + t * a.i_st + ii * a.i_sn);
+      if (a.seed_v != nullptr) d_v = __fadd_rn(d_v, __ldg(a.seed_v + t * a.sv_ld + ii));
+      const float ds = has_s ? __ldg(a.seed_s + t * a.ss_ld + ii) : 0.0f;
+      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, has_s, acc);
+      if (on && a.d_i != nullptr) a.d_i[t * a.di_ld + ii] = di;
+      bool ok = finitef_(d_v);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[g]);
+      if (!ok && bad < 0 && on) bad = a.step_base + t;
+    }
+  }
+  if (on) {
+    a.adj_v[ii] = d_v;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii] = d_p[g];
+  }
+  if (bad >= 0) atomicMax(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
+  __shared__ double red[BWD_THREADS / 32][SLOTS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    double x = on ? acc[s] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp][s] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < SLOTS) {
+    double x = 0.0;
+    for (int w = 0; w < BWD_THREADS / 32; ++w) x += red[w][threadIdx.x];
+    a.partials[i64(blockIdx.x) * SLOTS + threadIdx.x] = x;
+  }
+}
+)";
+
+static std::string generate(const hhb_params_t* P) {
+  const Layout L = layout_of(P);
+  std::string src = kPrelude;
+  src += fmt("#define NG %d\n#define NGX %d\n#define SLOTS %d\n#define BWD_THREADS %d\n", L.ng,
+             L.ng > 0 ? L.ng : 1, kSlots, kBwdThreads);
+  src += fmt("#define THETA %s\n", F(P->v_theta).c_str());
+  src += emit_forward_step(P, L);
+  src += emit_backward_step(P, L);
+  src += kForwardBody;
+  return src;
+}
+
+// ------------------------------------------------------------ cache
+struct Module {
+  CUfunction fwd1 = nullptr, fwd4 = nullptr, bwd = nullptr;
+  bool ok = false;
+};
+static std::map<std::string, Module> g_cache;
+
+static std::string key_of(const hhb_params_t* P, int dev) {
+  hhb_params_t Q;
+  memset(&Q, 0, sizeof Q);
+  Q.n_gates = P->n_gates;
+  Q.n_channels = P->n_channels;
+  Q.c_m = P->c_m;
+  Q.dt = P->dt;
+  Q.v_theta = P->v_theta;
+  Q.rate_scale = P->rate_scale;
+  for (int g = 0; g < P->n_gates; ++g) {
+    Q.gates[g].alpha = {P->gates[g].alpha.kind, 0, P->gates[g].alpha.a, P->gates[g].alpha.v0, P->gates[g].alpha.b};
+    Q.gates[g].beta = {P->gates[g].beta.kind, 0, P->gates[g].beta.a, P->gates[g].beta.v0, P->gates[g].beta.b};
+    Q.gates[g].exponent = P->gates[g].exponent;
+    Q.gates[g].channel = P->gates[g].channel;
+  }
+  for (int c = 0; c < P->n_channels; ++c) Q.channels[c] = P->channels[c];
+  std::string k(reinterpret_cast<const char*>(&Q), sizeof Q);
+  k += std::to_string(dev);
+  return k;
+}
+
+static bool disabled() {
+  const char* e = getenv("HHB_NO_JIT");
+  return e && e[0] && e[0] != '0';
+}
+
+static Module* get_module(const hhb_params_t* P) {
+  if (disabled()) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_mu);
+  load_libs();
+  if (!g_nv.ok || !g_drv.ok) {
+    g_status = "jit unavailable: " + (g_nv.ok ? g_drv.why : g_nv.why);
+    return nullptr;
+  }
+  const std::string key = key_of(P, dev);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return it->second.ok ? &it->second : nullptr;
+  Module& m = g_cache[key];
+  const std::string src = generate(P);
+  nvrtcProgram prog;
+  if (g_nv.create(&prog, src.c_str(), "hh_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    g_status = "nvrtcCreateProgram failed";
+    return nullptr;
+  }
+  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-lineinfo", "-default-device"};
+  const nvrtcResult rc = g_nv.compile(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    g_nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    g_nv.log(prog, &log[0]);
+    g_status = "nvrtc compile failed: " + log.substr(0, 2000);
+    g_nv.destroy(&prog);
+    return nullptr;
+  }
+  size_t n = 0;
+  g_nv.cubin_size(prog, &n);
+  std::vector<char> cubin(n);
+  g_nv.cubin(prog, cubin.data());
+  g_nv.destroy(&prog);
+  CUmodule mod;
+  if (g_drv.load(&mod, cubin.data()) != CUDA_SUCCESS || g_drv.get(&m.fwd1, mod, "hh_fwd_v1") != CUDA_SUCCESS ||
+      g_drv.get(&m.fwd4, mod, "hh_fwd_v4") != CUDA_SUCCESS || g_drv.get(&m.bwd, mod, "hh_bwd") != CUDA_SUCCESS) {
+    g_status = "cuModuleLoadData / cuModuleGetFunction failed";
+    return nullptr;
+  }
+  m.ok = true;
+  g_status = "ok";
+  return &m;
+}
+
+}  // namespace jit
+
+// Returns true when the JIT kernel was launched (rc holds its status).
+bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, bool vec4, cudaStream_t st, int& rc) {
+  jit::Module* m = jit::get_module(P);
+  if (!m) return false;
+  const int VEC = vec4 ? 4 : 1;
+  const int64_t threads = (a.n + VEC - 1) / VEC;
+  const int tpb = fwd_block(threads);
+  const int64_t blocks = (threads + tpb - 1) / tpb;
+  FwdArgs<float> args = a;
+  void* params[] = {&args};
+  const CUresult r = jit::g_drv.launch(vec4 ? m->fwd4 : m->fwd1, unsigned(blocks), 1, 1, unsigned(tpb), 1, 1, 0,
+                                       reinterpret_cast<CUstream>(st), params, nullptr);
+  rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit forward launch failed");
+  return true;
+}
+
+bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs<float>& a, cudaStream_t st,
+                  int& rc) {
+  jit::Module* m = jit::get_module(P);
+  if (!m) return false;
+  const int64_t blocks = bwd_blocks(a.n);
+  DevSur<float> s = sur;
+  BwdArgs<float> args = a;
+  void* params[] = {&s, &args};
+  const CUresult r = jit::g_drv.launch(m->bwd, unsigned(blocks), 1, 1, unsigned(kBwdThreads), 1, 1, 0,
+                                       reinterpret_cast<CUstream>(st), params, nullptr);
+  rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit backward launch failed");
+  return true;
+}
+
+const char* jit_status() { return jit::g_status.c_str(); }
+
+std::string jit_source(const hhb_params_t* P) { return jit::generate(P); }
+
+}  // namespace hhb

