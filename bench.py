@@ -305,7 +305,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "k_forward_dram.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            traffic = json.load(open(tp))["bytes_per_neuron_step"] * ns_per_launch
         except (OSError, ValueError):
             traffic = None
     peaks = {}
