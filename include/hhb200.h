@@ -126,6 +126,22 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
                 int64_t step_base, int64_t* first_bad, void* stream);
 
 /*
+ * hhb_forward_poisson -- hhb_forward with the BASELINE config-2 stimulus
+ * I[t][j] = amp * Poisson(lam) drawn inside the kernel (Philox-4x32-10 keyed by
+ * (seed, neuron_base + j, (step_base + t) / 4)): bit-identical to running
+ * hhb_poisson_current into a buffer and hhb_forward on it, without the
+ * 4 B/neuron-step write and re-read.  Other arguments as hhb_forward.
+ */
+int hhb_forward_poisson(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                        const void* v_in, const void* g_in, int64_t g_ld,
+                        void* v_fin, void* g_fin,
+                        uint64_t seed, int64_t neuron_base, double lam, double amp,
+                        void* v_out, int64_t v_ld,
+                        uint32_t* spk_out, int64_t spk_ld,
+                        void* ckpt, int64_t ckpt_every, int64_t ckpt_ld,
+                        int64_t step_base, int64_t* first_bad, void* stream);
+
+/*
  * hhb_backward -- replaces backward_through_time() (adjoint.py:281-365) and
  * hh_step_backward() (adjoint.py:102-194).  One launch runs the whole reverse
  * sweep: for each checkpoint segment, newest first, it recomputes the segment

@@ -73,6 +73,13 @@ SIGNATURES = {
                             _vp, _i64,
                             _vp, _vp,
                             _i64, _vp, _vp]),
+    "hhb_forward_poisson": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
+                                   _vp, _vp, _i64, _vp, _vp,
+                                   C.c_uint64, _i64, _dbl, _dbl,
+                                   _vp, _i64,
+                                   _vp, _i64,
+                                   _vp, _i64, _i64,
+                                   _i64, _vp, _vp]),
     "hhb_backward_partials": (_i64, [_i64, _i32]),
     "hhb_gate_rates": (_i32, [C.POINTER(Gate), _dbl, _i32, _i64, _vp, _vp, _vp, _vp]),
     "hhb_rate_eval": (_i32, [C.POINTER(Rate), _i32, _i32, _i64, _vp, _vp, _vp]),

@@ -53,7 +53,36 @@ static int forward_t(const hhb_params_t* P, int64_t n, int64_t steps, const void
   a.ck_ld = ck_ld;
   a.step_base = step_base;
   a.first_bad = reinterpret_cast<long long*>(first_bad);
-  return Flavour<T>::forward(P, a, st);
+  return Flavour<T>::forward(P, a, nullptr, st);
+}
+
+template <typename T>
+static int forward_poisson_t(const hhb_params_t* P, int64_t n, int64_t steps, const void* v_in,
+                             const void* g_in, int64_t g_ld, void* v_fin, void* g_fin, uint64_t seed,
+                             int64_t nbase, double lam, double amp, void* v_out, int64_t v_ld,
+                             uint32_t* spk, int64_t spk_ld, void* ckpt, int64_t ck_every,
+                             int64_t ck_ld, int64_t step_base, int64_t* first_bad, cudaStream_t st) {
+  FwdArgs<T> a{};
+  a.n = n;
+  a.steps = steps;
+  a.v_in = static_cast<const T*>(v_in);
+  a.g_in = static_cast<const T*>(g_in);
+  a.g_ld = g_ld;
+  a.v_fin = static_cast<T*>(v_fin);
+  a.g_fin = static_cast<T*>(g_fin);
+  a.v_out = static_cast<T*>(v_out);
+  a.v_ld = v_ld;
+  a.spk = spk;
+  a.spk_ld = spk_ld;
+  a.ckpt = static_cast<T*>(ckpt);
+  a.ck_every = ck_every;
+  a.ck_ld = ck_ld;
+  a.step_base = step_base;
+  a.first_bad = reinterpret_cast<long long*>(first_bad);
+  a.seed = seed;
+  a.nbase = nbase;
+  const PoissonTab<T> tab = poisson_table<T>(lam, amp);
+  return Flavour<T>::forward(P, a, &tab, st);
 }
 
 template <typename T>
@@ -152,6 +181,30 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
   return forward_t<double>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                            v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
                            first_bad, ST(stream));
+}
+
+int hhb_forward_poisson(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                        const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
+                        uint64_t seed, int64_t neuron_base, double lam, double amp, void* v_out,
+                        int64_t v_ld, uint32_t* spk_out, int64_t spk_ld, void* ckpt, int64_t ckpt_every,
+                        int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream) {
+  int rc = check_params(params);
+  if (rc) return rc;
+  if ((rc = check_dtype(dtype))) return rc;
+  if (n < 0 || n_steps < 0 || !(lam >= 0)) return fail(HHB_EINVAL, "bad n, n_steps or lam");
+  if (n == 0) return HHB_OK;
+  if (!v_in || !v_fin || first_bad == nullptr) return fail(HHB_EINVAL, "v_in, v_fin, first_bad required");
+  if (params->n_gates > 0 && (!g_in || !g_fin || g_ld < n)) return fail(HHB_EINVAL, "gate state required");
+  if (v_out && v_ld < n) return fail(HHB_EINVAL, "v_ld < n");
+  if (spk_out && spk_ld < (n + 31) / 32) return fail(HHB_EINVAL, "spk_ld < ceil(n/32)");
+  if (ckpt && (ckpt_every < 1 || ckpt_ld < n)) return fail(HHB_EINVAL, "bad checkpoint layout");
+  if (dtype == HHB_F32)
+    return forward_poisson_t<float>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, seed, neuron_base,
+                                    lam, amp, v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld,
+                                    step_base, first_bad, ST(stream));
+  return forward_poisson_t<double>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, seed, neuron_base,
+                                   lam, amp, v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld,
+                                   step_base, first_bad, ST(stream));
 }
 
 int64_t hhb_backward_partials(int64_t n, int32_t dtype) {

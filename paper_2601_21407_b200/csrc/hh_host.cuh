@@ -184,8 +184,9 @@ inline int grid_1d(int64_t n, int threads) {
 }
 
 // ------------------------------------------------------------ launchers
-template <typename T, int VEC>
-int launch_forward_vec(const DevTable<T>& tb, const FwdArgs<T>& a, cudaStream_t st) {
+template <typename T, int VEC, bool POIS>
+int launch_forward_vec(const DevTable<T>& tb, const FwdArgs<T>& a, const PoissonTab<T>& ptab,
+                       cudaStream_t st) {
   const int64_t threads = (a.n + VEC - 1) / VEC;
   const int tpb = fwd_block(threads);
   const int64_t blocks = (threads + tpb - 1) / tpb;
@@ -193,7 +194,7 @@ int launch_forward_vec(const DevTable<T>& tb, const FwdArgs<T>& a, cudaStream_t 
   switch (tb.ng) {
 #define HHB_CASE(NG) \
   case NG:           \
-    k_forward<T, NG, VEC><<<unsigned(blocks), tpb, 0, st>>>(tb, a); \
+    k_forward<T, NG, VEC, POIS><<<unsigned(blocks), tpb, 0, st>>>(tb, a, ptab); \
     break;
     HHB_CASE(0) HHB_CASE(1) HHB_CASE(2) HHB_CASE(3) HHB_CASE(4)
     HHB_CASE(5) HHB_CASE(6) HHB_CASE(7) HHB_CASE(8)
@@ -246,16 +247,18 @@ int launch_ionic(const DevTable<T>& tb, int64_t n, const T* v, const T* g, int64
 
 // Runtime-specialised float kernels (jit.cu).  Return false when the JIT is
 // unavailable or disabled; the generic kernels then run.
-bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, bool vec4, cudaStream_t st, int& rc);
+bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTab<float>* ptab, bool vec4,
+                 cudaStream_t st, int& rc);
 bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs<float>& a, cudaStream_t st,
                   int& rc);
 const char* jit_status();
 std::string jit_source(const hhb_params_t* P);
 
 template <typename T>
-inline bool try_jit_fwd(const hhb_params_t* P, const FwdArgs<T>& a, bool vec4, cudaStream_t st, int& rc) {
+inline bool try_jit_fwd(const hhb_params_t* P, const FwdArgs<T>& a, const PoissonTab<T>* ptab, bool vec4,
+                        cudaStream_t st, int& rc) {
   if constexpr (sizeof(T) == 4) {
-    return jit_forward(P, a, vec4, st, rc);
+    return jit_forward(P, a, ptab, vec4, st, rc);
   } else {
     return false;
   }
@@ -273,7 +276,9 @@ inline bool try_jit_bwd(const hhb_params_t* P, const DevSur<T>& s, const BwdArgs
 // Flavour entry points (one definition per TU: hh_f32.cu / hh_f64.cu).
 template <typename T>
 struct Flavour {
-  static int forward(const hhb_params_t* P, const FwdArgs<T>& a, cudaStream_t st);
+  // ptab != nullptr: the current is the fused Poisson stimulus (a.seed, a.nbase)
+  static int forward(const hhb_params_t* P, const FwdArgs<T>& a, const PoissonTab<T>* ptab,
+                     cudaStream_t st);
   static int backward(const hhb_params_t* P, const hhb_surrogate_t* S, const BwdArgs<T>& a,
                       double* d_params, cudaStream_t st);
   static int gate_rates(const hhb_gate_t* G, double scale, int64_t n, const T* v, T* al, T* be,
@@ -294,20 +299,27 @@ struct Flavour {
 // Shared definitions, included once by each flavour TU with T fixed.
 #define HHB_DEFINE_FLAVOUR(T, VECW)                                                              \
   template <>                                                                                    \
-  int Flavour<T>::forward(const hhb_params_t* P, const FwdArgs<T>& a, cudaStream_t st) {         \
+  int Flavour<T>::forward(const hhb_params_t* P, const FwdArgs<T>& a, const PoissonTab<T>* ptab,  \
+                          cudaStream_t st) {                                                     \
     const DevTable<T> tb = pack_table<T>(P);                                                     \
+    const bool pois = ptab != nullptr;                                                           \
+    const PoissonTab<T> pt = pois ? *ptab : PoissonTab<T>{};                                     \
     const bool vec_ok =                                                                          \
-        (a.n % (VECW) == 0) && (a.i_sn == 1) && (a.i_st % (VECW) == 0) &&                        \
-        (reinterpret_cast<uintptr_t>(a.i_ext) % (sizeof(T) * (VECW)) == 0) &&                     \
+        (a.n % (VECW) == 0) &&                                                                   \
+        (pois || ((a.i_sn == 1) && (a.i_st % (VECW) == 0) &&                                     \
+                  (reinterpret_cast<uintptr_t>(a.i_ext) % (sizeof(T) * (VECW)) == 0))) &&        \
         (a.v_out == nullptr ||                                                                   \
          (a.v_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.v_out) % (sizeof(T) * (VECW)) == 0)) && \
         (a.ckpt == nullptr ||                                                                    \
          (a.ck_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.ckpt) % (sizeof(T) * (VECW)) == 0)); \
     const bool wide = vec_ok && a.n >= int64_t(kNumSMs) * 32 * (VECW);                            \
     int jrc = HHB_OK;                                                                            \
-    if (try_jit_fwd<T>(P, a, wide && (VECW) == 4, st, jrc)) return jrc;                          \
-    if (wide) return launch_forward_vec<T, VECW>(tb, a, st);                                     \
-    return launch_forward_vec<T, 1>(tb, a, st);                                                  \
+    if (try_jit_fwd<T>(P, a, ptab, wide && (VECW) == 4, st, jrc)) return jrc;                    \
+    if (pois)                                                                                    \
+      return wide ? launch_forward_vec<T, VECW, true>(tb, a, pt, st)                             \
+                  : launch_forward_vec<T, 1, true>(tb, a, pt, st);                               \
+    if (wide) return launch_forward_vec<T, VECW, false>(tb, a, pt, st);                          \
+    return launch_forward_vec<T, 1, false>(tb, a, pt, st);                                       \
   }                                                                                              \
   template <>                                                                                    \
   int Flavour<T>::backward(const hhb_params_t* P, const hhb_surrogate_t* S,                      \

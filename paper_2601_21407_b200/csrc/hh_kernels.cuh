@@ -39,6 +39,8 @@ struct FwdArgs {
   int64_t ck_every, ck_ld;
   int64_t step_base;
   long long* first_bad;
+  uint64_t seed;    // fused Poisson stimulus (hhb_forward_poisson): Philox key
+  int64_t nbase;    //   global id of neuron 0 of this launch
 };
 
 template <typename T>
@@ -97,6 +99,44 @@ struct Vec<double, 2> {
   }
 };
 
+// ------------------------------------------------------------ stimulus RNG
+// Philox-4x32-10 (Salmon et al. 2011): counter = (global neuron, global step/4),
+// key = seed; one block of 4 words drives 4 consecutive global steps.
+struct Philox {
+  __device__ static uint4 run(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+      const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+      c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    return c;
+  }
+  __device__ static uint4 block(uint64_t seed, int64_t gj, int64_t gq) {
+    return run(make_uint4(uint32_t(gj), uint32_t(uint64_t(gj) >> 32), uint32_t(gq), uint32_t(uint64_t(gq) >> 32)),
+               make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+  }
+};
+
+// inverse-CDF table of Poisson(lam), built on the host in fp64
+template <typename T>
+struct PoissonTab {
+  int size;      // entries used; cdf[size-1] >= 1 - 2^-33
+  T amp;
+  T cdf[48];
+};
+
+// amp * Poisson(lam) from one uniform 32-bit word (inverse CDF)
+template <typename T>
+__device__ __forceinline__ T poisson_draw(const PoissonTab<T>& tab, uint32_t word) {
+  const T u = (T(word) + T(0.5)) * T(2.3283064365386963e-10);
+  int k = 0;
+  while (k < tab.size - 1 && u > tab.cdf[k]) ++k;
+  return tab.amp * T(k);
+}
+
 // current of VEC consecutive neurons at step t; vector load when dense
 template <typename T, int VEC>
 __device__ __forceinline__ void load_cur(const FwdArgs<T>& a, int64_t t, int64_t n0, bool full,
@@ -128,14 +168,43 @@ __device__ __forceinline__ uint32_t spike_word(const bool (&s)[VEC], int lane) {
   }
 }
 
+// Per-thread source of the injected current: the i_ext array (load, with the
+// next step prefetched by the caller) or, for POIS, the Poisson stimulus drawn
+// in registers from the Philox block of (global neuron, global step / 4) --
+// the exact stream k_poisson writes, without its HBM round trip.
+template <typename T, int VEC, bool POIS>
+struct Stimulus {
+  uint4 blk[VEC];
+  __device__ __forceinline__ void at(const FwdArgs<T>& a, const PoissonTab<T>& tab, int64_t t, int64_t n0,
+                                     bool full, T (&c)[VEC]) {
+    if constexpr (POIS) {
+      const int64_t gt = a.step_base + t;
+      const int q = int(gt & 3);
+      if (q == 0 || t == 0) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) blk[j] = Philox::block(a.seed, a.nbase + n0 + j, gt >> 2);
+      }
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const uint32_t w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
+        c[j] = poisson_draw(tab, w);
+      }
+    } else {
+      load_cur<T, VEC>(a, t, n0, full, c);
+    }
+  }
+};
+
 // ------------------------------------------------------------ forward
-template <typename T, int NG, int VEC>
-__global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, const FwdArgs<T> a) {
+template <typename T, int NG, int VEC, bool POIS>
+__global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, const FwdArgs<T> a,
+                                                         const PoissonTab<T> ptab) {
   constexpr int NGX = NG > 0 ? NG : 1;
   const int lane = threadIdx.x & 31;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t n0 = tid * VEC;
   const bool full = n0 + VEC <= a.n;
+  Stimulus<T, VEC, POIS> stim;
 
   T v[VEC];
   T p[VEC][NGX];
@@ -151,10 +220,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
   int64_t ck_count = 0;
 
   T cur[VEC];
-  if (a.steps > 0) load_cur<T, VEC>(a, 0, n0, full, cur);
+  if (a.steps > 0) stim.at(a, ptab, 0, n0, full, cur);
   for (int64_t t = 0; t < a.steps; ++t) {
     T nxt[VEC];
-    if (t + 1 < a.steps) load_cur<T, VEC>(a, t + 1, n0, full, nxt);
+    if (t + 1 < a.steps) stim.at(a, ptab, t + 1, n0, full, nxt);
     if (a.ckpt != nullptr && ck_count == 0) {  // state BEFORE step t
       T* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       if (full) {
@@ -418,28 +487,6 @@ __global__ void k_surrogate(const DevSur<T> s, int64_t n, const T* u, T* out) {
 }
 
 // ------------------------------------------------------------ stimulus
-struct Philox {
-  __device__ static uint4 run(uint4 c, uint2 k) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-      const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-      const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-      c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    return c;
-  }
-};
-
-// inverse-CDF table of Poisson(lam), built on the host in fp64
-template <typename T>
-struct PoissonTab {
-  int size;      // entries used; cdf[size-1] >= 1 - 2^-33
-  T amp;
-  T cdf[48];
-};
-
 template <typename T>
 __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint64_t seed,
                                                  int64_t nbase, int64_t tbase,
@@ -458,10 +505,7 @@ __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint6
     for (int q = 0; q < 4; ++q) {
       const int64_t t = gq * 4 + q - tbase;
       if (t < 0 || t >= steps) continue;
-      const T u = (T(w[q]) + T(0.5)) * T(2.3283064365386963e-10);
-      int k = 0;
-      while (k < tab.size - 1 && u > tab.cdf[k]) ++k;
-      out[t * ld + j] = tab.amp * T(k);
+      out[t * ld + j] = poisson_draw(tab, w[q]);
     }
   }
 }

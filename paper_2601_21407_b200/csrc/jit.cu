@@ -320,7 +320,27 @@ typedef long long i64;
 typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
-  i64 ck_every, ck_ld; i64 step_base; i64* first_bad; };
+  i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase; };
+struct PoissonTab { int size; float amp; float cdf[48]; };
+__device__ __forceinline__ uint4 philox(unsigned long long seed, i64 gj, i64 gq) {
+  uint4 c = make_uint4(u32(gj), u32((unsigned long long)gj >> 32), u32(gq), u32((unsigned long long)gq >> 32));
+  uint2 k = make_uint2(u32(seed), u32(seed >> 32));
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const u32 hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const u32 hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+__device__ __forceinline__ float poisson_draw(const PoissonTab& tab, u32 word) {
+  const float u = (float(word) + 0.5f) * 2.3283064365386963e-10f;
+  int k = 0;
+  while (k < tab.size - 1 && u > tab.cdf[k]) ++k;
+  return tab.amp * float(k);
+}
 struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
   float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
   i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad; };
@@ -355,12 +375,35 @@ __device__ __forceinline__ void store_vec(float* p, const float (&x)[VEC], bool 
     for (int j = 0; j < VEC; ++j) if (n0 + j < n) p[n0 + j] = x[j];
   }
 }
-template <int VEC>
-__device__ __forceinline__ void fwd_body(const FwdArgs& a) {
+template <int VEC, bool POIS>
+struct Stimulus {
+  uint4 blk[VEC];
+  __device__ __forceinline__ void at(const FwdArgs& a, const PoissonTab& tab, i64 t, i64 n0, bool full,
+                                     float (&c)[VEC]) {
+    if (POIS) {
+      const i64 gt = a.step_base + t;
+      const int q = int(gt & 3);
+      if (q == 0 || t == 0) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) blk[j] = philox(a.seed, a.nbase + n0 + j, gt >> 2);
+      }
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const u32 w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
+        c[j] = poisson_draw(tab, w);
+      }
+    } else {
+      load_cur<VEC>(a, t, n0, full, c);
+    }
+  }
+};
+template <int VEC, bool POIS>
+__device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab) {
   const int lane = threadIdx.x & 31;
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = tid * VEC;
   const bool full = n0 + VEC <= a.n;
+  Stimulus<VEC, POIS> stim;
   float v[VEC];
   float p[VEC][NGX];
 #pragma unroll
@@ -372,10 +415,10 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a) {
   }
   i64 bad = LLMAX, ck_slot = 0, ck_count = 0;
   float cur[VEC];
-  if (a.steps > 0) load_cur<VEC>(a, 0, n0, full, cur);
+  if (a.steps > 0) stim.at(a, tab, 0, n0, full, cur);
   for (i64 t = 0; t < a.steps; ++t) {
     float nxt[VEC];
-    if (t + 1 < a.steps) load_cur<VEC>(a, t + 1, n0, full, nxt);
+    if (t + 1 < a.steps) stim.at(a, tab, t + 1, n0, full, nxt);
     if (a.ckpt != nullptr && ck_count == 0) {
       float* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       store_vec<VEC>(base, v, full, n0, a.n);
@@ -423,8 +466,10 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a) {
   }
   if (bad != LLMAX) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
 }
-extern "C" __global__ void __launch_bounds__(256) hh_fwd_v1(const FwdArgs a) { fwd_body<1>(a); }
-extern "C" __global__ void __launch_bounds__(256) hh_fwd_v4(const FwdArgs a) { fwd_body<4>(a); }
+extern "C" __global__ void __launch_bounds__(256) hh_fwd_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, false>(a, t); }
+extern "C" __global__ void __launch_bounds__(256) hh_fwd_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, false>(a, t); }
+extern "C" __global__ void __launch_bounds__(256) hh_fwdp_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, true>(a, t); }
+extern "C" __global__ void __launch_bounds__(256) hh_fwdp_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, true>(a, t); }
 
 __device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
   v = base[i];
@@ -519,7 +564,7 @@ static std::string generate(const hhb_params_t* P) {
 
 // ------------------------------------------------------------ cache
 struct Module {
-  CUfunction fwd1 = nullptr, fwd4 = nullptr, bwd = nullptr;
+  CUfunction fwd1 = nullptr, fwd4 = nullptr, fwdp1 = nullptr, fwdp4 = nullptr, bwd = nullptr;
   bool ok = false;
 };
 static std::map<std::string, Module> g_cache;
@@ -588,7 +633,8 @@ static Module* get_module(const hhb_params_t* P) {
   g_nv.destroy(&prog);
   CUmodule mod;
   if (g_drv.load(&mod, cubin.data()) != CUDA_SUCCESS || g_drv.get(&m.fwd1, mod, "hh_fwd_v1") != CUDA_SUCCESS ||
-      g_drv.get(&m.fwd4, mod, "hh_fwd_v4") != CUDA_SUCCESS || g_drv.get(&m.bwd, mod, "hh_bwd") != CUDA_SUCCESS) {
+      g_drv.get(&m.fwd4, mod, "hh_fwd_v4") != CUDA_SUCCESS || g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") != CUDA_SUCCESS ||
+      g_drv.get(&m.fwdp4, mod, "hh_fwdp_v4") != CUDA_SUCCESS || g_drv.get(&m.bwd, mod, "hh_bwd") != CUDA_SUCCESS) {
     g_status = "cuModuleLoadData / cuModuleGetFunction failed";
     return nullptr;
   }
@@ -600,7 +646,8 @@ static Module* get_module(const hhb_params_t* P) {
 }  // namespace jit
 
 // Returns true when the JIT kernel was launched (rc holds its status).
-bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, bool vec4, cudaStream_t st, int& rc) {
+bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTab<float>* ptab, bool vec4,
+                 cudaStream_t st, int& rc) {
   jit::Module* m = jit::get_module(P);
   if (!m) return false;
   const int VEC = vec4 ? 4 : 1;
@@ -608,8 +655,10 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, bool vec4, cuda
   const int tpb = fwd_block(threads);
   const int64_t blocks = (threads + tpb - 1) / tpb;
   FwdArgs<float> args = a;
-  void* params[] = {&args};
-  const CUresult r = jit::g_drv.launch(vec4 ? m->fwd4 : m->fwd1, unsigned(blocks), 1, 1, unsigned(tpb), 1, 1, 0,
+  PoissonTab<float> tab = ptab ? *ptab : PoissonTab<float>{};
+  void* params[] = {&args, &tab};
+  CUfunction f = ptab ? (vec4 ? m->fwdp4 : m->fwdp1) : (vec4 ? m->fwd4 : m->fwd1);
+  const CUresult r = jit::g_drv.launch(f, unsigned(blocks), 1, 1, unsigned(tpb), 1, 1, 0,
                                        reinterpret_cast<CUstream>(st), params, nullptr);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit forward launch failed");
   return true;

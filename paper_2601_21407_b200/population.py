@@ -9,8 +9,9 @@ tests/test_gpu_forward.py::test_chunked_simulation_equals_one_shot), each
 chunk's stimulus is produced on the device, and each chunk's trace (V and the
 spike bitmap) is written to a reused buffer the caller can consume.
 
-Launches per chunk: one stimulus kernel (if the stimulus is generated) and
-one hhb_forward.
+Launches per chunk: one hhb_forward_poisson when the stimulus is the
+Poisson drive (drawn in registers inside the forward kernel), otherwise the
+stimulus fill plus one hhb_forward.
 """
 
 from __future__ import annotations
@@ -22,7 +23,7 @@ import torch
 
 from . import _device as D
 from . import _native as nat
-from .dynamics import HHParams, _forward, _raise_if_bad, init_state
+from .dynamics import HHParams, _forward, _raise_if_bad, _table, init_state
 
 
 class PoissonCurrent:
@@ -50,8 +51,12 @@ class Population:
     """
 
     def __init__(self, params: HHParams, n: int, chunk: int = 100, device=None,
-                 record_v: bool = True, record_spikes: bool = True, neuron_base: int = 0):
+                 record_v: bool = True, record_spikes: bool = True, neuron_base: int = 0,
+                 fuse_stimulus: bool = True):
         self.params = params
+        # PoissonCurrent is drawn inside the forward kernel (hhb_forward_poisson)
+        # unless fuse_stimulus=False, which writes it to i_buf first
+        self.fuse_stimulus = bool(fuse_stimulus)
         self.n = int(n)
         self.chunk = int(chunk)
         self.neuron_base = int(neuron_base)
@@ -60,7 +65,7 @@ class Population:
         st = init_state(params, (self.n,), device=dev)
         self.v, self.g = st.v, st.gates
         td = D.torch_dtype(params.dtype)
-        self.i_buf = torch.empty((self.chunk, self.n), dtype=td, device=dev)
+        self.i_buf = None if self.fuse_stimulus else torch.empty((self.chunk, self.n), dtype=td, device=dev)
         self.v_buf = torch.empty((self.chunk, self.n), dtype=td, device=dev) if record_v else None
         words = (self.n + 31) // 32
         self.bits = torch.empty((self.chunk, words), dtype=torch.int32, device=dev) if record_spikes else None
@@ -83,18 +88,34 @@ class Population:
         self.first_bad.fill_(D.INT64_MAX)
         while done < steps:
             tc = min(self.chunk, steps - done)
-            cur = self.i_buf[:tc]
             e0 = e1 = e2 = None
             if events is not None:
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-            self.launches += stimulus.fill(cur, self.t, self.neuron_base)
+            fused = self.fuse_stimulus and isinstance(stimulus, PoissonCurrent)
+            if not fused:
+                if self.i_buf is None:
+                    self.i_buf = torch.empty((self.chunk, self.n), dtype=D.torch_dtype(self.params.dtype),
+                                             device=self.device)
+                cur = self.i_buf[:tc]
+                self.launches += stimulus.fill(cur, self.t, self.neuron_base)
             if events is not None:
                 e1.record()
-            _forward(self.params, self.v, self.g, cur, self.n, 1, tc, v_fin=self.v, g_fin=self.g,
-                     v_out=None if self.v_buf is None else self.v_buf[:tc],
-                     bits=None if self.bits is None else self.bits[:tc],
-                     step_base=self.t, first_bad=self.first_bad, reset_bad=False)
+            v_out = None if self.v_buf is None else self.v_buf[:tc]
+            bits = None if self.bits is None else self.bits[:tc]
+            if fused:
+                words = (self.n + 31) // 32
+                nat.check(nat.load().hhb_forward_poisson(
+                    C.byref(_table(self.params)), D.code(self.params.dtype), self.n, tc,
+                    self.v.data_ptr(), D.ptr(self.g) if self.g.numel() else None, self.n,
+                    self.v.data_ptr(), D.ptr(self.g) if self.g.numel() else None,
+                    stimulus.seed, self.neuron_base, stimulus.lam, stimulus.amp,
+                    D.ptr(v_out), self.n, D.ptr(bits), words, None, 1, self.n,
+                    self.t, self.first_bad.data_ptr(), D.stream()), "hhb_forward_poisson")
+            else:
+                _forward(self.params, self.v, self.g, cur, self.n, 1, tc, v_fin=self.v, g_fin=self.g,
+                         v_out=v_out, bits=bits, step_base=self.t, first_bad=self.first_bad,
+                         reset_bad=False)
             self.launches += 1
             if events is not None:
                 e2.record()

@@ -295,6 +295,28 @@ def test_gate_boundedness_and_rest_stability(cuda):
     assert np.all(np.abs(rest.v_series - p.v_rest) < 1.0) and not rest.spike_series.any()
 
 
+@pytest.mark.parametrize("n", [1000, 148 * 128 + 8])
+def test_fused_poisson_stimulus_matches_separate_generation(cuda, n):
+    """hhb_forward_poisson draws I in registers; it must equal hhb_poisson_current
+    into a buffer followed by hhb_forward, bit for bit, for any chunking."""
+    from paper_2601_21407_b200.population import PoissonCurrent, Population
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    stim = PoissonCurrent(2.0, 2.0, seed=77)
+    a = Population(p, n, chunk=50, device=cuda, neuron_base=12345, fuse_stimulus=True)
+    b = Population(p, n, chunk=37, device=cuda, neuron_base=12345, fuse_stimulus=False)
+    va, vb = [], []
+    a.advance(stim, 150, on_chunk=lambda t, v, s: va.append(v.clone()), check=True)
+    b.advance(stim, 150, on_chunk=lambda t, v, s: vb.append(v.clone()), check=True)
+    assert torch.equal(torch.cat(va), torch.cat(vb))
+    assert torch.equal(a.v, b.v) and torch.equal(a.g, b.g)
+    # the drawn currents have the Poisson(2) moments (x amp 2)
+    buf = torch.empty((200, n), dtype=torch.float32, device=cuda)
+    stim.fill(buf, 0, 0)
+    m = buf.double().mean().item()
+    var = buf.double().var().item()
+    assert abs(m - 4.0) < 0.05 and abs(var - 8.0) < 0.2
+
+
 def test_jit_specialised_kernels_are_active(cuda):
     from paper_2601_21407_b200 import _native as nat
     p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
