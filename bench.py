@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / fwd_bwd / cpu legs")
+    ap.add_argument("--no-fuse", action="store_true", help="stimulus as a separate kernel + HBM buffer")
     return ap.parse_args()
 
 
@@ -252,7 +253,8 @@ def main():
     nat.load()
 
     params = c2_params(np.float32)
-    pop = Population(params, args.neurons, chunk=args.chunk, device=dev, neuron_base=rank * args.neurons)
+    pop = Population(params, args.neurons, chunk=args.chunk, device=dev, neuron_base=rank * args.neurons,
+                     fuse_stimulus=not args.no_fuse)
     stim = PoissonCurrent(2.0, 2.0, seed=1234)
 
     # warm-up: W full passes

@@ -137,6 +137,38 @@ __device__ __forceinline__ T poisson_draw(const PoissonTab<T>& tab, uint32_t wor
   return tab.amp * T(k);
 }
 
+// The same draw through a guide table (Chen & Asau 1974) in shared memory:
+// guide[b] = min{k : cdf[k] >= b/256} <= the answer for every word whose top
+// byte is b (float(word) >= b * 2^24 exactly), so the search starts there and
+// usually stops at once.  Bit-identical to poisson_draw; avoids the warp
+// paying the longest of 32 (x VEC) linear searches.
+template <typename T>
+struct PoissonSmem {
+  int guide[256];
+  T cdf[48];
+  int size;
+  T amp;
+  __device__ void fill(const PoissonTab<T>& tab) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+      const T lo = T(b) * T(0.00390625);
+      int k = 0;
+      while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
+      guide[b] = k;
+    }
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = tab.cdf[k];
+    if (threadIdx.x == 0) {
+      size = tab.size;
+      amp = tab.amp;
+    }
+  }
+  __device__ __forceinline__ T draw(uint32_t word) const {
+    const T u = (T(word) + T(0.5)) * T(2.3283064365386963e-10);
+    int k = guide[word >> 24];
+    while (k < size - 1 && u > cdf[k]) ++k;
+    return amp * T(k);
+  }
+};
+
 // current of VEC consecutive neurons at step t; vector load when dense
 template <typename T, int VEC>
 __device__ __forceinline__ void load_cur(const FwdArgs<T>& a, int64_t t, int64_t n0, bool full,
@@ -175,7 +207,7 @@ __device__ __forceinline__ uint32_t spike_word(const bool (&s)[VEC], int lane) {
 template <typename T, int VEC, bool POIS>
 struct Stimulus {
   uint4 blk[VEC];
-  __device__ __forceinline__ void at(const FwdArgs<T>& a, const PoissonTab<T>& tab, int64_t t, int64_t n0,
+  __device__ __forceinline__ void at(const FwdArgs<T>& a, const PoissonSmem<T>& tab, int64_t t, int64_t n0,
                                      bool full, T (&c)[VEC]) {
     if constexpr (POIS) {
       const int64_t gt = a.step_base + t;
@@ -187,7 +219,7 @@ struct Stimulus {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         const uint32_t w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
-        c[j] = poisson_draw(tab, w);
+        c[j] = tab.draw(w);
       }
     } else {
       load_cur<T, VEC>(a, t, n0, full, c);
@@ -205,6 +237,11 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
   const int64_t n0 = tid * VEC;
   const bool full = n0 + VEC <= a.n;
   Stimulus<T, VEC, POIS> stim;
+  __shared__ PoissonSmem<T> ps;
+  if constexpr (POIS) {
+    ps.fill(ptab);
+    __syncthreads();
+  }
 
   T v[VEC];
   T p[VEC][NGX];
@@ -220,10 +257,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
   int64_t ck_count = 0;
 
   T cur[VEC];
-  if (a.steps > 0) stim.at(a, ptab, 0, n0, full, cur);
+  if (a.steps > 0) stim.at(a, ps, 0, n0, full, cur);
   for (int64_t t = 0; t < a.steps; ++t) {
     T nxt[VEC];
-    if (t + 1 < a.steps) stim.at(a, ptab, t + 1, n0, full, nxt);
+    if (t + 1 < a.steps) stim.at(a, ps, t + 1, n0, full, nxt);
     if (a.ckpt != nullptr && ck_count == 0) {  // state BEFORE step t
       T* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       if (full) {
@@ -492,6 +529,9 @@ __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint6
                                                  int64_t nbase, int64_t tbase,
                                                  const PoissonTab<T> tab, T* out, int64_t ld) {
   // one thread = one neuron x 4 consecutive global steps (one Philox block)
+  __shared__ PoissonSmem<T> ps;
+  ps.fill(tab);
+  __syncthreads();
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t gj = j + nbase;
@@ -505,7 +545,7 @@ __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint6
     for (int q = 0; q < 4; ++q) {
       const int64_t t = gq * 4 + q - tbase;
       if (t < 0 || t >= steps) continue;
-      out[t * ld + j] = poisson_draw(tab, w[q]);
+      out[t * ld + j] = ps.draw(w[q]);
     }
   }
 }

@@ -335,12 +335,29 @@ __device__ __forceinline__ uint4 philox(unsigned long long seed, i64 gj, i64 gq)
   }
   return c;
 }
-__device__ __forceinline__ float poisson_draw(const PoissonTab& tab, u32 word) {
-  const float u = (float(word) + 0.5f) * 2.3283064365386963e-10f;
-  int k = 0;
-  while (k < tab.size - 1 && u > tab.cdf[k]) ++k;
-  return tab.amp * float(k);
-}
+// guide-table inverse CDF in shared memory (hh_kernels.cuh PoissonSmem)
+struct PoissonSmem {
+  int guide[256];
+  float cdf[48];
+  int size;
+  float amp;
+  __device__ void fill(const PoissonTab& tab) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+      const float lo = float(b) * 0.00390625f;
+      int k = 0;
+      while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
+      guide[b] = k;
+    }
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = tab.cdf[k];
+    if (threadIdx.x == 0) { size = tab.size; amp = tab.amp; }
+  }
+  __device__ __forceinline__ float draw(u32 word) const {
+    const float u = (float(word) + 0.5f) * 2.3283064365386963e-10f;
+    int k = guide[word >> 24];
+    while (k < size - 1 && u > cdf[k]) ++k;
+    return amp * float(k);
+  }
+};
 struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
   float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
   i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad; };
@@ -378,7 +395,7 @@ __device__ __forceinline__ void store_vec(float* p, const float (&x)[VEC], bool 
 template <int VEC, bool POIS>
 struct Stimulus {
   uint4 blk[VEC];
-  __device__ __forceinline__ void at(const FwdArgs& a, const PoissonTab& tab, i64 t, i64 n0, bool full,
+  __device__ __forceinline__ void at(const FwdArgs& a, const PoissonSmem& tab, i64 t, i64 n0, bool full,
                                      float (&c)[VEC]) {
     if (POIS) {
       const i64 gt = a.step_base + t;
@@ -390,7 +407,7 @@ struct Stimulus {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         const u32 w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
-        c[j] = poisson_draw(tab, w);
+        c[j] = tab.draw(w);
       }
     } else {
       load_cur<VEC>(a, t, n0, full, c);
@@ -404,6 +421,11 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   const i64 n0 = tid * VEC;
   const bool full = n0 + VEC <= a.n;
   Stimulus<VEC, POIS> stim;
+  __shared__ PoissonSmem ps;
+  if (POIS) {
+    ps.fill(tab);
+    __syncthreads();
+  }
   float v[VEC];
   float p[VEC][NGX];
 #pragma unroll
@@ -415,10 +437,10 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   }
   i64 bad = LLMAX, ck_slot = 0, ck_count = 0;
   float cur[VEC];
-  if (a.steps > 0) stim.at(a, tab, 0, n0, full, cur);
+  if (a.steps > 0) stim.at(a, ps, 0, n0, full, cur);
   for (i64 t = 0; t < a.steps; ++t) {
     float nxt[VEC];
-    if (t + 1 < a.steps) stim.at(a, tab, t + 1, n0, full, nxt);
+    if (t + 1 < a.steps) stim.at(a, ps, t + 1, n0, full, nxt);
     if (a.ckpt != nullptr && ck_count == 0) {
       float* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       store_vec<VEC>(base, v, full, n0, a.n);
