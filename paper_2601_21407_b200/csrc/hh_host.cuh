@@ -305,7 +305,7 @@ struct Flavour {
     const bool pois = ptab != nullptr;                                                           \
     const PoissonTab<T> pt = pois ? *ptab : PoissonTab<T>{};                                     \
     const bool vec_ok =                                                                          \
-        (a.n % (VECW) == 0) &&                                                                   \
+        (a.n % (VECW) == 0) && (!pois || (VECW) != 4 || (a.nbase & 3) == 0) &&                   \
         (pois || ((a.i_sn == 1) && (a.i_st % (VECW) == 0) &&                                     \
                   (reinterpret_cast<uintptr_t>(a.i_ext) % (sizeof(T) * (VECW)) == 0))) &&        \
         (a.v_out == nullptr ||                                                                   \
@@ -383,8 +383,10 @@ struct Flavour {
   int Flavour<T>::poisson(int64_t n, int64_t steps, uint64_t seed, int64_t nbase, int64_t tbase, \
                           double lam, double amp, T* out, int64_t ld, cudaStream_t st) {         \
     if (n <= 0 || steps <= 0) return HHB_OK;                                                     \
-    const int64_t groups = ((tbase + steps - 1) >> 2) - (tbase >> 2) + 1;                        \
-    dim3 grid(unsigned((n + 255) / 256), unsigned(groups < 65535 ? groups : 65535));             \
+    const int64_t bx = ((n + 3) / 4 + 255) / 256;                                                \
+    int64_t by = (int64_t(kNumSMs) * 8 + bx - 1) / bx;                                           \
+    by = by < 1 ? 1 : (by > steps ? steps : (by > 65535 ? 65535 : by));                          \
+    dim3 grid(unsigned(bx), unsigned(by));                                                       \
     k_poisson<T><<<grid, 256, 0, st>>>(n, steps, seed, nbase, tbase, poisson_table<T>(lam, amp),  \
                                        out, ld);                                                 \
     return cuda_check("k_poisson launch");                                                       \

@@ -100,8 +100,8 @@ struct Vec<double, 2> {
 };
 
 // ------------------------------------------------------------ stimulus RNG
-// Philox-4x32-10 (Salmon et al. 2011): counter = (global neuron, global step/4),
-// key = seed; one block of 4 words drives 4 consecutive global steps.
+// Philox-4x32-10 (Salmon et al. 2011): counter = (global neuron / 4, global
+// step), key = seed; word i of a block drives global neuron 4*group + i.
 struct Philox {
   __device__ static uint4 run(uint4 c, uint2 k) {
 #pragma unroll
@@ -114,9 +114,16 @@ struct Philox {
     }
     return c;
   }
-  __device__ static uint4 block(uint64_t seed, int64_t gj, int64_t gq) {
-    return run(make_uint4(uint32_t(gj), uint32_t(uint64_t(gj) >> 32), uint32_t(gq), uint32_t(uint64_t(gq) >> 32)),
+  __device__ static uint4 block(uint64_t seed, int64_t group, int64_t gt) {
+    return run(make_uint4(uint32_t(group), uint32_t(uint64_t(group) >> 32), uint32_t(gt),
+                          uint32_t(uint64_t(gt) >> 32)),
                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+  }
+  // the word of global neuron gj at global step gt
+  __device__ static uint32_t word(uint64_t seed, int64_t gj, int64_t gt) {
+    const uint4 r = block(seed, gj >> 2, gt);
+    const int i = int(gj & 3);
+    return i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w;
   }
 };
 
@@ -155,16 +162,23 @@ struct PoissonSmem {
       while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
       guide[b] = k;
     }
-    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = tab.cdf[k];
+    // entries from size-1 on are raised to 2 (> any u): the search then stops at
+    // size-1 by itself, exactly where the capped linear search stops
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : T(2);
     if (threadIdx.x == 0) {
       size = tab.size;
       amp = tab.amp;
     }
   }
+  // Call from warp-converged code: the rare tail walk is a warp-uniform branch.
   __device__ __forceinline__ T draw(uint32_t word) const {
     const T u = (T(word) + T(0.5)) * T(2.3283064365386963e-10);
     int k = guide[word >> 24];
-    while (k < size - 1 && u > cdf[k]) ++k;
+    k += int(u > cdf[k]);
+    k += int(u > cdf[k]);
+    if (__any_sync(0xffffffffu, u > cdf[k])) {
+      while (u > cdf[k]) ++k;
+    }
     return amp * T(k);
   }
 };
@@ -202,24 +216,25 @@ __device__ __forceinline__ uint32_t spike_word(const bool (&s)[VEC], int lane) {
 
 // Per-thread source of the injected current: the i_ext array (load, with the
 // next step prefetched by the caller) or, for POIS, the Poisson stimulus drawn
-// in registers from the Philox block of (global neuron, global step / 4) --
-// the exact stream k_poisson writes, without its HBM round trip.
+// in registers from the Philox block of (global neuron / 4, global step) --
+// the exact stream k_poisson writes, without its HBM round trip.  VEC == 4
+// needs (nbase + n0) % 4 == 0 (the host checks nbase % 4) and then uses one
+// block per thread and step.
 template <typename T, int VEC, bool POIS>
 struct Stimulus {
-  uint4 blk[VEC];
   __device__ __forceinline__ void at(const FwdArgs<T>& a, const PoissonSmem<T>& tab, int64_t t, int64_t n0,
                                      bool full, T (&c)[VEC]) {
     if constexpr (POIS) {
       const int64_t gt = a.step_base + t;
-      const int q = int(gt & 3);
-      if (q == 0 || t == 0) {
+      if constexpr (VEC == 4) {
+        const uint4 r = Philox::block(a.seed, (a.nbase + n0) >> 2, gt);
+        c[0] = tab.draw(r.x);
+        c[1] = tab.draw(r.y);
+        c[2] = tab.draw(r.z);
+        c[3] = tab.draw(r.w);
+      } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) blk[j] = Philox::block(a.seed, a.nbase + n0 + j, gt >> 2);
-      }
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        const uint32_t w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
-        c[j] = tab.draw(w);
+        for (int j = 0; j < VEC; ++j) c[j] = tab.draw(Philox::word(a.seed, a.nbase + n0 + j, gt));
       }
     } else {
       load_cur<T, VEC>(a, t, n0, full, c);
@@ -528,24 +543,40 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint64_t seed,
                                                  int64_t nbase, int64_t tbase,
                                                  const PoissonTab<T> tab, T* out, int64_t ld) {
-  // one thread = one neuron x 4 consecutive global steps (one Philox block)
+  // one thread = 4 consecutive neurons (one Philox block per step when the
+  // global ids are 4-aligned), steps strided over gridDim.y; no early exit:
+  // draw() votes across the warp
   __shared__ PoissonSmem<T> ps;
   ps.fill(tab);
   __syncthreads();
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const int64_t gj = j + nbase;
-  const int64_t g_first = tbase >> 2, g_last = (tbase + steps - 1) >> 2;
-  for (int64_t gq = g_first + int64_t(blockIdx.y); gq <= g_last; gq += gridDim.y) {
-    const uint4 r = Philox::run(make_uint4(uint32_t(gj), uint32_t(uint64_t(gj) >> 32), uint32_t(gq),
-                                           uint32_t(uint64_t(gq) >> 32)),
-                                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
-    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  const int64_t j0 = 4 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  const bool aligned = (nbase & 3) == 0;
+  const bool vec = aligned && j0 + 4 <= n && (ld & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out) % (4 * sizeof(T))) == 0;
+  for (int64_t t = blockIdx.y; t < steps; t += gridDim.y) {
+    T c[4];
+    if (aligned) {
+      const uint4 r = Philox::block(seed, (nbase + j0) >> 2, tbase + t);
+      c[0] = ps.draw(r.x);
+      c[1] = ps.draw(r.y);
+      c[2] = ps.draw(r.z);
+      c[3] = ps.draw(r.w);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t t = gq * 4 + q - tbase;
-      if (t < 0 || t >= steps) continue;
-      out[t * ld + j] = ps.draw(w[q]);
+      for (int q = 0; q < 4; ++q) c[q] = ps.draw(Philox::word(seed, nbase + j0 + q, tbase + t));
+    }
+    T* row = out + t * ld + j0;
+    if (vec) {
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(row) = make_float4(c[0], c[1], c[2], c[3]);
+      } else {
+        reinterpret_cast<double2*>(row)[0] = make_double2(c[0], c[1]);
+        reinterpret_cast<double2*>(row)[1] = make_double2(c[2], c[3]);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j0 + q < n) row[q] = c[q];
     }
   }
 }

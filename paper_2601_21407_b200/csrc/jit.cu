@@ -348,13 +348,17 @@ struct PoissonSmem {
       while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
       guide[b] = k;
     }
-    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = tab.cdf[k];
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
     if (threadIdx.x == 0) { size = tab.size; amp = tab.amp; }
   }
   __device__ __forceinline__ float draw(u32 word) const {
     const float u = (float(word) + 0.5f) * 2.3283064365386963e-10f;
     int k = guide[word >> 24];
-    while (k < size - 1 && u > cdf[k]) ++k;
+    k += int(u > cdf[k]);
+    k += int(u > cdf[k]);
+    if (__any_sync(0xffffffffu, u > cdf[k])) {
+      while (u > cdf[k]) ++k;
+    }
     return amp * float(k);
   }
 };
@@ -394,20 +398,23 @@ __device__ __forceinline__ void store_vec(float* p, const float (&x)[VEC], bool 
 }
 template <int VEC, bool POIS>
 struct Stimulus {
-  uint4 blk[VEC];
   __device__ __forceinline__ void at(const FwdArgs& a, const PoissonSmem& tab, i64 t, i64 n0, bool full,
                                      float (&c)[VEC]) {
     if (POIS) {
       const i64 gt = a.step_base + t;
-      const int q = int(gt & 3);
-      if (q == 0 || t == 0) {
+      if (VEC == 4) {  // host guarantees (nbase + n0) % 4 == 0
+        const uint4 r = philox(a.seed, (a.nbase + n0) >> 2, gt);
+        const u32 w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) blk[j] = philox(a.seed, a.nbase + n0 + j, gt >> 2);
-      }
+        for (int j = 0; j < VEC; ++j) c[j] = tab.draw(w[j]);
+      } else {
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        const u32 w = q == 0 ? blk[j].x : q == 1 ? blk[j].y : q == 2 ? blk[j].z : blk[j].w;
-        c[j] = tab.draw(w);
+        for (int j = 0; j < VEC; ++j) {
+          const i64 gj = a.nbase + n0 + j;
+          const uint4 r = philox(a.seed, gj >> 2, gt);
+          const int i = int(gj & 3);
+          c[j] = tab.draw(i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w);
+        }
       }
     } else {
       load_cur<VEC>(a, t, n0, full, c);
@@ -488,10 +495,10 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   }
   if (bad != LLMAX) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
 }
-extern "C" __global__ void __launch_bounds__(256) hh_fwd_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, false>(a, t); }
-extern "C" __global__ void __launch_bounds__(256) hh_fwd_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, false>(a, t); }
-extern "C" __global__ void __launch_bounds__(256) hh_fwdp_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, true>(a, t); }
-extern "C" __global__ void __launch_bounds__(256) hh_fwdp_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, true>(a, t); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, false>(a, t); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, false>(a, t); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, true>(a, t); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, true>(a, t); }
 
 __device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
   v = base[i];
@@ -578,6 +585,9 @@ static std::string generate(const hhb_params_t* P) {
   src += fmt("#define NG %d\n#define NGX %d\n#define SLOTS %d\n#define BWD_THREADS %d\n", L.ng,
              L.ng > 0 ? L.ng : 1, kSlots, kBwdThreads);
   src += fmt("#define THETA %s\n", F(P->v_theta).c_str());
+  // occupancy knob for experiments: minimum resident 256-thread blocks per SM
+  const char* mb = getenv("HHB_JIT_MINB");
+  src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 1);
   src += emit_forward_step(P, L);
   src += emit_backward_step(P, L);
   src += kForwardBody;
@@ -609,6 +619,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   for (int c = 0; c < P->n_channels; ++c) Q.channels[c] = P->channels[c];
   std::string k(reinterpret_cast<const char*>(&Q), sizeof Q);
   k += std::to_string(dev);
+  const char* mb = getenv("HHB_JIT_MINB");
+  k += mb ? mb : "";
   return k;
 }
 
