@@ -386,7 +386,7 @@ struct Flavour {
     const int64_t bx = ((n + 3) / 4 + 255) / 256;                                                \
     int64_t by = (int64_t(kNumSMs) * 8 + bx - 1) / bx;                                           \
     by = by < 1 ? 1 : (by > steps ? steps : (by > 65535 ? 65535 : by));                          \
-    dim3 grid(unsigned(bx), unsigned(by));                                                       \
+    const dim3 grid{unsigned(bx), unsigned(by), 1u};                                             \
     k_poisson<T><<<grid, 256, 0, st>>>(n, steps, seed, nbase, tbase, poisson_table<T>(lam, amp),  \
                                        out, ld);                                                 \
     return cuda_check("k_poisson launch");                                                       \

@@ -30,6 +30,15 @@ def _declared():
     return sorted(set(re.findall(r"\b(hhb_[a-z0-9_]+)\s*\(", txt)))
 
 
+def test_library_is_newer_than_its_sources():
+    """A stale libhhb200.so would silently test old kernels."""
+    lib_t = os.path.getmtime(nat.LIB_PATH)
+    csrc = os.path.join(ROOT, "paper_2601_21407_b200", "csrc")
+    srcs = [os.path.join(csrc, f) for f in os.listdir(csrc)] + [HEADER]
+    stale = [s for s in srcs if os.path.getmtime(s) > lib_t]
+    assert not stale, f"rebuild: python -m paper_2601_21407_b200._build ({stale})"
+
+
 def test_library_exports_every_declared_symbol():
     lib = nat.load()
     names = _declared()
