@@ -587,7 +587,9 @@ static std::string generate(const hhb_params_t* P) {
   src += fmt("#define THETA %s\n", F(P->v_theta).c_str());
   // occupancy knob for experiments: minimum resident 256-thread blocks per SM
   const char* mb = getenv("HHB_JIT_MINB");
-  src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 1);
+  // 4 resident 256-thread blocks (<= 64 registers) measured best for config 2
+  // on B200 (profiles/r1_variants.md); 1 lets ptxas take ~100+ registers
+  src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 4);
   src += emit_forward_step(P, L);
   src += emit_backward_step(P, L);
   src += kForwardBody;
