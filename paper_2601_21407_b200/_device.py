@@ -59,7 +59,11 @@ def to_dev(x, dtype, dev=None) -> torch.Tensor:
 
 
 def to_host(t: torch.Tensor, dtype=None) -> np.ndarray:
-    a = t.detach().cpu().numpy()
+    """Device tensor -> numpy; a dtype change is done on the device first."""
+    t = t.detach()
+    if dtype is not None and np.dtype(dtype) in _NP_TO_TORCH and t.dtype != _NP_TO_TORCH[np.dtype(dtype)]:
+        t = t.to(_NP_TO_TORCH[np.dtype(dtype)])
+    a = t.cpu().numpy()
     return a if dtype is None else a.astype(dtype, copy=False)
 
 

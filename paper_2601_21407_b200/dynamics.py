@@ -565,9 +565,11 @@ def simulate(params, i_series, state0: NeuronState | None = None, record_state: 
         tr = Trace(empty_v, empty_s, params.dt)
         return (tr, state0) if record_state else tr
     dev = D.require_cuda()
-    cur = D.to_dev(i_series, dtype, dev).reshape(T, n)
     v = D.to_dev(state0.v, dtype, dev).reshape(n)
     g = D.to_dev(state0.gates, dtype, dev).reshape(ng, n)
+    if not on_dev and T * n >= _PIPELINE_MIN_ELEMS:
+        return _simulate_pipelined(params, np.asarray(i_series).reshape(T, n), v, g, T, shape, record_state)
+    cur = D.to_dev(i_series, dtype, dev).reshape(T, n)
     v_out = torch.empty((T, n), dtype=cur.dtype, device=dev)
     bits = torch.empty((T, (n + 31) // 32), dtype=torch.int32, device=dev)
     v_fin, g_fin, bad = _forward(params, v, g, cur, n, 1, T, v_out=v_out, bits=bits)
@@ -582,6 +584,32 @@ def simulate(params, i_series, state0: NeuronState | None = None, record_state: 
         fin = NeuronState(D.to_host(v_fin).reshape(shape), D.to_host(g_fin).reshape((ng,) + shape))
     if record_state:
         return tr, fin
+    return tr
+
+
+_PIPELINE_MIN_ELEMS = 1 << 22
+
+
+def _simulate_pipelined(params, i2, v, g, T, shape, record_state):
+    """numpy-in/numpy-out simulate for large calls: time chunks with host
+    copy, H2D, kernel and D2H overlapped (see _pipeline.py)."""
+    from . import _pipeline
+    n = v.numel()
+    ng = g.shape[0]
+    first_bad = torch.full((1,), D.INT64_MAX, dtype=torch.int64, device=v.device)
+
+    def fwd(cur, tc, v_out, bits, t0):
+        _forward(params, v, g, cur, n, 1, tc, v_fin=v, g_fin=g, v_out=v_out, bits=bits, step_base=t0,
+                 first_bad=first_bad, reset_bad=False)
+
+    def unpack(bits, tc, nn, out):
+        _unpack(bits, tc, nn, out)
+
+    vs, ss = _pipeline.simulate_host(params, i2, v, g, fwd, unpack)
+    _raise_if_bad(first_bad)
+    tr = Trace(vs.reshape((T,) + shape), ss.reshape((T,) + shape), params.dt)
+    if record_state:
+        return tr, NeuronState(D.to_host(v).reshape(shape), D.to_host(g).reshape((ng,) + shape))
     return tr
 
 

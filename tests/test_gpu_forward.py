@@ -317,6 +317,30 @@ def test_fused_poisson_stimulus_matches_separate_generation(cuda, n):
     assert abs(m - 4.0) < 0.05 and abs(var - 8.0) < 0.2
 
 
+@pytest.mark.parametrize("chunk_bytes", [1 << 20, 256 << 20])
+def test_pipelined_host_path_equals_device_path(cuda, chunk_bytes, monkeypatch):
+    """numpy in/out simulate of a large call runs the chunked copy/compute
+    pipeline; it must return exactly the device path's trace (float64 V)."""
+    from paper_2601_21407_b200 import _pipeline
+    monkeypatch.setattr(_pipeline, "CHUNK_BYTES", chunk_bytes)
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    rng = np.random.default_rng(12)
+    i = (2.0 * rng.poisson(2.0, size=(301, 20000))).astype(np.float32)
+    i[:, 7] += 40.0
+    tr_h, fin_h = Dy.simulate(p, i, record_state=True)
+    tr_d, fin_d = Dy.simulate(p, torch.from_numpy(i).to(cuda), record_state=True)
+    assert tr_h.v_series.dtype == np.float64 and tr_h.spike_series.dtype == bool
+    assert np.array_equal(tr_h.v_series, tr_d.v_series.double().cpu().numpy())
+    assert np.array_equal(tr_h.spike_series, tr_d.spike_series.cpu().numpy())
+    assert tr_h.spike_series.any()
+    assert np.array_equal(fin_h.v, fin_d.v.cpu().numpy())
+    bad = i.copy()
+    bad[150, 3] = np.inf
+    with pytest.raises(NumericalOverflowError) as e:
+        Dy.simulate(p, bad)
+    assert e.value.step_index == 150
+
+
 def test_jit_specialised_kernels_are_active(cuda):
     from paper_2601_21407_b200 import _native as nat
     p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
