@@ -129,4 +129,9 @@ def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forw
             stage_and_load(k + 1)               # host copy overlaps the kernel
     d2h.synchronize()
     compute.synchronize()
+    if TRACE:
+        print(f"[pipeline] T={T} n={n} chunks={len(chunks)} x {tc_max} steps", flush=True)
     return out_v, out_s
+
+
+TRACE = bool(int(os.environ.get("HHB_PIPE_TRACE", "0")))

@@ -554,7 +554,9 @@ def simulate(params, i_series, state0: NeuronState | None = None, record_state: 
     n = int(np.prod(shape, dtype=np.int64))
     ng = params.n_gates
     if state0 is None:
-        state0 = init_state(params, shape, device=D.require_cuda() if on_dev else None)
+        # built on the device even for numpy calls: only the final state, if
+        # requested, travels back to the host
+        state0 = init_state(params, shape, device=D.require_cuda() if (on_dev or T > 0) else None)
     elif tuple(state0.v.shape) != shape and T > 0:
         raise UsageError(f"state shape {tuple(state0.v.shape)} does not match input shape {shape}")
     if T == 0:
