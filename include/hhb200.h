@@ -209,6 +209,29 @@ int hhb_poisson_current(int32_t dtype, int64_t n, int64_t n_steps, uint64_t seed
                         int64_t neuron_base, int64_t step_base, double lam, double amp,
                         void* out, int64_t ld, void* stream);
 
+/* ---- dense synaptic projection (tcgen05) ---------------------------------- */
+
+enum hhb_gemm_in { HHB_GEMM_BF16 = 0, HHB_GEMM_TF32 = 1 };
+
+/* D[M][ldd] (fp32) = A[M][K] . B[N][K]^T (+ bias[N]) on the 5th-gen tensor
+ * cores (tcgen05.mma, fp32 accumulation in TMEM, TMA-fed 128B-swizzled smem).
+ * Replaces DenseLayer.__call__ (learn.py:210-211) and the gradient einsum
+ * (learn.py:272) of the HH readout/SNN layer.  A and B are K-major (row
+ * pitch lda/ldb elements, 16-byte aligned): bf16 for HHB_GEMM_BF16, fp32
+ * read as tf32 for HHB_GEMM_TF32.  splits > 1 splits K over CTAs into fp32
+ * partial slices (workspace: hhb_gemm_workspace floats) summed in a fixed
+ * order -- deterministic. */
+int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+             const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
+             int32_t splits, float* workspace, void* stream);
+int64_t hhb_gemm_workspace(int64_t M, int64_t N, int32_t splits);
+/* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16 */
+int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int64_t lds,
+                  void* dst, int64_t ldd, void* stream);
+int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream);
+/* out[c] += sum_r src[r][c] in row order (bias gradient, learn.py:273) */
+int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, void* stream);
+
 /* ---- runtime specialisation ----------------------------------------------- */
 
 /* The float (HHB_F32) forward/backward kernels are generated per parameter

@@ -91,6 +91,11 @@ SIGNATURES = {
     "hhb_poisson_current": (_i32, [_i32, _i64, _i64, C.c_uint64, _i64, _i64, _dbl, _dbl,
                                    _vp, _i64, _vp]),
     "hhb_pipe_probe": (_i32, [_i32, _i64, _vp, C.POINTER(C.c_int64), _vp]),
+    "hhb_gemm": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "hhb_gemm_workspace": (_i64, [_i64, _i64, _i32]),
+    "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
+    "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }

@@ -1,0 +1,432 @@
+// proj_gemm.cu -- dense synaptic projection of the HH SNN layer on the 5th-gen
+// tensor cores (DenseLayer learn.py:203-216, its gradient
+// learn.py:264-274).
+//
+//   D[M][N] (fp32) = A[M][K] . B[N][K]^T (+ bias[N])      both operands K-major
+//
+// Forward  I = X W^T + b          : A = X  [T*B][K_in],   B = W   [N_out][K_in]
+// dX       = dI W                 : A = dI [T*B][N_out],  B = W^T [K_in][N_out]
+// dW       = dI^T X               : A = dI^T [N_out][T*B], B = X^T [K_in][T*B]
+// (the transposes are produced by hhb_transpose; fp32 operands use kind::tf32).
+//
+// One CTA computes a 128 x BN tile: warp 0 (one lane) streams A/B k-blocks
+// with TMA into a 4-stage ring of 128B-swizzled smem tiles, warp 1 (one lane)
+// issues tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) into a TMEM
+// accumulator and releases smem stages with tcgen05.commit, warps 2-5 drain
+// TMEM with tcgen05.ld (32 lanes x 32 columns each) and store fp32 rows.
+// Split-K writes fp32 partial slices that hhb_gemm_reduce sums in a fixed
+// order (deterministic).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "hh_host.cuh"
+
+namespace hhb {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int STAGES = 4;
+constexpr int kThreads = 192;
+
+struct Args {
+  int64_t M, N, K;
+  float* D;
+  int64_t ldd;
+  const float* bias;
+  int64_t split_stride;  // floats between split slices of D (0 when splits == 1)
+  int kb_per_split;
+  int kb_total;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x,
+                                            int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// K-major operand tile with 128B swizzle (TMA SWIZZLE_128B layout): rows of
+// 128 B, 8-row atoms of 1024 B -> SBO = 1024 B, LBO unused (1), version 1.
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  const uint32_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= uint64_t((a & 0x3FFFF) >> 4);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+template <bool TF32>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                     uint32_t accumulate) {
+  if constexpr (TF32) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN, bool TF32>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_umma_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Args args) {
+  constexpr uint32_t kStageA = BM * 128;
+  constexpr uint32_t kStageB = BN * 128;
+  constexpr int kUmmaK = TF32 ? 8 : 16;                // elements per MMA
+  constexpr int kBK = TF32 ? 32 : 64;                  // elements per 128 B row
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kStageB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int kb0 = blockIdx.z * args.kb_per_split;
+  const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+  const int nkb = max(0, kb1 - kb0);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(uint32_t(BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kStageA + kStageB);
+        const int32_t kx = (kb0 + i) * kBK;
+        tma_load_2d(&ta, &full[s], sA + s * kStageA, kx, int32_t(m0));
+        tma_load_2d(&tb, &full[s], sB + s * kStageB, kx, int32_t(n0));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < kBK / kUmmaK; ++k) {
+          const uint64_t ad = smem_desc(sA + s * kStageA + k * 32);
+          const uint64_t bd = smem_desc(sB + s * kStageB + k * 32);
+          umma<TF32>(tmem, ad, bd, args.idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    const int64_t row = m0 + q * 32 + lane;
+    float* drow = args.D + int64_t(blockIdx.z) * args.split_stride + row * args.ldd;
+    const bool add_bias = args.bias != nullptr && args.split_stride == 0;
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      if (nkb > 0) {
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), r);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      }
+      if (row < args.M) {
+        const int64_t cb = n0 + c0;
+        const bool vec = (cb + 32 <= args.N) && ((args.ldd & 3) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(drow) & 15) == 0);
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 o;
+            o.x = __uint_as_float(r[j + 0]) + (add_bias ? __ldg(args.bias + cb + j + 0) : 0.f);
+            o.y = __uint_as_float(r[j + 1]) + (add_bias ? __ldg(args.bias + cb + j + 1) : 0.f);
+            o.z = __uint_as_float(r[j + 2]) + (add_bias ? __ldg(args.bias + cb + j + 2) : 0.f);
+            o.w = __uint_as_float(r[j + 3]) + (add_bias ? __ldg(args.bias + cb + j + 3) : 0.f);
+            *reinterpret_cast<float4*>(drow + cb + j) = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cb + j < args.N)
+              drow[cb + j] = __uint_as_float(r[j]) + (add_bias ? __ldg(args.bias + cb + j) : 0.f);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(BN)));
+  }
+}
+
+// fixed-order split-K reduction (+ bias)
+__global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits, int64_t split_stride,
+                              const float* bias, float* D, int64_t ldd) {
+  const int64_t total = M * N;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = i / N, n = i % N;
+    float acc = 0.f;
+    for (int z = 0; z < splits; ++z) acc += ws[z * split_stride + m * N + n];
+    D[m * ldd + n] = acc + (bias ? bias[n] : 0.f);
+  }
+}
+
+// tiled transpose (fp32 or bf16): dst[c][r] = src[r][c]; optional fp32 -> bf16
+template <typename S, typename Dt>
+__global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t lds, Dt* dst, int64_t ldd) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? float(src[r * lds + c]) : 0.f;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[c * ldd + r] = Dt(tile[threadIdx.x][k]);
+  }
+}
+
+__global__ void k_cast_bf16(int64_t n, const float* src, __nv_bfloat16* dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// deterministic column sums of a [rows][cols] fp32 matrix (bias gradient,
+// learn.py:273): one thread per column walks the rows in order
+__global__ void k_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double acc = 0.0;
+  for (int64_t r = 0; r < rows; ++r) acc += double(src[r * ld + c]);
+  out[c] += acc;
+}
+
+// ------------------------------------------------------------ host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, bool tf32, const void* base, int64_t rows, int64_t k, int64_t ld,
+                    int box_rows) {
+  EncodeFn enc = encoder();
+  if (!enc) return fail(HHB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const int eb = tf32 ? 4 : 2;
+  const cuuint64_t dims[2] = {cuuint64_t(k), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * eb};
+  const cuuint32_t box[2] = {cuuint32_t(128 / eb), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HHB_EINVAL, "cuTensorMapEncodeTiled rejected the operand layout");
+  return HHB_OK;
+}
+
+template <int BN, bool TF32>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Args& a, int splits, cudaStream_t st) {
+  const size_t smem = 1024 + size_t(STAGES) * (BM * 128 + BN * 128) + 256;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_umma_gemm<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  });
+  if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
+  const dim3 grid{unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(splits)};
+  k_umma_gemm<BN, TF32><<<grid, kThreads, smem, st>>>(ta, tb, a);
+  return cuda_check("k_umma_gemm launch");
+}
+
+static uint32_t instr_desc(bool tf32, int bn) {
+  const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+}  // namespace gemm
+}  // namespace hhb
+
+using namespace hhb;
+
+extern "C" {
+
+int64_t hhb_gemm_workspace(int64_t M, int64_t N, int32_t splits) { return splits > 1 ? int64_t(splits) * M * N : 0; }
+
+int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+             int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
+             void* stream) {
+  using namespace hhb::gemm;
+  const bool tf32 = in_kind == HHB_GEMM_TF32;
+  if (in_kind != HHB_GEMM_BF16 && in_kind != HHB_GEMM_TF32) return fail(HHB_EINVAL, "in_kind");
+  if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
+  if (M == 0 || N == 0) return HHB_OK;
+  const int eb = tf32 ? 4 : 2;
+  if ((lda * eb) % 16 || (ldb * eb) % 16 || reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
+    return fail(HHB_EINVAL, "gemm operands need 16-byte aligned base and row pitch");
+  if (lda < K || ldb < K) return fail(HHB_EINVAL, "lda/ldb < K");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int bk = 128 / eb;
+  const int kb_total = int((K + bk - 1) / bk);
+  if (splits < 1) splits = 1;
+  if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
+  if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  CUtensorMap ta, tb;
+  int rc = make_map(&ta, tf32, A, M, K, lda, BM);
+  if (rc) return rc;
+  if ((rc = make_map(&tb, tf32, B, N, K, ldb, bn))) return rc;
+  Args a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.kb_total = kb_total;
+  a.kb_per_split = (kb_total + splits - 1) / splits;
+  a.idesc = instr_desc(tf32, bn);
+  if (splits > 1) {
+    a.D = workspace;
+    a.ldd = N;
+    a.split_stride = M * N;
+    a.bias = nullptr;
+  } else {
+    a.D = D;
+    a.ldd = ldd;
+    a.split_stride = 0;
+    a.bias = bias;
+  }
+  if (bn == 64) rc = tf32 ? launch<64, true>(ta, tb, a, splits, st) : launch<64, false>(ta, tb, a, splits, st);
+  else if (bn == 128) rc = tf32 ? launch<128, true>(ta, tb, a, splits, st) : launch<128, false>(ta, tb, a, splits, st);
+  else rc = tf32 ? launch<256, true>(ta, tb, a, splits, st) : launch<256, false>(ta, tb, a, splits, st);
+  if (rc || splits == 1) return rc;
+  k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+  return cuda_check("k_gemm_reduce launch");
+}
+
+int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int64_t lds, void* dst, int64_t ldd,
+                  void* stream) {
+  if (rows <= 0 || cols <= 0) return HHB_OK;
+  const dim3 grid{unsigned((cols + 31) / 32), unsigned((rows + 31) / 32), 1u};
+  const dim3 block{32u, 8u, 1u};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (kind == 0)
+    hhb::gemm::k_transpose<float, float><<<grid, block, 0, st>>>(rows, cols, static_cast<const float*>(src), lds,
+                                                                 static_cast<float*>(dst), ldd);
+  else if (kind == 1)
+    hhb::gemm::k_transpose<float, __nv_bfloat16><<<grid, block, 0, st>>>(
+        rows, cols, static_cast<const float*>(src), lds, static_cast<__nv_bfloat16*>(dst), ldd);
+  else if (kind == 2)
+    hhb::gemm::k_transpose<__nv_bfloat16, __nv_bfloat16><<<grid, block, 0, st>>>(
+        rows, cols, static_cast<const __nv_bfloat16*>(src), lds, static_cast<__nv_bfloat16*>(dst), ldd);
+  else
+    return fail(HHB_EINVAL, "transpose kind");
+  return cuda_check("k_transpose launch");
+}
+
+int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {
+  if (n <= 0) return HHB_OK;
+  hhb::gemm::k_cast_bf16<<<grid_1d(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n, src, static_cast<__nv_bfloat16*>(dst));
+  return cuda_check("k_cast_bf16 launch");
+}
+
+int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, void* stream) {
+  if (rows <= 0 || cols <= 0) return HHB_OK;
+  hhb::gemm::k_col_sum<<<unsigned((cols + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(rows, cols, src,
+                                                                                                      ld, out);
+  return cuda_check("k_col_sum launch");
+}
+
+}  // extern "C"

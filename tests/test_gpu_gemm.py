@@ -1,0 +1,94 @@
+"""GPU tests of the tcgen05 projection GEMM (hhb_gemm) against fp64 references
+on the same (bf16- / tf32-rounded) operands: D = A B^T + bias."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2601_21407_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+
+def gemm(A, B, bias=None, splits=1, kind=0):
+    M, K = A.shape
+    N = B.shape[0]
+    D = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    lib = nat.load()
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
+    ws = torch.empty(max(1, ws_n), dtype=torch.float32, device=A.device)
+    rc = lib.hhb_gemm(kind, M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                      None if bias is None else bias.data_ptr(), D.data_ptr(), N, splits, ws.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+    nat.check(rc, "hhb_gemm")
+    return D
+
+
+def tf32_round(x):
+    """Round-to-nearest tf32 (10-bit mantissa) of an fp32 tensor, as float64."""
+    b = x.contiguous().view(torch.int32).to(torch.int64)
+    b = (b + 0x1000) & ~0x1FFF
+    return b.to(torch.int32).view(torch.float32).double()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (1000, 200, 100), (25600, 1024, 784), (257, 10, 2048),
+                                   (300, 2048, 2048)])
+def test_bf16_gemm_matches_reference(cuda, M, N, K):
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    A = torch.randn((M, K), device=cuda, generator=g).to(torch.bfloat16)
+    B = torch.randn((N, K), device=cuda, generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device=cuda, generator=g)
+    D = gemm(A, B, bias)
+    ref = A.double() @ B.double().T + bias.double()
+    err = (D.double() - ref).norm() / ref.norm()
+    assert err < 1e-6, float(err)
+    assert torch.isfinite(D).all()
+
+
+def test_bf16_gemm_without_bias_and_tail_rows(cuda):
+    A = torch.randn((77, 96), device=cuda).to(torch.bfloat16)
+    B = torch.randn((33, 96), device=cuda).to(torch.bfloat16)
+    D = gemm(A, B)
+    ref = A.double() @ B.double().T
+    assert ((D.double() - ref).abs().max() / ref.abs().max()) < 1e-6
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(1024, 784, 25600, 8), (10, 2048, 25600, 16), (256, 256, 512, 1)])
+def test_tf32_split_k_gemm_is_deterministic(cuda, M, N, K, splits):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    A = torch.randn((M, K), device=cuda, generator=g)
+    B = torch.randn((N, K), device=cuda, generator=g)
+    D1 = gemm(A, B, splits=splits, kind=1)
+    D2 = gemm(A, B, splits=splits, kind=1)
+    assert torch.equal(D1, D2)
+    ref_t = tf32_round(A) @ tf32_round(B).T        # tensor cores round fp32 -> tf32
+    ref_x = A.double() @ B.double().T
+    err_t = float((D1.double() - ref_t).norm() / ref_t.norm())
+    err_x = float((D1.double() - ref_x).norm() / ref_x.norm())
+    # either rounding or truncation of the operands to tf32; both within 1e-3 of exact
+    assert min(err_t, err_x) < 1e-3, (err_t, err_x)
+    Ds = gemm(A, B, splits=1, kind=1)
+    assert float((Ds - D1).norm() / D1.norm()) < 1e-5
+
+
+def test_transpose_cast_colsum(cuda):
+    lib = nat.load()
+    x = torch.randn((333, 129), device=cuda)
+    t = torch.empty((129, 333), device=cuda)
+    nat.check(lib.hhb_transpose(0, 333, 129, x.data_ptr(), 129, t.data_ptr(), 333, None), "t")
+    torch.cuda.synchronize()
+    assert torch.equal(t, x.T.contiguous())
+    tb = torch.empty((129, 333), dtype=torch.bfloat16, device=cuda)
+    nat.check(lib.hhb_transpose(1, 333, 129, x.data_ptr(), 129, tb.data_ptr(), 333, None), "t")
+    torch.cuda.synchronize()
+    assert torch.equal(tb, x.T.contiguous().to(torch.bfloat16))
+    cb = torch.empty_like(x, dtype=torch.bfloat16)
+    nat.check(lib.hhb_cast_bf16(x.numel(), x.data_ptr(), cb.data_ptr(), None), "c")
+    torch.cuda.synchronize()
+    assert torch.equal(cb, x.to(torch.bfloat16))
+    s = torch.zeros(129, dtype=torch.float64, device=cuda)
+    nat.check(lib.hhb_col_sum(333, 129, x.data_ptr(), 129, s.data_ptr(), None), "s")
+    torch.cuda.synchronize()
+    assert torch.allclose(s, x.double().sum(0), rtol=1e-12, atol=1e-9)
