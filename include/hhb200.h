@@ -225,9 +225,16 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
              const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
              int32_t splits, float* workspace, void* stream);
 int64_t hhb_gemm_workspace(int64_t M, int64_t N, int32_t splits);
-/* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16 */
+/* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16,
+ * 3: fp32 -> bf16 hi at [c][r] and lo = x - hi at [c][rows + r] (bf16x2 split),
+ * 4: bf16 -> bf16 written to [c][r] and [c][rows + r].  Kinds 3 + 4 turn a
+ * product with one fp32 operand into one bf16 GEMM with K doubled whose
+ * result carries ~16 mantissa bits of that operand. */
 int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int64_t lds,
                   void* dst, int64_t ldd, void* stream);
+/* row-wise bf16x2 split: dst[r][c] = hi(src[r][c]), dst[r][cols + c] = lo */
+int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst,
+                        int64_t ldd, void* stream);
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream);
 /* out[c] += sum_r src[r][c] in row order (bias gradient, learn.py:273) */
 int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, void* stream);

