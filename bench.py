@@ -210,31 +210,98 @@ def e2e_leg(torch, args, params, rank):
 
 
 def fwd_bwd_leg(torch, dev):
-    """Forward + BPTT (backward_through_time, full storage) on the config-3
-    shaped HH layer: RS neurons, 256 x 1024, 100 steps, fp32, device tensors."""
-    import numpy as np
-    from paper_2601_21407_b200 import adjoint as A
-    from paper_2601_21407_b200 import defaults as DF
-    from paper_2601_21407_b200 import dynamics as Dy
-    p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
-    B, N, T = 256, 1024, 100
+    """BASELINE config 3: differentiable HH SNN layer forward + BPTT, batch 256,
+    784 -> 1024 RS neurons, 100 steps, x = Bernoulli(0.2) + 0.1 N(0,1),
+    W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = bf16 tcgen05 projection,
+    HH forward (full storage), BPTT, dW / db / dX gradient GEMMs."""
+    from paper_2601_21407_b200.layer import HHLayer
+    B, N, T, K_in = 256, 1024, 100, 784
+    torch.manual_seed(0)
+    layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, device=dev)
     g = torch.Generator(device=dev).manual_seed(0)
-    i = 7.8 + 3.0 * torch.randn((T, B, N), device=dev, generator=g)
-    sv = torch.randn((T, B, N), device=dev, generator=g) * 1e-4
-    s0 = Dy.init_state(p, (B, N), device=dev)
-    for _ in range(2):
-        A.backward_through_time(p, s0, i, sv)
+    x = ((torch.rand((T, B, K_in), device=dev, generator=g) < 0.2).float()
+         + 0.1 * torch.randn((T, B, K_in), device=dev, generator=g)).requires_grad_(True)
+
+    def step():
+        layer.zero_grad(set_to_none=True)
+        V, S = layer(x)
+        (V * V).mean().backward()
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "config": "BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, bf16 tcgen05 "
+                      "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs "
+                      "(one unit = one neuron-step through forward and backward)"}
+
+
+def c4_leg(torch, dev):
+    """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
+    batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
+    training step per unit of work."""
+    from paper_2601_21407_b200.layer import HHLayer
+    B, T = 256, 100
+    torch.manual_seed(1)
+    net = torch.nn.ModuleList([HHLayer(784, 2048, w_mean=0.05, w_std=0.1, device=dev),
+                               HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, device=dev),
+                               HHLayer(2048, 10, w_mean=0.02, w_std=0.05, device=dev)])
+    opt = torch.optim.Adam(net.parameters(), lr=5e-4)
+    g = torch.Generator(device=dev).manual_seed(1)
+    x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() \
+        + 0.1 * torch.randn((T, B, 784), device=dev, generator=g)
+    y = torch.randint(0, 10, (B,), device=dev, generator=g)
+
+    import torch.distributed as dist
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    params = [p for p in net.parameters()]
+    flat = torch.empty(sum(p.numel() for p in params), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def step():
+        opt.zero_grad(set_to_none=True)
+        h = x
+        for lyr in net[:-1]:
+            _, h = lyr(h)
+        v, _ = net[-1](h)
+        loss = torch.nn.functional.cross_entropy(v.mean(0), y)
+        loss.backward()
+        if world > 1:  # data parallel over the batch shards of the ranks (SURVEY §8 e2)
+            off = 0
+            for p in params:
+                flat[off:off + p.numel()].copy_(p.grad.reshape(-1))
+                off += p.numel()
+            dist.all_reduce(flat)
+            flat.div_(world)
+            off = 0
+            for p in params:
+                p.grad.copy_(flat[off:off + p.numel()].view_as(p.grad))
+                off += p.numel()
+        opt.step()
+        return loss
+
+    for _ in range(3):
+        step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 5
     e0.record()
     for _ in range(reps):
-        A.backward_through_time(p, s0, i, sv)
+        loss = step()
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
-            "config": "RS layer 256x1024 neurons, 100 steps, fp32, forward + full-storage BPTT "
+    ns = B * T * (2048 + 2048 + 10)
+    return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "loss": float(loss.item()),
+            "config": "BASELINE config 4: stacked HH SNN 784->2048->2048->10, batch 256, 100 steps, "
+                      "bf16 tcgen05 projections, fp32 gating state, CE on time-mean V, Adam "
                       "(one unit = one neuron-step through forward and backward)"}
 
 
@@ -337,6 +404,7 @@ def main():
             dist.all_reduce(ev, op=dist.ReduceOp.MAX)
         extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
         extras["fwd_bwd"] = fwd_bwd_leg(torch, dev)
+        extras["c4_train_step"] = c4_leg(torch, dev)
         if world > 1:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(fb, op=dist.ReduceOp.MAX)
@@ -356,6 +424,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
+                "c4_train_step": extras.get("c4_train_step"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)
