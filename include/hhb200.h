@@ -202,6 +202,9 @@ int hhb_surrogate_grad(const hhb_surrogate_t* surrogate, int32_t dtype, int64_t 
 /* bitmap [T][words] -> bool bytes [T][n] (Trace.spike_series) */
 int hhb_unpack_spikes(const uint32_t* bits, int64_t words_ld, int64_t n_steps, int64_t n,
                       uint8_t* out, int64_t out_ld, void* stream);
+/* the same as float 0/1 (the SNN layer's spike output) */
+int hhb_unpack_spikes_f32(const uint32_t* bits, int64_t words_ld, int64_t n_steps, int64_t n,
+                          float* out, int64_t out_ld, void* stream);
 /* Synthetic stimulus (BASELINE config 2): out[t][j] = amp * Poisson(lam), Philox-4x32-10
  * keyed by (seed, global neuron j + neuron_base, global step t + step_base) so a
  * sharded population draws the same numbers as an unsharded one. */
@@ -236,8 +239,11 @@ int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int
 int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst,
                         int64_t ldd, void* stream);
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream);
-/* out[c] += sum_r src[r][c] in row order (bias gradient, learn.py:273) */
-int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, void* stream);
+/* out[c] += sum_r src[r][c] (bias gradient, learn.py:273), fixed-order two-pass
+ * reduction through hhb_col_sum_scratch(rows, cols) doubles of scratch */
+int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out,
+                double* scratch, void* stream);
+int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols);
 
 /* ---- runtime specialisation ----------------------------------------------- */
 

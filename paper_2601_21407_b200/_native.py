@@ -88,6 +88,7 @@ SIGNATURES = {
     "hhb_spike_detect": (_i32, [_i32, _i64, _vp, _vp, _dbl, _vp, _vp]),
     "hhb_surrogate_grad": (_i32, [C.POINTER(Surrogate), _i32, _i64, _vp, _vp, _vp]),
     "hhb_unpack_spikes": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "hhb_unpack_spikes_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "hhb_poisson_current": (_i32, [_i32, _i64, _i64, C.c_uint64, _i64, _i64, _dbl, _dbl,
                                    _vp, _i64, _vp]),
     "hhb_pipe_probe": (_i32, [_i32, _i64, _vp, C.POINTER(C.c_int64), _vp]),
@@ -96,7 +97,8 @@ SIGNATURES = {
     "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
     "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
-    "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp]),
+    "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "hhb_col_sum_scratch": (_i64, [_i64, _i64]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }

@@ -318,7 +318,17 @@ int hhb_unpack_spikes(const uint32_t* bits, int64_t words_ld, int64_t n_steps, i
                       uint8_t* out, int64_t out_ld, void* stream) {
   if (n <= 0 || n_steps <= 0) return HHB_OK;
   if (!bits || !out || words_ld < (n + 31) / 32 || out_ld < n) return fail(HHB_EINVAL, "bad unpack args");
-  k_unpack<<<grid_1d(n * n_steps, 256), 256, 0, ST(stream)>>>(bits, words_ld, n_steps, n, out, out_ld);
+  const dim3 grid{unsigned((n + 255) / 256), unsigned(n_steps < 65535 ? n_steps : 65535), 1u};
+  k_unpack<uint8_t><<<grid, 256, 0, ST(stream)>>>(bits, words_ld, n_steps, n, out, out_ld);
+  return cuda_check("k_unpack launch");
+}
+
+int hhb_unpack_spikes_f32(const uint32_t* bits, int64_t words_ld, int64_t n_steps, int64_t n, float* out,
+                          int64_t out_ld, void* stream) {
+  if (n <= 0 || n_steps <= 0) return HHB_OK;
+  if (!bits || !out || words_ld < (n + 31) / 32 || out_ld < n) return fail(HHB_EINVAL, "bad unpack args");
+  const dim3 grid{unsigned((n + 255) / 256), unsigned(n_steps < 65535 ? n_steps : 65535), 1u};
+  k_unpack<float><<<grid, 256, 0, ST(stream)>>>(bits, words_ld, n_steps, n, out, out_ld);
   return cuda_check("k_unpack launch");
 }
 

@@ -581,14 +581,14 @@ __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint6
   }
 }
 
-static __global__ void k_unpack(const uint32_t* bits, int64_t wld, int64_t steps, int64_t n, uint8_t* out,
-                         int64_t old) {
-  const int64_t total = steps * n;
-  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
-       q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = q / n, i = q % n;
-    out[t * old + i] = (bits[t * wld + (i >> 5)] >> (i & 31)) & 1u;
-  }
+// bitmap row t -> one value per neuron (uint8 0/1 for Trace.spike_series, or
+// float 0/1 for the SNN layer); grid.y strides the steps, grid.x the neurons
+template <typename O>
+__global__ void k_unpack(const uint32_t* bits, int64_t wld, int64_t steps, int64_t n, O* out, int64_t old) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t t = blockIdx.y; t < steps; t += gridDim.y)
+    out[t * old + i] = O((bits[t * wld + (i >> 5)] >> (i & 31)) & 1u);
 }
 
 }  // namespace hhb

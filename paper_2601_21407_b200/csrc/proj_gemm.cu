@@ -288,9 +288,9 @@ __global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t ld
 // row-wise bf16x2 split without transposing: dst[r][c] = hi, dst[r][cols + c] = lo
 __global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64_t lds, __nv_bfloat16* dst,
                              int64_t ldd) {
-  const int64_t total = rows * cols;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = i / cols, c = i % cols;
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     const float x = src[r * lds + c];
     const __nv_bfloat16 hi = __float2bfloat16_rn(x);
     dst[r * ldd + c] = hi;
@@ -304,13 +304,33 @@ __global__ void k_cast_bf16(int64_t n, const float* src, __nv_bfloat16* dst) {
 }
 
 // deterministic column sums of a [rows][cols] fp32 matrix (bias gradient,
-// learn.py:273): one thread per column walks the rows in order
-__global__ void k_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out) {
+// learn.py:273).  Pass 1: block (bx, by) covers 32 columns x one row chunk;
+// its 8 row-lanes stride the chunk in order (coalesced 128 B rows), then the
+// lanes are summed in order into part[by][c].  Pass 2 sums the chunks in order.
+constexpr int kColChunks = 64;
+__global__ void __launch_bounds__(256) k_col_sum_part(int64_t rows, int64_t cols, const float* src, int64_t ld,
+                                                      double* part) {
+  __shared__ double red[8][33];
+  const int64_t c = int64_t(blockIdx.x) * 32 + threadIdx.x;
+  const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
+  const int64_t r0 = int64_t(blockIdx.y) * per, r1 = min(rows, r0 + per);
+  double acc = 0.0;
+  if (c < cols)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) acc += double(src[r * ld + c]);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    part[int64_t(blockIdx.y) * cols + c] = s;
+  }
+}
+__global__ void k_col_sum_final(int64_t cols, int chunks, const double* part, double* out) {
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
-  double acc = 0.0;
-  for (int64_t r = 0; r < rows; ++r) acc += double(src[r * ld + c]);
-  out[c] += acc;
+  double s = 0.0;
+  for (int k = 0; k < chunks; ++k) s += part[int64_t(k) * cols + c];
+  out[c] += s;
 }
 
 // ------------------------------------------------------------ host
@@ -449,7 +469,8 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
                         void* stream) {
   if (rows <= 0 || cols <= 0) return HHB_OK;
   if (ldd < 2 * cols) return fail(HHB_EINVAL, "ldd < 2*cols");
-  hhb::gemm::k_split_rows<<<grid_1d(rows * cols, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  const dim3 grid{unsigned((cols + 255) / 256), unsigned(rows < 65535 ? rows : 65535), 1u};
+  hhb::gemm::k_split_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
   return cuda_check("k_split_rows launch");
 }
@@ -461,10 +482,23 @@ int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {
   return cuda_check("k_cast_bf16 launch");
 }
 
-int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, void* stream) {
+static int col_chunks(int64_t rows) {
+  return int(rows < hhb::gemm::kColChunks * 8 ? (rows + 7) / 8 : hhb::gemm::kColChunks);
+}
+
+int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols) { return rows > 0 && cols > 0 ? col_chunks(rows) * cols : 0; }
+
+int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out, double* scratch,
+                void* stream) {
   if (rows <= 0 || cols <= 0) return HHB_OK;
-  hhb::gemm::k_col_sum<<<unsigned((cols + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(rows, cols, src,
-                                                                                                      ld, out);
+  if (!scratch) return fail(HHB_EINVAL, "col_sum needs hhb_col_sum_scratch doubles of scratch");
+  using namespace hhb::gemm;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int chunks = col_chunks(rows);
+  const dim3 grid{unsigned((cols + 31) / 32), unsigned(chunks), 1u};
+  const dim3 block{32u, 8u, 1u};
+  k_col_sum_part<<<grid, block, 0, st>>>(rows, cols, src, ld, scratch);
+  k_col_sum_final<<<unsigned((cols + 127) / 128), 128, 0, st>>>(cols, chunks, scratch, out);
   return cuda_check("k_col_sum launch");
 }
 

@@ -104,8 +104,11 @@ def grad_input(dI: torch.Tensor, wb: torch.Tensor, k_in: int) -> torch.Tensor:
 
 def col_sum(dI: torch.Tensor) -> torch.Tensor:
     M, N = dI.shape
+    lib = nat.load()
     out = torch.zeros(N, dtype=torch.float64, device=dI.device)
-    nat.check(nat.load().hhb_col_sum(M, N, dI.data_ptr(), dI.stride(0), out.data_ptr(), _stream()), "colsum")
+    scratch = torch.empty(max(1, int(lib.hhb_col_sum_scratch(M, N))), dtype=torch.float64, device=dI.device)
+    nat.check(lib.hhb_col_sum(M, N, dI.data_ptr(), dI.stride(0), out.data_ptr(), scratch.data_ptr(), _stream()),
+              "colsum")
     return out
 
 
@@ -126,7 +129,9 @@ class _HHLayerFn(torch.autograd.Function):
         v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
         bits = torch.empty((T, (n + 31) // 32), dtype=torch.int32, device=x.device)
         _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, bits=bits, ckpt=ckpt, ckpt_every=K)
-        spikes = _unpack(bits, T, n).to(torch.float32)
+        spikes = torch.empty((T, n), dtype=torch.float32, device=x.device)
+        nat.check(nat.load().hhb_unpack_spikes_f32(bits.data_ptr(), bits.shape[1], T, n, spikes.data_ptr(), n,
+                                                   _stream()), "unpack")
         if layer.check_finite:
             _raise_if_bad(bad)
         ctx.save_for_backward(xb, wb, cur, ckpt)

@@ -90,6 +90,7 @@ def test_transpose_cast_colsum(cuda):
     torch.cuda.synchronize()
     assert torch.equal(cb, x.to(torch.bfloat16))
     s = torch.zeros(129, dtype=torch.float64, device=cuda)
-    nat.check(lib.hhb_col_sum(333, 129, x.data_ptr(), 129, s.data_ptr(), None), "s")
+    scratch = torch.empty(int(lib.hhb_col_sum_scratch(333, 129)), dtype=torch.float64, device=cuda)
+    nat.check(lib.hhb_col_sum(333, 129, x.data_ptr(), 129, s.data_ptr(), scratch.data_ptr(), None), "s")
     torch.cuda.synchronize()
     assert torch.allclose(s, x.double().sum(0), rtol=1e-12, atol=1e-9)
