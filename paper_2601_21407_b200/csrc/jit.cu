@@ -539,20 +539,35 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
         if (on) store_state(a.seg + (t + 1 - lo) * sstride, a.ck_ld, ii, v, p);
       }
     }
+    // operands of step t are loaded while step t+1 (the previous iteration)
+    // computes: state (K == 1: checkpoint row; else the recomputed segment),
+    // current and seeds -- software pipelining of the long-latency loads
+    if (K == 1) load_state(a.ckpt + (hi - 1) * sstride, a.ck_ld, ii, v, p);
+    float cur = __ldg(a.i_ext + (hi - 1) * a.i_st + ii * a.i_sn);
+    float sv = a.seed_v != nullptr ? __ldg(a.seed_v + (hi - 1) * a.sv_ld + ii) : 0.0f;
+    float ds = has_s ? __ldg(a.seed_s + (hi - 1) * a.ss_ld + ii) : 0.0f;
     for (i64 t = hi - 1; t >= lo; --t) {
-      if (t != hi - 1 || K == 1) {
-        const float* src = (K == 1) ? a.ckpt + t * sstride : (t == lo ? ck : a.seg + (t - lo) * sstride);
-        load_state(src, a.ck_ld, ii, v, p);
+      float nv = 0.0f, np_[NGX], ncur = 0.0f, nsv = 0.0f, nds = 0.0f;
+      if (t > lo) {
+        const float* src = (K == 1) ? a.ckpt + (t - 1) * sstride : (t - 1 == lo ? ck : a.seg + (t - 1 - lo) * sstride);
+        load_state(src, a.ck_ld, ii, nv, np_);
+        ncur = __ldg(a.i_ext + (t - 1) * a.i_st + ii * a.i_sn);
+        if (a.seed_v != nullptr) nsv = __ldg(a.seed_v + (t - 1) * a.sv_ld + ii);
+        if (has_s) nds = __ldg(a.seed_s + (t - 1) * a.ss_ld + ii);
       }
-      const float cur = __ldg(a.i_ext + t * a.i_st + ii * a.i_sn);
-      if (a.seed_v != nullptr) d_v = __fadd_rn(d_v, __ldg(a.seed_v + t * a.sv_ld + ii));
-      const float ds = has_s ? __ldg(a.seed_s + t * a.ss_ld + ii) : 0.0f;
+      d_v = __fadd_rn(d_v, sv);
       const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, has_s, acc);
       if (on && a.d_i != nullptr) a.d_i[t * a.di_ld + ii] = di;
       bool ok = finitef_(d_v);
 #pragma unroll
       for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[g]);
       if (!ok && bad < 0 && on) bad = a.step_base + t;
+      v = nv;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) p[g] = np_[g];
+      cur = ncur;
+      sv = nsv;
+      ds = nds;
     }
   }
   if (on) {
