@@ -245,6 +245,26 @@ int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double
                 double* scratch, void* stream);
 int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols);
 
+/* ---- recurrent network (BASELINE config 5) ---------------------------------- */
+
+/* Per-step input of the cortex network (cortex.py:283-301) for n local
+ * neurons: arrived = ring[t % depth][i] * w_scale (int64 fixed point, row then
+ * zeroed), psp = psp*decay + arrived + background, cur = psp (+ extra).
+ * bg_mode 0: none; 1: bg[i] supplied (e.g. the reference RNG's sample);
+ * 2: compound Poisson N*mu + sigma*sqrt(N)*z, N ~ Poisson(lam[i]) drawn with
+ * Philox keyed by (seed, neuron_base + i, t). */
+int hhb_cortex_input(int32_t dtype, int64_t n, int64_t t, int64_t depth, int64_t* ring, void* psp,
+                     double decay, int32_t bg_mode, const void* bg, const double* lam, double mu,
+                     double sigma, uint64_t seed, int64_t neuron_base, const void* extra, void* cur,
+                     double w_scale, void* stream);
+/* Delayed spike delivery (SpikeBuffer.enqueue, cortex.py:248-250, 304-308):
+ * for every set bit s of bits[0..words) (global source ids) and every synapse
+ * j in offsets[s] .. offsets[s+1]: ring[(t + delays[j]) % depth][targets[j]]
+ * += weights_fx[j] (int64 atomics: order-independent, deterministic). */
+int hhb_spike_deliver(int64_t words, const uint32_t* bits, const int64_t* offsets,
+                      const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
+                      int64_t t, int64_t depth, int64_t n_local, int64_t* ring, void* stream);
+
 /* ---- runtime specialisation ----------------------------------------------- */
 
 /* The float (HHB_F32) forward/backward kernels are generated per parameter

@@ -99,6 +99,9 @@ SIGNATURES = {
     "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "hhb_col_sum_scratch": (_i64, [_i64, _i64]),
+    "hhb_cortex_input": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _dbl, _dbl,
+                                C.c_uint64, _i64, _vp, _vp, _dbl, _vp]),
+    "hhb_spike_deliver": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }

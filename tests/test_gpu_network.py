@@ -1,0 +1,79 @@
+"""GPU tests of the config-5 network (ring input, HH step, fixed-point
+delivery): raster parity with the reference's run_network, and bit-exact
+invariance under sharding the population over P ranks (emulated on one GPU:
+every rank's local step, then the concatenated bitmap to every rank)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from paper_2601_21407_b200 import network as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _small():
+    g = golden("cortex_small")
+    return g, N.build_network(float(g["scale"]), int(g["seed"]))
+
+
+def test_fp64_network_reproduces_reference_raster(cuda):
+    g, topo = _small()
+    cfg = N.REST_CONFIG
+    hb = N.HostBackground(topo, N.make_background(cfg), cfg.dt, np.random.default_rng(int(g["run_seed"])))
+    net = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float64, background="host", host_bg=hb)
+    steps = int(round(float(g["duration_ms"]) / cfg.dt))
+    t, i = net.run(steps)
+    order = np.lexsort((i, t))
+    ref = np.lexsort((g["spike_id"], g["spike_t"]))
+    assert np.array_equal(i[order], g["spike_id"][ref])
+    assert np.allclose(t[order], g["spike_t"][ref])
+
+
+def _run_sharded(topo, cfg, world, steps, dtype, cuda):
+    nets = [N.CortexNetwork(topo, cfg, device=cuda, dtype=dtype, rank=r, world=world, background="philox",
+                            seed=5) for r in range(world)]
+    per = N.words_per_rank(topo.n_neurons, world)
+    total = (topo.n_neurons + 31) // 32
+    rows = []
+    for _ in range(steps):
+        allw = torch.cat([net.advance_local()[:per] for net in nets])[:total].contiguous()
+        for net in nets:
+            net.deliver(allw)
+        rows.append(allw.clone())
+    return torch.stack(rows).cpu().numpy(), [net.v.cpu().numpy() for net in nets]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_sharding_is_bit_exact(cuda, dtype):
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    ref, v1 = _run_sharded(topo, cfg, 1, 300, dtype, cuda)
+    assert ref.any()
+    for world in (2, 4, 7):
+        got, vs = _run_sharded(topo, cfg, world, 300, dtype, cuda)
+        assert np.array_equal(got, ref), world
+        assert np.array_equal(np.concatenate(vs), v1[0])
+
+
+def test_philox_background_moments(cuda):
+    """The device compound-Poisson drive has the reference's moments:
+    mean lam*mu, variance lam*(mu^2 + sigma^2) per neuron-step (cortex.py:225-232)."""
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    net = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float64, background="philox", seed=9)
+    net.decay = 0.0                       # psp = this step's background only
+    samples = []
+    for _ in range(400):
+        net._input()
+        samples.append(net.cur[:net.n].clone())
+        net.t += 1
+    x = torch.stack(samples).cpu().numpy()
+    lam = N.background_lambda(topo, N.make_background(cfg), cfg.dt)
+    mu, sd = cfg.bg_mean, cfg.bg_std
+    for k, p in enumerate(topo.populations):
+        xs = x[:, p.offset:p.offset + p.size]
+        L = lam[p.offset]
+        assert abs(xs.mean() - L * mu) < 0.02 * L * mu
+        assert abs(xs.var() - L * (mu * mu + sd * sd)) < 0.05 * L * (mu * mu + sd * sd)
