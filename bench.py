@@ -244,6 +244,45 @@ def fwd_bwd_leg(torch, dev):
                       "(one unit = one neuron-step through forward and backward)"}
 
 
+def c5_leg(torch, dev, steps=1000):
+    """BASELINE config 5: recurrent HH cortex, build_network(scale=0.5, seed=0)
+    (38,586 RS neurons, 71.2M synapses, delays up to 193 steps), REST_CONFIG,
+    fp32, device Philox background; per step: ring drain + PSP + background,
+    HH step, bitmap all-gather (NCCL when N > 1), fixed-point delivery.
+    One unit = one neuron-step of the whole network (strong scaling)."""
+    import numpy as np
+    import torch.distributed as dist
+    from paper_2601_21407_b200 import network as N
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    t0 = time.perf_counter()
+    topo = N.build_network(0.5, 0)
+    build_s = time.perf_counter() - t0
+    ex = N.allgather_exchange(topo.n_neurons) if world > 1 else None
+    net = N.CortexNetwork(topo, N.REST_CONFIG, device=dev, dtype=np.float32, rank=rank, world=world,
+                          exchange=ex, background="philox", seed=1)
+    for _ in range(100):
+        net.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    spikes = torch.zeros((), dtype=torch.int64, device=dev)
+    e0.record()
+    for _ in range(steps):
+        g = net.step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    m = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    ms = float(m.item())
+    return {"value": topo.n_neurons * steps / (ms * 1e-3), "unit": UNIT, "ms_per_network_step": ms / steps,
+            "steps": steps, "neurons": topo.n_neurons, "synapses": topo.n_synapses,
+            "host_build_s": build_s,
+            "config": "BASELINE config 5: recurrent HH cortex scale 0.5 (38,586 neurons, 71.2M synapses), "
+                      "REST_CONFIG, fp32, per-step spike-bitmap all-gather"}
+
+
 def c4_leg(torch, dev):
     """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
     batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
@@ -405,6 +444,7 @@ def main():
         extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
         extras["fwd_bwd"] = fwd_bwd_leg(torch, dev)
         extras["c4_train_step"] = c4_leg(torch, dev)
+        extras["c5_network"] = c5_leg(torch, dev)
         if world > 1:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(fb, op=dist.ReduceOp.MAX)
@@ -424,7 +464,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
-                "c4_train_step": extras.get("c4_train_step"),
+                "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)
