@@ -149,36 +149,53 @@ __device__ __forceinline__ T poisson_draw(const PoissonTab<T>& tab, uint32_t wor
 // byte is b (float(word) >= b * 2^24 exactly), so the search starts there and
 // usually stops at once.  Bit-identical to poisson_draw; avoids the warp
 // paying the longest of 32 (x VEC) linear searches.
+//
+// Each bucket stores {amp*k0, C(k0), C(k0+1), C(k0+2)} (C(j) = cdf[j], raised to 2 > any
+// u from j = size-1 on, where the capped search stops), so a draw is one 16-byte
+// shared load, two compares and, for the rare u > C(k0+2), a tail walk.  The
+// uniform is (word >> 9) * 2^-23, built from the mantissa bits (no int->float).
 template <typename T>
 struct PoissonSmem {
-  int guide[256];
+  __align__(16) T g4[256][4];
+  int k0[256];
   T cdf[48];
-  int size;
   T amp;
   __device__ void fill(const PoissonTab<T>& tab) {
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : T(2);
+    if (threadIdx.x == 0) amp = tab.amp;
     for (int b = threadIdx.x; b < 256; b += blockDim.x) {
       const T lo = T(b) * T(0.00390625);
       int k = 0;
       while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
-      guide[b] = k;
-    }
-    // entries from size-1 on are raised to 2 (> any u): the search then stops at
-    // size-1 by itself, exactly where the capped linear search stops
-    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : T(2);
-    if (threadIdx.x == 0) {
-      size = tab.size;
-      amp = tab.amp;
+      k0[b] = k;
+      const auto C = [&](int j) { return j < tab.size - 1 ? tab.cdf[j] : T(2); };
+      g4[b][0] = tab.amp * T(k);
+      g4[b][1] = C(k);
+      g4[b][2] = C(k + 1);
+      g4[b][3] = C(k + 2);
     }
   }
-  // Call from warp-converged code: the rare tail walk is a warp-uniform branch.
-  __device__ __forceinline__ T draw(uint32_t word) const {
-    const T u = (T(word) + T(0.5)) * T(2.3283064365386963e-10);
-    int k = guide[word >> 24];
-    k += int(u > cdf[k]);
-    k += int(u > cdf[k]);
-    if (__any_sync(0xffffffffu, u > cdf[k])) {
-      while (u > cdf[k]) ++k;
+  __device__ __forceinline__ static T uniform(uint32_t w) {
+    if constexpr (sizeof(T) == 4) {
+      return __uint_as_float(0x3F800000u | (w >> 9)) - 1.0f;
+    } else {
+      return T(w >> 9) * T(1.1920928955078125e-07);
     }
+  }
+  // the draw, and whether it needs the tail walk (u beyond C(k0+2))
+  __device__ __forceinline__ T draw(uint32_t w, bool& tail) const {
+    const T u = uniform(w);
+    const T* e = g4[w >> 24];
+    T val = e[0];
+    val = (u > e[1]) ? val + amp : val;
+    val = (u > e[2]) ? val + amp : val;
+    tail = u > e[3];
+    return val;
+  }
+  __device__ T tail_draw(uint32_t w) const {
+    const T u = uniform(w);
+    int k = k0[w >> 24] + 3;
+    while (u > cdf[k]) ++k;
     return amp * T(k);
   }
 };
@@ -226,15 +243,27 @@ struct Stimulus {
                                      bool full, T (&c)[VEC]) {
     if constexpr (POIS) {
       const int64_t gt = a.step_base + t;
+      uint32_t w[VEC];
       if constexpr (VEC == 4) {
         const uint4 r = Philox::block(a.seed, (a.nbase + n0) >> 2, gt);
-        c[0] = tab.draw(r.x);
-        c[1] = tab.draw(r.y);
-        c[2] = tab.draw(r.z);
-        c[3] = tab.draw(r.w);
+        w[0] = r.x;
+        w[1] = r.y;
+        w[2] = r.z;
+        w[3] = r.w;
       } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) c[j] = tab.draw(Philox::word(a.seed, a.nbase + n0 + j, gt));
+        for (int j = 0; j < VEC; ++j) w[j] = Philox::word(a.seed, a.nbase + n0 + j, gt);
+      }
+      bool tail[VEC], any_tail = false;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        c[j] = tab.draw(w[j], tail[j]);
+        any_tail = any_tail || tail[j];
+      }
+      if (__any_sync(0xffffffffu, any_tail)) {  // one vote for all VEC draws
+#pragma unroll
+        for (int j = 0; j < VEC; ++j)
+          if (tail[j]) c[j] = tab.tail_draw(w[j]);
       }
     } else {
       load_cur<T, VEC>(a, t, n0, full, c);
@@ -554,16 +583,28 @@ __global__ void __launch_bounds__(256) k_poisson(int64_t n, int64_t steps, uint6
   const bool vec = aligned && j0 + 4 <= n && (ld & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(out) % (4 * sizeof(T))) == 0;
   for (int64_t t = blockIdx.y; t < steps; t += gridDim.y) {
-    T c[4];
+    uint32_t w[4];
     if (aligned) {
       const uint4 r = Philox::block(seed, (nbase + j0) >> 2, tbase + t);
-      c[0] = ps.draw(r.x);
-      c[1] = ps.draw(r.y);
-      c[2] = ps.draw(r.z);
-      c[3] = ps.draw(r.w);
+      w[0] = r.x;
+      w[1] = r.y;
+      w[2] = r.z;
+      w[3] = r.w;
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = ps.draw(Philox::word(seed, nbase + j0 + q, tbase + t));
+      for (int q = 0; q < 4; ++q) w[q] = Philox::word(seed, nbase + j0 + q, tbase + t);
+    }
+    T c[4];
+    bool tail[4], any_tail = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[q] = ps.draw(w[q], tail[q]);
+      any_tail = any_tail || tail[q];
+    }
+    if (__any_sync(0xffffffffu, any_tail)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (tail[q]) c[q] = ps.tail_draw(w[q]);
     }
     T* row = out + t * ld + j0;
     if (vec) {

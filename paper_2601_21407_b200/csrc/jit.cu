@@ -116,12 +116,25 @@ static std::string F(double x) {
   return std::string("(") + buf + ")";
 }
 
+// How a step variant treats the linoid's removable singularity:
+//   kFast   -- direct formula only (the kernel proved no lane of the warp is
+//              within |x/b| < 1/2 of any linoid's v0 this step)
+//   kSeries -- direct formula with the Bernoulli series selected per lane
+// Both give identical bits on lanes outside the series region, so which
+// variant a warp ran never changes a neuron's result.
+enum SeriesMode { kFast = 0, kSeries = 1 };
+
 // One rate: value (and slope) of kind(a, v0, b) * scale at `v`.
 static void emit_rate(std::string& o, const hhb_rate_t& r, double scale, const std::string& val,
-                      const std::string* slope) {
+                      const std::string* slope, SeriesMode mode) {
   const double A = r.a * scale, K2 = -kLog2e / r.b;
   o += "  {\n";
-  if (r.kind == HHB_RATE_EXP || r.kind == HHB_RATE_SIGMOID) {
+  if (r.kind == HHB_RATE_EXP && A > 0) {
+    // a*2^y = 2^(y + log2 a): the amplitude rides in the exponent (one FMUL less)
+    o += fmt("    %s = ex2f_(__fmaf_rn(v, %s, %s));\n", val.c_str(), F(K2).c_str(),
+             F(-r.v0 * K2 + std::log2(A)).c_str());
+    if (slope) o += fmt("    %s = __fmul_rn(%s, %s);\n", slope->c_str(), F(-1.0 / r.b).c_str(), val.c_str());
+  } else if (r.kind == HHB_RATE_EXP || r.kind == HHB_RATE_SIGMOID) {
     o += fmt("    const float e = ex2f_(__fmaf_rn(v, %s, %s));\n", F(K2).c_str(), F(-r.v0 * K2).c_str());
     if (r.kind == HHB_RATE_EXP) {
       o += fmt("    %s = __fmul_rn(%s, e);\n", val.c_str(), F(A).c_str());
@@ -144,8 +157,12 @@ static void emit_rate(std::string& o, const hhb_rate_t& r, double scale, const s
       o += fmt("    %s = __fmul_rn(__fmul_rn(%s, __fsub_rn(den, __fmul_rn(__fmul_rn(x, %s), e))), "
                "__fmul_rn(rd, rd));\n",
                slope->c_str(), F(A).c_str(), F(1.0 / r.b).c_str());
+    if (mode == kFast) {
+      o += "  }\n";
+      return;
+    }
     o += fmt("    const bool sm = fabsf(x) < %s;\n", F(0.5 * std::fabs(r.b)).c_str());
-    o += "    if (__any_sync(0xffffffffu, sm)) {\n";
+    o += "    {\n";
     o += fmt("      const float u = __fmul_rn(x, %s);\n", F(1.0 / r.b).c_str());
     o += "      const float w = __fmul_rn(u, u);\n";
     o += "      float f = __fmaf_rn(w, -8.267195767195767e-07f, 3.3068783068783070e-05f);\n";
@@ -203,12 +220,22 @@ static Layout layout_of(const hhb_params_t* P) {
   return L;
 }
 
-// step_fwd(v, p[], cur) -> v' ; p[] updated in place (hh_step, dynamics.py:472-528)
-static std::string emit_forward_step(const hhb_params_t* P, const Layout& L) {
+// near_linoid(v): is v inside the series region |v - v0| < |b|/2 of any linoid rate?
+static std::string emit_near_linoid(const hhb_params_t* P) {
+  std::string o = "__device__ __forceinline__ bool near_linoid(const float v) {\n  bool n = false;\n";
+  for (int g = 0; g < P->n_gates; ++g)
+    for (const hhb_rate_t* r : {&P->gates[g].alpha, &P->gates[g].beta})
+      if (r->kind == HHB_RATE_LINOID)
+        o += fmt("  n = n || (fabsf(__fsub_rn(v, %s)) < %s);\n", F(r->v0).c_str(), F(0.5 * std::fabs(r->b)).c_str());
+  return o + "  return n;\n}\n";
+}
+
+// step_fwd_<f|s>(v, p[], cur) -> v' ; p[] updated in place (hh_step, dynamics.py:472-528)
+static std::string emit_forward_step(const hhb_params_t* P, const Layout& L, SeriesMode mode) {
   std::string o;
   const int NG = L.ng;
-  o += fmt("__device__ __forceinline__ float step_fwd(const float v, float (&p)[%d], const float cur) {\n",
-           NG > 0 ? NG : 1);
+  o += fmt("__device__ __forceinline__ float step_fwd_%s(const float v, float (&p)[%d], const float cur) {\n",
+           mode == kFast ? "f" : "s", NG > 0 ? NG : 1);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += "  float eta = 1.0f;\n";
@@ -220,8 +247,8 @@ static std::string emit_forward_step(const hhb_params_t* P, const Layout& L) {
     o += "  const float pk = " + pow_expr(pg, G.exponent) + ";\n";
     o += L.first[g] ? "  eta = pk;\n" : "  eta = __fmul_rn(eta, pk);\n";
     o += "  float a, b;\n";
-    emit_rate(o, G.alpha, P->rate_scale, "a", nullptr);
-    emit_rate(o, G.beta, P->rate_scale, "b", nullptr);
+    emit_rate(o, G.alpha, P->rate_scale, "a", nullptr, mode);
+    emit_rate(o, G.beta, P->rate_scale, "b", nullptr, mode);
     o += "  const float s = __fadd_rn(a, b);\n";
     o += "  const float pinf = __fmul_rn(a, rcpf_(s));\n";
     o += fmt("  const float dec = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
@@ -237,15 +264,15 @@ static std::string emit_forward_step(const hhb_params_t* P, const Layout& L) {
 }
 
 // adjoint of step_fwd (hh_step_backward, adjoint.py:116-188)
-static std::string emit_backward_step(const hhb_params_t* P, const Layout& L) {
+static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, SeriesMode mode) {
   std::string o;
   const int NG = L.ng, NGX = NG > 0 ? NG : 1;
   const double dtcm = P->dt / P->c_m;
   o += fmt(
-      "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[%d], "
+      "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
       "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
       "double (&acc)[%d]) {\n",
-      NGX, NGX, kSlots);
+      mode == kFast ? "f" : "s", NGX, NGX, kSlots);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += fmt("  float gsum = %s;\n", F(L.gl).c_str());
@@ -283,8 +310,8 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L) {
     const hhb_channel_t& C = P->channels[L.chan[g]];
     o += fmt("  // gate %d\n  {\n  float a, b, da, db;\n", g);
     std::string sa = "da", sb = "db";
-    emit_rate(o, G.alpha, P->rate_scale, "a", &sa);
-    emit_rate(o, G.beta, P->rate_scale, "b", &sb);
+    emit_rate(o, G.alpha, P->rate_scale, "a", &sa, mode);
+    emit_rate(o, G.beta, P->rate_scale, "b", &sb, mode);
     o += "  const float s = __fadd_rn(a, b);\n";
     o += "  const float rs = rcpf_(s);\n";
     o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
@@ -337,28 +364,38 @@ __device__ __forceinline__ uint4 philox(unsigned long long seed, i64 gj, i64 gq)
 }
 // guide-table inverse CDF in shared memory (hh_kernels.cuh PoissonSmem)
 struct PoissonSmem {
-  int guide[256];
+  float4 g4[256];
+  int k0[256];
   float cdf[48];
-  int size;
   float amp;
   __device__ void fill(const PoissonTab& tab) {
+    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
+    if (threadIdx.x == 0) amp = tab.amp;
     for (int b = threadIdx.x; b < 256; b += blockDim.x) {
       const float lo = float(b) * 0.00390625f;
       int k = 0;
       while (k < tab.size - 1 && tab.cdf[k] < lo) ++k;
-      guide[b] = k;
+      k0[b] = k;
+      const float c0 = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
+      const float c1 = k + 1 < tab.size - 1 ? tab.cdf[k + 1] : 2.0f;
+      const float c2 = k + 2 < tab.size - 1 ? tab.cdf[k + 2] : 2.0f;
+      g4[b] = make_float4(tab.amp * float(k), c0, c1, c2);
     }
-    for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
-    if (threadIdx.x == 0) { size = tab.size; amp = tab.amp; }
   }
-  __device__ __forceinline__ float draw(u32 word) const {
-    const float u = (float(word) + 0.5f) * 2.3283064365386963e-10f;
-    int k = guide[word >> 24];
-    k += int(u > cdf[k]);
-    k += int(u > cdf[k]);
-    if (__any_sync(0xffffffffu, u > cdf[k])) {
-      while (u > cdf[k]) ++k;
-    }
+  __device__ __forceinline__ static float uniform(u32 w) { return __uint_as_float(0x3F800000u | (w >> 9)) - 1.0f; }
+  __device__ __forceinline__ float draw(u32 w, bool& tail) const {
+    const float u = uniform(w);
+    const float4 e = g4[w >> 24];
+    float val = e.x;
+    val = (u > e.y) ? val + amp : val;
+    val = (u > e.z) ? val + amp : val;
+    tail = u > e.w;
+    return val;
+  }
+  __device__ float tail_draw(u32 w) const {
+    const float u = uniform(w);
+    int k = k0[w >> 24] + 3;
+    while (u > cdf[k]) ++k;
     return amp * float(k);
   }
 };
@@ -402,19 +439,32 @@ struct Stimulus {
                                      float (&c)[VEC]) {
     if (POIS) {
       const i64 gt = a.step_base + t;
+      u32 w[VEC];
       if (VEC == 4) {  // host guarantees (nbase + n0) % 4 == 0
         const uint4 r = philox(a.seed, (a.nbase + n0) >> 2, gt);
-        const u32 w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) c[j] = tab.draw(w[j]);
+        w[0] = r.x;
+        w[VEC > 1 ? 1 : 0] = r.y;
+        w[VEC > 2 ? 2 : 0] = r.z;
+        w[VEC > 3 ? 3 : 0] = r.w;
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           const i64 gj = a.nbase + n0 + j;
           const uint4 r = philox(a.seed, gj >> 2, gt);
           const int i = int(gj & 3);
-          c[j] = tab.draw(i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w);
+          w[j] = i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w;
         }
+      }
+      bool tail[VEC], any_tail = false;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        c[j] = tab.draw(w[j], tail[j]);
+        any_tail = any_tail || tail[j];
+      }
+      if (__any_sync(0xffffffffu, any_tail)) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j)
+          if (tail[j]) c[j] = tab.tail_draw(w[j]);
       }
     } else {
       load_cur<VEC>(a, t, n0, full, c);
@@ -463,12 +513,24 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
     }
     --ck_count;
     u32 nib = 0;
+    // one warp vote per step for all VEC neurons of every lane: the
+    // branch-free variant unless a neuron sits in a linoid's series region
+    bool near = false;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) near = near || near_linoid(v[j]);
+    float vn[VEC];
+    if (__any_sync(0xffffffffu, near)) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_s(v[j], p[j], cur[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_f(v[j], p[j], cur[j]);
+    }
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      const float vn = step_fwd(v[j], p[j], cur[j]);
-      nib |= u32((v[j] < THETA) && (vn >= THETA) && (n0 + j < a.n)) << j;
-      if (!finitef_(vn) && bad == LLMAX && n0 + j < a.n) bad = a.step_base + t;
-      v[j] = vn;
+      nib |= u32((v[j] < THETA) && (vn[j] >= THETA) && (n0 + j < a.n)) << j;
+      if (!finitef_(vn[j]) && bad == LLMAX && n0 + j < a.n) bad = a.step_base + t;
+      v[j] = vn[j];
     }
     if (a.v_out != nullptr) store_vec<VEC>(a.v_out + t * a.v_ld, v, full, n0, a.n);
     if (a.spk != nullptr) {
@@ -605,8 +667,24 @@ static std::string generate(const hhb_params_t* P) {
   // 4 resident 256-thread blocks (<= 64 registers) measured best for config 2
   // on B200 (profiles/r1_variants.md); 1 lets ptxas take ~100+ registers
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 4);
-  src += emit_forward_step(P, L);
-  src += emit_backward_step(P, L);
+  src += emit_near_linoid(P);
+  src += emit_forward_step(P, L, kFast);
+  src += emit_forward_step(P, L, kSeries);
+  src += emit_backward_step(P, L, kFast);
+  src += emit_backward_step(P, L, kSeries);
+  // one-neuron dispatch: a warp vote picks the branch-free variant unless some
+  // lane is inside a linoid's series region this step
+  src += fmt(
+      "__device__ __forceinline__ float step_fwd(const float v, float (&p)[%d], const float cur) {\n"
+      "  return __any_sync(0xffffffffu, near_linoid(v)) ? step_fwd_s(v, p, cur) : step_fwd_f(v, p, cur);\n}\n",
+      L.ng > 0 ? L.ng : 1);
+  src += fmt(
+      "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[%d], "
+      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, double (&acc)[%d]) {\n"
+      "  return __any_sync(0xffffffffu, near_linoid(v))\n"
+      "      ? step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc)\n"
+      "      : step_bwd_f(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc);\n}\n",
+      L.ng > 0 ? L.ng : 1, L.ng > 0 ? L.ng : 1, kSlots);
   src += kForwardBody;
   return src;
 }
