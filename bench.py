@@ -35,12 +35,25 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 METRIC = "HH neuron-steps/sec (fwd; fwd+bwd) at 1/2/4/8 B200 vs CPU ref, % roofline"
 UNIT = "neuron-steps/s"
-# MUFU (transcendental) operations per neuron-step of the config-2 channel set:
-# per gate 2 (1/(a+b), exp decay) + 1 per exp-form rate + 2 per linoid/sigmoid
-# rate; SURVEY.md §8 tau = 31.  Algorithmic HBM bytes per neuron-step of the
-# forward kernel: I read 4 + V write 4 + spike bit 1/8.
+# Transcendentals per neuron-step of the config-2 channel set in the
+# reference's formulation (SURVEY.md §8 tau = 31: per gate 2 rate exps, 1 decay
+# exp, 1/(a+b), plus 1 reciprocal per linoid/sigmoid rate).  The merged-form
+# kernel evaluates the same step with fewer MUFU ops (shared rate exps, one
+# reciprocal per gate); that count is read from the generated step itself.
+# Algorithmic HBM bytes per neuron-step of the forward kernel: V write 4 +
+# spike bit 1/8, plus the I read 4 when the stimulus is not fused.
 TAU_C2 = 31
-BYTES_PER_NS = 8.125
+BYTES_PER_NS = 4.125
+BYTES_PER_NS_UNFUSED = 8.125
+
+
+def mufu_per_step(nat, params):
+    """MUFU ops (ex2 + rcp) per neuron-step of the generated regular-lane step."""
+    src = nat.jit_source(params)
+    fn = "step_fwd_m(" if "step_fwd_m(" in src else "step_fwd_s("
+    body = src[src.index("__device__ __forceinline__ float " + fn):]
+    body = body[:body.index("\n}\n")]
+    return body.count("ex2f_(") + body.count("rcpf_("), fn[:-1]
 
 
 def parse():
@@ -412,28 +425,45 @@ def main():
     fwd_avg_s = fwd_ms * 1e-3 / n_fwd
     ns_per_launch = args.neurons * args.chunk
     mufu_peak = probe_mufu_peak(torch, nat, dev)
-    achieved = TAU_C2 * ns_per_launch / fwd_avg_s
-    traffic = None
+    mufu, step_fn = mufu_per_step(nat, params)
+    bpn = BYTES_PER_NS_UNFUSED if args.no_fuse else BYTES_PER_NS
+    achieved = mufu * ns_per_launch / fwd_avg_s
+    prof = {}
     tp = os.path.join(ROOT, "profiles", "k_forward_dram.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp))["bytes_per_neuron_step"] * ns_per_launch
+            prof = json.load(open(tp))
         except (OSError, ValueError):
-            traffic = None
+            prof = {}
+    traffic = prof["bytes_per_neuron_step"] * ns_per_launch if "bytes_per_neuron_step" in prof else None
     peaks = {}
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk):
         peaks = json.load(open(pk))
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kname = ("hh_fwdp_v4" if not args.no_fuse else "hh_fwd_v4") + " (NVRTC-specialised, hhb_forward"
+    kname += "_poisson)" if not args.no_fuse else ")"
     roof = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9, "unit": "Gop/s",
-            "frac": achieved / mufu_peak, "traffic": traffic,
-            "kernel": "k_forward<float,6,4> (hhb_forward)",
-            "algorithmic": f"{TAU_C2} MUFU ops per neuron-step x {ns_per_launch} neuron-steps per launch",
+            "frac": achieved / mufu_peak, "traffic": traffic, "kernel": kname,
+            "algorithmic": f"{mufu} MUFU ops per neuron-step ({step_fn}: shared rate exps + one "
+                           f"reciprocal per gate) x {ns_per_launch} neuron-steps per launch",
             "peak_source": "measured live: hhb_pipe_probe MUFU.EX2 throughput on this GPU",
             "avg_launch_ms": fwd_avg_s * 1e3, "share_of_step": fwd_ms / sum(step_ms),
-            "hbm": {"achieved_gbs": BYTES_PER_NS * ns_per_launch / fwd_avg_s / 1e9,
-                    "peak_gbs": hbm_peak, "frac": BYTES_PER_NS * ns_per_launch / fwd_avg_s / 1e9 / hbm_peak,
+            "reference_tau": {"transcendentals_per_neuron_step": TAU_C2,
+                              "frac": TAU_C2 * ns_per_launch / fwd_avg_s / mufu_peak,
+                              "note": "the reference formulation's 31 transcendentals per neuron-step "
+                                      "delivered per second, over the same MUFU peak"},
+            "hbm": {"achieved_gbs": bpn * ns_per_launch / fwd_avg_s / 1e9,
+                    "peak_gbs": hbm_peak, "frac": bpn * ns_per_launch / fwd_avg_s / 1e9 / hbm_peak,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}}
+    if "inst_per_neuron_step" in prof and not args.no_fuse:
+        # instruction-issue view: 4 warp-instructions / clk / SM = 128 thread-instructions
+        sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+        issue_bound = 148 * 128 * sm_hz / prof["inst_per_neuron_step"]
+        roof["issue"] = {"inst_per_neuron_step": prof["inst_per_neuron_step"],
+                         "bound_neuron_steps_per_s": issue_bound,
+                         "frac": ns_per_launch / fwd_avg_s / issue_bound,
+                         "source": prof.get("source")}
 
     extras = {}
     if not args.no_extras:

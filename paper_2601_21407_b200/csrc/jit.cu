@@ -341,6 +341,335 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
   return o;
 }
 
+// ------------------------------------------------------------ merged step
+// The MUFU pipe (16 ops/clk/SM) bounds the step above: config 2 needs 12 rate
+// exps, 6 decay exps and 13 reciprocals per neuron-step.  The merged form
+// spends fewer of them on the same arithmetic:
+//  * rates whose slopes |b| are equal share one exponential: with
+//    E = exp(-(v - vc)/b_g), a rate of slope +b_g needs c * E and one of slope
+//    -b_g needs c' / E (c, c' constants); the reciprocal never materialises
+//    because every rate is kept as a fraction n / d;
+//  * a gate's two fractions merge: s = a + b = N / D and p_inf = a / s = A / N
+//    with A = n_a d_b, N = A + n_b d_a, D = d_a d_b, and one reciprocal
+//    r = 1 / (N D) serves both divisions (1/D = N r, 1/N = D r);
+//  * -dt*log2(e) (and rate_scale) are folded into the numerators, so N / D is
+//    the exp2 argument of the decay factor directly.
+// Config 2: 8 shared exps + 6 decay exps + 6 reciprocals = 20 MUFU ops.
+//
+// The algebra is exact; what changes is rounding (a few ulp) and the range of
+// the intermediates, so the host analyses the step in double over a voltage
+// grid: one reciprocal per gate where N * D stays inside [2^-100, 2^100], two
+// where only N and D do; the window [lo, hi] around v_rest where every
+// intermediate is in range becomes a per-lane predicate.  Lanes outside it
+// take the direct form (step_fwd_s), selected per lane, so a neuron's result
+// depends only on its own state -- never on which warp-variant ran.
+// A linoid's removable singularity: where |d| < 1/8 (|x/b| < ~0.13) the
+// fraction is replaced per lane by (a b (1 + u/2 + u^2/12), 1), u = x/b,
+// whose truncation error (u^4/720) is below float rounding there.
+namespace mg {
+
+constexpr double kRangeLo = 0x1p-100, kRangeHi = 0x1p100;
+constexpr double kSingThr = 0.125;
+
+struct Group {
+  double b;       // signed slope of the first member; E = exp(-(v - vc) / b)
+  double vc;
+  int members = 0;
+};
+
+struct RatePlan {
+  int kind;
+  int group;
+  int sigma;      // +1: e_r = c E ; -1: e_r = c / E
+  double c;
+  double Sa;      // a * rate_scale * (-dt log2 e)
+  double v0, b;
+  bool direct;    // single-member exp: value = sign(Sa) * ex2(v K2 + C + log2|Sa|)
+  bool rational() const { return !(kind == HHB_RATE_EXP && sigma > 0); }
+};
+
+struct GatePlan {
+  RatePlan a, b;
+  bool one_rcp = true;
+};
+
+struct Plan {
+  bool ok = false;
+  std::string why;
+  std::vector<Group> groups;
+  std::vector<GatePlan> gates;
+  double lo = 0, hi = 0;   // regular window
+};
+
+static bool inrange(double x) {
+  const double a = std::fabs(x);
+  return a >= kRangeLo && a <= kRangeHi && std::isfinite(x);
+}
+
+// exp argument of group g at v (what the kernel feeds ex2)
+static double group_E(const Group& g, double v) { return std::exp(-(v - g.vc) / g.b); }
+
+// emulate one rate at v in double, exactly as emitted: returns (n, d) of the
+// selected fraction or the plain value (d = 1, plain = true); ok &= ranges
+static void rate_nd(const RatePlan& r, const std::vector<Group>& G, double v, double& n, double& d, bool& ok) {
+  const double E = group_E(G[r.group], v);
+  ok = ok && inrange(E);
+  const double x = v - r.v0;
+  switch (r.kind) {
+    case HHB_RATE_EXP:
+      if (r.sigma > 0) { n = r.Sa * r.c * E; d = 1.0; }
+      else { n = r.Sa * r.c; d = E; }
+      break;
+    case HHB_RATE_SIGMOID:
+      if (r.sigma > 0) { n = r.Sa; d = r.c * E + 1.0; }
+      else { n = r.Sa * E; d = E + r.c; }
+      break;
+    default: {  // linoid
+      double thr;
+      if (r.sigma > 0) { n = r.Sa * x; d = 1.0 - r.c * E; thr = kSingThr; }
+      else { n = r.Sa * x * E; d = E - r.c; thr = kSingThr * r.c; }
+      if (std::fabs(d) < thr) {
+        const double u = x / r.b;
+        n = r.Sa * r.b * (1.0 + u * (0.5 + u / 12.0));
+        d = 1.0;
+      }
+    }
+  }
+  ok = ok && inrange(n) && inrange(d);
+}
+
+// reference value of a rate in double (dynamics.py:56-65), times Sa / a
+static double rate_ref(const RatePlan& r, double v) {
+  const double x = v - r.v0;
+  const double e = std::exp(-x / r.b);
+  const double a = r.Sa;
+  if (r.kind == HHB_RATE_EXP) return a * e;
+  if (r.kind == HHB_RATE_SIGMOID) return a / (1.0 + e);
+  if (std::fabs(x / r.b) < 1e-6) return a * r.b;
+  return a * x / (1.0 - e);
+}
+
+// is the merged gate computation valid at v (ranges + agreement with the
+// direct formulas)?
+static bool gate_ok(const GatePlan& g, const std::vector<Group>& G, double v, bool one_rcp) {
+  bool ok = true;
+  double na, da, nb, db;
+  rate_nd(g.a, G, v, na, da, ok);
+  rate_nd(g.b, G, v, nb, db, ok);
+  const double A = na * db, N = nb * da + A, D = da * db;
+  ok = ok && inrange(A) && inrange(N) && inrange(D);
+  if (one_rcp) ok = ok && inrange(N * D) && inrange(1.0 / (N * D)) && inrange(N / (N * D)) && inrange(D / (N * D));
+  else ok = ok && inrange(1.0 / N) && inrange(1.0 / D);
+  if (!ok) return false;
+  const double s = N / D, pinf = A / N;
+  const double ra = rate_ref(g.a, v), rb = rate_ref(g.b, v);
+  const double s_ref = ra + rb, pinf_ref = ra / s_ref;
+  return std::fabs(s - s_ref) <= 1e-6 * std::fabs(s_ref) && std::fabs(pinf - pinf_ref) <= 1e-6 * std::fabs(pinf_ref) + 1e-12;
+}
+
+// largest [lo, hi] around v_rest (grid 1/64 mV, up to +-400 mV) where pred holds
+template <typename F>
+static void window(double vr, F pred, double& lo, double& hi) {
+  const double h = 1.0 / 64;
+  lo = hi = vr;
+  if (!pred(vr)) { lo = hi = NAN; return; }
+  for (double v = vr; v >= vr - 400.0 && pred(v); v -= h) lo = v;
+  for (double v = vr; v <= vr + 400.0 && pred(v); v += h) hi = v;
+}
+
+static Plan plan_of(const hhb_params_t* P) {
+  Plan M;
+  const double S = P->rate_scale * (-P->dt * kLog2e);
+  if (!(S < 0.0) || !std::isfinite(S)) { M.why = "rate_scale * dt must be positive"; return M; }
+  // groups by |b|
+  auto group_of = [&](const hhb_rate_t& r) -> int {
+    for (size_t i = 0; i < M.groups.size(); ++i)
+      if (std::fabs(M.groups[i].b) == std::fabs(r.b)) return int(i);
+    Group g;
+    g.b = r.b;
+    g.vc = r.v0;
+    M.groups.push_back(g);
+    return int(M.groups.size() - 1);
+  };
+  for (int gi = 0; gi < P->n_gates; ++gi)
+    for (const hhb_rate_t* r : {&P->gates[gi].alpha, &P->gates[gi].beta}) {
+      if (r->a == 0.0 || !std::isfinite(r->a) || !std::isfinite(r->b) || !std::isfinite(r->v0)) {
+        M.why = "zero or non-finite rate parameter";
+        return M;
+      }
+      const int g = group_of(*r);
+      Group& G = M.groups[g];
+      ++G.members;
+      // a linoid centres the group on its own singularity (smallest exp
+      // argument, so the least rounding where 1 - e cancels)
+      if (r->kind == HHB_RATE_LINOID && G.members == 1) G.vc = r->v0;
+    }
+  for (int gi = 0; gi < P->n_gates; ++gi) {
+    GatePlan gp;
+    for (int w = 0; w < 2; ++w) {
+      const hhb_rate_t& r = w ? P->gates[gi].beta : P->gates[gi].alpha;
+      RatePlan rp;
+      rp.kind = r.kind;
+      rp.group = group_of(r);
+      const Group& G = M.groups[rp.group];
+      rp.sigma = (r.b == G.b) ? 1 : -1;
+      rp.c = rp.sigma > 0 ? std::exp((r.v0 - G.vc) / G.b) : std::exp((G.vc - r.v0) / G.b);
+      rp.Sa = r.a * S;
+      rp.v0 = r.v0;
+      rp.b = r.b;
+      rp.direct = r.kind == HHB_RATE_EXP && rp.sigma > 0 && G.members == 1;
+      (w ? gp.b : gp.a) = rp;
+    }
+    M.gates.push_back(gp);
+  }
+  const double vr = P->v_rest;
+  for (auto& g : M.gates) {
+    double lo1, hi1;
+    window(vr, [&](double v) { return gate_ok(g, M.groups, v, true); }, lo1, hi1);
+    g.one_rcp = lo1 <= vr - 60.0 && hi1 >= vr + 140.0;
+  }
+  window(vr, [&](double v) {
+    for (const auto& g : M.gates)
+      if (!gate_ok(g, M.groups, v, g.one_rcp)) return false;
+    return true;
+  }, M.lo, M.hi);
+  if (!(M.lo <= vr - 30.0 && M.hi >= vr + 100.0)) {
+    M.why = "merged-form window too narrow";
+    return M;
+  }
+  M.ok = true;
+  return M;
+}
+
+static bool disabled() {
+  const char* e = getenv("HHB_JIT_NOMERGE");
+  return e && e[0] && e[0] != '0';
+}
+
+// step_fwd_m(v, p[], cur) -> v' : the merged-form step (regular lanes only)
+static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan& M) {
+  std::string o;
+  const int NG = L.ng;
+  o += fmt("__device__ __forceinline__ bool regular(const float v) { return fabsf(__fsub_rn(v, %s)) < %s; }\n",
+           F(0.5 * (M.lo + M.hi)).c_str(), F(0.5 * (M.hi - M.lo)).c_str());
+  o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
+           NG > 0 ? NG : 1);
+  // shared exponentials (independent MUFU ops, issued back to back)
+  std::vector<int> direct_only(M.groups.size(), 1);
+  for (const auto& g : M.gates)
+    for (const RatePlan* r : {&g.a, &g.b})
+      if (!r->direct) direct_only[r->group] = 0;
+  for (size_t i = 0; i < M.groups.size(); ++i) {
+    if (direct_only[i]) continue;
+    const double K2 = -kLog2e / M.groups[i].b;
+    o += fmt("  const float E%d = ex2f_(__fmaf_rn(v, %s, %s));\n", int(i), F(K2).c_str(),
+             F(-M.groups[i].vc * K2).c_str());
+  }
+  o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
+                         : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
+  o += "  float eta = 1.0f;\n";
+  auto neg = [](double x, const std::string& e) { return x < 0 ? "(-" + e + ")" : e; };
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    const GatePlan& gp = M.gates[g];
+    o += fmt("  // gate %d (channel %d), exponent %d, %s reciprocal(s)\n  {\n", g, L.chan[g], G.exponent,
+             gp.one_rcp ? "one" : "two");
+    const std::string pg = fmt("p[%d]", g);
+    o += "  const float pk = " + pow_expr(pg, G.exponent) + ";\n";
+    o += L.first[g] ? "  eta = pk;\n" : "  eta = __fmul_rn(eta, pk);\n";
+    // each rate -> plain value <w>v or fraction <w>n / <w>d
+    for (int w = 0; w < 2; ++w) {
+      const RatePlan& r = w ? gp.b : gp.a;
+      const char* nm = w ? "b" : "a";
+      const std::string E = fmt("E%d", r.group);
+      if (r.kind == HHB_RATE_EXP && r.sigma > 0) {
+        if (r.direct) {
+          const double K2 = -kLog2e / r.b;
+          o += fmt("  const float %sv = %s;\n", nm,
+                   neg(r.Sa, fmt("ex2f_(__fmaf_rn(v, %s, %s))", F(K2).c_str(),
+                                 F(-r.v0 * K2 + std::log2(std::fabs(r.Sa))).c_str())).c_str());
+        } else {
+          o += fmt("  const float %sv = __fmul_rn(%s, %s);\n", nm, F(r.Sa * r.c).c_str(), E.c_str());
+        }
+        continue;
+      }
+      switch (r.kind) {
+        case HHB_RATE_EXP:  // sigma < 0
+          o += fmt("  const float %sn = %s;\n  const float %sd = %s;\n", nm, F(r.Sa * r.c).c_str(), nm, E.c_str());
+          break;
+        case HHB_RATE_SIGMOID:
+          if (r.sigma > 0)
+            o += fmt("  const float %sn = %s;\n  const float %sd = __fmaf_rn(%s, %s, 1.0f);\n", nm, F(r.Sa).c_str(),
+                     nm, F(r.c).c_str(), E.c_str());
+          else
+            o += fmt("  const float %sn = __fmul_rn(%s, %s);\n  const float %sd = __fadd_rn(%s, %s);\n", nm,
+                     F(r.Sa).c_str(), E.c_str(), nm, E.c_str(), F(r.c).c_str());
+          break;
+        default: {
+          o += fmt("  const float %sx = __fsub_rn(v, %s);\n", nm, F(r.v0).c_str());
+          std::string n0, d0;
+          double thr;
+          if (r.sigma > 0) {
+            n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), nm);
+            d0 = fmt("__fmaf_rn(%s, %s, 1.0f)", F(-r.c).c_str(), E.c_str());
+            thr = kSingThr;
+          } else {
+            n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), nm, E.c_str());
+            d0 = fmt("__fsub_rn(%s, %s)", E.c_str(), F(r.c).c_str());
+            thr = kSingThr * r.c;
+          }
+          o += fmt("  const float %sd0 = %s;\n", nm, d0.c_str());
+          o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm, nm, F(thr).c_str());
+          // a b (1 + u/2 + u^2/12), u = x / b, as a Horner form in x
+          o += fmt("  const float %sns = __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s);\n", nm, nm, nm,
+                   F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), F(r.Sa * r.b).c_str());
+          o += fmt("  const float %sn = %ssg ? %sns : %s;\n", nm, nm, nm, n0.c_str());
+          o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, nm);
+        }
+      }
+    }
+    const bool ra = gp.a.rational(), rb = gp.b.rational();
+    if (!ra && !rb) {
+      o += "  const float s = __fadd_rn(av, bv);\n";
+      o += "  const float pinf = __fmul_rn(av, rcpf_(s));\n";
+    } else {
+      if (ra && rb) {
+        o += "  const float A = __fmul_rn(an, bd);\n";
+        o += "  const float N = __fmaf_rn(bn, ad, A);\n";
+        o += "  const float D = __fmul_rn(ad, bd);\n";
+      } else if (ra) {
+        o += "  const float A = an;\n";
+        o += "  const float N = __fmaf_rn(bv, ad, an);\n";
+        o += "  const float D = ad;\n";
+      } else {
+        o += "  const float A = __fmul_rn(av, bd);\n";
+        o += "  const float N = __fmaf_rn(av, bd, bn);\n";
+        o += "  const float D = bd;\n";
+      }
+      if (gp.one_rcp) {
+        o += "  const float r = rcpf_(__fmul_rn(N, D));\n";
+        o += "  const float s = __fmul_rn(N, __fmul_rn(N, r));\n";
+        o += "  const float pinf = __fmul_rn(A, __fmul_rn(D, r));\n";
+      } else {
+        o += "  const float s = __fmul_rn(N, rcpf_(D));\n";
+        o += "  const float pinf = __fmul_rn(A, rcpf_(N));\n";
+      }
+    }
+    // s is already -dt * log2(e) * (alpha + beta)
+    o += "  const float dec = ex2f_(s);\n";
+    o += fmt("  %s = __fmaf_rn(__fsub_rn(%s, pinf), dec, pinf);\n", pg.c_str(), pg.c_str());
+    if (L.last[g])
+      o += fmt("  ion = __fmaf_rn(eta, __fmaf_rn(v, %s, %s), ion);\n", F(C.g_max).c_str(),
+               F(-C.g_max * C.e_rev).c_str());
+    o += "  }\n";
+  }
+  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n}\n", F(P->dt / P->c_m).c_str());
+  return o;
+}
+
+}  // namespace mg
+
 // Kernel bodies (parameterised by NG through the generated step functions).
 static const char* kPrelude = R"(
 typedef long long i64;
@@ -349,16 +678,16 @@ struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; f
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase; };
 struct PoissonTab { int size; float amp; float cdf[48]; };
-__device__ __forceinline__ uint4 philox(unsigned long long seed, i64 gj, i64 gq) {
+// Philox-4x32-10 with the key schedule precomputed on the host (one kernel
+// parameter per round key: LOP3 takes them straight from the constant bank)
+struct Keys { u32 k[20]; };
+__device__ __forceinline__ uint4 philox(const Keys& ks, i64 gj, i64 gq) {
   uint4 c = make_uint4(u32(gj), u32((unsigned long long)gj >> 32), u32(gq), u32((unsigned long long)gq >> 32));
-  uint2 k = make_uint2(u32(seed), u32(seed >> 32));
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const u32 hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
     const u32 hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
+    c = make_uint4(hi1 ^ c.y ^ ks.k[2 * r], lo1, hi0 ^ c.w ^ ks.k[2 * r + 1], lo0);
   }
   return c;
 }
@@ -435,13 +764,13 @@ __device__ __forceinline__ void store_vec(float* p, const float (&x)[VEC], bool 
 }
 template <int VEC, bool POIS>
 struct Stimulus {
-  __device__ __forceinline__ void at(const FwdArgs& a, const PoissonSmem& tab, i64 t, i64 n0, bool full,
-                                     float (&c)[VEC]) {
+  __device__ __forceinline__ void at(const FwdArgs& a, const Keys& ks, const PoissonSmem& tab, i64 t, i64 n0,
+                                     bool full, float (&c)[VEC]) {
     if (POIS) {
       const i64 gt = a.step_base + t;
       u32 w[VEC];
       if (VEC == 4) {  // host guarantees (nbase + n0) % 4 == 0
-        const uint4 r = philox(a.seed, (a.nbase + n0) >> 2, gt);
+        const uint4 r = philox(ks, (a.nbase + n0) >> 2, gt);
         w[0] = r.x;
         w[VEC > 1 ? 1 : 0] = r.y;
         w[VEC > 2 ? 2 : 0] = r.z;
@@ -450,7 +779,7 @@ struct Stimulus {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           const i64 gj = a.nbase + n0 + j;
-          const uint4 r = philox(a.seed, gj >> 2, gt);
+          const uint4 r = philox(ks, gj >> 2, gt);
           const int i = int(gj & 3);
           w[j] = i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w;
         }
@@ -472,7 +801,7 @@ struct Stimulus {
   }
 };
 template <int VEC, bool POIS>
-__device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab) {
+__device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab, const Keys& ks) {
   const int lane = threadIdx.x & 31;
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = tid * VEC;
@@ -485,19 +814,28 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   }
   float v[VEC];
   float p[VEC][NGX];
+  u32 valid = 0;
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
     const bool on = n0 + j < a.n;
+    valid |= u32(on) << j;
     v[j] = on ? a.v_in[n0 + j] : -65.0f;
 #pragma unroll
     for (int g = 0; g < NG; ++g) p[j][g] = on ? a.g_in[g * a.g_ld + n0 + j] : 0.5f;
   }
   i64 bad = LLMAX, ck_slot = 0, ck_count = 0;
+  // running output pointers (one 64-bit add per step instead of t * ld)
+  float* vo = a.v_out != nullptr ? a.v_out + n0 : nullptr;
+  u32* so = a.spk != nullptr ? a.spk + n0 / 32 : nullptr;
+  const bool spk_writer = lane % (32 / VEC) == 0 && n0 < a.n;
+  // loaded currents are prefetched one step ahead (HBM latency); the drawn
+  // stimulus is made at the top of its own step (no registers held across it)
   float cur[VEC];
-  if (a.steps > 0) stim.at(a, ps, 0, n0, full, cur);
+  if (!POIS && a.steps > 0) stim.at(a, ks, ps, 0, n0, full, cur);
   for (i64 t = 0; t < a.steps; ++t) {
     float nxt[VEC];
-    if (t + 1 < a.steps) stim.at(a, ps, t + 1, n0, full, nxt);
+    if (POIS) stim.at(a, ks, ps, t, n0, full, cur);
+    else if (t + 1 < a.steps) stim.at(a, ks, ps, t + 1, n0, full, nxt);
     if (a.ckpt != nullptr && ck_count == 0) {
       float* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       store_vec<VEC>(base, v, full, n0, a.n);
@@ -512,28 +850,31 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
       ck_count = a.ck_every;
     }
     --ck_count;
-    u32 nib = 0;
-    // one warp vote per step for all VEC neurons of every lane: the
-    // branch-free variant unless a neuron sits in a linoid's series region
-    bool near = false;
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) near = near || near_linoid(v[j]);
     float vn[VEC];
-    if (__any_sync(0xffffffffu, near)) {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_s(v[j], p[j], cur[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_f(v[j], p[j], cur[j]);
-    }
+    step_all<VEC>(v, p, cur, vn);
+    u32 nib = 0;
+    bool fin = true;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      nib |= u32((v[j] < THETA) && (vn[j] >= THETA) && (n0 + j < a.n)) << j;
-      if (!finitef_(vn[j]) && bad == LLMAX && n0 + j < a.n) bad = a.step_base + t;
+      nib |= u32((v[j] < THETA) && (vn[j] >= THETA)) << j;
+      fin = fin && finitef_(vn[j]);
       v[j] = vn[j];
     }
-    if (a.v_out != nullptr) store_vec<VEC>(a.v_out + t * a.v_ld, v, full, n0, a.n);
-    if (a.spk != nullptr) {
+    nib &= valid;
+    if (!fin && bad == LLMAX) {  // rare: locate the neuron (padding lanes never count)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j)
+        if (!finitef_(v[j]) && ((valid >> j) & 1u)) bad = a.step_base + t;
+    }
+    if (vo != nullptr) {
+      if (VEC == 4 && full) *reinterpret_cast<float4*>(vo) = make_float4(v[0], v[VEC > 1 ? 1 : 0], v[VEC > 2 ? 2 : 0], v[VEC > 3 ? 3 : 0]);
+      else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) vo[j] = v[j];
+      }
+      vo += a.v_ld;
+    }
+    if (so != nullptr) {
       u32 w;
       if (VEC == 1) {
         w = __ballot_sync(0xffffffffu, nib != 0);
@@ -542,10 +883,13 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
 #pragma unroll
         for (int o = 1; o < 32 / VEC; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
       }
-      if (lane % (32 / VEC) == 0 && n0 < a.n) a.spk[t * a.spk_ld + n0 / 32] = w;
+      if (spk_writer) *so = w;
+      so += a.spk_ld;
     }
+    if (!POIS) {
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
+      for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
+    }
   }
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
@@ -557,10 +901,10 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   }
   if (bad != LLMAX) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
 }
-extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, false>(a, t); }
-extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, false>(a, t); }
-extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v1(const FwdArgs a, const PoissonTab t) { fwd_body<1, true>(a, t); }
-extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v4(const FwdArgs a, const PoissonTab t) { fwd_body<4, true>(a, t); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v1(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<1, false>(a, t, k); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v4(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<4, false>(a, t, k); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v1(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<1, true>(a, t, k); }
+extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v4(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<4, true>(a, t, k); }
 
 __device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
   v = base[i];
@@ -664,19 +1008,75 @@ static std::string generate(const hhb_params_t* P) {
   src += fmt("#define THETA %s\n", F(P->v_theta).c_str());
   // occupancy knob for experiments: minimum resident 256-thread blocks per SM
   const char* mb = getenv("HHB_JIT_MINB");
-  // 4 resident 256-thread blocks (<= 64 registers) measured best for config 2
-  // on B200 (profiles/r1_variants.md); 1 lets ptxas take ~100+ registers
-  src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 4);
+  // merged step: 2 resident 256-thread blocks (<= 128 registers, no spills)
+  // measured best for config 2 on B200 (profiles/r1_variants.md: 1.49e11 vs
+  // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
+  src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
   src += emit_near_linoid(P);
   src += emit_forward_step(P, L, kFast);
   src += emit_forward_step(P, L, kSeries);
   src += emit_backward_step(P, L, kFast);
   src += emit_backward_step(P, L, kSeries);
-  // one-neuron dispatch: a warp vote picks the branch-free variant unless some
-  // lane is inside a linoid's series region this step
+  const mg::Plan M = mg::disabled() ? mg::Plan{} : mg::plan_of(P);
+  if (M.ok) {
+    // merged form on every regular lane; one warp vote per step sends the
+    // warp through the per-lane select only when some lane left the window
+    src += mg::emit_step(P, L, M);
+    src += R"(template <int VEC>
+__device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][NGX], const float (&cur)[VEC],
+                                         float (&vn)[VEC]) {
+  bool irr = false;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) irr = irr || !regular(v[j]);
+  if (__any_sync(0xffffffffu, irr)) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      float pm[NGX];
+#pragma unroll
+      for (int g = 0; g < NGX; ++g) pm[g] = p[j][g];
+      const float vm = step_fwd_m(v[j], pm, cur[j]);
+      const bool reg = regular(v[j]);
+      const float vs = step_fwd_s(v[j], p[j], cur[j]);
+      vn[j] = reg ? vm : vs;
+#pragma unroll
+      for (int g = 0; g < NGX; ++g) p[j][g] = reg ? pm[g] : p[j][g];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_m(v[j], p[j], cur[j]);
+  }
+}
+)";
+  } else {
+    // one warp vote per step for all VEC neurons of every lane: the
+    // branch-free variant unless a neuron sits in a linoid's series region
+    src += "// merged form off: " + M.why + "\n";
+    src += R"(template <int VEC>
+__device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][NGX], const float (&cur)[VEC],
+                                         float (&vn)[VEC]) {
+  bool near = false;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) near = near || near_linoid(v[j]);
+  if (__any_sync(0xffffffffu, near)) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_s(v[j], p[j], cur[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_f(v[j], p[j], cur[j]);
+  }
+}
+)";
+  }
+  // one-neuron step (the backward's segment recompute): same dispatch, so it
+  // reproduces the forward's states bit for bit
   src += fmt(
       "__device__ __forceinline__ float step_fwd(const float v, float (&p)[%d], const float cur) {\n"
-      "  return __any_sync(0xffffffffu, near_linoid(v)) ? step_fwd_s(v, p, cur) : step_fwd_f(v, p, cur);\n}\n",
+      "  float vv[1] = {v}, cc[1] = {cur}, vn[1];\n"
+      "  float pp[1][NGX];\n"
+      "#pragma unroll\n  for (int g = 0; g < NGX; ++g) pp[0][g] = p[g];\n"
+      "  step_all<1>(vv, pp, cc, vn);\n"
+      "#pragma unroll\n  for (int g = 0; g < NGX; ++g) p[g] = pp[0][g];\n"
+      "  return vn[0];\n}\n",
       L.ng > 0 ? L.ng : 1);
   src += fmt(
       "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[%d], "
@@ -716,6 +1116,7 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += std::to_string(dev);
   const char* mb = getenv("HHB_JIT_MINB");
   k += mb ? mb : "";
+  k += mg::disabled() ? "nomerge" : "";
   return k;
 }
 
@@ -785,7 +1186,13 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
   const int64_t blocks = (threads + tpb - 1) / tpb;
   FwdArgs<float> args = a;
   PoissonTab<float> tab = ptab ? *ptab : PoissonTab<float>{};
-  void* params[] = {&args, &tab};
+  // Philox-4x32-10 key schedule of a.seed (round r uses k + r * W)
+  uint32_t keys[20];
+  for (int r = 0; r < 10; ++r) {
+    keys[2 * r] = uint32_t(a.seed) + uint32_t(r) * 0x9E3779B9u;
+    keys[2 * r + 1] = uint32_t(a.seed >> 32) + uint32_t(r) * 0xBB67AE85u;
+  }
+  void* params[] = {&args, &tab, keys};
   CUfunction f = ptab ? (vec4 ? m->fwdp4 : m->fwdp1) : (vec4 ? m->fwd4 : m->fwd1);
   const CUresult r = jit::g_drv.launch(f, unsigned(blocks), 1, 1, unsigned(tpb), 1, 1, 0,
                                        reinterpret_cast<CUstream>(st), params, nullptr);

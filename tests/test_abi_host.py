@@ -178,3 +178,36 @@ def test_jit_source_compiles_for_sm100a(mk, tmp_path):
     r = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-O3", str(f),
                         "-o", str(tmp_path / "g.cubin")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
+
+
+def _mufu_ops(src: str, fn: str) -> int:
+    body = src[src.index("__device__ __forceinline__ float " + fn + "("):]
+    body = body[:body.index("\n}\n")]
+    return body.count("ex2f_(") + body.count("rcpf_(")
+
+
+@pytest.mark.parametrize("mk,tau,merged", [(lambda: DF.na_kdr_cal_kca_params(), 31, 20),
+                                           (lambda: DF.cortical_rs_params(), 16, 10),
+                                           (lambda: DF.squid_axon_params(), 15, 10)])
+def test_merged_step_mufu_budget(mk, tau, merged):
+    """jit.cu mg::plan_of: rates of equal |b| share one exp and each gate's
+    divisions share one reciprocal; the direct step keeps the reference's
+    transcendental count."""
+    src = nat.jit_source(mk())
+    assert "// merged form off" not in src
+    assert _mufu_ops(src, "step_fwd_m") == merged
+    assert _mufu_ops(src, "step_fwd_s") == tau
+
+
+def test_merged_step_window_and_fallback():
+    """The merged form is used only inside the voltage window where every
+    intermediate stays in float range; a table it cannot prove (a zero rate
+    amplitude) keeps the direct step."""
+    src = nat.jit_source(DF.na_kdr_cal_kca_params())
+    line = next(l for l in src.splitlines() if "bool regular(" in l)
+    assert "fabsf" in line
+    m = Dy.RateFn("sigmoid", 0.0, -20.0, 5.0)
+    ch = Dy.ChannelSpec("x", 1.0, -90.0, (Dy.GateSpec("c", m, Dy.RateFn("exp", 0.005, -65.0, 40.0), 1),))
+    p = Dy.HHParams(1.0, (ch, Dy.ChannelSpec("leak", 0.1, -70.0)), -70.0, 0.0, 0.01)
+    src = nat.jit_source(p)
+    assert "// merged form off" in src and "step_fwd_m" not in src

@@ -346,3 +346,34 @@ def test_jit_specialised_kernels_are_active(cuda):
     p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)
     Dy.simulate(p, np.full((3, 40), 5.0, dtype=np.float32))
     assert nat.jit_status() == "ok"
+
+
+def test_fp32_merged_step_irregular_lanes(cuda):
+    """The merged-form step (jit.cu mg::) runs on lanes inside its voltage
+    window; lanes outside it, and lanes sitting exactly on a linoid's
+    removable singularity, take the per-lane fallbacks.  Mix them in one warp:
+    every neuron must still meet the float32 contract against the float64
+    oracle, and the 4-neurons/thread and 1-neuron/thread kernels (different
+    warp groupings, so different warp votes) must agree bit for bit."""
+    p64 = DF.na_kdr_cal_kca_params(dt=0.01)
+    p = p64.with_(dtype=np.float32)
+    n_big = 148 * 32 * 4 + 64
+    rng = np.random.default_rng(11)
+    v0 = rng.uniform(-80.0, -60.0, size=n_big)
+    v0[::37] = -190.0                          # below the window (about -157 mV)
+    v0[5::37] = -175.0
+    sing = np.float32([-43.2, -16.2, -41.2, -27.0])   # linoid v0's: x == 0 exactly
+    v0[10:10 + 4 * 64:4] = np.tile(sing, 16)
+    v0 = v0.astype(np.float32).astype(np.float64)
+    g0 = np.repeat(np.asarray(O.steady_gates(p64, -70.3), dtype=np.float64)[:, None], n_big, axis=1)
+    i = (2.0 * rng.poisson(2.0, size=(400, n_big))).astype(np.float32)
+    s0 = Dy.NeuronState(torch.tensor(v0, dtype=torch.float32, device=cuda),
+                        torch.tensor(g0, dtype=torch.float32, device=cuda))
+    big = Dy.simulate(p, torch.from_numpy(i).to(cuda), state0=s0)
+    k = 1000
+    s1 = Dy.NeuronState(s0.v[:k].clone(), s0.gates[:, :k].clone())
+    small = Dy.simulate(p, torch.from_numpy(i[:, :k].copy()).to(cuda), state0=s1)
+    assert torch.equal(big.v_series[:, :k], small.v_series)
+    assert torch.equal(big.spike_series[:, :k], small.spike_series)
+    v_ref, s_ref = O.simulate(p64, i[:, :k].astype(np.float64), v0=v0[:k], g0=g0[:, :k])
+    check_fp32_contract(big.v_series[:, :k].cpu().numpy(), big.spike_series[:, :k].cpu().numpy(), v_ref, s_ref)

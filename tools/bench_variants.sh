@@ -7,7 +7,7 @@ i=0
 for spec in "$@"; do
   i=$((i+1))
   envs="${spec%%--*}"; flags=""
-  [[ "$spec" == *"--"* ]] && flags="--${spec#*--}"
+  [[ "$spec" == *"-- "* ]] && flags="${spec#*-- }"
   env $envs timeout 600 python bench.py --steps 2 --warmup 1 --no-extras $flags > gpurun_out/var$i.log 2>&1 \
     && summ gpurun_out/var$i.log "$spec" || { echo "variant $spec failed"; tail -5 gpurun_out/var$i.log; }
 done
