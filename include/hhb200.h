@@ -228,6 +228,18 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
              const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
              int32_t splits, float* workspace, void* stream);
 int64_t hhb_gemm_workspace(int64_t M, int64_t N, int32_t splits);
+/* bf16 generalisation of hhb_gemm for the layer gradients (learn.py:264-274):
+ *   D[M][ldd] = (A (+ A2)) . B^T (+ bias)
+ * HHB_GEMM_A_MN: A is stored MN-major, A[k][m] at A + k*lda + m (else
+ * A[m][k] at A + m*lda + k); HHB_GEMM_B_MN likewise for B[k][n].  A2 (same
+ * layout as A, or NULL) is accumulated into the same tensor-memory tile: with
+ * A/A2 the bf16 hi/lo halves of an fp32 operand the product carries ~16
+ * mantissa bits of it.  So dW = dI^T X and dX = dI W read dI, X and W in
+ * their natural row-major layouts, without transposed or split copies. */
+enum hhb_gemm_flags { HHB_GEMM_A_MN = 1, HHB_GEMM_B_MN = 2 };
+int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
+                const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
+                float* workspace, void* stream);
 /* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16,
  * 3: fp32 -> bf16 hi at [c][r] and lo = x - hi at [c][rows + r] (bf16x2 split),
  * 4: bf16 -> bf16 written to [c][r] and [c][rows + r].  Kinds 3 + 4 turn a

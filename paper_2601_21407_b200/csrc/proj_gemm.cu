@@ -27,7 +27,6 @@ namespace hhb {
 namespace gemm {
 
 constexpr int BM = 128;
-constexpr int STAGES = 4;
 constexpr int kThreads = 192;
 
 struct Args {
@@ -121,21 +120,54 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, bool TF32>
+// MN-major operand tile (bf16, SWIZZLE_128B): TMA boxes of 64 MN-elements x 64
+// K-rows (8 KB), placed 8 KB apart along MN.  Canonical UMMA MN-major layout
+// ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units: LBO = 8192 B between
+// 64-element MN chunks, SBO = 1024 B between 8-row K groups.
+__device__ __forceinline__ uint64_t smem_desc_mn(const void* p) {
+  const uint32_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= uint64_t((a & 0x3FFFF) >> 4);
+  d |= uint64_t(8192 >> 4) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+template <int BN, bool TF32, bool DUAL>
+struct Cfg {
+  static constexpr uint32_t kStageA = BM * 128;
+  static constexpr uint32_t kStageB = BN * 128;
+  static constexpr uint32_t kStage = kStageA * (DUAL ? 2 : 1) + kStageB;
+  static constexpr int kStages = (200 * 1024) / kStage > 6 ? 6 : (200 * 1024) / kStage;
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + 256;
+};
+
+// D = sum_s A_s . B^T over the K range of this split; A_s = A (and A2 when DUAL:
+// the bf16 hi and lo halves of an fp32 operand, accumulated into one TMEM
+// tile).  A_MN / B_MN: operand stored MN-major ([K][M] / [K][N], MN
+// contiguous) -- the natural layout of dI^T, X and W^T in the layer gradients,
+// so no transposed copy is ever made.
+template <int BN, bool TF32, bool A_MN, bool B_MN, bool DUAL>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_umma_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Args args) {
-  constexpr uint32_t kStageA = BM * 128;
-  constexpr uint32_t kStageB = BN * 128;
+    k_umma_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
+                const __grid_constant__ CUtensorMap tb, const Args args) {
+  using C = Cfg<BN, TF32, DUAL>;
+  constexpr int STAGES_ = C::kStages;
+  constexpr uint32_t kStageA = C::kStageA;
+  constexpr uint32_t kStageB = C::kStageB;
   constexpr int kUmmaK = TF32 ? 8 : 16;                // elements per MMA
   constexpr int kBK = TF32 ? 32 : 64;                  // elements per 128 B row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * kStageA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kStageB);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
+  uint8_t* sA = smem;                                   // [stage][A (, A2)]
+  uint8_t* sB = smem + STAGES_ * kStageA * (DUAL ? 2 : 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES_ * kStageB);
+  uint64_t* empty = full + STAGES_;
+  uint64_t* tmem_full = empty + STAGES_;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  constexpr uint32_t kAStride = kStageA * (DUAL ? 2 : 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
@@ -145,8 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    if (DUAL) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta2)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < STAGES_; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -166,27 +199,50 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
+        const int s = i % STAGES_;
+        const uint32_t ph = (i / STAGES_) & 1;
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], kStageA + kStageB);
+        mbar_expect_tx(&full[s], kStageA * (DUAL ? 2 : 1) + kStageB);
         const int32_t kx = (kb0 + i) * kBK;
-        tma_load_2d(&ta, &full[s], sA + s * kStageA, kx, int32_t(m0));
-        tma_load_2d(&tb, &full[s], sB + s * kStageB, kx, int32_t(n0));
+        uint8_t* a_dst = sA + s * kAStride;
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 64; ++c) {
+            tma_load_2d(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
+            if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
+          }
+        } else {
+          tma_load_2d(&ta, &full[s], a_dst, kx, int32_t(m0));
+          if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c)
+            tma_load_2d(&tb, &full[s], sB + s * kStageB + c * 8192, int32_t(n0) + 64 * c, kx);
+        } else {
+          tma_load_2d(&tb, &full[s], sB + s * kStageB, kx, int32_t(n0));
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = args.idesc;
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
+        const int s = i % STAGES_;
+        const uint32_t ph = (i / STAGES_) & 1;
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint8_t* a_src = sA + s * kAStride;
+        const uint8_t* b_src = sB + s * kStageB;
 #pragma unroll
         for (int k = 0; k < kBK / kUmmaK; ++k) {
-          const uint64_t ad = smem_desc(sA + s * kStageA + k * 32);
-          const uint64_t bd = smem_desc(sB + s * kStageB + k * 32);
-          umma<TF32>(tmem, ad, bd, args.idesc, (i > 0 || k > 0) ? 1u : 0u);
+          const uint64_t bd = B_MN ? smem_desc_mn(b_src + k * 2048) : smem_desc(b_src + k * 32);
+          const uint64_t ad = A_MN ? smem_desc_mn(a_src + k * 2048) : smem_desc(a_src + k * 32);
+          umma<TF32>(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          if (DUAL) {
+            const uint64_t ad2 = A_MN ? smem_desc_mn(a_src + kStageA + k * 2048) : smem_desc(a_src + kStageA + k * 32);
+            umma<TF32>(tmem, ad2, bd, idesc, 1u);
+          }
         }
         umma_commit(&empty[s]);
       }
@@ -367,23 +423,49 @@ static int make_map(CUtensorMap* map, bool tf32, const void* base, int64_t rows,
   return HHB_OK;
 }
 
-template <int BN, bool TF32>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Args& a, int splits, cudaStream_t st) {
-  const size_t smem = 1024 + size_t(STAGES) * (BM * 128 + BN * 128) + 256;
+// MN-major bf16 operand: global [K][ld] (MN contiguous), boxes of 64 x 64
+static int make_map_mn(CUtensorMap* map, const void* base, int64_t mn, int64_t k, int64_t ld) {
+  EncodeFn enc = encoder();
+  if (!enc) return fail(HHB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cuuint64_t(mn), cuuint64_t(k)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+  const cuuint32_t box[2] = {64u, 64u};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HHB_EINVAL, "cuTensorMapEncodeTiled rejected the MN-major operand layout");
+  return HHB_OK;
+}
+
+template <int BN, bool TF32, bool A_MN, bool B_MN, bool DUAL>
+static int launch(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tb, const Args& a, int splits,
+                  cudaStream_t st) {
+  const size_t smem = Cfg<BN, TF32, DUAL>::kSmem;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(k_umma_gemm<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr_err = cudaFuncSetAttribute(k_umma_gemm<BN, TF32, A_MN, B_MN, DUAL>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   });
   if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
   const dim3 grid{unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(splits)};
-  k_umma_gemm<BN, TF32><<<grid, kThreads, smem, st>>>(ta, tb, a);
+  k_umma_gemm<BN, TF32, A_MN, B_MN, DUAL><<<grid, kThreads, smem, st>>>(ta, ta2, tb, a);
   return cuda_check("k_umma_gemm launch");
 }
 
-static uint32_t instr_desc(bool tf32, int bn) {
+template <bool TF32, bool A_MN, bool B_MN, bool DUAL>
+static int launch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tb, const Args& a,
+                     int splits, cudaStream_t st) {
+  if (bn == 64) return launch<64, TF32, A_MN, B_MN, DUAL>(ta, ta2, tb, a, splits, st);
+  if (bn == 128) return launch<128, TF32, A_MN, B_MN, DUAL>(ta, ta2, tb, a, splits, st);
+  return launch<256, TF32, A_MN, B_MN, DUAL>(ta, ta2, tb, a, splits, st);
+}
+
+static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false) {
   const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
-  return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
 }  // namespace gemm
@@ -436,9 +518,67 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
     a.split_stride = 0;
     a.bias = bias;
   }
-  if (bn == 64) rc = tf32 ? launch<64, true>(ta, tb, a, splits, st) : launch<64, false>(ta, tb, a, splits, st);
-  else if (bn == 128) rc = tf32 ? launch<128, true>(ta, tb, a, splits, st) : launch<128, false>(ta, tb, a, splits, st);
-  else rc = tf32 ? launch<256, true>(ta, tb, a, splits, st) : launch<256, false>(ta, tb, a, splits, st);
+  rc = tf32 ? launch_bn<true, false, false, false>(bn, ta, ta, tb, a, splits, st)
+            : launch_bn<false, false, false, false>(bn, ta, ta, tb, a, splits, st);
+  if (rc || splits == 1) return rc;
+  k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+  return cuda_check("k_gemm_reduce launch");
+}
+
+int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
+                const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
+                float* workspace, void* stream) {
+  using namespace hhb::gemm;
+  const bool a_mn = flags & HHB_GEMM_A_MN, b_mn = flags & HHB_GEMM_B_MN, dual = A2 != nullptr;
+  if (flags & ~(HHB_GEMM_A_MN | HHB_GEMM_B_MN)) return fail(HHB_EINVAL, "gemm flags");
+  if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
+  if (M == 0 || N == 0) return HHB_OK;
+  if ((lda * 2) % 16 || (ldb * 2) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
+      reinterpret_cast<uintptr_t>(A2) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
+    return fail(HHB_EINVAL, "gemm operands need 16-byte aligned base and row pitch");
+  if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int kb_total = int((K + 63) / 64);
+  if (splits < 1) splits = 1;
+  if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
+  if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  CUtensorMap ta, ta2, tb;
+  int rc = a_mn ? make_map_mn(&ta, A, M, K, lda) : make_map(&ta, false, A, M, K, lda, BM);
+  if (rc) return rc;
+  if (dual && (rc = a_mn ? make_map_mn(&ta2, A2, M, K, lda) : make_map(&ta2, false, A2, M, K, lda, BM))) return rc;
+  if ((rc = b_mn ? make_map_mn(&tb, B, N, K, ldb) : make_map(&tb, false, B, N, K, ldb, bn))) return rc;
+  if (!dual) ta2 = ta;
+  Args a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.kb_total = kb_total;
+  a.kb_per_split = (kb_total + splits - 1) / splits;
+  a.idesc = instr_desc(false, bn, a_mn, b_mn);
+  if (splits > 1) {
+    a.D = workspace;
+    a.ldd = N;
+    a.split_stride = M * N;
+    a.bias = nullptr;
+  } else {
+    a.D = D;
+    a.ldd = ldd;
+    a.split_stride = 0;
+    a.bias = bias;
+  }
+#define HHB_GEMM_CASE(AM, BMN, DU)                                   \
+  if (a_mn == AM && b_mn == BMN && dual == DU)                       \
+    rc = launch_bn<false, AM, BMN, DU>(bn, ta, ta2, tb, a, splits, st);
+  HHB_GEMM_CASE(false, false, false)
+  HHB_GEMM_CASE(false, false, true)
+  HHB_GEMM_CASE(false, true, false)
+  HHB_GEMM_CASE(false, true, true)
+  HHB_GEMM_CASE(true, false, false)
+  HHB_GEMM_CASE(true, false, true)
+  HHB_GEMM_CASE(true, true, false)
+  HHB_GEMM_CASE(true, true, true)
+#undef HHB_GEMM_CASE
   if (rc || splits == 1) return rc;
   k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
   return cuda_check("k_gemm_reduce launch");

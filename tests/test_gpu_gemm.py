@@ -94,3 +94,57 @@ def test_transpose_cast_colsum(cuda):
     nat.check(lib.hhb_col_sum(333, 129, x.data_ptr(), 129, s.data_ptr(), scratch.data_ptr(), None), "s")
     torch.cuda.synchronize()
     assert torch.allclose(s, x.double().sum(0), rtol=1e-12, atol=1e-9)
+
+
+def gemm_ex(A, B, *, a_mn=False, b_mn=False, A2=None, bias=None, splits=1):
+    """D = (A (+A2)) B^T; A given as (M, K) (K-major) or (K, M) (a_mn), B as (N, K) or (K, N)."""
+    M = A.shape[1] if a_mn else A.shape[0]
+    K = A.shape[0] if a_mn else A.shape[1]
+    N = B.shape[1] if b_mn else B.shape[0]
+    D = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    lib = nat.load()
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
+    ws = torch.empty(max(1, ws_n), dtype=torch.float32, device=A.device)
+    flags = (1 if a_mn else 0) | (2 if b_mn else 0)
+    rc = lib.hhb_gemm_ex(flags, M, N, K, A.data_ptr(), None if A2 is None else A2.data_ptr(), A.stride(0),
+                         B.data_ptr(), B.stride(0), None if bias is None else bias.data_ptr(), D.data_ptr(), N,
+                         splits, ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    nat.check(rc, "hhb_gemm_ex")
+    return D
+
+
+@pytest.mark.parametrize("a_mn,b_mn,dual", [(a, b, d) for a in (False, True) for b in (False, True)
+                                            for d in (False, True)])
+@pytest.mark.parametrize("M,N,K,splits", [(1024, 784, 2560, 4), (300, 200, 136, 1), (128, 64, 64, 1)])
+def test_gemm_ex_layouts_and_dual_operand(cuda, a_mn, b_mn, dual, M, N, K, splits):
+    """MN-major operands (UMMA descriptors with LBO = 8 KB chunks) and the
+    dual-A accumulation against an fp64 product of the same bf16 values."""
+    g = torch.Generator(device=cuda).manual_seed(M + N + K + 2 * a_mn + b_mn)
+    Am = torch.randn((M, K), device=cuda, generator=g)
+    hi = Am.to(torch.bfloat16)
+    lo = (Am - hi.float()).to(torch.bfloat16)
+    Bm = torch.randn((N, K), device=cuda, generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device=cuda, generator=g)
+    def mn(x):   # (R, K) -> (K, R) view with a 16-byte aligned row pitch
+        r = x.shape[0]
+        buf = torch.zeros((x.shape[1], (r + 7) // 8 * 8), dtype=x.dtype, device=x.device)
+        buf[:, :r] = x.T
+        return buf[:, :r]
+
+    def km(x):
+        k = x.shape[1]
+        buf = torch.zeros((x.shape[0], (k + 7) // 8 * 8), dtype=x.dtype, device=x.device)
+        buf[:, :k] = x
+        return buf[:, :k]
+
+    A1 = mn(hi) if a_mn else km(hi)
+    A2 = (mn(lo) if a_mn else km(lo)) if dual else None
+    B1 = mn(Bm) if b_mn else km(Bm)
+    D = gemm_ex(A1, B1, a_mn=a_mn, b_mn=b_mn, A2=A2, bias=bias, splits=splits)
+    Aref = hi.double() + (lo.double() if dual else 0.0)
+    ref = Aref @ Bm.double().T + bias.double()
+    err = float((D.double() - ref).norm() / ref.norm())
+    assert err < 2e-6 * max(1.0, K / 1024), err
+    if dual:   # the pair carries ~16 mantissa bits of the fp32 operand
+        full = Am.double() @ Bm.double().T + bias.double()
+        assert float((D.double() - full).norm() / full.norm()) < 5e-5
