@@ -73,6 +73,15 @@ SIGNATURES = {
                             _vp, _i64,
                             _vp, _vp,
                             _i64, _vp, _vp]),
+    "hhb_backward_ex": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
+                               _vp, _i64, _i64,
+                               _vp, _i64, _i64, _vp,
+                               _vp, _i64, _vp, _i64,
+                               _vp, _vp, _i64,
+                               _vp, _i64,
+                               _vp, _vp,
+                               _i64, _vp,
+                               _vp, _vp, _i64, _vp, _vp]),
     "hhb_forward_poisson": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
                                    _vp, _vp, _i64, _vp, _vp,
                                    C.c_uint64, _i64, _dbl, _dbl,

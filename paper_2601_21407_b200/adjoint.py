@@ -105,8 +105,11 @@ class AdjointState:
 # ---------------------------------------------------------------------------
 
 def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_v, adj_g,
-              d_i=None, step_base=0):
-    """One hhb_backward launch; returns (d_i, d_params np.array[1+nch], first_bad)."""
+              d_i=None, step_base=0, want_d_i=True, split=None, d_sum=None):
+    """One hhb_backward(_ex) launch; returns (d_i or None, d_params np.array[1+nch], first_bad).
+
+    split = (hi, lo) uint16/bf16 [T][n] tensors receive dI as bf16 hi/lo halves
+    and d_sum [n] float accumulates the per-neuron sums of dI (SNN layer)."""
     dev = adj_v.device
     ng = params.n_gates
     nch = len(params.channels)
@@ -118,15 +121,16 @@ def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_
     parts = torch.empty(int(lib.hhb_backward_partials(n, dt)), dtype=torch.float64, device=dev)
     d_params = torch.zeros(1 + nch, dtype=torch.float64, device=dev)
     bad = torch.full((1,), -1, dtype=torch.int64, device=dev)
-    if d_i is None:
+    if d_i is None and want_d_i:
         d_i = torch.empty((T, n), dtype=adj_v.dtype, device=dev)
-    rc = lib.hhb_backward(
+    hi, lo = split if split is not None else (None, None)
+    rc = lib.hhb_backward_ex(
         C.byref(P), C.byref(S), dt, n, T, cur.data_ptr(), i_st, i_sn,
         ckpt.data_ptr(), K, n, D.ptr(seg),
         D.ptr(seed_v), n, D.ptr(seed_s), n,
         adj_v.data_ptr(), D.ptr(adj_g) if ng else None, n,
-        d_i.data_ptr(), n, d_params.data_ptr(), parts.data_ptr(),
-        step_base, bad.data_ptr(), D.stream())
+        D.ptr(d_i), n, d_params.data_ptr(), parts.data_ptr(),
+        step_base, bad.data_ptr(), D.ptr(hi), D.ptr(lo), n, D.ptr(d_sum), D.stream())
     nat.check(rc, "hhb_backward")
     return d_i, d_params, bad
 

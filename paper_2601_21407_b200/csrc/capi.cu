@@ -91,8 +91,13 @@ static int backward_t(const hhb_params_t* P, const hhb_surrogate_t* S, int64_t n
                       int64_t ck_every, int64_t ck_ld, void* seg, const void* seed_v,
                       int64_t sv_ld, const void* seed_s, int64_t ss_ld, void* adj_v, void* adj_g,
                       int64_t ag_ld, void* d_i, int64_t di_ld, double* d_params, double* partials,
-                      int64_t step_base, int64_t* first_bad, cudaStream_t st) {
+                      int64_t step_base, int64_t* first_bad, cudaStream_t st, void* di_hi = nullptr,
+                      void* di_lo = nullptr, int64_t dh_ld = 0, float* di_sum = nullptr) {
   BwdArgs<T> a{};
+  a.di_hi = static_cast<uint16_t*>(di_hi);
+  a.di_lo = static_cast<uint16_t*>(di_lo);
+  a.dh_ld = dh_ld;
+  a.di_sum = di_sum;
   a.n = n;
   a.steps = steps;
   a.i_ext = static_cast<const T*>(i_ext);
@@ -219,6 +224,22 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
                  void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
                  double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
                  void* stream) {
+  return hhb_backward_ex(params, surrogate, dtype, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every, ckpt_ld,
+                         seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v, adj_g, adj_g_ld, d_i, d_i_ld,
+                         d_params, partials, step_base, first_bad, nullptr, nullptr, 0, nullptr, stream);
+}
+
+int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
+                    int64_t n, int64_t n_steps, const void* i_ext, int64_t i_st, int64_t i_sn,
+                    const void* ckpt, int64_t ckpt_every, int64_t ckpt_ld, void* seg_buf,
+                    const void* seed_v, int64_t seed_v_ld, const void* seed_spk, int64_t seed_spk_ld,
+                    void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
+                    double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
+                    void* d_i_hi, void* d_i_lo, int64_t d_split_ld, float* d_i_sum, void* stream) {
+  if ((d_i_hi || d_i_lo || d_i_sum) && dtype != HHB_F32)
+    return fail(HHB_EINVAL, "split / summed dI outputs are float-only");
+  if ((d_i_hi != nullptr) != (d_i_lo != nullptr) || (d_i_hi && d_split_ld < n))
+    return fail(HHB_EINVAL, "d_i_hi and d_i_lo go together, with d_split_ld >= n");
   int rc = check_params(params);
   if (rc) return rc;
   if ((rc = check_dtype(dtype))) return rc;
@@ -235,7 +256,7 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
     return backward_t<float>(params, surrogate, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every,
                              ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                              adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base,
-                             first_bad, ST(stream));
+                             first_bad, ST(stream), d_i_hi, d_i_lo, d_split_ld, d_i_sum);
   return backward_t<double>(params, surrogate, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every,
                             ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                             adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base, first_bad,

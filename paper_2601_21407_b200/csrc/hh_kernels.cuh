@@ -63,7 +63,22 @@ struct BwdArgs {
   double* partials;
   int64_t step_base;
   long long* first_bad;
+  // layer outputs (float only; NULL = off): dI as bf16 hi + lo planes
+  // ([steps][dh_ld] each, hi = bf16(dI), lo = bf16(dI - hi)) for the bf16x2
+  // gradient GEMMs, and per-neuron sums of dI over the steps (+=) for d_bias
+  uint16_t* di_hi;
+  uint16_t* di_lo;
+  int64_t dh_ld;
+  float* di_sum;
 };
+
+__device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t h = (b + 0x7FFFu + ((b >> 16) & 1u)) & 0xFFFF0000u;
+  const uint32_t c = __float_as_uint(__fsub_rn(x, __uint_as_float(h)));
+  hi = uint16_t(h >> 16);
+  lo = uint16_t((c + 0x7FFFu + ((c >> 16) & 1u)) >> 16);
+}
 
 // ------------------------------------------------------------ vector I/O
 template <typename T, int VEC>
@@ -397,6 +412,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) acc[s] = 0.0;
   long long bad = -1;
+  double csum = 0.0;
 
   T d_v = on ? a.adj_v[ii] : T(0);
   T d_p[NGX];
@@ -433,6 +449,15 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
       const T ds = has_s ? __ldg(a.seed_s + t * a.ss_ld + ii) : T(0);
       const T di = step_backward<T, NG>(tb, sur, v, p, cur, d_v, d_p, ds, has_s, acc);
       if (on && a.d_i != nullptr) a.d_i[t * a.di_ld + ii] = di;
+      if constexpr (sizeof(T) == 4) {
+        if (on && a.di_hi != nullptr) {
+          uint16_t h, l;
+          split_bf16(float(di), h, l);
+          a.di_hi[t * a.dh_ld + ii] = h;
+          a.di_lo[t * a.dh_ld + ii] = l;
+        }
+        csum += double(di);
+      }
       bool ok = finite_(d_v);
 #pragma unroll
       for (int g = 0; g < NG; ++g) ok = ok && finite_(d_p[g]);
@@ -443,6 +468,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
     a.adj_v[ii] = d_v;
 #pragma unroll
     for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii] = d_p[g];
+    if (a.di_sum != nullptr) a.di_sum[ii] += float(csum);
   }
   if (bad >= 0) atomicMax(a.first_bad, bad);
 

@@ -263,84 +263,6 @@ static std::string emit_forward_step(const hhb_params_t* P, const Layout& L, Ser
   return o;
 }
 
-// adjoint of step_fwd (hh_step_backward, adjoint.py:116-188)
-static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, SeriesMode mode) {
-  std::string o;
-  const int NG = L.ng, NGX = NG > 0 ? NG : 1;
-  const double dtcm = P->dt / P->c_m;
-  o += fmt(
-      "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
-      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
-      "double (&acc)[%d]) {\n",
-      mode == kFast ? "f" : "s", NGX, NGX, kSlots);
-  o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
-                         : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
-  o += fmt("  float gsum = %s;\n", F(L.gl).c_str());
-  o += fmt("  float pk[%d], eta_c[%d];\n", NGX, NGX);
-  o += "  float eta = 1.0f;\n";
-  for (int g = 0; g < NG; ++g) {
-    const hhb_gate_t& G = P->gates[g];
-    const hhb_channel_t& C = P->channels[L.chan[g]];
-    o += fmt("  pk[%d] = %s;\n", g, pow_expr(fmt("p[%d]", g), G.exponent).c_str());
-    o += L.first[g] ? fmt("  eta = pk[%d];\n", g) : fmt("  eta = __fmul_rn(eta, pk[%d]);\n", g);
-    o += fmt("  eta_c[%d] = eta;\n", g);
-    if (L.last[g]) {
-      o += fmt("  ion = __fmaf_rn(__fmul_rn(eta, %s), __fsub_rn(v, %s), ion);\n", F(C.g_max).c_str(),
-               F(C.e_rev).c_str());
-      o += fmt("  gsum = __fmaf_rn(%s, eta, gsum);\n", F(C.g_max).c_str());
-    }
-  }
-  o += fmt("  const float vn = __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n", F(dtcm).c_str());
-  o += "  float g_vp = d_v;\n";
-  o += fmt("  if (has_s) g_vp = __fmaf_rn(d_spike, surrogate(sur, __fsub_rn(vn, %s)), g_vp);\n",
-           F(P->v_theta).c_str());
-  o += "  acc[0] += double(__fmul_rn(g_vp, __fsub_rn(cur, ion)));\n";
-  for (int g = 0; g < NG; ++g) {
-    if (!L.last[g]) continue;
-    const hhb_channel_t& C = P->channels[L.chan[g]];
-    o += fmt("  acc[%d] += double(__fmul_rn(__fmul_rn(g_vp, eta_c[%d]), __fsub_rn(v, %s)));\n", 1 + g, g,
-             F(C.e_rev).c_str());
-  }
-  for (size_t j = 0; j < L.leak_ch.size(); ++j)
-    o += fmt("  acc[%d] += double(__fmul_rn(g_vp, __fsub_rn(v, %s)));\n", 1 + kMaxGates + int(j),
-             F(P->channels[L.leak_ch[j]].e_rev).c_str());
-  o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
-  for (int g = 0; g < NG; ++g) {
-    const hhb_gate_t& G = P->gates[g];
-    const hhb_channel_t& C = P->channels[L.chan[g]];
-    o += fmt("  // gate %d\n  {\n  float a, b, da, db;\n", g);
-    std::string sa = "da", sb = "db";
-    emit_rate(o, G.alpha, P->rate_scale, "a", &sa, mode);
-    emit_rate(o, G.beta, P->rate_scale, "b", &sb, mode);
-    o += "  const float s = __fadd_rn(a, b);\n";
-    o += "  const float rs = rcpf_(s);\n";
-    o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
-    o += "  const float pinf = __fmul_rn(a, rs);\n";
-    o += "  const float dpinf = __fmul_rn(__fsub_rn(__fmul_rn(da, b), __fmul_rn(a, db)), __fmul_rn(rs, rs));\n";
-    o += fmt("  const float term = __fmaf_rn(dpinf, __fsub_rn(1.0f, e), __fmul_rn(__fsub_rn(p[%d], pinf), "
-             "__fmul_rn(__fmul_rn(%s, __fadd_rn(da, db)), e)));\n",
-             g, F(-P->dt).c_str());
-    o += "  const bool pos = s > 0.0f;\n";
-    o += fmt("  const float up = d_p[%d];\n", g);
-    o += "  dv_in = pos ? __fmaf_rn(up, term, dv_in) : dv_in;\n";
-    o += "  float dp = pos ? __fmul_rn(up, e) : up;\n";
-    if (G.exponent > 0) {
-      // d eta / d p = k p^(k-1) prod(other gates of the channel)
-      std::string der = fmt("__fmul_rn(%s, %s)", F(double(G.exponent)).c_str(),
-                            pow_expr(fmt("p[%d]", g), G.exponent - 1).c_str());
-      const hhb_channel_t& CC = P->channels[L.chan[g]];
-      for (int o2 = CC.gate_begin; o2 < CC.gate_begin + CC.gate_count; ++o2)
-        if (o2 != g) der = fmt("__fmul_rn(%s, pk[%d])", der.c_str(), o2);
-      o += fmt("  dp = __fmaf_rn(__fmul_rn(__fmul_rn(g_vp, %s), __fsub_rn(v, %s)), %s, dp);\n",
-               F(-dtcm * C.g_max).c_str(), F(C.e_rev).c_str(), der.c_str());
-    }
-    o += fmt("  d_p[%d] = dp;\n  }\n", g);
-  }
-  o += "  d_v = dv_in;\n";
-  o += fmt("  return __fmul_rn(g_vp, %s);\n}\n", F(dtcm).c_str());
-  return o;
-}
-
 // ------------------------------------------------------------ merged step
 // The MUFU pipe (16 ops/clk/SM) bounds the step above: config 2 needs 12 rate
 // exps, 6 decay exps and 13 reciprocals per neuron-step.  The merged form
@@ -462,6 +384,7 @@ static bool gate_ok(const GatePlan& g, const std::vector<Group>& G, double v, bo
   else ok = ok && inrange(1.0 / N) && inrange(1.0 / D);
   if (!ok) return false;
   const double s = N / D, pinf = A / N;
+  if (!(s < 0.0)) return false;   // scaled by -dt log2(e): the reference's s > 0 branch
   const double ra = rate_ref(g.a, v), rb = rate_ref(g.b, v);
   const double s_ref = ra + rb, pinf_ref = ra / s_ref;
   return std::fabs(s - s_ref) <= 1e-6 * std::fabs(s_ref) && std::fabs(pinf - pinf_ref) <= 1e-6 * std::fabs(pinf_ref) + 1e-12;
@@ -546,15 +469,9 @@ static bool disabled() {
   return e && e[0] && e[0] != '0';
 }
 
-// step_fwd_m(v, p[], cur) -> v' : the merged-form step (regular lanes only)
-static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan& M) {
+// shared exponentials (independent MUFU ops, issued back to back)
+static std::string emit_exps(const Plan& M) {
   std::string o;
-  const int NG = L.ng;
-  o += fmt("__device__ __forceinline__ bool regular(const float v) { return fabsf(__fsub_rn(v, %s)) < %s; }\n",
-           F(0.5 * (M.lo + M.hi)).c_str(), F(0.5 * (M.hi - M.lo)).c_str());
-  o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
-           NG > 0 ? NG : 1);
-  // shared exponentials (independent MUFU ops, issued back to back)
   std::vector<int> direct_only(M.groups.size(), 1);
   for (const auto& g : M.gates)
     for (const RatePlan* r : {&g.a, &g.b})
@@ -565,6 +482,183 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
     o += fmt("  const float E%d = ex2f_(__fmaf_rn(v, %s, %s));\n", int(i), F(K2).c_str(),
              F(-M.groups[i].vc * K2).c_str());
   }
+  return o;
+}
+
+// symbolic float expression that knows when it is identically zero (the
+// compiler may not fold x * 0.0f: x could be inf or NaN)
+struct X {
+  std::string e;
+  bool zero = false;
+};
+static X Z() { return X{"0.0f", true}; }
+static X V(const std::string& e) { return X{e, false}; }
+static X mulx(const X& a, const X& b) { return (a.zero || b.zero) ? Z() : V("__fmul_rn(" + a.e + ", " + b.e + ")"); }
+static X addx(const X& a, const X& b) {
+  if (a.zero) return b;
+  if (b.zero) return a;
+  return V("__fadd_rn(" + a.e + ", " + b.e + ")");
+}
+static X fmax_(const X& a, const X& b, const X& c) {
+  if (a.zero || b.zero) return c;
+  if (c.zero) return mulx(a, b);
+  return V("__fmaf_rn(" + a.e + ", " + b.e + ", " + c.e + ")");
+}
+static X negx(const X& a) { return a.zero ? a : V("(-" + a.e + ")"); }
+// bind an expression to a named const (keeps the emitted source readable)
+static X bind(std::string& o, const std::string& name, const X& x) {
+  if (x.zero) return x;
+  o += "  const float " + name + " = " + x.e + ";\n";
+  return V(name);
+}
+
+// one rate of the backward: value (v) and V-slope (v1) as a plain number, or
+// a fraction n / d with slopes n1, d1 (E' = -E / b_g)
+struct RateX {
+  bool rat;
+  X v, v1, n, d, n1, d1;
+};
+static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<Group>& G, const char* nm) {
+  RateX R;
+  const std::string E = fmt("E%d", r.group);
+  const double bg = G[r.group].b;
+  const std::string w(nm);
+  if (r.kind == HHB_RATE_EXP && r.sigma > 0) {
+    R.rat = false;
+    if (r.direct) {
+      const double K2 = -kLog2e / r.b;
+      R.v = bind(o, w + "v", V(std::string(r.Sa < 0 ? "(-" : "(") + fmt("ex2f_(__fmaf_rn(v, %s, %s)))", F(K2).c_str(),
+                   F(-r.v0 * K2 + std::log2(std::fabs(r.Sa))).c_str())));
+    } else {
+      R.v = bind(o, w + "v", mulx(V(F(r.Sa * r.c)), V(E)));
+    }
+    R.v1 = bind(o, w + "v1", mulx(R.v, V(F(-1.0 / r.b))));
+    return R;
+  }
+  R.rat = true;
+  switch (r.kind) {
+    case HHB_RATE_EXP:  // sigma < 0: n = Sa c, d = E
+      R.n = V(F(r.Sa * r.c));
+      R.d = V(E);
+      R.n1 = Z();
+      R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-1.0 / bg))));
+      break;
+    case HHB_RATE_SIGMOID:
+      if (r.sigma > 0) {
+        R.n = V(F(r.Sa));
+        R.d = bind(o, w + "d", V(fmt("__fmaf_rn(%s, %s, 1.0f)", F(r.c).c_str(), E.c_str())));
+        R.n1 = Z();
+        R.d1 = bind(o, w + "d1", V(fmt("__fmul_rn(%s, %s)", F(-r.c / bg).c_str(), E.c_str())));
+      } else {
+        R.n = bind(o, w + "n", mulx(V(F(r.Sa)), V(E)));
+        R.d = bind(o, w + "d", V(fmt("__fadd_rn(%s, %s)", E.c_str(), F(r.c).c_str())));
+        R.n1 = bind(o, w + "n1", mulx(R.n, V(F(-1.0 / bg))));
+        R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-1.0 / bg))));
+      }
+      break;
+    default: {
+      o += fmt("  const float %sx = __fsub_rn(v, %s);\n", nm, F(r.v0).c_str());
+      std::string n0, d0, n10, d10;
+      double thr;
+      if (r.sigma > 0) {
+        n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), nm);
+        d0 = fmt("__fmaf_rn(%s, %s, 1.0f)", F(-r.c).c_str(), E.c_str());
+        n10 = F(r.Sa);
+        d10 = fmt("__fmul_rn(%s, %s)", F(r.c / bg).c_str(), E.c_str());
+        thr = kSingThr;
+      } else {
+        n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), nm, E.c_str());
+        d0 = fmt("__fsub_rn(%s, %s)", E.c_str(), F(r.c).c_str());
+        n10 = fmt("__fmul_rn(__fmaf_rn(%sx, %s, %s), %s)", nm, F(-r.Sa / bg).c_str(), F(r.Sa).c_str(), E.c_str());
+        d10 = fmt("__fmul_rn(%s, %s)", E.c_str(), F(-1.0 / bg).c_str());
+        thr = kSingThr * r.c;
+      }
+      o += fmt("  const float %sd0 = %s;\n", nm, d0.c_str());
+      o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm, nm, F(thr).c_str());
+      o += fmt("  const float %sns = __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s);\n", nm, nm, nm,
+               F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), F(r.Sa * r.b).c_str());
+      o += fmt("  const float %sn = %ssg ? %sns : %s;\n", nm, nm, nm, n0.c_str());
+      o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, nm);
+      // slopes: d/dx of a b (1 + u/2 + u^2/12) = a (1/2 + u/6) in the series region
+      o += fmt("  const float %sn1 = %ssg ? __fmaf_rn(%sx, %s, %s) : %s;\n", nm, nm, nm,
+               F(r.Sa / (6.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), n10.c_str());
+      o += fmt("  const float %sd1 = %ssg ? 0.0f : %s;\n", nm, nm, d10.c_str());
+      R.n = V(w + "n");
+      R.d = V(w + "d");
+      R.n1 = V(w + "n1");
+      R.d1 = V(w + "d1");
+    }
+  }
+  return R;
+}
+
+// merged backward of one gate: emits s (scaled: the decay's exp2 argument),
+// e, pinf, and term = dpinf/dV (1 - e) + (p - pinf) (-dt)(a' + b') e
+// (adjoint.py:155-164); with s~ = -dt log2(e) s, (-dt)(a' + b') = ln2 s~'.
+static std::string emit_gate_bwd(const GatePlan& gp, const std::vector<Group>& G, int g) {
+  std::string o;
+  const RateX a = emit_rate_bwd(o, gp.a, G, "a");
+  const RateX b = emit_rate_bwd(o, gp.b, G, "b");
+  X s, s1, pinf, dpinf;
+  if (!a.rat && !b.rat) {
+    s = bind(o, "s", addx(a.v, b.v));
+    s1 = bind(o, "s1", addx(a.v1, b.v1));
+    const X rs = bind(o, "rs", V("rcpf_(s)"));
+    pinf = bind(o, "pinf", mulx(a.v, rs));
+    dpinf = bind(o, "dpinf", mulx(fmax_(a.v1, b.v, negx(mulx(a.v, b.v1))), mulx(rs, rs)));
+  } else {
+    X A, A1, N, N1, D, D1;
+    if (a.rat && b.rat) {
+      A = bind(o, "A", mulx(a.n, b.d));
+      A1 = bind(o, "A1", fmax_(a.n1, b.d, mulx(a.n, b.d1)));
+      N = bind(o, "N", fmax_(b.n, a.d, A));
+      N1 = bind(o, "N1", fmax_(b.n1, a.d, fmax_(b.n, a.d1, A1)));
+      D = bind(o, "D", mulx(a.d, b.d));
+      D1 = bind(o, "D1", fmax_(a.d1, b.d, mulx(a.d, b.d1)));
+    } else if (a.rat) {
+      A = a.n;
+      A1 = a.n1;
+      N = bind(o, "N", fmax_(b.v, a.d, a.n));
+      N1 = bind(o, "N1", fmax_(b.v1, a.d, fmax_(b.v, a.d1, a.n1)));
+      D = a.d;
+      D1 = a.d1;
+    } else {
+      A = bind(o, "A", mulx(a.v, b.d));
+      A1 = bind(o, "A1", fmax_(a.v1, b.d, mulx(a.v, b.d1)));
+      N = bind(o, "N", addx(A, b.n));
+      N1 = bind(o, "N1", addx(A1, b.n1));
+      D = b.d;
+      D1 = b.d1;
+    }
+    X iD, iN;
+    if (gp.one_rcp) {
+      const X r = bind(o, "r", V("rcpf_(" + mulx(N, D).e + ")"));
+      iD = bind(o, "iD", mulx(N, r));
+      iN = bind(o, "iN", mulx(D, r));
+    } else {
+      iD = bind(o, "iD", V("rcpf_(" + D.e + ")"));
+      iN = bind(o, "iN", V("rcpf_(" + N.e + ")"));
+    }
+    s = bind(o, "s", mulx(N, iD));
+    pinf = bind(o, "pinf", mulx(A, iN));
+    s1 = bind(o, "s1", mulx(fmax_(negx(s), D1, N1), iD));
+    dpinf = bind(o, "dpinf", mulx(fmax_(negx(pinf), N1, A1), iN));
+  }
+  o += "  const float e = ex2f_(s);\n";
+  const X t2 = mulx(mulx(V(fmt("__fsub_rn(p[%d], %s)", g, pinf.e.c_str())), mulx(V(F(std::log(2.0))), s1)), V("e"));
+  o += "  const float term = " + fmax_(dpinf, V("__fsub_rn(1.0f, e)"), t2).e + ";\n";
+  return o;
+}
+
+// step_fwd_m(v, p[], cur) -> v' : the merged-form step (regular lanes only)
+static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan& M) {
+  std::string o;
+  const int NG = L.ng;
+  o += fmt("__device__ __forceinline__ bool regular(const float v) { return fabsf(__fsub_rn(v, %s)) < %s; }\n",
+           F(0.5 * (M.lo + M.hi)).c_str(), F(0.5 * (M.hi - M.lo)).c_str());
+  o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
+           NG > 0 ? NG : 1);
+  o += emit_exps(M);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += "  float eta = 1.0f;\n";
@@ -670,6 +764,97 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
 
 }  // namespace mg
 
+// adjoint of step_fwd (hh_step_backward, adjoint.py:116-188)
+static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, SeriesMode mode,
+                                      const mg::Plan* M = nullptr) {
+  std::string o;
+  const int NG = L.ng, NGX = NG > 0 ? NG : 1;
+  const double dtcm = P->dt / P->c_m;
+  o += fmt(
+      "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
+      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
+      "float (&cb)[%d]) {\n",
+      M ? "m" : (mode == kFast ? "f" : "s"), NGX, NGX, kSlots);
+  if (M) o += mg::emit_exps(*M);
+  o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
+                         : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
+  o += fmt("  float gsum = %s;\n", F(L.gl).c_str());
+  o += fmt("  float pk[%d], eta_c[%d];\n", NGX, NGX);
+  o += "  float eta = 1.0f;\n";
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  pk[%d] = %s;\n", g, pow_expr(fmt("p[%d]", g), G.exponent).c_str());
+    o += L.first[g] ? fmt("  eta = pk[%d];\n", g) : fmt("  eta = __fmul_rn(eta, pk[%d]);\n", g);
+    o += fmt("  eta_c[%d] = eta;\n", g);
+    if (L.last[g]) {
+      o += fmt("  ion = __fmaf_rn(__fmul_rn(eta, %s), __fsub_rn(v, %s), ion);\n", F(C.g_max).c_str(),
+               F(C.e_rev).c_str());
+      o += fmt("  gsum = __fmaf_rn(%s, eta, gsum);\n", F(C.g_max).c_str());
+    }
+  }
+  o += fmt("  const float vn = __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n", F(dtcm).c_str());
+  o += "  float g_vp = d_v;\n";
+  o += fmt("  if (has_s) g_vp = __fmaf_rn(d_spike, surrogate(sur, __fsub_rn(vn, %s)), g_vp);\n",
+           F(P->v_theta).c_str());
+  o += "  cb[0] = __fmul_rn(g_vp, __fsub_rn(cur, ion));\n";
+  for (int g = 0; g < NG; ++g) {
+    if (!L.last[g]) continue;
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  cb[%d] = __fmul_rn(__fmul_rn(g_vp, eta_c[%d]), __fsub_rn(v, %s));\n", 1 + g, g,
+             F(C.e_rev).c_str());
+  }
+  for (size_t j = 0; j < L.leak_ch.size(); ++j)
+    o += fmt("  cb[%d] = __fmul_rn(g_vp, __fsub_rn(v, %s));\n", 1 + kMaxGates + int(j),
+             F(P->channels[L.leak_ch[j]].e_rev).c_str());
+  o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
+  for (int g = 0; g < NG; ++g) {
+    const hhb_gate_t& G = P->gates[g];
+    const hhb_channel_t& C = P->channels[L.chan[g]];
+    o += fmt("  // gate %d\n  {\n", g);
+    if (M) {
+      // merged form: s, p_inf, their V-slopes from the fractions; every lane
+      // here has s > 0 (checked over the window), so no zero-rate branch
+      o += mg::emit_gate_bwd(M->gates[g], M->groups, g);
+      o += fmt("  const float up = d_p[%d];\n", g);
+      o += "  dv_in = __fmaf_rn(up, term, dv_in);\n";
+      o += "  float dp = __fmul_rn(up, e);\n";
+    } else {
+    o += "  float a, b, da, db;\n";
+    std::string sa = "da", sb = "db";
+    emit_rate(o, G.alpha, P->rate_scale, "a", &sa, mode);
+    emit_rate(o, G.beta, P->rate_scale, "b", &sb, mode);
+    o += "  const float s = __fadd_rn(a, b);\n";
+    o += "  const float rs = rcpf_(s);\n";
+    o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
+    o += "  const float pinf = __fmul_rn(a, rs);\n";
+    o += "  const float dpinf = __fmul_rn(__fsub_rn(__fmul_rn(da, b), __fmul_rn(a, db)), __fmul_rn(rs, rs));\n";
+    o += fmt("  const float term = __fmaf_rn(dpinf, __fsub_rn(1.0f, e), __fmul_rn(__fsub_rn(p[%d], pinf), "
+             "__fmul_rn(__fmul_rn(%s, __fadd_rn(da, db)), e)));\n",
+             g, F(-P->dt).c_str());
+    o += "  const bool pos = s > 0.0f;\n";
+    o += fmt("  const float up = d_p[%d];\n", g);
+    o += "  dv_in = pos ? __fmaf_rn(up, term, dv_in) : dv_in;\n";
+    o += "  float dp = pos ? __fmul_rn(up, e) : up;\n";
+    }
+    if (G.exponent > 0) {
+      // d eta / d p = k p^(k-1) prod(other gates of the channel)
+      std::string der = fmt("__fmul_rn(%s, %s)", F(double(G.exponent)).c_str(),
+                            pow_expr(fmt("p[%d]", g), G.exponent - 1).c_str());
+      const hhb_channel_t& CC = P->channels[L.chan[g]];
+      for (int o2 = CC.gate_begin; o2 < CC.gate_begin + CC.gate_count; ++o2)
+        if (o2 != g) der = fmt("__fmul_rn(%s, pk[%d])", der.c_str(), o2);
+      o += fmt("  dp = __fmaf_rn(__fmul_rn(__fmul_rn(g_vp, %s), __fsub_rn(v, %s)), %s, dp);\n",
+               F(-dtcm * C.g_max).c_str(), F(C.e_rev).c_str(), der.c_str());
+    }
+    o += fmt("  d_p[%d] = dp;\n  }\n", g);
+  }
+  o += "  d_v = dv_in;\n";
+  o += fmt("  return __fmul_rn(g_vp, %s);\n}\n", F(dtcm).c_str());
+  return o;
+}
+
+
 // Kernel bodies (parameterised by NG through the generated step functions).
 static const char* kPrelude = R"(
 typedef long long i64;
@@ -730,7 +915,17 @@ struct PoissonSmem {
 };
 struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
   float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
-  i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad; };
+  i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad;
+  unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; };
+__device__ __forceinline__ void split_bf16(float x, unsigned short& hi, unsigned short& lo) {
+  // round-to-nearest-even bf16 of x, then of the remainder x - hi (exact in fp32)
+  const u32 b = __float_as_uint(x);
+  const u32 h = (b + 0x7FFFu + ((b >> 16) & 1u)) & 0xFFFF0000u;
+  const float r = __fsub_rn(x, __uint_as_float(h));
+  const u32 c = __float_as_uint(r);
+  hi = (unsigned short)(h >> 16);
+  lo = (unsigned short)((c + 0x7FFFu + ((c >> 16) & 1u)) >> 16);
+}
 struct Sur { int kind; float w, inv_w, k2, half_inv_w; };
 #define LLMAX 0x7fffffffffffffffLL
 __device__ __forceinline__ float ex2f_(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
@@ -923,6 +1118,11 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
   double acc[SLOTS];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) acc[s] = 0.0;
+  float accf[SLOTS];
+  cb_zero(accf);
+  int nf = 0;
+  double csum = 0.0;
+  float csumf = 0.0f;
   i64 bad = -1;
   float d_v = on ? a.adj_v[ii] : 0.0f;
   float d_p[NGX];
@@ -932,6 +1132,13 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
   const i64 nseg = (a.steps + K - 1) / K;
   const i64 sstride = (1 + NG) * a.ck_ld;
   const bool has_s = a.seed_s != nullptr;
+  // per-thread column bases; rows are reached by t * stride
+  const float* ib = a.i_ext + ii * a.i_sn;
+  const float* svb = a.seed_v != nullptr ? a.seed_v + ii : nullptr;
+  const float* ssb = has_s ? a.seed_s + ii : nullptr;
+  float* dib = (on && a.d_i != nullptr) ? a.d_i + ii : nullptr;
+  unsigned short* dhb = (on && a.di_hi != nullptr) ? a.di_hi + ii : nullptr;
+  unsigned short* dlb = (on && a.di_lo != nullptr) ? a.di_lo + ii : nullptr;
   for (i64 seg = nseg - 1; seg >= 0; --seg) {
     const i64 lo = seg * K;
     const i64 hi = (lo + K < a.steps) ? lo + K : a.steps;
@@ -939,31 +1146,53 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
     float v, p[NGX];
     load_state(ck, a.ck_ld, ii, v, p);
     if (K > 1) {
+      const float* ip = ib + lo * a.i_st;
+      float* sp = a.seg + sstride;
       for (i64 t = lo; t < hi - 1; ++t) {
-        const float cur = __ldg(a.i_ext + t * a.i_st + ii * a.i_sn);
+        const float cur = __ldg(ip);
+        ip += a.i_st;
         v = step_fwd(v, p, cur);
-        if (on) store_state(a.seg + (t + 1 - lo) * sstride, a.ck_ld, ii, v, p);
+        if (on) store_state(sp, a.ck_ld, ii, v, p);
+        sp += sstride;
       }
     }
     // operands of step t are loaded while step t+1 (the previous iteration)
     // computes: state (K == 1: checkpoint row; else the recomputed segment),
     // current and seeds -- software pipelining of the long-latency loads
-    if (K == 1) load_state(a.ckpt + (hi - 1) * sstride, a.ck_ld, ii, v, p);
-    float cur = __ldg(a.i_ext + (hi - 1) * a.i_st + ii * a.i_sn);
-    float sv = a.seed_v != nullptr ? __ldg(a.seed_v + (hi - 1) * a.sv_ld + ii) : 0.0f;
-    float ds = has_s ? __ldg(a.seed_s + (hi - 1) * a.ss_ld + ii) : 0.0f;
+    const float* rp = (K == 1) ? a.ckpt + (hi - 1) * sstride : a.seg + (hi - 1 - lo) * sstride;
+    if (K == 1) load_state(rp, a.ck_ld, ii, v, p);
+    const float* ip = ib + (hi - 1) * a.i_st;
+    float cur = __ldg(ip);
+    float sv = svb != nullptr ? __ldg(svb + (hi - 1) * a.sv_ld) : 0.0f;
+    float ds = has_s ? __ldg(ssb + (hi - 1) * a.ss_ld) : 0.0f;
     for (i64 t = hi - 1; t >= lo; --t) {
       float nv = 0.0f, np_[NGX], ncur = 0.0f, nsv = 0.0f, nds = 0.0f;
+      rp -= sstride;
+      ip -= a.i_st;
       if (t > lo) {
-        const float* src = (K == 1) ? a.ckpt + (t - 1) * sstride : (t - 1 == lo ? ck : a.seg + (t - 1 - lo) * sstride);
-        load_state(src, a.ck_ld, ii, nv, np_);
-        ncur = __ldg(a.i_ext + (t - 1) * a.i_st + ii * a.i_sn);
-        if (a.seed_v != nullptr) nsv = __ldg(a.seed_v + (t - 1) * a.sv_ld + ii);
-        if (has_s) nds = __ldg(a.seed_s + (t - 1) * a.ss_ld + ii);
+        load_state((K == 1 || t - 1 > lo) ? rp : ck, a.ck_ld, ii, nv, np_);
+        ncur = __ldg(ip);
+        if (svb != nullptr) nsv = __ldg(svb + (t - 1) * a.sv_ld);
+        if (has_s) nds = __ldg(ssb + (t - 1) * a.ss_ld);
       }
       d_v = __fadd_rn(d_v, sv);
-      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, has_s, acc);
-      if (on && a.d_i != nullptr) a.d_i[t * a.di_ld + ii] = di;
+      float cb[SLOTS];
+      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, has_s, cb);
+      cb_add(accf, cb);
+      csumf = __fadd_rn(csumf, di);
+      if (++nf == 8) {
+        cb_flush(acc, accf);
+        csum += double(csumf);
+        csumf = 0.0f;
+        nf = 0;
+      }
+      if (dib != nullptr) dib[t * a.di_ld] = di;
+      if (dhb != nullptr) {
+        unsigned short h, l;
+        split_bf16(di, h, l);
+        dhb[t * a.dh_ld] = h;
+        dlb[t * a.dh_ld] = l;
+      }
       bool ok = finitef_(d_v);
 #pragma unroll
       for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[g]);
@@ -976,10 +1205,13 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
       ds = nds;
     }
   }
+  cb_flush(acc, accf);
+  csum += double(csumf);
   if (on) {
     a.adj_v[ii] = d_v;
 #pragma unroll
     for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii] = d_p[g];
+    if (a.di_sum != nullptr) a.di_sum[ii] += float(csum);
   }
   if (bad >= 0) atomicMax(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
   __shared__ double red[BWD_THREADS / 32][SLOTS];
@@ -1078,13 +1310,54 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
       "#pragma unroll\n  for (int g = 0; g < NGX; ++g) p[g] = pp[0][g];\n"
       "  return vn[0];\n}\n",
       L.ng > 0 ? L.ng : 1);
-  src += fmt(
-      "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[%d], "
-      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, double (&acc)[%d]) {\n"
-      "  return __any_sync(0xffffffffu, near_linoid(v))\n"
-      "      ? step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc)\n"
-      "      : step_bwd_f(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc);\n}\n",
-      L.ng > 0 ? L.ng : 1, L.ng > 0 ? L.ng : 1, kSlots);
+  // parameter-gradient contributions of one step: fp32 per step, added into
+  // fp32 partials that are flushed into fp64 every 8 steps (fixed order, so
+  // the sums do not depend on the checkpoint plan)
+  {
+    std::vector<int> used = {0};
+    for (int g = 0; g < L.ng; ++g)
+      if (L.last[g]) used.push_back(1 + g);
+    for (size_t j = 0; j < L.leak_ch.size(); ++j) used.push_back(1 + kMaxGates + int(j));
+    std::string add = "__device__ __forceinline__ void cb_add(float (&a)[SLOTS], const float (&c)[SLOTS]) {\n";
+    std::string fl = "__device__ __forceinline__ void cb_flush(double (&d)[SLOTS], float (&a)[SLOTS]) {\n";
+    std::string ze = "__device__ __forceinline__ void cb_zero(float (&a)[SLOTS]) {\n";
+    std::string se = "__device__ __forceinline__ void cb_sel(bool q, float (&a)[SLOTS], const float (&c)[SLOTS]) {\n";
+    for (int k : used) {
+      add += fmt("  a[%d] = __fadd_rn(a[%d], c[%d]);\n", k, k, k);
+      fl += fmt("  d[%d] += double(a[%d]); a[%d] = 0.0f;\n", k, k, k);
+      ze += fmt("  a[%d] = 0.0f;\n", k);
+      se += fmt("  a[%d] = q ? c[%d] : a[%d];\n", k, k, k);
+    }
+    src += add + "}\n" + fl + "}\n" + ze + "}\n" + se + "}\n";
+  }
+  const char* bwd_sig =
+      "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[NGX], "
+      "const float cur, float& d_v, float (&d_p)[NGX], const float d_spike, const bool has_s, float (&cb)[SLOTS])";
+  if (M.ok) {
+    src += emit_backward_step(P, L, kSeries, &M);
+    src += std::string(bwd_sig) + R"( {
+  if (__all_sync(0xffffffffu, regular(v))) return step_bwd_m(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
+  // some lane left the window: both forms, selected per lane
+  float dvm = d_v, dpm[NGX], cbm[SLOTS];
+#pragma unroll
+  for (int g = 0; g < NGX; ++g) dpm[g] = d_p[g];
+  const float dim = step_bwd_m(sur, v, p, cur, dvm, dpm, d_spike, has_s, cbm);
+  const float dis = step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
+  const bool reg = regular(v);
+  d_v = reg ? dvm : d_v;
+#pragma unroll
+  for (int g = 0; g < NGX; ++g) d_p[g] = reg ? dpm[g] : d_p[g];
+  cb_sel(reg, cb, cbm);
+  return reg ? dim : dis;
+}
+)";
+  } else {
+    src += std::string(bwd_sig) + R"( {
+  return __any_sync(0xffffffffu, near_linoid(v)) ? step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb)
+                                                 : step_bwd_f(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
+}
+)";
+  }
   src += kForwardBody;
   return src;
 }

@@ -102,6 +102,26 @@ def grad_input(dI: torch.Tensor, wb: torch.Tensor, k_in: int) -> torch.Tensor:
     return gemm(a, b, n2)
 
 
+def gemm_ex(flags: int, M: int, N: int, K: int, A: torch.Tensor, A2, lda: int, B: torch.Tensor, ldb: int,
+            splits: int | None = None) -> torch.Tensor:
+    """out[M][N] = (A + A2) . B^T with MN-major operands where flags say so (hhb_gemm_ex)."""
+    out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    lib = nat.load()
+    if splits is None:
+        bn = 64 if N <= 64 else (128 if N <= 128 else 256)
+        tiles = math.ceil(M / 128) * math.ceil(N / bn)
+        kb = math.ceil(K / 64)
+        splits = max(1, min(kb // 4, math.ceil(2 * 148 / tiles))) if tiles < 148 else 1
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
+    ws = torch.empty(ws_n, dtype=torch.float32, device=A.device) if ws_n else None
+    nat.check(lib.hhb_gemm_ex(flags, M, N, K, A.data_ptr(), D.ptr(A2), lda, B.data_ptr(), ldb, None,
+                              out.data_ptr(), N, splits, D.ptr(ws), _stream()), "hhb_gemm_ex")
+    return out
+
+
+A_MN, B_MN = 1, 2
+
+
 def col_sum(dI: torch.Tensor) -> torch.Tensor:
     M, N = dI.shape
     lib = nat.load()
@@ -152,12 +172,31 @@ class _HHLayerFn(torch.autograd.Function):
             sv = torch.zeros((T, n), dtype=torch.float32, device=cur.device)
         adj_v = torch.zeros(n, dtype=torch.float32, device=cur.device)
         adj_g = torch.zeros((p.n_gates, n), dtype=torch.float32, device=cur.device)
-        d_i, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v, adj_g)
+        direct = n_out % 8 == 0
+        if direct:
+            # dI leaves the BPTT kernel as bf16 hi/lo planes + per-neuron sums;
+            # the gradient GEMMs read them (and X, W) in place, MN-major
+            hi = torch.empty((T, n), dtype=torch.bfloat16, device=cur.device)
+            lo = torch.empty((T, n), dtype=torch.bfloat16, device=cur.device)
+            dsum = torch.zeros(n, dtype=torch.float32, device=cur.device)
+            _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
+                                          adj_g, want_d_i=False, split=(hi, lo), d_sum=dsum)
+        else:
+            d_i, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
+                                            adj_g)
         if layer.check_finite:
             b = int(gbad.item())
             if b >= 0:
                 raise GradientOverflowError("adjoint state became non-finite", b)
         layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
+        if direct:
+            # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
+            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, n_out, xb, xb.stride(0))
+            db = col_sum(dsum.view(B, n_out)).float()
+            # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
+            dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, n_out, wb, wb.stride(0)).view(T, B, k_in)
+                  if ctx.x_requires_grad else None)
+            return dX, dW, db, None
         dI = d_i.view(M, n_out)
         dW = grad_weight(dI, xb, k_in)
         db = col_sum(dI).float()

@@ -19,9 +19,11 @@ def nrel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("budget", [None, 4])
-def test_layer_matches_oracle_composition(cuda, budget):
-    T, B, k_in, n_out = 40, 3, 24, 8
+@pytest.mark.parametrize("budget,n_out", [(None, 8), (4, 8), (None, 10), (4, 16)])
+def test_layer_matches_oracle_composition(cuda, budget, n_out):
+    """n_out % 8 == 0 takes the split-dI path (bf16 hi/lo planes straight out of
+    the BPTT kernel into MN-major GEMMs); n_out = 10 the transposing path."""
+    T, B, k_in = 40, 3, 24
     torch.manual_seed(0)
     layer = HHLayer(k_in, n_out, DF.cortical_rs_params(dt=0.1), budget=budget, w_mean=0.6, w_std=0.5,
                     device=cuda)
