@@ -125,6 +125,14 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
                 void* ckpt, int64_t ckpt_every, int64_t ckpt_ld,
                 int64_t step_base, int64_t* first_bad, void* stream);
 
+/* hhb_forward plus spk_val[n_steps][spk_val_ld] (dtype of V, NULL = off): the
+ * spike flags as 0/1 values, the SNN layer's differentiable spike output,
+ * written by the forward kernel itself (no bitmap round trip). */
+int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                   const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
+                   const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
+                   uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
+                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream);
 /*
  * hhb_forward_poisson -- hhb_forward with the BASELINE config-2 stimulus
  * I[t][j] = amp * Poisson(lam) drawn inside the kernel (Philox-4x32-10 keyed by

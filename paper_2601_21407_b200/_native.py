@@ -65,6 +65,14 @@ SIGNATURES = {
                            _vp, _i64,
                            _vp, _i64, _i64,
                            _i64, _vp, _vp]),
+    "hhb_forward_ex": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
+                              _vp, _vp, _i64, _vp, _vp,
+                              _vp, _i64, _i64,
+                              _vp, _i64,
+                              _vp, _i64,
+                              _vp, _i64,
+                              _vp, _i64, _i64,
+                              _i64, _vp, _vp]),
     "hhb_backward": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
                             _vp, _i64, _i64,
                             _vp, _i64, _i64, _vp,

@@ -41,6 +41,8 @@ struct FwdArgs {
   long long* first_bad;
   uint64_t seed;    // fused Poisson stimulus (hhb_forward_poisson): Philox key
   int64_t nbase;    //   global id of neuron 0 of this launch
+  T* spk_val;       // optional spike flags as 0/1 values [steps][spkv_ld] (SNN layer output)
+  int64_t spkv_ld;
 };
 
 template <typename T>
@@ -363,6 +365,12 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
         for (int j = 0; j < VEC; ++j)
           if (n0 + j < a.n) row[n0 + j] = v[j];
       }
+    }
+    if (a.spk_val != nullptr) {
+      T* row = a.spk_val + t * a.spkv_ld;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j)
+        if (n0 + j < a.n) row[n0 + j] = spk[j] ? T(1) : T(0);
     }
     if (a.spk != nullptr) {
 #pragma unroll

@@ -861,7 +861,8 @@ typedef long long i64;
 typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
-  i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase; };
+  i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
+  float* spk_val; i64 spkv_ld; };
 struct PoissonTab { int size; float amp; float cdf[48]; };
 // Philox-4x32-10 with the key schedule precomputed on the host (one kernel
 // parameter per round key: LOP3 takes them straight from the constant bank)
@@ -1022,6 +1023,7 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
   // running output pointers (one 64-bit add per step instead of t * ld)
   float* vo = a.v_out != nullptr ? a.v_out + n0 : nullptr;
   u32* so = a.spk != nullptr ? a.spk + n0 / 32 : nullptr;
+  float* svo = a.spk_val != nullptr ? a.spk_val + n0 : nullptr;
   const bool spk_writer = lane % (32 / VEC) == 0 && n0 < a.n;
   // loaded currents are prefetched one step ahead (HBM latency); the drawn
   // stimulus is made at the top of its own step (no registers held across it)
@@ -1069,6 +1071,17 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab
       }
       vo += a.v_ld;
     }
+    if (svo != nullptr) {
+      float f[VEC];
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) f[j] = ((nib >> j) & 1u) ? 1.0f : 0.0f;
+      if (VEC == 4 && full) *reinterpret_cast<float4*>(svo) = make_float4(f[0], f[VEC > 1 ? 1 : 0], f[VEC > 2 ? 2 : 0], f[VEC > 3 ? 3 : 0]);
+      else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) svo[j] = f[j];
+      }
+      svo += a.spkv_ld;
+    }
     if (so != nullptr) {
       u32 w;
       if (VEC == 1) {
@@ -1101,6 +1114,9 @@ extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v4(const FwdA
 extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v1(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<1, true>(a, t, k); }
 extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v4(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<4, true>(a, t, k); }
 
+)";
+
+static const char* kBwdKernel = R"(
 __device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
   v = base[i];
 #pragma unroll
@@ -1111,7 +1127,23 @@ __device__ __forceinline__ void store_state(float* base, i64 ld, i64 i, float v,
 #pragma unroll
   for (int g = 0; g < NG; ++g) base[(1 + g) * ld + i] = p[g];
 }
-extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, const BwdArgs a) {
+// Reverse-sweep operand prefetch: each thread streams its own operands of
+// step t (state row, current, seeds) into a DEPTH-deep shared-memory ring with
+// 4-byte cp.async, DEPTH-1 steps ahead of the step it computes, so HBM latency
+// hides behind compute without holding the operands in registers.  The module
+// is specialised on which optional streams exist (BF_* below), so the sweep
+// carries no run-time tests; every stream advances by a running pointer.
+#define DEPTH 6
+#define NOPS (NG + 4)   // v, p[NG], cur, seed_v, seed_s
+#define RING_STRIDE (NOPS * BWD_THREADS)
+__device__ __forceinline__ void cpa4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((u32)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory"); }
+
+extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const Sur sur, const BwdArgs a) {
+  __shared__ float ring[DEPTH * RING_STRIDE];
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool on = i < a.n;
   const i64 ii = on ? i : 0;
@@ -1128,82 +1160,111 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
   float d_p[NGX];
 #pragma unroll
   for (int g = 0; g < NG; ++g) d_p[g] = on ? a.adj_g[g * a.ag_ld + ii] : 0.0f;
-  const i64 K = a.ck_every;
-  const i64 nseg = (a.steps + K - 1) / K;
+  const i64 K = BF_K1 ? 1 : a.ck_every;
   const i64 sstride = (1 + NG) * a.ck_ld;
-  const bool has_s = a.seed_s != nullptr;
-  // per-thread column bases; rows are reached by t * stride
+  i64 goff[NGX];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) goff[g] = (1 + g) * a.ck_ld;
   const float* ib = a.i_ext + ii * a.i_sn;
-  const float* svb = a.seed_v != nullptr ? a.seed_v + ii : nullptr;
-  const float* ssb = has_s ? a.seed_s + ii : nullptr;
-  float* dib = (on && a.d_i != nullptr) ? a.d_i + ii : nullptr;
-  unsigned short* dhb = (on && a.di_hi != nullptr) ? a.di_hi + ii : nullptr;
-  unsigned short* dlb = (on && a.di_lo != nullptr) ? a.di_lo + ii : nullptr;
+  const float* svb = BF_SV ? a.seed_v + ii : nullptr;
+  const float* ssb = BF_SS ? a.seed_s + ii : nullptr;
+  float* const ring_t = ring + threadIdx.x;
+  // K == 1: one stream over all steps; K > 1: one stream per recomputed segment
+  const i64 nseg = BF_K1 ? 1 : (a.steps + K - 1) / K;
   for (i64 seg = nseg - 1; seg >= 0; --seg) {
-    const i64 lo = seg * K;
-    const i64 hi = (lo + K < a.steps) ? lo + K : a.steps;
+    const i64 lo = BF_K1 ? 0 : seg * K;
+    const i64 hi = BF_K1 ? a.steps : ((lo + K < a.steps) ? lo + K : a.steps);
     const float* ck = a.ckpt + seg * sstride;
-    float v, p[NGX];
-    load_state(ck, a.ck_ld, ii, v, p);
-    if (K > 1) {
-      const float* ip = ib + lo * a.i_st;
+    if (!BF_K1) {
+      float v, p[NGX];
+      load_state(ck, a.ck_ld, ii, v, p);
       float* sp = a.seg + sstride;
+      const float* ip = ib + lo * a.i_st;
       for (i64 t = lo; t < hi - 1; ++t) {
-        const float cur = __ldg(ip);
+        v = step_fwd(v, p, __ldg(ip));
         ip += a.i_st;
-        v = step_fwd(v, p, cur);
         if (on) store_state(sp, a.ck_ld, ii, v, p);
         sp += sstride;
       }
     }
-    // operands of step t are loaded while step t+1 (the previous iteration)
-    // computes: state (K == 1: checkpoint row; else the recomputed segment),
-    // current and seeds -- software pipelining of the long-latency loads
-    const float* rp = (K == 1) ? a.ckpt + (hi - 1) * sstride : a.seg + (hi - 1 - lo) * sstride;
-    if (K == 1) load_state(rp, a.ck_ld, ii, v, p);
-    const float* ip = ib + (hi - 1) * a.i_st;
-    float cur = __ldg(ip);
-    float sv = svb != nullptr ? __ldg(svb + (hi - 1) * a.sv_ld) : 0.0f;
-    float ds = has_s ? __ldg(ssb + (hi - 1) * a.ss_ld) : 0.0f;
+    // issue pointers: operands of step tn (walk down from hi - 1)
+    const float* rq = BF_K1 ? a.ckpt + (hi - 1) * sstride + ii : a.seg + (hi - 1 - lo) * sstride + ii;
+    const float* iq = ib + (hi - 1) * a.i_st;
+    const float* vq = BF_SV ? svb + (hi - 1) * a.sv_ld : nullptr;
+    const float* sq = BF_SS ? ssb + (hi - 1) * a.ss_ld : nullptr;
+    i64 tn = hi - 1;
+    int wslot = 0;
+    auto issue = [&]() {
+      float* r = ring_t + wslot * RING_STRIDE;
+      const float* src = (!BF_K1 && tn == lo) ? ck + ii : rq;
+      cpa4(r, src);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) cpa4(r + (1 + g) * BWD_THREADS, src + goff[g]);
+      cpa4(r + (NG + 1) * BWD_THREADS, iq);
+      if (BF_SV) cpa4(r + (NG + 2) * BWD_THREADS, vq);
+      if (BF_SS) cpa4(r + (NG + 3) * BWD_THREADS, sq);
+    };
+    auto advance = [&]() {
+      --tn;
+      rq -= sstride;
+      iq -= a.i_st;
+      if (BF_SV) vq -= a.sv_ld;
+      if (BF_SS) sq -= a.ss_ld;
+      wslot = (wslot + 1 == DEPTH) ? 0 : wslot + 1;
+    };
+#pragma unroll
+    for (int k = 0; k < DEPTH - 1; ++k) {
+      if (tn >= lo) issue();
+      cpa_commit();
+      advance();
+    }
+    float* dib = (BF_DI && on) ? a.d_i + (hi - 1) * a.di_ld + ii : nullptr;
+    unsigned short* dhb = (BF_SPLIT && on) ? a.di_hi + (hi - 1) * a.dh_ld + ii : nullptr;
+    unsigned short* dlb = (BF_SPLIT && on) ? a.di_lo + (hi - 1) * a.dh_ld + ii : nullptr;
+    int rslot = 0;
     for (i64 t = hi - 1; t >= lo; --t) {
-      float nv = 0.0f, np_[NGX], ncur = 0.0f, nsv = 0.0f, nds = 0.0f;
-      rp -= sstride;
-      ip -= a.i_st;
-      if (t > lo) {
-        load_state((K == 1 || t - 1 > lo) ? rp : ck, a.ck_ld, ii, nv, np_);
-        ncur = __ldg(ip);
-        if (svb != nullptr) nsv = __ldg(svb + (t - 1) * a.sv_ld);
-        if (has_s) nds = __ldg(ssb + (t - 1) * a.ss_ld);
-      }
-      d_v = __fadd_rn(d_v, sv);
+      if (tn >= lo) issue();
+      cpa_commit();
+      advance();
+      cpa_wait();
+      const float* r = ring_t + rslot * RING_STRIDE;
+      rslot = (rslot + 1 == DEPTH) ? 0 : rslot + 1;
+      float v = r[0], p[NGX];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) p[g] = r[(1 + g) * BWD_THREADS];
+      const float cur = r[(NG + 1) * BWD_THREADS];
+      if (BF_SV) d_v = __fadd_rn(d_v, r[(NG + 2) * BWD_THREADS]);
+      const float ds = BF_SS ? r[(NG + 3) * BWD_THREADS] : 0.0f;
       float cb[SLOTS];
-      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, has_s, cb);
+      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, BF_SS, cb);
       cb_add(accf, cb);
-      csumf = __fadd_rn(csumf, di);
+      if (BF_SUM) csumf = __fadd_rn(csumf, di);
       if (++nf == 8) {
         cb_flush(acc, accf);
-        csum += double(csumf);
-        csumf = 0.0f;
+        if (BF_SUM) {
+          csum += double(csumf);
+          csumf = 0.0f;
+        }
         nf = 0;
       }
-      if (dib != nullptr) dib[t * a.di_ld] = di;
-      if (dhb != nullptr) {
+      if (BF_DI && on) {
+        *dib = di;
+        dib -= a.di_ld;
+      }
+      if (BF_SPLIT && on) {
         unsigned short h, l;
         split_bf16(di, h, l);
-        dhb[t * a.dh_ld] = h;
-        dlb[t * a.dh_ld] = l;
+        *dhb = h;
+        *dlb = l;
+        dhb -= a.dh_ld;
+        dlb -= a.dh_ld;
       }
       bool ok = finitef_(d_v);
 #pragma unroll
       for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[g]);
       if (!ok && bad < 0 && on) bad = a.step_base + t;
-      v = nv;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) p[g] = np_[g];
-      cur = ncur;
-      sv = nsv;
-      ds = nds;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   cb_flush(acc, accf);
   csum += double(csumf);
@@ -1211,7 +1272,7 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
     a.adj_v[ii] = d_v;
 #pragma unroll
     for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii] = d_p[g];
-    if (a.di_sum != nullptr) a.di_sum[ii] += float(csum);
+    if (BF_SUM) a.di_sum[ii] += float(csum);
   }
   if (bad >= 0) atomicMax(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
   __shared__ double red[BWD_THREADS / 32][SLOTS];
@@ -1232,7 +1293,10 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS) hh_bwd(const Sur sur, 
 }
 )";
 
-static std::string generate(const hhb_params_t* P) {
+// bwd_flags < 0: the forward module; >= 0: the backward module specialised
+// on BF_* (which optional streams the launch has); -2: both, for inspection
+enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32 };
+static std::string generate(const hhb_params_t* P, int bwd_flags = -2) {
   const Layout L = layout_of(P);
   std::string src = kPrelude;
   src += fmt("#define NG %d\n#define NGX %d\n#define SLOTS %d\n#define BWD_THREADS %d\n", L.ng,
@@ -1244,6 +1308,8 @@ static std::string generate(const hhb_params_t* P) {
   // measured best for config 2 on B200 (profiles/r1_variants.md: 1.49e11 vs
   // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
+  const char* bmb = getenv("HHB_JIT_BWD_MINB");
+  src += fmt("#define BWD_MINB %d\n", bmb ? atoi(bmb) : 1);
   src += emit_near_linoid(P);
   src += emit_forward_step(P, L, kFast);
   src += emit_forward_step(P, L, kSeries);
@@ -1358,7 +1424,15 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
 }
 )";
   }
-  src += kForwardBody;
+  if (bwd_flags == -1 || bwd_flags == -2) src += kForwardBody;
+  if (bwd_flags != -1) {
+    const int f = bwd_flags < 0 ? (BF_SV | BF_DI) : bwd_flags;
+    src += fmt("#define BF_SV %d\n#define BF_SS %d\n#define BF_DI %d\n#define BF_SPLIT %d\n#define BF_SUM %d\n"
+               "#define BF_K1 %d\n",
+               (f & BF_SV) ? 1 : 0, (f & BF_SS) ? 1 : 0, (f & BF_DI) ? 1 : 0, (f & BF_SPLIT) ? 1 : 0,
+               (f & BF_SUM) ? 1 : 0, (f & BF_K1) ? 1 : 0);
+    src += kBwdKernel;
+  }
   return src;
 }
 
@@ -1390,6 +1464,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   const char* mb = getenv("HHB_JIT_MINB");
   k += mb ? mb : "";
   k += mg::disabled() ? "nomerge" : "";
+  const char* bmb = getenv("HHB_JIT_BWD_MINB");
+  k += bmb ? std::string("b") + bmb : "";
   return k;
 }
 
@@ -1398,7 +1474,7 @@ static bool disabled() {
   return e && e[0] && e[0] != '0';
 }
 
-static Module* get_module(const hhb_params_t* P) {
+static Module* get_module(const hhb_params_t* P, int bwd_flags) {
   if (disabled()) return nullptr;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
@@ -1408,11 +1484,11 @@ static Module* get_module(const hhb_params_t* P) {
     g_status = "jit unavailable: " + (g_nv.ok ? g_drv.why : g_nv.why);
     return nullptr;
   }
-  const std::string key = key_of(P, dev);
+  const std::string key = key_of(P, dev) + "|" + std::to_string(bwd_flags);
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second.ok ? &it->second : nullptr;
   Module& m = g_cache[key];
-  const std::string src = generate(P);
+  const std::string src = generate(P, bwd_flags);
   nvrtcProgram prog;
   if (g_nv.create(&prog, src.c_str(), "hh_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     g_status = "nvrtcCreateProgram failed";
@@ -1435,9 +1511,13 @@ static Module* get_module(const hhb_params_t* P) {
   g_nv.cubin(prog, cubin.data());
   g_nv.destroy(&prog);
   CUmodule mod;
-  if (g_drv.load(&mod, cubin.data()) != CUDA_SUCCESS || g_drv.get(&m.fwd1, mod, "hh_fwd_v1") != CUDA_SUCCESS ||
-      g_drv.get(&m.fwd4, mod, "hh_fwd_v4") != CUDA_SUCCESS || g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") != CUDA_SUCCESS ||
-      g_drv.get(&m.fwdp4, mod, "hh_fwdp_v4") != CUDA_SUCCESS || g_drv.get(&m.bwd, mod, "hh_bwd") != CUDA_SUCCESS) {
+  bool loaded = g_drv.load(&mod, cubin.data()) == CUDA_SUCCESS;
+  if (loaded && bwd_flags < 0)
+    loaded = g_drv.get(&m.fwd1, mod, "hh_fwd_v1") == CUDA_SUCCESS && g_drv.get(&m.fwd4, mod, "hh_fwd_v4") == CUDA_SUCCESS &&
+             g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") == CUDA_SUCCESS &&
+             g_drv.get(&m.fwdp4, mod, "hh_fwdp_v4") == CUDA_SUCCESS;
+  if (loaded && bwd_flags >= 0) loaded = g_drv.get(&m.bwd, mod, "hh_bwd") == CUDA_SUCCESS;
+  if (!loaded) {
     g_status = "cuModuleLoadData / cuModuleGetFunction failed";
     return nullptr;
   }
@@ -1451,7 +1531,7 @@ static Module* get_module(const hhb_params_t* P) {
 // Returns true when the JIT kernel was launched (rc holds its status).
 bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTab<float>* ptab, bool vec4,
                  cudaStream_t st, int& rc) {
-  jit::Module* m = jit::get_module(P);
+  jit::Module* m = jit::get_module(P, -1);
   if (!m) return false;
   const int VEC = vec4 ? 4 : 1;
   const int64_t threads = (a.n + VEC - 1) / VEC;
@@ -1475,7 +1555,10 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
 
 bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs<float>& a, cudaStream_t st,
                   int& rc) {
-  jit::Module* m = jit::get_module(P);
+  using namespace jit;
+  const int flags = (a.seed_v ? BF_SV : 0) | (a.seed_s ? BF_SS : 0) | (a.d_i ? BF_DI : 0) |
+                    (a.di_hi ? BF_SPLIT : 0) | (a.di_sum ? BF_SUM : 0) | (a.ck_every == 1 ? BF_K1 : 0);
+  jit::Module* m = jit::get_module(P, flags);
   if (!m) return false;
   const int64_t blocks = bwd_blocks(a.n);
   DevSur<float> s = sur;

@@ -354,6 +354,16 @@ __global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64
   }
 }
 
+// 8 elements per thread: two 16-byte loads, one 16-byte store (16-byte aligned
+// src/dst, checked by the caller); the scalar kernel takes the rest
+__global__ void k_cast_bf16_v8(int64_t n8, const float4* src, uint4* dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 a = __ldg(src + 2 * i), b = __ldg(src + 2 * i + 1);
+    __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                           __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+    dst[i] = *reinterpret_cast<uint4*>(h);
+  }
+}
 __global__ void k_cast_bf16(int64_t n, const float* src, __nv_bfloat16* dst) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
@@ -617,8 +627,17 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
 
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {
   if (n <= 0) return HHB_OK;
-  hhb::gemm::k_cast_bf16<<<grid_1d(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      n, src, static_cast<__nv_bfloat16*>(dst));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t done = 0;
+  if (reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && n >= 8) {
+    const int64_t n8 = n / 8;
+    hhb::gemm::k_cast_bf16_v8<<<grid_1d(n8, 256), 256, 0, st>>>(n8, reinterpret_cast<const float4*>(src),
+                                                                  static_cast<uint4*>(dst));
+    done = n8 * 8;
+  }
+  if (done < n)
+    hhb::gemm::k_cast_bf16<<<grid_1d(n - done, 256), 256, 0, st>>>(n - done, src + done,
+                                                                    static_cast<__nv_bfloat16*>(dst) + done);
   return cuda_check("k_cast_bf16 launch");
 }
 

@@ -147,11 +147,8 @@ class _HHLayerFn(torch.autograd.Function):
         nck = (T + K - 1) // K
         ckpt = torch.empty((nck, 1 + p.n_gates, n), dtype=torch.float32, device=x.device)
         v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
-        bits = torch.empty((T, (n + 31) // 32), dtype=torch.int32, device=x.device)
-        _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, bits=bits, ckpt=ckpt, ckpt_every=K)
         spikes = torch.empty((T, n), dtype=torch.float32, device=x.device)
-        nat.check(nat.load().hhb_unpack_spikes_f32(bits.data_ptr(), bits.shape[1], T, n, spikes.data_ptr(), n,
-                                                   _stream()), "unpack")
+        _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
         if layer.check_finite:
             _raise_if_bad(bad)
         ctx.save_for_backward(xb, wb, cur, ckpt)
