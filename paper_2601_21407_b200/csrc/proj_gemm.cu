@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "hh_host.cuh"
@@ -297,6 +298,219 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- persistent
+// Persistent variant: one CTA per SM walks the tile list (tile = blockIdx.x,
+// + gridDim.x, ...).  The accumulator is double-buffered in tensor memory
+// (2 x BN columns), so the MMA warp starts tile i+1 while the epilogue warps
+// drain tile i; the epilogue stages 32x32 fp32 blocks in 128B-swizzled shared
+// memory and writes them with TMA bulk-tensor stores (full 128-byte lines,
+// asynchronous), instead of per-thread row stores.
+template <int BN, bool DUAL>
+struct PCfg {
+  static constexpr uint32_t kStageA = BM * 128;
+  static constexpr uint32_t kStageB = BN * 128;
+  static constexpr uint32_t kStage = kStageA * (DUAL ? 2 : 1) + kStageB;
+  static constexpr uint32_t kStaging = 4 * 2 * 32 * 32 * 4;   // 4 warps x 2 buffers x 32x32 fp32
+  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 6 ? 6 : int((225 * 1024 - kStaging) / kStage);
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 256;
+};
+
+struct PArgs {
+  int64_t M, N;
+  int m_tiles, n_tiles, splits, tiles;
+  int kb_per_split, kb_total;
+  uint32_t idesc;
+  const float* bias;   // only when splits == 1
+};
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
+                                             int32_t z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_umma_gemm_p(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
+                  const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap td, const PArgs args) {
+  using C = PCfg<BN, DUAL>;
+  constexpr int ST = C::kStages;
+  constexpr uint32_t kStageA = C::kStageA, kStageB = C::kStageB;
+  constexpr uint32_t kAStride = kStageA * (DUAL ? 2 : 1);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ST * kAStride;
+  float* stg = reinterpret_cast<float*>(sB + ST * kStageB);          // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::kStaging);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    if (DUAL) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&td)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(uint32_t(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+  const int per_split = args.m_tiles * args.n_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int it = 0;
+      for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
+        const int z = tile / per_split, r = tile % per_split;
+        const int64_t m0 = int64_t(r % args.m_tiles) * BM, n0 = int64_t(r / args.m_tiles) * BN;
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kAStride + kStageB);
+          const int32_t kx = kb * 64;
+          uint8_t* a_dst = sA + s * kAStride;
+          if (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) {
+              tma_load_2d(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
+              if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
+            }
+          } else {
+            tma_load_2d(&ta, &full[s], a_dst, kx, int32_t(m0));
+            if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d(&tb, &full[s], sB + s * kStageB + c * 8192, int32_t(n0) + 64 * c, kx);
+          } else {
+            tma_load_2d(&tb, &full[s], sB + s * kStageB, kx, int32_t(n0));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, local = 0;
+      for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x, ++local) {
+        const int z = tile / per_split;
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        const int b = local & 1;
+        mbar_wait(&tempty[b], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + uint32_t(b * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* a_src = sA + s * kAStride;
+          const uint8_t* b_src = sB + s * kStageB;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bd = B_MN ? smem_desc_mn(b_src + k * 2048) : smem_desc(b_src + k * 32);
+            const uint64_t ad = A_MN ? smem_desc_mn(a_src + k * 2048) : smem_desc(a_src + k * 32);
+            umma<false>(acc, ad, bd, args.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (DUAL) {
+              const uint64_t ad2 =
+                  A_MN ? smem_desc_mn(a_src + kStageA + k * 2048) : smem_desc(a_src + kStageA + k * 32);
+              umma<false>(acc, ad2, bd, args.idesc, 1u);
+            }
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[b]);
+      }
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quarter q = warp % 4
+    const int q = warp & 3;
+    float* my_stg = stg + (warp - 2) * 2 * 1024;
+    int local = 0, nstore = 0;
+    for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x, ++local) {
+      const int z = tile / per_split, r = tile % per_split;
+      const int64_t m0 = int64_t(r % args.m_tiles) * BM, n0 = int64_t(r / args.m_tiles) * BN;
+      const int kb0 = z * args.kb_per_split;
+      const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
+      const int b = local & 1;
+      mbar_wait(&tfull[b], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int32_t row0 = int32_t(m0 + q * 32);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (n0 + c0 >= args.N) break;
+        uint32_t rr[32];
+        if (any_k) {
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(b * BN + c0), rr);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = 0u;
+        }
+        float* buf = my_stg + (nstore & 1) * 1024;
+        // the store that last used this buffer must have finished reading it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        // row `lane` of the 32x32 block, 16-byte chunks XOR-swizzled by row % 8
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o;
+          const int64_t cb = n0 + c0 + 4 * j;
+          o.x = __uint_as_float(rr[4 * j + 0]);
+          o.y = __uint_as_float(rr[4 * j + 1]);
+          o.z = __uint_as_float(rr[4 * j + 2]);
+          o.w = __uint_as_float(rr[4 * j + 3]);
+          if (args.bias != nullptr) {
+            o.x += cb + 0 < args.N ? __ldg(args.bias + cb + 0) : 0.f;
+            o.y += cb + 1 < args.N ? __ldg(args.bias + cb + 1) : 0.f;
+            o.z += cb + 2 < args.N ? __ldg(args.bias + cb + 2) : 0.f;
+            o.w += cb + 3 < args.N ? __ldg(args.bias + cb + 3) : 0.f;
+          }
+          *reinterpret_cast<float4*>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&td, buf, int32_t(n0 + c0), row0, z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++nstore;
+      }
+      // all TMEM reads of this accumulator are complete (tcgen05.ld waited)
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(2 * BN)));
+  }
+}
+
 // fixed-order split-K reduction (+ bias)
 __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits, int64_t split_stride,
                               const float* bias, float* D, int64_t ldd) {
@@ -472,6 +686,57 @@ static int launch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& ta2, cons
   return launch<256, TF32, A_MN, B_MN, DUAL>(ta, ta2, tb, a, splits, st);
 }
 
+// D (fp32) as a 3-D tensor {N, M, splits}: 32x32 store boxes, 128B swizzle,
+// clipped at the edges of each split slice
+static int make_map_d(CUtensorMap* map, float* base, int64_t M, int64_t N, int64_t ldd, int splits) {
+  EncodeFn enc = encoder();
+  if (!enc) return fail(HHB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {cuuint64_t(N), cuuint64_t(M), cuuint64_t(splits)};
+  const cuuint64_t strides[2] = {cuuint64_t(ldd) * 4, cuuint64_t(ldd) * 4 * cuuint64_t(M)};
+  const cuuint32_t box[3] = {32u, 32u, 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HHB_EINVAL, "cuTensorMapEncodeTiled rejected the output layout");
+  return HHB_OK;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
+static int launch_p(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tb, const CUtensorMap& td,
+                    const PArgs& a, cudaStream_t st) {
+  const size_t smem = PCfg<BN, DUAL>::kSmem;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_umma_gemm_p<BN, A_MN, B_MN, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem));
+  });
+  if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
+  const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
+  k_umma_gemm_p<BN, A_MN, B_MN, DUAL><<<grid, kThreads, smem, st>>>(ta, ta2, tb, td, a);
+  return cuda_check("k_umma_gemm_p launch");
+}
+
+template <bool A_MN, bool B_MN, bool DUAL>
+static int launch_p_bn(int bn, const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tb,
+                       const CUtensorMap& td, const PArgs& a, cudaStream_t st) {
+  if (bn == 64) return launch_p<64, A_MN, B_MN, DUAL>(ta, ta2, tb, td, a, st);
+  if (bn == 128) return launch_p<128, A_MN, B_MN, DUAL>(ta, ta2, tb, td, a, st);
+  return launch_p<256, A_MN, B_MN, DUAL>(ta, ta2, tb, td, a, st);
+}
+
 static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false) {
   const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
@@ -493,6 +758,7 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
   using namespace hhb::gemm;
   const bool tf32 = in_kind == HHB_GEMM_TF32;
   if (in_kind != HHB_GEMM_BF16 && in_kind != HHB_GEMM_TF32) return fail(HHB_EINVAL, "in_kind");
+  if (!tf32) return hhb_gemm_ex(0, M, N, K, A, nullptr, lda, B, ldb, bias, D, ldd, splits, workspace, stream);
   if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
   if (M == 0 || N == 0) return HHB_OK;
   const int eb = tf32 ? 4 : 2;
@@ -559,6 +825,38 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   if (dual && (rc = a_mn ? make_map_mn(&ta2, A2, M, K, lda) : make_map(&ta2, false, A2, M, K, lda, BM))) return rc;
   if ((rc = b_mn ? make_map_mn(&tb, B, N, K, ldb) : make_map(&tb, false, B, N, K, ldb, bn))) return rc;
   if (!dual) ta2 = ta;
+  float* dst = splits > 1 ? workspace : D;
+  const int64_t dld = splits > 1 ? N : ldd;
+  if (dld % 4 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && !getenv("HHB_GEMM_NONPERSISTENT")) {
+    CUtensorMap td;
+    if ((rc = make_map_d(&td, dst, M, N, dld, splits))) return rc;
+    PArgs pa{};
+    pa.M = M;
+    pa.N = N;
+    pa.m_tiles = int((M + BM - 1) / BM);
+    pa.n_tiles = int((N + bn - 1) / bn);
+    pa.kb_total = kb_total;
+    pa.kb_per_split = (kb_total + splits - 1) / splits;
+    pa.splits = splits;
+    pa.tiles = pa.m_tiles * pa.n_tiles * splits;
+    pa.idesc = instr_desc(false, bn, a_mn, b_mn);
+    pa.bias = splits > 1 ? nullptr : bias;
+#define HHB_GEMM_PCASE(AM, BMN, DU)                                   \
+  if (a_mn == AM && b_mn == BMN && dual == DU)                        \
+    rc = launch_p_bn<AM, BMN, DU>(bn, ta, ta2, tb, td, pa, st);
+    HHB_GEMM_PCASE(false, false, false)
+    HHB_GEMM_PCASE(false, false, true)
+    HHB_GEMM_PCASE(false, true, false)
+    HHB_GEMM_PCASE(false, true, true)
+    HHB_GEMM_PCASE(true, false, false)
+    HHB_GEMM_PCASE(true, false, true)
+    HHB_GEMM_PCASE(true, true, false)
+    HHB_GEMM_PCASE(true, true, true)
+#undef HHB_GEMM_PCASE
+    if (rc || splits == 1) return rc;
+    k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+    return cuda_check("k_gemm_reduce launch");
+  }
   Args a{};
   a.M = M;
   a.N = N;
