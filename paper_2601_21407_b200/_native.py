@@ -89,7 +89,7 @@ SIGNATURES = {
                                _vp, _i64,
                                _vp, _vp,
                                _i64, _vp,
-                               _vp, _vp, _i64, _vp, _vp]),
+                               _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "hhb_forward_poisson": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
                                    _vp, _vp, _i64, _vp, _vp,
                                    C.c_uint64, _i64, _dbl, _dbl,

@@ -108,7 +108,8 @@ def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_
               d_i=None, step_base=0, want_d_i=True, split=None, d_sum=None):
     """One hhb_backward(_ex) launch; returns (d_i or None, d_params np.array[1+nch], first_bad).
 
-    split = (hi, lo) uint16/bf16 [T][n] tensors receive dI as bf16 hi/lo halves
+    split = (hi, lo[, group, pitch]) bf16 [T][ld] tensors receive dI as bf16 hi/lo halves
+    (neuron i at (i // group) * pitch + i % group when group > 0)
     and d_sum [n] float accumulates the per-neuron sums of dI (SNN layer)."""
     dev = adj_v.device
     ng = params.n_gates
@@ -123,14 +124,16 @@ def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_
     bad = torch.full((1,), -1, dtype=torch.int64, device=dev)
     if d_i is None and want_d_i:
         d_i = torch.empty((T, n), dtype=adj_v.dtype, device=dev)
-    hi, lo = split if split is not None else (None, None)
+    hi, lo = (split[0], split[1]) if split is not None else (None, None)
+    grp, pitch = (split[2], split[3]) if split is not None and len(split) > 2 else (0, 0)
+    ld_split = hi.shape[-1] if hi is not None else n
     rc = lib.hhb_backward_ex(
         C.byref(P), C.byref(S), dt, n, T, cur.data_ptr(), i_st, i_sn,
         ckpt.data_ptr(), K, n, D.ptr(seg),
         D.ptr(seed_v), n, D.ptr(seed_s), n,
         adj_v.data_ptr(), D.ptr(adj_g) if ng else None, n,
         D.ptr(d_i), n, d_params.data_ptr(), parts.data_ptr(),
-        step_base, bad.data_ptr(), D.ptr(hi), D.ptr(lo), n, D.ptr(d_sum), D.stream())
+        step_base, bad.data_ptr(), D.ptr(hi), D.ptr(lo), ld_split, grp, pitch, D.ptr(d_sum), D.stream())
     nat.check(rc, "hhb_backward")
     return d_i, d_params, bad
 

@@ -95,8 +95,11 @@ static int backward_t(const hhb_params_t* P, const hhb_surrogate_t* S, int64_t n
                       int64_t sv_ld, const void* seed_s, int64_t ss_ld, void* adj_v, void* adj_g,
                       int64_t ag_ld, void* d_i, int64_t di_ld, double* d_params, double* partials,
                       int64_t step_base, int64_t* first_bad, cudaStream_t st, void* di_hi = nullptr,
-                      void* di_lo = nullptr, int64_t dh_ld = 0, float* di_sum = nullptr) {
+                      void* di_lo = nullptr, int64_t dh_ld = 0, float* di_sum = nullptr, int64_t dh_grp = 0,
+                      int64_t dh_pitch = 0) {
   BwdArgs<T> a{};
+  a.dh_grp = dh_grp;
+  a.dh_pitch = dh_pitch;
   a.di_hi = static_cast<uint16_t*>(di_hi);
   a.di_lo = static_cast<uint16_t*>(di_lo);
   a.dh_ld = dh_ld;
@@ -240,7 +243,7 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
                  void* stream) {
   return hhb_backward_ex(params, surrogate, dtype, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every, ckpt_ld,
                          seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v, adj_g, adj_g_ld, d_i, d_i_ld,
-                         d_params, partials, step_base, first_bad, nullptr, nullptr, 0, nullptr, stream);
+                         d_params, partials, step_base, first_bad, nullptr, nullptr, 0, 0, 0, nullptr, stream);
 }
 
 int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
@@ -249,10 +252,14 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
                     const void* seed_v, int64_t seed_v_ld, const void* seed_spk, int64_t seed_spk_ld,
                     void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
                     double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
-                    void* d_i_hi, void* d_i_lo, int64_t d_split_ld, float* d_i_sum, void* stream) {
+                    void* d_i_hi, void* d_i_lo, int64_t d_split_ld, int64_t d_split_group,
+                    int64_t d_split_pitch, float* d_i_sum, void* stream) {
+  if (d_split_group < 0 || (d_split_group > 0 && d_split_pitch < d_split_group))
+    return fail(HHB_EINVAL, "d_split_pitch < d_split_group");
   if ((d_i_hi || d_i_lo || d_i_sum) && dtype != HHB_F32)
     return fail(HHB_EINVAL, "split / summed dI outputs are float-only");
-  if ((d_i_hi != nullptr) != (d_i_lo != nullptr) || (d_i_hi && d_split_ld < n))
+  const int64_t split_cols = d_split_group > 0 ? (n + d_split_group - 1) / d_split_group * d_split_pitch : n;
+  if ((d_i_hi != nullptr) != (d_i_lo != nullptr) || (d_i_hi && d_split_ld < split_cols))
     return fail(HHB_EINVAL, "d_i_hi and d_i_lo go together, with d_split_ld >= n");
   int rc = check_params(params);
   if (rc) return rc;
@@ -270,7 +277,8 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
     return backward_t<float>(params, surrogate, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every,
                              ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                              adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base,
-                             first_bad, ST(stream), d_i_hi, d_i_lo, d_split_ld, d_i_sum);
+                             first_bad, ST(stream), d_i_hi, d_i_lo, d_split_ld, d_i_sum, d_split_group,
+                             d_split_pitch);
   return backward_t<double>(params, surrogate, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every,
                             ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                             adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base, first_bad,

@@ -72,7 +72,12 @@ struct BwdArgs {
   uint16_t* di_lo;
   int64_t dh_ld;
   float* di_sum;
+  int64_t dh_grp, dh_pitch;   // > 0: neuron i at column (i / grp) * pitch + i % grp
 };
+
+__host__ __device__ inline int64_t split_col(int64_t i, int64_t grp, int64_t pitch) {
+  return grp > 0 ? (i / grp) * pitch + i % grp : i;
+}
 
 __device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) {
   const uint32_t b = __float_as_uint(x);
@@ -461,8 +466,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
         if (on && a.di_hi != nullptr) {
           uint16_t h, l;
           split_bf16(float(di), h, l);
-          a.di_hi[t * a.dh_ld + ii] = h;
-          a.di_lo[t * a.dh_ld + ii] = l;
+          const int64_t col = split_col(ii, a.dh_grp, a.dh_pitch);
+          a.di_hi[t * a.dh_ld + col] = h;
+          a.di_lo[t * a.dh_ld + col] = l;
         }
         csum += double(di);
       }

@@ -917,7 +917,7 @@ struct PoissonSmem {
 struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
   float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
   i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad;
-  unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; };
+  unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; i64 dh_grp, dh_pitch; };
 __device__ __forceinline__ void split_bf16(float x, unsigned short& hi, unsigned short& lo) {
   // round-to-nearest-even bf16 of x, then of the remainder x - hi (exact in fp32)
   const u32 b = __float_as_uint(x);
@@ -1219,8 +1219,9 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
       advance();
     }
     float* dib = (BF_DI && on) ? a.d_i + (hi - 1) * a.di_ld + ii : nullptr;
-    unsigned short* dhb = (BF_SPLIT && on) ? a.di_hi + (hi - 1) * a.dh_ld + ii : nullptr;
-    unsigned short* dlb = (BF_SPLIT && on) ? a.di_lo + (hi - 1) * a.dh_ld + ii : nullptr;
+    const i64 scol = a.dh_grp > 0 ? (ii / a.dh_grp) * a.dh_pitch + ii % a.dh_grp : ii;
+    unsigned short* dhb = (BF_SPLIT && on) ? a.di_hi + (hi - 1) * a.dh_ld + scol : nullptr;
+    unsigned short* dlb = (BF_SPLIT && on) ? a.di_lo + (hi - 1) * a.dh_ld + scol : nullptr;
     int rslot = 0;
     for (i64 t = hi - 1; t >= lo; --t) {
       if (tn >= lo) issue();

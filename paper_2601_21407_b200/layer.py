@@ -149,8 +149,10 @@ class _HHLayerFn(torch.autograd.Function):
         v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
         spikes = torch.empty((T, n), dtype=torch.float32, device=x.device)
         _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
+        layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)
+        ctx.set_materialize_grads(False)    # an unused output (V or spikes) seeds nothing
         ctx.save_for_backward(xb, wb, cur, ckpt)
         ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
         ctx.x_requires_grad = x.requires_grad
@@ -165,22 +167,25 @@ class _HHLayerFn(torch.autograd.Function):
         p = layer.params
         sv = None if d_v is None else d_v.reshape(T, n).float().contiguous()
         ss = None if d_s is None else d_s.reshape(T, n).float().contiguous()
-        if sv is None:
-            sv = torch.zeros((T, n), dtype=torch.float32, device=cur.device)
-        adj_v = torch.zeros(n, dtype=torch.float32, device=cur.device)
-        adj_g = torch.zeros((p.n_gates, n), dtype=torch.float32, device=cur.device)
-        direct = n_out % 8 == 0
+        # adjoint state (d_v, d_gates) and the per-neuron dI sums: one zeroed block
+        zb = torch.zeros((2 + p.n_gates) * n, dtype=torch.float32, device=cur.device)
+        adj_v = zb[:n]
+        adj_g = zb[n:(1 + p.n_gates) * n].view(p.n_gates, n)
+        direct = True
         if direct:
-            # dI leaves the BPTT kernel as bf16 hi/lo planes + per-neuron sums;
-            # the gradient GEMMs read them (and X, W) in place, MN-major
-            hi = torch.empty((T, n), dtype=torch.bfloat16, device=cur.device)
-            lo = torch.empty((T, n), dtype=torch.bfloat16, device=cur.device)
-            dsum = torch.zeros(n, dtype=torch.float32, device=cur.device)
+            # dI leaves the BPTT kernel as bf16 hi/lo planes [T*B][P] (P = n_out
+            # padded to 8 for TMA pitches) + per-neuron sums; the gradient GEMMs
+            # read them (and X, W) in place, MN-major
+            P = _pad8(n_out)
+            hi = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
+            lo = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
+            dsum = zb[(1 + p.n_gates) * n:]
             _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
-                                          adj_g, want_d_i=False, split=(hi, lo), d_sum=dsum)
+                                          adj_g, want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum)
         else:
             d_i, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
                                             adj_g)
+        layer._last_gbad = gbad
         if layer.check_finite:
             b = int(gbad.item())
             if b >= 0:
@@ -188,10 +193,10 @@ class _HHLayerFn(torch.autograd.Function):
         layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
         if direct:
             # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
-            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, n_out, xb, xb.stride(0))
+            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
             db = col_sum(dsum.view(B, n_out)).float()
             # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
-            dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, n_out, wb, wb.stride(0)).view(T, B, k_in)
+            dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0)).view(T, B, k_in)
                   if ctx.x_requires_grad else None)
             return dX, dW, db, None
         dI = d_i.view(M, n_out)
@@ -231,18 +236,32 @@ class HHLayer(torch.nn.Module):
         self.param_grads = None
         self._rest = None
 
+    def check(self):
+        """Deferred form of check_finite (for check_finite=False training loops,
+        which then never wait on the device inside a step): raise the
+        NumericalOverflowError / GradientOverflowError of the last forward /
+        backward, if any."""
+        if getattr(self, "_last_bad", None) is not None:
+            _raise_if_bad(self._last_bad)
+        gb = getattr(self, "_last_gbad", None)
+        if gb is not None and int(gb.item()) >= 0:
+            raise GradientOverflowError("adjoint state became non-finite", int(gb.item()))
+
     def segment(self, T: int) -> int:
         return 1 if self.budget is None else make_plan(T, self.budget).segment_length
 
     def rest_state(self, n: int, dev):
-        if self._rest is None:
-            self._rest = (float(self.params.v_rest), steady_state_gates(self.params, self.params.v_rest))
-        v_rest, fr = self._rest
-        v = torch.full((n,), v_rest, dtype=torch.float32, device=dev)
-        g = torch.empty((len(fr), n), dtype=torch.float32, device=dev)
-        for i, f in enumerate(fr):
-            g[i].fill_(f)
-        return v, g
+        """Rest state (v_rest, steady-state gates) of n neurons; the forward only
+        reads it, so one device copy per (n, device) is kept."""
+        key = (n, str(dev))
+        if self._rest is None or self._rest[0] != key:
+            fr = steady_state_gates(self.params, self.params.v_rest)
+            v = torch.full((n,), float(self.params.v_rest), dtype=torch.float32, device=dev)
+            g = torch.empty((len(fr), n), dtype=torch.float32, device=dev)
+            for i, f in enumerate(fr):
+                g[i].fill_(f)
+            self._rest = (key, v, g)
+        return self._rest[1], self._rest[2]
 
     def forward(self, x: torch.Tensor):
         if x.dim() != 3:

@@ -1,0 +1,45 @@
+"""GPU tests of the training plumbing (paper_2601_21407_b200.learn, SURVEY §8
+f2) against the oracle restatement of learn.py:80-107."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hh_oracle as O
+from paper_2601_21407_b200 import learn as L
+from paper_2601_21407_b200.errors import UsageError
+
+pytestmark = pytest.mark.gpu
+
+
+def test_mse_loss_and_seed_match_reference(cuda):
+    rng = np.random.default_rng(0)
+    pred, target = rng.normal(size=(7, 5, 3)), rng.normal(size=(7, 5, 3))
+    loss, seed = L.mse_loss(pred, target)
+    ref_loss, ref_seed = O.mse_loss(pred, target)
+    assert abs(loss - ref_loss) <= 1e-12 * abs(ref_loss)
+    assert np.allclose(seed, ref_seed, rtol=1e-12, atol=0)
+    with pytest.raises(UsageError):
+        L.mse_loss(pred, target[:2])
+
+
+def test_cross_entropy_loss_and_seed_match_reference(cuda):
+    rng = np.random.default_rng(1)
+    logits, y = rng.normal(size=(9, 10)) * 3, rng.integers(0, 10, size=9)
+    loss, seed = L.cross_entropy_loss(logits, y)
+    ref_loss, ref_seed = O.cross_entropy_loss(logits, y)
+    assert abs(loss - ref_loss) <= 1e-12 * abs(ref_loss)
+    assert np.allclose(seed, ref_seed, rtol=1e-10, atol=1e-15)
+
+
+@pytest.mark.parametrize("with_target", [False, True])
+def test_mse_autograd_gradient_is_the_reference_seed(cuda, with_target):
+    g = torch.Generator(device=cuda).manual_seed(2)
+    v = torch.randn((40, 3, 8), device=cuda, generator=g, dtype=torch.float64).requires_grad_(True)
+    t = torch.randn((40, 3, 8), device=cuda, generator=g, dtype=torch.float64) if with_target else None
+    loss = L.mse(v, t)
+    loss.backward()
+    ref_loss, ref_seed = O.mse_loss(v.detach().cpu().numpy(),
+                                    np.zeros((40, 3, 8)) if t is None else t.cpu().numpy())
+    assert abs(loss.item() - ref_loss) <= 1e-12 * ref_loss
+    assert np.allclose(v.grad.cpu().numpy(), ref_seed, rtol=1e-12, atol=0)

@@ -153,3 +153,13 @@ def test_readout_composition():
     d_drive = np.moveaxis(res["d_i"].reshape(T, B, Oo), 0, 1)
     assert np.allclose(res["d_i"].reshape(T, B, Oo), g["d_i"], rtol=1e-12, atol=1e-300)
     assert np.allclose(O.dense_grad_w(d_drive, g["x"]), g["d_w"], rtol=1e-11)
+
+
+def test_oracle_losses_match_reference_goldens():
+    """oracle mse_loss / cross_entropy_loss (learn.py:80-107) vs the reference's outputs."""
+    ka = golden("known_answers")
+    loss, seed = O.mse_loss(ka["mse_pred"], ka["mse_target"])
+    assert loss == float(ka["mse_loss"]) and np.array_equal(seed, ka["mse_seed"])
+    loss, seed = O.cross_entropy_loss(ka["ce_logits"], ka["ce_target"])
+    assert abs(loss - float(ka["ce_loss"])) <= 1e-15 * abs(loss)
+    assert np.allclose(seed, ka["ce_seed"], rtol=1e-14, atol=0)
