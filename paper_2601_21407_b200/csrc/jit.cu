@@ -520,6 +520,7 @@ struct RateX {
 };
 static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<Group>& G, const char* nm) {
   RateX R;
+  const double l2 = 1.0;   // slope scale (the decay term applies ln2 to s' itself)
   const std::string E = fmt("E%d", r.group);
   const double bg = G[r.group].b;
   const std::string w(nm);
@@ -532,7 +533,7 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
     } else {
       R.v = bind(o, w + "v", mulx(V(F(r.Sa * r.c)), V(E)));
     }
-    R.v1 = bind(o, w + "v1", mulx(R.v, V(F(-1.0 / r.b))));
+    R.v1 = bind(o, w + "v1", mulx(R.v, V(F(-l2 / r.b))));
     return R;
   }
   R.rat = true;
@@ -541,19 +542,19 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
       R.n = V(F(r.Sa * r.c));
       R.d = V(E);
       R.n1 = Z();
-      R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-1.0 / bg))));
+      R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-l2 / bg))));
       break;
     case HHB_RATE_SIGMOID:
       if (r.sigma > 0) {
         R.n = V(F(r.Sa));
         R.d = bind(o, w + "d", V(fmt("__fmaf_rn(%s, %s, 1.0f)", F(r.c).c_str(), E.c_str())));
         R.n1 = Z();
-        R.d1 = bind(o, w + "d1", V(fmt("__fmul_rn(%s, %s)", F(-r.c / bg).c_str(), E.c_str())));
+        R.d1 = bind(o, w + "d1", V(fmt("__fmul_rn(%s, %s)", F(-l2 * r.c / bg).c_str(), E.c_str())));
       } else {
         R.n = bind(o, w + "n", mulx(V(F(r.Sa)), V(E)));
         R.d = bind(o, w + "d", V(fmt("__fadd_rn(%s, %s)", E.c_str(), F(r.c).c_str())));
-        R.n1 = bind(o, w + "n1", mulx(R.n, V(F(-1.0 / bg))));
-        R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-1.0 / bg))));
+        R.n1 = bind(o, w + "n1", mulx(R.n, V(F(-l2 / bg))));
+        R.d1 = bind(o, w + "d1", mulx(V(E), V(F(-l2 / bg))));
       }
       break;
     default: {
@@ -563,14 +564,15 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
       if (r.sigma > 0) {
         n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), nm);
         d0 = fmt("__fmaf_rn(%s, %s, 1.0f)", F(-r.c).c_str(), E.c_str());
-        n10 = F(r.Sa);
-        d10 = fmt("__fmul_rn(%s, %s)", F(r.c / bg).c_str(), E.c_str());
+        n10 = F(l2 * r.Sa);
+        d10 = fmt("__fmul_rn(%s, %s)", F(l2 * r.c / bg).c_str(), E.c_str());
         thr = kSingThr;
       } else {
         n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), nm, E.c_str());
         d0 = fmt("__fsub_rn(%s, %s)", E.c_str(), F(r.c).c_str());
-        n10 = fmt("__fmul_rn(__fmaf_rn(%sx, %s, %s), %s)", nm, F(-r.Sa / bg).c_str(), F(r.Sa).c_str(), E.c_str());
-        d10 = fmt("__fmul_rn(%s, %s)", E.c_str(), F(-1.0 / bg).c_str());
+        n10 = fmt("__fmul_rn(__fmaf_rn(%sx, %s, %s), %s)", nm, F(-l2 * r.Sa / bg).c_str(), F(l2 * r.Sa).c_str(),
+                  E.c_str());
+        d10 = fmt("__fmul_rn(%s, %s)", E.c_str(), F(-l2 / bg).c_str());
         thr = kSingThr * r.c;
       }
       o += fmt("  const float %sd0 = %s;\n", nm, d0.c_str());
@@ -581,7 +583,7 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
       o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, nm);
       // slopes: d/dx of a b (1 + u/2 + u^2/12) = a (1/2 + u/6) in the series region
       o += fmt("  const float %sn1 = %ssg ? __fmaf_rn(%sx, %s, %s) : %s;\n", nm, nm, nm,
-               F(r.Sa / (6.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), n10.c_str());
+               F(l2 * r.Sa / (6.0 * r.b)).c_str(), F(l2 * 0.5 * r.Sa).c_str(), n10.c_str());
       o += fmt("  const float %sd1 = %ssg ? 0.0f : %s;\n", nm, nm, d10.c_str());
       R.n = V(w + "n");
       R.d = V(w + "d");
@@ -645,8 +647,9 @@ static std::string emit_gate_bwd(const GatePlan& gp, const std::vector<Group>& G
     dpinf = bind(o, "dpinf", mulx(fmax_(negx(pinf), N1, A1), iN));
   }
   o += "  const float e = ex2f_(s);\n";
-  const X t2 = mulx(mulx(V(fmt("__fsub_rn(p[%d], %s)", g, pinf.e.c_str())), mulx(V(F(std::log(2.0))), s1)), V("e"));
-  o += "  const float term = " + fmax_(dpinf, V("__fsub_rn(1.0f, e)"), t2).e + ";\n";
+  // term = dpinf (1 - e) + (p - pinf) ln2 s1 e = e ((p - pinf) ln2 s1 - dpinf) + dpinf
+  o += fmt("  const float term = __fmaf_rn(e, __fmaf_rn(__fsub_rn(p[%d], %s), %s, %s), %s);\n", g, pinf.e.c_str(),
+           s1.zero ? "0.0f" : fmt("__fmul_rn(%s, %s)", s1.e.c_str(), F(std::log(2.0)).c_str()).c_str(), negx(dpinf).e.c_str(), dpinf.e.c_str());
   return o;
 }
 
@@ -764,7 +767,12 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
 
 }  // namespace mg
 
-// adjoint of step_fwd (hh_step_backward, adjoint.py:116-188)
+// adjoint of step_fwd (hh_step_backward, adjoint.py:116-188).  The parameter-
+// gradient terms (adjoint.py:144, :147) are accumulated straight into the
+// caller's fp32 partials acc[] with FFMAs; per gated channel c the factor
+// w_c = g_vp (v - E_c) is shared by its d_g_max term and the dp' chain rule of
+// all its gates.  Merged variant: term = e ((p - pinf) ln2 s' - dpinf) + dpinf
+// (s' the slope of the exp2 argument) costs 4 ops per gate.
 static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, SeriesMode mode,
                                       const mg::Plan* M = nullptr) {
   std::string o;
@@ -773,7 +781,7 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
   o += fmt(
       "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
       "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
-      "float (&cb)[%d]) {\n",
+      "float (&acc)[%d]) {\n",
       M ? "m" : (mode == kFast ? "f" : "s"), NGX, NGX, kSlots);
   if (M) o += mg::emit_exps(*M);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
@@ -793,59 +801,62 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
       o += fmt("  gsum = __fmaf_rn(%s, eta, gsum);\n", F(C.g_max).c_str());
     }
   }
-  o += fmt("  const float vn = __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n", F(dtcm).c_str());
+  o += "  const float dI = __fsub_rn(cur, ion);\n";
+  o += fmt("  const float vn = __fmaf_rn(dI, %s, v);\n", F(dtcm).c_str());
   o += "  float g_vp = d_v;\n";
   o += fmt("  if (has_s) g_vp = __fmaf_rn(d_spike, surrogate(sur, __fsub_rn(vn, %s)), g_vp);\n",
            F(P->v_theta).c_str());
-  o += "  cb[0] = __fmul_rn(g_vp, __fsub_rn(cur, ion));\n";
+  o += "  acc[0] = __fmaf_rn(g_vp, dI, acc[0]);\n";
+  // per gated channel: w_c = g_vp (v - E_c)
   for (int g = 0; g < NG; ++g) {
     if (!L.last[g]) continue;
     const hhb_channel_t& C = P->channels[L.chan[g]];
-    o += fmt("  cb[%d] = __fmul_rn(__fmul_rn(g_vp, eta_c[%d]), __fsub_rn(v, %s));\n", 1 + g, g,
-             F(C.e_rev).c_str());
+    o += fmt("  const float w%d = __fmul_rn(g_vp, __fsub_rn(v, %s));\n", L.chan[g], F(C.e_rev).c_str());
+    o += fmt("  acc[%d] = __fmaf_rn(w%d, eta_c[%d], acc[%d]);\n", 1 + g, L.chan[g], g, 1 + g);
   }
-  for (size_t j = 0; j < L.leak_ch.size(); ++j)
-    o += fmt("  cb[%d] = __fmul_rn(g_vp, __fsub_rn(v, %s));\n", 1 + kMaxGates + int(j),
-             F(P->channels[L.leak_ch[j]].e_rev).c_str());
+  for (size_t j = 0; j < L.leak_ch.size(); ++j) {
+    const int k = 1 + kMaxGates + int(j);
+    o += fmt("  acc[%d] = __fmaf_rn(g_vp, __fsub_rn(v, %s), acc[%d]);\n", k,
+             F(P->channels[L.leak_ch[j]].e_rev).c_str(), k);
+  }
   o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
   for (int g = 0; g < NG; ++g) {
     const hhb_gate_t& G = P->gates[g];
     const hhb_channel_t& C = P->channels[L.chan[g]];
     o += fmt("  // gate %d\n  {\n", g);
     if (M) {
-      // merged form: s, p_inf, their V-slopes from the fractions; every lane
-      // here has s > 0 (checked over the window), so no zero-rate branch
       o += mg::emit_gate_bwd(M->gates[g], M->groups, g);
       o += fmt("  const float up = d_p[%d];\n", g);
       o += "  dv_in = __fmaf_rn(up, term, dv_in);\n";
       o += "  float dp = __fmul_rn(up, e);\n";
     } else {
-    o += "  float a, b, da, db;\n";
-    std::string sa = "da", sb = "db";
-    emit_rate(o, G.alpha, P->rate_scale, "a", &sa, mode);
-    emit_rate(o, G.beta, P->rate_scale, "b", &sb, mode);
-    o += "  const float s = __fadd_rn(a, b);\n";
-    o += "  const float rs = rcpf_(s);\n";
-    o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
-    o += "  const float pinf = __fmul_rn(a, rs);\n";
-    o += "  const float dpinf = __fmul_rn(__fsub_rn(__fmul_rn(da, b), __fmul_rn(a, db)), __fmul_rn(rs, rs));\n";
-    o += fmt("  const float term = __fmaf_rn(dpinf, __fsub_rn(1.0f, e), __fmul_rn(__fsub_rn(p[%d], pinf), "
-             "__fmul_rn(__fmul_rn(%s, __fadd_rn(da, db)), e)));\n",
-             g, F(-P->dt).c_str());
-    o += "  const bool pos = s > 0.0f;\n";
-    o += fmt("  const float up = d_p[%d];\n", g);
-    o += "  dv_in = pos ? __fmaf_rn(up, term, dv_in) : dv_in;\n";
-    o += "  float dp = pos ? __fmul_rn(up, e) : up;\n";
+      o += "  float a, b, da, db;\n";
+      std::string sa = "da", sb = "db";
+      emit_rate(o, G.alpha, P->rate_scale, "a", &sa, mode);
+      emit_rate(o, G.beta, P->rate_scale, "b", &sb, mode);
+      o += "  const float s = __fadd_rn(a, b);\n";
+      o += "  const float rs = rcpf_(s);\n";
+      o += fmt("  const float e = ex2f_(__fmul_rn(s, %s));\n", F(-P->dt * kLog2e).c_str());
+      o += "  const float pinf = __fmul_rn(a, rs);\n";
+      o += "  const float dpinf = __fmul_rn(__fsub_rn(__fmul_rn(da, b), __fmul_rn(a, db)), __fmul_rn(rs, rs));\n";
+      o += fmt("  const float term = __fmaf_rn(dpinf, __fsub_rn(1.0f, e), __fmul_rn(__fsub_rn(p[%d], pinf), "
+               "__fmul_rn(__fmul_rn(%s, __fadd_rn(da, db)), e)));\n",
+               g, F(-P->dt).c_str());
+      o += "  const bool pos = s > 0.0f;\n";
+      o += fmt("  const float up = d_p[%d];\n", g);
+      o += "  dv_in = pos ? __fmaf_rn(up, term, dv_in) : dv_in;\n";
+      o += "  float dp = pos ? __fmul_rn(up, e) : up;\n";
     }
     if (G.exponent > 0) {
-      // d eta / d p = k p^(k-1) prod(other gates of the channel)
-      std::string der = fmt("__fmul_rn(%s, %s)", F(double(G.exponent)).c_str(),
-                            pow_expr(fmt("p[%d]", g), G.exponent - 1).c_str());
+      // d eta / d p = k p^(k-1) prod(other gates of the channel), times the
+      // constant -dt/c_m g_c of the membrane step, against w_c
+      const double kc = -dtcm * C.g_max * double(G.exponent);
+      std::string der = G.exponent > 1 ? pow_expr(fmt("p[%d]", g), G.exponent - 1) : "";
       const hhb_channel_t& CC = P->channels[L.chan[g]];
       for (int o2 = CC.gate_begin; o2 < CC.gate_begin + CC.gate_count; ++o2)
-        if (o2 != g) der = fmt("__fmul_rn(%s, pk[%d])", der.c_str(), o2);
-      o += fmt("  dp = __fmaf_rn(__fmul_rn(__fmul_rn(g_vp, %s), __fsub_rn(v, %s)), %s, dp);\n",
-               F(-dtcm * C.g_max).c_str(), F(C.e_rev).c_str(), der.c_str());
+        if (o2 != g) der = der.empty() ? fmt("pk[%d]", o2) : fmt("__fmul_rn(%s, pk[%d])", der.c_str(), o2);
+      const std::string dk = der.empty() ? F(kc) : fmt("__fmul_rn(%s, %s)", F(kc).c_str(), der.c_str());
+      o += fmt("  dp = __fmaf_rn(w%d, %s, dp);\n", L.chan[g], dk.c_str());
     }
     o += fmt("  d_p[%d] = dp;\n  }\n", g);
   }
@@ -919,13 +930,15 @@ struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* 
   i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad;
   unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; i64 dh_grp, dh_pitch; };
 __device__ __forceinline__ void split_bf16(float x, unsigned short& hi, unsigned short& lo) {
-  // round-to-nearest-even bf16 of x, then of the remainder x - hi (exact in fp32)
-  const u32 b = __float_as_uint(x);
-  const u32 h = (b + 0x7FFFu + ((b >> 16) & 1u)) & 0xFFFF0000u;
-  const float r = __fsub_rn(x, __uint_as_float(h));
-  const u32 c = __float_as_uint(r);
-  hi = (unsigned short)(h >> 16);
-  lo = (unsigned short)((c + 0x7FFFu + ((c >> 16) & 1u)) >> 16);
+  // round-to-nearest-even bf16 of x (cvt.rn.bf16x2.f32), then of the remainder
+  // x - hi, which is exact in fp32; one packed cvt yields both halves
+  u32 h;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(0.0f), "f"(x));
+  const float r = __fsub_rn(x, __uint_as_float(h << 16));
+  u32 pk;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(r), "f"(x));
+  hi = (unsigned short)(pk & 0xFFFFu);
+  lo = (unsigned short)(pk >> 16);
 }
 struct Sur { int kind; float w, inv_w, k2, half_inv_w; };
 #define LLMAX 0x7fffffffffffffffLL
@@ -1133,7 +1146,7 @@ __device__ __forceinline__ void store_state(float* base, i64 ld, i64 i, float v,
 // hides behind compute without holding the operands in registers.  The module
 // is specialised on which optional streams exist (BF_* below), so the sweep
 // carries no run-time tests; every stream advances by a running pointer.
-#define DEPTH 6
+#define DEPTH 8   // power of two: slot wrap is a mask
 #define NOPS (NG + 4)   // v, p[NG], cur, seed_v, seed_s
 #define RING_STRIDE (NOPS * BWD_THREADS)
 __device__ __forceinline__ void cpa4(float* dst, const float* src) {
@@ -1210,7 +1223,7 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
       iq -= a.i_st;
       if (BF_SV) vq -= a.sv_ld;
       if (BF_SS) sq -= a.ss_ld;
-      wslot = (wslot + 1 == DEPTH) ? 0 : wslot + 1;
+      wslot = (wslot + 1) & (DEPTH - 1);
     };
 #pragma unroll
     for (int k = 0; k < DEPTH - 1; ++k) {
@@ -1229,16 +1242,14 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
       advance();
       cpa_wait();
       const float* r = ring_t + rslot * RING_STRIDE;
-      rslot = (rslot + 1 == DEPTH) ? 0 : rslot + 1;
+      rslot = (rslot + 1) & (DEPTH - 1);
       float v = r[0], p[NGX];
 #pragma unroll
       for (int g = 0; g < NG; ++g) p[g] = r[(1 + g) * BWD_THREADS];
       const float cur = r[(NG + 1) * BWD_THREADS];
       if (BF_SV) d_v = __fadd_rn(d_v, r[(NG + 2) * BWD_THREADS]);
       const float ds = BF_SS ? r[(NG + 3) * BWD_THREADS] : 0.0f;
-      float cb[SLOTS];
-      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, BF_SS, cb);
-      cb_add(accf, cb);
+      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, BF_SS, accf);
       if (BF_SUM) csumf = __fadd_rn(csumf, di);
       if (++nf == 8) {
         cb_flush(acc, accf);
@@ -1389,13 +1400,15 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
     std::string fl = "__device__ __forceinline__ void cb_flush(double (&d)[SLOTS], float (&a)[SLOTS]) {\n";
     std::string ze = "__device__ __forceinline__ void cb_zero(float (&a)[SLOTS]) {\n";
     std::string se = "__device__ __forceinline__ void cb_sel(bool q, float (&a)[SLOTS], const float (&c)[SLOTS]) {\n";
+    std::string cp = "__device__ __forceinline__ void cb_copy(float (&a)[SLOTS], const float (&c)[SLOTS]) {\n";
     for (int k : used) {
       add += fmt("  a[%d] = __fadd_rn(a[%d], c[%d]);\n", k, k, k);
       fl += fmt("  d[%d] += double(a[%d]); a[%d] = 0.0f;\n", k, k, k);
       ze += fmt("  a[%d] = 0.0f;\n", k);
       se += fmt("  a[%d] = q ? c[%d] : a[%d];\n", k, k, k);
+      cp += fmt("  a[%d] = c[%d];\n", k, k);
     }
-    src += add + "}\n" + fl + "}\n" + ze + "}\n" + se + "}\n";
+    src += add + "}\n" + fl + "}\n" + ze + "}\n" + se + "}\n" + cp + "}\n";
   }
   const char* bwd_sig =
       "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[NGX], "
@@ -1405,16 +1418,17 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
     src += std::string(bwd_sig) + R"( {
   if (__all_sync(0xffffffffu, regular(v))) return step_bwd_m(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
   // some lane left the window: both forms, selected per lane
-  float dvm = d_v, dpm[NGX], cbm[SLOTS];
+  float dvm = d_v, dpm[NGX], accm[SLOTS];
 #pragma unroll
   for (int g = 0; g < NGX; ++g) dpm[g] = d_p[g];
-  const float dim = step_bwd_m(sur, v, p, cur, dvm, dpm, d_spike, has_s, cbm);
+  cb_copy(accm, cb);
+  const float dim = step_bwd_m(sur, v, p, cur, dvm, dpm, d_spike, has_s, accm);
   const float dis = step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
   const bool reg = regular(v);
   d_v = reg ? dvm : d_v;
 #pragma unroll
   for (int g = 0; g < NGX; ++g) d_p[g] = reg ? dpm[g] : d_p[g];
-  cb_sel(reg, cb, cbm);
+  cb_sel(reg, cb, accm);
   return reg ? dim : dis;
 }
 )";
