@@ -127,12 +127,15 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
 
 /* hhb_forward plus spk_val[n_steps][spk_val_ld] (dtype of V, NULL = off): the
  * spike flags as 0/1 values, the SNN layer's differentiable spike output,
- * written by the forward kernel itself (no bitmap round trip). */
+ * written by the forward kernel itself (no bitmap round trip); and
+ * step_base_dev (NULL = off): *step_base_dev is added to step_base on the
+ * device (first_bad indices inside a replayed CUDA graph). */
 int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
                    const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
-                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream);
+                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
+                   const int64_t* step_base_dev, void* stream);
 /*
  * hhb_forward_poisson -- hhb_forward with the BASELINE config-2 stimulus
  * I[t][j] = amp * Poisson(lam) drawn inside the kernel (Philox-4x32-10 keyed by
@@ -300,6 +303,28 @@ int hhb_cortex_input(int32_t dtype, int64_t n, int64_t t, int64_t depth, int64_t
 int hhb_spike_deliver(int64_t words, const uint32_t* bits, const int64_t* offsets,
                       const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
                       int64_t t, int64_t depth, int64_t n_local, int64_t* ring, void* stream);
+/* CUDA-graph forms: the step index is read from device memory t_dev (when
+ * non-NULL, t is ignored), so one captured network step replays for every t;
+ * hhb_cortex_tick adds 1 to *t_dev (the last node of a captured step). */
+int hhb_cortex_input_dev(int32_t dtype, int64_t n, int64_t t, const int64_t* t_dev, int64_t depth,
+                         int64_t* ring, void* psp, double decay, int32_t bg_mode, const void* bg,
+                         const double* lam, double mu, double sigma, uint64_t seed, int64_t neuron_base,
+                         const void* extra, void* cur, double w_scale, void* stream);
+int hhb_spike_deliver_dev(int64_t words, const uint32_t* bits, const int64_t* offsets,
+                          const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
+                          int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring,
+                          void* stream);
+int hhb_cortex_tick(int64_t* t_dev, void* stream);
+/* hhb_spike_deliver_dev in two kernels for the sparse per-step case: one
+ * block lists the spiking sources (ascending) with the prefix of their row
+ * lengths, then every (spike, synapse) pair gets its own thread.  Same ring
+ * (bit-identical: integer atomics).  scratch: hhb_spike_scratch(words * 32)
+ * int64 of device memory. */
+int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* offsets,
+                           const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
+                           int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring,
+                           int64_t* scratch, void* stream);
+int64_t hhb_spike_scratch(int64_t n_sources);
 
 /* ---- runtime specialisation ----------------------------------------------- */
 

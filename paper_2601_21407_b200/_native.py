@@ -72,7 +72,7 @@ SIGNATURES = {
                               _vp, _i64,
                               _vp, _i64,
                               _vp, _i64, _i64,
-                              _i64, _vp, _vp]),
+                              _i64, _vp, _vp, _vp]),
     "hhb_backward": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
                             _vp, _i64, _i64,
                             _vp, _i64, _i64, _vp,
@@ -120,6 +120,12 @@ SIGNATURES = {
     "hhb_cortex_input": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _dbl, _dbl,
                                 C.c_uint64, _i64, _vp, _vp, _dbl, _vp]),
     "hhb_spike_deliver": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "hhb_cortex_input_dev": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _dbl, _dbl,
+                                    C.c_uint64, _i64, _vp, _vp, _dbl, _vp]),
+    "hhb_spike_deliver_dev": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp]),
+    "hhb_cortex_tick": (_i32, [_vp, _vp]),
+    "hhb_spike_deliver_flat": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "hhb_spike_scratch": (_i64, [_i64]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }

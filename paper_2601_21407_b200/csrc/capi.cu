@@ -33,8 +33,9 @@ static int forward_t(const hhb_params_t* P, int64_t n, int64_t steps, const void
                      int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld, uint32_t* spk,
                      int64_t spk_ld, void* ckpt, int64_t ck_every, int64_t ck_ld,
                      int64_t step_base, int64_t* first_bad, cudaStream_t st, void* spk_val = nullptr,
-                     int64_t spkv_ld = 0) {
+                     int64_t spkv_ld = 0, const int64_t* step_base_dev = nullptr) {
   FwdArgs<T> a{};
+  a.step_dev = reinterpret_cast<const long long*>(step_base_dev);
   a.spk_val = static_cast<T*>(spk_val);
   a.spkv_ld = spkv_ld;
   a.n = n;
@@ -176,14 +177,15 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
                 int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream) {
   return hhb_forward_ex(params, dtype, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn, v_out,
                         v_ld, spk_out, spk_ld, nullptr, 0, ckpt, ckpt_every, ckpt_ld, step_base, first_bad,
-                        stream);
+                        nullptr, stream);
 }
 
 int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
                    const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
-                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream) {
+                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
+                   const int64_t* step_base_dev, void* stream) {
   if (spk_val && spk_val_ld < n) return fail(HHB_EINVAL, "spk_val_ld < n");
   int rc = check_params(params);
   if (rc) return rc;
@@ -199,10 +201,10 @@ int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t
   if (dtype == HHB_F32)
     return forward_t<float>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                             v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                            first_bad, ST(stream), spk_val, spk_val_ld);
+                            first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev);
   return forward_t<double>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                            v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                           first_bad, ST(stream), spk_val, spk_val_ld);
+                           first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev);
 }
 
 int hhb_forward_poisson(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,

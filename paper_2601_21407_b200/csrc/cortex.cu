@@ -15,12 +15,15 @@
 namespace hhb {
 namespace cortex {
 
+// t_dev != NULL: the step index is read from device memory (CUDA-graph replay
+// of the network step; hhb_cortex_tick advances it), else t is used
 template <typename T>
-__global__ void k_cortex_input(int64_t n, int64_t t, int64_t depth, long long* ring, T* psp, T decay, int mode,
-                               const T* bg, const double* lam, T mu, T sigma, uint64_t seed, int64_t nbase,
-                               const T* extra, T* cur, T w_scale) {
+__global__ void k_cortex_input(int64_t n, int64_t t, const long long* t_dev, int64_t depth, long long* ring, T* psp,
+                               T decay, int mode, const T* bg, const double* lam, T mu, T sigma, uint64_t seed,
+                               int64_t nbase, const T* extra, T* cur, T w_scale) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (t_dev) t = *t_dev;
   long long* slot = ring + (t % depth) * n + i;
   const long long arr = *slot;
   *slot = 0;
@@ -35,21 +38,24 @@ __global__ void k_cortex_input(int64_t n, int64_t t, int64_t depth, long long* r
     const uint4 r = Philox::run(make_uint4(uint32_t(i + nbase), uint32_t(uint64_t(i + nbase) >> 32), uint32_t(t),
                                            uint32_t(uint64_t(t) >> 32)),
                                 make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
-    const double L = lam[i];
-    const double u = (double(r.x) + 0.5) * 2.3283064365386963e-10;
-    double p = exp(-L), c = p;
+    // single precision with fast intrinsics: the draw sits on every step's
+    // critical path (one thread per neuron, few warps per SM), and the sampler
+    // only has to be distributionally exact (Philox stream, not the reference RNG)
+    const float L = float(lam[i]);
+    const float u = (float(r.x) + 0.5f) * 2.3283064365386963e-10f;
+    float p = __expf(-L), c = p;
     int k = 0;
     while (u > c && k < 64) {
       ++k;
-      p *= L / k;
+      p *= __fdividef(L, float(k));
       c += p;
     }
-    double add = double(k) * double(mu);
+    float add = float(k) * float(mu);
     if (sigma > T(0) && k > 0) {
-      const double u1 = (double(r.y) + 0.5) * 2.3283064365386963e-10;
-      const double u2 = (double(r.z) + 0.5) * 2.3283064365386963e-10;
-      const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
-      add += double(sigma) * sqrt(double(k)) * z;
+      const float u1 = (float(r.y) + 0.5f) * 2.3283064365386963e-10f;
+      const float u2 = (float(r.z) + 0.5f) * 2.3283064365386963e-10f;
+      const float z = sqrtf(-2.0f * __logf(u1)) * __cosf(6.283185307179586f * u2);
+      add += float(sigma) * sqrtf(float(k)) * z;
     }
     x = x + T(add);
   }
@@ -59,9 +65,11 @@ __global__ void k_cortex_input(int64_t n, int64_t t, int64_t depth, long long* r
 
 __global__ void __launch_bounds__(128) k_spike_deliver(int64_t words, const uint32_t* bits, const int64_t* off,
                                                        const int32_t* tgt, const int32_t* w, const int32_t* delay,
-                                                       int64_t t, int64_t depth, int64_t n, long long* ring) {
+                                                       int64_t t, const long long* t_dev, int64_t depth, int64_t n,
+                                                       long long* ring) {
   const int64_t b = blockIdx.x;
   if (b >= words) return;
+  if (t_dev) t = *t_dev;
   uint32_t word = bits[b];
   while (word) {
     const int bit = __ffs(int(word)) - 1;
@@ -76,6 +84,87 @@ __global__ void __launch_bounds__(128) k_spike_deliver(int64_t words, const uint
   }
 }
 
+__global__ void k_tick(long long* t) { *t += 1; }
+
+// Flattened delivery for the latency-bound per-step case (a few dozen spikes
+// out of ~10^5 sources, ~10^3 synapses each): k_spike_compact (one block)
+// lists the spiking sources of the bitmap in ascending order with the
+// exclusive prefix of their synapse-row lengths; k_spike_scatter then gives
+// every (spike, synapse) pair its own thread (grid-stride), instead of one
+// block walking each word's rows serially.  The int64 fixed-point atomics
+// commute, so the ring is bit-identical to k_spike_deliver's.
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) k_spike_compact(int64_t words, const uint32_t* bits,
+                                                                    const int64_t* off, int32_t* src,
+                                                                    int64_t* pre, int64_t* totals) {
+  __shared__ int64_t scan[kCompactThreads];
+  const int tid = threadIdx.x;
+  const int64_t per = (words + kCompactThreads - 1) / kCompactThreads;
+  const int64_t w0 = tid * per, w1 = min(words, w0 + per);
+  int cnt = 0;
+  int64_t len = 0;
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t x = bits[w];
+    cnt += __popc(x);
+    while (x) {
+      const int b = __ffs(int(x)) - 1;
+      x &= x - 1;
+      const int64_t s = w * 32 + b;
+      len += off[s + 1] - off[s];
+    }
+  }
+  // block-wide exclusive scans of (count, length), packed: count << 40 | length
+  scan[tid] = (int64_t(cnt) << 40) | len;
+  __syncthreads();
+  for (int o = 1; o < kCompactThreads; o <<= 1) {
+    const int64_t v = tid >= o ? scan[tid - o] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  const int64_t incl = scan[tid];
+  const int64_t excl = incl - ((int64_t(cnt) << 40) | len);
+  int64_t k = excl >> 40, acc = excl & ((int64_t(1) << 40) - 1);
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t x = bits[w];
+    while (x) {
+      const int b = __ffs(int(x)) - 1;
+      x &= x - 1;
+      const int64_t s = w * 32 + b;
+      src[k] = int32_t(s);
+      pre[k] = acc;
+      acc += off[s + 1] - off[s];
+      ++k;
+    }
+  }
+  if (tid == kCompactThreads - 1) {
+    totals[0] = incl >> 40;                               // spikes
+    totals[1] = incl & ((int64_t(1) << 40) - 1);          // synapses
+    pre[incl >> 40] = totals[1];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spike_scatter(const int32_t* src, const int64_t* pre, const int64_t* totals,
+                                                       const int64_t* off, const int32_t* tgt, const int32_t* w,
+                                                       const int32_t* delay, int64_t t, const long long* t_dev,
+                                                       int64_t depth, int64_t n, long long* ring) {
+  const int64_t ns = totals[0], total = totals[1];
+  if (t_dev) t = *t_dev;
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+    // last k with pre[k] <= g
+    int64_t lo = 0, hi = ns;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(pre + mid) <= g) lo = mid;
+      else hi = mid;
+    }
+    const int64_t j = off[src[lo]] + (g - pre[lo]);
+    const int64_t slot = (t + delay[j]) % depth;
+    atomicAdd(reinterpret_cast<unsigned long long*>(ring + slot * n + tgt[j]),
+              static_cast<unsigned long long>(static_cast<long long>(w[j])));
+  }
+}
+
 }  // namespace cortex
 }  // namespace hhb
 
@@ -86,6 +175,15 @@ extern "C" {
 int hhb_cortex_input(int32_t dtype, int64_t n, int64_t t, int64_t depth, int64_t* ring, void* psp, double decay,
                      int32_t bg_mode, const void* bg, const double* lam, double mu, double sigma, uint64_t seed,
                      int64_t neuron_base, const void* extra, void* cur, double w_scale, void* stream) {
+  return hhb_cortex_input_dev(dtype, n, t, nullptr, depth, ring, psp, decay, bg_mode, bg, lam, mu, sigma, seed,
+                              neuron_base, extra, cur, w_scale, stream);
+}
+
+int hhb_cortex_input_dev(int32_t dtype, int64_t n, int64_t t, const int64_t* t_dev, int64_t depth, int64_t* ring,
+                         void* psp, double decay, int32_t bg_mode, const void* bg, const double* lam, double mu,
+                         double sigma, uint64_t seed, int64_t neuron_base, const void* extra, void* cur,
+                         double w_scale, void* stream) {
+  const long long* td = reinterpret_cast<const long long*>(t_dev);
   if (n <= 0) return HHB_OK;
   if (!ring || !psp || !cur || depth < 1 || (bg_mode == 1 && !bg) || (bg_mode == 2 && !lam))
     return fail(HHB_EINVAL, "bad cortex_input args");
@@ -93,12 +191,12 @@ int hhb_cortex_input(int32_t dtype, int64_t n, int64_t t, int64_t depth, int64_t
   long long* rg = reinterpret_cast<long long*>(ring);
   const unsigned grid = unsigned((n + 255) / 256);
   if (dtype == HHB_F32) {
-    cortex::k_cortex_input<float><<<grid, 256, 0, st>>>(n, t, depth, rg, (float*)psp, float(decay), bg_mode,
+    cortex::k_cortex_input<float><<<grid, 256, 0, st>>>(n, t, td, depth, rg, (float*)psp, float(decay), bg_mode,
                                                         (const float*)bg, lam, float(mu), float(sigma), seed,
                                                         neuron_base, (const float*)extra, (float*)cur,
                                                         float(w_scale));
   } else if (dtype == HHB_F64) {
-    cortex::k_cortex_input<double><<<grid, 256, 0, st>>>(n, t, depth, rg, (double*)psp, decay, bg_mode,
+    cortex::k_cortex_input<double><<<grid, 256, 0, st>>>(n, t, td, depth, rg, (double*)psp, decay, bg_mode,
                                                          (const double*)bg, lam, mu, sigma, seed, neuron_base,
                                                          (const double*)extra, (double*)cur, w_scale);
   } else {
@@ -110,11 +208,47 @@ int hhb_cortex_input(int32_t dtype, int64_t n, int64_t t, int64_t depth, int64_t
 int hhb_spike_deliver(int64_t words, const uint32_t* bits, const int64_t* offsets, const int32_t* targets,
                       const int32_t* weights_fx, const int32_t* delays, int64_t t, int64_t depth, int64_t n_local,
                       int64_t* ring, void* stream) {
+  return hhb_spike_deliver_dev(words, bits, offsets, targets, weights_fx, delays, t, nullptr, depth, n_local, ring,
+                               stream);
+}
+
+int hhb_spike_deliver_dev(int64_t words, const uint32_t* bits, const int64_t* offsets, const int32_t* targets,
+                          const int32_t* weights_fx, const int32_t* delays, int64_t t, const int64_t* t_dev,
+                          int64_t depth, int64_t n_local, int64_t* ring, void* stream) {
   if (words <= 0 || n_local <= 0) return HHB_OK;
   if (!bits || !offsets || !ring || depth < 1) return fail(HHB_EINVAL, "bad spike_deliver args");
   cortex::k_spike_deliver<<<unsigned(words), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      words, bits, offsets, targets, weights_fx, delays, t, depth, n_local, reinterpret_cast<long long*>(ring));
+      words, bits, offsets, targets, weights_fx, delays, t, reinterpret_cast<const long long*>(t_dev), depth,
+      n_local, reinterpret_cast<long long*>(ring));
   return cuda_check("k_spike_deliver launch");
+}
+
+int64_t hhb_spike_scratch(int64_t n_sources) { return 2 * n_sources + 3; }
+
+int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* offsets, const int32_t* targets,
+                           const int32_t* weights_fx, const int32_t* delays, int64_t t, const int64_t* t_dev,
+                           int64_t depth, int64_t n_local, int64_t* ring, int64_t* scratch, void* stream) {
+  if (words <= 0 || n_local <= 0) return HHB_OK;
+  if (!bits || !offsets || !ring || depth < 1 || !scratch) return fail(HHB_EINVAL, "bad spike_deliver_flat args");
+  if (words * 32 >= (int64_t(1) << 23))    // the compaction packs spike counts in 23 bits
+    return hhb_spike_deliver_dev(words, bits, offsets, targets, weights_fx, delays, t, t_dev, depth, n_local, ring,
+                                 stream);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // scratch (int64): totals[2] | pre[words*32 + 1] | src (int32, words*32)
+  int64_t* totals = scratch;
+  int64_t* pre = scratch + 2;
+  int32_t* src = reinterpret_cast<int32_t*>(pre + words * 32 + 1);
+  cortex::k_spike_compact<<<1, cortex::kCompactThreads, 0, st>>>(words, bits, offsets, src, pre, totals);
+  cortex::k_spike_scatter<<<2 * kNumSMs, 256, 0, st>>>(src, pre, totals, offsets, targets, weights_fx, delays, t,
+                                                        reinterpret_cast<const long long*>(t_dev), depth, n_local,
+                                                        reinterpret_cast<long long*>(ring));
+  return cuda_check("k_spike_compact / k_spike_scatter launch");
+}
+
+int hhb_cortex_tick(int64_t* t_dev, void* stream) {
+  if (!t_dev) return fail(HHB_EINVAL, "t_dev is NULL");
+  cortex::k_tick<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<long long*>(t_dev));
+  return cuda_check("k_tick launch");
 }
 
 }  // extern "C"

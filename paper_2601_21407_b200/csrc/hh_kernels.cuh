@@ -43,6 +43,7 @@ struct FwdArgs {
   int64_t nbase;    //   global id of neuron 0 of this launch
   T* spk_val;       // optional spike flags as 0/1 values [steps][spkv_ld] (SNN layer output)
   int64_t spkv_ld;
+  const long long* step_dev;   // optional: device value added to step_base
 };
 
 template <typename T>
@@ -295,8 +296,10 @@ struct Stimulus {
 
 // ------------------------------------------------------------ forward
 template <typename T, int NG, int VEC, bool POIS>
-__global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, const FwdArgs<T> a,
+__global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, const FwdArgs<T> a_in,
                                                          const PoissonTab<T> ptab) {
+  FwdArgs<T> a = a_in;
+  if (a.step_dev != nullptr) a.step_base += *a.step_dev;
   constexpr int NGX = NG > 0 ? NG : 1;
   const int lane = threadIdx.x & 31;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

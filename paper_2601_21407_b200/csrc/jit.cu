@@ -873,7 +873,7 @@ typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
-  float* spk_val; i64 spkv_ld; };
+  float* spk_val; i64 spkv_ld; const long long* step_dev; };
 struct PoissonTab { int size; float amp; float cdf[48]; };
 // Philox-4x32-10 with the key schedule precomputed on the host (one kernel
 // parameter per round key: LOP3 takes them straight from the constant bank)
@@ -1010,7 +1010,9 @@ struct Stimulus {
   }
 };
 template <int VEC, bool POIS>
-__device__ __forceinline__ void fwd_body(const FwdArgs& a, const PoissonTab& tab, const Keys& ks) {
+__device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& tab, const Keys& ks) {
+  FwdArgs a = a_in;
+  if (a.step_dev != nullptr) a.step_base += *a.step_dev;
   const int lane = threadIdx.x & 31;
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = tid * VEC;

@@ -331,6 +331,10 @@ class CortexNetwork:
         self.seed = int(seed)
         self.bg_buf = torch.empty(max(1, self.n), dtype=self.td, device=dev)
         self.t = 0
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=dev)   # step index for graph replay
+        self._graphs = {}
+        self.scratch = torch.empty(int(nat.load().hhb_spike_scratch(self.words_global * 32)), dtype=torch.int64,
+                                   device=dev)
 
     def _input(self, extra=None):
         lib = nat.load()
@@ -359,10 +363,10 @@ class CortexNetwork:
     def deliver(self, gwords: torch.Tensor):
         """Enqueue the synapses of every spiking source (global bitmap) whose
         target is local, then move to the next step."""
-        nat.check(nat.load().hhb_spike_deliver(
+        nat.check(nat.load().hhb_spike_deliver_flat(
             self.words_global, gwords.data_ptr(), self.off.data_ptr(), self.tgt.data_ptr(),
-            self.w.data_ptr(), self.delay.data_ptr(), self.t, self.depth, self.n, self.ring.data_ptr(),
-            D.stream()), "hhb_spike_deliver")
+            self.w.data_ptr(), self.delay.data_ptr(), self.t, None, self.depth, self.n, self.ring.data_ptr(),
+            self.scratch.data_ptr(), D.stream()), "hhb_spike_deliver")
         self.t += 1
 
     def step(self, extra=None):
@@ -374,6 +378,78 @@ class CortexNetwork:
             self.exchange(words, self.gwords)
         self.deliver(self.gwords)
         return self.gwords
+
+    # ---------------------------------------------------------------- graphs
+    def _step_dev(self):
+        """One step whose step index lives in self.t_dev (capturable)."""
+        lib = nat.load()
+        mode = 2 if (self.bg_mode == "philox" and self.bg_spec.rate_hz > 0) else 0
+        nat.check(lib.hhb_cortex_input_dev(
+            D.code(self.dtype), self.n, 0, self.t_dev.data_ptr(), self.depth, self.ring.data_ptr(),
+            self.psp.data_ptr(), self.decay, mode, None, self.lam.data_ptr(), self.bg_spec.w_mean,
+            self.bg_spec.w_std, self.seed, self.lo, None, self.cur.data_ptr(),
+            float(1.0 / (1 << W_FRAC_BITS)), D.stream()), "hhb_cortex_input_dev")
+        _forward(self.params, self.v, self.g, self.cur[:self.n], 0, 1, 1, v_fin=self.v, g_fin=self.g,
+                 bits=self.words.view(1, -1), step_base=0, first_bad=self.first_bad, reset_bad=False,
+                 step_dev=self.t_dev)
+        if self.exchange is None:
+            gw = self.words            # one rank: the local bitmap is the global one (no copy)
+        else:
+            self.exchange(self.words, self.gwords)
+            gw = self.gwords
+        nat.check(lib.hhb_spike_deliver_flat(
+            self.words_global, gw.data_ptr(), self.off.data_ptr(), self.tgt.data_ptr(),
+            self.w.data_ptr(), self.delay.data_ptr(), 0, self.t_dev.data_ptr(), self.depth, self.n,
+            self.ring.data_ptr(), self.scratch.data_ptr(), D.stream()), "hhb_spike_deliver_flat")
+        nat.check(lib.hhb_cortex_tick(self.t_dev.data_ptr(), D.stream()), "hhb_cortex_tick")
+        return gw
+
+    def advance(self, n_steps: int, steps_per_graph: int = 64, record: torch.Tensor | None = None):
+        """Advance n_steps by replaying a CUDA graph of `steps_per_graph`
+        network steps (input, HH step, exchange, delivery, tick): the per-step
+        host work of `step()` (~5 launches) becomes one graph launch per
+        steps_per_graph steps.  Results are bit-identical to `step()`.
+        record: optional int32 [n_steps][words_global] device buffer receiving
+        each step's global spike words.  Host-RNG background cannot be captured
+        (use step())."""
+        if self.bg_mode == "host":
+            raise UsageError("advance(): the host background is drawn per step; use step()")
+        self.t_dev.fill_(self.t)
+        S = max(1, min(int(steps_per_graph), n_steps)) if n_steps > 0 else 1
+        done = 0
+        rec_key = record is not None
+        if n_steps >= S:
+            key = (S, rec_key)
+            if key not in self._graphs:
+                buf = torch.empty((S, self.words_global), dtype=torch.int32, device=self.dev) if rec_key else None
+                t0 = self.t_dev.clone()
+                snap = (self.v.clone(), self.g.clone(), self.psp.clone(), self.ring.clone())
+                self._step_dev()                  # warm-up outside capture (module load, allocations)
+                self.t_dev.copy_(t0)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for k in range(S):
+                        gw = self._step_dev()
+                        if rec_key:
+                            buf[k].copy_(gw[:self.words_global])
+                # the capture did not run the steps; undo the warm-up step
+                self.v.copy_(snap[0]); self.g.copy_(snap[1]); self.psp.copy_(snap[2]); self.ring.copy_(snap[3])
+                self.t_dev.copy_(t0)
+                self._graphs[key] = (g, buf)
+            g, buf = self._graphs[key]
+            while n_steps - done >= S:
+                g.replay()
+                if rec_key:
+                    record[done:done + S].copy_(buf)
+                done += S
+        while done < n_steps:
+            gw = self._step_dev()
+            if rec_key:
+                record[done].copy_(gw[:self.words_global])
+            done += 1
+        self.t += n_steps
+        return record
 
     def run(self, n_steps: int, record: bool = True):
         """Advance n_steps; returns (times_ms, neuron_ids) of the spikes of ALL

@@ -77,3 +77,26 @@ def test_philox_background_moments(cuda):
         L = lam[p.offset]
         assert abs(xs.mean() - L * mu) < 0.02 * L * mu
         assert abs(xs.var() - L * (mu * mu + sd * sd)) < 0.05 * L * (mu * mu + sd * sd)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_graph_replay_equals_eager_steps(cuda, dtype):
+    """CortexNetwork.advance (CUDA graph of S steps, step index on the device)
+    must reproduce step() bit for bit: rasters, membrane state and ring."""
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    a = N.CortexNetwork(topo, cfg, device=cuda, dtype=dtype, background="philox", seed=3)
+    b = N.CortexNetwork(topo, cfg, device=cuda, dtype=dtype, background="philox", seed=3)
+    steps = 250                       # 3 graph replays of 64 + 58 eager device steps
+    rows = torch.stack([a.step().clone() for _ in range(steps)])
+    rec = torch.empty((steps, b.words_global), dtype=torch.int32, device=cuda)
+    b.advance(steps, steps_per_graph=64, record=rec)
+    assert rows.any()
+    assert torch.equal(rows, rec)
+    assert torch.equal(a.v, b.v) and torch.equal(a.g, b.g) and torch.equal(a.ring, b.ring)
+    assert a.t == b.t == steps
+    # and continuing after a replay (t on the device resynchronised)
+    more = torch.stack([a.step().clone() for _ in range(70)])
+    rec2 = torch.empty((70, b.words_global), dtype=torch.int32, device=cuda)
+    b.advance(70, steps_per_graph=64, record=rec2)
+    assert torch.equal(more, rec2)
