@@ -1323,7 +1323,9 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = -2) {
   // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
-  src += fmt("#define BWD_MINB %d\n", bmb ? atoi(bmb) : 1);
+  // 6 resident 128-thread blocks (<= 80 registers, no spills for up to 6 gates)
+  // measured best at the config-3 shape: 259 us vs 276 us unconstrained
+  src += fmt("#define BWD_MINB %d\n", bmb ? atoi(bmb) : 6);
   src += emit_near_linoid(P);
   src += emit_forward_step(P, L, kFast);
   src += emit_forward_step(P, L, kSeries);
