@@ -238,6 +238,7 @@ def fwd_bwd_leg(torch, dev):
 
     def step():
         layer.zero_grad(set_to_none=True)
+        x.grad = None            # dX is produced every step, not accumulated across steps
         V, S = layer(x)
         # MSE(V, 0): one reduction forward, one elementwise pass backward
         # (seed_v = 2 V / numel, learn.py:86-88)

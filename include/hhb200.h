@@ -335,6 +335,10 @@ int64_t hhb_spike_scratch(int64_t n_sources);
  * hhb_jit_status: "ok", "not initialised" or the reason the JIT is off.
  * hhb_jit_source: writes the generated CUDA source for `params` into buf
  * (NUL-terminated, truncated to cap) and returns the full size + 1, or -1. */
+/* out[i] = x[i] * (scale[0] * c), fp32, scale read on the device: the
+ * autograd seed of a reduction loss, e.g. MSE's 2 (V - target) / n times the
+ * incoming gradient (learn.py:86-88), in one pass with no host sync. */
+int hhb_scale_f32(int64_t n, const float* x, const float* scale, double c, float* out, void* stream);
 const char* hhb_jit_status(void);
 int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap);
 

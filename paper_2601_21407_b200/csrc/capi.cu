@@ -133,6 +133,25 @@ static int backward_t(const hhb_params_t* P, const hhb_surrogate_t* S, int64_t n
 
 using namespace hhb;
 
+// out = x * (scale[0] * c): the autograd seed of a reduction loss (learn.py:86-88
+// seed 2 diff / n times the incoming gradient) in one vectorised pass, the scale
+// read on the device (no host sync)
+static __global__ void k_scale_f32(int64_t n4, const float4* x, const float* scale, float c, float4* out) {
+  const float k = scale[0] * c;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = x[i];
+    v.x *= k;
+    v.y *= k;
+    v.z *= k;
+    v.w *= k;
+    out[i] = v;
+  }
+}
+static __global__ void k_scale_tail(int64_t n, const float* x, const float* scale, float c, float* out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = x[i] * (scale[0] * c);
+}
+
 // independent 8-wide chains so the probe measures pipe throughput, not latency
 static __global__ void __launch_bounds__(256) k_pipe_probe(int which, int64_t iters, float* sink) {
   float x[8];
@@ -388,6 +407,22 @@ int hhb_poisson_current(int32_t dtype, int64_t n, int64_t n_steps, uint64_t seed
                                    ld, ST(stream));
   return Flavour<double>::poisson(n, n_steps, seed, neuron_base, step_base, lam, amp, (double*)out,
                                   ld, ST(stream));
+}
+
+int hhb_scale_f32(int64_t n, const float* x, const float* scale, double c, float* out, void* stream) {
+  if (n <= 0) return HHB_OK;
+  if (!x || !scale || !out) return fail(HHB_EINVAL, "hhb_scale_f32: NULL pointer");
+  cudaStream_t st = ST(stream);
+  int64_t done = 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+    const int64_t n4 = n / 4;
+    if (n4 > 0)
+      k_scale_f32<<<grid_1d(n4, 256), 256, 0, st>>>(n4, reinterpret_cast<const float4*>(x), scale, float(c),
+                                                    reinterpret_cast<float4*>(out));
+    done = n4 * 4;
+  }
+  if (done < n) k_scale_tail<<<grid_1d(n - done, 256), 256, 0, st>>>(n - done, x + done, scale, float(c), out + done);
+  return cuda_check("k_scale launch");
 }
 
 const char* hhb_jit_status(void) { return jit_status(); }

@@ -15,6 +15,7 @@ import numpy as np
 import torch
 
 from . import _device as D
+from . import _native as nat
 from .errors import UsageError
 
 
@@ -66,7 +67,13 @@ class _MSE(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         (diff,) = ctx.saved_tensors
-        seed = diff * (g * (2.0 / diff.numel()))
+        c = 2.0 / diff.numel()
+        if diff.dtype == torch.float32 and diff.is_contiguous() and g.dtype == torch.float32:
+            seed = torch.empty_like(diff)
+            nat.check(nat.load().hhb_scale_f32(diff.numel(), diff.data_ptr(), g.contiguous().data_ptr(), c,
+                                               seed.data_ptr(), D.stream()), "hhb_scale_f32")
+        else:
+            seed = diff * (g * c)
         return seed, (-seed if ctx.has_target else None)
 
 

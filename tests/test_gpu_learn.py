@@ -43,3 +43,12 @@ def test_mse_autograd_gradient_is_the_reference_seed(cuda, with_target):
                                     np.zeros((40, 3, 8)) if t is None else t.cpu().numpy())
     assert abs(loss.item() - ref_loss) <= 1e-12 * ref_loss
     assert np.allclose(v.grad.cpu().numpy(), ref_seed, rtol=1e-12, atol=0)
+
+
+def test_mse_autograd_fp32_fused_seed(cuda):
+    """float32 path: the seed comes from hhb_scale_f32 (one pass, device scale)."""
+    g = torch.Generator(device=cuda).manual_seed(4)
+    v = torch.randn((100, 7, 33), device=cuda, generator=g).requires_grad_(True)   # n % 4 != 0 tail
+    (3.0 * L.mse(v)).backward()
+    ref = 3.0 * 2.0 * v.detach().double() / v.numel()
+    assert torch.allclose(v.grad.double(), ref, rtol=1e-6, atol=0)
