@@ -1157,33 +1157,57 @@ __device__ __forceinline__ void cpa4(float* dst, const float* src) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory"); }
 
-extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const Sur sur, const BwdArgs a) {
-  __shared__ float ring[DEPTH * RING_STRIDE];
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool on = i < a.n;
-  const i64 ii = on ? i : 0;
+// VEC neurons per thread (1 or 2; 2 when the host proved every stream 8-byte
+// aligned and neuron-contiguous): a block always covers BWD_THREADS neurons, so
+// the partial-sum layout (one slot row per block) is the same for both.
+template <int VEC>
+__device__ __forceinline__ void cpa(float* dst, const float* src) {
+  if (VEC == 2)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((u32)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((u32)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
+  constexpr int TPB = BWD_THREADS / VEC;
+  __shared__ __align__(16) float ring[DEPTH * RING_STRIDE];
+  const i64 i0 = i64(blockIdx.x) * BWD_THREADS + i64(threadIdx.x) * VEC;
+  bool on[VEC];
+  i64 ii[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    on[j] = i0 + j < a.n;
+    ii[j] = on[j] ? i0 + j : 0;
+  }
+  const i64 ib0 = on[0] ? i0 : 0;      // VEC == 2: the host guarantees n even (both or neither on)
   double acc[SLOTS];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) acc[s] = 0.0;
   float accf[SLOTS];
   cb_zero(accf);
   int nf = 0;
-  double csum = 0.0;
-  float csumf = 0.0f;
+  double csum[VEC];
+  float csumf[VEC];
   i64 bad = -1;
-  float d_v = on ? a.adj_v[ii] : 0.0f;
-  float d_p[NGX];
+  float d_v[VEC], d_p[VEC][NGX];
 #pragma unroll
-  for (int g = 0; g < NG; ++g) d_p[g] = on ? a.adj_g[g * a.ag_ld + ii] : 0.0f;
+  for (int j = 0; j < VEC; ++j) {
+    csum[j] = 0.0;
+    csumf[j] = 0.0f;
+    d_v[j] = on[j] ? a.adj_v[ii[j]] : 0.0f;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) d_p[j][g] = on[j] ? a.adj_g[g * a.ag_ld + ii[j]] : 0.0f;
+  }
   const i64 K = BF_K1 ? 1 : a.ck_every;
   const i64 sstride = (1 + NG) * a.ck_ld;
   i64 goff[NGX];
 #pragma unroll
   for (int g = 0; g < NG; ++g) goff[g] = (1 + g) * a.ck_ld;
-  const float* ib = a.i_ext + ii * a.i_sn;
-  const float* svb = BF_SV ? a.seed_v + ii : nullptr;
-  const float* ssb = BF_SS ? a.seed_s + ii : nullptr;
-  float* const ring_t = ring + threadIdx.x;
+  const float* ib = a.i_ext + ib0 * a.i_sn;
+  const float* svb = BF_SV ? a.seed_v + ib0 : nullptr;
+  const float* ssb = BF_SS ? a.seed_s + ib0 : nullptr;
+  float* const ring_t = ring + threadIdx.x * VEC;
   // K == 1: one stream over all steps; K > 1: one stream per recomputed segment
   const i64 nseg = BF_K1 ? 1 : (a.steps + K - 1) / K;
   for (i64 seg = nseg - 1; seg >= 0; --seg) {
@@ -1191,19 +1215,22 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
     const i64 hi = BF_K1 ? a.steps : ((lo + K < a.steps) ? lo + K : a.steps);
     const float* ck = a.ckpt + seg * sstride;
     if (!BF_K1) {
-      float v, p[NGX];
-      load_state(ck, a.ck_ld, ii, v, p);
-      float* sp = a.seg + sstride;
-      const float* ip = ib + lo * a.i_st;
-      for (i64 t = lo; t < hi - 1; ++t) {
-        v = step_fwd(v, p, __ldg(ip));
-        ip += a.i_st;
-        if (on) store_state(sp, a.ck_ld, ii, v, p);
-        sp += sstride;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        float v, p[NGX];
+        load_state(ck, a.ck_ld, ii[j], v, p);
+        float* sp = a.seg + sstride;
+        const float* ip = a.i_ext + ii[j] * a.i_sn + lo * a.i_st;
+        for (i64 t = lo; t < hi - 1; ++t) {
+          v = step_fwd(v, p, __ldg(ip));
+          ip += a.i_st;
+          if (on[j]) store_state(sp, a.ck_ld, ii[j], v, p);
+          sp += sstride;
+        }
       }
     }
     // issue pointers: operands of step tn (walk down from hi - 1)
-    const float* rq = BF_K1 ? a.ckpt + (hi - 1) * sstride + ii : a.seg + (hi - 1 - lo) * sstride + ii;
+    const float* rq = BF_K1 ? a.ckpt + (hi - 1) * sstride + ib0 : a.seg + (hi - 1 - lo) * sstride + ib0;
     const float* iq = ib + (hi - 1) * a.i_st;
     const float* vq = BF_SV ? svb + (hi - 1) * a.sv_ld : nullptr;
     const float* sq = BF_SS ? ssb + (hi - 1) * a.ss_ld : nullptr;
@@ -1211,13 +1238,13 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
     int wslot = 0;
     auto issue = [&]() {
       float* r = ring_t + wslot * RING_STRIDE;
-      const float* src = (!BF_K1 && tn == lo) ? ck + ii : rq;
-      cpa4(r, src);
+      const float* src = (!BF_K1 && tn == lo) ? ck + ib0 : rq;
+      cpa<VEC>(r, src);
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cpa4(r + (1 + g) * BWD_THREADS, src + goff[g]);
-      cpa4(r + (NG + 1) * BWD_THREADS, iq);
-      if (BF_SV) cpa4(r + (NG + 2) * BWD_THREADS, vq);
-      if (BF_SS) cpa4(r + (NG + 3) * BWD_THREADS, sq);
+      for (int g = 0; g < NG; ++g) cpa<VEC>(r + (1 + g) * BWD_THREADS, src + goff[g]);
+      cpa<VEC>(r + (NG + 1) * BWD_THREADS, iq);
+      if (BF_SV) cpa<VEC>(r + (NG + 2) * BWD_THREADS, vq);
+      if (BF_SS) cpa<VEC>(r + (NG + 3) * BWD_THREADS, sq);
     };
     auto advance = [&]() {
       --tn;
@@ -1233,10 +1260,10 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
       cpa_commit();
       advance();
     }
-    float* dib = (BF_DI && on) ? a.d_i + (hi - 1) * a.di_ld + ii : nullptr;
-    const i64 scol = a.dh_grp > 0 ? (ii / a.dh_grp) * a.dh_pitch + ii % a.dh_grp : ii;
-    unsigned short* dhb = (BF_SPLIT && on) ? a.di_hi + (hi - 1) * a.dh_ld + scol : nullptr;
-    unsigned short* dlb = (BF_SPLIT && on) ? a.di_lo + (hi - 1) * a.dh_ld + scol : nullptr;
+    float* dib = (BF_DI && on[0]) ? a.d_i + (hi - 1) * a.di_ld + ib0 : nullptr;
+    const i64 scol = a.dh_grp > 0 ? (ib0 / a.dh_grp) * a.dh_pitch + ib0 % a.dh_grp : ib0;
+    unsigned short* dhb = (BF_SPLIT && on[0]) ? a.di_hi + (hi - 1) * a.dh_ld + scol : nullptr;
+    unsigned short* dlb = (BF_SPLIT && on[0]) ? a.di_lo + (hi - 1) * a.dh_ld + scol : nullptr;
     int rslot = 0;
     for (i64 t = hi - 1; t >= lo; --t) {
       if (tn >= lo) issue();
@@ -1245,55 +1272,76 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
       cpa_wait();
       const float* r = ring_t + rslot * RING_STRIDE;
       rslot = (rslot + 1) & (DEPTH - 1);
-      float v = r[0], p[NGX];
+      float di[VEC];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) p[g] = r[(1 + g) * BWD_THREADS];
-      const float cur = r[(NG + 1) * BWD_THREADS];
-      if (BF_SV) d_v = __fadd_rn(d_v, r[(NG + 2) * BWD_THREADS]);
-      const float ds = BF_SS ? r[(NG + 3) * BWD_THREADS] : 0.0f;
-      const float di = step_bwd(sur, v, p, cur, d_v, d_p, ds, BF_SS, accf);
-      if (BF_SUM) csumf = __fadd_rn(csumf, di);
+      for (int j = 0; j < VEC; ++j) {
+        float v = r[j], p[NGX];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) p[g] = r[(1 + g) * BWD_THREADS + j];
+        const float cur = r[(NG + 1) * BWD_THREADS + j];
+        if (BF_SV) d_v[j] = __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
+        const float ds = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
+        di[j] = step_bwd(sur, v, p, cur, d_v[j], d_p[j], ds, BF_SS, accf);
+        if (BF_SUM) csumf[j] = __fadd_rn(csumf[j], di[j]);
+      }
       if (++nf == 8) {
         cb_flush(acc, accf);
         if (BF_SUM) {
-          csum += double(csumf);
-          csumf = 0.0f;
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            csum[j] += double(csumf[j]);
+            csumf[j] = 0.0f;
+          }
         }
         nf = 0;
       }
-      if (BF_DI && on) {
-        *dib = di;
+      if (BF_DI && on[0]) {
+        if (VEC == 2) *reinterpret_cast<float2*>(dib) = make_float2(di[0], di[VEC - 1]);
+        else *dib = di[0];
         dib -= a.di_ld;
       }
-      if (BF_SPLIT && on) {
-        unsigned short h, l;
-        split_bf16(di, h, l);
-        *dhb = h;
-        *dlb = l;
+      if (BF_SPLIT && on[0]) {
+        unsigned short h[VEC], l[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) split_bf16(di[j], h[j], l[j]);
+        if (VEC == 2) {
+          *reinterpret_cast<u32*>(dhb) = u32(h[0]) | (u32(h[VEC - 1]) << 16);
+          *reinterpret_cast<u32*>(dlb) = u32(l[0]) | (u32(l[VEC - 1]) << 16);
+        } else {
+          *dhb = h[0];
+          *dlb = l[0];
+        }
         dhb -= a.dh_ld;
         dlb -= a.dh_ld;
       }
-      bool ok = finitef_(d_v);
+      bool ok = true;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[g]);
-      if (!ok && bad < 0 && on) bad = a.step_base + t;
+      for (int j = 0; j < VEC; ++j) {
+        ok = ok && finitef_(d_v[j]);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) ok = ok && finitef_(d_p[j][g]);
+      }
+      if (!ok && bad < 0 && on[0]) bad = a.step_base + t;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
   cb_flush(acc, accf);
-  csum += double(csumf);
-  if (on) {
-    a.adj_v[ii] = d_v;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii] = d_p[g];
-    if (BF_SUM) a.di_sum[ii] += float(csum);
+  for (int j = 0; j < VEC; ++j) {
+    csum[j] += double(csumf[j]);
+    if (on[j]) {
+      a.adj_v[ii[j]] = d_v[j];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) a.adj_g[g * a.ag_ld + ii[j]] = d_p[j][g];
+      if (BF_SUM) a.di_sum[ii[j]] += float(csum[j]);
+    }
   }
   if (bad >= 0) atomicMax(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
-  __shared__ double red[BWD_THREADS / 32][SLOTS];
+  __shared__ double red[TPB / 32][SLOTS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
-    double x = on ? acc[s] : 0.0;
+    double x = on[0] ? acc[s] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     if (lane == 0) red[warp][s] = x;
@@ -1301,9 +1349,15 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const
   __syncthreads();
   if (threadIdx.x < SLOTS) {
     double x = 0.0;
-    for (int w = 0; w < BWD_THREADS / 32; ++w) x += red[w][threadIdx.x];
+    for (int w = 0; w < TPB / 32; ++w) x += red[w][threadIdx.x];
     a.partials[i64(blockIdx.x) * SLOTS + threadIdx.x] = x;
   }
+}
+extern "C" __global__ void __launch_bounds__(BWD_THREADS, BWD_MINB) hh_bwd(const Sur sur, const BwdArgs a) {
+  bwd_body<1>(sur, a);
+}
+extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2(const Sur sur, const BwdArgs a) {
+  bwd_body<2>(sur, a);
 }
 )";
 
@@ -1322,6 +1376,8 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = -2) {
   // measured best for config 2 on B200 (profiles/r1_variants.md: 1.49e11 vs
   // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
+  const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
+  src += fmt("#define BWD2_MINB %d\n", bmb2 ? atoi(bmb2) : 6);
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
   // 6 resident 128-thread blocks (<= 80 registers, no spills for up to 6 gates)
   // measured best at the config-3 shape: 259 us vs 276 us unconstrained
@@ -1457,7 +1513,7 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
 
 // ------------------------------------------------------------ cache
 struct Module {
-  CUfunction fwd1 = nullptr, fwd4 = nullptr, fwdp1 = nullptr, fwdp4 = nullptr, bwd = nullptr;
+  CUfunction fwd1 = nullptr, fwd4 = nullptr, fwdp1 = nullptr, fwdp4 = nullptr, bwd = nullptr, bwd2 = nullptr;
   bool ok = false;
 };
 static std::map<std::string, Module> g_cache;
@@ -1485,6 +1541,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += mg::disabled() ? "nomerge" : "";
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
   k += bmb ? std::string("b") + bmb : "";
+  const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
+  k += bmb2 ? std::string("c") + bmb2 : "";
   return k;
 }
 
@@ -1535,7 +1593,8 @@ static Module* get_module(const hhb_params_t* P, int bwd_flags) {
     loaded = g_drv.get(&m.fwd1, mod, "hh_fwd_v1") == CUDA_SUCCESS && g_drv.get(&m.fwd4, mod, "hh_fwd_v4") == CUDA_SUCCESS &&
              g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") == CUDA_SUCCESS &&
              g_drv.get(&m.fwdp4, mod, "hh_fwdp_v4") == CUDA_SUCCESS;
-  if (loaded && bwd_flags >= 0) loaded = g_drv.get(&m.bwd, mod, "hh_bwd") == CUDA_SUCCESS;
+  if (loaded && bwd_flags >= 0)
+    loaded = g_drv.get(&m.bwd, mod, "hh_bwd") == CUDA_SUCCESS && g_drv.get(&m.bwd2, mod, "hh_bwd2") == CUDA_SUCCESS;
   if (!loaded) {
     g_status = "cuModuleLoadData / cuModuleGetFunction failed";
     return nullptr;
@@ -1583,7 +1642,19 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
   DevSur<float> s = sur;
   BwdArgs<float> args = a;
   void* params[] = {&s, &args};
-  const CUresult r = jit::g_drv.launch(m->bwd, unsigned(blocks), 1, 1, unsigned(kBwdThreads), 1, 1, 0,
+  // two neurons per thread when every stream is neuron-contiguous and 8-byte
+  // aligned for the pair (float2 / packed bf16x2 accesses)
+  auto even = [](int64_t x) { return (x & 1) == 0; };
+  auto al8 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; };
+  const bool vec2 = !getenv("HHB_JIT_BWD_VEC1") && even(a.n) && a.i_sn == 1 && even(a.i_st) && even(a.ck_ld) &&
+                    al8(a.i_ext) && al8(a.ckpt) && (a.ck_every == 1 || al8(a.seg)) &&
+                    (!a.seed_v || (even(a.sv_ld) && al8(a.seed_v))) &&
+                    (!a.seed_s || (even(a.ss_ld) && al8(a.seed_s))) && (!a.d_i || (even(a.di_ld) && al8(a.d_i))) &&
+                    (!a.di_hi || (even(a.dh_ld) && (a.dh_grp == 0 || (even(a.dh_grp) && even(a.dh_pitch))) &&
+                                  (reinterpret_cast<uintptr_t>(a.di_hi) & 3) == 0 &&
+                                  (reinterpret_cast<uintptr_t>(a.di_lo) & 3) == 0));
+  const CUresult r = jit::g_drv.launch(vec2 ? m->bwd2 : m->bwd, unsigned(blocks), 1, 1,
+                                       unsigned(vec2 ? kBwdThreads / 2 : kBwdThreads), 1, 1, 0,
                                        reinterpret_cast<CUstream>(st), params, nullptr);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit backward launch failed");
   return true;
