@@ -1272,17 +1272,36 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
       cpa_wait();
       const float* r = ring_t + rslot * RING_STRIDE;
       rslot = (rslot + 1) & (DEPTH - 1);
-      float di[VEC];
+      float di[VEC], v[VEC], p[VEC][NGX], cur[VEC], ds[VEC];
+      bool reg = true;
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        float v = r[j], p[NGX];
+        v[j] = r[j];
 #pragma unroll
-        for (int g = 0; g < NG; ++g) p[g] = r[(1 + g) * BWD_THREADS + j];
-        const float cur = r[(NG + 1) * BWD_THREADS + j];
+        for (int g = 0; g < NG; ++g) p[j][g] = r[(1 + g) * BWD_THREADS + j];
+        cur[j] = r[(NG + 1) * BWD_THREADS + j];
         if (BF_SV) d_v[j] = __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
-        const float ds = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
-        di[j] = step_bwd(sur, v, p, cur, d_v[j], d_p[j], ds, BF_SS, accf);
-        if (BF_SUM) csumf[j] = __fadd_rn(csumf[j], di[j]);
+        ds[j] = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
+#if HAS_MERGED
+        reg = reg && regular(v[j]);
+#endif
+      }
+#if HAS_MERGED
+      // one warp vote per step for all VEC neurons of every lane
+      if (__all_sync(0xffffffffu, reg)) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) di[j] = step_bwd_m(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) di[j] = step_bwd_irr(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+      }
+#else
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) di[j] = step_bwd(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+#endif
+      if (BF_SUM) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) csumf[j] = __fadd_rn(csumf[j], di[j]);
       }
       if (++nf == 8) {
         cb_flush(acc, accf);
@@ -1475,6 +1494,25 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
       "const float cur, float& d_v, float (&d_p)[NGX], const float d_spike, const bool has_s, float (&cb)[SLOTS])";
   if (M.ok) {
     src += emit_backward_step(P, L, kSeries, &M);
+    src += "#define HAS_MERGED 1\n";
+    src += R"(// some lane of the warp left the merged form's window: both forms, per lane
+__device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, const float (&p)[NGX], const float cur,
+                                           float& d_v, float (&d_p)[NGX], const float d_spike, const bool has_s,
+                                           float (&cb)[SLOTS]) {
+  float dvm = d_v, dpm[NGX], accm[SLOTS];
+#pragma unroll
+  for (int g = 0; g < NGX; ++g) dpm[g] = d_p[g];
+  cb_copy(accm, cb);
+  const float dim = step_bwd_m(sur, v, p, cur, dvm, dpm, d_spike, has_s, accm);
+  const float dis = step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
+  const bool reg = regular(v);
+  d_v = reg ? dvm : d_v;
+#pragma unroll
+  for (int g = 0; g < NGX; ++g) d_p[g] = reg ? dpm[g] : d_p[g];
+  cb_sel(reg, cb, accm);
+  return reg ? dim : dis;
+}
+)";
     src += std::string(bwd_sig) + R"( {
   if (__all_sync(0xffffffffu, regular(v))) return step_bwd_m(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
   // some lane left the window: both forms, selected per lane
@@ -1493,6 +1531,7 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
 }
 )";
   } else {
+    src += "#define HAS_MERGED 0\n";
     src += std::string(bwd_sig) + R"( {
   return __any_sync(0xffffffffu, near_linoid(v)) ? step_bwd_s(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb)
                                                  : step_bwd_f(sur, v, p, cur, d_v, d_p, d_spike, has_s, cb);
