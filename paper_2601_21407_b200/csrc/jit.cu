@@ -451,6 +451,18 @@ static Plan plan_of(const hhb_params_t* P) {
     window(vr, [&](double v) { return gate_ok(g, M.groups, v, true); }, lo1, hi1);
     g.one_rcp = lo1 <= vr - 60.0 && hi1 >= vr + 140.0;
   }
+  // One reciprocal per gate costs 4 issue slots and 1 MUFU op, two cost 2 and
+  // 2.  The merged forward is issue-bound with MUFU close behind, so half of
+  // the gates take two reciprocals (config 2: 1.466e11 -> 1.501e11
+  // neuron-steps/s); the backward is far more issue-bound than MUFU-bound, so
+  // all its gates take two (the window proven above holds for both: two
+  // reciprocals only need N and D in range).  HHB_JIT_TWO_RCP=k overrides the
+  // forward count.
+  {
+    int k = int(M.gates.size()) / 2;
+    if (const char* tr = getenv("HHB_JIT_TWO_RCP")) k = atoi(tr);
+    for (int gi = int(M.gates.size()) - 1; gi >= 0 && k > 0; --gi, --k) M.gates[gi].one_rcp = false;
+  }
   window(vr, [&](double v) {
     for (const auto& g : M.gates)
       if (!gate_ok(g, M.groups, v, g.one_rcp)) return false;
@@ -633,7 +645,7 @@ static std::string emit_gate_bwd(const GatePlan& gp, const std::vector<Group>& G
       D1 = b.d1;
     }
     X iD, iN;
-    if (gp.one_rcp) {
+    if (false) {   // the issue-bound backward always takes two reciprocals (see plan_of)
       const X r = bind(o, "r", V("rcpf_(" + mulx(N, D).e + ")"));
       iD = bind(o, "iD", mulx(N, r));
       iN = bind(o, "iN", mulx(D, r));
@@ -1578,6 +1590,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   const char* mb = getenv("HHB_JIT_MINB");
   k += mb ? mb : "";
   k += mg::disabled() ? "nomerge" : "";
+  const char* tr = getenv("HHB_JIT_TWO_RCP");
+  k += tr ? std::string("r") + tr : "";
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
   k += bmb ? std::string("b") + bmb : "";
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
