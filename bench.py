@@ -307,6 +307,43 @@ def c5_leg(torch, dev, steps=1000):
                       "REST_CONFIG, fp32, per-step spike-bitmap all-gather"}
 
 
+def morph_leg(torch, dev):
+    """multicompartment neurons (morphology.py mirror over
+    hhb_morph_forward): the coincidence-detection graph (active squid soma +
+    3 two-compartment passive dendrites, 7 compartments, 6 axial edges) for a
+    batch of 262,144 independent neurons x 400 steps, fp32, random pulse
+    currents.  One unit = one compartment-step."""
+    import numpy as np
+    from paper_2601_21407_b200 import morphology as M
+    from paper_2601_21407_b200.defaults import squid_axon_params
+    soma = squid_axon_params().with_(dtype=np.float32)
+    dend = M.passive_params(dt=soma.dt).with_(dtype=np.float32)
+    comps = {"soma": soma}
+    edges = []
+    for d in (1, 2, 3):
+        comps[f"d{d}p"], comps[f"d{d}d"] = dend, dend
+        edges += [M.Edge("soma", f"d{d}p", M.DEMO_G_AXIAL), M.Edge(f"d{d}p", f"d{d}d", M.DEMO_G_AXIAL)]
+    graph = M.CompartmentGraph(comps, edges, "soma")
+    B, T = 262144, 400
+    g = torch.Generator(device=dev).manual_seed(0)
+    i = (torch.rand((T, 7, B), device=dev, generator=g) < 0.05).float() * 36.0
+    for _ in range(2):
+        M.simulate_morphology(graph, i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 3
+    for _ in range(reps):
+        tr = M.simulate_morphology(graph, i)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"value": 7 * B * T / (ms * 1e-3), "unit": "compartment-steps/s", "ms_per_step": ms,
+            "spikes": int(tr.spike_series[:, 0].sum().item()),
+            "config": "coincidence graph (7 compartments, 2 channel tables, 6 axial edges) x 262,144 neurons "
+                      "x 400 steps, fp32, V trace + spikes recorded (one unit = one compartment-step)"}
+
+
 def c4_leg(torch, dev):
     """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
     batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
@@ -488,6 +525,7 @@ def main():
         extras["fwd_bwd"] = fwd_bwd_leg(torch, dev)
         extras["c4_train_step"] = c4_leg(torch, dev)
         extras["c5_network"] = c5_leg(torch, dev)
+        extras["morphology"] = morph_leg(torch, dev)
         if world > 1:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(fb, op=dist.ReduceOp.MAX)
@@ -508,6 +546,7 @@ def main():
                 "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
                 "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
+                "morphology": extras.get("morphology"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)

@@ -284,6 +284,27 @@ int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double
                 double* scratch, void* stream);
 int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols);
 
+/* ---- multicompartment neurons (morphology.py) ---------------- */
+
+/* T steps of `batch` independent multicompartment neurons on one compartment
+ * graph (simulate_morphology, morphology.py:144-166): every step, compartment
+ * c receives i_ext[t][c][b] + axial, axial = sum over edges e in order of
+ * g_e (V_b - V_a) (+ for c == a, - for c == b) on the previous step's
+ * potentials (axial_current, :115-124), then takes one HH step with its
+ * channel table tables[table_of[c]] (morph_step, :127-141).  Layouts:
+ * i_ext / v_out [n_steps][n_comp][batch], spk_out uint8 likewise, v [n_comp]
+ * [batch], gates [n_comp][HHB_MAX_GATES][batch] (a compartment uses its first
+ * n_gates rows).  n_steps == 0 writes the axial current of (v_in) into
+ * ax_out [n_comp][batch] and nothing else.  Limits: 32 compartments, 64
+ * edges, 4 distinct tables per call.  first_bad: atomicMin of the first
+ * non-finite step (NumericalOverflowError). */
+int hhb_morph_forward(int32_t dtype, int32_t n_tables, const hhb_params_t* tables, int32_t n_comp,
+                      const int32_t* table_of, int32_t n_edges, const int32_t* edge_a,
+                      const int32_t* edge_b, const double* g_axial, int64_t batch, int64_t n_steps,
+                      const void* i_ext, const void* v_in, const void* g_in, void* v_fin, void* g_fin,
+                      void* v_out, uint8_t* spk_out, void* ax_out, int64_t step_base, int64_t* first_bad,
+                      void* stream);
+
 /* ---- recurrent network (BASELINE config 5) ---------------------------------- */
 
 /* Per-step input of the cortex network (cortex.py:283-301) for n local

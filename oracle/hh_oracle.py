@@ -501,3 +501,44 @@ def network_step(params, v, g, psp, ring, t, offsets, targets, weights, delays,
         if hi > lo:
             ring.push(t, targets[lo:hi], weights[lo:hi], delays[lo:hi])
     return v, g, psp, spikes
+
+
+# ---------------------------------------------------------------------------
+# multicompartment neurons (morphology.py:115-166)
+# ---------------------------------------------------------------------------
+
+def morph_axial(v, edges):
+    """axial_current (morphology.py:115-124): v (n_comp, ...), edges
+    [(i, j, g)] in declaration order; out[i] += g (v_j - v_i), out[j] -= it."""
+    out = np.zeros_like(v)
+    for i, j, g in edges:
+        flow = g * (v[j] - v[i])
+        out[i] += flow
+        out[j] -= flow
+    return out
+
+
+def morph_simulate(params_list, edges, i_series, dtype=np.float64):
+    """simulate_morphology (morphology.py:144-166) for compartments with
+    channel tables params_list (graph order); i_series (T, n_comp) + batch.
+    Returns (V (T, n_comp) + batch float64, spikes bool)."""
+    i_series = np.asarray(i_series, dtype=np.float64)
+    T, nc = i_series.shape[:2]
+    shape = i_series.shape[2:]
+    n = int(np.prod(shape, dtype=np.int64)) if shape else 1
+    vs, gs = [], []
+    for p in params_list:
+        v, g = rest_state(p, n, dtype=dtype)
+        vs.append(v)
+        gs.append(g)
+    v_out = np.empty((T, nc, n))
+    s_out = np.empty((T, nc, n), dtype=bool)
+    for t in range(T):
+        ax = morph_axial(np.stack(vs), edges)
+        for k, p in enumerate(params_list):
+            cur = (i_series[t, k].reshape(n) + ax[k]).astype(dtype)
+            v_new, g_new, spk = step(p, vs[k], gs[k], cur, step_index=t)
+            vs[k], gs[k] = v_new, g_new
+            v_out[t, k] = v_new
+            s_out[t, k] = spk
+    return v_out.reshape((T, nc) + shape), s_out.reshape((T, nc) + shape)

@@ -35,6 +35,13 @@ def _ref():
     return dyn, adj, defaults, learn, cortex, naive
 
 
+def _morph():
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import hhengine.morphology as morph
+    return morph
+
+
 def c2_params(dyn, dt=0.01):
     """BASELINE config 2 custom set."""
     R, G, C = dyn.RateFn, dyn.GateSpec, dyn.ChannelSpec
@@ -107,6 +114,23 @@ def main():
     ll, ly = 3.0 * rng_l.normal(size=(9, 10)), rng_l.integers(0, 10, size=9)
     ka["ce_logits"], ka["ce_target"] = ll, ly
     ka["ce_loss"], ka["ce_seed"] = learn.cross_entropy_loss(ll, ly)
+    # multicompartment (morphology.py): coincidence demo, a random-current chain
+    # with a batch axis, and axial_current of a random state
+    morph = _morph()
+    tr_demo = morph.coincidence_experiment(morph.coincidence_graph(), morph.demo_trials())
+    chain = morph.chain_graph(5, defaults.squid_axon_params(dt=0.01), 0.5)
+    rng_m = np.random.default_rng(7)
+    i_chain = rng_m.uniform(0.0, 15.0, size=(300, 5, 3))
+    tr_chain = morph.simulate_morphology(chain, i_chain)
+    st_m = morph.init_morph_state(morph.coincidence_graph(), (4,))
+    for k, s in enumerate(st_m.states):
+        s.v[...] = rng_m.normal(-60.0, 8.0, size=4)
+    ax_m = morph.axial_current(st_m, morph.coincidence_graph())
+    np.savez_compressed(os.path.join(OUT, "morph.npz"),
+                        demo_v0=tr_demo[0].v_series, demo_s0=tr_demo[0].spike_series,
+                        demo_v1=tr_demo[1].v_series, demo_s1=tr_demo[1].spike_series,
+                        chain_i=i_chain, chain_v=tr_chain.v_series, chain_s=tr_chain.spike_series,
+                        ax_v=np.stack([s.v for s in st_m.states]), ax=ax_m)
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

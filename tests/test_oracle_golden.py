@@ -163,3 +163,53 @@ def test_oracle_losses_match_reference_goldens():
     loss, seed = O.cross_entropy_loss(ka["ce_logits"], ka["ce_target"])
     assert abs(loss - float(ka["ce_loss"])) <= 1e-15 * abs(loss)
     assert np.allclose(seed, ka["ce_seed"], rtol=1e-14, atol=0)
+
+
+def test_oracle_morphology_matches_reference_goldens():
+    """oracle morph_simulate / morph_axial (morphology.py:115-166) vs the reference."""
+    from paper_2601_21407_b200 import defaults as DF
+    from paper_2601_21407_b200 import morphology as M
+    g = golden("morph")
+    chain = M.chain_graph(5, DF.squid_axon_params(dt=0.01), 0.5)
+    edges = [(chain.index(e.a), chain.index(e.b), e.g_axial) for e in chain.edges]
+    params = [chain.compartments[c] for c in chain.order]
+    v, s = O.morph_simulate(params, edges, g["chain_i"])
+    assert np.array_equal(v, g["chain_v"]) and np.array_equal(s, g["chain_s"])
+    cg = M.coincidence_graph()
+    edges = [(cg.index(e.a), cg.index(e.b), e.g_axial) for e in cg.edges]
+    assert np.array_equal(O.morph_axial(g["ax_v"], edges), g["ax"])
+    params = [cg.compartments[c] for c in cg.order]
+    for k, trial in enumerate(M.demo_trials()):
+        T = int(round(40.0 / cg.dt))
+        i = np.zeros((T, cg.n_compartments))
+        for st in trial:
+            lo, hi = int(round(st.t_on_ms / cg.dt)), int(round((st.t_on_ms + st.duration_ms) / cg.dt))
+            i[lo:hi, cg.index(st.compartment)] += st.amplitude
+        v, s = O.morph_simulate(params, edges, i)
+        assert np.array_equal(v, g[f"demo_v{k}"]) and np.array_equal(s, g[f"demo_s{k}"])
+
+
+def test_morphology_graph_validation_matches_reference():
+    """CompartmentGraph checks (morphology.py:37-84) are host code: no GPU."""
+    import warnings
+    from paper_2601_21407_b200 import defaults as DF
+    from paper_2601_21407_b200 import morphology as M
+    from paper_2601_21407_b200.errors import ConfigurationError
+    p = DF.squid_axon_params()
+    with pytest.raises(ConfigurationError):
+        M.CompartmentGraph({"a": p}, [], "zz")
+    with pytest.raises(ConfigurationError):
+        M.CompartmentGraph({"a": p, "b": p}, [M.Edge("a", "c", 1.0)], "a")
+    with pytest.raises(ConfigurationError):
+        M.CompartmentGraph({"a": p, "b": p}, [M.Edge("a", "b", -1.0)], "a")
+    with pytest.raises(ConfigurationError):
+        M.CompartmentGraph({"a": p, "b": p}, [], "a")           # disconnected
+    with pytest.raises(ConfigurationError):
+        M.CompartmentGraph({"a": p, "b": DF.squid_axon_params(dt=0.01)}, [M.Edge("a", "b", 1.0)], "a")
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        M.chain_graph(3, p, 100.0)                              # dt*g/c_m > 0.5
+        assert any("unstable" in str(x.message) for x in w)
+    gd = M.graph_from_dict({"compartments": [{"id": "s"}, {"id": "d", "params": p.to_dict()}],
+                            "edges": [{"a": "s", "b": "d", "g_axial": 1.0}], "soma": "s"})
+    assert gd.order == ["s", "d"] and gd.index("d") == 1
