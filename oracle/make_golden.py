@@ -131,6 +131,24 @@ def main():
                         demo_v1=tr_demo[1].v_series, demo_s1=tr_demo[1].spike_series,
                         chain_i=i_chain, chain_v=tr_chain.v_series, chain_s=tr_chain.spike_series,
                         ax_v=np.stack([s.v for s in st_m.states]), ax=ax_m)
+    # run_network with a thalamic transient + SpikeRecord statistics (cortex.py:319-464)
+    topo_t = cortex.build_network(0.02, 0, cortex.THALAMIC_CONFIG)
+    thal = {"t_on_ms": 4.0, "duration_ms": 10.0, "rate_hz": 120.0, "weight": 0.22, "weight_std": 0.022}
+    rec_t = cortex.run_network(topo_t, cortex.THALAMIC_CONFIG, 20.0, seed=3, warmup_ms=2.0, thalamic=thal)
+    stats = {}
+    for pop in ("L4e", "L2/3e", "L6i"):
+        key = pop.replace("/", "")
+        stats[f"rate_{key}"] = rec_t.pop_rate(pop)
+        stats[f"quart_{key}"] = rec_t.rate_quartiles(pop)
+        stats[f"cv_{key}"] = rec_t.isi_cv(pop)
+        stats[f"hist_{key}"] = rec_t.rate_histogram(pop, 2.0)[1]
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        fn = os.path.join(td, "r.ndjson")
+        rec_t.to_ndjson(fn)
+        nd = open(fn).read()
+    np.savez_compressed(os.path.join(OUT, "cortex_thalamic.npz"), spike_t=rec_t.times_ms, spike_id=rec_t.neuron_ids,
+                        ndjson=np.array(nd), **stats)
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

@@ -466,3 +466,156 @@ class CortexNetwork:
         t_idx, n_idx = np.nonzero(np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")
                                   [:, :self.n_global])
         return (t_idx + 1 + (self.t - n_steps)) * self.config.dt, n_idx.astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# run_network / SpikeRecord (cortex.py:319-464): the reference's driver and
+# its output record, on the device network
+# ---------------------------------------------------------------------------
+
+@dataclass
+class SpikeRecord:
+    """Spike events plus per-population rate statistics (cortex.py:319-376)."""
+
+    times_ms: np.ndarray
+    neuron_ids: np.ndarray
+    duration_ms: float
+    warmup_ms: float
+    topo: NetworkTopology
+
+    def _mask(self, name: str, warm: bool = True):
+        sl = self.topo.pop_slice(name)
+        m = (self.neuron_ids >= sl.start) & (self.neuron_ids < sl.stop)
+        if warm:
+            m &= self.times_ms >= self.warmup_ms
+        return sl, m
+
+    def pop_rate(self, name: str) -> float:
+        """Mean rate (Hz) per neuron over the post-warmup window."""
+        sl, m = self._mask(name)
+        window_s = (self.duration_ms - self.warmup_ms) / 1000.0
+        return float(m.sum()) / (sl.stop - sl.start) / window_s
+
+    def rate_quartiles(self, name: str):
+        sl, m = self._mask(name)
+        counts = np.bincount(self.neuron_ids[m] - sl.start, minlength=sl.stop - sl.start)
+        window_s = (self.duration_ms - self.warmup_ms) / 1000.0
+        return np.percentile(counts / window_s, [25, 50, 75])
+
+    def isi_cv(self, name: str) -> float:
+        """Mean ISI coefficient of variation over neurons with >= 3 spikes."""
+        _, m = self._mask(name)
+        ids, ts = self.neuron_ids[m], self.times_ms[m]
+        cvs = []
+        for nid in np.unique(ids):
+            tt = np.sort(ts[ids == nid])
+            if tt.size >= 3:
+                isi = np.diff(tt)
+                if isi.mean() > 0:
+                    cvs.append(isi.std() / isi.mean())
+        return float(np.mean(cvs)) if cvs else float("nan")
+
+    def rate_histogram(self, name: str, bin_ms: float = 1.0):
+        """(bin centers ms, rate Hz) over the full duration."""
+        sl, m = self._mask(name, warm=False)
+        edges = np.arange(0.0, self.duration_ms + bin_ms, bin_ms)
+        hist, _ = np.histogram(self.times_ms[m], bins=edges)
+        rate = hist / (sl.stop - sl.start) / (bin_ms / 1000.0)
+        return 0.5 * (edges[:-1] + edges[1:]), rate
+
+    def to_ndjson(self, path) -> None:
+        """One event per line: {t_ms, pop, neuron} (cortex.py:369-376)."""
+        import json
+        pop_of = np.empty(self.topo.n_neurons, dtype=object)
+        for p in self.topo.populations:
+            pop_of[p.offset:p.offset + p.size] = p.name
+        with open(path, "w") as f:
+            for t, n in zip(self.times_ms, self.neuron_ids):
+                f.write(json.dumps({"t_ms": round(float(t), 6), "pop": pop_of[n], "neuron": int(n)}) + "\n")
+
+
+def _thalamic_setup(topo: NetworkTopology, thalamic: dict, duration_ms: float, dt: float, rng):
+    """Thalamic targets/weights with the reference's RNG calls (cortex.py:401-423)."""
+    if thalamic["t_on_ms"] + thalamic["duration_ms"] > duration_ms:
+        raise UsageError("thalamic stimulus extends beyond the simulation")
+    scale = topo.populations[0].size / conn.FULL_SIZES[0]
+    n_thal = max(int(round(conn.N_THALAMUS * scale)), 1)
+    tt, tw = [], []
+    for pop_name, p in conn.THALAMIC_PROBS.items():
+        sl = topo.pop_slice(pop_name)
+        size = sl.stop - sl.start
+        count = int(rng.binomial(n_thal * size, p))
+        if count == 0:
+            continue
+        ids = rng.choice(n_thal * size, size=count, replace=False)
+        tt.append(sl.start + (ids % size))
+        tw.append(np.maximum(rng.normal(thalamic["weight"], thalamic.get("weight_std", 0.0), size=count), 0.0))
+    targets = np.concatenate(tt) if tt else np.zeros(0, dtype=int)
+    weights = np.concatenate(tw) if tw else np.zeros(0)
+    lam = thalamic["rate_hz"] * dt / 1000.0
+    lo = int(round(thalamic["t_on_ms"] / dt))
+    hi = int(round((thalamic["t_on_ms"] + thalamic["duration_ms"]) / dt))
+    return targets, weights, lam, lo, hi
+
+
+def run_network(topo: NetworkTopology, config: CortexConfig, duration_ms: float, seed: int,
+                warmup_ms: float = 0.0, thalamic: dict | None = None, background: str = "host",
+                dtype=np.float64, device=None) -> SpikeRecord:
+    """Simulate and collect spikes (cortex.py:379-438) on the device network.
+
+    background="host" (default) draws the compound-Poisson background and the
+    thalamic events from the reference's RNG stream (np.random.default_rng(seed),
+    same call order), so a float64 run reproduces the reference raster;
+    background="philox" draws the background on the device (statistically the
+    same process, keyed by (seed, neuron, step)) and replays 64-step CUDA graphs
+    when there is no thalamic drive -- the throughput path."""
+    rng = np.random.default_rng(seed)
+    n_steps = int(round(duration_ms / config.dt))
+    thal = None
+    if thalamic is not None:
+        thal = _thalamic_setup(topo, thalamic, duration_ms, config.dt, rng)
+    if background == "host":
+        hb = HostBackground(topo, make_background(config), config.dt, rng)
+        net = CortexNetwork(topo, config, device=device, dtype=dtype, background="host", host_bg=hb)
+    elif background == "philox":
+        net = CortexNetwork(topo, config, device=device, dtype=dtype, background="philox", seed=seed)
+    else:
+        raise UsageError(f"unknown background {background!r}")
+    rows = torch.empty((n_steps, net.words_global), dtype=torch.int32, device=net.dev)
+    if background == "philox" and thal is None:
+        net.advance(n_steps, record=rows)
+    else:
+        for t in range(n_steps):
+            extra = None
+            if thal is not None and thal[3] <= t < thal[4] and thal[0].size:
+                targets, weights, lam = thal[0], thal[1], thal[2]
+                events = rng.random(targets.size) < lam
+                if events.any():
+                    extra = np.zeros(topo.n_neurons)
+                    np.add.at(extra, targets[events], weights[events])
+                    extra = extra[net.lo:net.hi]
+            rows[t].copy_(net.step(extra))
+    _raise_if_bad(net.first_bad)
+    bits = rows.cpu().numpy().view(np.uint32)
+    t_idx, n_idx = np.nonzero(np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")[:, :topo.n_neurons])
+    return SpikeRecord((t_idx + 1) * config.dt, n_idx.astype(np.int64), duration_ms, warmup_ms, topo)
+
+
+def rest_state_run(duration_ms: float, scale: float, seed: int, config: CortexConfig | None = None,
+                   warmup_ms: float = 200.0, **kw) -> SpikeRecord:
+    """Spontaneous-activity run with the rest-state parameter set (cortex.py:441-448)."""
+    cfg = replace(config if config is not None else REST_CONFIG, scale=scale)
+    topo = build_network(scale, seed, cfg)
+    return run_network(topo, cfg, duration_ms, seed + 1, warmup_ms=warmup_ms, **kw)
+
+
+def thalamic_stimulus_run(duration_ms: float, scale: float, seed: int, t_on_ms: float,
+                          config: CortexConfig | None = None, warmup_ms: float = 200.0,
+                          rate_hz: float | None = None, **kw) -> SpikeRecord:
+    """Thalamic-transient run: weaker background, brief strong L4/L6 drive (cortex.py:451-464)."""
+    cfg = replace(config if config is not None else THALAMIC_CONFIG, scale=scale)
+    topo = build_network(scale, seed, cfg)
+    thal = {"t_on_ms": t_on_ms, "duration_ms": conn.THALAMIC_DURATION_MS,
+            "rate_hz": rate_hz if rate_hz is not None else conn.THALAMIC_RATE_HZ,
+            "weight": cfg.bg_mean, "weight_std": cfg.bg_std}
+    return run_network(topo, cfg, duration_ms, seed + 1, warmup_ms=warmup_ms, thalamic=thal, **kw)

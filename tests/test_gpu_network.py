@@ -100,3 +100,36 @@ def test_graph_replay_equals_eager_steps(cuda, dtype):
     rec2 = torch.empty((70, b.words_global), dtype=torch.int32, device=cuda)
     b.advance(70, steps_per_graph=64, record=rec2)
     assert torch.equal(more, rec2)
+
+
+def test_run_network_reproduces_reference_spike_records(cuda, tmp_path):
+    """run_network (host background: the reference's RNG stream) reproduces the
+    reference rasters, rest-state and with a thalamic transient, and the
+    SpikeRecord statistics / ndjson output (cortex.py:319-464)."""
+    g, topo = _small()
+    rec = N.run_network(topo, N.REST_CONFIG, float(g["duration_ms"]), seed=int(g["run_seed"]))
+    o, r = np.lexsort((rec.neuron_ids, rec.times_ms)), np.lexsort((g["spike_id"], g["spike_t"]))
+    assert np.array_equal(rec.neuron_ids[o], g["spike_id"][r]) and np.allclose(rec.times_ms[o], g["spike_t"][r])
+    h = golden("cortex_thalamic")
+    topo_t = N.build_network(0.02, 0, N.THALAMIC_CONFIG)
+    thal = {"t_on_ms": 4.0, "duration_ms": 10.0, "rate_hz": 120.0, "weight": 0.22, "weight_std": 0.022}
+    rec = N.run_network(topo_t, N.THALAMIC_CONFIG, 20.0, seed=3, warmup_ms=2.0, thalamic=thal)
+    assert np.array_equal(rec.neuron_ids, h["spike_id"]) and np.allclose(rec.times_ms, h["spike_t"], rtol=0, atol=1e-12)
+    for pop in ("L4e", "L2/3e", "L6i"):
+        key = pop.replace("/", "")
+        assert rec.pop_rate(pop) == float(h[f"rate_{key}"])
+        assert np.array_equal(rec.rate_quartiles(pop), h[f"quart_{key}"])
+        cv = rec.isi_cv(pop)
+        assert (np.isnan(cv) and np.isnan(h[f"cv_{key}"])) or cv == float(h[f"cv_{key}"])
+        assert np.array_equal(rec.rate_histogram(pop, 2.0)[1], h[f"hist_{key}"])
+    fn = tmp_path / "r.ndjson"
+    rec.to_ndjson(fn)
+    assert fn.read_text() == str(h["ndjson"])
+
+
+def test_run_network_philox_graph_path(cuda):
+    """The device-background path (graph replay) runs and fires; same record type."""
+    _, topo = _small()
+    rec = N.run_network(topo, N.REST_CONFIG, 30.0, seed=2, background="philox", dtype=np.float32)
+    assert isinstance(rec, N.SpikeRecord) and rec.times_ms.size > 0
+    assert rec.times_ms.max() <= 30.0 + 1e-9
