@@ -284,6 +284,22 @@ int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double
                 double* scratch, void* stream);
 int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols);
 
+/* ---- LIF baseline (dynamics.py:227-244, :532-538; adjoint.py:197-227) ------ */
+
+/* n_steps of n LIF neurons in one launch: v' = v + (dt/tau)(i - v), spike =
+ * v' >= v_theta, v = spike ? v_reset : v'.  i_ext[t*i_st + j*i_sn]; v_out
+ * [n_steps][n] and spk_out uint8 [n_steps][n] optional; v_fin [n]. */
+int hhb_lif_forward(int32_t dtype, int64_t n, int64_t n_steps, double tau, double dt, double v_theta,
+                    double v_reset, const void* v_in, const void* i_ext, int64_t i_st, int64_t i_sn,
+                    void* v_out, uint8_t* spk_out, void* v_fin, void* stream);
+/* lif_step_backward: d_v_pre = g_v_out ((1 - s) + (v_reset - v_pre) sg) +
+ * g_spike sg (g_spike may be NULL), d_v_in = d_v_pre (1 - k), d_i = d_v_pre k;
+ * *bad set >= 0 when d_v_in is non-finite (GradientOverflowError). */
+int hhb_lif_backward(int32_t dtype, int64_t n, double tau, double dt, double v_theta, double v_reset,
+                     const hhb_surrogate_t* surrogate, const void* v, const void* i_ext, int64_t i_sn,
+                     const void* g_v_out, const void* g_spike, void* d_v_in, void* d_i, int64_t* bad,
+                     void* stream);
+
 /* ---- multicompartment neurons (morphology.py) ---------------- */
 
 /* T steps of `batch` independent multicompartment neurons on one compartment

@@ -149,6 +149,24 @@ def main():
         nd = open(fn).read()
     np.savez_compressed(os.path.join(OUT, "cortex_thalamic.npz"), spike_t=rec_t.times_ms, spike_id=rec_t.neuron_ids,
                         ndjson=np.array(nd), **stats)
+    # LIF baseline (dynamics.py:532-586 LIF branch, adjoint.py:197-227)
+    lifp = defaults.lif_params()
+    rng_l2 = np.random.default_rng(11)
+    i_lif = rng_l2.uniform(0.0, 2.5, size=(400, 6))
+    tr_lif = dyn.simulate(lifp, i_lif)
+    tr_lif32 = dyn.simulate(lifp.__class__(lifp.tau, lifp.v_theta, lifp.v_reset, lifp.dt, np.float32),
+                            i_lif.astype(np.float32))
+    st_l = dyn.NeuronState(rng_l2.uniform(0.0, 1.2, size=6), np.zeros((0, 6)))
+    adj_o = adj.AdjointState(rng_l2.normal(size=6), np.zeros((0, 6)), 0.0, np.zeros(0),
+                             d_spike=rng_l2.normal(size=6))
+    sur_l = adj.default_surrogate(lifp)
+    a_in, d_i_l = adj.lif_step_backward(st_l, i_lif[0], lifp, adj_o, sur_l)
+    adj_o2 = adj.AdjointState(adj_o.d_v, np.zeros((0, 6)), 0.0, np.zeros(0))
+    a_in2, d_i_l2 = adj.lif_step_backward(st_l, i_lif[0], lifp, adj_o2, sur_l)
+    np.savez_compressed(os.path.join(OUT, "lif.npz"), i=i_lif, v=tr_lif.v_series, s=tr_lif.spike_series,
+                        v32=tr_lif32.v_series, s32=tr_lif32.spike_series, st_v=st_l.v, d_v=adj_o.d_v,
+                        d_spike=adj_o.d_spike, sur_w=sur_l.width, bwd_dv=a_in.d_v, bwd_di=d_i_l,
+                        bwd2_dv=a_in2.d_v, bwd2_di=d_i_l2)
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 # per-source extra flags: the double flavour must not contract into FMA (NumPy parity)
-EXTRA = {"hh_f64.cu": ["-fmad=false"], "morph_f64.cu": ["-fmad=false"]}
+EXTRA = {"hh_f64.cu": ["-fmad=false"], "morph_f64.cu": ["-fmad=false"], "lif_f64.cu": ["-fmad=false"]}
 LINK_LIBS: list[str] = ["-ldl"]
 
 

@@ -191,20 +191,29 @@ def hh_step_backward(state_in: NeuronState, i_ext, params: HHParams, adj_out: Ad
 
 def lif_step_backward(state_in: NeuronState, i_ext, params: LIFParams, adj_out: AdjointState,
                       surrogate: SurrogateSpec, step_index: int | None = None):
-    """Adjoint of one LIF step with the surrogate reset factor (adjoint.py:197-227)."""
+    """Adjoint of one LIF step with the surrogate reset factor (adjoint.py:197-227),
+    float64 as in the reference, one hhb_lif_backward launch."""
     on_dev = D.is_dev(state_in.v)
     dev = D.require_cuda()
     v = D.to_dev(state_in.v, np.float64, dev)
-    k = params.dt / params.tau
-    v_pre = v + k * (D.to_dev(i_ext, np.float64, dev) - v)
-    spikes = (v_pre >= params.v_theta).to(torch.float64)
-    sg = D.to_dev(surrogate_grad(v_pre - params.v_theta, surrogate), np.float64, dev)
-    g_out = D.to_dev(adj_out.d_v, np.float64, dev)
-    g_sp = D.to_dev(adj_out.d_spike, np.float64, dev) if adj_out.d_spike is not None else 0.0
-    d_v_pre = g_out * ((1.0 - spikes) + (params.v_reset - v_pre) * sg) + g_sp * sg
-    d_v_in = d_v_pre * (1.0 - k)
-    d_i = d_v_pre * k
-    if not bool(torch.isfinite(d_v_in).all()):
+    shape = tuple(v.shape)
+    n = v.numel()
+    cur = D.to_dev(i_ext, np.float64, dev)
+    i_sn = 0 if cur.numel() == 1 else 1
+    if i_sn:
+        cur = cur.expand(shape).contiguous()
+    g_out = D.to_dev(adj_out.d_v, np.float64, dev).expand(shape).contiguous()
+    g_sp = (D.to_dev(adj_out.d_spike, np.float64, dev).expand(shape).contiguous()
+            if adj_out.d_spike is not None else None)
+    d_v_in = torch.empty(shape, dtype=torch.float64, device=dev)
+    d_i = torch.empty(shape, dtype=torch.float64, device=dev)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    S = nat.pack_surrogate(surrogate)
+    nat.check(nat.load().hhb_lif_backward(D.code(torch.float64), n, params.tau, params.dt, params.v_theta,
+                                          params.v_reset, C.byref(S), v.contiguous().data_ptr(), cur.data_ptr(),
+                                          i_sn, g_out.data_ptr(), D.ptr(g_sp), d_v_in.data_ptr(), d_i.data_ptr(),
+                                          bad.data_ptr(), D.stream()), "hhb_lif_backward")
+    if int(bad.item()) >= 0:
         raise GradientOverflowError("adjoint state became non-finite", step_index)
     zeros_g = torch.zeros_like(D.to_dev(adj_out.d_gates, np.float64, dev))
     if on_dev:

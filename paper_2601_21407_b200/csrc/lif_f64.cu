@@ -1,0 +1,65 @@
+// lif_f64.cu -- LIF kernels (lif.cuh), both flavours, and their C ABI.  Built
+// with -fmad=false: the float64 flavour then rounds like NumPy.
+#include "lif.cuh"
+
+using namespace hhb;
+
+namespace {
+template <typename T>
+int lif_fwd(int64_t n, int64_t steps, double tau, double dt, double theta, double v_reset, const void* v_in,
+            const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, uint8_t* spk, void* v_fin,
+            cudaStream_t st) {
+  const T k = T(dt / tau);
+  lif::k_lif_forward<T><<<grid_1d(n, 256), 256, 0, st>>>(n, steps, k, T(theta), T(v_reset), (const T*)v_in,
+                                                         (const T*)i_ext, i_st, i_sn, (T*)v_out, spk, (T*)v_fin);
+  return cuda_check("k_lif_forward launch");
+}
+template <typename T>
+int lif_bwd(int64_t n, double tau, double dt, double theta, double v_reset, const hhb_surrogate_t* S, const void* v,
+            const void* i_ext, int64_t i_sn, const void* g_v, const void* g_s, void* d_v, void* d_i, int64_t* bad,
+            cudaStream_t st) {
+  const T k = T(dt / tau);
+  lif::k_lif_backward<T><<<grid_1d(n, 256), 256, 0, st>>>(n, k, T(theta), T(v_reset), pack_sur<T>(S), (const T*)v,
+                                                          (const T*)i_ext, i_sn, (const T*)g_v, (const T*)g_s,
+                                                          (T*)d_v, (T*)d_i, reinterpret_cast<long long*>(bad));
+  return cuda_check("k_lif_backward launch");
+}
+}  // namespace
+
+extern "C" {
+
+int hhb_lif_forward(int32_t dtype, int64_t n, int64_t n_steps, double tau, double dt, double v_theta,
+                    double v_reset, const void* v_in, const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out,
+                    uint8_t* spk_out, void* v_fin, void* stream) {
+  if (!(tau > 0) || !(dt > 0) || !(v_theta > v_reset)) return fail(HHB_EINVAL, "bad LIF parameters");
+  if (n < 0 || n_steps < 0) return fail(HHB_EINVAL, "n and n_steps must be >= 0");
+  if (n == 0) return HHB_OK;
+  if (!v_in || !v_fin || (n_steps > 0 && !i_ext)) return fail(HHB_EINVAL, "v_in, v_fin, i_ext required");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HHB_F32)
+    return lif_fwd<float>(n, n_steps, tau, dt, v_theta, v_reset, v_in, i_ext, i_st, i_sn, v_out, spk_out, v_fin, st);
+  if (dtype == HHB_F64)
+    return lif_fwd<double>(n, n_steps, tau, dt, v_theta, v_reset, v_in, i_ext, i_st, i_sn, v_out, spk_out, v_fin,
+                           st);
+  return fail(HHB_EINVAL, "dtype");
+}
+
+int hhb_lif_backward(int32_t dtype, int64_t n, double tau, double dt, double v_theta, double v_reset,
+                     const hhb_surrogate_t* surrogate, const void* v, const void* i_ext, int64_t i_sn,
+                     const void* g_v_out, const void* g_spike, void* d_v_in, void* d_i, int64_t* bad,
+                     void* stream) {
+  if (!(tau > 0) || !(dt > 0)) return fail(HHB_EINVAL, "bad LIF parameters");
+  if (!surrogate || !(surrogate->width > 0)) return fail(HHB_EINVAL, "bad surrogate");
+  if (n <= 0) return HHB_OK;
+  if (!v || !i_ext || !g_v_out || !d_v_in || !d_i || !bad) return fail(HHB_EINVAL, "missing pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HHB_F32)
+    return lif_bwd<float>(n, tau, dt, v_theta, v_reset, surrogate, v, i_ext, i_sn, g_v_out, g_spike, d_v_in, d_i,
+                          bad, st);
+  if (dtype == HHB_F64)
+    return lif_bwd<double>(n, tau, dt, v_theta, v_reset, surrogate, v, i_ext, i_sn, g_v_out, g_spike, d_v_in, d_i,
+                           bad, st);
+  return fail(HHB_EINVAL, "dtype");
+}
+
+}  // extern "C"

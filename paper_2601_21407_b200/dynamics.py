@@ -525,14 +525,34 @@ def hh_step(state: NeuronState, i_ext, params: HHParams, workspace: Workspace | 
     return out_state, (sp[()] if len(shape) == 0 else sp)
 
 
+def _lif_run(params: LIFParams, v: torch.Tensor, cur: torch.Tensor, steps: int, i_st: int, i_sn: int,
+             record: bool):
+    """hhb_lif_forward on device tensors: v (n,), cur flat; returns (v_fin, V, spikes)."""
+    n = v.numel()
+    v_fin = torch.empty_like(v)
+    vs = torch.empty((steps, n), dtype=v.dtype, device=v.device) if record else None
+    ss = torch.empty((steps, n), dtype=torch.uint8, device=v.device)
+    nat.check(nat.load().hhb_lif_forward(D.code(v.dtype), n, steps, params.tau, params.dt, params.v_theta,
+                                         params.v_reset, v.data_ptr(), cur.data_ptr(), i_st, i_sn, D.ptr(vs),
+                                         ss.data_ptr(), v_fin.data_ptr(), D.stream()), "hhb_lif_forward")
+    return v_fin, vs, ss.view(torch.bool)
+
+
 def lif_step(state: NeuronState, i, params: LIFParams):
     """Leaky integration with inclusive threshold and hard reset (dynamics.py:532-538)."""
     on_dev = D.is_dev(state.v)
-    v = D.to_dev(state.v, params.dtype)
-    cur = D.to_dev(i, params.dtype)
-    v_new = v + (params.dt / params.tau) * (cur - v)
-    spikes = v_new >= params.v_theta
-    v_out = torch.where(spikes, torch.full_like(v_new, params.v_reset), v_new)
+    dev = D.require_cuda()
+    # numpy inputs compute in NumPy's promoted type, as the reference does
+    # (a float64 current promotes a float32 LIF state)
+    dt_ = params.dtype if on_dev else np.result_type(np.asarray(state.v).dtype, np.asarray(i).dtype)
+    v = D.to_dev(state.v, dt_, dev)
+    shape = tuple(v.shape)
+    cur = D.to_dev(i, dt_, dev)
+    i_sn = 0 if cur.numel() == 1 else 1
+    if i_sn:
+        cur = cur.expand(shape).contiguous()
+    v_fin, _, ss = _lif_run(params, v.reshape(-1).contiguous(), cur.reshape(-1), 1, 0, i_sn, False)
+    v_out, spikes = v_fin.reshape(shape), ss[0].reshape(shape)
     if on_dev:
         return NeuronState(v_out, state.gates), spikes
     return NeuronState(D.to_host(v_out), state.gates), D.to_host(spikes)
@@ -616,18 +636,23 @@ def _simulate_pipelined(params, i2, v, g, T, shape, record_state):
 
 
 def _simulate_lif(params: LIFParams, i_series, state0, record_state):
+    """All T LIF steps in one hhb_lif_forward launch."""
     on_dev = D.is_dev(i_series)
     shape_all = tuple(i_series.shape) if on_dev else np.shape(i_series)
     T, shape = int(shape_all[0]), tuple(shape_all[1:])
     dev = D.require_cuda()
-    cur = D.to_dev(i_series, np.float64 if not on_dev else params.dtype, dev)
+    # the reference casts the series to float64 (dynamics.py:552), so its LIF
+    # arithmetic is float64 whatever params.dtype says; device tensors keep
+    # params.dtype
+    cdt = params.dtype if on_dev else np.float64
+    cur = D.to_dev(i_series, cdt, dev)
+    n = int(np.prod(shape, dtype=np.int64)) if shape else 1
     state = state0 if state0 is not None else init_state(params, shape, device=dev)
-    st = NeuronState(D.to_dev(state.v, cur.dtype, dev), state.gates)
-    vs = torch.empty((T,) + shape, dtype=cur.dtype, device=dev)
-    ss = torch.empty((T,) + shape, dtype=torch.bool, device=dev)
-    for t in range(T):
-        st, sp = lif_step(st, cur[t], params)
-        vs[t], ss[t] = st.v, sp
+    v0 = D.to_dev(state.v, cdt, dev).reshape(n).contiguous()
+    cur = cur.reshape(T, n).contiguous()
+    v_fin, vs, ss = _lif_run(params, v0, cur, T, n, 1, True)
+    vs, ss = vs.reshape((T,) + shape), ss.reshape((T,) + shape)
+    st = NeuronState(v_fin.reshape(shape), state.gates)
     if on_dev:
         tr = Trace(vs, ss, params.dt)
     else:
