@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -472,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         // row `lane` of the 32x32 block, 16-byte chunks XOR-swizzled by row % 8
+        // bias of the chunk's 32 columns (the same for every row / lane):
+        // float4 loads when the chunk is full and aligned, else per element
+        const bool bvec = args.bias != nullptr && n0 + c0 + 32 <= args.N &&
+                          (reinterpret_cast<uintptr_t>(args.bias + n0 + c0) & 15) == 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float4 o;
@@ -480,7 +485,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           o.y = __uint_as_float(rr[4 * j + 1]);
           o.z = __uint_as_float(rr[4 * j + 2]);
           o.w = __uint_as_float(rr[4 * j + 3]);
-          if (args.bias != nullptr) {
+          if (bvec) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(args.bias + cb));
+            o.x += bb.x;
+            o.y += bb.y;
+            o.z += bb.z;
+            o.w += bb.w;
+          } else if (args.bias != nullptr) {
             o.x += cb + 0 < args.N ? __ldg(args.bias + cb + 0) : 0.f;
             o.y += cb + 1 < args.N ? __ldg(args.bias + cb + 1) : 0.f;
             o.z += cb + 2 < args.N ? __ldg(args.bias + cb + 2) : 0.f;
@@ -508,6 +519,262 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(2 * BN)));
+  }
+}
+
+// ---------------------------------------------------------------- CTA pair
+// 2-SM variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x BN tile.  Each CTA loads its own 128 rows of A and half (BN/2) of the
+// columns of B; the leader (rank 0) issues tcgen05.mma.cta_group::2 (M = 256),
+// which reads B from both CTAs' shared memory, and each CTA's tensor memory
+// holds the accumulator of its 128 rows.  Per SM that halves the shared-memory
+// traffic of the operands (a 1-SM 128x256 tile needs ~192 B/clk of smem at
+// tensor peak against 128 B/clk available; the pair needs ~128).
+// Synchronisation: both CTAs' TMA loads complete on the LEADER's full barrier
+// (expect_tx = both halves, two arrivals); the leader's commits multicast to
+// both CTAs' empty / tmem-full barriers; the peer's epilogue warps arrive on
+// the leader's tmem-empty barrier (8 arrivals).
+template <int BN, bool DUAL>
+struct P2Cfg {
+  static constexpr uint32_t kStageA = BM * 128;             // this CTA's 128 rows x 64 k
+  static constexpr uint32_t kStageB = (BN / 2) * 128;       // half of B
+  static constexpr uint32_t kStage = kStageA * (DUAL ? 2 : 1) + kStageB;
+  static constexpr int kStgBufs = 2;                          // TMA-store staging buffers per epilogue warp (4 measured slower: fewer stages)
+  static constexpr uint32_t kStaging = 4 * kStgBufs * 32 * 32 * 4;
+  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 8 ? 8 : int((225 * 1024 - kStaging) / kStage);
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion goes to the pair leader's mbarrier (bit 24 of a
+// shared::cluster address selects the odd CTA of the pair)
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x,
+                                                int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                      uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_umma_gemm_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
+                    const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap td, const PArgs args) {
+  using C = P2Cfg<BN, DUAL>;
+  constexpr int ST = C::kStages;
+  constexpr uint32_t kStageA = C::kStageA, kStageB = C::kStageB;
+  constexpr uint32_t kAStride = kStageA * (DUAL ? 2 : 1);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ST * kAStride;
+  float* stg = reinterpret_cast<float*>(sB + ST * kStageB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::kStaging);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    if (DUAL) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&td)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(uint32_t(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+  const int per_split = args.m_tiles * args.n_tiles;      // m_tiles counts 256-row pair tiles
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own A rows, own half of B
+      int it = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs) {
+        const int z = tile / per_split, r = tile % per_split;
+        const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+        const int64_t n0 = int64_t(r / args.m_tiles) * BN + int64_t(rank) * (BN / 2);
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          if (leader) mbar_expect_tx_only(&full[s], 2 * (kAStride + kStageB));
+          else mbar_arrive_leader(&full[s]);
+          const int32_t kx = kb * 64;
+          uint8_t* a_dst = sA + s * kAStride;
+          if (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) {
+              tma_load_2d_2sm(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
+              if (DUAL) tma_load_2d_2sm(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
+            }
+          } else {
+            tma_load_2d_2sm(&ta, &full[s], a_dst, kx, int32_t(m0));
+            if (DUAL) tma_load_2d_2sm(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < (BN / 2) / 64; ++c)
+              tma_load_2d_2sm(&tb, &full[s], sB + s * kStageB + c * 8192, int32_t(n0) + 64 * c, kx);
+          } else {
+            tma_load_2d_2sm(&tb, &full[s], sB + s * kStageB, kx, int32_t(n0));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer: the pair leader only
+      int it = 0, local = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+        const int z = tile / per_split;
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        const int b = local & 1;
+        mbar_wait(&tempty[b], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + uint32_t(b * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* a_src = sA + s * kAStride;
+          const uint8_t* b_src = sB + s * kStageB;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bd = B_MN ? smem_desc_mn(b_src + k * 2048) : smem_desc(b_src + k * 32);
+            const uint64_t ad = A_MN ? smem_desc_mn(a_src + k * 2048) : smem_desc(a_src + k * 32);
+            umma2(acc, ad, bd, args.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (DUAL) {
+              const uint64_t ad2 =
+                  A_MN ? smem_desc_mn(a_src + kStageA + k * 2048) : smem_desc(a_src + kStageA + k * 32);
+              umma2(acc, ad2, bd, args.idesc, 1u);
+            }
+          }
+          umma2_commit(&empty[s]);
+        }
+        umma2_commit(&tfull[b]);
+      }
+    }
+  } else {  // epilogue warps 2..5 of both CTAs: this CTA's 128 rows
+    const int q = warp & 3;
+    float* my_stg = stg + (warp - 2) * C::kStgBufs * 1024;
+    int local = 0, nstore = 0;
+    for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+      const int z = tile / per_split, r = tile % per_split;
+      const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int64_t n0 = int64_t(r / args.m_tiles) * BN;
+      const int kb0 = z * args.kb_per_split;
+      const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
+      const int b = local & 1;
+      mbar_wait(&tfull[b], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int32_t row0 = int32_t(m0 + q * 32);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (n0 + c0 >= args.N) break;
+        uint32_t rr[32];
+        if (any_k) {
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(b * BN + c0), rr);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = 0u;
+        }
+        float* buf = my_stg + (nstore % C::kStgBufs) * 1024;
+        // the store that last used this buffer (kStgBufs stores ago) must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kStgBufs - 1) : "memory");
+        __syncwarp();
+        // bias of the chunk's 32 columns (the same for every row / lane):
+        // float4 loads when the chunk is full and aligned, else per element
+        const bool bvec = args.bias != nullptr && n0 + c0 + 32 <= args.N &&
+                          (reinterpret_cast<uintptr_t>(args.bias + n0 + c0) & 15) == 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o;
+          const int64_t cb = n0 + c0 + 4 * j;
+          o.x = __uint_as_float(rr[4 * j + 0]);
+          o.y = __uint_as_float(rr[4 * j + 1]);
+          o.z = __uint_as_float(rr[4 * j + 2]);
+          o.w = __uint_as_float(rr[4 * j + 3]);
+          if (bvec) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(args.bias + cb));
+            o.x += bb.x;
+            o.y += bb.y;
+            o.z += bb.z;
+            o.w += bb.w;
+          } else if (args.bias != nullptr) {
+            o.x += cb + 0 < args.N ? __ldg(args.bias + cb + 0) : 0.f;
+            o.y += cb + 1 < args.N ? __ldg(args.bias + cb + 1) : 0.f;
+            o.z += cb + 2 < args.N ? __ldg(args.bias + cb + 2) : 0.f;
+            o.w += cb + 3 < args.N ? __ldg(args.bias + cb + 3) : 0.f;
+          }
+          *reinterpret_cast<float4*>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&td, buf, int32_t(n0 + c0), row0, z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++nstore;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[b]);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(2 * BN)));
   }
 }
 
@@ -737,10 +1004,49 @@ static int launch_p_bn(int bn, const CUtensorMap& ta, const CUtensorMap& ta2, co
   return launch_p<256, A_MN, B_MN, DUAL>(ta, ta2, tb, td, a, st);
 }
 
-static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false) {
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
+static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tb, const CUtensorMap& td,
+                      const PArgs& a, cudaStream_t st) {
+  const size_t smem = P2Cfg<BN, DUAL>::kSmem;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  });
+  if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
+  // persistent: as many pairs as can be co-resident (not every SM has a
+  // usable TPC partner), queried once
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL>, &cfg) != cudaSuccess || n <= 0)
+      n = num_sms() / 2;
+    (void)cudaGetLastError();
+    max_pairs = n;
+  }
+  int pairs = max_pairs;
+  if (a.tiles < pairs) pairs = a.tiles;
+  if (getenv("HHB_GEMM_PAIRS_DEBUG")) fprintf(stderr, "k_umma_gemm_2sm: %d co-resident pairs\n", max_pairs);
+  k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL><<<2 * pairs, kThreads, smem, st>>>(ta, ta2, tb, td, a);
+  return cuda_check("k_umma_gemm_2sm launch");
+}
+
+static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false, int m = BM) {
   const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
-         (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+         (uint32_t(bn >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
 }  // namespace gemm
@@ -815,10 +1121,32 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kb_total = int((K + 63) / 64);
-  if (splits < 1) splits = 1;
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  if (splits < 1) {
+    // auto (splits <= 0): minimise a time model of the persistent grid --
+    // waves x k-blocks per unit x ~0.28 us per 64-deep k-block of a tile
+    // (doubled for the dual-A form), plus the split-K traffic (partials
+    // written and re-read, result written: (2 sp + 1) M N fp32 at ~5 TB/s);
+    // CTA-pair tiles (256 x BN) when M >= 512
+    const bool pairs = bn >= 128 && M >= 512;
+    const int64_t tiles = ((M + (pairs ? 2 * BM : BM) - 1) / (pairs ? 2 * BM : BM)) * ((N + bn - 1) / bn);
+    const int64_t P = pairs ? hhb::gemm::num_sms() / 2 : hhb::gemm::num_sms();
+    const double t_kb = 0.28 * (A2 != nullptr ? 2.0 : 1.0) * (pairs ? 1.0 : 0.5) * (double(bn) / 256.0);
+    const double t_mn = double(M) * double(N) * 4.0 / 5e12 * 1e6;
+    double best = 1e300;
+    splits = 1;
+    for (int sp = 1; sp <= (kb_total >= 8 ? kb_total / 4 : 1) && sp <= 32; ++sp) {
+      const int64_t units = tiles * sp;
+      const double cost = double((units + P - 1) / P) * double((kb_total + sp - 1) / sp) * t_kb +
+                          (sp > 1 ? double(2 * sp + 1) * t_mn : 0.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = sp;
+      }
+    }
+  }
   if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
   if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
-  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   CUtensorMap ta, ta2, tb;
   int rc = a_mn ? make_map_mn(&ta, A, M, K, lda) : make_map(&ta, false, A, M, K, lda, BM);
   if (rc) return rc;
@@ -830,6 +1158,39 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   if (dld % 4 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && !getenv("HHB_GEMM_NONPERSISTENT")) {
     CUtensorMap td;
     if ((rc = make_map_d(&td, dst, M, N, dld, splits))) return rc;
+    // CTA pairs (cta_group::2, 256 x BN tiles) when there are enough rows
+    if (bn >= 128 && M >= 512 && !getenv("HHB_GEMM_NO2SM")) {
+      CUtensorMap tb2;
+      if (!b_mn && (rc = make_map(&tb2, false, B, N, K, ldb, bn / 2))) return rc;
+      if (b_mn) tb2 = tb;
+      PArgs pa{};
+      pa.M = M;
+      pa.N = N;
+      pa.m_tiles = int((M + 2 * BM - 1) / (2 * BM));
+      pa.n_tiles = int((N + bn - 1) / bn);
+      pa.kb_total = kb_total;
+      pa.kb_per_split = (kb_total + splits - 1) / splits;
+      pa.splits = splits;
+      pa.tiles = pa.m_tiles * pa.n_tiles * splits;
+      pa.idesc = instr_desc(false, bn, a_mn, b_mn, 2 * BM);
+      pa.bias = splits > 1 ? nullptr : bias;
+#define HHB_GEMM_2CASE(AM, BMN, DU)                                                              \
+  if (a_mn == AM && b_mn == BMN && dual == DU)                                                   \
+    rc = bn == 128 ? launch_2sm<128, AM, BMN, DU>(ta, ta2, tb2, td, pa, st)                      \
+                   : launch_2sm<256, AM, BMN, DU>(ta, ta2, tb2, td, pa, st);
+      HHB_GEMM_2CASE(false, false, false)
+      HHB_GEMM_2CASE(false, false, true)
+      HHB_GEMM_2CASE(false, true, false)
+      HHB_GEMM_2CASE(false, true, true)
+      HHB_GEMM_2CASE(true, false, false)
+      HHB_GEMM_2CASE(true, false, true)
+      HHB_GEMM_2CASE(true, true, false)
+      HHB_GEMM_2CASE(true, true, true)
+#undef HHB_GEMM_2CASE
+      if (rc || splits == 1) return rc;
+      k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+      return cuda_check("k_gemm_reduce launch");
+    }
     PArgs pa{};
     pa.M = M;
     pa.N = N;

@@ -52,12 +52,9 @@ def gemm(A: torch.Tensor, B: torch.Tensor, K: int, bias=None, out=None, splits: 
         out = torch.empty((M, N), dtype=torch.float32, device=A.device)
     lib = nat.load()
     if splits is None:
-        bn = 64 if N <= 64 else (128 if N <= 128 else 256)
-        tiles = math.ceil(M / 128) * math.ceil(N / bn)
-        kb = math.ceil(K / 64)
-        splits = max(1, min(kb // 4, math.ceil(2 * 148 / tiles))) if tiles < 148 else 1
-    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
-    ws = torch.empty(ws_n, dtype=torch.float32, device=A.device) if ws_n else None
+        splits = 0          # the library picks the split count for its tile grid
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits if splits > 0 else 32))
+    ws = _workspace(ws_n, A.device) if ws_n else None
     nat.check(lib.hhb_gemm(BF16, M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                            D.ptr(bias), out.data_ptr(), out.stride(0), splits, D.ptr(ws), _stream()), "hhb_gemm")
     return out
@@ -108,15 +105,25 @@ def gemm_ex(flags: int, M: int, N: int, K: int, A: torch.Tensor, A2, lda: int, B
     out = torch.empty((M, N), dtype=torch.float32, device=A.device)
     lib = nat.load()
     if splits is None:
-        bn = 64 if N <= 64 else (128 if N <= 128 else 256)
-        tiles = math.ceil(M / 128) * math.ceil(N / bn)
-        kb = math.ceil(K / 64)
-        splits = max(1, min(kb // 4, math.ceil(2 * 148 / tiles))) if tiles < 148 else 1
-    ws_n = int(lib.hhb_gemm_workspace(M, N, splits))
-    ws = torch.empty(ws_n, dtype=torch.float32, device=A.device) if ws_n else None
+        splits = 0          # the library picks the split count for its tile grid
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits if splits > 0 else 32))
+    ws = _workspace(ws_n, A.device) if ws_n else None
     nat.check(lib.hhb_gemm_ex(flags, M, N, K, A.data_ptr(), D.ptr(A2), lda, B.data_ptr(), ldb, None,
                               out.data_ptr(), N, splits, D.ptr(ws), _stream()), "hhb_gemm_ex")
     return out
+
+
+_WS = {}
+
+
+def _workspace(n: int, dev) -> torch.Tensor:
+    """Split-K scratch, kept per device (grows; the stream orders its reuse)."""
+    key = str(dev)
+    w = _WS.get(key)
+    if w is None or w.numel() < n:
+        w = torch.empty(n, dtype=torch.float32, device=dev)
+        _WS[key] = w
+    return w
 
 
 A_MN, B_MN = 1, 2
