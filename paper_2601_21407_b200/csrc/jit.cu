@@ -1046,8 +1046,13 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
 #pragma unroll
     for (int g = 0; g < NG; ++g) p[j][g] = on ? a.g_in[g * a.g_ld + n0 + j] : 0.5f;
   }
-  i64 bad = LLMAX, ck_slot = 0, ck_count = 0;
-  // running output pointers (one 64-bit add per step instead of t * ld)
+  i64 bad = LLMAX;
+  int ck_count = 0;
+  // running pointers (one 64-bit add per step instead of t * ld)
+  float* ckp = a.ckpt != nullptr ? a.ckpt + n0 : nullptr;
+  const i64 sstride = (1 + NG) * a.ck_ld;
+  const float* ip = POIS ? nullptr : a.i_ext + n0 * a.i_sn;
+  const bool vec_in = VEC == 4 && full && a.i_sn == 1;
   float* vo = a.v_out != nullptr ? a.v_out + n0 : nullptr;
   u32* so = a.spk != nullptr ? a.spk + n0 / 32 : nullptr;
   float* svo = a.spk_val != nullptr ? a.spk_val + n0 : nullptr;
@@ -1055,23 +1060,40 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   // loaded currents are prefetched one step ahead (HBM latency); the drawn
   // stimulus is made at the top of its own step (no registers held across it)
   float cur[VEC];
-  if (!POIS && a.steps > 0) stim.at(a, ks, ps, 0, n0, full, cur);
+  auto load_in = [&](float (&c)[VEC]) {
+    if (vec_in) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(ip));
+      c[0] = q.x; c[VEC > 1 ? 1 : 0] = q.y; c[VEC > 2 ? 2 : 0] = q.z; c[VEC > 3 ? 3 : 0] = q.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) c[j] = ((valid >> j) & 1u) ? __ldg(ip + j * a.i_sn) : 0.0f;
+    }
+    ip += a.i_st;
+  };
+  if (!POIS && a.steps > 0) load_in(cur);
   for (i64 t = 0; t < a.steps; ++t) {
     float nxt[VEC];
     if (POIS) stim.at(a, ks, ps, t, n0, full, cur);
-    else if (t + 1 < a.steps) stim.at(a, ks, ps, t + 1, n0, full, nxt);
-    if (a.ckpt != nullptr && ck_count == 0) {
-      float* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
-      store_vec<VEC>(base, v, full, n0, a.n);
+    else if (t + 1 < a.steps) load_in(nxt);
+    if (ckp != nullptr && ck_count == 0) {      // state BEFORE step t
+      if (VEC == 4 && full) {
+        *reinterpret_cast<float4*>(ckp) = make_float4(v[0], v[VEC > 1 ? 1 : 0], v[VEC > 2 ? 2 : 0], v[VEC > 3 ? 3 : 0]);
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        float q[VEC];
+        for (int g = 0; g < NG; ++g)
+          *reinterpret_cast<float4*>(ckp + (1 + g) * a.ck_ld) =
+              make_float4(p[0][g], p[VEC > 1 ? 1 : 0][g], p[VEC > 2 ? 2 : 0][g], p[VEC > 3 ? 3 : 0][g]);
+      } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) q[j] = p[j][g];
-        store_vec<VEC>(base + (1 + g) * a.ck_ld, q, full, n0, a.n);
+        for (int j = 0; j < VEC; ++j) {
+          if ((valid >> j) & 1u) {
+            ckp[j] = v[j];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) ckp[(1 + g) * a.ck_ld + j] = p[j][g];
+          }
+        }
       }
-      ++ck_slot;
-      ck_count = a.ck_every;
+      ckp += sstride;
+      ck_count = int(a.ck_every);
     }
     --ck_count;
     float vn[VEC];
