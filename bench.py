@@ -222,6 +222,26 @@ def e2e_leg(torch, args, params, rank):
             "sample": f"simulate(numpy float32 I[{T}, {n}]) -> Trace(float64 V, bool spikes)"}
 
 
+def graph_step(torch, step):
+    """Capture one training step into a CUDA graph (after eager warm-up: JIT
+    modules, workspaces and the gradient tensors exist).  None if capture fails."""
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        torch.cuda.synchronize()
+        return g
+    except Exception as e:  # noqa: BLE001 -- fall back to eager timing
+        print(f"bench: CUDA graph capture failed ({e}); timing eager steps", file=sys.stderr)
+        return None
+
+
 def fwd_bwd_leg(torch, dev):
     """BASELINE config 3: differentiable HH SNN layer forward + BPTT, batch 256,
     784 -> 1024 RS neurons, 100 steps, x = Bernoulli(0.2) + 0.1 N(0,1),
@@ -244,19 +264,26 @@ def fwd_bwd_leg(torch, dev):
         # (seed_v = 2 V / numel, learn.py:86-88)
         mse(V).backward()
 
+    def timed(fn, reps=10):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
     for _ in range(3):
         step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    e0.record()
-    for _ in range(reps):
-        step()
-    e1.record()
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    eager_ms = timed(step)
+    # the whole training step (forward, loss, backward: ~25 launches) as one
+    # CUDA graph: the same kernels without the host launch gaps
+    graph = graph_step(torch, step)
+    ms = timed(graph.replay) if graph is not None else eager_ms
     layer.check()      # the overflow checks, deferred out of the timed steps
-    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
+            "cuda_graph": graph is not None,
             "config": "BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, bf16 tcgen05 "
                       "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs, "
                       "loss MSE(V, 0) (one unit = one neuron-step through forward and backward)"}
@@ -354,14 +381,14 @@ def c4_leg(torch, dev):
     net = torch.nn.ModuleList([HHLayer(784, 2048, w_mean=0.05, w_std=0.1, check_finite=False, device=dev),
                                HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, check_finite=False, device=dev),
                                HHLayer(2048, 10, w_mean=0.02, w_std=0.05, check_finite=False, device=dev)])
-    opt = torch.optim.Adam(net.parameters(), lr=5e-4)
+    import torch.distributed as dist
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    # capturable Adam keeps its step counters on the device (CUDA-graph safe)
+    opt = torch.optim.Adam(net.parameters(), lr=5e-4, capturable=(world == 1))
     g = torch.Generator(device=dev).manual_seed(1)
     x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() \
         + 0.1 * torch.randn((T, B, 784), device=dev, generator=g)
     y = torch.randint(0, 10, (B,), device=dev, generator=g)
-
-    import torch.distributed as dist
-    world = dist.get_world_size() if dist.is_initialized() else 1
     params = [p for p in net.parameters()]
     flat = torch.empty(sum(p.numel() for p in params), dtype=torch.float32, device=dev) if world > 1 else None
 
@@ -385,23 +412,33 @@ def c4_leg(torch, dev):
                 p.grad.copy_(flat[off:off + p.numel()].view_as(p.grad))
                 off += p.numel()
         opt.step()
-        return loss
+        return loss.detach()     # no autograd graph kept alive across steps (graph capture)
+
+    def timed(fn, reps=5):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
 
     for _ in range(3):
-        step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
-    e0.record()
-    for _ in range(reps):
         loss = step()
-    e1.record()
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    eager_ms = timed(step)
+    # one CUDA graph per training step (forward, CE, backward, Adam) on one GPU;
+    # under torchrun the NCCL all-reduce keeps the step eager
+    box = {}
+    graph = graph_step(torch, lambda: box.__setitem__("loss", step())) if world == 1 else None
+    ms = timed(graph.replay) if graph is not None else eager_ms
+    if graph is not None:
+        loss = box["loss"]
     for lyr in net:
         lyr.check()
     ns = B * T * (2048 + 2048 + 10)
-    return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "loss": float(loss.item()),
+    return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
+            "cuda_graph": graph is not None, "loss": float(loss.item()),
             "config": "BASELINE config 4: stacked HH SNN 784->2048->2048->10, batch 256, 100 steps, "
                       "bf16 tcgen05 projections, fp32 gating state, CE on time-mean V, Adam "
                       "(one unit = one neuron-step through forward and backward)"}
