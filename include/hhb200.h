@@ -300,6 +300,14 @@ int hhb_lif_backward(int32_t dtype, int64_t n, double tau, double dt, double v_t
                      const void* g_v_out, const void* g_spike, void* d_v_in, void* d_i, int64_t* bad,
                      void* stream);
 
+/* ---- training plumbing (learn.py) ----------------------------- */
+
+/* psp_filter (learn.py:52-55): y[t][c] = causal FIR of x[.][c] with taps[0..ntaps)
+ * (device float64 array), in scipy.signal.lfilter's direct-form-II-transposed
+ * operation order; x, y [steps][cols] of dtype. */
+int hhb_psp_filter(int32_t dtype, int64_t steps, int64_t cols, int32_t ntaps, const double* taps_dev,
+                   const void* x, void* y, void* stream);
+
 /* ---- multicompartment neurons (morphology.py) ---------------- */
 
 /* T steps of `batch` independent multicompartment neurons on one compartment

@@ -167,6 +167,25 @@ def main():
                         v32=tr_lif32.v_series, s32=tr_lif32.spike_series, st_v=st_l.v, d_v=adj_o.d_v,
                         d_spike=adj_o.d_spike, sur_w=sur_l.width, bwd_dv=a_in.d_v, bwd_di=d_i_l,
                         bwd2_dv=a_in2.d_v, bwd2_di=d_i_l2)
+    # training plumbing (learn.py:33-151): psp_filter, smape, adam_step
+    kern = learn.PSPKernel(2.0, 12, 0.1)
+    rng_p = np.random.default_rng(13)
+    sp_in = (rng_p.random((80, 3, 7)) < 0.2).astype(np.float64) + 0.05 * rng_p.normal(size=(80, 3, 7))
+    ka["psp_in"], ka["psp_out"] = sp_in, learn.psp_filter(sp_in, kern)
+    ka["smape_a"], ka["smape_b"] = rng_p.normal(size=40), rng_p.normal(size=40)
+    ka["smape_a"][3] = ka["smape_b"][3] = 0.0
+    ka["smape"] = learn.smape(ka["smape_a"], ka["smape_b"])
+    st_a = learn.AdamState(lr=1e-2)
+    pa = {"w": rng_p.normal(size=(4, 3)), "b": rng_p.normal(size=3)}
+    ka["adam_w0"], ka["adam_b0"] = pa["w"].copy(), pa["b"].copy()
+    gs = []
+    for k in range(3):
+        gr = {"w": rng_p.normal(size=(4, 3)), "b": rng_p.normal(size=3)}
+        gs.append(gr)
+        pa = learn.adam_step(pa, gr, st_a, lr=learn.cosine_lr(1e-2, k, 3))
+    ka["adam_gw"] = np.stack([g["w"] for g in gs])
+    ka["adam_gb"] = np.stack([g["b"] for g in gs])
+    ka["adam_w3"], ka["adam_b3"] = pa["w"], pa["b"]
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

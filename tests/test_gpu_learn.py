@@ -52,3 +52,21 @@ def test_mse_autograd_fp32_fused_seed(cuda):
     (3.0 * L.mse(v)).backward()
     ref = 3.0 * 2.0 * v.detach().double() / v.numel()
     assert torch.allclose(v.grad.double(), ref, rtol=1e-6, atol=0)
+
+
+def test_psp_filter_smape_adam_match_reference(cuda):
+    """psp_filter (lfilter order), smape and the Adam sequence with cosine lr
+    against the reference's outputs (learn.py:33-151)."""
+    from conftest import golden
+    ka = golden("known_answers")
+    y = L.psp_filter(ka["psp_in"], L.PSPKernel(2.0, 12, 0.1))
+    assert np.allclose(y, ka["psp_out"], rtol=1e-14, atol=1e-16), float(np.max(np.abs(y - ka["psp_out"])))
+    yd = L.psp_filter(torch.tensor(ka["psp_in"], dtype=torch.float32, device=cuda), L.PSPKernel(2.0, 12, 0.1))
+    assert yd.dtype == torch.float32 and np.allclose(yd.cpu().numpy(), ka["psp_out"], rtol=1e-5, atol=1e-6)
+    assert abs(L.smape(ka["smape_a"], ka["smape_b"]) - float(ka["smape"])) < 1e-12
+    st = L.AdamState(lr=1e-2)
+    p = {"w": ka["adam_w0"], "b": ka["adam_b0"]}
+    for k in range(3):
+        p = L.adam_step(p, {"w": ka["adam_gw"][k], "b": ka["adam_gb"][k]}, st, lr=L.cosine_lr(1e-2, k, 3))
+    assert np.allclose(p["w"], ka["adam_w3"], rtol=1e-13, atol=1e-15)
+    assert np.allclose(p["b"], ka["adam_b3"], rtol=1e-13, atol=1e-15)
