@@ -553,17 +553,27 @@ def main():
                          "source": prof.get("source")}
 
     extras = {}
+
+    def leg(name, fn):
+        # a failing secondary leg is reported in the line, not fatal to it
+        try:
+            extras[name] = fn()
+        except Exception as e:  # noqa: BLE001
+            extras[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            print(f"bench: {name} failed: {e}", file=sys.stderr)
+
     if not args.no_extras:
-        extras["e2e"] = e2e_leg(torch, args, params, rank)
-        ev = torch.tensor([extras["e2e"]["seconds_per_step"]], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ev, op=dist.ReduceOp.MAX)
-        extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
-        extras["fwd_bwd"] = fwd_bwd_leg(torch, dev)
-        extras["c4_train_step"] = c4_leg(torch, dev)
-        extras["c5_network"] = c5_leg(torch, dev)
-        extras["morphology"] = morph_leg(torch, dev)
-        if world > 1:
+        leg("e2e", lambda: e2e_leg(torch, args, params, rank))
+        if "seconds_per_step" in extras["e2e"]:
+            ev = torch.tensor([extras["e2e"]["seconds_per_step"]], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ev, op=dist.ReduceOp.MAX)
+            extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
+        leg("fwd_bwd", lambda: fwd_bwd_leg(torch, dev))
+        leg("c4_train_step", lambda: c4_leg(torch, dev))
+        leg("c5_network", lambda: c5_leg(torch, dev))
+        leg("morphology", lambda: morph_leg(torch, dev))
+        if world > 1 and "ms_per_step" in extras["fwd_bwd"]:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(fb, op=dist.ReduceOp.MAX)
             extras["fwd_bwd"]["value"] = 256 * 1024 * 100 * world / (float(fb.item()) * 1e-3)
