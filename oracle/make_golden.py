@@ -186,6 +186,10 @@ def main():
     ka["adam_gw"] = np.stack([g["w"] for g in gs])
     ka["adam_gb"] = np.stack([g["b"] for g in gs])
     ka["adam_w3"], ka["adam_b3"] = pa["w"], pa["b"]
+    # rest-state population rates at scale 0.1 (cortex.py:441-448), the
+    # statistical target of the device-background runs
+    rec_r = cortex.rest_state_run(1200.0, 0.1, 0, warmup_ms=200.0)
+    ka["rest_rates"] = np.array([rec_r.pop_rate(p.name) for p in rec_r.topo.populations])
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

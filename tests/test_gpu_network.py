@@ -133,3 +133,49 @@ def test_run_network_philox_graph_path(cuda):
     rec = N.run_network(topo, N.REST_CONFIG, 30.0, seed=2, background="philox", dtype=np.float32)
     assert isinstance(rec, N.SpikeRecord) and rec.times_ms.size > 0
     assert rec.times_ms.max() <= 30.0 + 1e-9
+
+
+def test_delay_impulse_and_dale_signs(cuda):
+    """SPEC known answers of step_network: one forced presynaptic spike with
+    delay d gives a postsynaptic current first nonzero exactly d steps later;
+    excitatory rows deliver >= 0, inhibitory <= 0 (Dale)."""
+    _, topo = _small()
+    pops = topo.populations
+    for k, p in enumerate(pops):
+        w = topo.syn_weight[topo.syn_offsets[p.offset]:topo.syn_offsets[p.offset + p.size]]
+        assert (w >= 0).all() if p.name.endswith("e") else (w <= 0).all()
+    cfg = N.REST_CONFIG
+    net = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float64, background="philox", seed=0)
+    src = int(np.argmax(np.diff(topo.syn_offsets)))          # the source with most synapses
+    lo, hi = topo.syn_offsets[src], topo.syn_offsets[src + 1]
+    tgt, dly = topo.syn_target[lo:hi], topo.syn_delay[lo:hi]
+    d_min = int(dly.min())
+    words = torch.zeros(net.words_global, dtype=torch.int32, device=cuda)
+    words[src // 32] = int(np.int32(np.uint32(1 << (src % 32))))
+    net.deliver(words)                                       # spike of `src` at step 0
+    ring = net.ring.cpu().numpy()
+    for d in range(net.depth):
+        row = ring[(d) % net.depth]
+        hit = np.flatnonzero(row)
+        exp_t = np.unique(tgt[dly == d])
+        assert np.array_equal(hit, exp_t), d
+    assert ring[d_min % net.depth].any() and not ring[0].any()
+
+
+def test_zero_drive_stays_at_rest_and_rest_rates_match_reference(cuda):
+    """No background and no activity: no spikes (rates 0).  The rest
+    configuration at scale 0.1 with the device (Philox) background reproduces
+    the reference's per-population rates from its own RNG stream (golden: the
+    reference rest_state_run, 1 s after 200 ms warm-up) within 10%: the same
+    compound-Poisson process, a different random stream."""
+    from dataclasses import replace
+    ka = golden("known_answers")
+    topo = N.build_network(0.1, 0)
+    quiet = replace(N.REST_CONFIG, bg_rate_hz=0.0)
+    rec = N.run_network(topo, quiet, 50.0, seed=1, background="philox", dtype=np.float32)
+    assert rec.times_ms.size == 0
+    rec = N.run_network(topo, N.REST_CONFIG, 1200.0, seed=1, warmup_ms=200.0, background="philox",
+                        dtype=np.float32)
+    rates = np.array([rec.pop_rate(p.name) for p in topo.populations])
+    ref = ka["rest_rates"]
+    assert np.all(np.abs(rates - ref) <= 0.1 * ref + 0.2), (rates, ref)
