@@ -371,6 +371,34 @@ def morph_leg(torch, dev):
                       "x 400 steps, fp32, V trace + spikes recorded (one unit = one compartment-step)"}
 
 
+def c5_replicas_leg(torch, dev, topo=None, replicas=(8, 32, 64), steps=640):
+    """Config 5 in the paper's "replicas x speed" view: R
+    independent copies of the scale-0.5 network stepped together on one GPU
+    (CortexReplicas: one input, one HH and one delivery launch per step for all
+    replicas, CUDA-graph replay).  One unit = one neuron-step of one replica."""
+    import numpy as np
+    from paper_2601_21407_b200 import network as N
+    topo = topo or N.build_network(0.5, 0)
+    out = {}
+    for R in replicas:
+        rep = N.CortexReplicas(topo, N.REST_CONFIG, R, device=dev, dtype=np.float32, seed=1)
+        rep.advance(128)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep.advance(steps)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out[str(R)] = {"ms_per_network_step": ms, "value": R * topo.n_neurons / (ms * 1e-3)}
+        del rep
+        torch.cuda.empty_cache()
+    best = max(out, key=lambda k: out[k]["value"])
+    return {"value": out[best]["value"], "unit": UNIT, "replicas": int(best), "by_replicas": out,
+            "config": "BASELINE config 5 network (scale 0.5, 38,586 neurons, 71.2M synapses), R independent "
+                      "replicas per GPU, fp32, device background (one unit = one neuron-step of one replica)"}
+
+
 def c4_leg(torch, dev):
     """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
     batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
@@ -573,6 +601,7 @@ def main():
         leg("c4_train_step", lambda: c4_leg(torch, dev))
         leg("c5_network", lambda: c5_leg(torch, dev))
         leg("morphology", lambda: morph_leg(torch, dev))
+        leg("c5_replicas", lambda: c5_replicas_leg(torch, dev))
         if world > 1 and "ms_per_step" in extras["fwd_bwd"]:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(fb, op=dist.ReduceOp.MAX)
@@ -593,7 +622,7 @@ def main():
                 "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
                 "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
-                "morphology": extras.get("morphology"),
+                "morphology": extras.get("morphology"), "c5_replicas": extras.get("c5_replicas"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)

@@ -370,6 +370,20 @@ int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* o
                            int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring,
                            int64_t* scratch, void* stream);
 int64_t hhb_spike_scratch(int64_t n_sources);
+/* `replicas` independent copies of one network on one GPU ("replicas x speed",
+ * PAPER.md:193; SPEC data-parallel batching): per-replica state rows of n_pad
+ * (= 32-aligned neuron count) neurons, ring [replicas][depth][n_pad], bitmap
+ * [replicas][n_pad/32] words, Philox background keyed by (seed + replica,
+ * neuron, step), step index on the device.  phase 0 = the input of every
+ * replica (ring drain, PSP, background: cortex.py:283-301); phase 1 =
+ * compaction + delivery of every replica's spikes (cortex.py:304-308); the HH
+ * step of all replicas runs in between as one population (hhb_forward_ex).
+ * scratch: replicas * hhb_spike_scratch(n_pad) int64. */
+int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_t words, const int64_t* t_dev,
+                          int64_t depth, int64_t* ring, void* psp, double decay, const double* lam, double mu,
+                          double sigma, uint64_t seed, void* cur, double w_scale, const uint32_t* bits,
+                          const int64_t* offsets, const int32_t* targets, const int32_t* weights_fx,
+                          const int32_t* delays, int64_t* scratch, int32_t phase, void* stream);
 
 /* ---- runtime specialisation ----------------------------------------------- */
 

@@ -133,6 +133,8 @@ SIGNATURES = {
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hhb_spike_deliver_flat": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
     "hhb_spike_scratch": (_i64, [_i64]),
+    "hhb_cortex_step_batch": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _dbl, _vp, _dbl, _dbl, C.c_uint64,
+                                     _vp, _dbl, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
 }

@@ -20,10 +20,16 @@ namespace cortex {
 template <typename T>
 __global__ void k_cortex_input(int64_t n, int64_t t, const long long* t_dev, int64_t depth, long long* ring, T* psp,
                                T decay, int mode, const T* bg, const double* lam, T mu, T sigma, uint64_t seed,
-                               int64_t nbase, const T* extra, T* cur, T w_scale) {
+                               int64_t nbase, const T* extra, T* cur, T w_scale, int64_t rep_ring = 0) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (t_dev) t = *t_dev;
+  // replica blockIdx.y: its own ring / psp / current rows and key seed + r
+  const int64_t r = blockIdx.y;
+  ring += r * rep_ring;
+  psp += r * n;
+  cur += r * n;
+  seed += uint64_t(r);
   long long* slot = ring + (t % depth) * n + i;
   const long long arr = *slot;
   *slot = 0;
@@ -96,8 +102,16 @@ __global__ void k_tick(long long* t) { *t += 1; }
 constexpr int kCompactThreads = 1024;
 __global__ void __launch_bounds__(kCompactThreads) k_spike_compact(int64_t words, const uint32_t* bits,
                                                                     const int64_t* off, int32_t* src,
-                                                                    int64_t* pre, int64_t* totals) {
+                                                                    int64_t* pre, int64_t* totals,
+                                                                    int64_t rep_scratch = 0) {
   __shared__ int64_t scan[kCompactThreads];
+  {  // replica blockIdx.x: its bitmap and its slice of the scratch
+    const int64_t r = blockIdx.x;
+    bits += r * words;
+    totals = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(totals) + r * rep_scratch);
+    pre = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(pre) + r * rep_scratch);
+    src = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(src) + r * rep_scratch);
+  }
   const int tid = threadIdx.x;
   const int64_t per = (words + kCompactThreads - 1) / kCompactThreads;
   const int64_t w0 = tid * per, w1 = min(words, w0 + per);
@@ -147,7 +161,15 @@ __global__ void __launch_bounds__(kCompactThreads) k_spike_compact(int64_t words
 __global__ void __launch_bounds__(256) k_spike_scatter(const int32_t* src, const int64_t* pre, const int64_t* totals,
                                                        const int64_t* off, const int32_t* tgt, const int32_t* w,
                                                        const int32_t* delay, int64_t t, const long long* t_dev,
-                                                       int64_t depth, int64_t n, long long* ring) {
+                                                       int64_t depth, int64_t n, long long* ring,
+                                                       int64_t rep_scratch = 0, int64_t rep_ring = 0) {
+  {  // replica blockIdx.y
+    const int64_t r = blockIdx.y;
+    totals = reinterpret_cast<const int64_t*>(reinterpret_cast<const char*>(totals) + r * rep_scratch);
+    pre = reinterpret_cast<const int64_t*>(reinterpret_cast<const char*>(pre) + r * rep_scratch);
+    src = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(src) + r * rep_scratch);
+    ring += r * rep_ring;
+  }
   const int64_t ns = totals[0], total = totals[1];
   if (t_dev) t = *t_dev;
   for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
@@ -225,6 +247,7 @@ int hhb_spike_deliver_dev(int64_t words, const uint32_t* bits, const int64_t* of
 
 int64_t hhb_spike_scratch(int64_t n_sources) { return 2 * n_sources + 3; }
 
+
 int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* offsets, const int32_t* targets,
                            const int32_t* weights_fx, const int32_t* delays, int64_t t, const int64_t* t_dev,
                            int64_t depth, int64_t n_local, int64_t* ring, int64_t* scratch, void* stream) {
@@ -243,6 +266,50 @@ int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* o
                                                         reinterpret_cast<const long long*>(t_dev), depth, n_local,
                                                         reinterpret_cast<long long*>(ring));
   return cuda_check("k_spike_compact / k_spike_scatter launch");
+}
+
+int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_t words, const int64_t* t_dev,
+                          int64_t depth, int64_t* ring, void* psp, double decay, const double* lam, double mu,
+                          double sigma, uint64_t seed, void* cur, double w_scale, const uint32_t* bits,
+                          const int64_t* offsets, const int32_t* targets, const int32_t* weights_fx,
+                          const int32_t* delays, int64_t* scratch, int32_t phase, void* stream) {
+  // phase 0: the input of every replica; phase 1: compaction + delivery of every
+  // replica's bitmap (the HH step of all replicas' neurons runs in between as
+  // one population of replicas * n_pad neurons)
+  if (replicas < 1 || n_pad <= 0 || n_pad % 32 || words != n_pad / 32 || !t_dev || !ring)
+    return fail(HHB_EINVAL, "bad cortex batch args");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long* rg = reinterpret_cast<long long*>(ring);
+  const int64_t rep_ring = depth * n_pad;
+  if (phase == 0) {
+    if (!psp || !cur || !lam) return fail(HHB_EINVAL, "bad cortex batch input args");
+    const dim3 grid{unsigned((n_pad + 255) / 256), unsigned(replicas), 1u};
+    const long long* td = reinterpret_cast<const long long*>(t_dev);
+    if (dtype == HHB_F32)
+      cortex::k_cortex_input<float><<<grid, 256, 0, st>>>(n_pad, 0, td, depth, rg, (float*)psp, float(decay), 2,
+                                                          nullptr, lam, float(mu), float(sigma), seed, 0, nullptr,
+                                                          (float*)cur, float(w_scale), rep_ring);
+    else if (dtype == HHB_F64)
+      cortex::k_cortex_input<double><<<grid, 256, 0, st>>>(n_pad, 0, td, depth, rg, (double*)psp, decay, 2, nullptr,
+                                                           lam, mu, sigma, seed, 0, nullptr, (double*)cur, w_scale,
+                                                           rep_ring);
+    else
+      return fail(HHB_EINVAL, "dtype");
+    return cuda_check("k_cortex_input (batch) launch");
+  }
+  if (!bits || !offsets || !scratch) return fail(HHB_EINVAL, "bad cortex batch delivery args");
+  if (words * 32 >= (int64_t(1) << 23)) return fail(HHB_EINVAL, "cortex batch: too many neurons per replica");
+  const int64_t per = hhb_spike_scratch(words * 32);         // int64 per replica
+  int64_t* totals = scratch;
+  int64_t* pre = scratch + 2;
+  int32_t* src = reinterpret_cast<int32_t*>(pre + words * 32 + 1);
+  cortex::k_spike_compact<<<unsigned(replicas), cortex::kCompactThreads, 0, st>>>(words, bits, offsets, src, pre,
+                                                                                  totals, per * 8);
+  const dim3 g2{unsigned(kNumSMs), unsigned(replicas), 1u};
+  cortex::k_spike_scatter<<<g2, 256, 0, st>>>(src, pre, totals, offsets, targets, weights_fx, delays, 0,
+                                              reinterpret_cast<const long long*>(t_dev), depth, n_pad, rg, per * 8,
+                                              rep_ring);
+  return cuda_check("k_spike_compact / k_spike_scatter (batch) launch");
 }
 
 int hhb_cortex_tick(int64_t* t_dev, void* stream) {

@@ -619,3 +619,108 @@ def thalamic_stimulus_run(duration_ms: float, scale: float, seed: int, t_on_ms: 
             "rate_hz": rate_hz if rate_hz is not None else conn.THALAMIC_RATE_HZ,
             "weight": cfg.bg_mean, "weight_std": cfg.bg_std}
     return run_network(topo, cfg, duration_ms, seed + 1, warmup_ms=warmup_ms, thalamic=thal, **kw)
+
+
+class CortexReplicas:
+    """`replicas` independent copies of one network on one GPU, stepped
+    together ("replicas x speed"; SPEC's data-parallel batching):
+    one input launch, one HH launch over replicas * n_pad neurons and one
+    delivery launch per step for all of them, replayed as CUDA graphs.  Replica
+    r draws the device background with seed + r and reproduces, bit for bit, a
+    single `CortexNetwork(..., background="philox", seed=seed + r)` run.  The
+    per-step cost of one network is launch-latency-bound; a batch fills the GPU."""
+
+    def __init__(self, topo: NetworkTopology, config: CortexConfig, replicas: int, device=None,
+                 dtype=np.float32, seed: int = 0):
+        if replicas < 1:
+            raise UsageError("replicas must be >= 1")
+        self.topo, self.config, self.R = topo, config, int(replicas)
+        self.dev = device or D.require_cuda()
+        self.params = config.resolved_neuron().with_(dtype=dtype)
+        self.dtype = np.dtype(dtype)
+        self.td = D.torch_dtype(self.dtype)
+        self.n = topo.n_neurons
+        self.n_pad = (self.n + 31) // 32 * 32
+        self.words = self.n_pad // 32
+        self.depth = topo.max_delay + 1
+        dev = self.dev
+        off, tgt, w, d = local_synapses(topo, 0, self.n)
+        self.off = torch.from_numpy(off).to(dev)
+        self.tgt = torch.from_numpy(tgt).to(dev)
+        self.w = torch.from_numpy(quantise_weights(w)).to(dev)
+        self.delay = torch.from_numpy(d.astype(np.int32)).to(dev)
+        NT = self.R * self.n_pad
+        st = init_state(self.params, (NT,), device=dev)
+        self.v, self.g = st.v.contiguous(), st.gates.contiguous()
+        self.psp = torch.zeros(NT, dtype=self.td, device=dev)
+        self.cur = torch.empty(NT, dtype=self.td, device=dev)
+        self.ring = torch.zeros((self.R, self.depth, self.n_pad), dtype=torch.int64, device=dev)
+        self.bits = torch.zeros(self.R * self.words, dtype=torch.int32, device=dev)
+        lib = nat.load()
+        self.scratch = torch.empty(self.R * int(lib.hhb_spike_scratch(self.n_pad)), dtype=torch.int64, device=dev)
+        bg = make_background(config)
+        self.bg = bg
+        lam = np.zeros(self.n_pad)
+        lam[:self.n] = background_lambda(topo, bg, config.dt)
+        self.lam = torch.from_numpy(lam).to(dev)
+        self.decay = math.exp(-config.dt / config.psp_tau_ms)
+        self.seed = int(seed)
+        self.first_bad = torch.full((1,), D.INT64_MAX, dtype=torch.int64, device=dev)
+        self.t = 0
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._graphs = {}
+
+    def _phase(self, phase: int):
+        nat.check(nat.load().hhb_cortex_step_batch(
+            D.code(self.dtype), self.R, self.n_pad, self.words, self.t_dev.data_ptr(), self.depth,
+            self.ring.data_ptr(), self.psp.data_ptr(), self.decay, self.lam.data_ptr(), self.bg.w_mean,
+            self.bg.w_std, self.seed, self.cur.data_ptr(), float(1.0 / (1 << W_FRAC_BITS)), self.bits.data_ptr(),
+            self.off.data_ptr(), self.tgt.data_ptr(), self.w.data_ptr(), self.delay.data_ptr(),
+            self.scratch.data_ptr(), phase, D.stream()), "hhb_cortex_step_batch")
+
+    def _step_dev(self):
+        self._phase(0)
+        _forward(self.params, self.v, self.g, self.cur, 0, 1, 1, v_fin=self.v, g_fin=self.g,
+                 bits=self.bits.view(1, -1), step_base=0, first_bad=self.first_bad, reset_bad=False,
+                 step_dev=self.t_dev)
+        self._phase(1)
+        nat.check(nat.load().hhb_cortex_tick(self.t_dev.data_ptr(), D.stream()), "hhb_cortex_tick")
+
+    def advance(self, n_steps: int, steps_per_graph: int = 32, record: torch.Tensor | None = None):
+        """Advance all replicas n_steps (CUDA graphs of steps_per_graph steps).
+        record: optional int32 [n_steps][replicas][n_pad/32] spike words."""
+        self.t_dev.fill_(self.t)
+        S = max(1, min(int(steps_per_graph), n_steps)) if n_steps > 0 else 1
+        done, rec = 0, record is not None
+        if n_steps >= S:
+            key = (S, rec)
+            if key not in self._graphs:
+                buf = torch.empty((S, self.R * self.words), dtype=torch.int32, device=self.dev) if rec else None
+                t0 = self.t_dev.clone()
+                snap = (self.v.clone(), self.g.clone(), self.psp.clone(), self.ring.clone())
+                self._step_dev()
+                self.t_dev.copy_(t0)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for k in range(S):
+                        self._step_dev()
+                        if rec:
+                            buf[k].copy_(self.bits)
+                self.v.copy_(snap[0]); self.g.copy_(snap[1]); self.psp.copy_(snap[2]); self.ring.copy_(snap[3])
+                self.t_dev.copy_(t0)
+                self._graphs[key] = (g, buf)
+            g, buf = self._graphs[key]
+            while n_steps - done >= S:
+                g.replay()
+                if rec:
+                    record[done:done + S].copy_(buf.view(S, self.R, self.words))
+                done += S
+        while done < n_steps:
+            self._step_dev()
+            if rec:
+                record[done].copy_(self.bits.view(self.R, self.words))
+            done += 1
+        self.t += n_steps
+        _raise_if_bad(self.first_bad)
+        return record

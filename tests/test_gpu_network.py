@@ -179,3 +179,20 @@ def test_zero_drive_stays_at_rest_and_rest_rates_match_reference(cuda):
     rates = np.array([rec.pop_rate(p.name) for p in topo.populations])
     ref = ka["rest_rates"]
     assert np.all(np.abs(rates - ref) <= 0.1 * ref + 0.2), (rates, ref)
+
+
+def test_replicas_reproduce_single_network_runs(cuda):
+    """CortexReplicas: replica r (seed + r) is bit-identical to a lone
+    CortexNetwork run with seed + r (SPEC data-parallel batching)."""
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    R, steps = 5, 200
+    rep = N.CortexReplicas(topo, cfg, R, device=cuda, dtype=np.float32, seed=7)
+    rec = torch.empty((steps, R, rep.words), dtype=torch.int32, device=cuda)
+    rep.advance(steps, steps_per_graph=32, record=rec)
+    assert rec.any()
+    for r in (0, 3, 4):
+        single = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=7 + r)
+        rows = torch.stack([single.step().clone() for _ in range(steps)])
+        assert torch.equal(rows, rec[:, r, :rows.shape[1]]), r
+        assert torch.equal(single.v, rep.v[r * rep.n_pad:r * rep.n_pad + topo.n_neurons])
