@@ -308,6 +308,19 @@ int hhb_lif_backward(int32_t dtype, int64_t n, double tau, double dt, double v_t
 int hhb_psp_filter(int32_t dtype, int64_t steps, int64_t cols, int32_t ntaps, const double* taps_dev,
                    const void* x, void* y, void* stream);
 
+/* ReadoutModel dendrite layer (learn.py:238-247, one output channel):
+ * drive[t][b] = bias[0] + sum_c x(b,t,c) w[c], x(b,t,c) at x[b*x_sb + t*x_st + c];
+ * drive is written time-major [steps][batch] (the HH i_series).  w, bias device. */
+int hhb_readout_drive(int32_t dtype, int64_t batch, int64_t steps, int64_t n_in, const void* x, int64_t x_sb,
+                      int64_t x_st, const void* w, const void* bias, void* drive, void* stream);
+/* ReadoutModel.grads weight part (learn.py:269-273): d_w[c] = sum d_drive[t][b] x(b,t,c),
+ * d_b[0] = sum d_drive; deterministic (fixed-order two-stage reduction) into a
+ * caller workspace of hhb_readout_workspace(dtype, n_in) bytes. */
+int64_t hhb_readout_workspace(int32_t dtype, int64_t n_in);
+int hhb_readout_grad(int32_t dtype, int64_t batch, int64_t steps, int64_t n_in, const void* x, int64_t x_sb,
+                     int64_t x_st, const void* d_drive, void* d_w, void* d_b, void* workspace, int64_t ws_bytes,
+                     void* stream);
+
 /* ---- multicompartment neurons (morphology.py) ---------------- */
 
 /* T steps of `batch` independent multicompartment neurons on one compartment

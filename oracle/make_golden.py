@@ -304,6 +304,29 @@ def main():
                         d_b=d_drive.sum(axis=(0, 1)), d_c_m=np.float64(res.d_c_m),
                         d_g_max=res.d_g_max)
 
+    # -- teacher-student readout fitting (learn.py:223-377) -------------------
+    task = learn.make_teacher_student_task(n_channels=16, n_steps=120, n_train=4, n_val=3, pad_len=20, seed=2)
+    student = learn.make_student(task, seed=5)
+    w_init = student.dense.weights.copy()
+    filt = task.teacher.filter_inputs(task.train_inputs)
+    pred_t, v_t = task.teacher.forward(filt)
+    rng_g = np.random.default_rng(17)
+    seed_pred = rng_g.normal(size=pred_t.shape) * 1e-2
+    g_t = task.teacher.grads(filt, seed_pred, v_t)
+    hist = learn.fit(student, task, learn.TrainConfig(epochs=5, lr=2e-2))
+    seg = learn.segment_traces(np.arange(50.0), 2.0 * np.arange(50.0), learn.SegmentationScheme(7, 9))
+    tr_idx, te_idx = learn.split_dataset(11, np.random.default_rng(4))
+    np.savez_compressed(os.path.join(OUT, "readout_fit.npz"),
+                        train_inputs=task.train_inputs, train_targets=task.train_targets,
+                        val_inputs=task.val_inputs, val_targets=task.val_targets,
+                        teacher_w=task.teacher.dense.weights, filtered=filt, teacher_v=v_t,
+                        seed_pred=seed_pred, g_w=g_t["w"], g_b=g_t["b"], g_sw=np.float64(g_t["scale_w"]),
+                        g_sb=np.float64(g_t["scale_b"]), student_w0=w_init, history=np.array(hist),
+                        final_w=student.dense.weights, final_b=student.dense.bias,
+                        final_sw=np.float64(student.scale_w), final_sb=np.float64(student.scale_b),
+                        seg_in=np.array([a for a, _ in seg]), seg_out=np.array([b for _, b in seg]),
+                        split_train=tr_idx, split_test=te_idx)
+
     # -- cortex topology + short network run (cortex.py:138-218, :379-438) ---
     topo = cortex.build_network(0.02, 0)
     rec = cortex.run_network(topo, cortex.REST_CONFIG, 20.0, seed=1)

@@ -126,6 +126,9 @@ SIGNATURES = {
     "hhb_cortex_tick": (_i32, [_vp, _vp]),
     "hhb_scale_f32": (_i32, [_i64, _vp, _vp, _dbl, _vp, _vp]),
     "hhb_psp_filter": (_i32, [_i32, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "hhb_readout_drive": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "hhb_readout_workspace": (_i64, [_i32, _i64]),
+    "hhb_readout_grad": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "hhb_lif_forward": (_i32, [_i32, _i64, _i64, _dbl, _dbl, _dbl, _dbl, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "hhb_lif_backward": (_i32, [_i32, _i64, _dbl, _dbl, _dbl, _dbl, C.POINTER(Surrogate), _vp, _vp, _i64, _vp, _vp,
                                 _vp, _vp, _vp, _vp]),

@@ -92,7 +92,7 @@ def mse(v: torch.Tensor, target: torch.Tensor | None = None) -> torch.Tensor:
 import math
 from dataclasses import dataclass, field
 
-from .errors import ConfigurationError
+from .errors import ConfigurationError, TrainingDivergedError
 
 
 @dataclass(frozen=True)
@@ -190,3 +190,328 @@ def adam_step(params: dict, grads: dict, state: AdamState, lr: float | None = No
 def cosine_lr(base_lr: float, epoch: int, total_epochs: int) -> float:
     """Cosine annealing from base_lr to 0 over the run (learn.py:149-151)."""
     return base_lr * 0.5 * (1.0 + math.cos(math.pi * epoch / max(total_epochs, 1)))
+
+
+# ---------------------------------------------------------------------------
+# trace segmentation and dataset split (learn.py:158-196)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SegmentationScheme:
+    """pad_len warm-up steps followed by out_len supervised steps per sample;
+    consecutive supervised windows tile the trace (learn.py:158-170)."""
+
+    pad_len: int
+    out_len: int
+
+    def __post_init__(self):
+        if self.pad_len < 0 or self.out_len <= 0:
+            raise ConfigurationError("invalid segmentation scheme")
+
+
+def segment_traces(input_trace, output_trace, scheme: SegmentationScheme):
+    """[(input[lo:lo+pad+out], output[lo+pad:lo+pad+out]) for lo = k*out_len]
+    (learn.py:173-189); views of the caller's arrays, as the reference."""
+    x = np.asarray(input_trace)
+    y = np.asarray(output_trace)
+    if x.shape[0] != y.shape[0]:
+        raise UsageError("input and output traces must share length")
+    count = max((x.shape[0] - scheme.pad_len) // scheme.out_len, 0)
+    width = scheme.pad_len + scheme.out_len
+    return [(x[k * scheme.out_len:k * scheme.out_len + width],
+             y[k * scheme.out_len + scheme.pad_len:k * scheme.out_len + width]) for k in range(count)]
+
+
+def split_dataset(n_samples: int, rng: np.random.Generator, ratio=(3, 1)):
+    """Shuffled (train, test) index split, floor on the train side (learn.py:192-196)."""
+    order = rng.permutation(n_samples)
+    cut = n_samples * ratio[0] // (ratio[0] + ratio[1])
+    return order[:cut], order[cut:]
+
+
+# ---------------------------------------------------------------------------
+# dense layer and the teacher-student readout model (learn.py:203-274)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DenseLayer:
+    """y = x @ W.T + b over the trailing axis (learn.py:203-216).  numpy in ->
+    numpy out (computed on the device); CUDA tensors in -> tensors out."""
+
+    weights: object   # (out, in)
+    bias: object      # (out,)
+
+    def __call__(self, x):
+        on_dev = D.is_dev(x)
+        xd = _dev(x)
+        w = _dev(self.weights).to(xd.dtype)
+        b = _dev(self.bias).to(xd.dtype)
+        y = torch.matmul(xd, w.t()) + b
+        return y if on_dev else y.cpu().numpy()
+
+    @staticmethod
+    def init(n_out: int, n_in: int, rng: np.random.Generator, scale: float | None = None) -> "DenseLayer":
+        s = 1.0 / math.sqrt(n_in) if scale is None else scale
+        return DenseLayer(rng.normal(0.0, s, size=(n_out, n_in)), np.zeros(n_out))
+
+
+def _readout_ws(n_in: int, dev) -> torch.Tensor:
+    nbytes = int(nat.load().hhb_readout_workspace(nat.F64, n_in))
+    key = (dev, nbytes)
+    ws = _READOUT_WS.get(key)
+    if ws is None:
+        ws = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
+        _READOUT_WS[key] = ws
+    return ws
+
+
+_READOUT_WS: dict = {}
+
+
+def _x3(filtered) -> torch.Tensor:
+    """(B, T, C) float64 device tensor with unit channel stride (views kept)."""
+    x = _dev(filtered).double()
+    if x.dim() != 3:
+        raise UsageError("filtered inputs must be (batch, steps, channels)")
+    return x if x.stride(2) == 1 else x.contiguous()
+
+
+def _readout_drive(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """dense(filtered)[..., 0] written time-major (T, B): the HH i_series."""
+    B, T, C = x.shape
+    out = torch.empty((T, B), dtype=torch.float64, device=x.device)
+    nat.check(nat.load().hhb_readout_drive(nat.F64, B, T, C, x.data_ptr(), x.stride(0), x.stride(1),
+                                           w.data_ptr(), b.data_ptr(), out.data_ptr(), D.stream()),
+              "hhb_readout_drive")
+    return out
+
+
+@dataclass
+class ReadoutModel:
+    """PSP filter -> dense dendrite layer -> HH point neuron -> affine output
+    scaling (learn.py:223-274).  The dendrite GEMV and its weight gradient are
+    hhb_readout_drive / hhb_readout_grad, the neuron is the fused forward and
+    BPTT kernels; numpy in -> numpy out like the reference, CUDA tensors in ->
+    tensors out (what `fit` uses so the whole loop stays on the device)."""
+
+    dense: DenseLayer
+    scale_w: float
+    scale_b: float
+    neuron: object
+    kernel: PSPKernel
+
+    def filter_inputs(self, spikes):
+        """spikes (B, T, C) -> filtered currents (B, T, C) (learn.py:233-235)."""
+        on_dev = D.is_dev(spikes)
+        x = _dev(spikes).double().permute(1, 0, 2).contiguous()     # (T, B, C)
+        y = psp_filter(x, self.kernel).permute(1, 0, 2)              # (B, T, C) view
+        return y if on_dev else y.cpu().numpy()
+
+    def _params_dev(self, dev):
+        w = _dev(self.dense.weights).double().reshape(-1).contiguous()
+        b = _dev(self.dense.bias).double().reshape(-1).contiguous()
+        if b.numel() != 1:
+            raise UsageError("ReadoutModel has one output channel")
+        return w, b
+
+    def _drive(self, filtered):
+        x = _x3(filtered)
+        w, b = self._params_dev(x.device)
+        if w.numel() != x.shape[2]:
+            raise UsageError("dense weights do not match the channel count")
+        return x, _readout_drive(x, w, b)
+
+    def forward(self, filtered):
+        """filtered (B, T, C) -> (prediction (B, T), membrane (B, T)) (learn.py:237-245)."""
+        from .dynamics import init_state, simulate
+        on_dev = D.is_dev(filtered)
+        _, i_series = self._drive(filtered)                         # (T, B)
+        state0 = init_state(self.neuron, i_series.shape[1:], device=i_series.device)
+        trace = simulate(self.neuron, i_series, state0=state0)
+        v = trace.v_series.double().t()                              # (B, T)
+        pred = v * _scalar(self.scale_w, v) + _scalar(self.scale_b, v)
+        if on_dev:
+            return pred, v
+        return pred.cpu().numpy(), v.contiguous().cpu().numpy()
+
+    def params(self) -> dict:
+        return {"w": self.dense.weights, "b": self.dense.bias,
+                "scale_w": self.scale_w if D.is_dev(self.scale_w) else np.float64(self.scale_w),
+                "scale_b": self.scale_b if D.is_dev(self.scale_b) else np.float64(self.scale_b)}
+
+    def load_params(self, p: dict) -> None:
+        """learn.py:255-259; device tensors are kept on the device."""
+        if D.is_dev(p["w"]):
+            self.dense.weights, self.dense.bias = p["w"], p["b"]
+            self.scale_w, self.scale_b = p["scale_w"], p["scale_b"]
+            return
+        self.dense.weights = np.asarray(p["w"], dtype=np.float64)
+        self.dense.bias = np.asarray(p["b"], dtype=np.float64)
+        self.scale_w = float(p["scale_w"])
+        self.scale_b = float(p["scale_b"])
+
+    def grads(self, filtered, seed_pred, v, surrogate=None) -> dict:
+        """d(loss)/d(prediction) -> every trainable (learn.py:261-274)."""
+        from .adjoint import backward_through_time
+        from .dynamics import init_state
+        on_dev = D.is_dev(filtered)
+        sp = _dev(seed_pred).double()
+        vd = _dev(v).double()
+        d_scale_w = (sp * vd).sum()
+        d_scale_b = sp.sum()
+        seed_v = (sp * _scalar(self.scale_w, sp)).t().contiguous()  # (T, B)
+        x, i_series = self._drive(filtered)
+        state0 = init_state(self.neuron, i_series.shape[1:], device=i_series.device)
+        res = backward_through_time(self.neuron, state0, i_series, seed_v, surrogate=surrogate)
+        d_i = res.d_i.double().contiguous()                          # (T, B) = d_drive time-major
+        B, T, C = x.shape
+        d_w = torch.empty((1, C), dtype=torch.float64, device=x.device)
+        d_b = torch.empty(1, dtype=torch.float64, device=x.device)
+        ws = _readout_ws(C, x.device)
+        nat.check(nat.load().hhb_readout_grad(nat.F64, B, T, C, x.data_ptr(), x.stride(0), x.stride(1),
+                                              d_i.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), ws.data_ptr(),
+                                              ws.numel() * 8, D.stream()), "hhb_readout_grad")
+        if on_dev:
+            return {"w": d_w, "b": d_b, "scale_w": d_scale_w, "scale_b": d_scale_b}
+        return {"w": d_w.cpu().numpy(), "b": d_b.cpu().numpy(), "scale_w": float(d_scale_w.item()),
+                "scale_b": float(d_scale_b.item())}
+
+
+def _scalar(s, like: torch.Tensor):
+    return s.to(like.dtype) if isinstance(s, torch.Tensor) else float(s)
+
+
+@dataclass
+class TeacherStudentTask:
+    """Frozen teacher readout labelling Poisson spike trains (learn.py:277-286)."""
+
+    teacher: ReadoutModel
+    train_inputs: np.ndarray   # (B, T, C) binary
+    train_targets: np.ndarray  # (B, T)
+    val_inputs: np.ndarray
+    val_targets: np.ndarray
+    pad_len: int
+
+
+def make_teacher_student_task(n_channels: int = 64, n_steps: int = 500, n_train: int = 16, n_val: int = 8,
+                              rate_hz: float = 60.0, pad_len: int = 50, seed: int = 0,
+                              neuron=None) -> TeacherStudentTask:
+    """The synthetic fitting task (learn.py:289-327): signed teacher weights
+    (first half excitatory U(0.5, 1.5), second half inhibitory -U(0.1, 0.6),
+    scaled by 16 / n_channels, bias 0.45) and Bernoulli(rate·dt) spike trains,
+    drawn from default_rng(seed) in the reference's order; targets from the
+    teacher's device forward."""
+    from .defaults import cortical_rs_params
+    rng = np.random.default_rng(seed)
+    neuron = cortical_rs_params(dt=0.1) if neuron is None else neuron
+    kernel = PSPKernel(tau_decay=2.0, length=64, dt=neuron.dt)
+    n_exc = n_channels // 2
+    w = np.empty((1, n_channels))
+    w[0, :n_exc] = rng.uniform(0.5, 1.5, n_exc)
+    w[0, n_exc:] = -rng.uniform(0.1, 0.6, n_channels - n_exc)
+    w *= 16.0 / n_channels
+    teacher = ReadoutModel(DenseLayer(w, np.array([0.45])), 1.0, 0.0, neuron, kernel)
+    p_spike = rate_hz * neuron.dt / 1000.0
+    train_inputs = (rng.random((n_train, n_steps, n_channels)) < p_spike).astype(np.float64)
+    val_inputs = (rng.random((n_val, n_steps, n_channels)) < p_spike).astype(np.float64)
+    train_targets, _ = teacher.forward(teacher.filter_inputs(train_inputs))
+    val_targets, _ = teacher.forward(teacher.filter_inputs(val_inputs))
+    return TeacherStudentTask(teacher, train_inputs, train_targets, val_inputs, val_targets, pad_len)
+
+
+def make_student(task: TeacherStudentTask, seed: int = 1) -> ReadoutModel:
+    """Teacher architecture with re-initialised trainables (learn.py:330-336)."""
+    rng = np.random.default_rng(seed)
+    t = task.teacher
+    n_in = np.shape(t.dense.weights)[1]
+    return ReadoutModel(DenseLayer.init(1, n_in, rng, scale=4.0 / n_in), 1.0, 0.0, t.neuron, t.kernel)
+
+
+@dataclass
+class TrainConfig:
+    epochs: int = 200
+    lr: float = 5e-4
+    cosine: bool = True
+    freeze: bool = False
+
+
+def evaluate_smape(model: ReadoutModel, inputs, targets, pad_len: int) -> float:
+    """sMAPE of the model's prediction past the warm-up prefix (learn.py:346-348)."""
+    pred, _ = model.forward(model.filter_inputs(inputs))
+    return smape(_dev(pred)[:, pad_len:], _dev(targets)[:, pad_len:])
+
+
+def fit(model: ReadoutModel, task: TeacherStudentTask, config: TrainConfig):
+    """Full-batch fitting loop (learn.py:351-377), device-resident: inputs are
+    filtered once (train and validation -- the reference re-filters the
+    validation set each epoch; the filter is deterministic, so the values are
+    the same), parameters and Adam moments stay on the device, and each epoch
+    reads back only the loss and the validation sMAPE.  Returns the history
+    rows (epoch, train_loss, val_smape); the model ends with numpy parameters
+    as the reference's."""
+    dev = D.require_cuda()
+    filtered = model.filter_inputs(torch.as_tensor(np.asarray(task.train_inputs, dtype=np.float64), device=dev))
+    val_filtered = model.filter_inputs(torch.as_tensor(np.asarray(task.val_inputs, dtype=np.float64), device=dev))
+    targets = _dev(task.train_targets).double()
+    val_targets = _dev(task.val_targets).double()
+    pad = task.pad_len
+    mask = torch.zeros_like(targets)
+    mask[:, pad:] = 1.0
+    masked_targets = targets * mask
+    opt = AdamState(lr=config.lr)
+    p0 = model.params()
+    params = {k: _dev(v).double() for k, v in p0.items()}
+    history = []
+    for epoch in range(config.epochs):
+        model.load_params(params)
+        pred, v = model.forward(filtered)
+        loss, seed = mse_loss(pred * mask, masked_targets)
+        loss_f = float(loss.item())
+        if not math.isfinite(loss_f):
+            raise TrainingDivergedError("training loss became non-finite", epoch)
+        if not config.freeze:
+            grads = model.grads(filtered, seed * mask, v)
+            lr = cosine_lr(config.lr, epoch, config.epochs) if config.cosine else config.lr
+            params = adam_step(params, grads, opt, lr=lr)
+        vpred, _ = model.forward(val_filtered)
+        history.append((epoch, loss_f, smape(vpred[:, pad:], val_targets[:, pad:])))
+    model.load_params({k: (t.cpu().numpy() if t.dim() else np.float64(t.item())) for k, t in params.items()})
+    return history
+
+
+# ---------------------------------------------------------------------------
+# dataset and history files (learn.py:384-414)
+# ---------------------------------------------------------------------------
+
+import json
+
+
+def write_ndjson_dataset(path, inputs, targets, pad_len: int) -> None:
+    """One JSON record per sample: {"input": 2-D, "target": 2-D, "pad_len"} (learn.py:384-395)."""
+    with open(path, "w") as f:
+        for x, y in zip(inputs, targets):
+            y = np.asarray(y)
+            tgt = y.reshape(-1, 1) if y.ndim == 1 else y
+            f.write(json.dumps({"input": np.asarray(x).tolist(), "target": tgt.tolist(),
+                                "pad_len": pad_len}) + "\n")
+
+
+def read_ndjson_dataset(path):
+    """(inputs, targets, pad_len) stacked from write_ndjson_dataset's format (learn.py:398-408)."""
+    xs, ys, pad = [], [], 0
+    with open(path) as f:
+        for line in f:
+            if line.strip():
+                rec = json.loads(line)
+                xs.append(np.asarray(rec["input"], dtype=np.float64))
+                ys.append(np.asarray(rec["target"], dtype=np.float64))
+                pad = int(rec["pad_len"])
+    return np.stack(xs), np.stack(ys), pad
+
+
+def write_history_csv(path, history) -> None:
+    """epoch,train_loss,val_smape with repr floats (learn.py:411-415)."""
+    with open(path, "w") as f:
+        f.write("epoch,train_loss,val_smape\n")
+        for epoch, loss, val in history:
+            f.write(f"{epoch},{loss!r},{val!r}\n")

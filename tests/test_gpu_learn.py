@@ -70,3 +70,100 @@ def test_psp_filter_smape_adam_match_reference(cuda):
         p = L.adam_step(p, {"w": ka["adam_gw"][k], "b": ka["adam_gb"][k]}, st, lr=L.cosine_lr(1e-2, k, 3))
     assert np.allclose(p["w"], ka["adam_w3"], rtol=1e-13, atol=1e-15)
     assert np.allclose(p["b"], ka["adam_b3"], rtol=1e-13, atol=1e-15)
+
+
+# ---------------------------------------------------------------------------
+# teacher-student readout fitting (learn.py:223-377) vs the reference's run
+# ---------------------------------------------------------------------------
+
+def _readout_task():
+    from conftest import golden
+    from paper_2601_21407_b200 import defaults as DF
+    g = golden("readout_fit")
+    neuron = DF.cortical_rs_params(dt=0.1)
+    teacher = L.ReadoutModel(L.DenseLayer(g["teacher_w"], np.array([0.45])), 1.0, 0.0, neuron,
+                             L.PSPKernel(tau_decay=2.0, length=64, dt=neuron.dt))
+    task = L.TeacherStudentTask(teacher, g["train_inputs"], g["train_targets"], g["val_inputs"],
+                                g["val_targets"], 20)
+    return g, task
+
+
+def test_teacher_student_task_matches_reference(cuda):
+    g, _ = _readout_task()
+    task = L.make_teacher_student_task(n_channels=16, n_steps=120, n_train=4, n_val=3, pad_len=20, seed=2)
+    assert np.array_equal(task.train_inputs, g["train_inputs"])
+    assert np.array_equal(task.val_inputs, g["val_inputs"])
+    assert np.array_equal(task.teacher.dense.weights, g["teacher_w"])
+    assert np.allclose(task.train_targets, g["train_targets"], rtol=1e-9, atol=1e-9)
+    assert np.allclose(task.val_targets, g["val_targets"], rtol=1e-9, atol=1e-9)
+    student = L.make_student(task, seed=5)
+    assert np.array_equal(student.dense.weights, g["student_w0"])
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_readout_forward_and_grads_match_reference(cuda, on_device):
+    g, task = _readout_task()
+    t = task.teacher
+    x = torch.as_tensor(g["train_inputs"], device=cuda) if on_device else g["train_inputs"]
+    filt = t.filter_inputs(x)
+    fh = filt.cpu().numpy() if on_device else filt
+    assert np.allclose(fh, g["filtered"], rtol=1e-13, atol=1e-15)
+    pred, v = t.forward(filt)
+    vh = v.cpu().numpy() if on_device else v
+    assert np.allclose(vh, g["teacher_v"], rtol=1e-9, atol=1e-9)
+    sp = torch.as_tensor(g["seed_pred"], device=cuda) if on_device else g["seed_pred"]
+    gr = t.grads(filt, sp, v)
+    host = {k: (x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)) for k, x in gr.items()}
+    assert host["w"].shape == (1, 16) and host["b"].shape == (1,)
+    assert np.allclose(host["w"], g["g_w"], rtol=1e-8, atol=1e-12)
+    assert np.allclose(host["b"], g["g_b"], rtol=1e-8)
+    assert np.isclose(float(host["scale_w"]), float(g["g_sw"]), rtol=1e-9)
+    assert np.isclose(float(host["scale_b"]), float(g["g_sb"]), rtol=1e-12)
+
+
+def test_fit_history_and_parameters_match_reference(cuda):
+    g, task = _readout_task()
+    student = L.ReadoutModel(L.DenseLayer(g["student_w0"].copy(), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                             task.teacher.kernel)
+    hist = L.fit(student, task, L.TrainConfig(epochs=5, lr=2e-2))
+    h = np.array(hist)
+    assert np.array_equal(h[:, 0], g["history"][:, 0])
+    assert np.allclose(h[:, 1:], g["history"][:, 1:], rtol=1e-7)
+    assert isinstance(student.dense.weights, np.ndarray)
+    assert np.allclose(student.dense.weights, g["final_w"], rtol=1e-7, atol=1e-10)
+    assert np.allclose(student.dense.bias, g["final_b"], rtol=1e-7)
+    assert np.isclose(student.scale_w, float(g["final_sw"]), rtol=1e-7)
+    assert np.isclose(student.scale_b, float(g["final_sb"]), rtol=1e-7)
+    # frozen: no parameter change, the loss repeats
+    frozen = L.ReadoutModel(L.DenseLayer(g["student_w0"].copy(), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                            task.teacher.kernel)
+    hf = L.fit(frozen, task, L.TrainConfig(epochs=2, lr=2e-2, freeze=True))
+    assert hf[0][1] == hf[1][1] and np.array_equal(frozen.dense.weights, g["student_w0"])
+    assert np.isclose(hf[0][1], g["history"][0, 1], rtol=1e-9)
+
+
+def test_readout_grad_kernel_layouts_and_empty(cuda):
+    """hhb_readout_grad over both x layouts, odd channel counts, fp32, vs einsum."""
+    rng = np.random.default_rng(9)
+    for B, T, C in ((3, 7, 1), (5, 33, 300), (2, 1000, 64)):
+        x = rng.normal(size=(B, T, C))
+        dd = rng.normal(size=(T, B))
+        ref_w = np.einsum("tb,btc->c", dd, x)
+        for layout in ("btc", "tbc"):
+            xd = torch.as_tensor(x, device=cuda)
+            if layout == "tbc":
+                xd = xd.permute(1, 0, 2).contiguous().permute(1, 0, 2)
+            d_w = torch.empty((1, C), dtype=torch.float64, device=cuda)
+            d_b = torch.empty(1, dtype=torch.float64, device=cuda)
+            ws = L._readout_ws(C, cuda)
+            from paper_2601_21407_b200 import _device as D, _native as nat
+            ddd = torch.as_tensor(dd, device=cuda)
+            nat.check(nat.load().hhb_readout_grad(nat.F64, B, T, C, xd.data_ptr(), xd.stride(0), xd.stride(1),
+                                                  ddd.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), ws.data_ptr(),
+                                                  ws.numel() * 8, D.stream()), "grad")
+            assert np.allclose(d_w.cpu().numpy()[0], ref_w, rtol=1e-11, atol=1e-11)
+            assert np.isclose(d_b.item(), dd.sum(), rtol=1e-12)
+            w = torch.as_tensor(rng.normal(size=C), device=cuda)
+            b = torch.tensor([0.3], dtype=torch.float64, device=cuda)
+            drv = L._readout_drive(xd, w, b)
+            assert np.allclose(drv.cpu().numpy(), (x @ w.cpu().numpy()).T + 0.3, rtol=1e-12, atol=1e-12)

@@ -213,3 +213,51 @@ def test_morphology_graph_validation_matches_reference():
     gd = M.graph_from_dict({"compartments": [{"id": "s"}, {"id": "d", "params": p.to_dict()}],
                             "edges": [{"a": "s", "b": "d", "g_axial": 1.0}], "soma": "s"})
     assert gd.order == ["s", "d"] and gd.index("d") == 1
+
+
+def test_oracle_readout_model_matches_reference_goldens():
+    """ReadoutModel.forward / grads (learn.py:237-274) restated with the oracle's
+    dense / simulate / bptt on the reference's teacher, vs the reference."""
+    g = golden("readout_fit")
+    p = DF.cortical_rs_params(dt=0.1)
+    x = g["filtered"]                                      # (B, T, C)
+    drive = O.dense(x, g["teacher_w"], np.array([0.45]))[..., 0]
+    i_s = np.ascontiguousarray(drive.T)                    # (T, B)
+    v, _ = O.simulate(p, i_s)
+    assert np.allclose(v.T, g["teacher_v"], rtol=1e-12, atol=1e-12)
+    seed_v = np.ascontiguousarray(g["seed_pred"].T)        # scale_w = 1
+    v0, g0 = O.rest_state(p, i_s.shape[1])
+    res = O.bptt(p, v0, g0, i_s, seed_v)
+    d_drive = res["d_i"].T
+    assert np.allclose(np.einsum("bt,btc->c", d_drive, x), g["g_w"][0], rtol=1e-10)
+    assert np.isclose(d_drive.sum(), g["g_b"][0], rtol=1e-10)
+    assert np.isclose((g["seed_pred"] * g["teacher_v"]).sum(), g["g_sw"], rtol=1e-12)
+
+
+def test_segmentation_and_split_match_reference():
+    """segment_traces / split_dataset (learn.py:158-196): host logic, exact."""
+    from paper_2601_21407_b200 import learn as L
+    g = golden("readout_fit")
+    seg = L.segment_traces(np.arange(50.0), 2.0 * np.arange(50.0), L.SegmentationScheme(7, 9))
+    assert np.array_equal(np.array([a for a, _ in seg]), g["seg_in"])
+    assert np.array_equal(np.array([b for _, b in seg]), g["seg_out"])
+    tr, te = L.split_dataset(11, np.random.default_rng(4))
+    assert np.array_equal(tr, g["split_train"]) and np.array_equal(te, g["split_test"])
+    assert L.segment_traces(np.arange(5.0), np.arange(5.0), L.SegmentationScheme(7, 9)) == []
+    with pytest.raises(Exception):
+        L.SegmentationScheme(1, 0)
+    with pytest.raises(Exception):
+        L.segment_traces(np.arange(5.0), np.arange(4.0), L.SegmentationScheme(1, 1))
+
+
+def test_dataset_and_history_files_roundtrip(tmp_path):
+    """write/read_ndjson_dataset and write_history_csv (learn.py:384-415)."""
+    from paper_2601_21407_b200 import learn as L
+    rng = np.random.default_rng(0)
+    x = (rng.random((3, 6, 4)) < 0.3).astype(np.float64)
+    y = rng.normal(size=(3, 6))
+    L.write_ndjson_dataset(tmp_path / "d.ndjson", x, y, 2)
+    x2, y2, pad = L.read_ndjson_dataset(tmp_path / "d.ndjson")
+    assert np.array_equal(x2, x) and np.array_equal(y2[..., 0], y) and pad == 2
+    L.write_history_csv(tmp_path / "h.csv", [(0, 1.5, 0.25), (1, 0.1, 1 / 3)])
+    assert (tmp_path / "h.csv").read_text() == "epoch,train_loss,val_smape\n0,1.5,0.25\n1,0.1,0.3333333333333333\n"
