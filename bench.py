@@ -371,6 +371,28 @@ def morph_leg(torch, dev):
                       "x 400 steps, fp32, V trace + spikes recorded (one unit = one compartment-step)"}
 
 
+def readout_fit_leg(torch, dev, epochs=20):
+    """the reference's teacher-student fitting loop (learn.fit,
+    learn.py:351-377) on its default task -- 64 channels, 500 steps, 16
+    training + 8 validation samples, RS neuron in float64 -- through
+    learn.fit: PSP filter, readout GEMV, HH forward, MSE, BPTT, weight
+    gradient, Adam, validation forward, per epoch.  The reference takes
+    0.40 s / epoch on one core of the build container."""
+    import time
+    from paper_2601_21407_b200 import learn as L
+    task = L.make_teacher_student_task()
+    L.fit(L.make_student(task), task, L.TrainConfig(epochs=3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hist = L.fit(L.make_student(task), task, L.TrainConfig(epochs=epochs))
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / epochs
+    return {"value": 1e3 / ms, "unit": "epochs/s", "ms_per_epoch": ms, "epochs": epochs,
+            "loss_first_last": [hist[0][1], hist[-1][1]],
+            "config": "make_teacher_student_task() defaults (64 ch, 500 steps, 16 train / 8 val), float64; "
+                      "host wall clock (the loop reads the loss back every epoch, as the reference)"}
+
+
 def c5_replicas_leg(torch, dev, topo=None, replicas=(8, 32, 64), steps=640):
     """Config 5 in the paper's "replicas x speed" view: R
     independent copies of the scale-0.5 network stepped together on one GPU
@@ -601,6 +623,7 @@ def main():
         leg("c4_train_step", lambda: c4_leg(torch, dev))
         leg("c5_network", lambda: c5_leg(torch, dev))
         leg("morphology", lambda: morph_leg(torch, dev))
+        leg("readout_fit", lambda: readout_fit_leg(torch, dev))
         leg("c5_replicas", lambda: c5_replicas_leg(torch, dev))
         if world > 1 and "ms_per_step" in extras["fwd_bwd"]:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int kGradBlocks = 296;   // 2 per SM; partial rows [kGradBlocks][C+1]
 constexpr int kGradThreads = 256;
+constexpr int64_t kMinRowsPerBlock = 128;
 
 template <typename T>
 __global__ void k_readout_drive(int64_t B, int64_t Tn, int64_t C, const T* __restrict__ x, int64_t sb, int64_t st,
@@ -74,14 +75,22 @@ __global__ void k_readout_grad_part(int64_t B, int64_t Tn, int64_t C, const T* _
   }
 }
 
+// Stage 2: one warp per column, lanes stride the block partials, fixed-order
+// butterfly: deterministic for a given (rows, C).
 template <typename T>
 __global__ void k_readout_grad_sum(int64_t C, int nblk, const T* __restrict__ part, T* __restrict__ d_w,
                                    T* __restrict__ d_b) {
-  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c <= C; c += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t c = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); c <= C; c += warps) {
     T s = T(0);
-    for (int g = 0; g < nblk; ++g) s += part[int64_t(g) * (C + 1) + c];
-    if (c < C) d_w[c] = s;
-    else d_b[0] = s;
+    for (int g = lane; g < nblk; g += 32) s += part[int64_t(g) * (C + 1) + c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (c < C) d_w[c] = s;
+      else d_b[0] = s;
+    }
   }
 }
 
@@ -90,14 +99,14 @@ int readout_grad(int64_t B, int64_t Tn, int64_t C, const void* x, int64_t sb, in
                  void* d_b, void* ws, cudaStream_t s) {
   const int64_t rows = B * Tn;
   int64_t per = (rows + kGradBlocks - 1) / kGradBlocks;
-  if (per < 1) per = 1;
+  if (per < kMinRowsPerBlock) per = kMinRowsPerBlock;
   const int nblk = int((rows + per - 1) / per);
   int bx = 32;
   while (bx < C + 1 && bx < kGradThreads) bx <<= 1;
   const dim3 blk(bx, kGradThreads / bx);
   k_readout_grad_part<T><<<nblk, blk, sizeof(T) * kGradThreads, s>>>(B, Tn, C, (const T*)x, sb, st, (const T*)dd,
                                                                         per, (T*)ws);
-  k_readout_grad_sum<T><<<unsigned((C + 1 + 127) / 128), 128, 0, s>>>(C, nblk, (const T*)ws, (T*)d_w, (T*)d_b);
+  k_readout_grad_sum<T><<<unsigned((C + 1 + 7) / 8), 256, 0, s>>>(C, nblk, (const T*)ws, (T*)d_w, (T*)d_b);
   return cuda_check("k_readout_grad launch");
 }
 

@@ -133,6 +133,14 @@ def psp_filter(spikes, kernel: PSPKernel):
     return y if on_dev else y.cpu().numpy()
 
 
+def _smape_dev(p: torch.Tensor, t: torch.Tensor) -> torch.Tensor:
+    p, t = p.double().reshape(-1), t.double().reshape(-1)
+    num = (p - t).abs()
+    den = p.abs() + t.abs()
+    terms = torch.where(den > 0, num / torch.where(den > 0, den, torch.ones_like(den)), torch.zeros_like(num))
+    return 100.0 * terms.mean()
+
+
 def smape(pred, truth) -> float:
     """Symmetric mean absolute percentage error in [0, 100] (learn.py:62-77)."""
     p = _dev(pred).double().reshape(-1)
@@ -141,10 +149,7 @@ def smape(pred, truth) -> float:
         raise UsageError("smape requires non-empty input")
     if p.shape != t.shape:
         raise UsageError("smape requires equal-length inputs")
-    num = (p - t).abs()
-    den = p.abs() + t.abs()
-    terms = torch.where(den > 0, num / torch.where(den > 0, den, torch.ones_like(den)), torch.zeros_like(num))
-    return float(100.0 * terms.mean().item())
+    return float(_smape_dev(p, t).item())
 
 
 @dataclass
@@ -442,40 +447,107 @@ def evaluate_smape(model: ReadoutModel, inputs, targets, pad_len: int) -> float:
 
 
 def fit(model: ReadoutModel, task: TeacherStudentTask, config: TrainConfig):
-    """Full-batch fitting loop (learn.py:351-377), device-resident: inputs are
-    filtered once (train and validation -- the reference re-filters the
-    validation set each epoch; the filter is deterministic, so the values are
-    the same), parameters and Adam moments stay on the device, and each epoch
-    reads back only the loss and the validation sMAPE.  Returns the history
-    rows (epoch, train_loss, val_smape); the model ends with numpy parameters
-    as the reference's."""
+    """Full-batch fitting loop (learn.py:351-377), device-resident.  Returns
+    the history rows (epoch, train_loss, val_smape); the model ends with numpy
+    parameters as the reference's.
+
+    Same arithmetic as the reference's loop, fewer passes: the training and
+    validation samples are filtered once and simulated as ONE population per
+    epoch (the validation forward of epoch e uses the parameters loaded at the
+    start of epoch e, exactly as the training forward does, and the neurons are
+    independent), and that forward also writes the per-step checkpoints the
+    BPTT kernel reads instead of re-simulating (backward_through_time with
+    plan=None recomputes the same states).  Parameters and Adam moments stay
+    on the device; each epoch reads back one small vector (loss, validation
+    sMAPE, overflow flags), and the errors are raised in the reference's
+    order: NumericalOverflowError (training forward), TrainingDivergedError,
+    GradientOverflowError, NumericalOverflowError (validation forward)."""
+    from .adjoint import _backward, default_surrogate
+    from .dynamics import _forward, init_state
+    from .errors import GradientOverflowError, NumericalOverflowError
     dev = D.require_cuda()
-    filtered = model.filter_inputs(torch.as_tensor(np.asarray(task.train_inputs, dtype=np.float64), device=dev))
-    val_filtered = model.filter_inputs(torch.as_tensor(np.asarray(task.val_inputs, dtype=np.float64), device=dev))
+    xt = np.asarray(task.train_inputs, dtype=np.float64)
+    xv = np.asarray(task.val_inputs, dtype=np.float64)
+    B, Bv = xt.shape[0], xv.shape[0]
+    n_all = B + Bv
+    x_all = _x3(model.filter_inputs(torch.as_tensor(np.concatenate([xt, xv], 0), device=dev)))
+    T = x_all.shape[1]
     targets = _dev(task.train_targets).double()
     val_targets = _dev(task.val_targets).double()
     pad = task.pad_len
     mask = torch.zeros_like(targets)
     mask[:, pad:] = 1.0
     masked_targets = targets * mask
+    neuron = model.neuron
+    ng = neuron.n_gates
+    s0 = init_state(neuron, (n_all,), device=dev)
+    v0, g0 = s0.v.reshape(n_all), s0.gates.reshape(ng, n_all)
+    v_out = torch.empty((T, n_all), dtype=v0.dtype, device=dev)
+    ckpt = torch.empty((T, 1 + ng, n_all), dtype=v0.dtype, device=dev)
+    adj_v = torch.empty(B, dtype=v0.dtype, device=dev)
+    adj_g = torch.empty((ng, B), dtype=v0.dtype, device=dev)
+    d_w = torch.empty((1, x_all.shape[2]), dtype=torch.float64, device=dev)
+    d_b = torch.empty(1, dtype=torch.float64, device=dev)
+    ws = _readout_ws(x_all.shape[2], dev)
+    sur = default_surrogate(neuron)
     opt = AdamState(lr=config.lr)
-    p0 = model.params()
-    params = {k: _dev(v).double() for k, v in p0.items()}
+    params = {k: _dev(v).double() for k, v in model.params().items()}
     history = []
+
+    def host_params(p):
+        return {k: (t.cpu().numpy() if t.dim() else np.float64(t.item())) for k, t in p.items()}
+
+    def first_bad_step(v_part):                                            # (T, n) -> first bad t
+        ok = torch.isfinite(v_part).all(dim=1)
+        return int(torch.nonzero(~ok)[0, 0].item()) if not bool(ok.all().item()) else None
+
     for epoch in range(config.epochs):
         model.load_params(params)
-        pred, v = model.forward(filtered)
-        loss, seed = mse_loss(pred * mask, masked_targets)
-        loss_f = float(loss.item())
-        if not math.isfinite(loss_f):
-            raise TrainingDivergedError("training loss became non-finite", epoch)
+        w, b = model._params_dev(dev)
+        cur = _readout_drive(x_all, w, b).to(v0.dtype)                      # (T, B + Bv)
+        _, _, fbad = _forward(neuron, v0, g0, cur, n_all, 1, T, v_out=v_out, ckpt=ckpt, ckpt_every=1)
+        v_all = v_out.double().t()                                          # (B + Bv, T)
+        pred_all = v_all * params["scale_w"] + params["scale_b"]
+        loss, seed = mse_loss(pred_all[:B] * mask, masked_targets)
+        gbad = None
         if not config.freeze:
-            grads = model.grads(filtered, seed * mask, v)
+            seed_m = seed * mask
+            v = v_all[:B]
+            grads = {"scale_w": (seed_m * v).sum(), "scale_b": seed_m.sum()}
+            seed_v = (seed_m * params["scale_w"]).t().contiguous().to(v0.dtype)   # (T, B)
+            adj_v.zero_()
+            adj_g.zero_()
+            d_i, _, gbad = _backward(neuron, sur, cur, n_all, 1, T, B, ckpt, 1, seed_v, None, adj_v, adj_g,
+                                     ck_ld=n_all)
+            d_i = d_i.double()
+            nat.check(nat.load().hhb_readout_grad(nat.F64, B, T, x_all.shape[2], x_all.data_ptr(), x_all.stride(0),
+                                                  x_all.stride(1), d_i.data_ptr(), d_w.data_ptr(), d_b.data_ptr(),
+                                                  ws.data_ptr(), ws.numel() * 8, D.stream()), "hhb_readout_grad")
+            grads["w"], grads["b"] = d_w, d_b
             lr = cosine_lr(config.lr, epoch, config.epochs) if config.cosine else config.lr
-            params = adam_step(params, grads, opt, lr=lr)
-        vpred, _ = model.forward(val_filtered)
-        history.append((epoch, loss_f, smape(vpred[:, pad:], val_targets[:, pad:])))
-    model.load_params({k: (t.cpu().numpy() if t.dim() else np.float64(t.item())) for k, t in params.items()})
+            new_params = adam_step(params, grads, opt, lr=lr)
+        val = _smape_dev(pred_all[B:, pad:], val_targets[:, pad:])
+        flags = torch.cat([t.double().reshape(1) for t in
+                           (loss, val, fbad != D.INT64_MAX, gbad if gbad is not None else torch.full_like(fbad, -1))])
+        loss_f, val_f, fb, gb = flags.cpu().tolist()
+        if fb:
+            step = first_bad_step(v_out[:, :B])
+            if step is not None:
+                model.load_params(host_params(params))
+                raise NumericalOverflowError("membrane potential became non-finite", step)
+        if not math.isfinite(loss_f):
+            model.load_params(host_params(params))
+            raise TrainingDivergedError("training loss became non-finite", epoch)
+        if gb >= 0:
+            model.load_params(host_params(params))
+            raise GradientOverflowError("adjoint state became non-finite", int(gb))
+        if fb:
+            model.load_params(host_params(params))
+            raise NumericalOverflowError("membrane potential became non-finite", first_bad_step(v_out[:, B:]))
+        if not config.freeze:
+            params = new_params
+        history.append((epoch, loss_f, val_f))
+    model.load_params(host_params(params))
     return history
 
 

@@ -167,3 +167,27 @@ def test_readout_grad_kernel_layouts_and_empty(cuda):
             b = torch.tensor([0.3], dtype=torch.float64, device=cuda)
             drv = L._readout_drive(xd, w, b)
             assert np.allclose(drv.cpu().numpy(), (x @ w.cpu().numpy()).T + 0.3, rtol=1e-12, atol=1e-12)
+
+
+def test_fit_raises_in_reference_order(cuda):
+    from paper_2601_21407_b200.errors import NumericalOverflowError, TrainingDivergedError
+    g, task = _readout_task()
+    bad_t = g["train_targets"].copy()
+    bad_t[1, 30] = np.nan
+    t2 = L.TeacherStudentTask(task.teacher, task.train_inputs, bad_t, task.val_inputs, task.val_targets, 20)
+    st = L.ReadoutModel(L.DenseLayer(g["student_w0"].copy(), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                        task.teacher.kernel)
+    with pytest.raises(TrainingDivergedError) as ei:
+        L.fit(st, t2, L.TrainConfig(epochs=3))
+    assert ei.value.epoch == 0 and isinstance(st.dense.weights, np.ndarray)
+    # a NaN before the supervised window is masked out, as in the reference
+    bad_t = g["train_targets"].copy()
+    bad_t[1, 3] = 1.0
+    t3 = L.TeacherStudentTask(task.teacher, task.train_inputs, bad_t, task.val_inputs, task.val_targets, 20)
+    h = L.fit(L.ReadoutModel(L.DenseLayer(g["student_w0"].copy(), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                             task.teacher.kernel), t3, L.TrainConfig(epochs=1))
+    assert np.isclose(h[0][1], g["history"][0, 1], rtol=1e-9)
+    huge = L.ReadoutModel(L.DenseLayer(np.full((1, 16), 1e300), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                          task.teacher.kernel)
+    with pytest.raises(NumericalOverflowError):
+        L.fit(huge, task, L.TrainConfig(epochs=1))
