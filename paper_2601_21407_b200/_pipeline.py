@@ -35,14 +35,21 @@ def _pool():
 
 def _par_copy(dst: np.ndarray, src: np.ndarray):
     """dst[...] = src (with dtype cast), split over worker threads; NumPy
-    releases the GIL inside the copy loop."""
-    rows = dst.shape[0]
-    k = min(rows, _pool()._max_workers) if rows > 1 else 1
-    if k <= 1 or dst.size < (1 << 20):
+    releases the GIL inside the copy loop.  Contiguous arrays are split by
+    elements (a one-row chunk still uses every thread), others by rows."""
+    workers = _pool()._max_workers
+    if dst.size < (1 << 20) or workers <= 1:
         np.copyto(dst, src, casting="unsafe")
         return
-    step = (rows + k - 1) // k
-    futs = [_pool().submit(np.copyto, dst[a:a + step], src[a:a + step], "unsafe") for a in range(0, rows, step)]
+    if dst.flags.c_contiguous and src.flags.c_contiguous and dst.shape == src.shape:
+        d, s_ = dst.reshape(-1), src.reshape(-1)
+        step = (d.size + workers - 1) // workers
+        step = (step + 1023) & ~1023
+        futs = [_pool().submit(np.copyto, d[a:a + step], s_[a:a + step], "unsafe") for a in range(0, d.size, step)]
+    else:
+        rows = dst.shape[0]
+        step = (rows + workers - 1) // workers
+        futs = [_pool().submit(np.copyto, dst[a:a + step], src[a:a + step], "unsafe") for a in range(0, rows, step)]
     for f in futs:
         f.result()
 
@@ -54,7 +61,7 @@ def pinned_empty(shape, dtype) -> np.ndarray:
     return t.numpy()
 
 
-CHUNK_BYTES = 256 << 20   # input bytes per pipelined chunk
+CHUNK_BYTES = int(os.environ.get("HHB_PIPE_CHUNK_MB", "64")) << 20   # input bytes per pipelined chunk
 
 
 def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forward, unpack,

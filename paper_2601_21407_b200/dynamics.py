@@ -312,14 +312,34 @@ def init_state(params, shape: tuple = (), v0: float | None = None, device=None) 
 
 
 def steady_state_gates(params: HHParams, v0: float) -> list:
-    """Per-gate open fraction alpha/(alpha+beta) at v0 (0.5 for zero rate)."""
+    """Per-gate open fraction alpha/(alpha+beta) at v0 (0.5 for zero rate);
+    memoised per (channel table, v0): every init_state of a population
+    otherwise pays one rate launch and read-back per gate."""
+    try:
+        key = (params, float(v0))
+        hit = _STEADY.get(key)
+    except TypeError:
+        key, hit = None, None
+    if hit is None:
+        hit = _steady_state_gates(params, v0)
+        if key is not None:
+            if len(_STEADY) > 256:
+                _STEADY.clear()
+            _STEADY[key] = hit
+    return list(hit)
+
+
+_STEADY: dict = {}
+
+
+def _steady_state_gates(params: HHParams, v0: float) -> tuple:
     out = []
     for _, gate in params.gate_layout:
         a, b = gate_rates(gate, np.float64(v0), params.rate_scale)
         a, b = float(a), float(b)
         s = a + b
         out.append(a / s if s > 0 else 0.5)
-    return out
+    return tuple(out)
 
 
 # ---------------------------------------------------------------------------
