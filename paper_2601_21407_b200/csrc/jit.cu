@@ -1021,6 +1021,11 @@ struct Stimulus {
     }
   }
 };
+// The module is specialised on which output streams the launch has (FF_VO V
+// trace, FF_SO spike bitmap, FF_SVO spike values, FF_CK checkpoints) and on
+// FF_AL: every stream neuron-contiguous and 16-byte aligned with n % 4 == 0,
+// so a live thread always moves whole float4s (no per-step null checks, no
+// per-neuron tails in the loop).
 template <int VEC, bool POIS>
 __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& tab, const Keys& ks) {
   FwdArgs a = a_in;
@@ -1029,6 +1034,8 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = tid * VEC;
   const bool full = n0 + VEC <= a.n;
+  constexpr bool AL = FF_AL && VEC == 4;
+  const bool live = n0 < a.n;                   // == full when AL
   Stimulus<VEC, POIS> stim;
   __shared__ PoissonSmem ps;
   if (POIS) {
@@ -1049,20 +1056,20 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   i64 bad = LLMAX;
   int ck_count = 0;
   // running pointers (one 64-bit add per step instead of t * ld)
-  float* ckp = a.ckpt != nullptr ? a.ckpt + n0 : nullptr;
+  float* ckp = FF_CK ? a.ckpt + n0 : nullptr;
   const i64 sstride = (1 + NG) * a.ck_ld;
   const float* ip = POIS ? nullptr : a.i_ext + n0 * a.i_sn;
-  const bool vec_in = VEC == 4 && full && a.i_sn == 1;
-  float* vo = a.v_out != nullptr ? a.v_out + n0 : nullptr;
-  u32* so = a.spk != nullptr ? a.spk + n0 / 32 : nullptr;
-  float* svo = a.spk_val != nullptr ? a.spk_val + n0 : nullptr;
-  const bool spk_writer = lane % (32 / VEC) == 0 && n0 < a.n;
+  const bool vec_in = VEC == 4 && (AL || (full && a.i_sn == 1));
+  float* vo = FF_VO ? a.v_out + n0 : nullptr;
+  u32* so = FF_SO ? a.spk + n0 / 32 : nullptr;
+  float* svo = FF_SVO ? a.spk_val + n0 : nullptr;
+  const bool spk_writer = lane % (32 / VEC) == 0 && live;
   // loaded currents are prefetched one step ahead (HBM latency); the drawn
   // stimulus is made at the top of its own step (no registers held across it)
   float cur[VEC];
   auto load_in = [&](float (&c)[VEC]) {
     if (vec_in) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(ip));
+      const float4 q = live ? __ldg(reinterpret_cast<const float4*>(ip)) : make_float4(0.f, 0.f, 0.f, 0.f);
       c[0] = q.x; c[VEC > 1 ? 1 : 0] = q.y; c[VEC > 2 ? 2 : 0] = q.z; c[VEC > 3 ? 3 : 0] = q.w;
     } else {
 #pragma unroll
@@ -1070,27 +1077,27 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
     }
     ip += a.i_st;
   };
+  auto store4 = [&](float* q, const float (&x)[VEC]) {
+    if (AL || (VEC == 4 && full)) {
+      if (live) *reinterpret_cast<float4*>(q) = make_float4(x[0], x[VEC > 1 ? 1 : 0], x[VEC > 2 ? 2 : 0], x[VEC > 3 ? 3 : 0]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) q[j] = x[j];
+    }
+  };
   if (!POIS && a.steps > 0) load_in(cur);
   for (i64 t = 0; t < a.steps; ++t) {
     float nxt[VEC];
     if (POIS) stim.at(a, ks, ps, t, n0, full, cur);
     else if (t + 1 < a.steps) load_in(nxt);
-    if (ckp != nullptr && ck_count == 0) {      // state BEFORE step t
-      if (VEC == 4 && full) {
-        *reinterpret_cast<float4*>(ckp) = make_float4(v[0], v[VEC > 1 ? 1 : 0], v[VEC > 2 ? 2 : 0], v[VEC > 3 ? 3 : 0]);
+    if (FF_CK && ck_count == 0) {      // state BEFORE step t
+      store4(ckp, v);
 #pragma unroll
-        for (int g = 0; g < NG; ++g)
-          *reinterpret_cast<float4*>(ckp + (1 + g) * a.ck_ld) =
-              make_float4(p[0][g], p[VEC > 1 ? 1 : 0][g], p[VEC > 2 ? 2 : 0][g], p[VEC > 3 ? 3 : 0][g]);
-      } else {
+      for (int g = 0; g < NG; ++g) {
+        float q[VEC];
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          if ((valid >> j) & 1u) {
-            ckp[j] = v[j];
-#pragma unroll
-            for (int g = 0; g < NG; ++g) ckp[(1 + g) * a.ck_ld + j] = p[j][g];
-          }
-        }
+        for (int j = 0; j < VEC; ++j) q[j] = p[j][g];
+        store4(ckp + (1 + g) * a.ck_ld, q);
       }
       ckp += sstride;
       ck_count = int(a.ck_every);
@@ -1112,26 +1119,18 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       for (int j = 0; j < VEC; ++j)
         if (!finitef_(v[j]) && ((valid >> j) & 1u)) bad = a.step_base + t;
     }
-    if (vo != nullptr) {
-      if (VEC == 4 && full) *reinterpret_cast<float4*>(vo) = make_float4(v[0], v[VEC > 1 ? 1 : 0], v[VEC > 2 ? 2 : 0], v[VEC > 3 ? 3 : 0]);
-      else {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) vo[j] = v[j];
-      }
+    if (FF_VO) {
+      store4(vo, v);
       vo += a.v_ld;
     }
-    if (svo != nullptr) {
+    if (FF_SVO) {
       float f[VEC];
 #pragma unroll
       for (int j = 0; j < VEC; ++j) f[j] = ((nib >> j) & 1u) ? 1.0f : 0.0f;
-      if (VEC == 4 && full) *reinterpret_cast<float4*>(svo) = make_float4(f[0], f[VEC > 1 ? 1 : 0], f[VEC > 2 ? 2 : 0], f[VEC > 3 ? 3 : 0]);
-      else {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) svo[j] = f[j];
-      }
+      store4(svo, f);
       svo += a.spkv_ld;
     }
-    if (so != nullptr) {
+    if (FF_SO) {
       u32 w;
       if (VEC == 1) {
         w = __ballot_sync(0xffffffffu, nib != 0);
@@ -1414,10 +1413,16 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2
 }
 )";
 
+// kind >= 0: the backward module specialised on BF_* (kind = flags);
+// kInspect: both (forward with the generic stream flags), for hhb_jit_source;
+// otherwise the forward module specialised on FF_* (kind = -1 - flags).
 // bwd_flags < 0: the forward module; >= 0: the backward module specialised
 // on BF_* (which optional streams the launch has); -2: both, for inspection
 enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32 };
-static std::string generate(const hhb_params_t* P, int bwd_flags = -2) {
+enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16 };
+constexpr int kInspect = -1000;
+static int fwd_kind(int ff) { return -1 - ff; }
+static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   const Layout L = layout_of(P);
   std::string src = kPrelude;
   src += fmt("#define NG %d\n#define NGX %d\n#define SLOTS %d\n#define BWD_THREADS %d\n", L.ng,
@@ -1572,8 +1577,14 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
 }
 )";
   }
-  if (bwd_flags == -1 || bwd_flags == -2) src += kForwardBody;
-  if (bwd_flags != -1) {
+  if (bwd_flags < 0) {
+    const int ff = bwd_flags == kInspect ? (FF_VO | FF_SO | FF_CK) : -1 - bwd_flags;
+    src += fmt("#define FF_VO %d\n#define FF_SO %d\n#define FF_SVO %d\n#define FF_CK %d\n#define FF_AL %d\n",
+               (ff & FF_VO) ? 1 : 0, (ff & FF_SO) ? 1 : 0, (ff & FF_SVO) ? 1 : 0, (ff & FF_CK) ? 1 : 0,
+               (ff & FF_AL) ? 1 : 0);
+    src += kForwardBody;
+  }
+  if (bwd_flags >= 0 || bwd_flags == kInspect) {
     const int f = bwd_flags < 0 ? (BF_SV | BF_DI) : bwd_flags;
     src += fmt("#define BF_SV %d\n#define BF_SS %d\n#define BF_DI %d\n#define BF_SPLIT %d\n#define BF_SUM %d\n"
                "#define BF_K1 %d\n",
@@ -1684,7 +1695,15 @@ static Module* get_module(const hhb_params_t* P, int bwd_flags) {
 // Returns true when the JIT kernel was launched (rc holds its status).
 bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTab<float>* ptab, bool vec4,
                  cudaStream_t st, int& rc) {
-  jit::Module* m = jit::get_module(P, -1);
+  using namespace jit;
+  const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const bool aligned = vec4 && a.n % 4 == 0 && (ptab || (a.i_sn == 1 && a.i_st % 4 == 0 && al16(a.i_ext))) &&
+                       (!a.v_out || (a.v_ld % 4 == 0 && al16(a.v_out))) &&
+                       (!a.spk_val || (a.spkv_ld % 4 == 0 && al16(a.spk_val))) &&
+                       (!a.ckpt || (a.ck_ld % 4 == 0 && al16(a.ckpt)));
+  const int ff = (a.v_out ? FF_VO : 0) | (a.spk ? FF_SO : 0) | (a.spk_val ? FF_SVO : 0) | (a.ckpt ? FF_CK : 0) |
+                 (aligned ? FF_AL : 0);
+  jit::Module* m = jit::get_module(P, fwd_kind(ff));
   if (!m) return false;
   const int VEC = vec4 ? 4 : 1;
   const int64_t threads = (a.n + VEC - 1) / VEC;
