@@ -452,14 +452,16 @@ static Plan plan_of(const hhb_params_t* P) {
     g.one_rcp = lo1 <= vr - 60.0 && hi1 >= vr + 140.0;
   }
   // One reciprocal per gate costs 4 issue slots and 1 MUFU op, two cost 2 and
-  // 2.  The merged forward is issue-bound with MUFU close behind, so half of
-  // the gates take two reciprocals (config 2: 1.466e11 -> 1.501e11
-  // neuron-steps/s); the backward is far more issue-bound than MUFU-bound, so
-  // all its gates take two (the window proven above holds for both: two
-  // reciprocals only need N and D in range).  HHB_JIT_TWO_RCP=k overrides the
-  // forward count.
+  // 2.  With half of the gates on two reciprocals the first stream-specialised
+  // forward sat at 0.80 of the MUFU peak, so every gate whose own window
+  // allows it takes one (config 2: 1.60e11 -> 1.68e11 neuron-steps/s; before
+  // the specialisation, issue-bound, half-and-half had won: 1.466e11 ->
+  // 1.501e11).  The backward is far more issue-bound than MUFU-bound, so all
+  // its gates take two (the window proven above holds for both: two
+  // reciprocals only need N and D in range).  HHB_JIT_TWO_RCP=k moves the
+  // last k forward gates to two.
   {
-    int k = int(M.gates.size()) / 2;
+    int k = 0;
     if (const char* tr = getenv("HHB_JIT_TWO_RCP")) k = atoi(tr);
     for (int gi = int(M.gates.size()) - 1; gi >= 0 && k > 0; --gi, --k) M.gates[gi].one_rcp = false;
   }
@@ -901,11 +903,19 @@ __device__ __forceinline__ uint4 philox(const Keys& ks, i64 gj, i64 gq) {
   return c;
 }
 // guide-table inverse CDF in shared memory (hh_kernels.cuh PoissonSmem)
+// guide-table Poisson draw (see hh_kernels.cuh PoissonSmem): each bucket holds
+// amp*k0 and the three next CDF values as integer thresholds on the raw word,
+// T(c) = ((floor(c 2^23) + 1) << 9) - 1, so u > c  <=>  w > T(c) exactly for
+// the uniform u = (w >> 9) 2^-23: no int->float conversion per draw and
+// bit-identical to the float compare of the generic kernels.
 struct PoissonSmem {
-  float4 g4[256];
+  uint4 g4[256];
   int k0[256];
   float cdf[48];
   float amp;
+  __device__ static u32 thr(float c) {
+    return c >= 1.0f ? 0xFFFFFFFFu : ((u32(floorf(c * 8388608.0f)) + 1u) << 9) - 1u;
+  }
   __device__ void fill(const PoissonTab& tab) {
     for (int k = threadIdx.x; k < 48; k += blockDim.x) cdf[k] = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
     if (threadIdx.x == 0) amp = tab.amp;
@@ -917,17 +927,16 @@ struct PoissonSmem {
       const float c0 = k < tab.size - 1 ? tab.cdf[k] : 2.0f;
       const float c1 = k + 1 < tab.size - 1 ? tab.cdf[k + 1] : 2.0f;
       const float c2 = k + 2 < tab.size - 1 ? tab.cdf[k + 2] : 2.0f;
-      g4[b] = make_float4(tab.amp * float(k), c0, c1, c2);
+      g4[b] = make_uint4(__float_as_uint(tab.amp * float(k)), thr(c0), thr(c1), thr(c2));
     }
   }
   __device__ __forceinline__ static float uniform(u32 w) { return __uint_as_float(0x3F800000u | (w >> 9)) - 1.0f; }
   __device__ __forceinline__ float draw(u32 w, bool& tail) const {
-    const float u = uniform(w);
-    const float4 e = g4[w >> 24];
-    float val = e.x;
-    val = (u > e.y) ? val + amp : val;
-    val = (u > e.z) ? val + amp : val;
-    tail = u > e.w;
+    const uint4 e = g4[w >> 24];
+    float val = __uint_as_float(e.x);
+    val = (w > e.y) ? val + amp : val;
+    val = (w > e.z) ? val + amp : val;
+    tail = w > e.w;
     return val;
   }
   __device__ float tail_draw(u32 w) const {

@@ -186,14 +186,14 @@ def _mufu_ops(src: str, fn: str) -> int:
     return body.count("ex2f_(") + body.count("rcpf_(")
 
 
-@pytest.mark.parametrize("mk,tau,merged", [(lambda: DF.na_kdr_cal_kca_params(), 31, 23),
-                                           (lambda: DF.cortical_rs_params(), 16, 11),
-                                           (lambda: DF.squid_axon_params(), 15, 11)])
+@pytest.mark.parametrize("mk,tau,merged", [(lambda: DF.na_kdr_cal_kca_params(), 31, 20),
+                                           (lambda: DF.cortical_rs_params(), 16, 10),
+                                           (lambda: DF.squid_axon_params(), 15, 10)])
 def test_merged_step_mufu_budget(mk, tau, merged):
     """jit.cu mg::plan_of: rates of equal |b| share one exp and each gate's
-    divisions share one reciprocal -- except on half of the gates, which take
-    two (config 2: 8 shared exps + 6 decays + 3 + 2*3 reciprocals = 23); the
-    direct step keeps the reference's transcendental count."""
+    divisions share one reciprocal (config 2: 8 shared exps + 6 decays + 6
+    reciprocals = 20); the direct step keeps the reference's transcendental
+    count."""
     src = nat.jit_source(mk())
     assert "// merged form off" not in src
     assert _mufu_ops(src, "step_fwd_m") == merged
