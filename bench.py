@@ -646,6 +646,7 @@ def main():
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
                 "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
                 "morphology": extras.get("morphology"), "c5_replicas": extras.get("c5_replicas"),
+                "readout_fit": extras.get("readout_fit"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)
