@@ -248,7 +248,6 @@ def fwd_bwd_leg(torch, dev):
     W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = bf16 tcgen05 projection,
     HH forward (full storage), BPTT, dW / db / dX gradient GEMMs."""
     from paper_2601_21407_b200.layer import HHLayer
-    from paper_2601_21407_b200.learn import mse
     B, N, T, K_in = 256, 1024, 100, 784
     torch.manual_seed(0)
     layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, check_finite=False, device=dev)
@@ -259,10 +258,10 @@ def fwd_bwd_leg(torch, dev):
     def step():
         layer.zero_grad(set_to_none=True)
         x.grad = None            # dX is produced every step, not accumulated across steps
-        V, S = layer(x)
-        # MSE(V, 0): one reduction forward, one elementwise pass backward
-        # (seed_v = 2 V / numel, learn.py:86-88)
-        mse(V).backward()
+        # MSE(V, 0) fused into the HH kernels: sum V^2 accumulated by the
+        # forward, the seed 2 V / numel (learn.py:86-88) read from the
+        # checkpoints by the BPTT kernel -- no V trace written, no seed pass
+        layer.mse_loss(x).backward()
 
     def timed(fn, reps=10):
         torch.cuda.synchronize()
@@ -286,7 +285,8 @@ def fwd_bwd_leg(torch, dev):
             "cuda_graph": graph is not None,
             "config": "BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, bf16 tcgen05 "
                       "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs, "
-                      "loss MSE(V, 0) (one unit = one neuron-step through forward and backward)"}
+                      "loss MSE(V, 0) fused into the HH kernels (layer.mse_loss; one unit = one "
+                      "neuron-step through forward and backward)"}
 
 
 def c5_leg(torch, dev, steps=1000):
@@ -428,9 +428,12 @@ def c4_leg(torch, dev):
     from paper_2601_21407_b200.layer import HHLayer
     B, T = 256, 100
     torch.manual_seed(1)
-    net = torch.nn.ModuleList([HHLayer(784, 2048, w_mean=0.05, w_std=0.1, check_finite=False, device=dev),
-                               HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, check_finite=False, device=dev),
-                               HHLayer(2048, 10, w_mean=0.02, w_std=0.05, check_finite=False, device=dev)])
+    # hidden layers hand on spikes only, the readout layer V only: the unused
+    # trace of each layer is never written
+    net = torch.nn.ModuleList([
+        HHLayer(784, 2048, w_mean=0.05, w_std=0.1, check_finite=False, device=dev, outputs="spikes"),
+        HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, check_finite=False, device=dev, outputs="spikes"),
+        HHLayer(2048, 10, w_mean=0.02, w_std=0.05, check_finite=False, device=dev, outputs="v")])
     import torch.distributed as dist
     world = dist.get_world_size() if dist.is_initialized() else 1
     # capturable Adam keeps its step counters on the device (CUDA-graph safe)

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define HHB_ABI_VERSION 1
+#define HHB_ABI_VERSION 2
 #define HHB_MAX_GATES 8
 #define HHB_MAX_CHANNELS 8
 
@@ -127,15 +127,19 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
 
 /* hhb_forward plus spk_val[n_steps][spk_val_ld] (dtype of V, NULL = off): the
  * spike flags as 0/1 values, the SNN layer's differentiable spike output,
- * written by the forward kernel itself (no bitmap round trip); and
+ * written by the forward kernel itself (no bitmap round trip);
  * step_base_dev (NULL = off): *step_base_dev is added to step_base on the
- * device (first_bad indices inside a replayed CUDA graph). */
+ * device (first_bad indices inside a replayed CUDA graph); and sq_partials
+ * (NULL = off): per-block partial sums of V'^2 over the launch, the fused
+ * forward half of an MSE(V, 0) loss (learn.py:80-88) -- hhb_forward_partials(n)
+ * doubles zeroed by the caller, summed by it in any fixed order. */
 int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
                    const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
                    int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
-                   const int64_t* step_base_dev, void* stream);
+                   const int64_t* step_base_dev, double* sq_partials, void* stream);
+int64_t hhb_forward_partials(int64_t n);
 /*
  * hhb_forward_poisson -- hhb_forward with the BASELINE config-2 stimulus
  * I[t][j] = amp * Poisson(lam) drawn inside the kernel (Philox-4x32-10 keyed by
@@ -192,7 +196,10 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
  * d_split_group > 0 neuron i sits at (i / group) * d_split_pitch + i % group
  * (rows of `group` neurons padded to a 16-byte pitch) -- and
  * d_i_sum[n] += sum over the steps of dI (the bias gradient before the
- * batch sum, learn.py:273). */
+ * batch sum, learn.py:273); seed_v_scale (device float, NULL = 1): seed_v is
+ * multiplied by *seed_v_scale as it is read -- with seed_v pointing at the V'
+ * values themselves (e.g. the checkpoint v-planes one slot ahead), the fused
+ * backward half of MSE(V, 0), seed = 2 V g / numel. */
 int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
                     int64_t n, int64_t n_steps, const void* i_ext, int64_t i_st, int64_t i_sn,
                     const void* ckpt, int64_t ckpt_every, int64_t ckpt_ld, void* seg_buf,
@@ -200,7 +207,7 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
                     void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
                     double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
                     void* d_i_hi, void* d_i_lo, int64_t d_split_ld, int64_t d_split_group,
-                    int64_t d_split_pitch, float* d_i_sum, void* stream);
+                    int64_t d_split_pitch, float* d_i_sum, const float* seed_v_scale, void* stream);
 int64_t hhb_backward_partials(int64_t n, int32_t dtype);
 
 /* ---- elementary ops (dynamics.py:324-381, adjoint.py:60-66) ------------ */

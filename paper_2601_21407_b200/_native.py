@@ -15,7 +15,7 @@ import threading
 from .errors import ConfigurationError, NativeLibraryError, UsageError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhhb200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_GATES = 8
 MAX_CHANNELS = 8
 
@@ -72,7 +72,8 @@ SIGNATURES = {
                               _vp, _i64,
                               _vp, _i64,
                               _vp, _i64, _i64,
-                              _i64, _vp, _vp, _vp]),
+                              _i64, _vp, _vp, _vp, _vp]),
+    "hhb_forward_partials": (_i64, [_i64]),
     "hhb_backward": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
                             _vp, _i64, _i64,
                             _vp, _i64, _i64, _vp,
@@ -89,7 +90,7 @@ SIGNATURES = {
                                _vp, _i64,
                                _vp, _vp,
                                _i64, _vp,
-                               _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+                               _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "hhb_forward_poisson": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
                                    _vp, _vp, _i64, _vp, _vp,
                                    C.c_uint64, _i64, _dbl, _dbl,

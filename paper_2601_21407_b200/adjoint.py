@@ -105,14 +105,16 @@ class AdjointState:
 # ---------------------------------------------------------------------------
 
 def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_v, adj_g,
-              d_i=None, step_base=0, want_d_i=True, split=None, d_sum=None, ck_ld=None):
+              d_i=None, step_base=0, want_d_i=True, split=None, d_sum=None, ck_ld=None, sv_ld=None,
+              sv_scale=None):
     """One hhb_backward(_ex) launch; returns (d_i or None, d_params np.array[1+nch], first_bad).
 
     split = (hi, lo[, group, pitch]) bf16 [T][ld] tensors receive dI as bf16 hi/lo halves
     (neuron i at (i // group) * pitch + i % group when group > 0)
     and d_sum [n] float accumulates the per-neuron sums of dI (SNN layer).
     ck_ld: leading dimension of the checkpoint planes (default n) -- the first
-    n neurons of a wider forward's checkpoints."""
+    n neurons of a wider forward's checkpoints.  sv_ld: seed_v row stride
+    (default n); sv_scale: device float multiplying seed_v as it is read."""
     dev = adj_v.device
     ng = params.n_gates
     nch = len(params.channels)
@@ -132,10 +134,11 @@ def _backward(params, spec, cur, i_st, i_sn, T, n, ckpt, K, seed_v, seed_s, adj_
     rc = lib.hhb_backward_ex(
         C.byref(P), C.byref(S), dt, n, T, cur.data_ptr(), i_st, i_sn,
         ckpt.data_ptr(), K, n if ck_ld is None else ck_ld, D.ptr(seg),
-        D.ptr(seed_v), n, D.ptr(seed_s), n,
+        D.ptr(seed_v), n if sv_ld is None else sv_ld, D.ptr(seed_s), n,
         adj_v.data_ptr(), D.ptr(adj_g) if ng else None, n,
         D.ptr(d_i), n, d_params.data_ptr(), parts.data_ptr(),
-        step_base, bad.data_ptr(), D.ptr(hi), D.ptr(lo), ld_split, grp, pitch, D.ptr(d_sum), D.stream())
+        step_base, bad.data_ptr(), D.ptr(hi), D.ptr(lo), ld_split, grp, pitch, D.ptr(d_sum), D.ptr(sv_scale),
+        D.stream())
     nat.check(rc, "hhb_backward")
     return d_i, d_params, bad
 

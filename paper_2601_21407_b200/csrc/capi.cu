@@ -33,8 +33,9 @@ static int forward_t(const hhb_params_t* P, int64_t n, int64_t steps, const void
                      int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld, uint32_t* spk,
                      int64_t spk_ld, void* ckpt, int64_t ck_every, int64_t ck_ld,
                      int64_t step_base, int64_t* first_bad, cudaStream_t st, void* spk_val = nullptr,
-                     int64_t spkv_ld = 0, const int64_t* step_base_dev = nullptr) {
+                     int64_t spkv_ld = 0, const int64_t* step_base_dev = nullptr, double* sq_part = nullptr) {
   FwdArgs<T> a{};
+  a.sq_part = sq_part;
   a.step_dev = reinterpret_cast<const long long*>(step_base_dev);
   a.spk_val = static_cast<T*>(spk_val);
   a.spkv_ld = spkv_ld;
@@ -97,8 +98,9 @@ static int backward_t(const hhb_params_t* P, const hhb_surrogate_t* S, int64_t n
                       int64_t ag_ld, void* d_i, int64_t di_ld, double* d_params, double* partials,
                       int64_t step_base, int64_t* first_bad, cudaStream_t st, void* di_hi = nullptr,
                       void* di_lo = nullptr, int64_t dh_ld = 0, float* di_sum = nullptr, int64_t dh_grp = 0,
-                      int64_t dh_pitch = 0) {
+                      int64_t dh_pitch = 0, const float* sv_scale = nullptr) {
   BwdArgs<T> a{};
+  a.sv_scale = sv_scale;
   a.dh_grp = dh_grp;
   a.dh_pitch = dh_pitch;
   a.di_hi = static_cast<uint16_t*>(di_hi);
@@ -196,7 +198,7 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
                 int64_t ckpt_ld, int64_t step_base, int64_t* first_bad, void* stream) {
   return hhb_forward_ex(params, dtype, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn, v_out,
                         v_ld, spk_out, spk_ld, nullptr, 0, ckpt, ckpt_every, ckpt_ld, step_base, first_bad,
-                        nullptr, stream);
+                        nullptr, nullptr, stream);
 }
 
 int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
@@ -204,7 +206,7 @@ int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t
                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
                    int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
-                   const int64_t* step_base_dev, void* stream) {
+                   const int64_t* step_base_dev, double* sq_partials, void* stream) {
   if (spk_val && spk_val_ld < n) return fail(HHB_EINVAL, "spk_val_ld < n");
   int rc = check_params(params);
   if (rc) return rc;
@@ -220,11 +222,13 @@ int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t
   if (dtype == HHB_F32)
     return forward_t<float>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                             v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                            first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev);
+                            first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials);
   return forward_t<double>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                            v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                           first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev);
+                           first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials);
 }
+
+int64_t hhb_forward_partials(int64_t n) { return (n < 1 ? 1 : (n + 31) / 32) + 1; }
 
 int hhb_forward_poisson(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
                         const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
@@ -264,7 +268,8 @@ int hhb_backward(const hhb_params_t* params, const hhb_surrogate_t* surrogate, i
                  void* stream) {
   return hhb_backward_ex(params, surrogate, dtype, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every, ckpt_ld,
                          seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v, adj_g, adj_g_ld, d_i, d_i_ld,
-                         d_params, partials, step_base, first_bad, nullptr, nullptr, 0, 0, 0, nullptr, stream);
+                         d_params, partials, step_base, first_bad, nullptr, nullptr, 0, 0, 0, nullptr, nullptr,
+                         stream);
 }
 
 int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate, int32_t dtype,
@@ -274,7 +279,7 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
                     void* adj_v, void* adj_g, int64_t adj_g_ld, void* d_i, int64_t d_i_ld,
                     double* d_params, double* partials, int64_t step_base, int64_t* first_bad,
                     void* d_i_hi, void* d_i_lo, int64_t d_split_ld, int64_t d_split_group,
-                    int64_t d_split_pitch, float* d_i_sum, void* stream) {
+                    int64_t d_split_pitch, float* d_i_sum, const float* seed_v_scale, void* stream) {
   if (d_split_group < 0 || (d_split_group > 0 && d_split_pitch < d_split_group))
     return fail(HHB_EINVAL, "d_split_pitch < d_split_group");
   if ((d_i_hi || d_i_lo || d_i_sum) && dtype != HHB_F32)
@@ -299,11 +304,11 @@ int hhb_backward_ex(const hhb_params_t* params, const hhb_surrogate_t* surrogate
                              ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                              adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base,
                              first_bad, ST(stream), d_i_hi, d_i_lo, d_split_ld, d_i_sum, d_split_group,
-                             d_split_pitch);
+                             d_split_pitch, seed_v_scale);
   return backward_t<double>(params, surrogate, n, n_steps, i_ext, i_st, i_sn, ckpt, ckpt_every,
                             ckpt_ld, seg_buf, seed_v, seed_v_ld, seed_spk, seed_spk_ld, adj_v,
                             adj_g, adj_g_ld, d_i, d_i_ld, d_params, partials, step_base, first_bad,
-                            ST(stream));
+                            ST(stream), nullptr, nullptr, 0, nullptr, 0, 0, seed_v_scale);
 }
 
 int hhb_gate_rates(const hhb_gate_t* gate, double rate_scale, int32_t dtype, int64_t n,

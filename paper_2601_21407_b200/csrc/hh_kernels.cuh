@@ -44,6 +44,7 @@ struct FwdArgs {
   T* spk_val;       // optional spike flags as 0/1 values [steps][spkv_ld] (SNN layer output)
   int64_t spkv_ld;
   const long long* step_dev;   // optional: device value added to step_base
+  double* sq_part;             // optional: per-block partial sums of V'^2 (fused MSE(V, 0) forward)
 };
 
 template <typename T>
@@ -74,6 +75,7 @@ struct BwdArgs {
   int64_t dh_ld;
   float* di_sum;
   int64_t dh_grp, dh_pitch;   // > 0: neuron i at column (i / grp) * pitch + i % grp
+  const float* sv_scale;      // optional: seed_v is read times *sv_scale (fused MSE(V, 0) backward)
 };
 
 __host__ __device__ inline int64_t split_col(int64_t i, int64_t grp, int64_t pitch) {
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
   long long bad = LLONG_MAX;
   int64_t ck_slot = 0;
   int64_t ck_count = 0;
+  double sq = 0.0;
 
   T cur[VEC];
   if (a.steps > 0) stim.at(a, ps, 0, n0, full, cur);
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
       const T vn = step_forward<T, NG>(tb, v[j], p[j], cur[j]);
       spk[j] = (v[j] < tb.theta) && (vn >= tb.theta);  // spike_detect, dynamics.py:379-381
       if (!finite_(vn) && bad == LLONG_MAX && n0 + j < a.n) bad = a.step_base + t;
+      if (a.sq_part != nullptr && n0 + j < a.n) sq += double(vn) * double(vn);
       v[j] = vn;
     }
     if (a.v_out != nullptr) {
@@ -398,6 +402,18 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
     }
   }
   if (bad != LLONG_MAX) atomicMin(a.first_bad, bad);
+  if (a.sq_part != nullptr) {   // block partial of sum V'^2: warp shuffle, warps in fixed order
+    __shared__ double red[kFwdThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) x += red[w];
+      a.sq_part[blockIdx.x] = x;
+    }
+  }
 }
 
 // ------------------------------------------------------------ backward
@@ -460,7 +476,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
         load_state<T, NG>(src, a.ck_ld, ii, v, p);
       }
       const T cur = __ldg(a.i_ext + t * a.i_st + ii * a.i_sn);
-      if (a.seed_v != nullptr) d_v = add_(d_v, __ldg(a.seed_v + t * a.sv_ld + ii));
+      if (a.seed_v != nullptr)
+        d_v = add_(d_v, a.sv_scale != nullptr ? T(__ldg(a.seed_v + t * a.sv_ld + ii) * T(*a.sv_scale))
+                                              : __ldg(a.seed_v + t * a.sv_ld + ii));
       const bool has_s = a.seed_s != nullptr;
       const T ds = has_s ? __ldg(a.seed_s + t * a.ss_ld + ii) : T(0);
       const T di = step_backward<T, NG>(tb, sur, v, p, cur, d_v, d_p, ds, has_s, acc);

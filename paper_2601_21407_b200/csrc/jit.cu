@@ -647,7 +647,8 @@ static std::string emit_gate_bwd(const GatePlan& gp, const std::vector<Group>& G
       D1 = b.d1;
     }
     X iD, iN;
-    if (false) {   // the issue-bound backward always takes two reciprocals (see plan_of)
+    static const bool bwd_one = getenv("HHB_JIT_BWD_ONE_RCP") && atoi(getenv("HHB_JIT_BWD_ONE_RCP")) > 0;
+    if (bwd_one && gp.one_rcp) {   // default: the issue-bound backward takes two reciprocals (see plan_of)
       const X r = bind(o, "r", V("rcpf_(" + mulx(N, D).e + ")"));
       iD = bind(o, "iD", mulx(N, r));
       iN = bind(o, "iN", mulx(D, r));
@@ -887,7 +888,7 @@ typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
-  float* spk_val; i64 spkv_ld; const long long* step_dev; };
+  float* spk_val; i64 spkv_ld; const long long* step_dev; double* sq_part; };
 struct PoissonTab { int size; float amp; float cdf[48]; };
 // Philox-4x32-10 with the key schedule precomputed on the host (one kernel
 // parameter per round key: LOP3 takes them straight from the constant bank)
@@ -949,7 +950,8 @@ struct PoissonSmem {
 struct BwdArgs { i64 n, steps; const float* i_ext; i64 i_st, i_sn; const float* ckpt; i64 ck_every, ck_ld;
   float* seg; const float* seed_v; i64 sv_ld; const float* seed_s; i64 ss_ld; float* adj_v; float* adj_g;
   i64 ag_ld; float* d_i; i64 di_ld; double* partials; i64 step_base; i64* first_bad;
-  unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; i64 dh_grp, dh_pitch; };
+  unsigned short* di_hi; unsigned short* di_lo; i64 dh_ld; float* di_sum; i64 dh_grp, dh_pitch;
+  const float* sv_scale; };
 __device__ __forceinline__ void split_bf16(float x, unsigned short& hi, unsigned short& lo) {
   // round-to-nearest-even bf16 of x (cvt.rn.bf16x2.f32), then of the remainder
   // x - hi, which is exact in fp32; one packed cvt yields both halves
@@ -1064,6 +1066,8 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   }
   i64 bad = LLMAX;
   int ck_count = 0;
+  float sqf = 0.0f;
+  double sqd = 0.0;
   // running pointers (one 64-bit add per step instead of t * ld)
   float* ckp = FF_CK ? a.ckpt + n0 : nullptr;
   const i64 sstride = (1 + NG) * a.ck_ld;
@@ -1122,6 +1126,11 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       fin = fin && finitef_(vn[j]);
       v[j] = vn[j];
     }
+    if (FF_L2) {   // fused MSE(V, 0) forward: fp32 partials, flushed to fp64 every 8 steps
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) sqf = __fmaf_rn(((valid >> j) & 1u) ? v[j] : 0.0f, v[j], sqf);
+      if ((t & 7) == 7) { sqd += double(sqf); sqf = 0.0f; }
+    }
     nib &= valid;
     if (!fin && bad == LLMAX) {  // rare: locate the neuron (padding lanes never count)
 #pragma unroll
@@ -1165,6 +1174,19 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
     }
   }
   if (bad != LLMAX) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)bad);
+  if (FF_L2) {   // block partial: warp shuffle, then the warps in a fixed order
+    __shared__ double red[8];
+    double x = sqd + double(sqf);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double y = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) y += red[w];
+      a.sq_part[blockIdx.x] = y;
+    }
+  }
 }
 extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v1(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<1, false>(a, t, k); }
 extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwd_v4(const FwdArgs a, const PoissonTab t, const Keys k) { fwd_body<4, false>(a, t, k); }
@@ -1242,6 +1264,7 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
     for (int g = 0; g < NG; ++g) d_p[j][g] = on[j] ? a.adj_g[g * a.ag_ld + ii[j]] : 0.0f;
   }
   const i64 K = BF_K1 ? 1 : a.ck_every;
+  const float svs = BF_SVS ? *a.sv_scale : 1.0f;
   const i64 sstride = (1 + NG) * a.ck_ld;
   i64 goff[NGX];
 #pragma unroll
@@ -1322,7 +1345,8 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) p[j][g] = r[(1 + g) * BWD_THREADS + j];
         cur[j] = r[(NG + 1) * BWD_THREADS + j];
-        if (BF_SV) d_v[j] = __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
+        if (BF_SV) d_v[j] = BF_SVS ? __fmaf_rn(svs, r[(NG + 2) * BWD_THREADS + j], d_v[j])
+                                   : __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
         ds[j] = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
 #if HAS_MERGED
         reg = reg && regular(v[j]);
@@ -1427,8 +1451,8 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2
 // otherwise the forward module specialised on FF_* (kind = -1 - flags).
 // bwd_flags < 0: the forward module; >= 0: the backward module specialised
 // on BF_* (which optional streams the launch has); -2: both, for inspection
-enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32 };
-enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16 };
+enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32, BF_SVS = 64 };
+enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16, FF_L2 = 32 };
 constexpr int kInspect = -1000;
 static int fwd_kind(int ff) { return -1 - ff; }
 static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
@@ -1588,17 +1612,18 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
   }
   if (bwd_flags < 0) {
     const int ff = bwd_flags == kInspect ? (FF_VO | FF_SO | FF_CK) : -1 - bwd_flags;
-    src += fmt("#define FF_VO %d\n#define FF_SO %d\n#define FF_SVO %d\n#define FF_CK %d\n#define FF_AL %d\n",
+    src += fmt("#define FF_VO %d\n#define FF_SO %d\n#define FF_SVO %d\n#define FF_CK %d\n#define FF_AL %d\n"
+               "#define FF_L2 %d\n",
                (ff & FF_VO) ? 1 : 0, (ff & FF_SO) ? 1 : 0, (ff & FF_SVO) ? 1 : 0, (ff & FF_CK) ? 1 : 0,
-               (ff & FF_AL) ? 1 : 0);
+               (ff & FF_AL) ? 1 : 0, (ff & FF_L2) ? 1 : 0);
     src += kForwardBody;
   }
   if (bwd_flags >= 0 || bwd_flags == kInspect) {
     const int f = bwd_flags < 0 ? (BF_SV | BF_DI) : bwd_flags;
     src += fmt("#define BF_SV %d\n#define BF_SS %d\n#define BF_DI %d\n#define BF_SPLIT %d\n#define BF_SUM %d\n"
-               "#define BF_K1 %d\n",
+               "#define BF_K1 %d\n#define BF_SVS %d\n",
                (f & BF_SV) ? 1 : 0, (f & BF_SS) ? 1 : 0, (f & BF_DI) ? 1 : 0, (f & BF_SPLIT) ? 1 : 0,
-               (f & BF_SUM) ? 1 : 0, (f & BF_K1) ? 1 : 0);
+               (f & BF_SUM) ? 1 : 0, (f & BF_K1) ? 1 : 0, (f & BF_SVS) ? 1 : 0);
     src += kBwdKernel;
   }
   return src;
@@ -1638,6 +1663,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += bmb ? std::string("b") + bmb : "";
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
   k += bmb2 ? std::string("c") + bmb2 : "";
+  const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
+  k += b1 ? std::string("o") + b1 : "";
   return k;
 }
 
@@ -1711,7 +1738,7 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
                        (!a.spk_val || (a.spkv_ld % 4 == 0 && al16(a.spk_val))) &&
                        (!a.ckpt || (a.ck_ld % 4 == 0 && al16(a.ckpt)));
   const int ff = (a.v_out ? FF_VO : 0) | (a.spk ? FF_SO : 0) | (a.spk_val ? FF_SVO : 0) | (a.ckpt ? FF_CK : 0) |
-                 (aligned ? FF_AL : 0);
+                 (aligned ? FF_AL : 0) | (a.sq_part ? FF_L2 : 0);
   jit::Module* m = jit::get_module(P, fwd_kind(ff));
   if (!m) return false;
   const int VEC = vec4 ? 4 : 1;
@@ -1738,7 +1765,8 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
                   int& rc) {
   using namespace jit;
   const int flags = (a.seed_v ? BF_SV : 0) | (a.seed_s ? BF_SS : 0) | (a.d_i ? BF_DI : 0) |
-                    (a.di_hi ? BF_SPLIT : 0) | (a.di_sum ? BF_SUM : 0) | (a.ck_every == 1 ? BF_K1 : 0);
+                    (a.di_hi ? BF_SPLIT : 0) | (a.di_sum ? BF_SUM : 0) | (a.ck_every == 1 ? BF_K1 : 0) |
+                    (a.seed_v && a.sv_scale ? BF_SVS : 0);
   jit::Module* m = jit::get_module(P, flags);
   if (!m) return false;
   const int64_t blocks = bwd_blocks(a.n);

@@ -446,7 +446,7 @@ class Workspace:
 def _forward(params: HHParams, v: torch.Tensor, g: torch.Tensor, cur: torch.Tensor, i_st: int,
              i_sn: int, steps: int, *, v_fin=None, g_fin=None, v_out=None, bits=None,
              ckpt=None, ckpt_every: int = 0, step_base: int = 0, first_bad=None,
-             reset_bad: bool = True, spk_val=None, step_dev=None):
+             reset_bad: bool = True, spk_val=None, step_dev=None, sq_part=None):
     """One hhb_forward launch on device tensors (flat v (n,), g (ng, n)).
     first_bad accumulates (atomicMin) across launches when reset_bad=False."""
     n = v.numel()
@@ -466,7 +466,7 @@ def _forward(params: HHParams, v: torch.Tensor, g: torch.Tensor, cur: torch.Tens
         D.ptr(cur), i_st, i_sn,
         D.ptr(v_out), n, D.ptr(bits), words, D.ptr(spk_val), n,
         D.ptr(ckpt), max(1, ckpt_every), n,
-        step_base, first_bad.data_ptr(), D.ptr(step_dev), D.stream())
+        step_base, first_bad.data_ptr(), D.ptr(step_dev), D.ptr(sq_part), D.stream())
     nat.check(rc, "hhb_forward")
     return v_fin, g_fin, first_bad
 

@@ -139,22 +139,64 @@ def col_sum(dI: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv_ld=None, sv_scale=None):
+    """BPTT of the layer's HH population from seeds (sv, ss) and the projection
+    gradients (dX, dW, db)."""
+    T, B, k_in, n_out = shape
+    M, n = T * B, B * n_out
+    p = layer.params
+    # adjoint state (d_v, d_gates) and the per-neuron dI sums: one zeroed block
+    zb = torch.zeros((2 + p.n_gates) * n, dtype=torch.float32, device=cur.device)
+    adj_v = zb[:n]
+    adj_g = zb[n:(1 + p.n_gates) * n].view(p.n_gates, n)
+    # dI leaves the BPTT kernel as bf16 hi/lo planes [T*B][P] (P = n_out padded
+    # to 8 for TMA pitches) + per-neuron sums; the gradient GEMMs read them (and
+    # X, W) in place, MN-major
+    P = _pad8(n_out)
+    hi = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
+    lo = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
+    dsum = zb[(1 + p.n_gates) * n:]
+    _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, K, sv, ss, adj_v, adj_g,
+                                  want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum, ck_ld=n, sv_ld=sv_ld,
+                                  sv_scale=sv_scale)
+    layer._last_gbad = gbad
+    if layer.check_finite:
+        b = int(gbad.item())
+        if b >= 0:
+            raise GradientOverflowError("adjoint state became non-finite", b)
+    layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
+    # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
+    dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+    db = col_sum(dsum.view(B, n_out)).float()
+    # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
+    dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0)).view(T, B, k_in)
+          if x_requires_grad else None)
+    return dX, dW, db
+
+
+def _project(x, weight, bias, layer):
+    T, B, k_in = x.shape
+    xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
+    wb = to_bf16_padded(weight.float().contiguous())
+    cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())        # (T*B, n_out) == (T, B*n_out)
+    return xb, wb, cur
+
+
 class _HHLayerFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, weight, bias, layer):
         T, B, k_in = x.shape
         n_out = weight.shape[0]
-        M, n = T * B, B * n_out
+        n = B * n_out
         p = layer.params
-        xb = to_bf16_padded(x.reshape(M, k_in).float().contiguous())
-        wb = to_bf16_padded(weight.float().contiguous())
-        cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())        # (T*B, n_out) == (T, B*n_out)
+        xb, wb, cur = _project(x, weight, bias, layer)
         v0, g0 = layer.rest_state(n, x.device)
         K = layer.segment(T)
         nck = (T + K - 1) // K
         ckpt = torch.empty((nck, 1 + p.n_gates, n), dtype=torch.float32, device=x.device)
-        v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
-        spikes = torch.empty((T, n), dtype=torch.float32, device=x.device)
+        want_v, want_s = layer.outputs in ("both", "v"), layer.outputs in ("both", "spikes")
+        v_out = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_v else None
+        spikes = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_s else None
         _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
         layer._last_bad = bad
         if layer.check_finite:
@@ -163,53 +205,68 @@ class _HHLayerFn(torch.autograd.Function):
         ctx.save_for_backward(xb, wb, cur, ckpt)
         ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
         ctx.x_requires_grad = x.requires_grad
-        return v_out.view(T, B, n_out), spikes.view(T, B, n_out)
+        return (v_out.view(T, B, n_out) if want_v else None), (spikes.view(T, B, n_out) if want_s else None)
 
     @staticmethod
     def backward(ctx, d_v, d_s):
         xb, wb, cur, ckpt = ctx.saved_tensors
-        layer = ctx.layer
         T, B, k_in, n_out = ctx.shape
-        M, n = T * B, B * n_out
-        p = layer.params
+        n = B * n_out
         sv = None if d_v is None else d_v.reshape(T, n).float().contiguous()
         ss = None if d_s is None else d_s.reshape(T, n).float().contiguous()
-        # adjoint state (d_v, d_gates) and the per-neuron dI sums: one zeroed block
-        zb = torch.zeros((2 + p.n_gates) * n, dtype=torch.float32, device=cur.device)
-        adj_v = zb[:n]
-        adj_g = zb[n:(1 + p.n_gates) * n].view(p.n_gates, n)
-        direct = True
-        if direct:
-            # dI leaves the BPTT kernel as bf16 hi/lo planes [T*B][P] (P = n_out
-            # padded to 8 for TMA pitches) + per-neuron sums; the gradient GEMMs
-            # read them (and X, W) in place, MN-major
-            P = _pad8(n_out)
-            hi = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
-            lo = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
-            dsum = zb[(1 + p.n_gates) * n:]
-            _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
-                                          adj_g, want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum)
+        dX, dW, db = _layer_grads(ctx.layer, xb, wb, cur, ckpt, ctx.K, ctx.shape, ctx.x_requires_grad, sv, ss)
+        return dX, dW, db, None
+
+
+class _HHLayerMSEFn(torch.autograd.Function):
+    """MSE(V, 0) of the layer's membrane trace, fused into its kernels: the
+    forward kernel accumulates sum V'^2 (per-block fp64 partials, summed in a
+    fixed order) and writes no V trace; the backward kernel reads its seed
+    2 V' g / numel (learn.py:86-88) straight from the checkpoints -- with full
+    storage the state before step t + 1 is V'(t), and the final state goes to
+    one extra slot -- scaled on the fly.  Same arithmetic as
+    mse(layer(x)[0]).backward() without the V and seed passes."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, layer):
+        T, B, k_in = x.shape
+        n_out = weight.shape[0]
+        n = B * n_out
+        p = layer.params
+        ng = p.n_gates
+        xb, wb, cur = _project(x, weight, bias, layer)
+        v0, g0 = layer.rest_state(n, x.device)
+        K = layer.segment(T)
+        sq = torch.zeros(int(nat.load().hhb_forward_partials(n)), dtype=torch.float64, device=x.device)
+        if K == 1:
+            ckpt = torch.empty((T + 1, 1 + ng, n), dtype=torch.float32, device=x.device)
+            v_out = None
+            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_fin=ckpt[T, 0], g_fin=ckpt[T, 1:], ckpt=ckpt,
+                                 ckpt_every=1, sq_part=sq)
         else:
-            d_i, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, ctx.K, sv, ss, adj_v,
-                                            adj_g)
-        layer._last_gbad = gbad
+            ckpt = torch.empty(((T + K - 1) // K, 1 + ng, n), dtype=torch.float32, device=x.device)
+            v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
+            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, ckpt=ckpt, ckpt_every=K, sq_part=sq)
+        layer._last_bad = bad
         if layer.check_finite:
-            b = int(gbad.item())
-            if b >= 0:
-                raise GradientOverflowError("adjoint state became non-finite", b)
-        layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
-        if direct:
-            # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
-            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
-            db = col_sum(dsum.view(B, n_out)).float()
-            # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
-            dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0)).view(T, B, k_in)
-                  if ctx.x_requires_grad else None)
-            return dX, dW, db, None
-        dI = d_i.view(M, n_out)
-        dW = grad_weight(dI, xb, k_in)
-        db = col_sum(dI).float()
-        dX = grad_input(dI, wb, k_in).view(T, B, k_in) if ctx.x_requires_grad else None
+            _raise_if_bad(bad)
+        ctx.save_for_backward(xb, wb, cur, ckpt, v_out)
+        ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
+        ctx.x_requires_grad = x.requires_grad
+        return (sq.sum() / (T * n)).float()
+
+    @staticmethod
+    def backward(ctx, g):
+        xb, wb, cur, ckpt, v_out = ctx.saved_tensors
+        T, B, k_in, n_out = ctx.shape
+        n = B * n_out
+        scale = (g.float() * (2.0 / (T * n))).reshape(1).contiguous()
+        if ctx.K == 1:
+            seed, sv_ld = ckpt[1:, 0], ckpt.stride(0)      # V'(t) = v-plane of slot t + 1
+        else:
+            seed, sv_ld = v_out, n
+        dX, dW, db = _layer_grads(ctx.layer, xb, wb, cur, ckpt, ctx.K, ctx.shape, ctx.x_requires_grad, seed,
+                                  None, sv_ld=sv_ld, sv_scale=scale)
         return dX, dW, db, None
 
 
@@ -217,7 +274,9 @@ class HHLayer(torch.nn.Module):
     """Linear(n_in -> n_out, bf16 tcgen05) followed by n_out HH neurons per batch
     row, stepped over the leading time axis of x (T, B, n_in).
 
-    Returns (V, spikes), both (T, B, n_out) fp32 on the device; spikes carry
+    Returns (V, spikes), both (T, B, n_out) fp32 on the device (outputs="v" or
+    "spikes" keeps only that one -- the other comes back None and is never
+    written); spikes carry
     gradients through the surrogate (seed_spike of adjoint.py:354-359), so
     layers stack.  HH parameters are fixed (like the reference's neuron in
     ReadoutModel); their gradients d_c_m / d_g_max of the last backward are in
@@ -228,8 +287,11 @@ class HHLayer(torch.nn.Module):
 
     def __init__(self, n_in: int, n_out: int, params: HHParams | None = None, budget: int | None = None,
                  surrogate: SurrogateSpec | None = None, w_mean: float = 0.0, w_std: float | None = None,
-                 check_finite: bool = True, device=None):
+                 check_finite: bool = True, device=None, outputs: str = "both"):
         super().__init__()
+        if outputs not in ("both", "v", "spikes"):
+            raise UsageError('outputs must be "both", "v" or "spikes"')
+        self.outputs = outputs
         dev = device or D.require_cuda()
         p = params if params is not None else cortical_rs_params(dt=0.1)
         self.params = p.with_(dtype=np.float32)
@@ -274,3 +336,16 @@ class HHLayer(torch.nn.Module):
         if x.dim() != 3:
             raise UsageError("HHLayer expects x of shape (T, B, n_in)")
         return _HHLayerFn.apply(x, self.weight, self.bias, self)
+
+    def mse_loss(self, x: torch.Tensor, target: torch.Tensor | None = None) -> torch.Tensor:
+        """MSE(V, target) of the layer's membrane trace (learn.py:80-88),
+        differentiable into W, b and x.  target None (= 0) runs the fused
+        kernels (_HHLayerMSEFn); otherwise learn.mse over the V output."""
+        if x.dim() != 3:
+            raise UsageError("HHLayer expects x of shape (T, B, n_in)")
+        if target is None:
+            return _HHLayerMSEFn.apply(x, self.weight, self.bias, self)
+        from .learn import mse
+        if self.outputs == "spikes":
+            raise UsageError('mse_loss with a target needs the V output (outputs "both" or "v")')
+        return mse(self(x)[0], target)

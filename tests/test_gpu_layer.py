@@ -93,3 +93,57 @@ def test_config3_shape_runs_and_is_deterministic(cuda):
     assert torch.equal(grads[0], grads[1])
     assert torch.isfinite(grads[0]).all() and grads[0].abs().sum() > 0
     assert 0 < S.sum().item() < S.numel()
+
+
+def _layer_and_input(cuda, budget, n_out, outputs="both", T=40, B=3, k_in=24):
+    torch.manual_seed(0)
+    layer = HHLayer(k_in, n_out, DF.cortical_rs_params(dt=0.1), budget=budget, w_mean=0.6, w_std=0.5,
+                    device=cuda, outputs=outputs)
+    with torch.no_grad():
+        layer.bias.copy_(torch.linspace(-1.0, 2.0, n_out, device=cuda))
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = ((torch.rand((T, B, k_in), device=cuda, generator=g) < 0.3).float()
+         + 0.1 * torch.randn((T, B, k_in), device=cuda, generator=g)).requires_grad_(True)
+    return layer, x
+
+
+@pytest.mark.parametrize("budget,n_out", [(None, 8), (4, 10), (None, 16)])
+def test_fused_mse_loss_matches_unfused(cuda, budget, n_out):
+    """layer.mse_loss(x) (sum V^2 in the forward kernel, seed 2 V' g / n read
+    from the checkpoints in the backward kernel) == mse(layer(x)[0])."""
+    from paper_2601_21407_b200.learn import mse
+    layer, x = _layer_and_input(cuda, budget, n_out)
+    V, _ = layer(x)
+    loss_u = mse(V)
+    (3.0 * loss_u).backward()
+    gu = [t.grad.detach().clone() for t in (layer.weight, layer.bias, x)]
+    pgu = layer.param_grads.clone()
+    for t in (layer.weight, layer.bias, x):
+        t.grad = None
+    loss_f = layer.mse_loss(x)
+    (3.0 * loss_f).backward()
+    assert loss_f.dtype == torch.float32 and loss_f.dim() == 0
+    assert abs(loss_f.item() - loss_u.item()) <= 1e-6 * abs(loss_u.item())
+    for a, b in zip((layer.weight.grad, layer.bias.grad, x.grad), gu):
+        assert nrel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
+    assert nrel(layer.param_grads.cpu().numpy(), pgu.cpu().numpy()) < 1e-5
+
+
+def test_layer_output_selection(cuda):
+    """outputs="v" / "spikes" returns (and writes) only that trace; values and
+    gradients are those of the full layer."""
+    full, x = _layer_and_input(cuda, None, 8)
+    V, S = full(x)
+    (S.sum() * 0.01 + (V * 0.001).sum()).backward()
+    for outputs in ("v", "spikes"):
+        lyr, x2 = _layer_and_input(cuda, None, 8, outputs=outputs)
+        V2, S2 = lyr(x2)
+        if outputs == "v":
+            assert S2 is None and torch.equal(V2, V)
+            (V2 * 0.001).sum().backward()
+        else:
+            assert V2 is None and torch.equal(S2, S)
+            (S2.sum() * 0.01).backward()
+        assert lyr.weight.grad is not None and torch.isfinite(lyr.weight.grad).all()
+    with pytest.raises(Exception):
+        HHLayer(4, 8, device=cuda, outputs="neither")
