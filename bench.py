@@ -425,7 +425,7 @@ def c4_leg(torch, dev):
     """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
     batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
     training step per unit of work."""
-    from paper_2601_21407_b200.layer import HHLayer
+    from paper_2601_21407_b200.layer import HHLayer, allreduce_gradients
     B, T = 256, 100
     torch.manual_seed(1)
     # hidden layers hand on spikes only, the readout layer V only: the unused
@@ -454,16 +454,7 @@ def c4_leg(torch, dev):
         loss = torch.nn.functional.cross_entropy(v.mean(0), y)
         loss.backward()
         if world > 1:  # data parallel over the batch shards of the ranks
-            off = 0
-            for p in params:
-                flat[off:off + p.numel()].copy_(p.grad.reshape(-1))
-                off += p.numel()
-            dist.all_reduce(flat)
-            flat.div_(world)
-            off = 0
-            for p in params:
-                p.grad.copy_(flat[off:off + p.numel()].view_as(p.grad))
-                off += p.numel()
+            allreduce_gradients(params, flat=flat)
         opt.step()
         return loss.detach()     # no autograd graph kept alive across steps (graph capture)
 

@@ -349,3 +349,30 @@ class HHLayer(torch.nn.Module):
         if self.outputs == "spikes":
             raise UsageError('mse_loss with a target needs the V output (outputs "both" or "v")')
         return mse(self(x)[0], target)
+
+
+def allreduce_gradients(params, group=None, flat: torch.Tensor | None = None) -> torch.Tensor | None:
+    """Data-parallel step of configs 3/4: average the gradients
+    of `params` over the ranks of `group` with ONE all-reduce of a flat
+    bucket (NCCL on the GPUs, gloo in the CPU tests), then copy the averages
+    back.  flat: optional reusable bucket (float32, >= total numel).  Returns
+    the bucket.  A no-op (None) without an initialised process group of
+    more than one rank."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return None
+    grads = [p.grad for p in params if p.grad is not None]
+    total = sum(g.numel() for g in grads)
+    if flat is None or flat.numel() < total:
+        flat = torch.empty(total, dtype=torch.float32, device=grads[0].device)
+    off = 0
+    for g in grads:
+        flat[off:off + g.numel()].copy_(g.reshape(-1))
+        off += g.numel()
+    dist.all_reduce(flat[:total], group=group)
+    flat[:total].div_(dist.get_world_size(group))
+    off = 0
+    for g in grads:
+        g.copy_(flat[off:off + g.numel()].view_as(g))
+        off += g.numel()
+    return flat

@@ -377,3 +377,23 @@ def test_fp32_merged_step_irregular_lanes(cuda):
     assert torch.equal(big.spike_series[:, :k], small.spike_series)
     v_ref, s_ref = O.simulate(p64, i[:, :k].astype(np.float64), v0=v0[:k], g0=g0[:, :k])
     check_fp32_contract(big.v_series[:, :k].cpu().numpy(), big.spike_series[:, :k].cpu().numpy(), v_ref, s_ref)
+
+
+def test_neuron_shards_equal_one_population(cuda):
+    """Configs 1/2 shard neurons across ranks with no collective:
+    two shards (neuron_base 0 and n/2) reproduce the unsharded population bit
+    for bit, the fused Philox stimulus being keyed by the global neuron id."""
+    from paper_2601_21407_b200.population import PoissonCurrent, Population
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    n, T = 8192, 120
+    stim = PoissonCurrent(2.0, 2.0, seed=5)
+    whole = Population(p, n, chunk=40, device=cuda)
+    vw = []
+    whole.advance(stim, T, on_chunk=lambda t, v, s: vw.append(v.clone()))
+    parts = []
+    for base in (0, n // 2):
+        sh = Population(p, n // 2, chunk=40, device=cuda, neuron_base=base)
+        vs = []
+        sh.advance(stim, T, on_chunk=lambda t, v, s: vs.append(v.clone()))
+        parts.append(torch.cat(vs))
+    assert torch.equal(torch.cat(vw), torch.cat(parts, dim=1))
