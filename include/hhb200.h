@@ -379,6 +379,27 @@ int hhb_spike_deliver_dev(int64_t words, const uint32_t* bits, const int64_t* of
                           const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
                           int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring,
                           void* stream);
+/* The whole network step loop of one rank in ONE cooperative launch
+ * (cortex.py:273-310 x steps; float32 neurons, JIT module): ring drain + PSP +
+ * Philox background (bg_mode 0 none / 2 philox, as hhb_cortex_input_dev), the
+ * HH step, the spike bitmap and the synapse delivery; one block per
+ * 256-neuron tile, one grid barrier per step (barrier: one device uint32 of
+ * scratch), n <= 65536.  Synapse rows must be sorted by target: segments[s][k]
+ * (int64, n_sources x (tiles + 1), tiles = ceil(n / 256)) is the index of the
+ * first synapse of row s with target >= 256 k, so a tile delivers only its
+ * own segment of each spiking row.  bits: [2][words] ping-pong, or with
+ * record != 0 [steps][words] -- the spike words of every step.  timing
+ * (NULL = off): [steps][tiles][4] %globaltimer stamps per block (step start,
+ * spikes written, barrier passed, delivery done) for profiling.  Bit-identical to stepping
+ * the same network with the per-step kernels; HHB_ENOTSUP when the JIT or
+ * cooperative launches are unavailable. */
+int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+                   float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
+                   uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
+                   uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
+                   const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
+                   uint32_t* barrier, uint64_t* timing, void* stream);
+
 int hhb_cortex_tick(int64_t* t_dev, void* stream);
 /* hhb_spike_deliver_dev in two kernels for the sparse per-step case: one
  * block lists the spiking sources (ascending) with the prefix of their row

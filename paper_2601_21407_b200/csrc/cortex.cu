@@ -15,6 +15,27 @@
 namespace hhb {
 namespace cortex {
 
+// compound Poisson N mu + sigma sqrt(N) z (cortex.py:225-232) in single
+// precision, explicit roundings (repeated verbatim by jit.cu hh_net's bg_draw)
+__device__ __forceinline__ float bg_draw_f32(float L, float mu, float sigma, uint4 r) {
+  const float u = __fmul_rn(__fadd_rn(__uint2float_rn(r.x), 0.5f), 2.3283064365386963e-10f);
+  float p = __expf(-L), c = p;
+  int k = 0;
+  while (u > c && k < 64) {
+    ++k;
+    p = __fmul_rn(p, __fdividef(L, float(k)));
+    c = __fadd_rn(c, p);
+  }
+  float add = __fmul_rn(float(k), mu);
+  if (sigma > 0.0f && k > 0) {
+    const float u1 = __fmul_rn(__fadd_rn(__uint2float_rn(r.y), 0.5f), 2.3283064365386963e-10f);
+    const float u2 = __fmul_rn(__fadd_rn(__uint2float_rn(r.z), 0.5f), 2.3283064365386963e-10f);
+    const float z = __fmul_rn(__fsqrt_rn(__fmul_rn(-2.0f, __logf(u1))), __cosf(__fmul_rn(6.283185307179586f, u2)));
+    add = __fadd_rn(add, __fmul_rn(__fmul_rn(sigma, __fsqrt_rn(float(k))), z));
+  }
+  return add;
+}
+
 // t_dev != NULL: the step index is read from device memory (CUDA-graph replay
 // of the network step; hhb_cortex_tick advances it), else t is used
 template <typename T>
@@ -33,11 +54,23 @@ __global__ void k_cortex_input(int64_t n, int64_t t, const long long* t_dev, int
   long long* slot = ring + (t % depth) * n + i;
   const long long arr = *slot;
   *slot = 0;
-  // reference order: psp *= decay; psp += arrived; psp += background (cortex.py:287-297)
-  T x = psp[i] * decay;
-  x = x + T(double(arr)) * w_scale;
+  // reference order: psp *= decay; psp += arrived; psp += background (cortex.py:287-297);
+  // single precision with explicit roundings: the persistent network kernel
+  // (jit.cu hh_net) repeats this arithmetic bit for bit
+  T x;
+  if constexpr (sizeof(T) == 4) {
+    x = __fadd_rn(__fmul_rn(psp[i], decay), __fmul_rn(float(double(arr)), w_scale));
+  } else {
+    x = psp[i] * decay;
+    x = x + T(double(arr)) * w_scale;
+  }
   if (mode == 1) {
     x = x + bg[i];
+  } else if (mode == 2 && sizeof(T) == 4) {
+    const uint4 r = Philox::run(make_uint4(uint32_t(i + nbase), uint32_t(uint64_t(i + nbase) >> 32), uint32_t(t),
+                                           uint32_t(uint64_t(t) >> 32)),
+                                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+    x = __fadd_rn(float(x), bg_draw_f32(float(lam[i]), float(mu), float(sigma), r));
   } else if (mode == 2) {
     // compound Poisson N*mu + sigma*sqrt(N)*z, N ~ Poisson(lam), z ~ N(0,1) (cortex.py:225-232);
     // Philox-4x32-10 keyed by (seed, global neuron, step): identical on every rank layout
@@ -310,6 +343,53 @@ int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_
                                               reinterpret_cast<const long long*>(t_dev), depth, n_pad, rg, per * 8,
                                               rep_ring);
   return cuda_check("k_spike_compact / k_spike_scatter (batch) launch");
+}
+
+int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+                   float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
+                   uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
+                   uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
+                   const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
+                   uint32_t* barrier, uint64_t* timing, void* stream) {
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (n <= 0 || steps <= 0) return HHB_OK;
+  if (tiles != (n + 255) / 256) return fail(HHB_EINVAL, "cortex_run: tiles != ceil(n / 256)");
+  if (!ring || !psp || !v || (params->n_gates > 0 && (!g || g_ld < n)) || !bits || !segments || !first_bad ||
+      !barrier || depth < 1 || words != (n + 31) / 32 || (bg_mode != 0 && bg_mode != 2) || (bg_mode == 2 && !lam))
+    return fail(HHB_EINVAL, "bad cortex_run args");
+  CortexRunArgs a{};
+  a.n = n;
+  a.steps = steps;
+  a.t0 = t0;
+  a.depth = depth;
+  a.ring = reinterpret_cast<long long*>(ring);
+  a.psp = psp;
+  a.lam = lam;
+  a.decay = float(decay);
+  a.mu = float(mu);
+  a.sigma = float(sigma);
+  a.w_scale = float(w_scale);
+  a.mode = bg_mode;
+  a.rec = record ? 1 : 0;
+  a.seed = seed;
+  a.nbase = neuron_base;
+  a.v = v;
+  a.g = g;
+  a.g_ld = g_ld;
+  a.bits = bits;
+  a.words = words;
+  a.seg = segments;
+  a.tiles = tiles;
+  a.tgt = targets;
+  a.w = weights_fx;
+  a.delay = delays;
+  a.first_bad = first_bad;
+  a.bar = barrier;
+  a.timing = reinterpret_cast<unsigned long long*>(timing);
+  if (!jit_cortex_run(params, a, static_cast<cudaStream_t>(stream), rc))
+    return fail(HHB_ENOTSUP, std::string("persistent network kernel unavailable: ") + jit_status());
+  return rc;
 }
 
 int hhb_cortex_tick(int64_t* t_dev, void* stream) {

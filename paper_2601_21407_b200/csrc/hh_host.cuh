@@ -251,6 +251,31 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
                  cudaStream_t st, int& rc);
 bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs<float>& a, cudaStream_t st,
                   int& rc);
+// host image of the JIT hh_net kernel's NetArgs (same member order and types)
+struct CortexRunArgs {
+  int64_t n, steps, t0, depth;
+  long long* ring;
+  float* psp;
+  const double* lam;
+  float decay, mu, sigma, w_scale;
+  int mode, rec;
+  unsigned long long seed;
+  int64_t nbase;
+  float* v;
+  float* g;
+  int64_t g_ld;
+  uint32_t* bits;
+  int64_t words;
+  const int64_t* seg;
+  int64_t tiles;
+  const int* tgt;
+  const int* w;
+  const int* delay;
+  int64_t* first_bad;
+  unsigned* bar;                 // grid-barrier counter (one uint32 of device scratch)
+  unsigned long long* timing;   // optional [steps][blocks][4] globaltimer stamps (profiling)
+};
+bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t st, int& rc);
 const char* jit_status();
 std::string jit_source(const hhb_params_t* P);
 

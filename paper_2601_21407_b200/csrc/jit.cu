@@ -49,6 +49,8 @@ struct Driver {
   decltype(&cuModuleLoadData) load = nullptr;
   decltype(&cuModuleGetFunction) get = nullptr;
   decltype(&cuLaunchKernel) launch = nullptr;
+  decltype(&cuLaunchCooperativeKernel) coop = nullptr;                        // optional
+  decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;  // optional
   bool ok = false;
   std::string why;
 };
@@ -93,6 +95,11 @@ static void load_libs() {
   g_drv.get = reinterpret_cast<decltype(g_drv.get)>(p);
   ok = ok && cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess && p;
   g_drv.launch = reinterpret_cast<decltype(g_drv.launch)>(p);
+  if (cudaGetDriverEntryPoint("cuLaunchCooperativeKernel", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+    g_drv.coop = reinterpret_cast<decltype(g_drv.coop)>(p);
+  if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p, cudaEnableDefault, &q) ==
+          cudaSuccess && p)
+    g_drv.occupancy = reinterpret_cast<decltype(g_drv.occupancy)>(p);
   g_drv.ok = ok;
   if (!ok) g_drv.why = "driver entry points unavailable";
 }
@@ -1195,6 +1202,272 @@ extern "C" __global__ void __launch_bounds__(256, FWD_MINB) hh_fwdp_v4(const Fwd
 
 )";
 
+// Persistent network kernel (BASELINE config 5, one rank): every network
+// step of cortex.py:273-310 -- ring drain + PSP + Philox background, the HH
+// step, spike bitmap, synapse delivery -- for `steps` steps in ONE cooperative
+// launch.  Block b owns the 256-neuron tile b (state in registers for the
+// whole launch) and is the only writer of its tile's ring columns: after the
+// grid barrier that publishes a step's spike bitmap, every block lists the
+// spiking sources and delivers, from each source's target-sorted synapse row,
+// just the segment that lands in its tile (seg[source][tile], precomputed).
+// One grid barrier per step; the ring drain of the next step needs only the
+// block's own barrier.  The input arithmetic is that of k_cortex_input
+// (cortex.cu, explicit roundings on both sides), the step the same step_fwd as
+// the forward module, the ring int64 fixed point: rasters, state and ring are
+// bit-identical to the per-step kernels.
+static const char* kNetKernel = R"(
+struct NetArgs { i64 n, steps, t0, depth; long long* ring; float* psp; const double* lam;
+  float decay, mu, sigma, w_scale; int mode, rec; unsigned long long seed; i64 nbase;
+  float* v; float* g; i64 g_ld; u32* bits; i64 words; const i64* seg; i64 tiles; const int* tgt; const int* w;
+  const int* delay; i64* first_bad; unsigned* bar; unsigned long long* timing; };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long x;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(x));
+  return x;
+}
+__device__ __forceinline__ uint4 philox_full(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const u32 hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const u32 hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+// compound Poisson N mu + sigma sqrt(N) z (cortex.py:225-232), as cortex.cu bg_draw_f32
+__device__ __forceinline__ float bg_draw(float L, float mu, float sigma, uint4 r) {
+  const float u = __fmul_rn(__fadd_rn(__uint2float_rn(r.x), 0.5f), 2.3283064365386963e-10f);
+  float p = __expf(-L), c = p;
+  int k = 0;
+  while (u > c && k < 64) {
+    ++k;
+    p = __fmul_rn(p, __fdividef(L, float(k)));
+    c = __fadd_rn(c, p);
+  }
+  float add = __fmul_rn(float(k), mu);
+  if (sigma > 0.0f && k > 0) {
+    const float u1 = __fmul_rn(__fadd_rn(__uint2float_rn(r.y), 0.5f), 2.3283064365386963e-10f);
+    const float u2 = __fmul_rn(__fadd_rn(__uint2float_rn(r.z), 0.5f), 2.3283064365386963e-10f);
+    const float z = __fmul_rn(__fsqrt_rn(__fmul_rn(-2.0f, __logf(u1))), __cosf(__fmul_rn(6.283185307179586f, u2)));
+    add = __fadd_rn(add, __fmul_rn(__fmul_rn(sigma, __fsqrt_rn(float(k))), z));
+  }
+  return add;
+}
+// grid barrier on a monotonic arrival counter (zeroed by the host per launch);
+// the launch is cooperative, so every block is resident.  (Measured against a
+// barrier-free exchange of tagged 64-bit spike words, whose polling by every
+// thread swamped L2: 9.3 vs 14.9 us per config-5 step.)
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // release-add (cumulative over the block's writes ordered by the bar.sync),
+    // relaxed polling (an acquire load would invalidate L1 on every spin), one
+    // acquire fence after
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned seen;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while (seen < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+#define NET_THREADS 256
+// exclusive block scan of one value per thread (warp shuffles + one smem pass)
+__device__ __forceinline__ i64 block_scan(i64 x, i64* s_w, i64& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  i64 inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const i64 y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  __syncthreads();
+  i64 before = 0;
+  total = 0;
+#pragma unroll
+  for (int k = 0; k < NET_THREADS / 32; ++k) {
+    const i64 wv = s_w[k];
+    if (k < wid) before += wv;
+    total += wv;
+  }
+  __syncthreads();
+  return before + inc - x;
+}
+extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a) {
+  __shared__ unsigned long long s_next[NET_THREADS];   // step t's delay-1 deliveries into the tile
+  __shared__ int s_src[NET_CAP];
+  __shared__ i64 s_beg[NET_CAP];
+  __shared__ i64 s_pre[NET_CAP + 1];
+  __shared__ i64 s_w[NET_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned nb = gridDim.x;
+  unsigned phase = 0;
+  const i64 tile = blockIdx.x;                    // host: gridDim.x == tiles
+  const i64 i = tile * NET_THREADS + tid;
+  const bool on = i < a.n;
+  // the tile's state lives in registers for the whole launch
+  float vv = -65.0f, psp = 0.0f, lam = 0.0f;
+  float pp[NGX];
+#pragma unroll
+  for (int q = 0; q < NGX; ++q) pp[q] = 0.5f;
+  if (on) {
+    vv = a.v[i];
+    psp = a.psp[i];
+    lam = a.mode == 2 ? float(a.lam[i]) : 0.0f;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) pp[q] = a.g[q * a.g_ld + i];
+  }
+  const i64 per = (a.words + NET_THREADS - 1) / NET_THREADS;
+  const i64 w0 = tid * per, w1 = min(a.words, w0 + per);
+  const i64 tlo = tile * NET_THREADS;             // this tile's neurons [tlo, tlo + 256)
+  // Ring row t + 1 of the tile is complete, except for step t's delay-1
+  // synapses, once step t starts: it is read (and cleared) then, off the
+  // critical path, and the delay-1 deliveries of step t go to s_next instead.
+  // int64 sums commute: the drained values are those of the per-step kernels.
+  long long ahead = 0;
+  s_next[tid] = 0ull;
+  if (on && a.steps > 0) {
+    long long* slot = a.ring + (a.t0 % a.depth) * a.n + i;
+    ahead = __ldcg(slot);
+    *slot = 0;
+  }
+  __syncthreads();
+  unsigned long long* tm = a.timing ? a.timing + blockIdx.x * 4 : nullptr;
+  for (i64 s = 0; s < a.steps; ++s) {
+    const i64 t = a.t0 + s;
+    u32* bw = a.rec ? a.bits + s * a.words : a.bits + (s & 1) * a.words;
+    if (tm && tid == 0) tm[s * nb * 4 + 0] = gtimer();
+    // ---- input + HH step of the tile (padding lanes run the step on a dummy state)
+    float cur = 0.0f;
+    const long long arr = ahead + (long long)s_next[tid];
+    s_next[tid] = 0ull;                             // (next written after this block's barriers)
+    if (on && s + 1 < a.steps) {
+      long long* slot = a.ring + ((t + 1) % a.depth) * a.n + i;
+      ahead = __ldcg(slot);
+      *slot = 0;
+    }
+    if (on) {
+      float x = __fadd_rn(__fmul_rn(psp, a.decay), __fmul_rn(float(double(arr)), a.w_scale));
+      if (a.mode == 2) {
+        const uint4 r = philox_full(make_uint4(u32(i + a.nbase), u32((unsigned long long)(i + a.nbase) >> 32),
+                                               u32(t), u32((unsigned long long)t >> 32)),
+                                    make_uint2(u32(a.seed), u32(a.seed >> 32)));
+        x = __fadd_rn(x, bg_draw(lam, a.mu, a.sigma, r));
+      }
+      psp = x;
+      cur = x;
+    }
+    const float vo = vv;
+    vv = step_fwd(vv, pp, cur);
+    const bool spk = on && (vo < THETA) && (vv >= THETA);
+    if (on && !finitef_(vv)) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)t);
+    const u32 word = __ballot_sync(0xffffffffu, spk);
+    if (lane == 0 && (i >> 5) < a.words) bw[i >> 5] = word;
+    if (tm) {
+      __syncthreads();
+      if (tid == 0) tm[s * nb * 4 + 1] = gtimer();
+    }
+    grid_sync(a.bar, ++phase * nb);
+    if (tm && tid == 0) tm[s * nb * 4 + 2] = gtimer();
+    u32 wr[8];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      wr[k] = (w0 + k < w1) ? __ldcg(bw + w0 + k) : 0u;
+      cnt += __popc(wr[k]);
+    }
+    // ---- delivery into this tile: list the spiking sources (ascending) ...
+    i64 ns = 0;
+    const i64 first = block_scan(cnt, s_w, ns);
+    for (i64 r0 = 0; r0 < ns; r0 += NET_CAP) {
+      const i64 m = min(i64(NET_CAP), ns - r0);
+      if (cnt > 0 && first < r0 + m && first + cnt > r0) {
+        i64 k = first;
+        auto emit = [&](u32 x, i64 wi) {
+          while (x) {
+            const int b = __ffs(int(x)) - 1;
+            x &= x - 1;
+            if (k >= r0 && k < r0 + m) s_src[k - r0] = int(wi * 32 + b);
+            ++k;
+          }
+        };
+#pragma unroll
+        for (int q = 0; q < 8; ++q) emit(wr[q], w0 + q);
+      }
+      __syncthreads();
+      // ... each source's segment of synapses with targets in the tile ...
+      i64 lsum = 0;
+      const i64 c0 = (m * tid) / NET_THREADS, c1 = (m * (tid + 1)) / NET_THREADS;
+      for (i64 c = c0; c < c1; ++c) {
+        const i64* sg = a.seg + i64(s_src[c]) * (a.tiles + 1) + tile;
+        const i64 beg = __ldg(sg), end = __ldg(sg + 1);
+        s_beg[c] = beg;
+        s_pre[c] = end - beg;                     // length, turned into a prefix below
+        lsum += end - beg;
+      }
+      i64 total = 0;
+      i64 run = block_scan(lsum, s_w, total);
+      for (i64 c = c0; c < c1; ++c) {
+        const i64 l = s_pre[c];
+        s_pre[c] = run;
+        run += l;
+      }
+      if (tid == 0) s_pre[m] = total;
+      __syncthreads();
+      // ... and one thread per (source, synapse) pair, NET_UNROLL pairs in
+      // flight per thread (their loads overlap)
+#ifndef NET_UNROLL
+#define NET_UNROLL 4
+#endif
+      for (i64 g0 = tid; g0 < total; g0 += NET_THREADS * NET_UNROLL) {
+        int d[NET_UNROLL], tg[NET_UNROLL], wv[NET_UNROLL];
+#pragma unroll
+        for (int u = 0; u < NET_UNROLL; ++u) {
+          const i64 gi = g0 + u * NET_THREADS;
+          d[u] = 0;
+          if (gi < total) {
+            int lo = 0, hi = int(m);
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (s_pre[mid] <= gi) lo = mid;
+              else hi = mid;
+            }
+            const i64 j = s_beg[lo] + (gi - s_pre[lo]);
+            d[u] = __ldg(a.delay + j);
+            tg[u] = __ldg(a.tgt + j);
+            wv[u] = __ldg(a.w + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < NET_UNROLL; ++u) {
+          if (d[u] == 0) continue;
+          const unsigned long long wq = (unsigned long long)(long long)wv[u];
+          if (d[u] == 1) atomicAdd(&s_next[tg[u] - tlo], wq);
+          else atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + ((t + d[u]) % a.depth) * a.n + tg[u]), wq);
+        }
+      }
+      __syncthreads();
+    }
+    if (tm && tid == 0) tm[s * nb * 4 + 3] = gtimer();
+  }
+  __syncthreads();
+  if (on && a.steps > 0) {   // the last step's delay-1 deliveries back into the ring
+    long long* slot = a.ring + ((a.t0 + a.steps) % a.depth) * a.n + i;
+    *slot = *slot + (long long)s_next[tid];
+  }
+  if (on) {
+    a.v[i] = vv;
+    a.psp[i] = psp;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) a.g[q * a.g_ld + i] = pp[q];
+  }
+}
+)";
+
 static const char* kBwdKernel = R"(
 __device__ __forceinline__ void load_state(const float* base, i64 ld, i64 i, float& v, float (&p)[NGX]) {
   v = base[i];
@@ -1454,6 +1727,7 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2
 enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32, BF_SVS = 64 };
 enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16, FF_L2 = 32 };
 constexpr int kInspect = -1000;
+constexpr int kNet = -2000;   // the persistent network kernel (hh_net)
 static int fwd_kind(int ff) { return -1 - ff; }
 static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   const Layout L = layout_of(P);
@@ -1610,6 +1884,15 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
 }
 )";
   }
+  if (bwd_flags == kNet) {
+    // spikes listed per delivery round (shared memory); HHB_NET_CAP lowers it (tests)
+    const char* cap = getenv("HHB_NET_CAP");
+    src += fmt("#define NET_CAP %d\n", cap && atoi(cap) > 0 && atoi(cap) < 2048 ? atoi(cap) : 2048);
+    const char* nun = getenv("HHB_NET_UNROLL");
+    src += fmt("#define NET_UNROLL %d\n", nun && atoi(nun) > 0 ? atoi(nun) : 4);
+    src += kNetKernel;
+    return src;
+  }
   if (bwd_flags < 0) {
     const int ff = bwd_flags == kInspect ? (FF_VO | FF_SO | FF_CK) : -1 - bwd_flags;
     src += fmt("#define FF_VO %d\n#define FF_SO %d\n#define FF_SVO %d\n#define FF_CK %d\n#define FF_AL %d\n"
@@ -1632,6 +1915,8 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
 // ------------------------------------------------------------ cache
 struct Module {
   CUfunction fwd1 = nullptr, fwd4 = nullptr, fwdp1 = nullptr, fwdp4 = nullptr, bwd = nullptr, bwd2 = nullptr;
+  CUfunction net = nullptr;
+  int net_blocks_per_sm = 0;
   bool ok = false;
 };
 static std::map<std::string, Module> g_cache;
@@ -1665,6 +1950,10 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += bmb2 ? std::string("c") + bmb2 : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
+  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL"}) {
+    const char* x = getenv(e);
+    k += x ? std::string("|") + e + x : "";
+  }
   return k;
 }
 
@@ -1711,7 +2000,10 @@ static Module* get_module(const hhb_params_t* P, int bwd_flags) {
   g_nv.destroy(&prog);
   CUmodule mod;
   bool loaded = g_drv.load(&mod, cubin.data()) == CUDA_SUCCESS;
-  if (loaded && bwd_flags < 0)
+  if (loaded && bwd_flags == kNet) {
+    loaded = g_drv.get(&m.net, mod, "hh_net") == CUDA_SUCCESS && g_drv.occupancy &&
+             g_drv.occupancy(&m.net_blocks_per_sm, m.net, 256, 0) == CUDA_SUCCESS && m.net_blocks_per_sm > 0;
+  } else if (loaded && bwd_flags < 0)
     loaded = g_drv.get(&m.fwd1, mod, "hh_fwd_v1") == CUDA_SUCCESS && g_drv.get(&m.fwd4, mod, "hh_fwd_v4") == CUDA_SUCCESS &&
              g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") == CUDA_SUCCESS &&
              g_drv.get(&m.fwdp4, mod, "hh_fwdp_v4") == CUDA_SUCCESS;
@@ -1788,6 +2080,36 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
                                        unsigned(vec2 ? kBwdThreads / 2 : kBwdThreads), 1, 1, 0,
                                        reinterpret_cast<CUstream>(st), params, nullptr);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit backward launch failed");
+  return true;
+}
+
+// hh_net (kNetKernel): one cooperative launch for `steps` network steps.
+// Returns false when the JIT or a cooperative launch is unavailable.
+bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t st, int& rc) {
+  using namespace jit;
+  jit::Module* m = jit::get_module(P, kNet);
+  if (!m || !g_drv.coop) return false;
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one block per 256-neuron tile, all resident (cooperative launch)
+  const int64_t tiles = (a.n + 255) / 256, most = int64_t(m->net_blocks_per_sm) * sms;
+  if (cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st) != cudaSuccess) {
+    rc = fail(HHB_ECUDA, "barrier reset failed");
+    return true;
+  }
+  if ((a.words + 255) / 256 > 8) {
+    rc = fail(HHB_ENOTSUP, "hh_net: more than 65536 neurons (8 bitmap words per thread)");
+    return true;
+  }
+  if (tiles > most || tiles != a.tiles) {
+    rc = fail(HHB_ENOTSUP, "hh_net: the population needs more resident 256-neuron tiles than the GPU holds");
+    return true;
+  }
+  const unsigned grid = unsigned(tiles);
+  CortexRunArgs args = a;
+  void* params[] = {&args};
+  const CUresult r = g_drv.coop(m->net, grid, 1, 1, 256, 1, 1, 0, reinterpret_cast<CUstream>(st), params);
+  rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "cooperative launch of hh_net failed");
   return true;
 }
 

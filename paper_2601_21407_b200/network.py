@@ -36,7 +36,7 @@ from . import _native as nat
 from . import connectivity as conn
 from .defaults import cortical_rs_params
 from .dynamics import HHParams, _forward, _raise_if_bad, _table, init_state
-from .errors import ConfigurationError, UsageError
+from .errors import ConfigurationError, NativeLibraryError, UsageError
 
 W_FRAC_BITS = 24  # weight quantum 2^-24 uA
 
@@ -404,16 +404,86 @@ class CortexNetwork:
         nat.check(lib.hhb_cortex_tick(self.t_dev.data_ptr(), D.stream()), "hhb_cortex_tick")
         return gw
 
+    def persistent_ok(self) -> bool:
+        """Whether advance() runs the persistent kernel (hhb_cortex_run): one
+        rank, float32 neurons, device (or no) background; HHB_NET_GRAPH=1
+        forces the graph path."""
+        import os
+        return (self.exchange is None and self.world == 1 and self.dtype == np.float32 and self.n > 0
+                and self.bg_mode != "host" and os.environ.get("HHB_NET_GRAPH", "0") in ("", "0"))
+
+    def _tile_segments(self):
+        """Sort every synapse row by target (delivery order does not change the
+        int64 ring) and index, per row, the first synapse of each 256-neuron
+        target tile: seg[s][k] for k = 0..tiles (hhb_cortex_run's layout)."""
+        if getattr(self, "_seg", None) is None:
+            dev = self.dev
+            n_src = self.off.numel() - 1
+            row = torch.repeat_interleave(torch.arange(n_src, device=dev), self.off[1:] - self.off[:-1])
+            key = (row << 32) | self.tgt.long()
+            del row
+            key, perm = torch.sort(key, stable=True)
+            self.tgt = self.tgt[perm].contiguous()
+            self.w = self.w[perm].contiguous()
+            self.delay = self.delay[perm].contiguous()
+            del perm
+            tiles = (self.n + 255) // 256
+            q = (torch.arange(n_src, device=dev)[:, None] << 32) | (torch.arange(tiles + 1, device=dev) * 256)[None, :]
+            self._seg = torch.searchsorted(key, q.reshape(-1)).reshape(n_src, tiles + 1).contiguous()
+            self._tiles = tiles
+        return self._seg, self._tiles
+
+    def _advance_persistent(self, n_steps: int, record: torch.Tensor | None):
+        """n_steps network steps in one cooperative launch (jit.cu hh_net)."""
+        lib = nat.load()
+        mode = 2 if (self.bg_mode == "philox" and self.bg_spec.rate_hz > 0) else 0
+        W = self.words_global
+        if record is not None:
+            if record.dtype != torch.int32 or not record.is_contiguous() or tuple(record.shape) < (n_steps, W):
+                raise UsageError("record must be a contiguous int32 [n_steps][words] tensor")
+            bits, rec = record, 1
+        else:
+            if getattr(self, "_pingpong", None) is None:
+                self._pingpong = torch.zeros((2, W), dtype=torch.int32, device=self.dev)
+            bits, rec = self._pingpong, 0
+        if getattr(self, "_barrier", None) is None:
+            self._barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        seg, tiles = self._tile_segments()
+        P = _table(self.params)
+        rc = lib.hhb_cortex_run(
+            C.byref(P), self.n, n_steps, self.t, self.depth, self.ring.data_ptr(), self.psp.data_ptr(), self.decay,
+            mode, self.lam.data_ptr(), self.bg_spec.w_mean, self.bg_spec.w_std, self.seed, self.lo,
+            float(1.0 / (1 << W_FRAC_BITS)), self.v.data_ptr(), self.g.data_ptr() if self.g.numel() else None,
+            self.n, bits.data_ptr(), rec, W, seg.data_ptr(), tiles, self.tgt.data_ptr(), self.w.data_ptr(),
+            self.delay.data_ptr(), self.first_bad.data_ptr(), self._barrier.data_ptr(),
+            D.ptr(getattr(self, "timing", None)), D.stream())
+        nat.check(rc, "hhb_cortex_run")
+        last = bits[n_steps - 1] if rec else bits[(n_steps - 1) & 1]
+        self.words[:W].copy_(last[:W])
+        self.t += n_steps
+        self.t_dev.fill_(self.t)
+        return record
+
     def advance(self, n_steps: int, steps_per_graph: int = 64, record: torch.Tensor | None = None):
-        """Advance n_steps by replaying a CUDA graph of `steps_per_graph`
-        network steps (input, HH step, exchange, delivery, tick): the per-step
-        host work of `step()` (~5 launches) becomes one graph launch per
-        steps_per_graph steps.  Results are bit-identical to `step()`.
-        record: optional int32 [n_steps][words_global] device buffer receiving
-        each step's global spike words.  Host-RNG background cannot be captured
-        (use step())."""
+        """Advance n_steps.  One rank with float32 neurons runs them in ONE
+        persistent cooperative kernel (hhb_cortex_run: the phases of each step
+        separated by grid barriers); otherwise a CUDA graph of
+        `steps_per_graph` network steps (input, HH step, exchange, delivery,
+        tick) is replayed, the per-step host work of `step()` (~5 launches)
+        becoming one graph launch per steps_per_graph steps.  Both are
+        bit-identical to `step()`.  record: optional int32
+        [n_steps][words_global] device buffer receiving each step's global
+        spike words.  Host-RNG background cannot run on the device (use
+        step())."""
         if self.bg_mode == "host":
             raise UsageError("advance(): the host background is drawn per step; use step()")
+        if n_steps > 0 and self.persistent_ok() and not getattr(self, "_no_persist", False):
+            try:
+                return self._advance_persistent(n_steps, record)
+            except NativeLibraryError as e:
+                if "hh_net" not in str(e) and "unavailable" not in str(e):
+                    raise
+                self._no_persist = True          # too many tiles / no cooperative launch: graph path
         self.t_dev.fill_(self.t)
         S = max(1, min(int(steps_per_graph), n_steps)) if n_steps > 0 else 1
         done = 0

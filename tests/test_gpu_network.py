@@ -196,3 +196,35 @@ def test_replicas_reproduce_single_network_runs(cuda):
         rows = torch.stack([single.step().clone() for _ in range(steps)])
         assert torch.equal(rows, rec[:, r, :rows.shape[1]]), r
         assert torch.equal(single.v, rep.v[r * rep.n_pad:r * rep.n_pad + topo.n_neurons])
+
+
+@pytest.mark.parametrize("cap", [None, "3"])
+def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap):
+    """advance() on one rank with float32 neurons runs the persistent
+    cooperative kernel (hhb_cortex_run); it must equal the graph path bit for
+    bit -- rasters, state, PSP and ring -- also when a step's spikes need
+    several delivery rounds (HHB_NET_CAP=3)."""
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    if cap:
+        monkeypatch.setenv("HHB_NET_CAP", cap)
+    a = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=11)
+    b = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=11)
+    assert a.persistent_ok()
+    steps = 300
+    ra = torch.empty((steps, a.words_global), dtype=torch.int32, device=cuda)
+    a.advance(steps, record=ra)
+    monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    assert not b.persistent_ok()
+    rb = torch.empty_like(ra)
+    b.advance(steps, steps_per_graph=64, record=rb)
+    assert ra.any() and int(ra.ne(0).sum()) > 50
+    assert torch.equal(ra, rb)
+    for x, y in ((a.v, b.v), (a.g, b.g), (a.psp, b.psp), (a.ring, b.ring)):
+        assert torch.equal(x, y)
+    # continuing: unrecorded (ping-pong) persistent run, then eager steps
+    monkeypatch.delenv("HHB_NET_GRAPH")
+    a.advance(37)
+    rows = torch.stack([b.step().clone() for _ in range(37)])
+    assert torch.equal(a.words[:a.words_global], rows[-1]) and torch.equal(a.v, b.v)
+    assert a.t == b.t == steps + 37
