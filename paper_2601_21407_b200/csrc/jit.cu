@@ -1299,6 +1299,7 @@ __device__ __forceinline__ i64 block_scan(i64 x, i64* s_w, i64& total) {
 }
 extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a) {
   __shared__ unsigned long long s_next[NET_THREADS];   // step t's delay-1 deliveries into the tile
+  __shared__ long long s_ahead[NET_THREADS];           // ring row t + 1 of the tile (cp.async prefetch)
   __shared__ int s_src[NET_CAP];
   __shared__ i64 s_beg[NET_CAP];
   __shared__ i64 s_pre[NET_CAP + 1];
@@ -1328,14 +1329,15 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
   // synapses, once step t starts: it is read (and cleared) then, off the
   // critical path, and the delay-1 deliveries of step t go to s_next instead.
   // int64 sums commute: the drained values are those of the per-step kernels.
-  long long ahead = 0;
+  // The row is copied asynchronously (cp.async: the thread does not wait for
+  // it) and cleared when consumed, one step later.
+  const int depth = int(a.depth);
+  int row = int(a.t0 % a.depth);                  // ring row of step t (32-bit modular counter)
+  // 16-byte pairs need an even row stride (and the tile's last pair whole)
+  const bool pair = (a.n & 1) == 0;
   s_next[tid] = 0ull;
-  if (on && a.steps > 0) {
-    long long* slot = a.ring + (a.t0 % a.depth) * a.n + i;
-    ahead = __ldcg(slot);
-    *slot = 0;
-  }
-  __syncthreads();
+  s_ahead[tid] = 0;
+  if (on && a.steps > 0) s_ahead[tid] = __ldcg(a.ring + i64(row) * a.n + i);
   unsigned long long* tm = a.timing ? a.timing + blockIdx.x * 4 : nullptr;
   for (i64 s = 0; s < a.steps; ++s) {
     const i64 t = a.t0 + s;
@@ -1343,12 +1345,19 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
     if (tm && tid == 0) tm[s * nb * 4 + 0] = gtimer();
     // ---- input + HH step of the tile (padding lanes run the step on a dummy state)
     float cur = 0.0f;
-    const long long arr = ahead + (long long)s_next[tid];
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();                                // (pairs: thread 2k copied entries 2k and 2k + 1)
+    const long long arr = (pair ? s_ahead[tid] : (on ? __ldcg(a.ring + i64(row) * a.n + i) : 0ll)) +
+                          (long long)s_next[tid];
     s_next[tid] = 0ull;                             // (next written after this block's barriers)
-    if (on && s + 1 < a.steps) {
-      long long* slot = a.ring + ((t + 1) % a.depth) * a.n + i;
-      ahead = __ldcg(slot);
-      *slot = 0;
+    const int row1 = row + 1 == depth ? 0 : row + 1;
+    if (on) a.ring[i64(row) * a.n + i] = 0;         // row t consumed
+    if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) {
+      // 16-byte L2-only async copy of this and the next neuron's entries
+      const unsigned sa = unsigned(__cvta_generic_to_shared(&s_ahead[tid]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(a.ring + i64(row1) * a.n + i)
+                   : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (on) {
       float x = __fadd_rn(__fmul_rn(psp, a.decay), __fmul_rn(float(double(arr)), a.w_scale));
@@ -1446,13 +1455,18 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
         for (int u = 0; u < NET_UNROLL; ++u) {
           if (d[u] == 0) continue;
           const unsigned long long wq = (unsigned long long)(long long)wv[u];
-          if (d[u] == 1) atomicAdd(&s_next[tg[u] - tlo], wq);
-          else atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + ((t + d[u]) % a.depth) * a.n + tg[u]), wq);
+          if (d[u] == 1) {
+            atomicAdd(&s_next[tg[u] - tlo], wq);
+          } else {
+            const int r = row + d[u] >= depth ? row + d[u] - depth : row + d[u];   // (t + d) % depth, d < depth
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + i64(r) * a.n + tg[u]), wq);
+          }
         }
       }
       __syncthreads();
     }
     if (tm && tid == 0) tm[s * nb * 4 + 3] = gtimer();
+    row = row1;
   }
   __syncthreads();
   if (on && a.steps > 0) {   // the last step's delay-1 deliveries back into the ring
