@@ -293,7 +293,8 @@ def c5_leg(torch, dev, steps=1000):
     """BASELINE config 5: recurrent HH cortex, build_network(scale=0.5, seed=0)
     (38,586 RS neurons, 71.2M synapses, delays up to 193 steps), REST_CONFIG,
     fp32, device Philox background; per step: ring drain + PSP + background,
-    HH step, bitmap all-gather (NCCL when N > 1), fixed-point delivery.
+    HH step, spike bitmap (all-gathered over NCCL when N > 1), fixed-point
+    delivery -- on one GPU all steps in one persistent cooperative kernel.
     One unit = one neuron-step of the whole network (strong scaling)."""
     import numpy as np
     import torch.distributed as dist
@@ -315,7 +316,7 @@ def c5_leg(torch, dev, steps=1000):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if graphs:
-        net.advance(steps)       # CUDA graphs of 64 network steps
+        net.advance(steps)       # one persistent cooperative kernel (graph replay if unavailable)
     else:
         for _ in range(steps):
             net.step()
@@ -329,9 +330,10 @@ def c5_leg(torch, dev, steps=1000):
     return {"value": topo.n_neurons * steps / (ms * 1e-3), "unit": UNIT, "ms_per_network_step": ms / steps,
             "steps": steps, "neurons": topo.n_neurons, "synapses": topo.n_synapses,
             "host_build_s": build_s,
-            "cuda_graph_steps": 64 if graphs else 0,
+            "path": ("persistent kernel" if net.persistent_ok() and not getattr(net, "_no_persist", False)
+                     else "cuda graphs of 64 steps") if graphs else "eager steps + NCCL all-gather",
             "config": "BASELINE config 5: recurrent HH cortex scale 0.5 (38,586 neurons, 71.2M synapses), "
-                      "REST_CONFIG, fp32, per-step spike-bitmap all-gather"}
+                      "REST_CONFIG, fp32, device Philox background"}
 
 
 def morph_leg(torch, dev):
