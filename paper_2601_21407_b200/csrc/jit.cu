@@ -1334,7 +1334,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
   const int depth = int(a.depth);
   int row = int(a.t0 % a.depth);                  // ring row of step t (32-bit modular counter)
   // 16-byte pairs need an even row stride (and the tile's last pair whole)
-  const bool pair = (a.n & 1) == 0;
+  const bool pair = (a.n & 1) == 0 && !NET_NOPAIR;
   s_next[tid] = 0ull;
   s_ahead[tid] = 0;
   if (on && a.steps > 0) s_ahead[tid] = __ldcg(a.ring + i64(row) * a.n + i);
@@ -1903,7 +1903,9 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
     const char* cap = getenv("HHB_NET_CAP");
     src += fmt("#define NET_CAP %d\n", cap && atoi(cap) > 0 && atoi(cap) < 2048 ? atoi(cap) : 2048);
     const char* nun = getenv("HHB_NET_UNROLL");
-    src += fmt("#define NET_UNROLL %d\n", nun && atoi(nun) > 0 ? atoi(nun) : 4);
+    const char* nop = getenv("HHB_NET_NOPAIR");   // tests: the odd-population (unpaired) ring path
+    src += fmt("#define NET_UNROLL %d\n#define NET_NOPAIR %d\n", nun && atoi(nun) > 0 ? atoi(nun) : 4,
+               nop && atoi(nop) > 0 ? 1 : 0);
     src += kNetKernel;
     return src;
   }
@@ -1964,7 +1966,7 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += bmb2 ? std::string("c") + bmb2 : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
-  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL"}) {
+  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR"}) {
     const char* x = getenv(e);
     k += x ? std::string("|") + e + x : "";
   }

@@ -1077,7 +1077,11 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
   if (splits < 1) splits = 1;
   if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
   if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
-  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  if (const char* e = getenv("HHB_GEMM_BN")) {   // experiments: force the tile width
+    const int f = atoi(e);
+    if ((f == 64 || f == 128 || f == 256) && f <= bn) bn = f;
+  }
   CUtensorMap ta, tb;
   int rc = make_map(&ta, tf32, A, M, K, lda, BM);
   if (rc) return rc;

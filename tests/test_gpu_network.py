@@ -198,8 +198,8 @@ def test_replicas_reproduce_single_network_runs(cuda):
         assert torch.equal(single.v, rep.v[r * rep.n_pad:r * rep.n_pad + topo.n_neurons])
 
 
-@pytest.mark.parametrize("cap", [None, "3"])
-def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap):
+@pytest.mark.parametrize("cap,nopair", [(None, False), ("3", False), (None, True)])
+def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap, nopair):
     """advance() on one rank with float32 neurons runs the persistent
     cooperative kernel (hhb_cortex_run); it must equal the graph path bit for
     bit -- rasters, state, PSP and ring -- also when a step's spikes need
@@ -208,6 +208,8 @@ def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap):
     cfg = N.REST_CONFIG
     if cap:
         monkeypatch.setenv("HHB_NET_CAP", cap)
+    if nopair:   # the ring path of odd populations (no 16-byte pairs)
+        monkeypatch.setenv("HHB_NET_NOPAIR", "1")
     a = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=11)
     b = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=11)
     assert a.persistent_ok()
