@@ -1595,7 +1595,7 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #pragma unroll
       for (int g = 0; g < NG; ++g) cpa<VEC>(r + (1 + g) * BWD_THREADS, src + goff[g]);
       cpa<VEC>(r + (NG + 1) * BWD_THREADS, iq);
-      if (BF_SV) cpa<VEC>(r + (NG + 2) * BWD_THREADS, vq);
+      if (BF_SV && !BF_SPREV) cpa<VEC>(r + (NG + 2) * BWD_THREADS, vq);
       if (BF_SS) cpa<VEC>(r + (NG + 3) * BWD_THREADS, sq);
     };
     auto advance = [&]() {
@@ -1617,6 +1617,12 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
     unsigned short* dhb = (BF_SPLIT && on[0]) ? a.di_hi + (hi - 1) * a.dh_ld + scol : nullptr;
     unsigned short* dlb = (BF_SPLIT && on[0]) ? a.di_lo + (hi - 1) * a.dh_ld + scol : nullptr;
     int rslot = 0;
+    // BF_SPREV: the seed of step t is svs * V'(t), and V'(t) is the v of state
+    // t + 1 -- loaded by the previous (later) step of this reverse sweep, so
+    // only the final state's v is read here
+    float vprev[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) vprev[j] = (BF_SPREV && on[j]) ? a.seed_v[(hi - 1) * a.sv_ld + ii[j]] : 0.0f;
     for (i64 t = hi - 1; t >= lo; --t) {
       if (tn >= lo) issue();
       cpa_commit();
@@ -1632,8 +1638,13 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) p[j][g] = r[(1 + g) * BWD_THREADS + j];
         cur[j] = r[(NG + 1) * BWD_THREADS + j];
-        if (BF_SV) d_v[j] = BF_SVS ? __fmaf_rn(svs, r[(NG + 2) * BWD_THREADS + j], d_v[j])
-                                   : __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
+        if (BF_SPREV) {
+          d_v[j] = __fmaf_rn(svs, vprev[j], d_v[j]);
+          vprev[j] = v[j];
+        } else if (BF_SV) {
+          d_v[j] = BF_SVS ? __fmaf_rn(svs, r[(NG + 2) * BWD_THREADS + j], d_v[j])
+                          : __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
+        }
         ds[j] = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
 #if HAS_MERGED
         reg = reg && regular(v[j]);
@@ -1738,7 +1749,7 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2
 // otherwise the forward module specialised on FF_* (kind = -1 - flags).
 // bwd_flags < 0: the forward module; >= 0: the backward module specialised
 // on BF_* (which optional streams the launch has); -2: both, for inspection
-enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32, BF_SVS = 64 };
+enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32, BF_SVS = 64, BF_SPREV = 128 };
 enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16, FF_L2 = 32 };
 constexpr int kInspect = -1000;
 constexpr int kNet = -2000;   // the persistent network kernel (hh_net)
@@ -1920,9 +1931,9 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
   if (bwd_flags >= 0 || bwd_flags == kInspect) {
     const int f = bwd_flags < 0 ? (BF_SV | BF_DI) : bwd_flags;
     src += fmt("#define BF_SV %d\n#define BF_SS %d\n#define BF_DI %d\n#define BF_SPLIT %d\n#define BF_SUM %d\n"
-               "#define BF_K1 %d\n#define BF_SVS %d\n",
+               "#define BF_K1 %d\n#define BF_SVS %d\n#define BF_SPREV %d\n",
                (f & BF_SV) ? 1 : 0, (f & BF_SS) ? 1 : 0, (f & BF_DI) ? 1 : 0, (f & BF_SPLIT) ? 1 : 0,
-               (f & BF_SUM) ? 1 : 0, (f & BF_K1) ? 1 : 0, (f & BF_SVS) ? 1 : 0);
+               (f & BF_SUM) ? 1 : 0, (f & BF_K1) ? 1 : 0, (f & BF_SVS) ? 1 : 0, (f & BF_SPREV) ? 1 : 0);
     src += kBwdKernel;
   }
   return src;
@@ -2074,7 +2085,12 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
   using namespace jit;
   const int flags = (a.seed_v ? BF_SV : 0) | (a.seed_s ? BF_SS : 0) | (a.d_i ? BF_DI : 0) |
                     (a.di_hi ? BF_SPLIT : 0) | (a.di_sum ? BF_SUM : 0) | (a.ck_every == 1 ? BF_K1 : 0) |
-                    (a.seed_v && a.sv_scale ? BF_SVS : 0);
+                    (a.seed_v && a.sv_scale ? BF_SVS : 0) |
+                    // the seed is the v-plane of the next checkpoint slot (fused MSE(V, 0) of the layer)
+                    (a.seed_v && a.sv_scale && a.ck_every == 1 && !getenv("HHB_JIT_NO_SPREV") &&
+                             a.seed_v == a.ckpt + (1 + P->n_gates) * a.ck_ld && a.sv_ld == (1 + P->n_gates) * a.ck_ld
+                         ? BF_SPREV
+                         : 0);
   jit::Module* m = jit::get_module(P, flags);
   if (!m) return false;
   const int64_t blocks = bwd_blocks(a.n);
