@@ -356,7 +356,7 @@ def morph_leg(torch, dev):
     B, T = 262144, 400
     g = torch.Generator(device=dev).manual_seed(0)
     i = (torch.rand((T, 7, B), device=dev, generator=g) < 0.05).float() * 36.0
-    for _ in range(2):
+    for _ in range(3):
         M.simulate_morphology(graph, i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -601,7 +601,14 @@ def main():
     extras = {}
 
     def leg(name, fn):
-        # a failing secondary leg is reported in the line, not fatal to it
+        # a failing secondary leg is reported in the line, not fatal to it;
+        # each leg starts from an emptied allocator cache (the previous legs'
+        # graph pools and temporaries would otherwise make its first
+        # allocations pay for fragmentation)
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         try:
             extras[name] = fn()
         except Exception as e:  # noqa: BLE001
