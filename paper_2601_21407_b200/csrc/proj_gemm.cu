@@ -30,6 +30,14 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int kThreads = 192;
+// CTA-pair kernel: producer warp, MMA warp, EPI2_WARPS epilogue warps
+#ifndef EPI2_WARPS
+#define EPI2_WARPS 8
+#endif
+#ifndef EPI2_BUFS
+#define EPI2_BUFS 1
+#endif
+constexpr int kThreads2 = 64 + 32 * EPI2_WARPS;
 
 struct Args {
   int64_t M, N, K;
@@ -539,8 +547,9 @@ struct P2Cfg {
   static constexpr uint32_t kStageA = BM * 128;             // this CTA's 128 rows x 64 k
   static constexpr uint32_t kStageB = (BN / 2) * 128;       // half of B
   static constexpr uint32_t kStage = kStageA * (DUAL ? 2 : 1) + kStageB;
-  static constexpr int kStgBufs = 2;                          // TMA-store staging buffers per epilogue warp (4 measured slower: fewer stages)
-  static constexpr uint32_t kStaging = 4 * kStgBufs * 32 * 32 * 4;
+  static constexpr int kEpiWarps = EPI2_WARPS;                // 2 per TMEM lane quadrant, each half of the columns
+  static constexpr int kStgBufs = EPI2_BUFS;                  // TMA-store staging buffers per epilogue warp
+  static constexpr uint32_t kStaging = kEpiWarps * kStgBufs * 32 * 32 * 4;
   static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 8 ? 8 : int((225 * 1024 - kStaging) / kStage);
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 256;
 };
@@ -585,7 +594,7 @@ __device__ __forceinline__ void umma2_commit(uint64_t* bar) {
 }
 
 template <int BN, bool A_MN, bool B_MN, bool DUAL>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     k_umma_gemm_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                     const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap td, const PArgs args) {
   using C = P2Cfg<BN, DUAL>;
@@ -617,7 +626,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);
+      mbar_init(&tempty[b], 2 * C::kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -702,8 +711,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         umma2_commit(&tfull[b]);
       }
     }
-  } else {  // epilogue warps 2..5 of both CTAs: this CTA's 128 rows
+  } else {  // epilogue warps of both CTAs: this CTA's 128 rows; warp w reads TMEM lane quadrant w % 4
     const int q = warp & 3;
+    const int half = C::kEpiWarps == 8 ? (warp - 2) >> 2 : 0;    // which half of the tile's columns
+    constexpr int kCols = C::kEpiWarps == 8 ? BN / 2 : BN;
     float* my_stg = stg + (warp - 2) * C::kStgBufs * 1024;
     int local = 0, nstore = 0;
     for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
@@ -717,7 +728,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int32_t row0 = int32_t(m0 + q * 32);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
         if (n0 + c0 >= args.N) break;
         uint32_t rr[32];
         if (any_k) {
@@ -1021,7 +1032,7 @@ static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUten
   if (max_pairs == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(kThreads2, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -1039,7 +1050,7 @@ static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUten
   int pairs = max_pairs;
   if (a.tiles < pairs) pairs = a.tiles;
   if (getenv("HHB_GEMM_PAIRS_DEBUG")) fprintf(stderr, "k_umma_gemm_2sm: %d co-resident pairs\n", max_pairs);
-  k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL><<<2 * pairs, kThreads, smem, st>>>(ta, ta2, tb, td, a);
+  k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL><<<2 * pairs, kThreads2, smem, st>>>(ta, ta2, tb, td, a);
   return cuda_check("k_umma_gemm_2sm launch");
 }
 
