@@ -191,3 +191,19 @@ def test_fit_raises_in_reference_order(cuda):
                           task.teacher.kernel)
     with pytest.raises(NumericalOverflowError):
         L.fit(huge, task, L.TrainConfig(epochs=1))
+
+
+def test_fit_edge_cases(cuda):
+    """epochs=0 leaves the parameters (as numpy) untouched; device inputs to
+    ReadoutModel give device outputs; the cosine schedule ends at lr 0."""
+    g, task = _readout_task()
+    st = L.ReadoutModel(L.DenseLayer(g["student_w0"].copy(), np.zeros(1)), 1.0, 0.0, task.teacher.neuron,
+                        task.teacher.kernel)
+    assert L.fit(st, task, L.TrainConfig(epochs=0)) == []
+    assert np.array_equal(st.dense.weights, g["student_w0"]) and st.scale_w == 1.0
+    x = torch.as_tensor(g["train_inputs"], device=cuda)
+    pred, v = st.forward(st.filter_inputs(x))
+    assert pred.is_cuda and v.is_cuda and tuple(pred.shape) == g["train_targets"].shape
+    assert L.cosine_lr(1.0, 10, 10) == pytest.approx(0.0, abs=1e-15)
+    h = L.fit(st, task, L.TrainConfig(epochs=2, lr=1e-2, cosine=False))
+    assert len(h) == 2 and all(np.isfinite(r[1]) and np.isfinite(r[2]) for r in h)
