@@ -1351,6 +1351,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
                           (long long)s_next[tid];
     s_next[tid] = 0ull;                             // (next written after this block's barriers)
     const int row1 = row + 1 == depth ? 0 : row + 1;
+    __syncwarp();                                   // lane 2k+1 has read s_ahead before lane 2k refills it
     if (on) a.ring[i64(row) * a.n + i] = 0;         // row t consumed
     if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) {
       // 16-byte L2-only async copy of this and the next neuron's entries
