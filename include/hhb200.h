@@ -400,6 +400,16 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
                    const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
                    uint32_t* barrier, uint64_t* timing, void* stream);
 
+/* Spike raster -> event list (SpikeRecord, cortex.py:422-438):
+ * bits [steps][words] (bit i of word w = neuron 32 w + i; neurons >= n ignored).
+ * hhb_spike_event_counts writes each step's event count; with offsets = the
+ * exclusive scan of the counts, hhb_spike_events writes the events sorted by
+ * (step, neuron) -- NumPy nonzero's order over the unpacked raster. */
+int hhb_spike_event_counts(int64_t steps, int64_t words, const uint32_t* bits, int64_t n, int64_t* counts,
+                           void* stream);
+int hhb_spike_events(int64_t steps, int64_t words, const uint32_t* bits, int64_t n, const int64_t* offsets,
+                     int32_t* out_step, int32_t* out_neuron, void* stream);
+
 int hhb_cortex_tick(int64_t* t_dev, void* stream);
 /* hhb_spike_deliver_dev in two kernels for the sparse per-step case: one
  * block lists the spiking sources (ascending) with the prefix of their row

@@ -125,6 +125,8 @@ SIGNATURES = {
                                     C.c_uint64, _i64, _vp, _vp, _dbl, _vp]),
     "hhb_spike_deliver_dev": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp]),
     "hhb_cortex_tick": (_i32, [_vp, _vp]),
+    "hhb_spike_event_counts": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp]),
+    "hhb_spike_events": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hhb_cortex_run": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
                               C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),

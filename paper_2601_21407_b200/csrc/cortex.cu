@@ -125,6 +125,67 @@ __global__ void __launch_bounds__(128) k_spike_deliver(int64_t words, const uint
 
 __global__ void k_tick(long long* t) { *t += 1; }
 
+// Spike bitmap [T][words] (bit i of word w = neuron 32w + i, neurons >= n
+// ignored) -> event list sorted by (step, neuron), the order of NumPy's
+// nonzero over the unpacked raster (SpikeRecord, cortex.py:422-438).  Pass 1
+// counts each row's events; the caller scans the counts; pass 2 writes each
+// row's events at its offset (one block per row, block-wide scan of the
+// per-thread word counts).
+constexpr int kEvThreads = 256;
+__device__ __forceinline__ uint32_t ev_word(const uint32_t* row, int64_t w, int64_t n) {
+  uint32_t x = row[w];
+  const int64_t left = n - w * 32;
+  if (left < 32) x &= left <= 0 ? 0u : ((1u << left) - 1u);
+  return x;
+}
+__global__ void __launch_bounds__(kEvThreads) k_event_counts(int64_t words, const uint32_t* bits, int64_t n,
+                                                             int64_t* counts) {
+  const uint32_t* row = bits + int64_t(blockIdx.x) * words;
+  int c = 0;
+  for (int64_t w = threadIdx.x; w < words; w += kEvThreads) c += __popc(ev_word(row, w, n));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ int part[kEvThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t s = 0;
+    for (int k = 0; k < kEvThreads / 32; ++k) s += part[k];
+    counts[blockIdx.x] = s;
+  }
+}
+__global__ void __launch_bounds__(kEvThreads) k_event_write(int64_t words, const uint32_t* bits, int64_t n,
+                                                            const int64_t* offsets, int32_t* out_t,
+                                                            int32_t* out_id) {
+  const int64_t t = blockIdx.x;
+  const uint32_t* row = bits + t * words;
+  // contiguous word range per thread keeps the output ascending
+  const int64_t per = (words + kEvThreads - 1) / kEvThreads;
+  const int64_t w0 = threadIdx.x * per, w1 = min(words, w0 + per);
+  int c = 0;
+  for (int64_t w = w0; w < w1; ++w) c += __popc(ev_word(row, w, n));
+  __shared__ int scan[kEvThreads];
+  scan[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < kEvThreads; o <<= 1) {
+    const int v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t k = offsets[t] + scan[threadIdx.x] - c;
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t x = ev_word(row, w, n);
+    while (x) {
+      const int b = __ffs(int(x)) - 1;
+      x &= x - 1;
+      out_t[k] = int32_t(t);
+      out_id[k] = int32_t(w * 32 + b);
+      ++k;
+    }
+  }
+}
+
 // Flattened delivery for the latency-bound per-step case (a few dozen spikes
 // out of ~10^5 sources, ~10^3 synapses each): k_spike_compact (one block)
 // lists the spiking sources of the bitmap in ascending order with the
@@ -390,6 +451,26 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
   if (!jit_cortex_run(params, a, static_cast<cudaStream_t>(stream), rc))
     return fail(HHB_ENOTSUP, std::string("persistent network kernel unavailable: ") + jit_status());
   return rc;
+}
+
+int hhb_spike_event_counts(int64_t steps, int64_t words, const uint32_t* bits, int64_t n, int64_t* counts,
+                           void* stream) {
+  if (steps < 0 || words < 0 || n < 0 || n > words * 32) return fail(HHB_EINVAL, "spike_event_counts: bad sizes");
+  if (steps == 0) return HHB_OK;
+  if (!bits || !counts) return fail(HHB_EINVAL, "spike_event_counts: NULL pointer");
+  cortex::k_event_counts<<<unsigned(steps), cortex::kEvThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      words, bits, n, counts);
+  return cuda_check("k_event_counts launch");
+}
+
+int hhb_spike_events(int64_t steps, int64_t words, const uint32_t* bits, int64_t n, const int64_t* offsets,
+                     int32_t* out_step, int32_t* out_neuron, void* stream) {
+  if (steps < 0 || words < 0 || n < 0 || n > words * 32) return fail(HHB_EINVAL, "spike_events: bad sizes");
+  if (steps == 0) return HHB_OK;
+  if (!bits || !offsets || !out_step || !out_neuron) return fail(HHB_EINVAL, "spike_events: NULL pointer");
+  cortex::k_event_write<<<unsigned(steps), cortex::kEvThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      words, bits, n, offsets, out_step, out_neuron);
+  return cuda_check("k_event_write launch");
 }
 
 int hhb_cortex_tick(int64_t* t_dev, void* stream) {

@@ -532,10 +532,10 @@ class CortexNetwork:
         _raise_if_bad(self.first_bad)
         if not record:
             return None
-        bits = torch.stack(rows).cpu().numpy().view(np.uint32)
-        t_idx, n_idx = np.nonzero(np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")
-                                  [:, :self.n_global])
-        return (t_idx + 1 + (self.t - n_steps)) * self.config.dt, n_idx.astype(np.int64)
+        if n_steps == 0:
+            return np.zeros(0), np.zeros(0, dtype=np.int64)
+        t_idx, n_idx = spike_events(torch.stack(rows).contiguous(), self.n_global)
+        return (t_idx + 1 + (self.t - n_steps)) * self.config.dt, n_idx
 
 
 # ---------------------------------------------------------------------------
@@ -666,9 +666,26 @@ def run_network(topo: NetworkTopology, config: CortexConfig, duration_ms: float,
                     extra = extra[net.lo:net.hi]
             rows[t].copy_(net.step(extra))
     _raise_if_bad(net.first_bad)
-    bits = rows.cpu().numpy().view(np.uint32)
-    t_idx, n_idx = np.nonzero(np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")[:, :topo.n_neurons])
-    return SpikeRecord((t_idx + 1) * config.dt, n_idx.astype(np.int64), duration_ms, warmup_ms, topo)
+    t_idx, n_idx = spike_events(rows, topo.n_neurons)
+    return SpikeRecord((t_idx + 1) * config.dt, n_idx, duration_ms, warmup_ms, topo)
+
+
+def spike_events(rows: torch.Tensor, n: int):
+    """Device spike raster (int32 [steps][words]) -> (step, neuron) event
+    arrays on the host, sorted by step then neuron (hhb_spike_event_counts /
+    hhb_spike_events): only the events cross PCIe, not the raster."""
+    lib = nat.load()
+    T, W = rows.shape
+    counts = torch.empty(max(1, T), dtype=torch.int64, device=rows.device)
+    nat.check(lib.hhb_spike_event_counts(T, W, rows.data_ptr(), n, counts.data_ptr(), D.stream()), "spike events")
+    ends = torch.cumsum(counts[:T], 0)
+    total = int(ends[-1].item()) if T else 0
+    offsets = ends - counts[:T]
+    st = torch.empty(max(1, total), dtype=torch.int32, device=rows.device)
+    nid = torch.empty(max(1, total), dtype=torch.int32, device=rows.device)
+    nat.check(lib.hhb_spike_events(T, W, rows.data_ptr(), n, offsets.data_ptr(), st.data_ptr(), nid.data_ptr(),
+                                   D.stream()), "spike events")
+    return st[:total].cpu().numpy().astype(np.int64), nid[:total].cpu().numpy().astype(np.int64)
 
 
 def rest_state_run(duration_ms: float, scale: float, seed: int, config: CortexConfig | None = None,

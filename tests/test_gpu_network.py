@@ -230,3 +230,20 @@ def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap, nopair):
     rows = torch.stack([b.step().clone() for _ in range(37)])
     assert torch.equal(a.words[:a.words_global], rows[-1]) and torch.equal(a.v, b.v)
     assert a.t == b.t == steps + 37
+
+
+def test_spike_events_match_numpy_unpack(cuda):
+    """hhb_spike_event_counts / hhb_spike_events == NumPy nonzero over the
+    unpacked raster (order included), with a partial last word and empty rows."""
+    rng = np.random.default_rng(4)
+    T, n = 57, 1000
+    W = (n + 31) // 32
+    raw = (rng.random((T, W * 32)) < 0.03)
+    raw[5] = False
+    raw[:, n:] = True                      # bits past n must be ignored
+    bits = np.packbits(raw, axis=1, bitorder="little").view(np.int32)
+    st, nid = N.spike_events(torch.from_numpy(bits.copy()).to(cuda), n)
+    t_ref, n_ref = np.nonzero(raw[:, :n])
+    assert np.array_equal(st, t_ref) and np.array_equal(nid, n_ref)
+    e_t, e_n = N.spike_events(torch.zeros((3, W), dtype=torch.int32, device=cuda), n)
+    assert e_t.size == 0 and e_n.size == 0
