@@ -439,7 +439,7 @@ def c4_leg(torch, dev):
     import torch.distributed as dist
     world = dist.get_world_size() if dist.is_initialized() else 1
     # capturable Adam keeps its step counters on the device (CUDA-graph safe)
-    opt = torch.optim.Adam(net.parameters(), lr=5e-4, capturable=(world == 1))
+    opt = torch.optim.Adam(net.parameters(), lr=5e-4, capturable=(world == 1), fused=True)
     g = torch.Generator(device=dev).manual_seed(1)
     x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() \
         + 0.1 * torch.randn((T, B, 784), device=dev, generator=g)
