@@ -397,3 +397,21 @@ def test_neuron_shards_equal_one_population(cuda):
         sh.advance(stim, T, on_chunk=lambda t, v, s: vs.append(v.clone()))
         parts.append(torch.cat(vs))
     assert torch.equal(torch.cat(vw), torch.cat(parts, dim=1))
+
+
+def test_fp32_parity_config2_scale(cuda):
+    """The bench path (float32 merged kernel) against the float64 kernel on the
+    config-2 stimulus at 1M neurons x 2,000 steps (tools/parity_fullscale.py;
+    the 10M x 10,000 run is in profiles/r1b_parity_fullscale.md)."""
+    import json
+    import subprocess
+    import sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tools/parity_fullscale.py", "--neurons", "1000000", "--steps", "2000"],
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["spikes_fp64_total"] > 10 ** 6
+    assert r["count_equal_frac"] >= 0.9999 and r["count_diff_max"] <= 1
+    assert r["spiked_in_one_run_only"] == 0 and r["first_spike_pm1_frac_of_both"] == 1.0
+    assert r["prespike_v_violations"] <= 1e-5 * r["prespike_v_checks"]
