@@ -147,3 +147,20 @@ def test_layer_output_selection(cuda):
         assert lyr.weight.grad is not None and torch.isfinite(lyr.weight.grad).all()
     with pytest.raises(Exception):
         HHLayer(4, 8, device=cuda, outputs="neither")
+
+
+def test_config3_full_shape_gradients_within_contract(cuda):
+    """The benchmarked config-3 step (fused MSE) at its full shape against the
+    float64 kernels (tools/parity_c3.py, profiles/r1b_parity_c3.md)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tools/parity_c3.py"], cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("dW", "db", "dX", "d_c_m", "d_g_max"):
+        assert r[k] < 1e-3, (k, r[k])
+    assert r["loss_rel"] < 1e-5
