@@ -190,6 +190,9 @@ def main():
     # statistical target of the device-background runs
     rec_r = cortex.rest_state_run(1200.0, 0.1, 0, warmup_ms=200.0)
     ka["rest_rates"] = np.array([rec_r.pop_rate(p.name) for p in rec_r.topo.populations])
+    # the step-level background draw (cortex.py:225-232)
+    ka["bg_lam"] = np.linspace(0.0, 3.0, 40)
+    ka["bg_sample"] = cortex.background_sample(ka["bg_lam"], 0.11, 0.02, 40, np.random.default_rng(21))
     np.savez_compressed(os.path.join(OUT, "known_answers.npz"), **ka)
 
     # -- forward traces (dynamics.simulate / reference.naive_simulate) -------

@@ -539,6 +539,126 @@ class CortexNetwork:
 
 
 # ---------------------------------------------------------------------------
+# the reference's step-level API (cortex.py:225-310) over the device network
+# ---------------------------------------------------------------------------
+
+def background_sample(lam_eff, mu: float, sigma: float, count, rng: np.random.Generator):
+    """Compound-Poisson draw N mu + sigma sqrt(N) z, N ~ Poisson(lam_eff),
+    with the reference's RNG call sequence (cortex.py:225-232): host NumPy, so a
+    seeded run reproduces the reference's stream draw for draw."""
+    n = rng.poisson(lam_eff, size=count)
+    out = n * mu
+    if sigma > 0:
+        out = out + sigma * np.sqrt(n) * rng.standard_normal(count)
+    return out
+
+
+class SpikeBuffer:
+    """Ring of per-step pending synaptic currents (cortex.py:238-256), on the
+    device in int64 fixed point (weight quantum 2^-W_FRAC_BITS): sums commute,
+    so any enqueue order gives the same ring.  `ring` (float64 numpy) is a
+    read-only snapshot."""
+
+    def __init__(self, depth: int, n_neurons: int, device=None, _ring: torch.Tensor | None = None):
+        if depth < 1:
+            raise ConfigurationError("ring depth must be >= 1")
+        self.depth = depth
+        dev = device or D.require_cuda()
+        self._ring = _ring if _ring is not None else torch.zeros((depth, max(1, n_neurons)), dtype=torch.int64,
+                                                                 device=dev)
+        self.n = n_neurons
+
+    @property
+    def ring(self) -> np.ndarray:
+        return self._ring[:, :self.n].cpu().numpy().astype(np.float64) / (1 << W_FRAC_BITS)
+
+    def enqueue(self, t: int, targets, weights, delays):
+        dev = self._ring.device
+        tg = torch.as_tensor(np.asarray(targets, dtype=np.int64), device=dev)
+        slots = (t + torch.as_tensor(np.asarray(delays, dtype=np.int64), device=dev)) % self.depth
+        wq = torch.as_tensor(quantise_weights(np.asarray(weights, dtype=np.float64)).astype(np.int64), device=dev)
+        self._ring.view(-1).index_add_(0, slots * self._ring.shape[1] + tg, wq)
+
+    def drain(self, t: int) -> np.ndarray:
+        row = self._ring[t % self.depth]
+        arrived = row[:self.n].cpu().numpy().astype(np.float64) / (1 << W_FRAC_BITS)
+        row.zero_()
+        return arrived
+
+
+class _OneShotBackground:
+    """HostBackground stand-in feeding CortexNetwork one pre-drawn sample."""
+
+    def __init__(self):
+        self.value = None
+
+    def sample(self):
+        return self.value
+
+
+class NetworkState:
+    """The reference's NetworkState (cortex.py:259-264) backed by a device
+    CortexNetwork: `neuron`, `psp` are host snapshots, `buffer` a view of the
+    device ring, `t` the step counter."""
+
+    def __init__(self, engine: "CortexNetwork"):
+        self._engine = engine
+
+    @property
+    def t(self) -> int:
+        return self._engine.t
+
+    @property
+    def neuron(self):
+        from .dynamics import NeuronState
+        e = self._engine
+        return NeuronState(D.to_host(e.v, np.float64), D.to_host(e.g, np.float64))
+
+    @property
+    def psp(self) -> np.ndarray:
+        return D.to_host(self._engine.psp, np.float64)
+
+    @property
+    def buffer(self) -> SpikeBuffer:
+        e = self._engine
+        return SpikeBuffer(e.depth, e.n, _ring=e.ring)
+
+
+def init_network_state(topo: NetworkTopology, config: CortexConfig, device=None,
+                       dtype=np.float64) -> NetworkState:
+    """Rest state, zero PSP, empty ring (cortex.py:267-270); float64 neurons
+    like the reference unless dtype says otherwise."""
+    eng = CortexNetwork(topo, config, device=device, dtype=dtype, background="host", host_bg=_OneShotBackground())
+    return NetworkState(eng)
+
+
+def step_network(net: NetworkState, topo: NetworkTopology, background: BackgroundSpec | None,
+                 config: CortexConfig, rng: np.random.Generator, params=None, workspace=None,
+                 extra_current=0.0) -> np.ndarray:
+    """One network step (cortex.py:273-310): drain the ring, decay the PSP,
+    add the background (drawn from `rng` exactly as the reference does), the
+    HH step, and the delivery of the new spikes -- on the device.  Returns the
+    step's spikes (bool, n).  `params` replaces the neuron set of the state's
+    config (the reference passes config.resolved_neuron()); `workspace` is
+    accepted for signature compatibility (the device step needs none)."""
+    eng = net._engine
+    if params is not None:
+        eng.params = params.with_(dtype=eng.dtype)
+    n = topo.n_neurons
+    if background is not None and background.rate_hz > 0:
+        lam = background_lambda(topo, background, config.dt)
+        eng.host_bg.value = background_sample(lam, background.w_mean, background.w_std, n, rng)
+    else:
+        eng.host_bg.value = np.zeros(n)
+    extra = None
+    if not (np.isscalar(extra_current) and extra_current == 0.0):
+        extra = np.broadcast_to(np.asarray(extra_current, dtype=np.float64), (n,))
+    words = eng.step(extra)
+    bits = words[:eng.words_global].cpu().numpy().view(np.uint8)
+    return np.unpackbits(bits, bitorder="little")[:n].astype(bool)
+
+
+# ---------------------------------------------------------------------------
 # run_network / SpikeRecord (cortex.py:319-464): the reference's driver and
 # its output record, on the device network
 # ---------------------------------------------------------------------------

@@ -247,3 +247,35 @@ def test_spike_events_match_numpy_unpack(cuda):
     assert np.array_equal(st, t_ref) and np.array_equal(nid, n_ref)
     e_t, e_n = N.spike_events(torch.zeros((3, W), dtype=torch.int32, device=cuda), n)
     assert e_t.size == 0 and e_n.size == 0
+
+
+def test_step_level_api_reproduces_reference_raster(cuda):
+    """init_network_state / step_network / background_sample driven exactly as
+    the reference's run_network loop (cortex.py:379-438) reproduce its raster."""
+    g, topo = _small()
+    cfg = N.REST_CONFIG
+    rng = np.random.default_rng(int(g["run_seed"]))
+    params = cfg.resolved_neuron()
+    bg = N.make_background(cfg)
+    net = N.init_network_state(topo, cfg, device=cuda)
+    steps = int(round(float(g["duration_ms"]) / cfg.dt))
+    times, ids = [], []
+    for t in range(steps):
+        spikes = N.step_network(net, topo, bg, cfg, rng, params)
+        nz = np.flatnonzero(spikes)
+        times.append(np.full(nz.size, (t + 1) * cfg.dt))
+        ids.append(nz)
+    t_all, i_all = np.concatenate(times), np.concatenate(ids)
+    assert np.array_equal(i_all, g["spike_id"]) and np.allclose(t_all, g["spike_t"])
+    assert net.t == steps and net.neuron.v.shape == (topo.n_neurons,) and net.psp.shape == (topo.n_neurons,)
+
+
+def test_spike_buffer_matches_reference_semantics(cuda):
+    """SpikeBuffer.enqueue / drain (cortex.py:238-256) in fixed point."""
+    buf = N.SpikeBuffer(5, 7, device=cuda)
+    buf.enqueue(3, np.array([1, 1, 6]), np.array([0.5, 0.25, -1.0]), np.array([1, 1, 4]))
+    assert np.allclose(buf.ring[4], [0, 0.75, 0, 0, 0, 0, 0]) and np.allclose(buf.ring[2, 6], -1.0)
+    assert np.allclose(buf.drain(4), [0, 0.75, 0, 0, 0, 0, 0]) and not buf.ring[4].any()
+    assert np.allclose(buf.drain(7)[6], -1.0)
+    with pytest.raises(Exception):
+        N.SpikeBuffer(0, 3, device=cuda)

@@ -134,3 +134,11 @@ def test_sharded_exchange_gloo_world2_equals_single_rank(tmp_path):
     t1, i1 = _oracle_run(topo, N.REST_CONFIG, steps, int(g["run_seed"]))
     assert np.array_equal(i2.astype(np.int64), i1) and np.allclose(t2, t1)
     assert i1.size > 100   # recurrent activity crosses the shard boundary
+
+
+def test_background_sample_matches_reference_draws():
+    """network.background_sample reproduces the reference's RNG call sequence."""
+    from conftest import golden
+    ka = golden("known_answers")
+    out = N.background_sample(ka["bg_lam"], 0.11, 0.02, 40, np.random.default_rng(21))
+    assert np.array_equal(out, ka["bg_sample"])
