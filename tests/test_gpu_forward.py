@@ -415,3 +415,22 @@ def test_fp32_parity_config2_scale(cuda):
     assert r["count_equal_frac"] >= 0.9999 and r["count_diff_max"] <= 1
     assert r["spiked_in_one_run_only"] == 0 and r["first_spike_pm1_frac_of_both"] == 1.0
     assert r["prespike_v_violations"] <= 1e-5 * r["prespike_v_checks"]
+
+
+def test_naive_reference_module_matches_fused(cuda):
+    """paper_2601_21407_b200.reference (the multi-pass naive step of
+    hhengine/reference.py) against the fused float64 simulate and the
+    reference's own traces."""
+    from paper_2601_21407_b200 import reference as R
+    g = golden("fwd_squid_ramp")
+    p = DF.squid_axon_params(dt=0.01)
+    T = 400
+    i = np.asarray(g["i"])[None, :].repeat(T, 0) if np.ndim(g["i"]) == 1 else np.asarray(g["i"])[:T]
+    tr_n = R.naive_simulate(p, i)
+    tr_f = Dy.simulate(p, i)
+    assert tr_n.v_series.dtype == np.float64 and tr_n.spike_series.dtype == bool
+    assert np.allclose(tr_n.v_series, tr_f.v_series, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(tr_n.spike_series, tr_f.spike_series)
+    assert np.allclose(tr_n.v_series, np.asarray(g["v"])[:T], rtol=1e-9, atol=1e-9)
+    s1, sp = R.naive_hh_step(Dy.init_state(p, (3,)), np.array([0.0, 5.0, 50.0]), p)
+    assert s1.v.shape == (3,) and sp.dtype == bool
