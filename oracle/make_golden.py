@@ -342,6 +342,19 @@ def main():
         head_target=topo.syn_target[:200], head_weight=topo.syn_weight[:200],
         head_delay=topo.syn_delay[:200], offsets=topo.syn_offsets,
         spike_t=rec.times_ms, spike_id=rec.neuron_ids)
+    # the reference's public API per module (names the drop-in must provide)
+    import importlib
+    import json
+    api = {}
+    for m in ("dynamics", "adjoint", "defaults", "errors", "learn", "morphology", "connectivity", "reference",
+              "cortex"):
+        mod = importlib.import_module("hhengine." + m)
+        names = {n for n in dir(mod) if not n.startswith("_")
+                 and getattr(getattr(mod, n), "__module__", None) == "hhengine." + m}
+        names |= {n for n in dir(mod) if n.isupper() and not n.startswith("_")}
+        api[m] = sorted(names)
+    with open(os.path.join(OUT, "api_names.json"), "w") as f:
+        json.dump(api, f, indent=1, sort_keys=True)
     print("golden fixtures written to", os.path.abspath(OUT))
 
 
