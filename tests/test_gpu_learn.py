@@ -207,3 +207,33 @@ def test_fit_edge_cases(cuda):
     assert L.cosine_lr(1.0, 10, 10) == pytest.approx(0.0, abs=1e-15)
     h = L.fit(st, task, L.TrainConfig(epochs=2, lr=1e-2, cosine=False))
     assert len(h) == 2 and all(np.isfinite(r[1]) and np.isfinite(r[2]) for r in h)
+
+
+
+def test_readout_kernels_float32(cuda):
+    """hhb_readout_drive / hhb_readout_grad in float32 (the kernels' second flavour)."""
+    from paper_2601_21407_b200 import _device as D, _native as nat
+    rng = np.random.default_rng(3)
+    B, T, C = 4, 50, 37
+    x = torch.as_tensor(rng.normal(size=(B, T, C)), dtype=torch.float32, device=cuda)
+    w = torch.as_tensor(rng.normal(size=C), dtype=torch.float32, device=cuda)
+    b = torch.tensor([0.25], dtype=torch.float32, device=cuda)
+    drv = torch.empty((T, B), dtype=torch.float32, device=cuda)
+    lib = nat.load()
+    nat.check(lib.hhb_readout_drive(nat.F32, B, T, C, x.data_ptr(), x.stride(0), x.stride(1), w.data_ptr(),
+                                    b.data_ptr(), drv.data_ptr(), D.stream()), "drive")
+    ref = (x.double() @ w.double()).t() + 0.25
+    assert torch.allclose(drv.double(), ref, rtol=1e-5, atol=1e-5)
+    dd = torch.as_tensor(rng.normal(size=(T, B)), dtype=torch.float32, device=cuda)
+    d_w = torch.empty(C, dtype=torch.float32, device=cuda)
+    d_b = torch.empty(1, dtype=torch.float32, device=cuda)
+    nbytes = int(lib.hhb_readout_workspace(nat.F32, C))
+    ws = torch.empty(nbytes // 4, dtype=torch.float32, device=cuda)
+    nat.check(lib.hhb_readout_grad(nat.F32, B, T, C, x.data_ptr(), x.stride(0), x.stride(1), dd.data_ptr(),
+                                   d_w.data_ptr(), d_b.data_ptr(), ws.data_ptr(), nbytes, D.stream()), "grad")
+    ref_w = torch.einsum("tb,btc->c", dd.double(), x.double())
+    assert torch.allclose(d_w.double(), ref_w, rtol=1e-4, atol=1e-4)
+    assert abs(d_b.item() - dd.double().sum().item()) < 1e-3
+    with pytest.raises(Exception):   # workspace too small
+        nat.check(lib.hhb_readout_grad(nat.F32, B, T, C, x.data_ptr(), x.stride(0), x.stride(1), dd.data_ptr(),
+                                       d_w.data_ptr(), d_b.data_ptr(), ws.data_ptr(), 8, D.stream()), "grad")

@@ -279,3 +279,22 @@ def test_spike_buffer_matches_reference_semantics(cuda):
     assert np.allclose(buf.drain(7)[6], -1.0)
     with pytest.raises(Exception):
         N.SpikeBuffer(0, 3, device=cuda)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_non_finite_state_is_reported_with_its_step(cuda, monkeypatch, graph):
+    """A non-finite membrane potential in the device network sets first_bad to
+    the step that produced it (persistent kernel and graph path alike), which
+    run_network turns into NumericalOverflowError (dynamics.py:526-527)."""
+    from paper_2601_21407_b200.errors import NumericalOverflowError
+    _, topo = _small()
+    if graph:
+        monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    net = N.CortexNetwork(topo, N.REST_CONFIG, device=cuda, dtype=np.float32, background="philox", seed=2)
+    net.advance(10)
+    assert int(net.first_bad.item()) == 2 ** 63 - 1
+    net.psp[17] = float("inf")
+    net.advance(5)
+    assert int(net.first_bad.item()) == 10
+    with pytest.raises(NumericalOverflowError):
+        N._raise_if_bad(net.first_bad)
