@@ -1,22 +1,30 @@
-"""Training plumbing either side of the HH layer: the
-reference's loss functions (learn.py:80-107) with their gradient seeds, on
-the device.
+"""Drop-in for `hhengine.learn`: the training plumbing either side
+of the HH hot path, on the device.
 
-`mse_loss` / `cross_entropy_loss` keep the reference signatures and return
-(loss, seed) -- seed = d(loss)/d(pred), what `backward_through_time` takes as
-seed_v.  `mse` is the autograd form used with `HHLayer`: one reduction pass
-forward and one elementwise pass backward (torch's `(V*V).mean()` spends
-five full passes over V on the same loss).
+* losses with their gradient seeds (learn.py:80-107): `mse_loss`,
+  `cross_entropy_loss` return (loss, seed), seed = d(loss)/d(pred), what
+  `backward_through_time` takes as seed_v; `mse` is the autograd form for
+  `HHLayer` outputs (one reduction forward, one `hhb_scale_f32` pass back);
+* `PSPKernel` / `psp_filter` (causal FIR, CUDA, lfilter's operation order),
+  `smape`, `AdamState` / `adam_step`, `cosine_lr` (learn.py:33-151);
+* trace segmentation and dataset split, the dense layer, the teacher-student
+  `ReadoutModel` (readout GEMV kernels around the HH forward/BPTT kernels),
+  `make_teacher_student_task` / `make_student` / `fit` / `evaluate_smape`, and
+  the ndjson dataset / csv history files (learn.py:158-415).
 """
 
 from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import _device as D
 from . import _native as nat
-from .errors import UsageError
+from .errors import ConfigurationError, TrainingDivergedError, UsageError
 
 
 def _dev(x):
@@ -89,10 +97,6 @@ def mse(v: torch.Tensor, target: torch.Tensor | None = None) -> torch.Tensor:
 # synaptic filtering, metric, optimizer (learn.py:33-156)
 # ---------------------------------------------------------------------------
 
-import math
-from dataclasses import dataclass, field
-
-from .errors import ConfigurationError, TrainingDivergedError
 
 
 @dataclass(frozen=True)
@@ -554,8 +558,6 @@ def fit(model: ReadoutModel, task: TeacherStudentTask, config: TrainConfig):
 # ---------------------------------------------------------------------------
 # dataset and history files (learn.py:384-414)
 # ---------------------------------------------------------------------------
-
-import json
 
 
 def write_ndjson_dataset(path, inputs, targets, pad_len: int) -> None:
