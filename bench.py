@@ -336,6 +336,53 @@ def c5_leg(torch, dev, steps=1000):
                       "REST_CONFIG, fp32, device Philox background"}
 
 
+def c1_leg(torch, dev, with_cpu=True):
+    """BASELINE config 1 (the reference's CPU-runnable case): squid axon
+    Na/K/leak, 1,024 neurons x 10,000 steps, dt 0.01 ms, constant 10 uA/cm^2,
+    fp32 forward, V + spikes recorded.  One fused launch; latency-bound (one
+    wave of 256 threads walks 10,000 dependent steps), so reported as an
+    absolute rate, not a roofline fraction.  Beside it the oracle port of the
+    reference loop on one host core over the full config (test/bench
+    infrastructure only) and the reference-facing numpy call."""
+    import numpy as np
+    from paper_2601_21407_b200 import dynamics as Dy
+    from paper_2601_21407_b200.defaults import squid_axon_params
+    p = squid_axon_params(dt=0.01).with_(dtype=np.float32)
+    n, T = 1024, 10000
+    i = torch.full((T, n), 10.0, dtype=torch.float32, device=dev)
+    for _ in range(2):
+        tr = Dy.simulate(p, i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        tr = Dy.simulate(p, i)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    spikes = int(tr.spike_series[:, 0].sum().item())
+    i_host = np.full((T, n), 10.0, dtype=np.float32)
+    Dy.simulate(p, i_host)
+    t0 = time.perf_counter()
+    Dy.simulate(p, i_host)
+    e2e_s = time.perf_counter() - t0
+    out = {"value": n * T / (ms * 1e-3), "unit": UNIT, "ms_per_run": ms, "spikes_per_neuron": spikes,
+           "e2e_numpy": {"value": n * T / e2e_s, "seconds": e2e_s,
+                         "sample": "simulate(numpy float32 I[10000, 1024]) -> Trace(float64 V, bool spikes)"},
+           "config": "BASELINE config 1: squid axon, 1,024 neurons x 10,000 steps, I = 10 uA/cm^2, fp32"}
+    if with_cpu:
+        sys.path.insert(0, ROOT)
+        from oracle import hh_oracle as O
+        p32 = squid_axon_params(dt=0.01).with_(dtype=np.float32)
+        t0 = time.perf_counter()
+        O.simulate(p32, i_host, dtype=np.float32)
+        cs = time.perf_counter() - t0
+        out["cpu_oracle"] = {"value": n * T / cs, "seconds": cs, "cores": 1, "kind": "port",
+                             "sample": "the whole config on one host core (oracle port of the reference loop, fp32)"}
+    return out
+
+
 def morph_leg(torch, dev):
     """multicompartment neurons (morphology.py mirror over
     hhb_morph_forward): the coincidence-detection graph (active squid soma +
@@ -623,6 +670,7 @@ def main():
                 dist.all_reduce(ev, op=dist.ReduceOp.MAX)
             extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
         leg("fwd_bwd", lambda: fwd_bwd_leg(torch, dev))
+        leg("c1", lambda: c1_leg(torch, dev, with_cpu=(rank == 0)))
         leg("c4_train_step", lambda: c4_leg(torch, dev))
         leg("c5_network", lambda: c5_leg(torch, dev))
         leg("morphology", lambda: morph_leg(torch, dev))
@@ -649,7 +697,7 @@ def main():
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
                 "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
                 "morphology": extras.get("morphology"), "c5_replicas": extras.get("c5_replicas"),
-                "readout_fit": extras.get("readout_fit"),
+                "readout_fit": extras.get("readout_fit"), "c1": extras.get("c1"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)
