@@ -117,8 +117,9 @@ _WS = {}
 
 
 def _workspace(n: int, dev) -> torch.Tensor:
-    """Split-K scratch, kept per device (grows; the stream orders its reuse)."""
-    key = str(dev)
+    """Split-K scratch, kept per device and stream (grows; the stream orders
+    its reuse; the side stream of overlapped weight gradients has its own)."""
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream)
     w = _WS.get(key)
     if w is None or w.numel() < n:
         w = torch.empty(n, dtype=torch.float32, device=dev)
@@ -165,13 +166,56 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         if b >= 0:
             raise GradientOverflowError("adjoint state became non-finite", b)
     layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
-    # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
-    dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
-    db = col_sum(dsum.view(B, n_out)).float()
+    if layer.overlap_weight_grad:
+        # dW, db on a side stream: they overlap the previous layer's BPTT (CUDA
+        # cores vs tensor cores); the grads are handed over when the backward
+        # pass ends (autograd engine callback: the main stream waits, then
+        # .grad is set or accumulated), so autograd gets None for them here
+        main = torch.cuda.current_stream(cur.device)
+        side = _side_stream(cur.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        side.wait_event(fork)
+        with torch.cuda.stream(side):
+            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+            db = col_sum(dsum.view(B, n_out)).float()
+            done = torch.cuda.Event()
+            done.record(side)
+        for t in (hi, lo, zb, xb):
+            t.record_stream(side)
+        weight, bias = layer.weight, layer.bias
+
+        def hand_over(gw=dW, gb=db):
+            cur_stream = torch.cuda.current_stream(gw.device)
+            cur_stream.wait_event(done)
+            gw.record_stream(cur_stream)
+            gb.record_stream(cur_stream)
+            for prm, g in ((weight, gw), (bias, gb)):
+                if prm.grad is None:
+                    prm.grad = g
+                else:
+                    prm.grad.add_(g)
+
+        torch.autograd.Variable._execution_engine.queue_callback(hand_over)
+        dW = db = None
+    else:
+        # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
+        dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+        db = col_sum(dsum.view(B, n_out)).float()
     # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
     dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0)).view(T, B, k_in)
           if x_requires_grad else None)
     return dX, dW, db
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    key = str(dev)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(dev)
+    return _SIDE[key]
 
 
 def _project(x, weight, bias, layer):
@@ -283,12 +327,17 @@ class HHLayer(torch.nn.Module):
     `param_grads` (device fp64 [1 + n_channels]).  budget=None keeps every
     state for the backward (the reference's full-storage mode), else
     checkpoints are spaced ceil(T/budget) (make_plan, adjoint.py:250-258).
+    overlap_weight_grad=True computes dW / db on a side stream, overlapping the
+    previous layer's BPTT in a stack; the grads land in .grad when the
+    backward pass ends.
     """
 
     def __init__(self, n_in: int, n_out: int, params: HHParams | None = None, budget: int | None = None,
                  surrogate: SurrogateSpec | None = None, w_mean: float = 0.0, w_std: float | None = None,
-                 check_finite: bool = True, device=None, outputs: str = "both"):
+                 check_finite: bool = True, device=None, outputs: str = "both",
+                 overlap_weight_grad: bool = False):
         super().__init__()
+        self.overlap_weight_grad = bool(overlap_weight_grad)
         if outputs not in ("both", "v", "spikes"):
             raise UsageError('outputs must be "both", "v" or "spikes"')
         self.outputs = outputs

@@ -164,3 +164,30 @@ def test_config3_full_shape_gradients_within_contract(cuda):
     for k in ("dW", "db", "dX", "d_c_m", "d_g_max"):
         assert r[k] < 1e-3, (k, r[k])
     assert r["loss_rel"] < 1e-5
+
+
+def test_overlapped_weight_grads_match(cuda):
+    """overlap_weight_grad=True (dW / db on a side stream, handed over at the end
+    of the backward pass) gives the same gradients as the in-order path, in a
+    two-layer stack, with gradient accumulation over two backward passes."""
+    def build(overlap):
+        torch.manual_seed(3)
+        l1 = HHLayer(24, 16, DF.cortical_rs_params(dt=0.1), w_mean=0.6, w_std=0.5, device=cuda,
+                     outputs="spikes", overlap_weight_grad=overlap)
+        l2 = HHLayer(16, 8, DF.cortical_rs_params(dt=0.1), w_mean=0.6, w_std=0.5, device=cuda,
+                     outputs="v", overlap_weight_grad=overlap)
+        return l1, l2
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = ((torch.rand((30, 4, 24), device=cuda, generator=g) < 0.3).float()
+         + 0.1 * torch.randn((30, 4, 24), device=cuda, generator=g))
+    grads = []
+    for overlap in (False, True):
+        l1, l2 = build(overlap)
+        for _ in range(2):
+            _, s = l1(x)
+            v, _ = l2(s)
+            (v ** 2).mean().backward()
+        torch.cuda.synchronize()
+        grads.append([t.grad.clone() for t in (l1.weight, l1.bias, l2.weight, l2.bias)])
+    for a, b in zip(*grads):
+        assert torch.allclose(a, b, rtol=1e-6, atol=1e-9)
