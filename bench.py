@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--neurons", type=int, default=10_000_000)
     ap.add_argument("--sim-steps", type=int, default=10_000)
-    ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--chunk", type=int, default=500)   # steps per launch (V trace buffer 20 GB at 10M neurons)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -168,7 +168,8 @@ def config_dict(args):
                         "(6 gates), I = 2*Poisson(2), fp32 forward, V + spike trace recorded",
             "neurons_per_gpu": args.neurons, "sim_steps": args.sim_steps, "dt_ms": 0.01,
             "chunk_steps": args.chunk, "parallelism": f"neuron-shard x{args.gpus} (weak, no collective)",
-            "l2": "inputs/outputs per chunk (4 GB) exceed the 126 MB L2; no flush needed"}
+            "l2": f"outputs per chunk ({args.neurons * args.chunk * 4 / 1e9:.0f} GB V trace) exceed the 126 MB L2; "
+                  "no flush needed"}
 
 
 # --------------------------------------------------------------------------- GPU legs
