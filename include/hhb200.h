@@ -399,6 +399,17 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
                    uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
                    const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
                    uint32_t* barrier, uint64_t* timing, void* stream);
+/* hhb_cortex_run for `replicas` (1..16) independent copies of the network in
+ * one launch (CortexReplicas): replica r's v / psp at r * ld (g rows: g_ld >=
+ * replicas * ld), its ring at r * depth * ld, its spike words at r * words of
+ * each step's [replicas][words] block, its background key seed + r. */
+int hhb_cortex_run_replicas(const hhb_params_t* params, int64_t replicas, int64_t ld, int64_t n, int64_t steps,
+                            int64_t t0, int64_t depth, int64_t* ring, float* psp, double decay, int32_t bg_mode,
+                            const double* lam, double mu, double sigma, uint64_t seed, int64_t neuron_base,
+                            double w_scale, float* v, float* g, int64_t g_ld, uint32_t* bits, int32_t record,
+                            int64_t words, const int64_t* segments, int64_t tiles, const int32_t* targets,
+                            const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad, uint32_t* barrier,
+                            uint64_t* timing, void* stream);
 
 /* Spike raster -> event list (SpikeRecord, cortex.py:422-438):
  * bits [steps][words] (bit i of word w = neuron 32 w + i; neurons >= n ignored).

@@ -130,6 +130,9 @@ SIGNATURES = {
     "hhb_cortex_run": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
                               C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
+    "hhb_cortex_run_replicas": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
+                              C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
+                              _vp, _vp, _vp, _vp]),
     "hhb_scale_f32": (_i32, [_i64, _vp, _vp, _dbl, _vp, _vp]),
     "hhb_psp_filter": (_i32, [_i32, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "hhb_readout_drive": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),

@@ -406,7 +406,7 @@ int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_
   return cuda_check("k_spike_compact / k_spike_scatter (batch) launch");
 }
 
-int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+int hhb_cortex_run_replicas(const hhb_params_t* params, int64_t replicas, int64_t ld, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
                    float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
                    uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
                    uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
@@ -415,9 +415,11 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
   int rc = check_params(params);
   if (rc) return rc;
   if (n <= 0 || steps <= 0) return HHB_OK;
+  if (replicas < 1 || ld < n) return fail(HHB_EINVAL, "cortex_run: replicas >= 1 and ld >= n");
   if (tiles != (n + 255) / 256) return fail(HHB_EINVAL, "cortex_run: tiles != ceil(n / 256)");
   if (!ring || !psp || !v || (params->n_gates > 0 && (!g || g_ld < n)) || !bits || !segments || !first_bad ||
-      !barrier || depth < 1 || words != (n + 31) / 32 || (bg_mode != 0 && bg_mode != 2) || (bg_mode == 2 && !lam))
+      !barrier || depth < 1 || words != (n + 31) / 32 || (bg_mode != 0 && bg_mode != 2) || (bg_mode == 2 && !lam) ||
+      (params->n_gates > 0 && g_ld < replicas * ld))
     return fail(HHB_EINVAL, "bad cortex_run args");
   CortexRunArgs a{};
   a.n = n;
@@ -448,6 +450,8 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
   a.first_bad = first_bad;
   a.bar = barrier;
   a.timing = reinterpret_cast<unsigned long long*>(timing);
+  a.reps = replicas;
+  a.ld = ld;
   if (!jit_cortex_run(params, a, static_cast<cudaStream_t>(stream), rc))
     return fail(HHB_ENOTSUP, std::string("persistent network kernel unavailable: ") + jit_status());
   return rc;
@@ -471,6 +475,17 @@ int hhb_spike_events(int64_t steps, int64_t words, const uint32_t* bits, int64_t
   cortex::k_event_write<<<unsigned(steps), cortex::kEvThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       words, bits, n, offsets, out_step, out_neuron);
   return cuda_check("k_event_write launch");
+}
+
+int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+                   float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
+                   uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
+                   uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
+                   const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
+                   uint32_t* barrier, uint64_t* timing, void* stream) {
+  return hhb_cortex_run_replicas(params, 1, n, n, steps, t0, depth, ring, psp, decay, bg_mode, lam, mu, sigma, seed,
+                                 neuron_base, w_scale, v, g, g_ld, bits, record, words, segments, tiles, targets,
+                                 weights_fx, delays, first_bad, barrier, timing, stream);
 }
 
 int hhb_cortex_tick(int64_t* t_dev, void* stream) {

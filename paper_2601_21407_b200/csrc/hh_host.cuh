@@ -274,6 +274,7 @@ struct CortexRunArgs {
   int64_t* first_bad;
   unsigned* bar;                 // grid-barrier counter (one uint32 of device scratch)
   unsigned long long* timing;   // optional [steps][blocks][4] globaltimer stamps (profiling)
+  int64_t reps, ld;              // replicas per launch; per-replica stride of v / psp / ring rows
 };
 bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t st, int& rc);
 const char* jit_status();

@@ -51,6 +51,7 @@ struct Driver {
   decltype(&cuLaunchKernel) launch = nullptr;
   decltype(&cuLaunchCooperativeKernel) coop = nullptr;                        // optional
   decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;  // optional
+  decltype(&cuFuncSetAttribute) set_attr = nullptr;                           // optional
   bool ok = false;
   std::string why;
 };
@@ -100,6 +101,8 @@ static void load_libs() {
   if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p, cudaEnableDefault, &q) ==
           cudaSuccess && p)
     g_drv.occupancy = reinterpret_cast<decltype(g_drv.occupancy)>(p);
+  if (cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+    g_drv.set_attr = reinterpret_cast<decltype(g_drv.set_attr)>(p);
   g_drv.ok = ok;
   if (!ok) g_drv.why = "driver entry points unavailable";
 }
@@ -1219,7 +1222,7 @@ static const char* kNetKernel = R"(
 struct NetArgs { i64 n, steps, t0, depth; long long* ring; float* psp; const double* lam;
   float decay, mu, sigma, w_scale; int mode, rec; unsigned long long seed; i64 nbase;
   float* v; float* g; i64 g_ld; u32* bits; i64 words; const i64* seg; i64 tiles; const int* tgt; const int* w;
-  const int* delay; i64* first_bad; unsigned* bar; unsigned long long* timing; };
+  const int* delay; i64* first_bad; unsigned* bar; unsigned long long* timing; i64 reps, ld; };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long x;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(x));
@@ -1297,12 +1300,23 @@ __device__ __forceinline__ i64 block_scan(i64 x, i64* s_w, i64& total) {
   __syncthreads();
   return before + inc - x;
 }
+// NET_REPS independent replicas of the network (CortexReplicas; 1 for one
+// network) share the launch, the tiles and the barrier: replica r's neurons,
+// PSP and ring live at r * ld (ring rows: r * depth * ld), its spike words at
+// r * words of the step's bitmap block, its background key is seed + r.
+#ifndef NET_REPS
+#define NET_REPS 1
+#endif
 extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a) {
-  __shared__ unsigned long long s_next[NET_THREADS];   // step t's delay-1 deliveries into the tile
-  __shared__ long long s_ahead[NET_THREADS];           // ring row t + 1 of the tile (cp.async prefetch)
-  __shared__ int s_src[NET_CAP];
-  __shared__ i64 s_beg[NET_CAP];
-  __shared__ i64 s_pre[NET_CAP + 1];
+  constexpr int R = NET_REPS;
+  // dynamic: step t's delay-1 deliveries into the tile, and ring row t + 1 of
+  // the tile (cp.async prefetch), per replica
+  extern __shared__ __align__(16) unsigned long long s_dyn[];
+  unsigned long long (*s_next)[NET_THREADS] = reinterpret_cast<unsigned long long (*)[NET_THREADS]>(s_dyn);
+  long long (*s_ahead)[NET_THREADS] = reinterpret_cast<long long (*)[NET_THREADS]>(s_dyn + R * NET_THREADS);
+  __shared__ int s_src[NET_CAP];                          // spiking sources, replica in bits 20+
+  __shared__ int s_beg[NET_CAP];                          // (synapse indices < 2^31)
+  __shared__ int s_pre[NET_CAP + 1];
   __shared__ i64 s_w[NET_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned nb = gridDim.x;
@@ -1310,21 +1324,20 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
   const i64 tile = blockIdx.x;                    // host: gridDim.x == tiles
   const i64 i = tile * NET_THREADS + tid;
   const bool on = i < a.n;
+  const i64 rring = a.depth * a.ld;               // one replica's ring
   // the tile's state lives in registers for the whole launch
-  float vv = -65.0f, psp = 0.0f, lam = 0.0f;
-  float pp[NGX];
+  float vv[R], psp[R], pp[R][NGX];
+  const float lam = (on && a.mode == 2) ? float(a.lam[i]) : 0.0f;
 #pragma unroll
-  for (int q = 0; q < NGX; ++q) pp[q] = 0.5f;
-  if (on) {
-    vv = a.v[i];
-    psp = a.psp[i];
-    lam = a.mode == 2 ? float(a.lam[i]) : 0.0f;
+  for (int r = 0; r < R; ++r) {
+    vv[r] = on ? a.v[r * a.ld + i] : -65.0f;
+    psp[r] = on ? a.psp[r * a.ld + i] : 0.0f;
 #pragma unroll
-    for (int q = 0; q < NG; ++q) pp[q] = a.g[q * a.g_ld + i];
+    for (int q = 0; q < NGX; ++q) pp[r][q] = (on && q < NG) ? a.g[q * a.g_ld + r * a.ld + i] : 0.5f;
   }
   const i64 per = (a.words + NET_THREADS - 1) / NET_THREADS;
   const i64 w0 = tid * per, w1 = min(a.words, w0 + per);
-  const i64 tlo = tile * NET_THREADS;             // this tile's neurons [tlo, tlo + 256)
+  const i64 tlo = tile * NET_THREADS;             // this tile's neurons [tlo, tlo + NET_THREADS)
   // Ring row t + 1 of the tile is complete, except for step t's delay-1
   // synapses, once step t starts: it is read (and cleared) then, off the
   // critical path, and the delay-1 deliveries of step t go to s_next instead.
@@ -1334,55 +1347,71 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
   const int depth = int(a.depth);
   int row = int(a.t0 % a.depth);                  // ring row of step t (32-bit modular counter)
   // 16-byte pairs need an even row stride (and the tile's last pair whole)
-  const bool pair = (a.n & 1) == 0 && !NET_NOPAIR;
-  s_next[tid] = 0ull;
-  s_ahead[tid] = 0;
-  if (on && a.steps > 0) s_ahead[tid] = __ldcg(a.ring + i64(row) * a.n + i);
+  const bool pair = (a.ld & 1) == 0 && (a.n & 1) == 0 && !NET_NOPAIR;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    s_next[r][tid] = 0ull;
+    s_ahead[r][tid] = (on && a.steps > 0) ? __ldcg(a.ring + r * rring + i64(row) * a.ld + i) : 0ll;
+  }
   unsigned long long* tm = a.timing ? a.timing + blockIdx.x * 4 : nullptr;
   for (i64 s = 0; s < a.steps; ++s) {
     const i64 t = a.t0 + s;
-    u32* bw = a.rec ? a.bits + s * a.words : a.bits + (s & 1) * a.words;
+    u32* bw = a.bits + (a.rec ? s : (s & 1)) * (R * a.words);
     if (tm && tid == 0) tm[s * nb * 4 + 0] = gtimer();
     // ---- input + HH step of the tile (padding lanes run the step on a dummy state)
-    float cur = 0.0f;
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();                                // (pairs: thread 2k copied entries 2k and 2k + 1)
-    const long long arr = (pair ? s_ahead[tid] : (on ? __ldcg(a.ring + i64(row) * a.n + i) : 0ll)) +
-                          (long long)s_next[tid];
-    s_next[tid] = 0ull;                             // (next written after this block's barriers)
+    long long arr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      arr[r] = (pair ? s_ahead[r][tid] : (on ? __ldcg(a.ring + r * rring + i64(row) * a.ld + i) : 0ll)) +
+               (long long)s_next[r][tid];
+      s_next[r][tid] = 0ull;                        // (next written after this block's barriers)
+    }
     const int row1 = row + 1 == depth ? 0 : row + 1;
     __syncwarp();                                   // lane 2k+1 has read s_ahead before lane 2k refills it
-    if (on) a.ring[i64(row) * a.n + i] = 0;         // row t consumed
-    if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) {
-      // 16-byte L2-only async copy of this and the next neuron's entries
-      const unsigned sa = unsigned(__cvta_generic_to_shared(&s_ahead[tid]));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(a.ring + i64(row1) * a.n + i)
-                   : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    if (on) {
-      float x = __fadd_rn(__fmul_rn(psp, a.decay), __fmul_rn(float(double(arr)), a.w_scale));
-      if (a.mode == 2) {
-        const uint4 r = philox_full(make_uint4(u32(i + a.nbase), u32((unsigned long long)(i + a.nbase) >> 32),
-                                               u32(t), u32((unsigned long long)t >> 32)),
-                                    make_uint2(u32(a.seed), u32(a.seed >> 32)));
-        x = __fadd_rn(x, bg_draw(lam, a.mu, a.sigma, r));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (on) a.ring[r * rring + i64(row) * a.ld + i] = 0;   // row t consumed
+      if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) {
+        // 16-byte L2-only async copy of this and the next neuron's entries
+        const unsigned sa = unsigned(__cvta_generic_to_shared(&s_ahead[r][tid]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                     "l"(a.ring + r * rring + i64(row1) * a.ld + i)
+                     : "memory");
       }
-      psp = x;
-      cur = x;
     }
-    const float vo = vv;
-    vv = step_fwd(vv, pp, cur);
-    const bool spk = on && (vo < THETA) && (vv >= THETA);
-    if (on && !finitef_(vv)) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)t);
-    const u32 word = __ballot_sync(0xffffffffu, spk);
-    if (lane == 0 && (i >> 5) < a.words) bw[i >> 5] = word;
+    if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float cur = 0.0f;
+      if (on) {
+        float x = __fadd_rn(__fmul_rn(psp[r], a.decay), __fmul_rn(float(double(arr[r])), a.w_scale));
+        if (a.mode == 2) {
+          const unsigned long long sd = a.seed + (unsigned long long)r;
+          const uint4 rv = philox_full(make_uint4(u32(i + a.nbase), u32((unsigned long long)(i + a.nbase) >> 32),
+                                                  u32(t), u32((unsigned long long)t >> 32)),
+                                       make_uint2(u32(sd), u32(sd >> 32)));
+          x = __fadd_rn(x, bg_draw(lam, a.mu, a.sigma, rv));
+        }
+        psp[r] = x;
+        cur = x;
+      }
+      const float vo = vv[r];
+      vv[r] = step_fwd(vv[r], pp[r], cur);
+      const bool spk = on && (vo < THETA) && (vv[r] >= THETA);
+      if (on && !finitef_(vv[r])) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)t);
+      const u32 word = __ballot_sync(0xffffffffu, spk);
+      if (lane == 0 && (i >> 5) < a.words) bw[r * a.words + (i >> 5)] = word;
+    }
     if (tm) {
       __syncthreads();
       if (tid == 0) tm[s * nb * 4 + 1] = gtimer();
     }
     grid_sync(a.bar, ++phase * nb);
     if (tm && tid == 0) tm[s * nb * 4 + 2] = gtimer();
+    // ---- delivery into this tile: list the spiking sources of every replica ...
+#if NET_REPS == 1
     u32 wr[8];
     int cnt = 0;
 #pragma unroll
@@ -1390,43 +1419,52 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
       wr[k] = (w0 + k < w1) ? __ldcg(bw + w0 + k) : 0u;
       cnt += __popc(wr[k]);
     }
-    // ---- delivery into this tile: list the spiking sources (ascending) ...
+#else
+    int cnt = 0;
+    for (int r = 0; r < R; ++r)
+      for (i64 wi = w0; wi < w1; ++wi) cnt += __popc(__ldcg(bw + r * a.words + wi));
+#endif
     i64 ns = 0;
     const i64 first = block_scan(cnt, s_w, ns);
     for (i64 r0 = 0; r0 < ns; r0 += NET_CAP) {
       const i64 m = min(i64(NET_CAP), ns - r0);
       if (cnt > 0 && first < r0 + m && first + cnt > r0) {
         i64 k = first;
-        auto emit = [&](u32 x, i64 wi) {
+        auto emit = [&](u32 x, i64 wi, int r) {
           while (x) {
             const int b = __ffs(int(x)) - 1;
             x &= x - 1;
-            if (k >= r0 && k < r0 + m) s_src[k - r0] = int(wi * 32 + b);
+            if (k >= r0 && k < r0 + m) s_src[k - r0] = int(wi * 32 + b) | (r << 20);
             ++k;
           }
         };
+#if NET_REPS == 1
 #pragma unroll
-        for (int q = 0; q < 8; ++q) emit(wr[q], w0 + q);
+        for (int q = 0; q < 8; ++q) emit(wr[q], w0 + q, 0);
+#else
+        for (int r = 0; r < R; ++r)
+          for (i64 wi = w0; wi < w1; ++wi) emit(__ldcg(bw + r * a.words + wi), wi, r);
+#endif
       }
       __syncthreads();
       // ... each source's segment of synapses with targets in the tile ...
       i64 lsum = 0;
       const i64 c0 = (m * tid) / NET_THREADS, c1 = (m * (tid + 1)) / NET_THREADS;
       for (i64 c = c0; c < c1; ++c) {
-        const i64* sg = a.seg + i64(s_src[c]) * (a.tiles + 1) + tile;
+        const i64* sg = a.seg + i64(s_src[c] & 0xFFFFF) * (a.tiles + 1) + tile;
         const i64 beg = __ldg(sg), end = __ldg(sg + 1);
-        s_beg[c] = beg;
-        s_pre[c] = end - beg;                     // length, turned into a prefix below
+        s_beg[c] = int(beg);
+        s_pre[c] = int(end - beg);                // length, turned into a prefix below
         lsum += end - beg;
       }
       i64 total = 0;
       i64 run = block_scan(lsum, s_w, total);
       for (i64 c = c0; c < c1; ++c) {
         const i64 l = s_pre[c];
-        s_pre[c] = run;
+        s_pre[c] = int(run);
         run += l;
       }
-      if (tid == 0) s_pre[m] = total;
+      if (tid == 0) s_pre[m] = int(total);
       __syncthreads();
       // ... and one thread per (source, synapse) pair, NET_UNROLL pairs in
       // flight per thread (their loads overlap)
@@ -1434,7 +1472,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
 #define NET_UNROLL 4
 #endif
       for (i64 g0 = tid; g0 < total; g0 += NET_THREADS * NET_UNROLL) {
-        int d[NET_UNROLL], tg[NET_UNROLL], wv[NET_UNROLL];
+        int d[NET_UNROLL], tg[NET_UNROLL], wv[NET_UNROLL], rr[NET_UNROLL];
 #pragma unroll
         for (int u = 0; u < NET_UNROLL; ++u) {
           const i64 gi = g0 + u * NET_THREADS;
@@ -1447,6 +1485,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
               else hi = mid;
             }
             const i64 j = s_beg[lo] + (gi - s_pre[lo]);
+            rr[u] = s_src[lo] >> 20;
             d[u] = __ldg(a.delay + j);
             tg[u] = __ldg(a.tgt + j);
             wv[u] = __ldg(a.w + j);
@@ -1457,10 +1496,12 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
           if (d[u] == 0) continue;
           const unsigned long long wq = (unsigned long long)(long long)wv[u];
           if (d[u] == 1) {
-            atomicAdd(&s_next[tg[u] - tlo], wq);
+            atomicAdd(&s_next[R == 1 ? 0 : rr[u]][tg[u] - tlo], wq);
           } else {
-            const int r = row + d[u] >= depth ? row + d[u] - depth : row + d[u];   // (t + d) % depth, d < depth
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + i64(r) * a.n + tg[u]), wq);
+            const int q = row + d[u] >= depth ? row + d[u] - depth : row + d[u];   // (t + d) % depth, d < depth
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + (R == 1 ? 0 : rr[u]) * rring + i64(q) * a.ld +
+                                                            tg[u]),
+                      wq);
           }
         }
       }
@@ -1470,15 +1511,18 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
     row = row1;
   }
   __syncthreads();
-  if (on && a.steps > 0) {   // the last step's delay-1 deliveries back into the ring
-    long long* slot = a.ring + ((a.t0 + a.steps) % a.depth) * a.n + i;
-    *slot = *slot + (long long)s_next[tid];
-  }
-  if (on) {
-    a.v[i] = vv;
-    a.psp[i] = psp;
 #pragma unroll
-    for (int q = 0; q < NG; ++q) a.g[q * a.g_ld + i] = pp[q];
+  for (int r = 0; r < R; ++r) {
+    if (on && a.steps > 0) {   // the last step's delay-1 deliveries back into the ring
+      long long* slot = a.ring + r * rring + ((a.t0 + a.steps) % a.depth) * a.ld + i;
+      *slot = *slot + (long long)s_next[r][tid];
+    }
+    if (on) {
+      a.v[r * a.ld + i] = vv[r];
+      a.psp[r * a.ld + i] = psp[r];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) a.g[q * a.g_ld + r * a.ld + i] = pp[r][q];
+    }
   }
 }
 )";
@@ -1910,7 +1954,8 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
 }
 )";
   }
-  if (bwd_flags == kNet) {
+  if (bwd_flags <= kNet) {
+    src += fmt("#define NET_REPS %d\n", kNet - bwd_flags + 1);
     // spikes listed per delivery round (shared memory); HHB_NET_CAP lowers it (tests)
     const char* cap = getenv("HHB_NET_CAP");
     src += fmt("#define NET_CAP %d\n", cap && atoi(cap) > 0 && atoi(cap) < 2048 ? atoi(cap) : 2048);
@@ -1944,7 +1989,7 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
 struct Module {
   CUfunction fwd1 = nullptr, fwd4 = nullptr, fwdp1 = nullptr, fwdp4 = nullptr, bwd = nullptr, bwd2 = nullptr;
   CUfunction net = nullptr;
-  int net_blocks_per_sm = 0;
+  int net_blocks_per_sm = 0, net_smem = 0;
   bool ok = false;
 };
 static std::map<std::string, Module> g_cache;
@@ -2028,9 +2073,14 @@ static Module* get_module(const hhb_params_t* P, int bwd_flags) {
   g_nv.destroy(&prog);
   CUmodule mod;
   bool loaded = g_drv.load(&mod, cubin.data()) == CUDA_SUCCESS;
-  if (loaded && bwd_flags == kNet) {
-    loaded = g_drv.get(&m.net, mod, "hh_net") == CUDA_SUCCESS && g_drv.occupancy &&
-             g_drv.occupancy(&m.net_blocks_per_sm, m.net, 256, 0) == CUDA_SUCCESS && m.net_blocks_per_sm > 0;
+  if (loaded && bwd_flags <= kNet) {
+    // dynamic shared memory: s_next + s_ahead, 2 x replicas x 256 x 8 bytes
+    const int dyn = 2 * (kNet - bwd_flags + 1) * 256 * 8;
+    loaded = g_drv.get(&m.net, mod, "hh_net") == CUDA_SUCCESS && g_drv.occupancy && g_drv.set_attr &&
+             g_drv.set_attr(m.net, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, dyn) == CUDA_SUCCESS &&
+             g_drv.occupancy(&m.net_blocks_per_sm, m.net, 256, size_t(dyn)) == CUDA_SUCCESS &&
+             m.net_blocks_per_sm > 0;
+    m.net_smem = dyn;
   } else if (loaded && bwd_flags < 0)
     loaded = g_drv.get(&m.fwd1, mod, "hh_fwd_v1") == CUDA_SUCCESS && g_drv.get(&m.fwd4, mod, "hh_fwd_v4") == CUDA_SUCCESS &&
              g_drv.get(&m.fwdp1, mod, "hh_fwdp_v1") == CUDA_SUCCESS &&
@@ -2120,7 +2170,11 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
 // Returns false when the JIT or a cooperative launch is unavailable.
 bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t st, int& rc) {
   using namespace jit;
-  jit::Module* m = jit::get_module(P, kNet);
+  if (a.reps < 1 || a.reps > 16) {
+    rc = fail(HHB_EINVAL, "hh_net: 1..16 replicas per launch");
+    return true;
+  }
+  jit::Module* m = jit::get_module(P, kNet - int(a.reps - 1));
   if (!m || !g_drv.coop) return false;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2141,7 +2195,8 @@ bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t 
   const unsigned grid = unsigned(tiles);
   CortexRunArgs args = a;
   void* params[] = {&args};
-  const CUresult r = g_drv.coop(m->net, grid, 1, 1, 256, 1, 1, 0, reinterpret_cast<CUstream>(st), params);
+  const CUresult r = g_drv.coop(m->net, grid, 1, 1, 256, 1, 1, unsigned(m->net_smem), reinterpret_cast<CUstream>(st),
+                                params);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "cooperative launch of hh_net failed");
   return true;
 }

@@ -427,7 +427,7 @@ class CortexNetwork:
             self.w = self.w[perm].contiguous()
             self.delay = self.delay[perm].contiguous()
             del perm
-            tiles = (self.n + 255) // 256
+            tiles = (getattr(self, "n_pad", self.n) + 255) // 256    # replicas: padded populations
             q = (torch.arange(n_src, device=dev)[:, None] << 32) | (torch.arange(tiles + 1, device=dev) * 256)[None, :]
             self._seg = torch.searchsorted(key, q.reshape(-1)).reshape(n_src, tiles + 1).contiguous()
             self._tiles = tiles
@@ -893,9 +893,65 @@ class CortexReplicas:
         self._phase(1)
         nat.check(nat.load().hhb_cortex_tick(self.t_dev.data_ptr(), D.stream()), "hhb_cortex_tick")
 
+    _tile_segments = CortexNetwork._tile_segments      # same attribute names (off, tgt, w, delay, n, dev)
+
+    def persistent_ok(self) -> bool:
+        """Replicas in the persistent kernel (groups of up to 16 per launch) are
+        opt-in (HHB_NET_REPLICAS_PERSIST=1): a block stepping R replicas runs
+        their HH steps and deliveries one after another (the step's warp votes
+        keep the compiler from interleaving them), so per replica-step it
+        measured no better than one network (R = 8: 62 µs per step against 36
+        for the batched graph path, which fills the GPU with R x 38,586
+        neurons per launch instead)."""
+        import os
+        return (self.dtype == np.float32 and os.environ.get("HHB_NET_REPLICAS_PERSIST", "0") not in ("", "0")
+                and os.environ.get("HHB_NET_GRAPH", "0") in ("", "0") and not getattr(self, "_no_persist", False))
+
+    def _advance_persistent(self, n_steps: int, record: torch.Tensor | None):
+        """All replicas n_steps in persistent launches of up to 16 replicas each
+        (hhb_cortex_run_replicas): replica r is bit-identical to the graph path."""
+        lib = nat.load()
+        seg, tiles = self._tile_segments()
+        Wd, R, npd = self.words, self.R, self.n_pad
+        G = min(R, 16)
+        mode = 2 if self.bg.rate_hz > 0 else 0
+        if getattr(self, "_barrier", None) is None:
+            self._barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        P = _table(self.params)
+        for r0 in range(0, R, G):
+            g = min(G, R - r0)
+            if record is not None:
+                buf = torch.empty((n_steps, g, Wd), dtype=torch.int32, device=self.dev)
+                rec = 1
+            else:
+                buf = torch.zeros((2, g, Wd), dtype=torch.int32, device=self.dev)
+                rec = 0
+            rc = lib.hhb_cortex_run_replicas(
+                C.byref(P), g, npd, npd, n_steps, self.t, self.depth,
+                self.ring[r0].data_ptr(), self.psp[r0 * npd:].data_ptr(), self.decay, mode, self.lam.data_ptr(),
+                self.bg.w_mean, self.bg.w_std, self.seed + r0, 0, float(1.0 / (1 << W_FRAC_BITS)),
+                self.v[r0 * npd:].data_ptr(), self.g[:, r0 * npd:].data_ptr() if self.g.numel() else None,
+                R * npd, buf.data_ptr(), rec, Wd, seg.data_ptr(), tiles, self.tgt.data_ptr(), self.w.data_ptr(),
+                self.delay.data_ptr(), self.first_bad.data_ptr(), self._barrier.data_ptr(), None, D.stream())
+            nat.check(rc, "hhb_cortex_run_replicas")
+            if record is not None:
+                record[:n_steps, r0:r0 + g].copy_(buf)
+        self.t += n_steps
+        self.t_dev.fill_(self.t)
+        return record
+
     def advance(self, n_steps: int, steps_per_graph: int = 32, record: torch.Tensor | None = None):
-        """Advance all replicas n_steps (CUDA graphs of steps_per_graph steps).
-        record: optional int32 [n_steps][replicas][n_pad/32] spike words."""
+        """Advance all replicas n_steps: float32 replicas in persistent
+        launches (groups of <= 16 replicas), otherwise CUDA graphs of
+        steps_per_graph steps.  record: optional int32
+        [n_steps][replicas][n_pad/32] spike words."""
+        if n_steps > 0 and self.persistent_ok():
+            try:
+                return self._advance_persistent(n_steps, record)
+            except NativeLibraryError as e:
+                if "hh_net" not in str(e) and "unavailable" not in str(e):
+                    raise
+                self._no_persist = True
         self.t_dev.fill_(self.t)
         S = max(1, min(int(steps_per_graph), n_steps)) if n_steps > 0 else 1
         done, rec = 0, record is not None

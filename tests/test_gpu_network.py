@@ -216,6 +216,7 @@ def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap, nopair):
     steps = 300
     ra = torch.empty((steps, a.words_global), dtype=torch.int32, device=cuda)
     a.advance(steps, record=ra)
+    assert not getattr(a, "_no_persist", False), "the persistent path fell back"
     monkeypatch.setenv("HHB_NET_GRAPH", "1")
     assert not b.persistent_ok()
     rb = torch.empty_like(ra)
@@ -298,3 +299,24 @@ def test_non_finite_state_is_reported_with_its_step(cuda, monkeypatch, graph):
     assert int(net.first_bad.item()) == 10
     with pytest.raises(NumericalOverflowError):
         N._raise_if_bad(net.first_bad)
+
+
+def test_persistent_replicas_equal_graph_replicas(cuda, monkeypatch):
+    """CortexReplicas in persistent launches (groups of <= 16 replicas) equal
+    the graph path bit for bit, across a group boundary (R = 19)."""
+    _, topo = _small()
+    cfg = N.REST_CONFIG
+    R, steps = 19, 120
+    monkeypatch.setenv("HHB_NET_REPLICAS_PERSIST", "1")
+    a = N.CortexReplicas(topo, cfg, R, device=cuda, dtype=np.float32, seed=4)
+    b = N.CortexReplicas(topo, cfg, R, device=cuda, dtype=np.float32, seed=4)
+    assert a.persistent_ok()
+    ra = torch.empty((steps, R, a.words), dtype=torch.int32, device=cuda)
+    a.advance(steps, record=ra)
+    assert not getattr(a, "_no_persist", False), "the persistent path fell back"
+    monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    rb = torch.empty_like(ra)
+    b.advance(steps, steps_per_graph=40, record=rb)
+    assert ra.any() and torch.equal(ra, rb)
+    for x, y in ((a.v, b.v), (a.g, b.g), (a.psp, b.psp), (a.ring, b.ring)):
+        assert torch.equal(x, y)
