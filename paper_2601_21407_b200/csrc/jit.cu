@@ -1382,9 +1382,10 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
       }
     }
     if (pair && (tid & 1) == 0 && i < a.n && s + 1 < a.steps) asm volatile("cp.async.commit_group;" ::: "memory");
+    float cur[R], vn[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      float cur = 0.0f;
+      cur[r] = 0.0f;
       if (on) {
         float x = __fadd_rn(__fmul_rn(psp[r], a.decay), __fmul_rn(float(double(arr[r])), a.w_scale));
         if (a.mode == 2) {
@@ -1395,10 +1396,16 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
           x = __fadd_rn(x, bg_draw(lam, a.mu, a.sigma, rv));
         }
         psp[r] = x;
-        cur = x;
+        cur[r] = x;
       }
+    }
+    // the R replicas' neurons as one VEC = R group: their steps interleave
+    // under one warp vote (step_all, as the 4-neurons-per-thread forward)
+    step_all<R>(vv, pp, cur, vn);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
       const float vo = vv[r];
-      vv[r] = step_fwd(vv[r], pp[r], cur);
+      vv[r] = vn[r];
       const bool spk = on && (vo < THETA) && (vv[r] >= THETA);
       if (on && !finitef_(vv[r])) atomicMin(reinterpret_cast<long long*>(a.first_bad), (long long)t);
       const u32 word = __ballot_sync(0xffffffffu, spk);
@@ -1411,19 +1418,16 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
     grid_sync(a.bar, ++phase * nb);
     if (tm && tid == 0) tm[s * nb * 4 + 2] = gtimer();
     // ---- delivery into this tile: list the spiking sources of every replica ...
-#if NET_REPS == 1
-    u32 wr[8];
+    // this thread's (<= 8) words of every replica, loaded together (one L2 round trip)
+    u32 wr[R][8];
     int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      wr[k] = (w0 + k < w1) ? __ldcg(bw + w0 + k) : 0u;
-      cnt += __popc(wr[k]);
-    }
-#else
-    int cnt = 0;
     for (int r = 0; r < R; ++r)
-      for (i64 wi = w0; wi < w1; ++wi) cnt += __popc(__ldcg(bw + r * a.words + wi));
-#endif
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wr[r][k] = (w0 + k < w1) ? __ldcg(bw + r * a.words + w0 + k) : 0u;
+        cnt += __popc(wr[r][k]);
+      }
     i64 ns = 0;
     const i64 first = block_scan(cnt, s_w, ns);
     for (i64 r0 = 0; r0 < ns; r0 += NET_CAP) {
@@ -1438,13 +1442,10 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
             ++k;
           }
         };
-#if NET_REPS == 1
 #pragma unroll
-        for (int q = 0; q < 8; ++q) emit(wr[q], w0 + q, 0);
-#else
         for (int r = 0; r < R; ++r)
-          for (i64 wi = w0; wi < w1; ++wi) emit(__ldcg(bw + r * a.words + wi), wi, r);
-#endif
+#pragma unroll
+          for (int q = 0; q < 8; ++q) emit(wr[r][q], w0 + q, r);
       }
       __syncthreads();
       // ... each source's segment of synapses with targets in the tile ...

@@ -899,10 +899,10 @@ class CortexReplicas:
         """Replicas in the persistent kernel (groups of up to 16 per launch) are
         opt-in (HHB_NET_REPLICAS_PERSIST=1): a block stepping R replicas runs
         their HH steps and deliveries one after another (the step's warp votes
-        keep the compiler from interleaving them), so per replica-step it
-        measured no better than one network (R = 8: 62 µs per step against 36
-        for the batched graph path, which fills the GPU with R x 38,586
-        neurons per launch instead)."""
+        and its delivery grows with R), so per replica-step it measured no
+        better than the batched graph path, which fills the GPU with
+        R x 38,586 neurons per launch (R = 4 at scale 0.5: 25.1 vs 25.3 µs per
+        step over the same window)."""
         import os
         return (self.dtype == np.float32 and os.environ.get("HHB_NET_REPLICAS_PERSIST", "0") not in ("", "0")
                 and os.environ.get("HHB_NET_GRAPH", "0") in ("", "0") and not getattr(self, "_no_persist", False))
@@ -932,7 +932,8 @@ class CortexReplicas:
                 self.bg.w_mean, self.bg.w_std, self.seed + r0, 0, float(1.0 / (1 << W_FRAC_BITS)),
                 self.v[r0 * npd:].data_ptr(), self.g[:, r0 * npd:].data_ptr() if self.g.numel() else None,
                 R * npd, buf.data_ptr(), rec, Wd, seg.data_ptr(), tiles, self.tgt.data_ptr(), self.w.data_ptr(),
-                self.delay.data_ptr(), self.first_bad.data_ptr(), self._barrier.data_ptr(), None, D.stream())
+                self.delay.data_ptr(), self.first_bad.data_ptr(), self._barrier.data_ptr(),
+                D.ptr(getattr(self, "timing", None)), D.stream())
             nat.check(rc, "hhb_cortex_run_replicas")
             if record is not None:
                 record[:n_steps, r0:r0 + g].copy_(buf)
