@@ -897,12 +897,11 @@ class CortexReplicas:
 
     def persistent_ok(self) -> bool:
         """Replicas in the persistent kernel (groups of up to 16 per launch) are
-        opt-in (HHB_NET_REPLICAS_PERSIST=1): a block stepping R replicas runs
-        their HH steps and deliveries one after another (the step's warp votes
-        and its delivery grows with R), so per replica-step it measured no
-        better than the batched graph path, which fills the GPU with
-        R x 38,586 neurons per launch (R = 4 at scale 0.5: 25.1 vs 25.3 µs per
-        step over the same window)."""
+        opt-in (HHB_NET_REPLICAS_PERSIST=1): a block stepping R replicas does R
+        times the input, step and delivery work of its tile behind one barrier,
+        and per replica-step that measured no better than the batched graph
+        path, which fills the GPU with R x 38,586 neurons per launch (R = 4 at
+        scale 0.5: 25.1 vs 25.3 µs per step over the same window)."""
         import os
         return (self.dtype == np.float32 and os.environ.get("HHB_NET_REPLICAS_PERSIST", "0") not in ("", "0")
                 and os.environ.get("HHB_NET_GRAPH", "0") in ("", "0") and not getattr(self, "_no_persist", False))
