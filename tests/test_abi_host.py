@@ -227,3 +227,30 @@ def test_every_reference_public_name_exists():
                for m, names in api.items()}
     assert not any(missing.values()), missing
     assert sum(len(v) for v in api.values()) > 100
+
+
+def test_new_entry_points_validate_arguments_without_a_gpu():
+    """Argument checks of the late entry points return HHB_EINVAL before any
+    CUDA call (so they run here, without a GPU), with a message."""
+    lib = nat.load()
+    P = Dy._table(DF.cortical_rs_params().with_(dtype=np.float32))
+    E = nat.EINVAL
+    # readout GEMV / gradient: negative sizes, NULL pointers, short workspace
+    assert lib.hhb_readout_drive(nat.F64, -1, 2, 3, None, 0, 0, None, None, None, None) == E
+    assert lib.hhb_readout_drive(nat.F64, 2, 2, 3, None, 6, 3, None, None, None, None) == E
+    assert lib.hhb_readout_workspace(nat.F64, 64) == 296 * 65 * 8
+    assert lib.hhb_readout_grad(nat.F64, 2, 2, 3, 1, 6, 3, 1, 1, 1, 1, 8, None) == E
+    # spike events: more neurons than the bitmap holds
+    assert lib.hhb_spike_event_counts(4, 2, 1, 65, 1, None) == E
+    assert lib.hhb_spike_events(4, 2, 1, 64, None, 1, 1, None) == E
+    # persistent network: replicas < 1, ld < n, bad bitmap width
+    args = [C.byref(P), 0, 100, 100, 10, 0, 5, 1, 1, 0.9, 0, None, 0.0, 0.0, 0, 0, 1.0, 1, 1, 100, 1, 0, 4, 1,
+            1, 1, 1, 1, 1, 1, None, None]
+    assert lib.hhb_cortex_run_replicas(*args) == E
+    args[1], args[2] = 1, 50
+    assert lib.hhb_cortex_run_replicas(*args) == E
+    args[2], args[22] = 100, 3
+    assert lib.hhb_cortex_run_replicas(*args) == E
+    assert b"cortex_run" in lib.hhb_last_error()
+    # fused-MSE partials: a count for any population size
+    assert lib.hhb_forward_partials(0) >= 1 and lib.hhb_forward_partials(10 ** 7) >= 10 ** 7 // 32
