@@ -254,3 +254,10 @@ def test_new_entry_points_validate_arguments_without_a_gpu():
     assert b"cortex_run" in lib.hhb_last_error()
     # fused-MSE partials: a count for any population size
     assert lib.hhb_forward_partials(0) >= 1 and lib.hhb_forward_partials(10 ** 7) >= 10 ** 7 // 32
+
+
+def test_integration_doc_maps_every_entry_point():
+    """INTEGRATION.md names every symbol include/hhb200.h declares."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    missing = [n for n in _declared() if n not in doc]
+    assert not missing, missing
