@@ -10,7 +10,7 @@ import bench  # noqa: E402
 
 dev = torch.device("cuda", 0)
 import gc
-for name, fn in (("fwd_bwd", bench.fwd_bwd_leg), ("c4", bench.c4_leg), ("c5", bench.c5_leg),
+for name, fn in (("c1", bench.c1_leg), ("fwd_bwd", bench.fwd_bwd_leg), ("c4", bench.c4_leg), ("c5", bench.c5_leg),
                  ("morph", bench.morph_leg), ("morph2", bench.morph_leg)):
     gc.collect()
     torch.cuda.synchronize()
