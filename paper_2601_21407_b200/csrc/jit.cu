@@ -1087,9 +1087,14 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   u32* so = FF_SO ? a.spk + n0 / 32 : nullptr;
   float* svo = FF_SVO ? a.spk_val + n0 : nullptr;
   const bool spk_writer = lane % (32 / VEC) == 0 && live;
-  // loaded currents are prefetched one step ahead (HBM latency); the drawn
-  // stimulus is made at the top of its own step (no registers held across it)
+  // loaded currents are prefetched FWD_PF steps ahead with one neuron per
+  // thread (small, latency-bound populations: one warp per SM, the step chain
+  // is shorter than an HBM load) and one step ahead with four (throughput-
+  // bound, registers are the limit); the drawn stimulus is made at the top of
+  // its own step (no registers held across it)
+  constexpr int PF = VEC == 1 ? FWD_PF : 1;
   float cur[VEC];
+  float pre[PF][VEC];
   auto load_in = [&](float (&c)[VEC]) {
     if (vec_in) {
       const float4 q = live ? __ldg(reinterpret_cast<const float4*>(ip)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1108,11 +1113,23 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) q[j] = x[j];
     }
   };
-  if (!POIS && a.steps > 0) load_in(cur);
+  if (!POIS) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k)
+      if (k < a.steps) load_in(pre[k]);
+  }
   for (i64 t = 0; t < a.steps; ++t) {
-    float nxt[VEC];
-    if (POIS) stim.at(a, ks, ps, t, n0, full, cur);
-    else if (t + 1 < a.steps) load_in(nxt);
+    if (POIS) {
+      stim.at(a, ks, ps, t, n0, full, cur);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) cur[j] = pre[0][j];
+#pragma unroll
+      for (int k = 0; k + 1 < PF; ++k)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) pre[k][j] = pre[k + 1][j];
+      if (t + PF < a.steps) load_in(pre[PF - 1]);
+    }
     if (FF_CK && ck_count == 0) {      // state BEFORE step t
       store4(ckp, v);
 #pragma unroll
@@ -1169,10 +1186,6 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       }
       if (spk_writer) *so = w;
       so += a.spk_ld;
-    }
-    if (!POIS) {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
     }
   }
 #pragma unroll
@@ -1812,6 +1825,8 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   // measured best for config 2 on B200 (profiles/r1_variants.md: 1.49e11 vs
   // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
+  const char* pf = getenv("HHB_JIT_FWD_PF");
+  src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 4);
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
   src += fmt("#define BWD2_MINB %d\n", bmb2 ? atoi(bmb2) : 6);
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
@@ -2022,6 +2037,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += bmb ? std::string("b") + bmb : "";
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
   k += bmb2 ? std::string("c") + bmb2 : "";
+  const char* pf = getenv("HHB_JIT_FWD_PF");
+  k += pf ? std::string("p") + pf : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
   for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR"}) {
