@@ -328,11 +328,38 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
   int64_t ck_count = 0;
   double sq = 0.0;
 
+  // one neuron per thread (small, latency-bound populations): the loaded
+  // current is prefetched PF steps ahead through registers that rotate by
+  // name (loop unrolled PF times); the loads are unconditional (padding lanes
+  // read element 0, rows past the end re-read the last one) and the value is
+  // copied out with an explicit add, so no register move waits on a load
+  // (float only: the float64 step is long enough to cover the load, and unrolling it
+  // measured slower -- instruction-cache pressure of four copies of the float64 step)
+  constexpr int PF = (VEC == 1 && !POIS && sizeof(T) == 4) ? 4 : 1;
   T cur[VEC];
-  if (a.steps > 0) stim.at(a, ps, 0, n0, full, cur);
-  for (int64_t t = 0; t < a.steps; ++t) {
+  T pre[PF];
+  const T* ib1 = (n0 < a.n) ? a.i_ext + n0 * a.i_sn : a.i_ext;
+  if (a.steps > 0) {
+    if constexpr (PF > 1) {
+#pragma unroll
+      for (int k = 0; k < PF; ++k) pre[k] = __ldg(ib1 + (k < a.steps ? k : a.steps - 1) * a.i_st);
+    } else {
+      stim.at(a, ps, 0, n0, full, cur);
+    }
+  }
+  for (int64_t t_blk = 0; t_blk < a.steps; t_blk += PF)
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int64_t t = t_blk + k;
+    if (PF > 1 && t >= a.steps) break;
     T nxt[VEC];
-    if (t + 1 < a.steps) stim.at(a, ps, t + 1, n0, full, nxt);
+    if constexpr (PF > 1) {
+      cur[0] = pre[k] + T(0);
+      const int64_t r = t + PF < a.steps ? t + PF : a.steps - 1;
+      pre[k] = __ldg(ib1 + r * a.i_st);
+    } else {
+      if (t + 1 < a.steps) stim.at(a, ps, t + 1, n0, full, nxt);
+    }
     if (a.ckpt != nullptr && ck_count == 0) {  // state BEFORE step t
       T* base = a.ckpt + ck_slot * (1 + NG) * a.ck_ld;
       if (full) {
@@ -390,8 +417,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
       const uint32_t w = spike_word<VEC>(spk, lane);
       if (lane % (32 / VEC) == 0 && n0 < a.n) a.spk[t * a.spk_ld + n0 / 32] = w;
     }
+    if constexpr (PF == 1) {
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
+      for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
+    }
   }
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {

@@ -1087,12 +1087,12 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   u32* so = FF_SO ? a.spk + n0 / 32 : nullptr;
   float* svo = FF_SVO ? a.spk_val + n0 : nullptr;
   const bool spk_writer = lane % (32 / VEC) == 0 && live;
-  // loaded currents are prefetched FWD_PF steps ahead with one neuron per
+  // loaded currents are prefetched FWD_PF (8) steps ahead with one neuron per
   // thread (small, latency-bound populations: one warp per SM, the step chain
   // is shorter than an HBM load) and one step ahead with four (throughput-
   // bound, registers are the limit); the drawn stimulus is made at the top of
   // its own step (no registers held across it)
-  constexpr int PF = VEC == 1 ? FWD_PF : 1;
+  constexpr int PF = (VEC == 1 && !POIS) ? FWD_PF : 1;
   float cur[VEC];
   float pre[PF][VEC];
   auto load_in = [&](float (&c)[VEC]) {
@@ -1113,23 +1113,22 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       for (int j = 0; j < VEC; ++j) if ((valid >> j) & 1u) q[j] = x[j];
     }
   };
-  if (!POIS) {
+  // PF > 1 (one neuron per thread): every prefetch is an unconditional load
+  // (padding lanes read element 0, rows past the end re-read the last row) so
+  // no select/phi copy of the loaded register is made -- such a copy waits for
+  // the load and undoes the prefetch
+  const float* ib1 = (n0 < a.n) ? a.i_ext + n0 * a.i_sn : a.i_ext;
+  auto load_row = [&](i64 r, float (&c)[VEC]) {
+    c[0] = __ldg(ib1 + (r < a.steps ? r : a.steps - 1) * a.i_st);
+  };
+  if (!POIS && a.steps > 0) {
 #pragma unroll
-    for (int k = 0; k < PF; ++k)
-      if (k < a.steps) load_in(pre[k]);
-  }
-  for (i64 t = 0; t < a.steps; ++t) {
-    if (POIS) {
-      stim.at(a, ks, ps, t, n0, full, cur);
-    } else {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) cur[j] = pre[0][j];
-#pragma unroll
-      for (int k = 0; k + 1 < PF; ++k)
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) pre[k][j] = pre[k + 1][j];
-      if (t + PF < a.steps) load_in(pre[PF - 1]);
+    for (int k = 0; k < PF; ++k) {
+      if (PF > 1) load_row(k, pre[k]);
+      else load_in(pre[k]);
     }
+  }
+  auto body = [&](const i64 t) {
     if (FF_CK && ck_count == 0) {      // state BEFORE step t
       store4(ckp, v);
 #pragma unroll
@@ -1186,6 +1185,27 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       }
       if (spk_writer) *so = w;
       so += a.spk_ld;
+    }
+  };
+  // unrolled PF times so that the prefetch registers rotate by name: step
+  // t + k consumes pre[k] (loaded PF steps earlier) and refills it
+  for (i64 tb = 0; tb < a.steps; tb += PF) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const i64 t = tb + k;
+      if (PF > 1 && t >= a.steps) break;
+      if (POIS) {
+        stim.at(a, ks, ps, t, n0, full, cur);
+      } else {
+#pragma unroll
+        // (PF > 1: an explicit add copies the value out, so the refill can
+        // land in pre[k]'s own register instead of a temporary moved back at
+        // the end of the step -- that move would wait for the load)
+        for (int j = 0; j < VEC; ++j) cur[j] = PF > 1 ? __fadd_rn(pre[k][j], 0.0f) : pre[k][j];
+        if (PF > 1) load_row(t + PF, pre[k]);
+        else if (t + PF < a.steps) load_in(pre[k]);
+      }
+      body(t);
     }
   }
 #pragma unroll
@@ -1826,7 +1846,7 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   // 1.47e11 at 3 and 1.43e11 at 4, where 64 registers spill)
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
   const char* pf = getenv("HHB_JIT_FWD_PF");
-  src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 4);
+  src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 8);
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
   src += fmt("#define BWD2_MINB %d\n", bmb2 ? atoi(bmb2) : 6);
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
