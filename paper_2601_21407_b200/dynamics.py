@@ -599,6 +599,14 @@ def simulate(params, i_series, state0: NeuronState | None = None, record_state: 
         state0 = init_state(params, shape, device=D.require_cuda() if (on_dev or T > 0) else None)
     elif tuple(state0.v.shape) != shape and T > 0:
         raise UsageError(f"state shape {tuple(state0.v.shape)} does not match input shape {shape}")
+    else:
+        # the reference's hh_step computes in the state's dtype (dynamics.py:459,
+        # :564-566): a float32 state0 runs float32 arithmetic even with float64
+        # params, and vice versa
+        sd = _state_dtype(state0.v)
+        if sd is not None and sd != dtype:
+            params = params.with_(dtype=sd)
+            dtype = sd
     if T == 0:
         empty_v = (torch.empty((0,) + shape, dtype=D.torch_dtype(dtype), device=D.require_cuda())
                    if on_dev else np.empty((0,) + shape, dtype=np.float64))
@@ -630,6 +638,15 @@ def simulate(params, i_series, state0: NeuronState | None = None, record_state: 
 
 
 _PIPELINE_MIN_ELEMS = 1 << 22
+
+
+def _state_dtype(v):
+    """float32 / float64 of a state array or tensor, None for anything else."""
+    try:
+        d = D.np_dtype(v.dtype) if isinstance(v, torch.Tensor) else np.dtype(np.asarray(v).dtype)
+    except Exception:
+        return None
+    return d if d in (np.dtype(np.float32), np.dtype(np.float64)) else None
 
 
 def _simulate_pipelined(params, i2, v, g, T, shape, record_state):

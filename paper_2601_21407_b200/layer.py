@@ -329,7 +329,11 @@ class HHLayer(torch.nn.Module):
     checkpoints are spaced ceil(T/budget) (make_plan, adjoint.py:250-258).
     overlap_weight_grad=True computes dW / db on a side stream, overlapping the
     previous layer's BPTT in a stack; the grads land in .grad when the
-    backward pass ends.
+    backward pass ends.  Limitation of that mode: autograd itself receives
+    None for weight and bias, so torch.autograd.grad(loss, [weight]), tensor /
+    module gradient hooks and DDP bucket hooks never see these gradients, and
+    .grad is written even under autograd.grad -- use the default
+    (overlap_weight_grad=False) with those APIs.
     """
 
     def __init__(self, n_in: int, n_out: int, params: HHParams | None = None, budget: int | None = None,

@@ -423,6 +423,8 @@ class CortexNetwork:
             key = (row << 32) | self.tgt.long()
             del row
             key, perm = torch.sort(key, stable=True)
+            # the arrays are replaced: graphs captured on the old pointers are stale
+            self._graphs.clear()
             self.tgt = self.tgt[perm].contiguous()
             self.w = self.w[perm].contiguous()
             self.delay = self.delay[perm].contiguous()
@@ -439,8 +441,9 @@ class CortexNetwork:
         mode = 2 if (self.bg_mode == "philox" and self.bg_spec.rate_hz > 0) else 0
         W = self.words_global
         if record is not None:
-            if record.dtype != torch.int32 or not record.is_contiguous() or tuple(record.shape) < (n_steps, W):
-                raise UsageError("record must be a contiguous int32 [n_steps][words] tensor")
+            if (record.dtype != torch.int32 or not record.is_contiguous() or record.dim() != 2
+                    or record.shape[0] < n_steps or record.shape[1] != W or record.device != self.v.device):
+                raise UsageError(f"record must be a contiguous int32 [>= {n_steps}][{W}] tensor on {self.v.device}")
             bits, rec = record, 1
         else:
             if getattr(self, "_pingpong", None) is None:
@@ -947,7 +950,9 @@ class CortexReplicas:
         [n_steps][replicas][n_pad/32] spike words."""
         if n_steps > 0 and self.persistent_ok():
             try:
-                return self._advance_persistent(n_steps, record)
+                out = self._advance_persistent(n_steps, record)
+                _raise_if_bad(self.first_bad)
+                return out
             except NativeLibraryError as e:
                 if "hh_net" not in str(e) and "unavailable" not in str(e):
                     raise

@@ -434,3 +434,18 @@ def test_naive_reference_module_matches_fused(cuda):
     assert np.allclose(tr_n.v_series, np.asarray(g["v"])[:T], rtol=1e-9, atol=1e-9)
     s1, sp = R.naive_hh_step(Dy.init_state(p, (3,)), np.array([0.0, 5.0, 50.0]), p)
     assert s1.v.shape == (3,) and sp.dtype == bool
+
+
+def test_state0_dtype_selects_the_arithmetic(cuda):
+    """simulate computes in state0's dtype, as the reference's hh_step does
+    (dynamics.py:459): a float32 state0 with float64 params runs float32."""
+    p64 = DF.squid_axon_params(dt=0.01)
+    i = np.full((300, 8), 10.0)
+    s32 = Dy.init_state(p64.with_(dtype=np.float32), (8,))
+    tr = Dy.simulate(p64, i, state0=s32)
+    ref32 = Dy.simulate(p64.with_(dtype=np.float32), i)
+    ref64 = Dy.simulate(p64, i)
+    assert np.array_equal(tr.v_series, ref32.v_series)
+    assert not np.array_equal(tr.v_series, ref64.v_series)
+    v_o, _ = O.simulate(p64, i, v0=s32.v, g0=s32.gates, dtype=np.float32)
+    assert np.max(np.abs(tr.v_series - v_o)) < 0.05

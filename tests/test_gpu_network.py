@@ -320,3 +320,50 @@ def test_persistent_replicas_equal_graph_replicas(cuda, monkeypatch):
     assert ra.any() and torch.equal(ra, rb)
     for x, y in ((a.v, b.v), (a.g, b.g), (a.psp, b.psp), (a.ring, b.ring)):
         assert torch.equal(x, y)
+
+
+def test_record_buffer_shape_is_checked(cuda):
+    """The persistent path writes n_steps * words int32 at a row pitch of
+    exactly `words`: a record of the wrong row width, too few rows or another
+    rank is refused (UsageError), a taller one is accepted."""
+    from paper_2601_21407_b200.errors import UsageError
+    _, topo = _small()
+    net = N.CortexNetwork(topo, N.REST_CONFIG, device=cuda, dtype=np.float32, background="philox", seed=2)
+    W = net.words_global
+    for shape in ((10, W + 3), (9, W), (10, 1)):
+        with pytest.raises(UsageError):
+            net.advance(10, record=torch.zeros(shape, dtype=torch.int32, device=cuda))
+    with pytest.raises(UsageError):
+        net.advance(10, record=torch.zeros((10, W), dtype=torch.int64, device=cuda))
+    tall = torch.zeros((15, W), dtype=torch.int32, device=cuda)
+    net.advance(10, record=tall)
+    assert not tall[10:].any()
+
+
+def test_graphs_captured_before_segment_sort_are_dropped(cuda, monkeypatch):
+    """A graph captured on the unsorted synapse arrays must not be replayed
+    after the persistent path re-sorted them (the old buffers are freed)."""
+    _, topo = _small()
+    monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    a = N.CortexNetwork(topo, N.REST_CONFIG, device=cuda, dtype=np.float32, background="philox", seed=3)
+    b = N.CortexNetwork(topo, N.REST_CONFIG, device=cuda, dtype=np.float32, background="philox", seed=3)
+    a.advance(40, steps_per_graph=20)
+    b.advance(40, steps_per_graph=20)
+    monkeypatch.setenv("HHB_NET_GRAPH", "0")
+    a.advance(30)                                   # persistent: sorts the rows
+    assert not a._graphs
+    monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    a.advance(40, steps_per_graph=20)               # recaptured on the sorted arrays
+    b.advance(70, steps_per_graph=10)
+    assert torch.equal(a.v, b.v) and torch.equal(a.ring, b.ring)
+
+
+def test_persistent_replicas_report_non_finite_state(cuda, monkeypatch):
+    from paper_2601_21407_b200.errors import NumericalOverflowError
+    _, topo = _small()
+    monkeypatch.setenv("HHB_NET_REPLICAS_PERSIST", "1")
+    r = N.CortexReplicas(topo, N.REST_CONFIG, 2, device=cuda, dtype=np.float32, seed=4)
+    r.advance(5)
+    r.psp[3] = float("inf")
+    with pytest.raises(NumericalOverflowError):
+        r.advance(5)
