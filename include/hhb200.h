@@ -284,6 +284,13 @@ int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int
 /* row-wise bf16x2 split: dst[r][c] = hi(src[r][c]), dst[r][cols + c] = lo */
 int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst,
                         int64_t ldd, void* stream);
+/* row-wise three-slot bf16 split (the fp32-class "bf16x3" projection):
+ * slots of `slot` (>= cols) elements per row; order 0: [hi | lo | hi],
+ * order 1: [hi | hi | lo].  A bf16 GEMM over K = 3 slot of an order-0 A and
+ * an order-1 B is x_h.W_h + x_l.W_h + x_h.W_l (~16 mantissa bits of both
+ * operands; replaces the float64 x @ W.T of DenseLayer, learn.py:210-211). */
+int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst,
+                    int64_t ldd, int64_t slot, int32_t order, void* stream);
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream);
 /* out[c] += sum_r src[r][c] (bias gradient, learn.py:273), fixed-order two-pass
  * reduction through hhb_col_sum_scratch(rows, cols) doubles of scratch */

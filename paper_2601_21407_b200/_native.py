@@ -116,6 +116,7 @@ SIGNATURES = {
     "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
     "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "hhb_split3_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp]),
     "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "hhb_col_sum_scratch": (_i64, [_i64, _i64]),
     "hhb_cortex_input": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _dbl, _dbl,

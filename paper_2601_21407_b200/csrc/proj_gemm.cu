@@ -846,6 +846,25 @@ __global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64
   }
 }
 
+// row-wise three-slot bf16 split for the fp32-class projection (bf16x3):
+// slots of width `slot` elements; order 0 writes [hi | lo | hi], order 1
+// [hi | hi | lo], so A3 . B3^T = xh.Wh + xl.Wh + xh.Wl (the x_lo.W_lo term,
+// ~2^-16 relative, is dropped).  Pad columns are left to the caller (zeros).
+__global__ void k_split3_rows(int64_t rows, int64_t cols, const float* src, int64_t lds, __nv_bfloat16* dst,
+                              int64_t ldd, int64_t slot, int order) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const float x = __ldg(src + r * lds + c);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    __nv_bfloat16* d = dst + r * ldd + c;
+    d[0] = hi;
+    d[slot] = order == 0 ? lo : hi;
+    d[2 * slot] = order == 0 ? hi : lo;
+  }
+}
+
 // 8 elements per thread: two 16-byte loads, one 16-byte store (16-byte aligned
 // src/dst, checked by the caller); the scalar kernel takes the rest
 __global__ void k_cast_bf16_v8(int64_t n8, const float4* src, uint4* dst) {
@@ -1297,6 +1316,16 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
   hhb::gemm::k_split_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
   return cuda_check("k_split_rows launch");
+}
+
+int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst, int64_t ldd,
+                    int64_t slot, int32_t order, void* stream) {
+  if (rows <= 0 || cols <= 0) return HHB_OK;
+  if (slot < cols || ldd < 3 * slot || (order != 0 && order != 1)) return fail(HHB_EINVAL, "split3 shape/order");
+  const dim3 grid{unsigned((cols + 255) / 256), unsigned(rows < 65535 ? rows : 65535), 1u};
+  hhb::gemm::k_split3_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd, slot, order);
+  return cuda_check("k_split3_rows launch");
 }
 
 int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {

@@ -73,6 +73,19 @@ def to_bf16_padded(x2: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def split3_padded(x2: torch.Tensor, order: int) -> tuple[torch.Tensor, int]:
+    """(rows, k) fp32 -> (rows, 3 kp) bf16 slots (kp = pad8(k)): order 0
+    [hi | lo | hi], order 1 [hi | hi | lo] (hhb_split3_bf16).  Returns the
+    buffer and the slot width kp."""
+    rows, k = x2.shape
+    kp = _pad8(k)
+    alloc = torch.empty if kp == k else torch.zeros
+    out = alloc((rows, 3 * kp), dtype=torch.bfloat16, device=x2.device)
+    nat.check(nat.load().hhb_split3_bf16(rows, k, x2.data_ptr(), x2.stride(0), out.data_ptr(), 3 * kp, kp, order,
+                                         _stream()), "split3")
+    return out, kp
+
+
 def grad_weight(dI: torch.Tensor, xb: torch.Tensor, k_in: int) -> torch.Tensor:
     """dW[N][k_in] = dI^T . xb  (dI (M, N) fp32, xb (M, >=k_in) bf16), bf16x2."""
     M, N = dI.shape
@@ -166,6 +179,17 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         if b >= 0:
             raise GradientOverflowError("adjoint state became non-finite", b)
     layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
+    x3 = layer.proj == "bf16x3"
+    kp = xb.shape[1] // 3 if x3 else 0
+
+    def weight_grad():
+        # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views;
+        # bf16x3: (dI_hi + dI_lo) . x_hi + dI_hi . x_lo (slots 0 and 1 of xb)
+        dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+        if x3:
+            dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, P, xb[:, kp:], xb.stride(0))
+        return dW
+
     if layer.overlap_weight_grad:
         # dW, db on a side stream: they overlap the previous layer's BPTT (CUDA
         # cores vs tensor cores); the grads are handed over when the backward
@@ -177,7 +201,7 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         fork.record(main)
         side.wait_event(fork)
         with torch.cuda.stream(side):
-            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+            dW = weight_grad()
             db = col_sum(dsum.view(B, n_out)).float()
             done = torch.cuda.Event()
             done.record(side)
@@ -199,12 +223,16 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         torch.autograd.Variable._execution_engine.queue_callback(hand_over)
         dW = db = None
     else:
-        # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views
-        dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+        dW = weight_grad()
         db = col_sum(dsum.view(B, n_out)).float()
-    # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W)
-    dX = (gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0)).view(T, B, k_in)
-          if x_requires_grad else None)
+    dX = None
+    if x_requires_grad:
+        # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W);
+        # bf16x3: (dI_hi + dI_lo) . W_hi + dI_hi . W_lo (slots 0 and 2 of wb)
+        dX = gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0))
+        if x3:
+            dX += gemm_ex(B_MN, M, k_in, n_out, hi, None, P, wb[:, 2 * kp:], wb.stride(0))
+        dX = dX.view(T, B, k_in)
     return dX, dW, db
 
 
@@ -220,6 +248,12 @@ def _side_stream(dev) -> torch.cuda.Stream:
 
 def _project(x, weight, bias, layer):
     T, B, k_in = x.shape
+    if layer.proj == "bf16x3":
+        # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
+        xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
+        wb, _ = split3_padded(weight.float().contiguous(), 1)
+        cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
+        return xb, wb, cur
     xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
     wb = to_bf16_padded(weight.float().contiguous())
     cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())        # (T*B, n_out) == (T, B*n_out)
@@ -334,13 +368,23 @@ class HHLayer(torch.nn.Module):
     module gradient hooks and DDP bucket hooks never see these gradients, and
     .grad is written even under autograd.grad -- use the default
     (overlap_weight_grad=False) with those APIs.
+
+    proj selects the projection precision: "bf16" (default; config 4's bf16
+    synaptic projection: x and W rounded to bf16, dI carried as bf16 hi + lo)
+    or "bf16x3" (x, W and dI all split into bf16 hi + lo, three tensor-core
+    products per GEMM: ~16 mantissa bits of every operand, the precision class
+    of the reference's float64 DenseLayer, learn.py:210-211, at ~3x the
+    projection FLOPs).
     """
 
     def __init__(self, n_in: int, n_out: int, params: HHParams | None = None, budget: int | None = None,
                  surrogate: SurrogateSpec | None = None, w_mean: float = 0.0, w_std: float | None = None,
                  check_finite: bool = True, device=None, outputs: str = "both",
-                 overlap_weight_grad: bool = False):
+                 overlap_weight_grad: bool = False, proj: str = "bf16"):
         super().__init__()
+        if proj not in ("bf16", "bf16x3"):
+            raise UsageError('proj must be "bf16" or "bf16x3"')
+        self.proj = proj
         self.overlap_weight_grad = bool(overlap_weight_grad)
         if outputs not in ("both", "v", "spikes"):
             raise UsageError('outputs must be "both", "v" or "spikes"')

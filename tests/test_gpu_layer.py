@@ -191,3 +191,53 @@ def test_overlapped_weight_grads_match(cuda):
         grads.append([t.grad.clone() for t in (l1.weight, l1.bias, l2.weight, l2.bias)])
     for a, b in zip(*grads):
         assert torch.allclose(a, b, rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("budget,n_out", [(None, 8), (4, 10), (None, 16)])
+def test_layer_bf16x3_matches_unrounded_oracle(cuda, budget, n_out):
+    """proj="bf16x3" against the reference composition on the UNROUNDED
+    operands (the float32 x and W taken exactly into float64, learn.py:210-211
+    computing in float64): the same contract as above."""
+    T, B, k_in = 40, 3, 20                  # k_in % 8 != 0: padded slots
+    torch.manual_seed(0)
+    layer = HHLayer(k_in, n_out, DF.cortical_rs_params(dt=0.1), budget=budget, w_mean=0.7, w_std=0.5,
+                    device=cuda, proj="bf16x3")
+    with torch.no_grad():
+        layer.bias.copy_(torch.linspace(-1.0, 2.0, n_out, device=cuda))
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = ((torch.rand((T, B, k_in), device=cuda, generator=g) < 0.3).float()
+         + 0.1 * torch.randn((T, B, k_in), device=cuda, generator=g)).requires_grad_(True)
+    V, S = layer(x)
+    ((V ** 2).mean()).backward()
+    xd = x.detach().double().cpu().numpy()
+    wd = layer.weight.detach().double().cpu().numpy()
+    drive = xd @ wd.T + layer.bias.detach().double().cpu().numpy()
+    p = DF.cortical_rs_params(dt=0.1)
+    v_ref, s_ref = O.simulate(p, drive.reshape(T, -1))
+    assert np.array_equal(S.detach().cpu().numpy().reshape(T, -1).astype(bool), s_ref)
+    v0, g0 = O.rest_state(p, B * n_out)
+    res = O.bptt(p, v0, g0, drive.reshape(T, -1), 2.0 * v_ref / v_ref.size)
+    dd = res["d_i"].reshape(T, B, n_out)
+    assert nrel(layer.weight.grad.cpu().numpy(), np.einsum("tbc,tbk->ck", dd, xd)) < 1e-3
+    assert nrel(layer.bias.grad.cpu().numpy(), dd.sum(axis=(0, 1))) < 1e-3
+    assert nrel(x.grad.cpu().numpy(), dd @ wd) < 1e-3
+    pg = layer.param_grads.cpu().numpy()
+    assert abs(pg[0] - res["d_c_m"]) <= 1e-3 * abs(res["d_c_m"])
+    assert nrel(pg[1:], res["d_g_max"]) < 1e-3
+
+
+def test_config3_full_shape_unrounded_bf16x3_within_contract(cuda):
+    """Config 3 at its full shape, proj="bf16x3", against the float64 kernels
+    on the unrounded float64 x and W (tools/parity_c3.py --unrounded)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tools/parity_c3.py", "--unrounded", "--proj", "bf16x3"], cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("dW", "db", "dX", "d_c_m", "d_g_max"):
+        assert r[k] < 1e-3, (k, r[k])
+    assert r["loss_rel"] < 1e-4

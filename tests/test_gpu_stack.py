@@ -1,0 +1,137 @@
+"""Config-4 composition parity: a scaled-down stacked HH SNN (24 -> 32 -> 32 -> 10,
+B 4, T 80, RS neurons, bf16 projections) trained exactly as the bench's config-4
+step (hidden layers hand on spikes only, the readout layer V only, softmax
+cross-entropy on the time-mean output V) against the oracle composition of the
+reference's pieces:
+
+  forward   drive_l = h_{l-1} . W_l^T + b_l          (learn.py:210-211)
+            V_l, S_l = simulate(drive_l)              (dynamics.py:541-586)
+            h_l = S_l (0/1 spikes, exact in bf16)
+  loss      CE(mean_t V_3, y)                         (learn.py:92-107)
+  backward  BPTT(seed_v, seed_spike)                  (adjoint.py:281-365, :354-359)
+            dW_l = sum_{t,b} d_drive (x) h_{l-1}      (learn.py:272)
+            seed_spike of layer l-1 = d_drive_l . W_l (the dX of layer l)
+
+Operands are bf16-rounded x and W cast back to float64 (config 4 states bf16
+projections), so only accumulation order and float32 state
+differ.  Contract: identical spikes in every layer; loss within
+1e-5; dW, db, d_c_m, d_g_max of every layer and dX of the input within 1e-3
+normwise.  The parameters were chosen with the oracle so that every layer spikes
+and the reference's own float32 mode reproduces every layer's raster.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hh_oracle as O
+from paper_2601_21407_b200 import defaults as DF
+from paper_2601_21407_b200.layer import HHLayer
+
+T, B = 80, 4
+SIZES = [24, 32, 32, 10]
+W_MEAN_STD = [(0.5, 0.5), (3.0, 2.0), (3.0, 2.0)]
+BIAS = [(2.0, 6.0), (6.0, 9.0), (2.0, 6.0)]
+
+
+def bf16(a):
+    return torch.tensor(np.asarray(a), dtype=torch.float32).to(torch.bfloat16).double().numpy()
+
+
+def nrel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def problem():
+    rng = np.random.default_rng(7)
+    x = bf16((rng.random((T, B, SIZES[0])) < 0.3) + 0.1 * rng.standard_normal((T, B, SIZES[0])))
+    Ws, bs = [], []
+    for l in range(3):
+        Ws.append(bf16(rng.normal(*W_MEAN_STD[l], (SIZES[l + 1], SIZES[l]))))
+        bs.append(np.linspace(*BIAS[l], SIZES[l + 1]).astype(np.float32).astype(np.float64))
+    y = rng.integers(0, SIZES[-1], B)
+    return x, Ws, bs, y
+
+
+def oracle_stack(p, x, Ws, bs, y):
+    drives, spikes, inputs = [], [], []
+    h = x
+    v = None
+    for W, b in zip(Ws, bs):
+        inputs.append(h)
+        d = h @ W.T + b
+        v, s = O.simulate(p, d.reshape(T, -1))
+        drives.append(d)
+        spikes.append(s.reshape(T, B, -1))
+        h = s.reshape(T, B, -1).astype(np.float64)
+    logits = v.reshape(T, B, -1).mean(0)
+    loss, d_logits = O.cross_entropy_loss(logits, y)
+    seed_v = np.broadcast_to(d_logits / T, (T, B, SIZES[-1])).copy()
+    seed_s = None
+    out = [None] * 3
+    for l in (2, 1, 0):
+        n = SIZES[l + 1]
+        v0, g0 = O.rest_state(p, B * n)
+        sv = seed_v if seed_v is not None else np.zeros((T, B, n))
+        res = O.bptt(p, v0, g0, drives[l].reshape(T, -1), sv.reshape(T, -1),
+                     seed_spike=None if seed_s is None else seed_s.reshape(T, -1))
+        dd = res["d_i"].reshape(T, B, n)
+        dX = dd @ Ws[l]
+        out[l] = {"dW": np.einsum("tbc,tbk->ck", dd, inputs[l]), "db": dd.sum(axis=(0, 1)), "dX": dX,
+                  "d_c_m": res["d_c_m"], "d_g_max": res["d_g_max"]}
+        seed_s, seed_v = dX, None
+    return loss, spikes, out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [False, True])
+def test_config4_stack_matches_oracle_composition(cuda, overlap):
+    p = DF.cortical_rs_params(dt=0.1)
+    x, Ws, bs, y = problem()
+    outs = ["spikes", "spikes", "v"]
+    net = [HHLayer(SIZES[l], SIZES[l + 1], p, device=cuda, outputs=outs[l], overlap_weight_grad=overlap)
+           for l in range(3)]
+    with torch.no_grad():
+        for lyr, W, b in zip(net, Ws, bs):
+            lyr.weight.copy_(torch.tensor(W, dtype=torch.float32))
+            lyr.bias.copy_(torch.tensor(b, dtype=torch.float32))
+    xt = torch.tensor(x, dtype=torch.float32, device=cuda).requires_grad_(True)
+    h = xt
+    hidden = []
+    for lyr in net[:-1]:
+        _, h = lyr(h)
+        hidden.append(h)
+    v, _ = net[-1](h)
+    loss = torch.nn.functional.cross_entropy(v.mean(0), torch.tensor(y, device=cuda))
+    loss.backward()
+    torch.cuda.synchronize()
+
+    loss_ref, spikes_ref, ref = oracle_stack(p, x, Ws, bs, y)
+    for l in range(2):
+        got = hidden[l].detach().cpu().numpy().astype(bool)
+        assert np.array_equal(got, spikes_ref[l]), f"layer {l} raster differs"
+        assert spikes_ref[l].sum() > 0
+    assert abs(loss.item() - loss_ref) <= 1e-5 * abs(loss_ref)
+    for l, lyr in enumerate(net):
+        r = ref[l]
+        assert nrel(lyr.weight.grad.cpu().numpy(), r["dW"]) < 1e-3, (l, "dW")
+        assert nrel(lyr.bias.grad.cpu().numpy(), r["db"]) < 1e-3, (l, "db")
+        pg = lyr.param_grads.cpu().numpy()
+        assert abs(pg[0] - r["d_c_m"]) <= 1e-3 * abs(r["d_c_m"]), (l, "d_c_m")
+        assert nrel(pg[1:], r["d_g_max"]) < 1e-3, (l, "d_g_max")
+    assert nrel(xt.grad.cpu().numpy(), ref[0]["dX"]) < 1e-3
+
+
+def test_config4_oracle_problem_is_well_posed():
+    """CPU check of the fixture itself: every layer spikes, and the reference's
+    own float32 mode gives the float64 rasters (so a float32 kernel can too)."""
+    p = DF.cortical_rs_params(dt=0.1)
+    x, Ws, bs, _ = problem()
+    h64 = h32 = x
+    for W, b in zip(Ws, bs):
+        _, s64 = O.simulate(p, (h64 @ W.T + b).reshape(T, -1))
+        _, s32 = O.simulate(p, (h32 @ W.T + b).reshape(T, -1), dtype=np.float32)
+        assert np.array_equal(s64, s32) and s64.sum() > 0
+        h64 = s64.reshape(T, B, -1).astype(np.float64)
+        h32 = s32.reshape(T, B, -1).astype(np.float64)
