@@ -37,64 +37,22 @@ sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 
+from contract import attribute, neuron_failures
 from oracle import hh_oracle as O
 from paper_2601_21407_b200 import defaults as DF
 from paper_2601_21407_b200.dynamics import _forward, _unpack, init_state
 from paper_2601_21407_b200.population import PoissonCurrent
 
 
-def neuron_failures(v, s, v_ref, s_ref):
-    """Per-neuron contract of check_fp32_contract (vectorised): returns a bool
-    mask of failing neurons and a reason string per failing neuron."""
-    T, n = v_ref.shape
-    fail = np.zeros(n, bool)
-    why = {}
-    cnt, cnt_ref = s.sum(0), s_ref.sum(0)
-    for j in np.flatnonzero(cnt != cnt_ref):
-        fail[j] = True
-        why[j] = f"count {int(cnt[j])} vs {int(cnt_ref[j])}"
-    for j in np.flatnonzero((cnt == cnt_ref) & (cnt > 0)):
-        a, b = np.flatnonzero(s[:, j]), np.flatnonzero(s_ref[:, j])
-        if np.any(np.abs(a - b) > 1):
-            fail[j] = True
-            why[j] = f"spike steps off by {int(np.abs(a - b).max())}"
-    first = np.where(s_ref.any(0), s_ref.argmax(0), T)
-    bad = np.abs(v - v_ref) > 1e-4 * np.abs(v_ref) + 0.02
-    before = np.arange(T)[:, None] < first[None, :]
-    vbad = (bad & before).any(0)
-    for j in np.flatnonzero(vbad & ~fail):
-        fail[j] = True
-        t = int(np.flatnonzero(bad[:, j] & before[:, j])[0])
-        why[j] = f"pre-spike V at step {t}: {v[t, j]:.6f} vs {v_ref[t, j]:.6f}"
-    return fail, why
-
-
-def attribute(p64, cols, v32, s32):
+def attribute_listed(p64, cols, v32, s32):
     """cols (T, K) float64 stimulus of the listed neurons; v32/s32 our float32
-    kernel's trace of them.  Returns per-neuron verdicts."""
+    kernel's trace of them.  Returns per-neuron verdicts against the oracle."""
     v64, s64 = O.simulate(p64, cols)
     ours_fail, ours_why = neuron_failures(v32, s32, v64, s64)
-    vr32, sr32 = O.simulate(p64, cols, dtype=np.float32)
-    ref32_fail, ref32_why = neuron_failures(vr32, sr32, v64, s64)
-    ill = np.zeros(cols.shape[1], bool)
-    rng = np.random.default_rng(99)
-    for _ in range(8):
-        u = rng.choice([-1.0, 1.0], size=cols.shape)
-        vp, sp = O.simulate(p64, cols * (1.0 + u * 2.0 ** -24))
-        f, _ = neuron_failures(vp, sp, v64, s64)
-        ill |= f
-    out = []
-    for k in range(cols.shape[1]):
-        if not ours_fail[k]:
-            verdict = "passes against the oracle"       # failed only against the float64 kernel's chunk ends
-        elif ref32_fail[k]:
-            verdict = "explained: reference float32 also fails (" + ref32_why[k] + ")"
-        elif ill[k]:
-            verdict = "explained: ill-conditioned (one-ulp stimulus perturbation of the float64 reference fails)"
-        else:
-            verdict = "unexplained"
-        out.append({"ours": ours_why.get(k, "ok"), "verdict": verdict})
-    return out
+    verdicts = attribute(p64, cols, np.flatnonzero(ours_fail), v64, s64)
+    return [{"ours": ours_why.get(k, "ok"),
+             "verdict": verdicts.get(k, "passes against the oracle (failed only a chunk-end check against the "
+                                        "float64 kernel)")} for k in range(cols.shape[1])]
 
 
 def main():
@@ -161,7 +119,7 @@ def main():
         "prespike_v_checks": v_checked, "prespike_v_violation_neurons": int(vbad.sum().item()),
         "listed_vs_fp64_kernel": int(ids.size),
     }
-    # re-run the listed neurons (and, for a control, as many passing ones) through the oracle
+    # re-run the listed neurons through the oracle
     ids = ids[:a.max_list]
     if ids.size:
         cols = torch.empty((T, ids.size), dtype=torch.float32, device=dev)
@@ -172,11 +130,11 @@ def main():
         bb = torch.empty((T, (ids.size + 31) // 32), dtype=torch.int32, device=dev)
         _forward(p32, st.v.contiguous(), st.gates.contiguous(), cols, ids.size, 1, T, v_out=vv, bits=bb)
         ss = _unpack(bb, T, ids.size).cpu().numpy().astype(bool)
-        verdicts = attribute(p64, cols.double().cpu().numpy(), vv.double().cpu().numpy(), ss)
+        verdicts = attribute_listed(p64, cols.double().cpu().numpy(), vv.double().cpu().numpy(), ss)
         # the kernel's own spike counts on the re-run match the population run's (independence)
         assert np.array_equal(ss.sum(0), cnt32[torch.as_tensor(ids, device=dev)].cpu().numpy())
         res["listed"] = [{"neuron": int(j), **vd} for j, vd in zip(ids.tolist(), verdicts)]
-        kinds = [vd["verdict"].split(":")[0] for vd in verdicts]
+        kinds = [vd["verdict"] for vd in verdicts]
         res["failing_vs_oracle"] = sum(vd["ours"] != "ok" for vd in verdicts)
         res["explained_ref_fp32"] = sum("reference float32" in vd["verdict"] for vd in verdicts)
         res["explained_ill_conditioned"] = sum("ill-conditioned" in vd["verdict"] for vd in verdicts)

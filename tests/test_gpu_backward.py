@@ -203,3 +203,67 @@ def test_device_tensors_path(cuda):
     assert isinstance(r.d_i, torch.Tensor) and r.d_i.is_cuda and r.d_i.dtype == torch.float32
     r2 = A.backward_through_time(p, s0, i.cpu().numpy(), sv.cpu().numpy(), plan=A.make_plan(60, 6))
     assert np.array_equal(r.d_i.cpu().numpy(), r2.d_i.astype(np.float32))
+
+
+def _fd_chains(cuda, p, n, T, rng, h=1e-5, hp=1e-5):
+    """n independent chains (one neuron each) of one parameter set: random
+    drive and random membrane-potential loss L_j = sum_t w[t, j] V[t, j]."""
+    mu = rng.uniform(0.0, 15.0, size=n)
+    i = rng.normal(mu, 3.0, size=(T, n))
+    w = rng.normal(0.0, 1.0, size=(T, n))
+    s0 = Dy.init_state(p, (n,))
+    it = torch.as_tensor(i, device=cuda)
+    res = A.backward_through_time(p, Dy.init_state(p, (n,), device=cuda), it, torch.as_tensor(w, device=cuda))
+    d_i = res.d_i.cpu().numpy()
+
+    def v_of(ii, q=p):
+        return Dy.simulate(q, torch.as_tensor(ii, device=cuda), state0=Dy.init_state(q, (n,), device=cuda)) \
+            .v_series.cpu().numpy()
+
+    errs = []
+    # d_i at three random steps per chain, all chains at once (chains are independent)
+    for _ in range(3):
+        ts = rng.integers(0, T, size=n)
+        ip, im = i.copy(), i.copy()
+        ip[ts, np.arange(n)] += h
+        im[ts, np.arange(n)] -= h
+        fd = (w * (v_of(ip) - v_of(im))).sum(0) / (2 * h)
+        ad = d_i[ts, np.arange(n)]
+        floor = 1e-6 * np.abs(d_i).max(0)
+        errs.append(np.abs(ad - fd) / np.maximum(np.abs(fd), floor))
+    # parameter gradients are population sums: one adjoint run per chain
+    d_cm = np.empty(n)
+    d_gm = np.empty((n, len(p.channels)))
+    for j in range(n):
+        r = A.backward_through_time(p, Dy.init_state(p, (1,), device=cuda), it[:, j:j + 1],
+                                    torch.as_tensor(w[:, j:j + 1], device=cuda))
+        d_cm[j] = r.d_c_m
+        d_gm[j] = np.asarray(r.d_g_max)
+    fd_cm = (w * (v_of(i, p.with_(c_m=p.c_m + hp)) - v_of(i, p.with_(c_m=p.c_m - hp)))).sum(0) / (2 * hp)
+    errs.append(np.abs(d_cm - fd_cm) / np.abs(fd_cm))
+    for ci, ch in enumerate(p.channels):
+        def with_g(dg):
+            chans = list(p.channels)
+            chans[ci] = Dy.ChannelSpec(ch.name, ch.g_max * (1 + dg), ch.e_rev, ch.gates)
+            return p.with_(channels=tuple(chans))
+        hg = hp * 10
+        fd_g = (w * (v_of(i, with_g(hg)) - v_of(i, with_g(-hg)))).sum(0) / (2 * hg * ch.g_max)
+        floor = 1e-6 * np.abs(d_gm).max()
+        errs.append(np.abs(d_gm[:, ci] - fd_g) / np.maximum(np.abs(fd_g), floor))
+    return np.concatenate(errs)
+
+
+def test_spec_acceptance1_fd_over_120_random_chains(cuda):
+    """SPEC.md:569 acceptance 1: over >= 100 random HH chains (T <= 100,
+    float64) the adjoint gradients match central finite differences within
+    1e-5 relative for membrane-potential losses.  120 chains = 40 each of the
+    squid, RS and config-2 parameter sets with random drive and random loss
+    weights; per chain d_i at 3 random steps, d_c_m and every d_g_max
+    (relative to max(|FD|, 1e-6 x the chain's largest gradient))."""
+    rng = np.random.default_rng(11)
+    errs = []
+    for p in (DF.squid_axon_params(dt=0.02), DF.cortical_rs_params(dt=0.05), DF.na_kdr_cal_kca_params(dt=0.02)):
+        errs.append(_fd_chains(cuda, p, 40, 100, rng))
+    e = np.concatenate(errs)
+    assert e.size >= 120 * 5
+    assert e.max() < 1e-5, float(e.max())

@@ -401,20 +401,48 @@ def test_neuron_shards_equal_one_population(cuda):
 
 def test_fp32_parity_config2_scale(cuda):
     """The bench path (float32 merged kernel) against the float64 kernel on the
-    config-2 stimulus at 1M neurons x 2,000 steps (tools/parity_fullscale.py;
-    the 10M x 10,000 run is in profiles/r1b_parity_fullscale.md)."""
+    config-2 Philox stimulus at 1M neurons x 2,000 steps
+    (tests/parity_fullscale.py; the 10M x 10,000 run is in
+    profiles/r2_parity_fullscale.md): every neuron failing a contract check is
+    listed and re-run through the oracle; none may stay unexplained."""
     import json
+    import os
     import subprocess
     import sys
-    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "tools/parity_fullscale.py", "--neurons", "1000000", "--steps", "2000"],
-                         cwd=root, capture_output=True, text=True, timeout=600)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tests/parity_fullscale.py", "--neurons", "1000000", "--steps", "2000"],
+                         cwd=root, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["spikes_fp64_total"] > 10 ** 6
-    assert r["count_equal_frac"] >= 0.9999 and r["count_diff_max"] <= 1
-    assert r["spiked_in_one_run_only"] == 0 and r["first_spike_pm1_frac_of_both"] == 1.0
-    assert r["prespike_v_violations"] <= 1e-5 * r["prespike_v_checks"]
+    assert r["listed_vs_fp64_kernel"] <= 1000                  # all of them attributed
+    assert r["unexplained"] == 0, [x for x in r["listed"] if x["verdict"] == "unexplained"]
+
+
+def test_config2_full_horizon_against_oracle(cuda):
+    """Config 2's channel set over its full 10,000-step horizon for 8,192
+    neurons on a host stimulus I = 2*Poisson(2) (np.random.default_rng(0),
+    SURVEY §8 d2), both builds against the ORACLE (the restated reference):
+    float64 within 1e-9 relative over the whole horizon with identical
+    spikes; float32 under the per-neuron contract with every failing neuron
+    listed and attributed (tests/contract.py) and none unexplained."""
+    from contract import check_against_oracle
+    p64 = DF.na_kdr_cal_kca_params(dt=0.01)
+    n, T = 8192, 10_000
+    i = 2.0 * np.random.default_rng(0).poisson(2.0, size=(T, n)).astype(np.float64)
+    v_ref, s_ref = O.simulate(p64, i)
+    assert s_ref.sum() > n                                 # every neuron fires on average
+    tr64 = Dy.simulate(p64, torch.as_tensor(i, device=cuda))
+    v64 = tr64.v_series.cpu().numpy()
+    assert np.array_equal(tr64.spike_series.cpu().numpy(), s_ref)
+    ok, err = _close64(v64, v_ref)
+    assert ok, err
+    del v64, tr64
+    p32 = p64.with_(dtype=np.float32)
+    tr32 = Dy.simulate(p32, torch.as_tensor(i, dtype=torch.float32, device=cuda))
+    rep = check_against_oracle(p64, i, tr32.v_series.cpu().numpy(), tr32.spike_series.cpu().numpy(), v_ref, s_ref)
+    print(rep["failing"], rep["listed"][:20])
+    assert rep["unexplained"] == 0, [x for x in rep["listed"] if x["verdict"] == "unexplained"]
 
 
 def test_naive_reference_module_matches_fused(cuda):

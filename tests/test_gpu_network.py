@@ -367,3 +367,43 @@ def test_persistent_replicas_report_non_finite_state(cuda, monkeypatch):
     r.psp[3] = float("inf")
     with pytest.raises(NumericalOverflowError):
         r.advance(5)
+
+
+def test_spec_acceptance8_compound_poisson_1e6_draws(cuda):
+    """SPEC.md:576 acceptance 8 / :407: 10^6 draws of the device compound-Poisson
+    sampler (hhb_cortex_input bg_mode 2, Philox keyed by (seed, neuron, step))
+    at lam = 3, mu = 0.17, sigma = 0.017: sample mean within 1 % of lam mu and
+    variance within 1 % of lam (mu^2 + sigma^2)."""
+    from paper_2601_21407_b200 import _native as nat
+    lib = nat.load()
+    n, depth = 250_000, 2
+    lam = torch.full((n,), 3.0, dtype=torch.float64, device=cuda)
+    ring = torch.zeros((depth, n), dtype=torch.int64, device=cuda)
+    psp = torch.zeros(n, dtype=torch.float64, device=cuda)
+    cur = torch.empty(n, dtype=torch.float64, device=cuda)
+    draws = []
+    for t in range(4):                       # 4 steps x 250,000 neurons = 10^6 draws
+        psp.zero_()
+        nat.check(lib.hhb_cortex_input(1, n, t, depth, ring.data_ptr(), psp.data_ptr(), 0.0, 2, None,
+                                       lam.data_ptr(), 0.17, 0.017, 2024, 0, None, cur.data_ptr(), 1.0,
+                                       torch.cuda.current_stream().cuda_stream), "cortex_input")
+        draws.append(cur.clone())
+    x = torch.cat(draws).cpu().numpy()
+    assert x.size == 10 ** 6
+    mean, var = 3 * 0.17, 3 * (0.17 ** 2 + 0.017 ** 2)
+    assert abs(x.mean() - mean) < 0.01 * mean, x.mean()
+    assert abs(x.var() - var) < 0.01 * var, x.var()
+    # the trivial cases of SPEC.md:405-406: lam = 0 gives 0; sigma = 0 gives N mu
+    lam.zero_()
+    psp.zero_()
+    nat.check(lib.hhb_cortex_input(1, n, 9, depth, ring.data_ptr(), psp.data_ptr(), 0.0, 2, None, lam.data_ptr(),
+                                   0.17, 0.017, 2024, 0, None, cur.data_ptr(), 1.0,
+                                   torch.cuda.current_stream().cuda_stream), "cortex_input")
+    assert torch.count_nonzero(cur).item() == 0
+    lam.fill_(3.0)
+    psp.zero_()
+    nat.check(lib.hhb_cortex_input(1, n, 9, depth, ring.data_ptr(), psp.data_ptr(), 0.0, 2, None, lam.data_ptr(),
+                                   0.17, 0.0, 2024, 0, None, cur.data_ptr(), 1.0,
+                                   torch.cuda.current_stream().cuda_stream), "cortex_input")
+    k = (cur / 0.17).cpu().numpy()
+    assert np.allclose(k, np.round(k), atol=1e-9)
