@@ -205,9 +205,12 @@ def test_device_tensors_path(cuda):
     assert np.array_equal(r.d_i.cpu().numpy(), r2.d_i.astype(np.float32))
 
 
-def _fd_chains(cuda, p, n, T, rng, h=1e-5, hp=1e-5):
+def _fd_chains(cuda, p, n, T, rng, h=2e-5, hp=2e-5):
     """n independent chains (one neuron each) of one parameter set: random
-    drive and random membrane-potential loss L_j = sum_t w[t, j] V[t, j]."""
+    drive and random membrane-potential loss L_j = sum_t w[t, j] V[t, j].
+    Central differences with one Richardson step, (4 D(h/2) - D(h)) / 3
+    (truncation O(h^4): the spike upstroke makes V strongly nonlinear in
+    I and the parameters); each difference sums w (V+ - V-) elementwise."""
     mu = rng.uniform(0.0, 15.0, size=n)
     i = rng.normal(mu, 3.0, size=(T, n))
     w = rng.normal(0.0, 1.0, size=(T, n))
@@ -224,13 +227,16 @@ def _fd_chains(cuda, p, n, T, rng, h=1e-5, hp=1e-5):
     # d_i at three random steps per chain, all chains at once (chains are independent)
     for _ in range(3):
         ts = rng.integers(0, T, size=n)
-        ip, im = i.copy(), i.copy()
-        ip[ts, np.arange(n)] += h
-        im[ts, np.arange(n)] -= h
-        fd = (w * (v_of(ip) - v_of(im))).sum(0) / (2 * h)
+        def d(hh):
+            ip, im = i.copy(), i.copy()
+            ip[ts, np.arange(n)] += hh
+            im[ts, np.arange(n)] -= hh
+            return (w * (v_of(ip) - v_of(im))).sum(0) / (2 * hh)
+        fd = (4 * d(h / 2) - d(h)) / 3
         ad = d_i[ts, np.arange(n)]
         floor = 1e-6 * np.abs(d_i).max(0)
         errs.append(np.abs(ad - fd) / np.maximum(np.abs(fd), floor))
+        print("d_i", p.channels[0].name, float(errs[-1].max()))
     # parameter gradients are population sums: one adjoint run per chain
     d_cm = np.empty(n)
     d_gm = np.empty((n, len(p.channels)))
@@ -239,17 +245,22 @@ def _fd_chains(cuda, p, n, T, rng, h=1e-5, hp=1e-5):
                                     torch.as_tensor(w[:, j:j + 1], device=cuda))
         d_cm[j] = r.d_c_m
         d_gm[j] = np.asarray(r.d_g_max)
-    fd_cm = (w * (v_of(i, p.with_(c_m=p.c_m + hp)) - v_of(i, p.with_(c_m=p.c_m - hp)))).sum(0) / (2 * hp)
+    def d_cm_fd(hh):
+        return (w * (v_of(i, p.with_(c_m=p.c_m + hh)) - v_of(i, p.with_(c_m=p.c_m - hh)))).sum(0) / (2 * hh)
+    fd_cm = (4 * d_cm_fd(hp / 2) - d_cm_fd(hp)) / 3
     errs.append(np.abs(d_cm - fd_cm) / np.abs(fd_cm))
+    print("d_c_m", float(errs[-1].max()))
     for ci, ch in enumerate(p.channels):
         def with_g(dg):
             chans = list(p.channels)
             chans[ci] = Dy.ChannelSpec(ch.name, ch.g_max * (1 + dg), ch.e_rev, ch.gates)
             return p.with_(channels=tuple(chans))
-        hg = hp * 10
-        fd_g = (w * (v_of(i, with_g(hg)) - v_of(i, with_g(-hg)))).sum(0) / (2 * hg * ch.g_max)
+        def d_g(hh):
+            return (w * (v_of(i, with_g(hh)) - v_of(i, with_g(-hh)))).sum(0) / (2 * hh * ch.g_max)
+        fd_g = (4 * d_g(hp / 2) - d_g(hp)) / 3
         floor = 1e-6 * np.abs(d_gm).max()
         errs.append(np.abs(d_gm[:, ci] - fd_g) / np.maximum(np.abs(fd_g), floor))
+        print("d_g_max", ch.name, float(errs[-1].max()))
     return np.concatenate(errs)
 
 
@@ -266,4 +277,5 @@ def test_spec_acceptance1_fd_over_120_random_chains(cuda):
         errs.append(_fd_chains(cuda, p, 40, 100, rng))
     e = np.concatenate(errs)
     assert e.size >= 120 * 5
+    print("FD max rel err", float(e.max()), "p99", float(np.quantile(e, 0.99)))
     assert e.max() < 1e-5, float(e.max())

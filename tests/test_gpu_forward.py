@@ -429,7 +429,8 @@ def test_config2_full_horizon_against_oracle(cuda):
     from contract import check_against_oracle
     p64 = DF.na_kdr_cal_kca_params(dt=0.01)
     n, T = 8192, 10_000
-    i = 2.0 * np.random.default_rng(0).poisson(2.0, size=(T, n)).astype(np.float64)
+    i_ext = 2.0 * np.random.default_rng(0).poisson(2.0, size=(T + 2, n)).astype(np.float64)
+    i = i_ext[:T]
     v_ref, s_ref = O.simulate(p64, i)
     assert s_ref.sum() > n                                 # every neuron fires on average
     tr64 = Dy.simulate(p64, torch.as_tensor(i, device=cuda))
@@ -439,8 +440,13 @@ def test_config2_full_horizon_against_oracle(cuda):
     assert ok, err
     del v64, tr64
     p32 = p64.with_(dtype=np.float32)
-    tr32 = Dy.simulate(p32, torch.as_tensor(i, dtype=torch.float32, device=cuda))
-    rep = check_against_oracle(p64, i, tr32.v_series.cpu().numpy(), tr32.spike_series.cpu().numpy(), v_ref, s_ref)
+
+    def ours(cols):
+        tr = Dy.simulate(p32, torch.as_tensor(cols, dtype=torch.float32, device=cuda))
+        return tr.v_series.cpu().numpy(), tr.spike_series.cpu().numpy()
+
+    v32, s32 = ours(i)
+    rep = check_against_oracle(p64, i, v32, s32, v_ref, s_ref, ours_ext=ours, i_ext=i_ext)
     print(rep["failing"], rep["listed"][:20])
     assert rep["unexplained"] == 0, [x for x in rep["listed"] if x["verdict"] == "unexplained"]
 

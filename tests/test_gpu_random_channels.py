@@ -70,8 +70,15 @@ def test_random_channel_tables_forward_and_bptt(cuda, seed):
     assert np.array_equal(tr64.spike_series.cpu().numpy(), s_ref)
     err = np.abs(v64.cpu().numpy() - v_ref)
     assert np.all(err <= 1e-9 * np.abs(v_ref) + 1e-9), float(err.max())
-    tr32 = Dy.simulate(p32, i, state0=Dy.init_state(p32, (n,), device=cuda))
-    rep = check_against_oracle(p64, ih, tr32.v_series.cpu().numpy(), tr32.spike_series.cpu().numpy(), v_ref, s_ref)
+
+    def ours(cols):
+        tr = Dy.simulate(p32, torch.as_tensor(cols, dtype=torch.float32, device=cuda),
+                         state0=Dy.init_state(p32, (cols.shape[1],), device=cuda))
+        return tr.v_series.cpu().numpy(), tr.spike_series.cpu().numpy()
+
+    v32, s32 = ours(ih)
+    i_ext = np.concatenate([ih, ih[-2:]])          # the constant drive continues
+    rep = check_against_oracle(p64, ih, v32, s32, v_ref, s_ref, ours_ext=ours, i_ext=i_ext)
     assert rep["unexplained"] == 0, [x for x in rep["listed"] if x["verdict"] == "unexplained"]
     # BPTT: d_i normwise within the 1e-3 contract (full storage)
     seed_v = 2.0 * v64 / v64.numel()
