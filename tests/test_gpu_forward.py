@@ -424,7 +424,7 @@ def test_config2_full_horizon_against_oracle(cuda):
     neurons on a host stimulus I = 2*Poisson(2) (np.random.default_rng(0),
     SURVEY §8 d2), both builds against the ORACLE (the restated reference):
     float64 within 1e-9 relative over the whole horizon with identical
-    spikes; float32 under the per-neuron contract with every failing neuron
+    spikes (absolute floor 1e-8 mV); float32 under the per-neuron contract with every failing neuron
     listed and attributed (tests/contract.py) and none unexplained."""
     from contract import check_against_oracle
     p64 = DF.na_kdr_cal_kca_params(dt=0.01)
@@ -436,8 +436,12 @@ def test_config2_full_horizon_against_oracle(cuda):
     tr64 = Dy.simulate(p64, torch.as_tensor(i, device=cuda))
     v64 = tr64.v_series.cpu().numpy()
     assert np.array_equal(tr64.spike_series.cpu().numpy(), s_ref)
-    ok, err = _close64(v64, v_ref)
+    # 1e-9 relative; the absolute floor is 1e-8 mV (not 1e-9) because over
+    # 10,000 steps and ~15 spikes per neuron the last-ulp differences of
+    # libdevice exp vs NumPy's exp reach ~7e-9 mV where V crosses 0 mV
+    ok, err = _close64(v64, v_ref, atol=1e-8)
     assert ok, err
+    assert np.linalg.norm(v64 - v_ref) <= 1e-11 * np.linalg.norm(v_ref)
     del v64, tr64
     p32 = p64.with_(dtype=np.float32)
 
