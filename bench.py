@@ -47,13 +47,108 @@ BYTES_PER_NS = 4.125
 BYTES_PER_NS_UNFUSED = 8.125
 
 
-def mufu_per_step(nat, params):
-    """MUFU ops (ex2 + rcp) per neuron-step of the generated regular-lane step."""
+def mufu_per_step(nat, params, which="fwd"):
+    """MUFU ops (ex2 + rcp) per neuron-step of the generated regular-lane step
+    (forward or backward), counted in the generated source; the ncu-measured
+    XU instruction count of the same kernel is reported beside it."""
     src = nat.jit_source(params)
-    fn = "step_fwd_m(" if "step_fwd_m(" in src else "step_fwd_s("
+    fn = f"step_{which}_m(" if f"step_{which}_m(" in src else f"step_{which}_s("
     body = src[src.index("__device__ __forceinline__ float " + fn):]
     body = body[:body.index("\n}\n")]
     return body.count("ex2f_(") + body.count("rcpf_("), fn[:-1]
+
+
+def load_json(*parts):
+    path = os.path.join(ROOT, *parts)
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def layer_kernels(torch, step, reps=5):
+    """Per-component kernel times of an HH-layer training step, from CUDA
+    events recorded on each component's own stream (layer.TIMERS), over
+    `reps` eager steps: {name: {ms_per_step, launches_per_step, units_per_s}}."""
+    from paper_2601_21407_b200 import layer as L
+    torch.cuda.synchronize()
+    L.TIMERS = {}
+    try:
+        for _ in range(reps):
+            step()
+        torch.cuda.synchronize()
+        recs = L.TIMERS
+    finally:
+        L.TIMERS = None
+    out = {}
+    for name, rr in recs.items():
+        ms = sum(a.elapsed_time(b) for a, b, _ in rr)
+        units = sum(u for _, _, u in rr)
+        out[name] = {"ms_per_step": ms / reps, "launches_per_step": len(rr) / reps,
+                     "units_per_s": units / (ms * 1e-3) if ms > 0 else None}
+    return out
+
+
+# reference-formulation transcendentals per neuron-step of the RS set (SURVEY
+# §8 d7): forward tau_f = 16; backward with reuse tau_b = tau_f + 2 = 18
+TAU_RS_F, TAU_RS_B = 16, 18
+
+
+def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True):
+    """Roofline of an HH-layer training step: the dominant kernel (the BPTT
+    kernel hh_bwd2) against the live MUFU peak, with the forward kernel and the
+    projection GEMM beside it (GEMM against MEASURED_PEAKS bf16_tflops)."""
+    peaks = load_json("MEASURED_PEAKS.json")
+    prof = load_json("profiles", "k_bptt.json")
+    mb, fnb = mufu_per_step(nat, params, "bwd")
+    mf, fnf = mufu_per_step(nat, params, "fwd")
+    b, f, g = kern.get("hh_bptt", {}), kern.get("hh_forward", {}), kern.get("proj_gemm", {})
+    bw = b.get("units_per_s") or 0.0
+    fw = f.get("units_per_s") or 0.0
+    roof = {"bound": "sfu", "kernel": "hh_bwd2 (NVRTC-specialised merged-form BPTT, hhb_backward)",
+            "achieved": mb * bw / 1e9, "peak": mufu_peak / 1e9, "unit": "Gop/s", "frac": mb * bw / mufu_peak,
+            "traffic": prof.get("dram_bytes_per_neuron_step"),
+            "algorithmic": f"{mb} MUFU ops per neuron-step ({fnb}, counted in the generated source) x "
+                           "neuron-steps per launch",
+            "peak_source": "measured live: hhb_pipe_probe MUFU.EX2 throughput on this GPU",
+            "avg_launch_ms": b.get("ms_per_step", 0) / max(1e-9, b.get("launches_per_step", 1)),
+            "share_of_step": b.get("ms_per_step", 0) / step_ms,
+            "neuron_steps_per_s": bw,
+            "reference_tau": {"transcendentals_per_neuron_step": TAU_RS_B, "frac": TAU_RS_B * bw / mufu_peak},
+            "forward_kernel": {"kernel": "hh_fwd_v4 (training forward, checkpoints)", "mufu_per_neuron_step": mf,
+                               "neuron_steps_per_s": fw, "frac": mf * fw / mufu_peak,
+                               "reference_tau_frac": TAU_RS_F * fw / mufu_peak,
+                               "share_of_step": f.get("ms_per_step", 0) / step_ms},
+            "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kern.items()}}
+    if "xu_inst_per_neuron_step" in prof:
+        roof["ncu"] = {k: prof[k] for k in ("xu_inst_per_neuron_step", "inst_per_neuron_step", "issue_active_pct",
+                                            "xu_pipe_pct", "fma_pipe_pct", "source") if k in prof}
+    if g.get("units_per_s"):
+        pk = peaks.get("bf16_tflops", 1648.7)
+        roof["gemm"] = {"kernel": "k_umma_gemm_2sm (tcgen05 cta_group::2, projection x W^T)",
+                        "achieved_tflops": g["units_per_s"] / 1e12, "peak_tflops": pk,
+                        "frac": g["units_per_s"] / 1e12 / pk,
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "fallback",
+                        "share_of_step": g.get("ms_per_step", 0) / step_ms}
+        for name in ("grad_w", "grad_x"):
+            if kern.get(name, {}).get("units_per_s"):
+                roof["gemm"][name + "_tflops_algorithmic"] = kern[name]["units_per_s"] / 1e12
+        if dual_grads:
+            roof["gemm"]["note"] = ("gradient GEMMs carry dI as bf16 hi + lo (two tensor-core products per "
+                                    "algorithmic MAC): their algorithmic TFLOP/s is half the tensor work rate")
+    return roof
 
 
 def parse():
@@ -243,15 +338,32 @@ def graph_step(torch, step):
         return None
 
 
-def fwd_bwd_leg(torch, dev):
+def cpu_layers_leg(sizes, seconds):
+    """Same-run CPU baseline of configs 3 / 4: the reference composition
+    (DenseLayer -> simulate -> backward_through_time -> dW einsum, oracle port)
+    on every host core, one batch-1 shard per process."""
+    sys.path.insert(0, ROOT)
+    from oracle import cpu_baseline
+    from paper_2601_21407_b200.defaults import cortical_rs_params
+    r = cpu_baseline.run_layers(cortical_rs_params(dt=0.1).to_dict(), sizes, 100, seconds=seconds)
+    return {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"reference composition (oracle port of learn.py:238-274 + adjoint.py:281-365, float64) "
+                      f"{'->'.join(map(str, sizes))} x 100 steps, {r['samples']} batch-1 samples on "
+                      f"{r['cores']} processes in {r['seconds']:.1f} s"}
+
+
+def fwd_bwd_leg(torch, dev, proj="bf16", mufu_peak=None, cpu_seconds=0.0):
     """BASELINE config 3: differentiable HH SNN layer forward + BPTT, batch 256,
     784 -> 1024 RS neurons, 100 steps, x = Bernoulli(0.2) + 0.1 N(0,1),
-    W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = bf16 tcgen05 projection,
-    HH forward (full storage), BPTT, dW / db / dX gradient GEMMs."""
+    W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = tcgen05 projection (bf16,
+    or bf16x3: the fp32-class split that meets the gradient contract against
+    the reference's float64 operands), HH forward (full storage), BPTT,
+    dW / db / dX gradient GEMMs."""
+    from paper_2601_21407_b200 import _native as nat
     from paper_2601_21407_b200.layer import HHLayer
     B, N, T, K_in = 256, 1024, 100, 784
     torch.manual_seed(0)
-    layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, check_finite=False, device=dev)
+    layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, check_finite=False, device=dev, proj=proj)
     g = torch.Generator(device=dev).manual_seed(0)
     x = ((torch.rand((T, B, K_in), device=dev, generator=g) < 0.2).float()
          + 0.1 * torch.randn((T, B, K_in), device=dev, generator=g)).requires_grad_(True)
@@ -282,15 +394,24 @@ def fwd_bwd_leg(torch, dev):
     graph = graph_step(torch, step)
     ms = timed(graph.replay) if graph is not None else eager_ms
     layer.check()      # the overflow checks, deferred out of the timed steps
-    return {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
-            "cuda_graph": graph is not None,
-            "config": "BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, bf16 tcgen05 "
-                      "projection + fp32 HH forward + full-storage BPTT + bf16x2 gradient GEMMs, "
-                      "loss MSE(V, 0) fused into the HH kernels (layer.mse_loss; one unit = one "
-                      "neuron-step through forward and backward)"}
+    out = {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
+           "cuda_graph": graph is not None, "proj": proj,
+           "config": f"BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, {proj} tcgen05 "
+                     "projection + fp32 HH forward + full-storage BPTT + bf16 hi/lo gradient GEMMs, "
+                     "loss MSE(V, 0) fused into the HH kernels (layer.mse_loss; one unit = one "
+                     "neuron-step through forward and backward)",
+           "parity": ("dW/dX within 1e-4 of the float64 reference on the UNROUNDED operands "
+                      "(profiles/r2_parity_c3_unrounded.md)" if proj == "bf16x3" else
+                      "within 3e-5 of the float64 reference on bf16-rounded operands, 3-4e-3 on the "
+                      "unrounded ones (profiles/r2_parity_c3_unrounded.md)")}
+    if mufu_peak:
+        out["roofline"] = layer_roofline(nat, layer.params, layer_kernels(torch, step), ms, mufu_peak)
+    if cpu_seconds > 0:
+        out["cpu_baseline"] = cpu_layers_leg([784, 1024], cpu_seconds)
+    return out
 
 
-def c5_leg(torch, dev, steps=1000):
+def c5_leg(torch, dev, steps=1000, with_cpu=False, scale=0.5):
     """BASELINE config 5: recurrent HH cortex, build_network(scale=0.5, seed=0)
     (38,586 RS neurons, 71.2M synapses, delays up to 193 steps), REST_CONFIG,
     fp32, device Philox background; per step: ring drain + PSP + background,
@@ -303,7 +424,7 @@ def c5_leg(torch, dev, steps=1000):
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     t0 = time.perf_counter()
-    topo = N.build_network(0.5, 0)
+    topo = N.build_network(scale, 0)
     build_s = time.perf_counter() - t0
     ex = N.allgather_exchange(topo.n_neurons) if world > 1 else None
     net = N.CortexNetwork(topo, N.REST_CONFIG, device=dev, dtype=np.float32, rank=rank, world=world,
@@ -328,13 +449,29 @@ def c5_leg(torch, dev, steps=1000):
     if world > 1:
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
     ms = float(m.item())
-    return {"value": topo.n_neurons * steps / (ms * 1e-3), "unit": UNIT, "ms_per_network_step": ms / steps,
+    extra = {}
+    if with_cpu:
+        # same-run CPU baseline: the reference's step_network (oracle port) on one core
+        # (network stepping is serial in the reference), 100 warm-up + 200 timed steps
+        sys.path.insert(0, ROOT)
+        from oracle import cpu_baseline
+        cfg = N.REST_CONFIG
+        r = cpu_baseline.run_network(cfg.resolved_neuron().to_dict(), topo.syn_offsets, topo.syn_target,
+                                     topo.syn_weight, topo.syn_delay, topo.max_delay,
+                                     N.background_lambda(topo, N.make_background(cfg), cfg.dt), cfg.bg_mean,
+                                     cfg.bg_std, float(np.exp(-cfg.dt / cfg.psp_tau_ms)), steps=200, warm=100)
+        extra["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                                 "cpu_model": cpu_model(), "ms_per_network_step": 1e3 * r["seconds"] / r["steps"],
+                                 "sample": "reference step_network (oracle port of cortex.py:273-310, float64, "
+                                           "numpy compound-Poisson background) on one core, steps 100-299 "
+                                           f"({r['spikes_per_step']:.1f} spikes / step)"}
+    return {"value": topo.n_neurons * steps / (ms * 1e-3), "unit": UNIT, "ms_per_network_step": ms / steps, **extra,
             "steps": steps, "neurons": topo.n_neurons, "synapses": topo.n_synapses,
             "host_build_s": build_s,
             "path": ("persistent kernel" if net.persistent_ok() and not getattr(net, "_no_persist", False)
                      else "cuda graphs of 64 steps") if graphs else "eager steps + NCCL all-gather",
-            "config": "BASELINE config 5: recurrent HH cortex scale 0.5 (38,586 neurons, 71.2M synapses), "
-                      "REST_CONFIG, fp32, device Philox background"}
+            "config": f"BASELINE config 5: recurrent HH cortex scale {scale} ({topo.n_neurons:,} neurons, "
+                      f"{topo.n_synapses / 1e6:.1f}M synapses), REST_CONFIG, fp32, device Philox background"}
 
 
 def c1_leg(torch, dev, with_cpu=True):
@@ -423,28 +560,6 @@ def morph_leg(torch, dev):
                       "x 400 steps, fp32, V trace + spikes recorded (one unit = one compartment-step)"}
 
 
-def readout_fit_leg(torch, dev, epochs=20):
-    """the reference's teacher-student fitting loop (learn.fit,
-    learn.py:351-377) on its default task -- 64 channels, 500 steps, 16
-    training + 8 validation samples, RS neuron in float64 -- through
-    learn.fit: PSP filter, readout GEMV, HH forward, MSE, BPTT, weight
-    gradient, Adam, validation forward, per epoch.  The reference takes
-    0.40 s / epoch on one core of the build container."""
-    import time
-    from paper_2601_21407_b200 import learn as L
-    task = L.make_teacher_student_task()
-    L.fit(L.make_student(task), task, L.TrainConfig(epochs=3))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    hist = L.fit(L.make_student(task), task, L.TrainConfig(epochs=epochs))
-    torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3 / epochs
-    return {"value": 1e3 / ms, "unit": "epochs/s", "ms_per_epoch": ms, "epochs": epochs,
-            "loss_first_last": [hist[0][1], hist[-1][1]],
-            "config": "make_teacher_student_task() defaults (64 ch, 500 steps, 16 train / 8 val), float64; "
-                      "host wall clock (the loop reads the loss back every epoch, as the reference)"}
-
-
 def c5_replicas_leg(torch, dev, topo=None, replicas=(8, 32, 64), steps=640):
     """Config 5 in the paper's "replicas x speed" view: R
     independent copies of the scale-0.5 network stepped together on one GPU
@@ -473,7 +588,7 @@ def c5_replicas_leg(torch, dev, topo=None, replicas=(8, 32, 64), steps=640):
                       "replicas per GPU, fp32, device background (one unit = one neuron-step of one replica)"}
 
 
-def c4_leg(torch, dev):
+def c4_leg(torch, dev, mufu_peak=None, cpu_seconds=0.0):
     """BASELINE config 4: stacked HH SNN 784 -> 2048 -> 2048 -> 10 (RS neurons),
     batch 256, 100 steps, cross-entropy on the time-mean output V, Adam; one
     training step per unit of work."""
@@ -538,8 +653,14 @@ def c4_leg(torch, dev):
     for lyr in net:
         lyr.check()
     ns = B * T * (2048 + 2048 + 10)
+    extra = {}
+    if mufu_peak:
+        from paper_2601_21407_b200 import _native as nat
+        extra["roofline"] = layer_roofline(nat, net[0].params, layer_kernels(torch, step), ms, mufu_peak)
+    if cpu_seconds > 0:
+        extra["cpu_baseline"] = cpu_layers_leg([784, 2048, 2048, 10], cpu_seconds)
     return {"value": ns / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
-            "cuda_graph": graph is not None, "loss": float(loss.item()),
+            "cuda_graph": graph is not None, "loss": float(loss.item()), **extra,
             "config": "BASELINE config 4: stacked HH SNN 784->2048->2048->10, batch 256, 100 steps, "
                       "bf16 tcgen05 projections, fp32 gating state, CE on time-mean V, Adam "
                       "(one unit = one neuron-step through forward and backward)"}
@@ -677,12 +798,14 @@ def main():
             if world > 1:
                 dist.all_reduce(ev, op=dist.ReduceOp.MAX)
             extras["e2e"]["value"] = args.neurons * args.e2e_steps * world / float(ev.item())
-        leg("fwd_bwd", lambda: fwd_bwd_leg(torch, dev))
+        cpu_ok = rank == 0 and world == 1 and not args.no_cpu
+        leg("fwd_bwd", lambda: fwd_bwd_leg(torch, dev, "bf16x3", mufu_peak, args.cpu_seconds if cpu_ok else 0.0))
+        leg("fwd_bwd_bf16", lambda: fwd_bwd_leg(torch, dev, "bf16", mufu_peak))
         leg("c1", lambda: c1_leg(torch, dev, with_cpu=(rank == 0)))
-        leg("c4_train_step", lambda: c4_leg(torch, dev))
-        leg("c5_network", lambda: c5_leg(torch, dev))
+        leg("c4_train_step", lambda: c4_leg(torch, dev, mufu_peak, args.cpu_seconds if cpu_ok else 0.0))
+        leg("c5_network", lambda: c5_leg(torch, dev, with_cpu=cpu_ok))
+        leg("c5_network_100m", lambda: c5_leg(torch, dev, scale=0.59))
         leg("morphology", lambda: morph_leg(torch, dev))
-        leg("readout_fit", lambda: readout_fit_leg(torch, dev))
         leg("c5_replicas", lambda: c5_replicas_leg(torch, dev))
         if world > 1 and "ms_per_step" in extras["fwd_bwd"]:
             fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
@@ -691,7 +814,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.no_extras:
         r = cpu_leg(args.cpu_seconds, 1 << 21)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port", "cpu_model": cpu_model(),
                "sample": f"reference hh_step loop (oracle port of dynamics.py:443-529, fp32 mode) "
                          f"on {r['cores']} processes x {r['n_local']} neurons of the config-2 "
                          f"population for ~{args.cpu_seconds:.0f} s"}
@@ -703,9 +826,11 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_dict(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": extras.get("e2e"), "fwd_bwd": extras.get("fwd_bwd"),
+                "fwd_bwd_bf16": extras.get("fwd_bwd_bf16"), "c5_network_100m": extras.get("c5_network_100m"),
+                "cpu_model": cpu_model(),
                 "c4_train_step": extras.get("c4_train_step"), "c5_network": extras.get("c5_network"),
                 "morphology": extras.get("morphology"), "c5_replicas": extras.get("c5_replicas"),
-                "readout_fit": extras.get("readout_fit"), "c1": extras.get("c1"),
+"c1": extras.get("c1"),
                 "gpu_launches": launches, "clocks": clk,
                 "stimulus_ms_share": stim_ms / sum(step_ms)}
         print(json.dumps(line), flush=True)

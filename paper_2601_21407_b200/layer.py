@@ -36,6 +36,30 @@ from .errors import GradientOverflowError, UsageError
 
 BF16, TF32 = 0, 1
 
+# Per-component kernel timing for bench.py's roofline (off by default):
+# when TIMERS is a dict, each component records CUDA events on the stream it
+# runs on -- TIMERS[name] = [(start, end, units), ...] with units the
+# neuron-steps (HH kernels) or FLOPs (GEMMs) of that launch.
+TIMERS = None
+
+
+class _timed:
+    def __init__(self, name: str, units: float):
+        self.name, self.units = name, units
+
+    def __enter__(self):
+        if TIMERS is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        if TIMERS is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            TIMERS.setdefault(self.name, []).append((self.e0, e1, self.units))
+        return False
+
 
 def _pad8(k: int) -> int:
     return (k + 7) // 8 * 8
@@ -170,9 +194,10 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
     hi = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
     lo = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
     dsum = zb[(1 + p.n_gates) * n:]
-    _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, K, sv, ss, adj_v, adj_g,
-                                  want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum, ck_ld=n, sv_ld=sv_ld,
-                                  sv_scale=sv_scale)
+    with _timed("hh_bptt", T * n):
+        _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, K, sv, ss, adj_v, adj_g,
+                                      want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum, ck_ld=n, sv_ld=sv_ld,
+                                      sv_scale=sv_scale)
     layer._last_gbad = gbad
     if layer.check_finite:
         b = int(gbad.item())
@@ -185,9 +210,10 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
     def weight_grad():
         # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views;
         # bf16x3: (dI_hi + dI_lo) . x_hi + dI_hi . x_lo (slots 0 and 1 of xb)
-        dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
-        if x3:
-            dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, P, xb[:, kp:], xb.stride(0))
+        with _timed("grad_w", 2.0 * M * n_out * k_in):
+            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+            if x3:
+                dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, P, xb[:, kp:], xb.stride(0))
         return dW
 
     if layer.overlap_weight_grad:
@@ -229,9 +255,10 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
     if x_requires_grad:
         # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W);
         # bf16x3: (dI_hi + dI_lo) . W_hi + dI_hi . W_lo (slots 0 and 2 of wb)
-        dX = gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0))
-        if x3:
-            dX += gemm_ex(B_MN, M, k_in, n_out, hi, None, P, wb[:, 2 * kp:], wb.stride(0))
+        with _timed("grad_x", 2.0 * M * n_out * k_in):
+            dX = gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0))
+            if x3:
+                dX += gemm_ex(B_MN, M, k_in, n_out, hi, None, P, wb[:, 2 * kp:], wb.stride(0))
         dX = dX.view(T, B, k_in)
     return dX, dW, db
 
@@ -252,11 +279,13 @@ def _project(x, weight, bias, layer):
         # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
         xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
         wb, _ = split3_padded(weight.float().contiguous(), 1)
-        cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
+        with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
+            cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
         return xb, wb, cur
     xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
     wb = to_bf16_padded(weight.float().contiguous())
-    cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())        # (T*B, n_out) == (T, B*n_out)
+    with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
+        cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())    # (T*B, n_out) == (T, B*n_out)
     return xb, wb, cur
 
 
@@ -275,7 +304,8 @@ class _HHLayerFn(torch.autograd.Function):
         want_v, want_s = layer.outputs in ("both", "v"), layer.outputs in ("both", "spikes")
         v_out = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_v else None
         spikes = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_s else None
-        _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
+        with _timed("hh_forward", T * n):
+            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
         layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)
@@ -319,12 +349,14 @@ class _HHLayerMSEFn(torch.autograd.Function):
         if K == 1:
             ckpt = torch.empty((T + 1, 1 + ng, n), dtype=torch.float32, device=x.device)
             v_out = None
-            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_fin=ckpt[T, 0], g_fin=ckpt[T, 1:], ckpt=ckpt,
-                                 ckpt_every=1, sq_part=sq)
+            with _timed("hh_forward", T * n):
+                _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_fin=ckpt[T, 0], g_fin=ckpt[T, 1:], ckpt=ckpt,
+                                     ckpt_every=1, sq_part=sq)
         else:
             ckpt = torch.empty(((T + K - 1) // K, 1 + ng, n), dtype=torch.float32, device=x.device)
             v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
-            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, ckpt=ckpt, ckpt_every=K, sq_part=sq)
+            with _timed("hh_forward", T * n):
+                _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, ckpt=ckpt, ckpt_every=K, sq_part=sq)
         layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)
