@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define HHB_ABI_VERSION 2
+#define HHB_ABI_VERSION 3
 #define HHB_MAX_GATES 8
 #define HHB_MAX_CHANNELS 8
 
@@ -41,7 +41,8 @@ enum hhb_status {
   HHB_OK = 0,
   HHB_EINVAL = 22,   /* bad shape / argument / parameter table */
   HHB_ENOTSUP = 95,  /* combination not compiled in */
-  HHB_ECUDA = 1000   /* CUDA launch or runtime error */
+  HHB_ECUDA = 1000,  /* CUDA launch or runtime error */
+  HHB_ECOMM = 1001   /* NCCL error (spike exchange) */
 };
 
 enum hhb_dtype { HHB_F32 = 0, HHB_F64 = 1 };
@@ -439,6 +440,34 @@ int hhb_spike_deliver_flat(int64_t words, const uint32_t* bits, const int64_t* o
                            int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring,
                            int64_t* scratch, void* stream);
 int64_t hhb_spike_scratch(int64_t n_sources);
+
+/* ---- multi-GPU spike exchange ----------------------------
+ * Replaces the single-process visibility of every spike in step_network
+ * (cortex.py:273-310, :304-308): with the network sharded by target neuron
+ * over `world` GPUs, each step every rank contributes its words_per_rank
+ * bitmap words and receives all of them (ncclAllGather on `stream`, NVLink /
+ * NVSwitch inside a node; capturable into CUDA graphs).  NCCL is loaded at
+ * run time; hhb_spk_exchange_available() is 0 without it (HHB_ENOTSUP). */
+typedef struct hhb_exchange hhb_exchange_t;
+int hhb_spk_exchange_available(void);
+/* rank 0 creates the 128-byte id (host buffer) and shares it out of band */
+int hhb_spk_exchange_unique_id(void* id, int64_t bytes);
+int hhb_spk_exchange_init(const void* id, int32_t rank, int32_t world, int64_t words_per_rank,
+                          hhb_exchange_t** out);
+/* global_words[r * words_per_rank + i] = rank r's local_words[i] */
+int hhb_spk_exchange_allgather(hhb_exchange_t* ex, const uint32_t* local_words, uint32_t* global_words,
+                               void* stream);
+/* spk_step: the all-gather fused with hhb_spike_deliver_flat of the gathered
+ * bitmap into this rank's ring (words_global <= world * words_per_rank) */
+int hhb_spk_step(hhb_exchange_t* ex, const uint32_t* local_words, uint32_t* global_words, int64_t words_global,
+                 const int64_t* offsets, const int32_t* targets, const int32_t* weights_fx, const int32_t* delays,
+                 int64_t t, const int64_t* t_dev, int64_t depth, int64_t n_local, int64_t* ring, int64_t* scratch,
+                 void* stream);
+/* HHB_OK, or HHB_ECOMM with the NCCL asynchronous error (ncclCommGetAsyncError) */
+int hhb_spk_exchange_status(hhb_exchange_t* ex);
+/* abort (after a timeout / error: unblocks pending collectives) or destroy; both free ex */
+int hhb_spk_exchange_abort(hhb_exchange_t* ex);
+int hhb_spk_exchange_destroy(hhb_exchange_t* ex);
 /* `replicas` independent copies of one network on one GPU ("replicas x speed",
  * PAPER.md:193; SPEC data-parallel batching): per-replica state rows of n_pad
  * (= 32-aligned neuron count) neurons, ring [replicas][depth][n_pad], bitmap

@@ -15,7 +15,7 @@ import threading
 from .errors import ConfigurationError, NativeLibraryError, UsageError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhhb200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_GATES = 8
 MAX_CHANNELS = 8
 
@@ -116,6 +116,14 @@ SIGNATURES = {
     "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
     "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "hhb_spk_exchange_available": (_i32, []),
+    "hhb_spk_exchange_unique_id": (_i32, [_vp, _i64]),
+    "hhb_spk_exchange_init": (_i32, [_vp, _i32, _i32, _i64, C.POINTER(_vp)]),
+    "hhb_spk_exchange_allgather": (_i32, [_vp, _vp, _vp, _vp]),
+    "hhb_spk_step": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "hhb_spk_exchange_status": (_i32, [_vp]),
+    "hhb_spk_exchange_abort": (_i32, [_vp]),
+    "hhb_spk_exchange_destroy": (_i32, [_vp]),
     "hhb_split3_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp]),
     "hhb_col_sum": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "hhb_col_sum_scratch": (_i64, [_i64, _i64]),

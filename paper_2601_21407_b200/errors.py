@@ -61,3 +61,10 @@ class NativeLibraryError(HHEngineError):
     Not in the reference: the reference has no native code.  There is no CPU
     fallback, so a missing library is always fatal.
     """
+
+
+class ExchangeError(HHEngineError):
+    """The multi-GPU spike exchange failed: an NCCL asynchronous error, or a
+    step that did not complete within the exchange timeout (the communicator
+    is aborted first, so no rank stays blocked in the collective).  Not part
+    of the reference's error contract (the reference is single-process)."""

@@ -36,7 +36,7 @@ from . import _native as nat
 from . import connectivity as conn
 from .defaults import cortical_rs_params
 from .dynamics import HHParams, _forward, _raise_if_bad, _table, init_state
-from .errors import ConfigurationError, NativeLibraryError, UsageError
+from .errors import ConfigurationError, ExchangeError, NativeLibraryError, UsageError
 
 W_FRAC_BITS = 24  # weight quantum 2^-24 uA
 
@@ -253,21 +253,120 @@ def words_per_rank(n: int, world: int) -> int:
 def allgather_exchange(n_global: int, group=None):
     """Bitmap all-gather over torch.distributed (NCCL between GPUs, gloo on CPU):
     every rank contributes words_per_rank words (its shard, zero padded) and
-    receives the global bitmap.  4.8 KB per step at 38,586 neurons."""
+    receives the global bitmap.  4.8 KB per step at 38,586 neurons.  With a
+    gloo group and device words the exchange is staged through host memory
+    (gloo has no device all-gather): every step then synchronises the stream,
+    which is what the CPU / one-GPU multi-process tests use."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     per = words_per_rank(n_global, world)
     total = (n_global + 31) // 32
+    staged = dist.get_backend(group) == "gloo"
     buf = {}
 
     def exchange(local_words: torch.Tensor, gwords: torch.Tensor):
-        out = buf.get(local_words.device)
+        dev = local_words.device
+        out = buf.get(dev)
         if out is None:
-            out = buf[local_words.device] = torch.empty(per * world, dtype=torch.int32, device=local_words.device)
-        dist.all_gather_into_tensor(out, local_words[:per].contiguous(), group=group)
-        gwords.copy_(out[:total])
+            out = buf[dev] = torch.empty(per * world, dtype=torch.int32, device="cpu" if staged else dev)
+        src = local_words[:per].contiguous()
+        dist.all_gather_into_tensor(out, src.cpu() if staged else src, group=group)
+        gwords[:total].copy_(out[:total])
 
     return exchange
+
+
+class LibraryExchange:
+    """The per-step spike-bitmap all-gather inside the C-ABI library
+    (hhb_spk_exchange_*: ncclAllGather on the caller's stream over NVLink /
+    NVSwitch), so CortexNetwork.advance() captures it into its CUDA graphs with
+    the step kernels.  The communicator is the library's own (rank 0's NCCL
+    unique id is broadcast over `group`, any torch.distributed backend).
+    check() raises ExchangeError on an NCCL asynchronous error; wait() blocks
+    until the stream's work is done or `timeout_s` passes, then aborts the
+    communicator and raises ExchangeError (a dead peer cannot hang a rank)."""
+
+    def __init__(self, n_global: int, group=None, timeout_s: float = 300.0, rank: int | None = None,
+                 world: int | None = None):
+        lib = nat.load()
+        if not lib.hhb_spk_exchange_available():
+            raise NativeLibraryError("NCCL (libnccl.so.2) is not loadable: no library spike exchange")
+        if rank is None or world is None:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            dist = None
+        self.rank, self.world = int(rank), int(world)
+        self.per = words_per_rank(n_global, self.world)
+        self.total = (n_global + 31) // 32
+        self.timeout_s = float(timeout_s)
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            nat.check(lib.hhb_spk_exchange_unique_id(uid, 128), "hhb_spk_exchange_unique_id")
+        if self.world > 1:
+            import torch.distributed as dist
+            obj = [bytes(uid.raw)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = C.create_string_buffer(obj[0], 128)
+        h = C.c_void_p()
+        nat.check(lib.hhb_spk_exchange_init(uid, self.rank, self.world, self.per, C.byref(h)),
+                  "hhb_spk_exchange_init")
+        self.handle = h
+        self._buf = {}
+
+    def gathered_words(self) -> int:
+        return self.per * self.world
+
+    def __call__(self, local_words: torch.Tensor, gwords: torch.Tensor):
+        """local_words: >= words_per_rank int32 (this rank's shard);
+        gwords: >= world * words_per_rank int32 receives every rank's words."""
+        if self.handle is None:
+            raise ExchangeError("spike exchange used after close()")
+        if gwords.numel() < self.per * self.world or local_words.numel() < self.per:
+            raise UsageError("exchange buffers too small")
+        nat.check(nat.load().hhb_spk_exchange_allgather(self.handle, local_words.data_ptr(), gwords.data_ptr(),
+                                                        D.stream()), "hhb_spk_exchange_allgather")
+
+    def check(self):
+        if self.handle is None:
+            return
+        lib = nat.load()
+        if lib.hhb_spk_exchange_status(self.handle) != 0:
+            msg = lib.hhb_last_error().decode(errors="replace")
+            self.abort()
+            raise ExchangeError(msg)
+
+    def wait(self, stream=None):
+        """Block until the work queued on `stream` (default: current) is done,
+        polling the NCCL status; abort + ExchangeError after timeout_s."""
+        import time
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        t0 = time.monotonic()
+        while not ev.query():
+            self.check()
+            if time.monotonic() - t0 > self.timeout_s:
+                self.abort()
+                raise ExchangeError(f"spike exchange did not complete within {self.timeout_s:.0f} s")
+            time.sleep(1e-4)
+        self.check()
+
+    def abort(self):
+        if self.handle is not None:
+            nat.load().hhb_spk_exchange_abort(self.handle)
+            self.handle = None
+
+    def close(self):
+        if self.handle is not None:
+            nat.load().hhb_spk_exchange_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 def quantise_weights(w: np.ndarray) -> np.ndarray:
@@ -319,7 +418,9 @@ class CortexNetwork:
         self.cur = torch.empty(max(1, self.n), dtype=self.td, device=dev)
         # padded to the same count on every rank for the all-gather
         self.words = torch.zeros(max(1, words_per_rank(self.n_global, world)), dtype=torch.int32, device=dev)
-        self.gwords = torch.zeros(self.words_global, dtype=torch.int32, device=dev)
+        # padded to world * words_per_rank: the all-gather writes every rank's words in place
+        self.gwords = torch.zeros(max(self.words_global, words_per_rank(self.n_global, world) * world),
+                                  dtype=torch.int32, device=dev)
         self.first_bad = torch.full((1,), D.INT64_MAX, dtype=torch.int64, device=dev)
         self.decay = math.exp(-config.dt / config.psp_tau_ms)
         self.bg_mode = background
@@ -373,11 +474,11 @@ class CortexNetwork:
         """One network step (cortex.py:273-310); returns the global spike words."""
         words = self.advance_local(extra)
         if self.exchange is None:
-            self.gwords.copy_(words[:self.words_global])
+            self.gwords[:self.words_global].copy_(words[:self.words_global])
         else:
             self.exchange(words, self.gwords)
         self.deliver(self.gwords)
-        return self.gwords
+        return self.gwords[:self.words_global]
 
     # ---------------------------------------------------------------- graphs
     def _step_dev(self):
