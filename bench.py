@@ -165,6 +165,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / fwd_bwd / cpu legs")
     ap.add_argument("--no-fuse", action="store_true", help="stimulus as a separate kernel + HBM buffer")
+    ap.add_argument("--legs", default="", help="comma-separated subset of the secondary legs (default: all)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend under torchrun (gloo: a smoke of the N > 1 code path, "
+                         "ranks may share one GPU)")
     return ap.parse_args()
 
 
@@ -426,10 +430,17 @@ def c5_leg(torch, dev, steps=1000, with_cpu=False, scale=0.5):
     t0 = time.perf_counter()
     topo = N.build_network(scale, 0)
     build_s = time.perf_counter() - t0
-    ex = N.allgather_exchange(topo.n_neurons) if world > 1 else None
+    ex, ex_kind = None, None
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            # the library exchange (hhb_spk_step: ncclAllGather + delivery), captured into
+            # the 64-step CUDA graphs with the step kernels
+            ex, ex_kind = N.LibraryExchange(topo.n_neurons), "library ncclAllGather in CUDA graphs"
+        else:
+            ex, ex_kind = N.allgather_exchange(topo.n_neurons), "torch.distributed all-gather (gloo, host-staged)"
     net = N.CortexNetwork(topo, N.REST_CONFIG, device=dev, dtype=np.float32, rank=rank, world=world,
                           exchange=ex, background="philox", seed=1)
-    graphs = world == 1          # the NCCL exchange stays eager under torchrun
+    graphs = world == 1 or isinstance(ex, N.LibraryExchange)
     for _ in range(100):
         net.step()
     if graphs:
@@ -469,7 +480,8 @@ def c5_leg(torch, dev, steps=1000, with_cpu=False, scale=0.5):
             "steps": steps, "neurons": topo.n_neurons, "synapses": topo.n_synapses,
             "host_build_s": build_s,
             "path": ("persistent kernel" if net.persistent_ok() and not getattr(net, "_no_persist", False)
-                     else "cuda graphs of 64 steps") if graphs else "eager steps + NCCL all-gather",
+                     else "cuda graphs of 64 steps") + (f" + {ex_kind}" if ex_kind else "") if graphs
+            else f"eager steps + {ex_kind}",
             "config": f"BASELINE config 5: recurrent HH cortex scale {scale} ({topo.n_neurons:,} neurons, "
                       f"{topo.n_synapses / 1e6:.1f}M synapses), REST_CONFIG, fp32, device Philox background"}
 
@@ -678,10 +690,17 @@ def main():
     from paper_2601_21407_b200 import _native as nat
     from paper_2601_21407_b200.population import Population, PoissonCurrent
 
+    local = local % torch.cuda.device_count()        # gloo smoke: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+        # a dead or hung rank fails the collective after 10 min instead of hanging the job
+        tmo = datetime.timedelta(minutes=10)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev, timeout=tmo)
+        else:
+            dist.init_process_group("gloo", timeout=tmo)
     nat.load()
 
     params = c2_params(np.float32)
@@ -776,7 +795,11 @@ def main():
 
     extras = {}
 
+    only = set(args.legs.split(",")) if args.legs else None
+
     def leg(name, fn):
+        if only is not None and name not in only:
+            return
         # a failing secondary leg is reported in the line, not fatal to it;
         # each leg starts from an emptied allocator cache (the previous legs'
         # graph pools and temporaries would otherwise make its first
@@ -793,7 +816,7 @@ def main():
 
     if not args.no_extras:
         leg("e2e", lambda: e2e_leg(torch, args, params, rank))
-        if "seconds_per_step" in extras["e2e"]:
+        if "seconds_per_step" in extras.get("e2e", {}):
             ev = torch.tensor([extras["e2e"]["seconds_per_step"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(ev, op=dist.ReduceOp.MAX)
@@ -807,10 +830,14 @@ def main():
         leg("c5_network_100m", lambda: c5_leg(torch, dev, scale=0.59))
         leg("morphology", lambda: morph_leg(torch, dev))
         leg("c5_replicas", lambda: c5_replicas_leg(torch, dev))
-        if world > 1 and "ms_per_step" in extras["fwd_bwd"]:
-            fb = torch.tensor([extras["fwd_bwd"]["ms_per_step"]], dtype=torch.float64, device=dev)
-            dist.all_reduce(fb, op=dist.ReduceOp.MAX)
-            extras["fwd_bwd"]["value"] = 256 * 1024 * 100 * world / (float(fb.item()) * 1e-3)
+        # data parallel (weak: batch 256 per rank): whole-job rate over the slowest rank
+        for name, ns in (("fwd_bwd", 256 * 1024 * 100), ("fwd_bwd_bf16", 256 * 1024 * 100),
+                         ("c4_train_step", 256 * 100 * (2048 + 2048 + 10))):
+            if world > 1 and "ms_per_step" in extras.get(name, {}):
+                fb = torch.tensor([extras[name]["ms_per_step"]], dtype=torch.float64, device=dev)
+                dist.all_reduce(fb, op=dist.ReduceOp.MAX)
+                extras[name]["value"] = ns * world / (float(fb.item()) * 1e-3)
+                extras[name]["ms_per_step_max_over_ranks"] = float(fb.item())
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.no_extras:
         r = cpu_leg(args.cpu_seconds, 1 << 21)

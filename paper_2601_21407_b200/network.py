@@ -493,6 +493,15 @@ class CortexNetwork:
         _forward(self.params, self.v, self.g, self.cur[:self.n], 0, 1, 1, v_fin=self.v, g_fin=self.g,
                  bits=self.words.view(1, -1), step_base=0, first_bad=self.first_bad, reset_bad=False,
                  step_dev=self.t_dev)
+        if isinstance(self.exchange, LibraryExchange):
+            # the all-gather and the delivery in one C-ABI call (hhb_spk_step)
+            nat.check(lib.hhb_spk_step(
+                self.exchange.handle, self.words.data_ptr(), self.gwords.data_ptr(), self.words_global,
+                self.off.data_ptr(), self.tgt.data_ptr(), self.w.data_ptr(), self.delay.data_ptr(), 0,
+                self.t_dev.data_ptr(), self.depth, self.n, self.ring.data_ptr(), self.scratch.data_ptr(),
+                D.stream()), "hhb_spk_step")
+            nat.check(lib.hhb_cortex_tick(self.t_dev.data_ptr(), D.stream()), "hhb_cortex_tick")
+            return self.gwords
         if self.exchange is None:
             gw = self.words            # one rank: the local bitmap is the global one (no copy)
         else:
@@ -623,6 +632,8 @@ class CortexNetwork:
                 record[done].copy_(gw[:self.words_global])
             done += 1
         self.t += n_steps
+        if hasattr(self.exchange, "wait"):
+            self.exchange.wait()        # NCCL async errors / a hung peer surface here (ExchangeError)
         return record
 
     def run(self, n_steps: int, record: bool = True):
