@@ -407,6 +407,35 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
                    uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
                    const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
                    uint32_t* barrier, uint64_t* timing, void* stream);
+/* Thalamic drive of run_network (cortex.py:398-429) drawn on the device: the
+ * thalamic synapses in CSR by target (offsets [n + 1] local positions,
+ * weights of the network's dtype); synapse k (global position id_base + k)
+ * fires at step t in [t_on, t_off) iff word (k mod 4) of the Philox-4x32-10
+ * block ((id_base + k) / 4, t) under key `seed` is < threshold (= lam 2^32,
+ * the reference's rng.random() < lam).  The current of neuron i is the sum of
+ * its firing synapses' weights in row order (deterministic, the same for any
+ * sharding); it is added to that step's current only (not to the PSP). */
+typedef struct {
+  const int64_t* offsets;
+  const void* weights;
+  int64_t id_base;
+  int64_t t_on, t_off;
+  uint32_t threshold;
+  uint32_t reserved;
+  uint64_t seed;
+} hhb_thalamic_t;
+/* extra[i] = the thalamic current of step t (*t_dev if t_dev != NULL) for the
+ * n local neurons; 0 outside [t_on, t_off).  Pass extra to hhb_cortex_input. */
+int hhb_thalamic_drive(int32_t dtype, int64_t n, int64_t t, const int64_t* t_dev, const hhb_thalamic_t* thal,
+                       void* extra, void* stream);
+/* hhb_cortex_run with the thalamic drive inside the persistent kernel
+ * (thal NULL = hhb_cortex_run); float32 weights. */
+int hhb_cortex_run_ex(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+                      float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
+                      uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
+                      uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
+                      const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
+                      uint32_t* barrier, uint64_t* timing, const hhb_thalamic_t* thal, void* stream);
 /* hhb_cortex_run for `replicas` (1..16) independent copies of the network in
  * one launch (CortexReplicas): replica r's v / psp at r * ld (g rows: g_ld >=
  * replicas * ld), its ring at r * depth * ld, its spike words at r * words of
@@ -497,6 +526,11 @@ int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_
  * incoming gradient (learn.py:86-88), in one pass with no host sync. */
 int hhb_scale_f32(int64_t n, const float* x, const float* scale, double c, float* out, void* stream);
 const char* hhb_jit_status(void);
+/* compile-only NVRTC build (no device needed) of one generated module for
+ * sm_100a: kind 0 forward + backward, 1 the persistent network kernel, 2 the
+ * network kernel for 4 replicas.  Returns the cubin size (copied into buf when
+ * cap suffices), -1 on error (hhb_last_error has the NVRTC log). */
+int64_t hhb_jit_cubin(const hhb_params_t* params, int32_t kind, void* buf, int64_t cap);
 int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap);
 
 /* ---- measurement ---------------------------------------------------------- */

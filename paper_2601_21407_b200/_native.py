@@ -47,6 +47,12 @@ class Params(C.Structure):
                 ("gates", Gate * MAX_GATES), ("channels", Channel * MAX_CHANNELS)]
 
 
+class Thalamic(C.Structure):
+    """hhb_thalamic_t"""
+    _fields_ = [("offsets", C.c_void_p), ("weights", C.c_void_p), ("id_base", C.c_int64), ("t_on", C.c_int64),
+                ("t_off", C.c_int64), ("threshold", C.c_uint32), ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+
+
 class Surrogate(C.Structure):
     _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("width", C.c_double)]
 
@@ -139,6 +145,10 @@ SIGNATURES = {
     "hhb_cortex_run": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
                               C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
+    "hhb_cortex_run_ex": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
+                                 C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, C.POINTER(Thalamic), _vp]),
+    "hhb_thalamic_drive": (_i32, [_i32, _i64, _i64, _vp, C.POINTER(Thalamic), _vp, _vp]),
     "hhb_cortex_run_replicas": (_i32, [C.POINTER(Params), _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _dbl, _dbl,
                               C.c_uint64, _i64, _dbl, _vp, _vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
@@ -158,6 +168,7 @@ SIGNATURES = {
                                      _vp, _dbl, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "hhb_jit_status": (C.c_char_p, []),
     "hhb_jit_source": (_i64, [C.POINTER(Params), C.c_char_p, _i64]),
+    "hhb_jit_cubin": (_i64, [C.POINTER(Params), _i32, _vp, _i64]),
 }
 
 _lock = threading.Lock()
@@ -238,6 +249,20 @@ def pack_hh(params) -> Params:
 
 def pack_surrogate(spec) -> Surrogate:
     return Surrogate(SUR_KIND[spec.kind], 0, float(spec.width))
+
+
+def jit_cubin(params, kind: int = 0) -> bytes:
+    """Compile-only NVRTC build of a generated module (0: forward + backward,
+    1: persistent network kernel, 2: its 4-replica variant) -> sm_100a cubin
+    bytes.  Needs libnvrtc only (no GPU)."""
+    lib = load()
+    P = pack_hh(params)
+    n = int(lib.hhb_jit_cubin(C.byref(P), kind, None, 0))
+    if n < 0:
+        raise NativeLibraryError(lib.hhb_last_error().decode(errors="replace"))
+    buf = C.create_string_buffer(n)
+    lib.hhb_jit_cubin(C.byref(P), kind, buf, n)
+    return buf.raw[:n]
 
 
 def jit_source(params) -> str:

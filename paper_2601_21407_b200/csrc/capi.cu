@@ -432,6 +432,22 @@ int hhb_scale_f32(int64_t n, const float* x, const float* scale, double c, float
 
 const char* hhb_jit_status(void) { return jit_status(); }
 
+int64_t hhb_jit_cubin(const hhb_params_t* params, int32_t kind, void* buf, int64_t cap) {
+  if (check_params(params)) return -1;
+  if (kind < 0 || kind > 2) {
+    fail(HHB_EINVAL, "jit_cubin: kind 0..2");
+    return -1;
+  }
+  std::vector<char> cubin;
+  std::string log;
+  if (jit_cubin(params, kind, cubin, log) != HHB_OK) {
+    fail(HHB_ECUDA, "nvrtc: " + log.substr(0, 4000));
+    return -1;
+  }
+  if (buf && cap >= int64_t(cubin.size())) memcpy(buf, cubin.data(), cubin.size());
+  return int64_t(cubin.size());
+}
+
 int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap) {
   if (check_params(params)) return -1;
   const std::string src = jit_source(params);

@@ -36,6 +36,43 @@ __device__ __forceinline__ float bg_draw_f32(float L, float mu, float sigma, uin
   return add;
 }
 
+// thalamic current of neuron i at step t (cortex.py:423-428: rng.random(n_syn)
+// < lam, np.add.at of the firing synapses' weights): its CSR row in order,
+// synapse k firing iff word (id mod 4) of Philox block (id / 4, t) < thr,
+// id = base + k.  Sequential adds in row order -- repeated verbatim (float) by
+// jit.cu hh_net, so the per-step kernels and the persistent kernel agree bit
+// for bit.
+template <typename T>
+__device__ __forceinline__ T thal_sum(const int64_t* off, const T* w, int64_t base, uint32_t thr, uint64_t seed,
+                                      int64_t i, int64_t t) {
+  const int64_t k0 = off[i], k1 = off[i + 1];
+  T s = T(0);
+  for (int64_t g = (base + k0) >> 2; 4 * g - base < k1; ++g) {
+    const uint4 r = Philox::run(make_uint4(uint32_t(g), uint32_t(uint64_t(g) >> 32), uint32_t(t),
+                                           uint32_t(uint64_t(t) >> 32)),
+                                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+    const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = 4 * g + q - base;
+      if (k >= k0 && k < k1 && wd[q] < thr) {
+        if constexpr (sizeof(T) == 4) s = __fadd_rn(s, w[k]);
+        else s = s + w[k];
+      }
+    }
+  }
+  return s;
+}
+
+template <typename T>
+__global__ void k_thalamic(int64_t n, int64_t t, const long long* t_dev, const int64_t* off, const T* w,
+                           int64_t base, int64_t t_on, int64_t t_off, uint32_t thr, uint64_t seed, T* extra) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (t_dev) t = *t_dev;
+  extra[i] = (t >= t_on && t < t_off) ? thal_sum<T>(off, w, base, thr, seed, i, t) : T(0);
+}
+
 // t_dev != NULL: the step index is read from device memory (CUDA-graph replay
 // of the network step; hhb_cortex_tick advances it), else t is used
 template <typename T>
@@ -406,12 +443,13 @@ int hhb_cortex_step_batch(int32_t dtype, int64_t replicas, int64_t n_pad, int64_
   return cuda_check("k_spike_compact / k_spike_scatter (batch) launch");
 }
 
-int hhb_cortex_run_replicas(const hhb_params_t* params, int64_t replicas, int64_t ld, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
-                   float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
-                   uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
-                   uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
-                   const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
-                   uint32_t* barrier, uint64_t* timing, void* stream) {
+static int cortex_run_impl(const hhb_params_t* params, int64_t replicas, int64_t ld, int64_t n, int64_t steps,
+                           int64_t t0, int64_t depth, int64_t* ring, float* psp, double decay, int32_t bg_mode,
+                           const double* lam, double mu, double sigma, uint64_t seed, int64_t neuron_base,
+                           double w_scale, float* v, float* g, int64_t g_ld, uint32_t* bits, int32_t record,
+                           int64_t words, const int64_t* segments, int64_t tiles, const int32_t* targets,
+                           const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad, uint32_t* barrier,
+                           uint64_t* timing, const hhb_thalamic_t* thal, void* stream) {
   int rc = check_params(params);
   if (rc) return rc;
   if (n <= 0 || steps <= 0) return HHB_OK;
@@ -452,6 +490,17 @@ int hhb_cortex_run_replicas(const hhb_params_t* params, int64_t replicas, int64_
   a.timing = reinterpret_cast<unsigned long long*>(timing);
   a.reps = replicas;
   a.ld = ld;
+  if (thal) {
+    if (replicas != 1) return fail(HHB_EINVAL, "cortex_run: the thalamic drive needs one replica");
+    if (!thal->offsets || !thal->weights) return fail(HHB_EINVAL, "cortex_run: bad thalamic table");
+    a.th_off = thal->offsets;
+    a.th_w = static_cast<const float*>(thal->weights);
+    a.th_base = thal->id_base;
+    a.th_on = thal->t_on;
+    a.th_end = thal->t_off;
+    a.th_thr = thal->threshold;
+    a.th_seed = thal->seed;
+  }
   if (!jit_cortex_run(params, a, static_cast<cudaStream_t>(stream), rc))
     return fail(HHB_ENOTSUP, std::string("persistent network kernel unavailable: ") + jit_status());
   return rc;
@@ -477,6 +526,29 @@ int hhb_spike_events(int64_t steps, int64_t words, const uint32_t* bits, int64_t
   return cuda_check("k_event_write launch");
 }
 
+int hhb_cortex_run_replicas(const hhb_params_t* params, int64_t replicas, int64_t ld, int64_t n, int64_t steps,
+                            int64_t t0, int64_t depth, int64_t* ring, float* psp, double decay, int32_t bg_mode,
+                            const double* lam, double mu, double sigma, uint64_t seed, int64_t neuron_base,
+                            double w_scale, float* v, float* g, int64_t g_ld, uint32_t* bits, int32_t record,
+                            int64_t words, const int64_t* segments, int64_t tiles, const int32_t* targets,
+                            const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad, uint32_t* barrier,
+                            uint64_t* timing, void* stream) {
+  return cortex_run_impl(params, replicas, ld, n, steps, t0, depth, ring, psp, decay, bg_mode, lam, mu, sigma, seed,
+                         neuron_base, w_scale, v, g, g_ld, bits, record, words, segments, tiles, targets, weights_fx,
+                         delays, first_bad, barrier, timing, nullptr, stream);
+}
+
+int hhb_cortex_run_ex(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
+                      float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
+                      uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
+                      uint32_t* bits, int32_t record, int64_t words, const int64_t* segments, int64_t tiles,
+                      const int32_t* targets, const int32_t* weights_fx, const int32_t* delays, int64_t* first_bad,
+                      uint32_t* barrier, uint64_t* timing, const hhb_thalamic_t* thal, void* stream) {
+  return cortex_run_impl(params, 1, n, n, steps, t0, depth, ring, psp, decay, bg_mode, lam, mu, sigma, seed,
+                         neuron_base, w_scale, v, g, g_ld, bits, record, words, segments, tiles, targets, weights_fx,
+                         delays, first_bad, barrier, timing, thal, stream);
+}
+
 int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t t0, int64_t depth, int64_t* ring,
                    float* psp, double decay, int32_t bg_mode, const double* lam, double mu, double sigma,
                    uint64_t seed, int64_t neuron_base, double w_scale, float* v, float* g, int64_t g_ld,
@@ -486,6 +558,27 @@ int hhb_cortex_run(const hhb_params_t* params, int64_t n, int64_t steps, int64_t
   return hhb_cortex_run_replicas(params, 1, n, n, steps, t0, depth, ring, psp, decay, bg_mode, lam, mu, sigma, seed,
                                  neuron_base, w_scale, v, g, g_ld, bits, record, words, segments, tiles, targets,
                                  weights_fx, delays, first_bad, barrier, timing, stream);
+}
+
+int hhb_thalamic_drive(int32_t dtype, int64_t n, int64_t t, const int64_t* t_dev, const hhb_thalamic_t* thal,
+                       void* extra, void* stream) {
+  if (n <= 0) return HHB_OK;
+  if (!thal || !thal->offsets || !thal->weights || !extra) return fail(HHB_EINVAL, "bad thalamic_drive args");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long* td = reinterpret_cast<const long long*>(t_dev);
+  const unsigned grid = unsigned((n + 255) / 256);
+  if (dtype == HHB_F32) {
+    cortex::k_thalamic<float><<<grid, 256, 0, st>>>(n, t, td, thal->offsets, (const float*)thal->weights,
+                                                    thal->id_base, thal->t_on, thal->t_off, thal->threshold,
+                                                    thal->seed, (float*)extra);
+  } else if (dtype == HHB_F64) {
+    cortex::k_thalamic<double><<<grid, 256, 0, st>>>(n, t, td, thal->offsets, (const double*)thal->weights,
+                                                     thal->id_base, thal->t_on, thal->t_off, thal->threshold,
+                                                     thal->seed, (double*)extra);
+  } else {
+    return fail(HHB_EINVAL, "dtype");
+  }
+  return cuda_check("k_thalamic launch");
 }
 
 int hhb_cortex_tick(int64_t* t_dev, void* stream) {

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "hh_kernels.cuh"
 
@@ -275,10 +276,18 @@ struct CortexRunArgs {
   unsigned* bar;                 // grid-barrier counter (one uint32 of device scratch)
   unsigned long long* timing;   // optional [steps][blocks][4] globaltimer stamps (profiling)
   int64_t reps, ld;              // replicas per launch; per-replica stride of v / psp / ring rows
+  // thalamic drive (hhb_thalamic_t; th_off == nullptr: none) -- appended in the
+  // order of NetArgs (jit.cu), which mirrors this struct field for field
+  const int64_t* th_off;
+  const float* th_w;
+  int64_t th_base, th_on, th_end;
+  uint32_t th_thr;
+  uint64_t th_seed;
 };
 bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t st, int& rc);
 const char* jit_status();
 std::string jit_source(const hhb_params_t* P);
+int jit_cubin(const hhb_params_t* P, int kind, std::vector<char>& cubin, std::string& log);
 
 template <typename T>
 inline bool try_jit_fwd(const hhb_params_t* P, const FwdArgs<T>& a, const PoissonTab<T>* ptab, bool vec4,

@@ -1255,7 +1255,8 @@ static const char* kNetKernel = R"(
 struct NetArgs { i64 n, steps, t0, depth; long long* ring; float* psp; const double* lam;
   float decay, mu, sigma, w_scale; int mode, rec; unsigned long long seed; i64 nbase;
   float* v; float* g; i64 g_ld; u32* bits; i64 words; const i64* seg; i64 tiles; const int* tgt; const int* w;
-  const int* delay; i64* first_bad; unsigned* bar; unsigned long long* timing; i64 reps, ld; };
+  const int* delay; i64* first_bad; unsigned* bar; unsigned long long* timing; i64 reps, ld;
+  const i64* th_off; const float* th_w; i64 th_base, th_on, th_end; unsigned th_thr; unsigned long long th_seed; };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long x;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(x));
@@ -1290,6 +1291,23 @@ __device__ __forceinline__ float bg_draw(float L, float mu, float sigma, uint4 r
     add = __fadd_rn(add, __fmul_rn(__fmul_rn(sigma, __fsqrt_rn(float(k))), z));
   }
   return add;
+}
+// thalamic current of neuron i at step t: cortex.cu thal_sum<float>, verbatim
+__device__ __forceinline__ float thal_sum(const NetArgs& a, i64 i, i64 t) {
+  const i64 k0 = a.th_off[i], k1 = a.th_off[i + 1];
+  float s = 0.0f;
+  for (i64 g = (a.th_base + k0) >> 2; 4 * g - a.th_base < k1; ++g) {
+    const uint4 r = philox_full(make_uint4(u32(g), u32((unsigned long long)g >> 32), u32(t),
+                                           u32((unsigned long long)t >> 32)),
+                                make_uint2(u32(a.th_seed), u32(a.th_seed >> 32)));
+    const u32 wd[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 k = 4 * g + q - a.th_base;
+      if (k >= k0 && k < k1 && wd[q] < a.th_thr) s = __fadd_rn(s, a.th_w[k]);
+    }
+  }
+  return s;
 }
 // grid barrier on a monotonic arrival counter (zeroed by the host per launch);
 // the launch is cooperative, so every block is resident.  (Measured against a
@@ -1430,6 +1448,8 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
         }
         psp[r] = x;
         cur[r] = x;
+        // thalamic drive (one replica): added to this step's current, not the PSP
+        if (a.th_off != nullptr && t >= a.th_on && t < a.th_end) cur[r] = __fadd_rn(x, thal_sum(a, i, t));
       }
     }
     // the R replicas' neurons as one VEC = R group: their steps interleave
@@ -2237,6 +2257,44 @@ bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t 
                                 params);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "cooperative launch of hh_net failed");
   return true;
+}
+
+// compile-only (no device, no module load): the cubin of one generated module
+// for sm_100a -- kind 0: forward + backward (inspection flags), 1: the
+// persistent network kernel, 2: the network kernel for 4 replicas.  For CPU
+// tests of the code generator and SASS inspection (cuobjdump / nvdisasm).
+int jit_cubin(const hhb_params_t* P, int kind, std::vector<char>& cubin, std::string& log) {
+  using namespace jit;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    load_libs();
+  }
+  if (!g_nv.ok) {
+    log = g_nv.why;
+    return HHB_ENOTSUP;
+  }
+  const int flags = kind == 0 ? kInspect : kind == 1 ? kNet : kNet - 3;
+  const std::string src = generate(P, flags);
+  nvrtcProgram prog;
+  if (g_nv.create(&prog, src.c_str(), "hh_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return HHB_ECUDA;
+  }
+  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-lineinfo", "-default-device"};
+  const nvrtcResult rc = g_nv.compile(prog, 4, opts);
+  size_t n = 0;
+  g_nv.log_size(prog, &n);
+  log.assign(n, '\0');
+  if (n) g_nv.log(prog, &log[0]);
+  if (rc != NVRTC_SUCCESS) {
+    g_nv.destroy(&prog);
+    return HHB_ECUDA;
+  }
+  g_nv.cubin_size(prog, &n);
+  cubin.resize(n);
+  g_nv.cubin(prog, cubin.data());
+  g_nv.destroy(&prog);
+  return HHB_OK;
 }
 
 const char* jit_status() { return jit::g_status.c_str(); }

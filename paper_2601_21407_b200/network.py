@@ -437,6 +437,38 @@ class CortexNetwork:
         self.scratch = torch.empty(int(nat.load().hhb_spike_scratch(self.words_global * 32)), dtype=torch.int64,
                                    device=dev)
 
+    THAL_SALT = 0x7468616C616D7573        # key of the thalamic Philox stream: seed ^ "thalamus"
+
+    def set_thalamic(self, targets, weights, lam: float, t_on: int, t_off: int):
+        """Thalamic drive drawn on the device (cortex.py:398-429): thalamic
+        synapse k (targets[k], weights[k], the reference's _thalamic_setup
+        table) fires at step t in [t_on, t_off) with probability lam, keyed
+        by (seed, k, t) -- the same draws for any sharding and any of the
+        eager / graph / persistent paths (hhb_thalamic_drive, hh_net).  Its
+        current is added to that step's input only (not to the PSP), as
+        step_network's extra_current."""
+        targets = np.asarray(targets, dtype=np.int64)
+        weights = np.asarray(weights, dtype=np.float64)
+        if targets.shape != weights.shape or (targets.size and (targets.min() < 0 or targets.max() >= self.n_global)):
+            raise UsageError("thalamic targets / weights must be matching arrays of global neuron ids")
+        order = np.argsort(targets, kind="stable")
+        goff = np.concatenate([[0], np.cumsum(np.bincount(targets, minlength=self.n_global))]).astype(np.int64)
+        k0, k1 = int(goff[self.lo]), int(goff[self.hi])
+        self.th_off = torch.from_numpy(goff[self.lo:self.hi + 1] - k0).to(self.dev)
+        w = np.zeros(max(1, k1 - k0))
+        w[:k1 - k0] = weights[order][k0:k1]
+        self.th_w = torch.from_numpy(w).to(self.td).to(self.dev)
+        thr = min(2 ** 32 - 1, int(math.floor(float(lam) * 2.0 ** 32)))
+        self.thal = nat.Thalamic(self.th_off.data_ptr(), self.th_w.data_ptr(), k0, int(t_on), int(t_off), thr, 0,
+                                 (self.seed ^ self.THAL_SALT) & (2 ** 64 - 1))
+        self.thal_buf = torch.zeros(max(1, self.n), dtype=self.td, device=self.dev)
+        self._graphs.clear()             # captured steps lack (or hold stale) thalamic launches
+
+    def _thalamic(self, t_dev=None):
+        nat.check(nat.load().hhb_thalamic_drive(D.code(self.dtype), self.n, self.t, D.ptr(t_dev), C.byref(self.thal),
+                                                self.thal_buf.data_ptr(), D.stream()), "hhb_thalamic_drive")
+        return self.thal_buf
+
     def _input(self, extra=None):
         lib = nat.load()
         mode = 0
@@ -447,6 +479,9 @@ class CortexNetwork:
         elif self.bg_mode == "philox" and self.bg_spec.rate_hz > 0:
             mode = 2
         ex = None if extra is None else D.to_dev(extra, self.dtype, self.dev)
+        if getattr(self, "thal", None) is not None:
+            th = self._thalamic()
+            ex = th if ex is None else th + ex
         nat.check(lib.hhb_cortex_input(
             D.code(self.dtype), self.n, self.t, self.depth, self.ring.data_ptr(), self.psp.data_ptr(),
             self.decay, mode, self.bg_buf.data_ptr() if mode == 1 else None, self.lam.data_ptr(),
@@ -485,10 +520,11 @@ class CortexNetwork:
         """One step whose step index lives in self.t_dev (capturable)."""
         lib = nat.load()
         mode = 2 if (self.bg_mode == "philox" and self.bg_spec.rate_hz > 0) else 0
+        ex = self._thalamic(self.t_dev) if getattr(self, "thal", None) is not None else None
         nat.check(lib.hhb_cortex_input_dev(
             D.code(self.dtype), self.n, 0, self.t_dev.data_ptr(), self.depth, self.ring.data_ptr(),
             self.psp.data_ptr(), self.decay, mode, None, self.lam.data_ptr(), self.bg_spec.w_mean,
-            self.bg_spec.w_std, self.seed, self.lo, None, self.cur.data_ptr(),
+            self.bg_spec.w_std, self.seed, self.lo, D.ptr(ex), self.cur.data_ptr(),
             float(1.0 / (1 << W_FRAC_BITS)), D.stream()), "hhb_cortex_input_dev")
         _forward(self.params, self.v, self.g, self.cur[:self.n], 0, 1, 1, v_fin=self.v, g_fin=self.g,
                  bits=self.words.view(1, -1), step_base=0, first_bad=self.first_bad, reset_bad=False,
@@ -563,14 +599,15 @@ class CortexNetwork:
             self._barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
         seg, tiles = self._tile_segments()
         P = _table(self.params)
-        rc = lib.hhb_cortex_run(
+        thal = getattr(self, "thal", None)
+        rc = lib.hhb_cortex_run_ex(
             C.byref(P), self.n, n_steps, self.t, self.depth, self.ring.data_ptr(), self.psp.data_ptr(), self.decay,
             mode, self.lam.data_ptr(), self.bg_spec.w_mean, self.bg_spec.w_std, self.seed, self.lo,
             float(1.0 / (1 << W_FRAC_BITS)), self.v.data_ptr(), self.g.data_ptr() if self.g.numel() else None,
             self.n, bits.data_ptr(), rec, W, seg.data_ptr(), tiles, self.tgt.data_ptr(), self.w.data_ptr(),
             self.delay.data_ptr(), self.first_bad.data_ptr(), self._barrier.data_ptr(),
-            D.ptr(getattr(self, "timing", None)), D.stream())
-        nat.check(rc, "hhb_cortex_run")
+            D.ptr(getattr(self, "timing", None)), C.byref(thal) if thal is not None else None, D.stream())
+        nat.check(rc, "hhb_cortex_run_ex")
         last = bits[n_steps - 1] if rec else bits[(n_steps - 1) & 1]
         self.words[:W].copy_(last[:W])
         self.t += n_steps
@@ -871,9 +908,10 @@ def run_network(topo: NetworkTopology, config: CortexConfig, duration_ms: float,
     background="host" (default) draws the compound-Poisson background and the
     thalamic events from the reference's RNG stream (np.random.default_rng(seed),
     same call order), so a float64 run reproduces the reference raster;
-    background="philox" draws the background on the device (statistically the
-    same process, keyed by (seed, neuron, step)) and replays 64-step CUDA graphs
-    when there is no thalamic drive -- the throughput path."""
+    background="philox" draws the background and the thalamic events on the
+    device (statistically the same processes, keyed by (seed, neuron, step)
+    and (seed, synapse, step)) and runs every step in the persistent kernel
+    (one GPU, float32) or 64-step CUDA graphs -- the throughput path."""
     rng = np.random.default_rng(seed)
     n_steps = int(round(duration_ms / config.dt))
     thal = None
@@ -887,7 +925,11 @@ def run_network(topo: NetworkTopology, config: CortexConfig, duration_ms: float,
     else:
         raise UsageError(f"unknown background {background!r}")
     rows = torch.empty((n_steps, net.words_global), dtype=torch.int32, device=net.dev)
-    if background == "philox" and thal is None:
+    if background == "philox":
+        # the thalamic events drawn on the device too (Philox keyed by (seed,
+        # synapse, step)): every step in the persistent kernel / CUDA graphs
+        if thal is not None:
+            net.set_thalamic(thal[0], thal[1], thal[2], thal[3], thal[4])
         net.advance(n_steps, record=rows)
     else:
         for t in range(n_steps):

@@ -261,3 +261,17 @@ def test_integration_doc_maps_every_entry_point():
     doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
     missing = [n for n in _declared() if n not in doc]
     assert not missing, missing
+
+
+@pytest.mark.parametrize("which", ["rs", "c2", "squid"])
+def test_generated_modules_compile_for_sm100a_without_a_gpu(which):
+    """Every NVRTC module the library generates (forward + backward, the
+    persistent network kernel, its 4-replica form) compiles for sm_100a here,
+    on the CPU (hhb_jit_cubin: NVRTC only, no device)."""
+    import numpy as np
+    from paper_2601_21407_b200 import defaults as DF
+    p = {"rs": DF.cortical_rs_params(dt=0.1), "c2": DF.na_kdr_cal_kca_params(dt=0.01),
+         "squid": DF.squid_axon_params(dt=0.01)}[which].with_(dtype=np.float32)
+    for kind in ((0, 1, 2) if which == "rs" else (0,)):
+        cubin = nat.jit_cubin(p, kind)
+        assert cubin[:4] == b"\x7fELF" and len(cubin) > 10000

@@ -407,3 +407,120 @@ def test_spec_acceptance8_compound_poisson_1e6_draws(cuda):
                                    torch.cuda.current_stream().cuda_stream), "cortex_input")
     k = (cur / 0.17).cpu().numpy()
     assert np.allclose(k, np.round(k), atol=1e-9)
+
+
+# ---------------------------------------------------------------- thalamic drive on the device
+
+def _philox4x32(c, key):
+    """Philox-4x32-10 on uint64-held uint32 arrays (Salmon et al. 2011), the
+    generator of hh_kernels.cuh / jit.cu, restated for the test."""
+    M = 0xFFFFFFFF
+    c0, c1, c2, c3 = (np.asarray(x, np.uint64) & M for x in c)
+    k0, k1 = np.uint64(key[0] & M), np.uint64(key[1] & M)
+    for _ in range(10):
+        p0 = np.uint64(0xD2511F53) * c0
+        p1 = np.uint64(0xCD9E8D57) * c2
+        c0, c1, c2, c3 = ((p1 >> np.uint64(32)) ^ c1 ^ k0) & M, p1 & M, ((p0 >> np.uint64(32)) ^ c3 ^ k1) & M, p0 & M
+        k0 = (k0 + np.uint64(0x9E3779B9)) & M
+        k1 = (k1 + np.uint64(0xBB67AE85)) & M
+    return c0, c1, c2, c3
+
+
+def _thalamic_table(topo, seed=3):
+    cfg = N.THALAMIC_CONFIG
+    thal = {"t_on_ms": 2.0, "duration_ms": 10.0, "rate_hz": 400.0, "weight": cfg.bg_mean, "weight_std": cfg.bg_std}
+    return N._thalamic_setup(topo, thal, 20.0, cfg.dt, np.random.default_rng(seed))
+
+
+def test_device_thalamic_drive_matches_restated_philox(cuda):
+    """hhb_thalamic_drive (float64) equals, bit for bit, the sum in row order
+    of the weights of the synapses whose Philox word (seed ^ salt, synapse / 4,
+    step) is below lam 2^32 -- the device form of cortex.py:423-428 -- and is
+    0 outside [t_on, t_off)."""
+    _, topo = _small()
+    targets, weights, lam, lo, hi = _thalamic_table(topo)
+    assert targets.size > 100
+    net = N.CortexNetwork(topo, N.THALAMIC_CONFIG, device=cuda, dtype=np.float64, background="philox", seed=9)
+    net.set_thalamic(targets, weights, lam, lo, hi)
+    order = np.argsort(targets, kind="stable")
+    tg, wg = targets[order], weights[order]
+    thr = min(2 ** 32 - 1, int(np.floor(lam * 2.0 ** 32)))
+    key = (net.seed ^ net.THAL_SALT) & (2 ** 64 - 1)
+    ids = np.arange(tg.size, dtype=np.uint64)
+    for t in (lo - 1, lo, lo + 3, hi - 1, hi):
+        net.t = t
+        got = net._thalamic().cpu().numpy()
+        want = np.zeros(topo.n_neurons)
+        if lo <= t < hi:
+            g = ids >> np.uint64(2)
+            words = _philox4x32((g, g >> np.uint64(32), np.full_like(g, t), np.zeros_like(g)),
+                                (key & 0xFFFFFFFF, key >> 32))
+            wd = np.choose((ids & np.uint64(3)).astype(np.int64), words)
+            fire = wd < thr
+            for k in np.flatnonzero(fire):           # row order = sorted-target order
+                want[tg[k]] += wg[k]
+            assert fire.any()
+        assert np.array_equal(got, want), t
+
+
+def test_thalamic_persistent_graph_eager_and_shards_agree(cuda, monkeypatch):
+    """With the device thalamic drive, the persistent kernel, the CUDA-graph
+    path and eager steps give the same rasters and state bit for bit, and so
+    does a 2-rank sharding (the draws are keyed by global synapse id)."""
+    _, topo = _small()
+    targets, weights, lam, lo, hi = _thalamic_table(topo)
+    cfg = N.THALAMIC_CONFIG
+    steps = 200
+
+    def make(rank=0, world=1):
+        net = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=13, rank=rank,
+                              world=world)
+        net.set_thalamic(targets, weights, lam, lo, hi)
+        return net
+
+    a = make()
+    assert a.persistent_ok()
+    ra = torch.empty((steps, a.words_global), dtype=torch.int32, device=cuda)
+    a.advance(steps, record=ra)
+    assert not getattr(a, "_no_persist", False)
+    monkeypatch.setenv("HHB_NET_GRAPH", "1")
+    b = make()
+    rb = torch.empty_like(ra)
+    b.advance(steps, record=rb)
+    monkeypatch.delenv("HHB_NET_GRAPH")
+    c = make()
+    rc = torch.stack([c.step().clone() for _ in range(steps)])
+    assert torch.equal(ra, rb) and torch.equal(ra, rc)
+    for x, y, z in ((a.v, b.v, c.v), (a.psp, b.psp, c.psp)):
+        assert torch.equal(x, y) and torch.equal(x, z)
+    # the drive changes the run (against no thalamic input)
+    d = N.CortexNetwork(topo, cfg, device=cuda, dtype=np.float32, background="philox", seed=13)
+    rd = torch.empty_like(ra)
+    d.advance(steps, record=rd)
+    assert not torch.equal(ra, rd)
+    # 2 ranks emulated on one GPU, sequentially (no kernel waits on another)
+    nets = [make(r, 2) for r in range(2)]
+    per = N.words_per_rank(topo.n_neurons, 2)
+    total = (topo.n_neurons + 31) // 32
+    rows = []
+    for _ in range(steps):
+        allw = torch.cat([net.advance_local()[:per] for net in nets])[:total].contiguous()
+        for net in nets:
+            net.deliver(allw)
+        rows.append(allw.clone())
+    assert torch.equal(torch.stack(rows), ra)
+
+
+def test_thalamic_stimulus_run_on_device(cuda):
+    """thalamic_stimulus_run(background="philox") runs through the device path
+    (no host RNG loop) and shows the L4 transient of SPEC.md:574 acceptance 7
+    qualitatively: L4 rates rise during the thalamic window."""
+    rec = N.thalamic_stimulus_run(120.0, 0.05, 7, t_on_ms=60.0, warmup_ms=0.0, background="philox",
+                                  dtype=np.float32)
+    t, ids = rec.times_ms, rec.neuron_ids
+    topo = rec.topo
+    l4 = topo.pop_slice("L4E")
+    inl4 = (ids >= l4.start) & (ids < l4.stop)
+    before = np.sum(inl4 & (t >= 40.0) & (t < 60.0))
+    during = np.sum(inl4 & (t >= 60.0) & (t < 80.0))
+    assert during > before
