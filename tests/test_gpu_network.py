@@ -519,7 +519,7 @@ def test_thalamic_stimulus_run_on_device(cuda):
                                   dtype=np.float32)
     t, ids = rec.times_ms, rec.neuron_ids
     topo = rec.topo
-    l4 = topo.pop_slice("L4E")
+    l4 = topo.pop_slice("L4e")
     inl4 = (ids >= l4.start) & (ids < l4.stop)
     before = np.sum(inl4 & (t >= 40.0) & (t < 60.0))
     during = np.sum(inl4 & (t >= 60.0) & (t < 80.0))
