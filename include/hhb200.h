@@ -528,7 +528,8 @@ int hhb_scale_f32(int64_t n, const float* x, const float* scale, double c, float
 const char* hhb_jit_status(void);
 /* compile-only NVRTC build (no device needed) of one generated module for
  * sm_100a: kind 0 forward + backward, 1 the persistent network kernel, 2 the
- * network kernel for 4 replicas.  Returns the cubin size (copied into buf when
+ * network kernel for 4 replicas, 16 + f the backward module specialised on
+ * optional-stream flags f, -1 - f the forward module on output flags f.  Returns the cubin size (copied into buf when
  * cap suffices), -1 on error (hhb_last_error has the NVRTC log). */
 int64_t hhb_jit_cubin(const hhb_params_t* params, int32_t kind, void* buf, int64_t cap);
 int64_t hhb_jit_source(const hhb_params_t* params, char* buf, int64_t cap);

@@ -434,8 +434,8 @@ const char* hhb_jit_status(void) { return jit_status(); }
 
 int64_t hhb_jit_cubin(const hhb_params_t* params, int32_t kind, void* buf, int64_t cap) {
   if (check_params(params)) return -1;
-  if (kind < 0 || kind > 2) {
-    fail(HHB_EINVAL, "jit_cubin: kind 0..2");
+  if ((kind > 2 && kind < 16) || kind > 16 + 255 || kind < -64) {
+    fail(HHB_EINVAL, "jit_cubin: kind 0..2, 16 + BF flags or -1 - FF flags");
     return -1;
   }
   std::vector<char> cubin;

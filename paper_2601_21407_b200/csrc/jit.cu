@@ -2261,7 +2261,9 @@ bool jit_cortex_run(const hhb_params_t* P, const CortexRunArgs& a, cudaStream_t 
 
 // compile-only (no device, no module load): the cubin of one generated module
 // for sm_100a -- kind 0: forward + backward (inspection flags), 1: the
-// persistent network kernel, 2: the network kernel for 4 replicas.  For CPU
+// persistent network kernel, 2: the network kernel for 4 replicas, >= 16: the
+// backward module for BF_* flags kind - 16, < 0: the forward module for FF_*
+// flags -1 - kind.  For CPU
 // tests of the code generator and SASS inspection (cuobjdump / nvdisasm).
 int jit_cubin(const hhb_params_t* P, int kind, std::vector<char>& cubin, std::string& log) {
   using namespace jit;
@@ -2273,7 +2275,7 @@ int jit_cubin(const hhb_params_t* P, int kind, std::vector<char>& cubin, std::st
     log = g_nv.why;
     return HHB_ENOTSUP;
   }
-  const int flags = kind == 0 ? kInspect : kind == 1 ? kNet : kNet - 3;
+  const int flags = kind == 0 ? kInspect : kind == 1 ? kNet : kind == 2 ? kNet - 3 : kind >= 16 ? kind - 16 : kind;
   const std::string src = generate(P, flags);
   nvrtcProgram prog;
   if (g_nv.create(&prog, src.c_str(), "hh_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
