@@ -1599,7 +1599,12 @@ __device__ __forceinline__ void store_state(float* base, i64 ld, i64 i, float v,
 // is specialised on which optional streams exist (BF_* below), so the sweep
 // carries no run-time tests; every stream advances by a running pointer.
 #define DEPTH 8   // power of two: slot wrap is a mask
-#define NOPS (NG + 4)   // v, p[NG], cur, seed_v, seed_s
+// ring slots per step: v, p[NG], cur, then seed_v (unless BF_SPREV reads it
+// from the previous step's state) and seed_s only when the launch has them --
+// a smaller ring leaves room for more resident blocks
+#define SV_SLOT (NG + 2)
+#define SS_SLOT (NG + 2 + ((BF_SV && !BF_SPREV) ? 1 : 0))
+#define NOPS (SS_SLOT + (BF_SS ? 1 : 0))
 #define RING_STRIDE (NOPS * BWD_THREADS)
 __device__ __forceinline__ void cpa4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((u32)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
@@ -1694,8 +1699,8 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #pragma unroll
       for (int g = 0; g < NG; ++g) cpa<VEC>(r + (1 + g) * BWD_THREADS, src + goff[g]);
       cpa<VEC>(r + (NG + 1) * BWD_THREADS, iq);
-      if (BF_SV && !BF_SPREV) cpa<VEC>(r + (NG + 2) * BWD_THREADS, vq);
-      if (BF_SS) cpa<VEC>(r + (NG + 3) * BWD_THREADS, sq);
+      if (BF_SV && !BF_SPREV) cpa<VEC>(r + SV_SLOT * BWD_THREADS, vq);
+      if (BF_SS) cpa<VEC>(r + SS_SLOT * BWD_THREADS, sq);
     };
     auto advance = [&]() {
       --tn;
@@ -1741,10 +1746,10 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
           d_v[j] = __fmaf_rn(svs, vprev[j], d_v[j]);
           vprev[j] = v[j];
         } else if (BF_SV) {
-          d_v[j] = BF_SVS ? __fmaf_rn(svs, r[(NG + 2) * BWD_THREADS + j], d_v[j])
-                          : __fadd_rn(d_v[j], r[(NG + 2) * BWD_THREADS + j]);
+          d_v[j] = BF_SVS ? __fmaf_rn(svs, r[SV_SLOT * BWD_THREADS + j], d_v[j])
+                          : __fadd_rn(d_v[j], r[SV_SLOT * BWD_THREADS + j]);
         }
-        ds[j] = BF_SS ? r[(NG + 3) * BWD_THREADS + j] : 0.0f;
+        ds[j] = BF_SS ? r[SS_SLOT * BWD_THREADS + j] : 0.0f;
 #if HAS_MERGED
         reg = reg && regular(v[j]);
 #endif
