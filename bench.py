@@ -78,10 +78,13 @@ def cpu_model():
     return None
 
 
-def layer_kernels(torch, step, reps=5):
+def layer_kernels(torch, step, reps=7):
     """Per-component kernel times of an HH-layer training step, from CUDA
-    events recorded on each component's own stream (layer.TIMERS), over
-    `reps` eager steps: {name: {ms_per_step, launches_per_step, units_per_s}}."""
+    events recorded on each component's own stream (layer.TIMERS) around its
+    launches, over `reps` eager steps; the median step is kept per component
+    (a GPU spin before each start event hides the host's launch preparation,
+    which an occasional allocation can still outlast):
+    {name: {ms_per_step, launches_per_step, units_per_s}}."""
     from paper_2601_21407_b200 import layer as L
     torch.cuda.synchronize()
     L.TIMERS = {}
@@ -94,9 +97,11 @@ def layer_kernels(torch, step, reps=5):
         L.TIMERS = None
     out = {}
     for name, rr in recs.items():
-        ms = sum(a.elapsed_time(b) for a, b, _ in rr)
-        units = sum(u for _, _, u in rr)
-        out[name] = {"ms_per_step": ms / reps, "launches_per_step": len(rr) / reps,
+        per = len(rr) // reps
+        steps = [rr[k * per:(k + 1) * per] for k in range(reps)]
+        ms_units = sorted((sum(a.elapsed_time(b) for a, b, _ in st), sum(u for _, _, u in st)) for st in steps)
+        ms, units = ms_units[reps // 2]
+        out[name] = {"ms_per_step": ms, "launches_per_step": per,
                      "units_per_s": units / (ms * 1e-3) if ms > 0 else None}
     return out
 

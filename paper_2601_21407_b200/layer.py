@@ -49,9 +49,9 @@ class _timed:
 
     def __enter__(self):
         if TIMERS is not None:
-            # keep the GPU busy (~100 us spin) while the host prepares the
+            # keep the GPU busy (~0.5 ms spin) while the host prepares the
             # component's launch, so the start event brackets the kernel only
-            torch.cuda._sleep(200_000)
+            torch.cuda._sleep(1_000_000)
             self.e0 = torch.cuda.Event(enable_timing=True)
             self.e0.record()
         return self

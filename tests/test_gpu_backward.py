@@ -45,6 +45,7 @@ def test_fp64_bptt_matches_reference(cuda, case):
     g = golden(case)
     p = CASES[case]()
     n = g["i"].shape[1]
+    s0 = Dy.init_state(p, (n,))
     T = g["i"].shape[0]
     full = A.backward_through_time(p, s0, g["i"], g["seed_v"], g["seed_spike"], surrogate=_sur(g))
     assert nrel(full.d_i, g["d_i"]) < 1e-9
@@ -70,6 +71,7 @@ def test_plan_invariance_is_bit_exact(cuda, dtype):
     i = rng.normal(25, 8, size=(T, n))
     sv = rng.normal(0, 0.01, size=(T, n))
     ss = rng.normal(0, 1, size=(T, n))
+    s0 = Dy.init_state(p, (n,))
     ref = A.backward_through_time(p, s0, i, sv, ss)
     for budget in (1, 5, 13, 97):
         r = A.backward_through_time(p, s0, i, sv, ss, plan=A.make_plan(T, budget))
@@ -112,6 +114,7 @@ def test_finite_differences_fp64(cuda):
     rng = np.random.default_rng(2)
     T, n = 50, 6
     i = rng.normal(6, 2, size=(T, n))
+    s0 = Dy.init_state(p, (n,))
     res = A.backward_through_time(p, s0, i, np.ones((T, n)))
 
     base = Dy.simulate(p, i, state0=s0).v_series
