@@ -893,6 +893,11 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
 
 // Kernel bodies (parameterised by NG through the generated step functions).
 static const char* kPrelude = R"(
+#if HHB_CHECK
+#define NET_CHK(c) do { if (!(c)) { printf("hhb check failed: %s (block %d thread %d)\n", #c, int(blockIdx.x), int(threadIdx.x)); __trap(); } } while (0)
+#else
+#define NET_CHK(c) do { } while (0)
+#endif
 typedef long long i64;
 typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
@@ -1420,6 +1425,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
       s_next[r][tid] = 0ull;                        // (next written after this block's barriers)
     }
     const int row1 = row + 1 == depth ? 0 : row + 1;
+    NET_CHK(row >= 0 && row < depth && i64(row) == (t % a.depth));
     __syncwarp();                                   // lane 2k+1 has read s_ahead before lane 2k refills it
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1492,6 +1498,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
             const int b = __ffs(int(x)) - 1;
             x &= x - 1;
             if (k >= r0 && k < r0 + m) s_src[k - r0] = int(wi * 32 + b) | (r << 20);
+            NET_CHK(wi * 32 + b < a.n);                  // no spike bit past the population
             ++k;
           }
         };
@@ -1520,6 +1527,7 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
       }
       if (tid == 0) s_pre[m] = int(total);
       __syncthreads();
+      NET_CHK(m <= NET_CAP && s_pre[0] == 0 && s_pre[m] == int(total) && total >= 0);
       // ... and one thread per (source, synapse) pair, NET_UNROLL pairs in
       // flight per thread (their loads overlap)
 #ifndef NET_UNROLL
@@ -1543,6 +1551,10 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
             d[u] = __ldg(a.delay + j);
             tg[u] = __ldg(a.tgt + j);
             wv[u] = __ldg(a.w + j);
+            NET_CHK(lo >= 0 && lo < m && s_pre[lo] <= gi && gi < s_pre[lo + 1]);
+            NET_CHK(j >= s_beg[lo] && rr[u] >= 0 && rr[u] < R);
+            NET_CHK(tg[u] >= tlo && tg[u] < tlo + NET_THREADS && tg[u] < a.n);    // the tile's own segment
+            NET_CHK(d[u] >= 1 && d[u] < depth);
           }
         }
 #pragma unroll
@@ -1733,6 +1745,8 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
       advance();
       cpa_wait();
       const float* r = ring_t + rslot * RING_STRIDE;
+      NET_CHK(rslot == int((hi - 1 - t) & (DEPTH - 1)) && wslot == int((hi - 1 - tn) & (DEPTH - 1)));
+      NET_CHK(tn == t - DEPTH && t >= lo && t < hi);
       rslot = (rslot + 1) & (DEPTH - 1);
       float di[VEC], v[VEC], p[VEC][NGX], cur[VEC], ds[VEC];
       bool reg = true;
@@ -1860,7 +1874,11 @@ constexpr int kNet = -2000;   // the persistent network kernel (hh_net)
 static int fwd_kind(int ff) { return -1 - ff; }
 static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   const Layout L = layout_of(P);
-  std::string src = kPrelude;
+  // HHB_JIT_CHECK=1: device-side bounds / invariant checks that trap (the
+  // substitute for compute-sanitizer, which this GPU pool does not allow)
+  const char* chk = getenv("HHB_JIT_CHECK");
+  std::string src = fmt("#define HHB_CHECK %d\n", chk && atoi(chk) > 0 ? 1 : 0);
+  src += kPrelude;
   src += fmt("#define NG %d\n#define NGX %d\n#define SLOTS %d\n#define BWD_THREADS %d\n", L.ng,
              L.ng > 0 ? L.ng : 1, kSlots, kBwdThreads);
   src += fmt("#define THETA %s\n", F(P->v_theta).c_str());
@@ -2086,7 +2104,7 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += pf ? std::string("p") + pf : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
-  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR"}) {
+  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK"}) {
     const char* x = getenv(e);
     k += x ? std::string("|") + e + x : "";
   }

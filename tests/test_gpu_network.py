@@ -535,3 +535,22 @@ def test_thalamic_run_on_device_drives_l4(cuda):
     rec = N.thalamic_stimulus_run(120.0, 0.05, 7, t_on_ms=60.0, warmup_ms=0.0, background="philox",
                                   dtype=np.float32)
     assert rec.times_ms.size > 0
+
+
+def test_checked_kernels_run_clean(cuda):
+    """HHB_JIT_CHECK=1 builds the generated kernels with device-side bounds and
+    invariant checks that trap (compute-sanitizer is not available on this GPU
+    pool): the persistent network kernel (grid barrier, delivery lists, tile
+    segments, ring rows; with 3-spike delivery rounds and the thalamic drive)
+    and the BPTT kernel (operand-ring slots) run through tools/sanitize_small.py
+    without tripping any of them."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"HHB_JIT_CHECK": "1"}, {"HHB_JIT_CHECK": "1", "HHB_NET_CAP": "3"}):
+        for which in ("net", "bwd", "fwd"):
+            out = subprocess.run([sys.executable, "tools/sanitize_small.py", which], cwd=root, capture_output=True,
+                                 text=True, timeout=600, env={**os.environ, **env})
+            assert out.returncode == 0 and "ok " + which in out.stdout, (env, which, out.stdout[-2000:],
+                                                                      out.stderr[-2000:])
