@@ -1890,8 +1890,11 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
   const char* pf = getenv("HHB_JIT_FWD_PF");
   src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 8);
+  // 2-neuron BPTT: 8 resident 64-thread blocks (128 registers, no spills; the
+  // operand ring holds only the launch's streams, 21.8 KB): 212 us vs 220 us
+  // at 6 blocks for the config-3 step (profiles/r2_bptt.md)
   const char* bmb2 = getenv("HHB_JIT_BWD2_MINB");
-  src += fmt("#define BWD2_MINB %d\n", bmb2 ? atoi(bmb2) : 6);
+  src += fmt("#define BWD2_MINB %d\n", bmb2 ? atoi(bmb2) : 8);
   const char* bmb = getenv("HHB_JIT_BWD_MINB");
   // 6 resident 128-thread blocks (<= 80 registers, no spills for up to 6 gates)
   // measured best at the config-3 shape: 259 us vs 276 us unconstrained
