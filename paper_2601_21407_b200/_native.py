@@ -14,7 +14,8 @@ import threading
 
 from .errors import ConfigurationError, NativeLibraryError, UsageError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhhb200.so")
+# HHB200_LIB: an alternative build of the library (kernel-variant experiments)
+LIB_PATH = os.environ.get("HHB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhhb200.so")
 ABI_VERSION = 3
 MAX_GATES = 8
 MAX_CHANNELS = 8

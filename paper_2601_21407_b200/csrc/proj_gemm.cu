@@ -550,7 +550,12 @@ struct P2Cfg {
   static constexpr int kEpiWarps = EPI2_WARPS;                // 2 per TMEM lane quadrant, each half of the columns
   static constexpr int kStgBufs = EPI2_BUFS;                  // TMA-store staging buffers per epilogue warp
   static constexpr uint32_t kStaging = kEpiWarps * kStgBufs * 32 * 32 * 4;
-  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 8 ? 8 : int((225 * 1024 - kStaging) / kStage);
+#ifndef GEMM2_MAX_STAGES
+#define GEMM2_MAX_STAGES 8
+#endif
+  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > GEMM2_MAX_STAGES
+                                     ? GEMM2_MAX_STAGES
+                                     : int((225 * 1024 - kStaging) / kStage);
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 256;
 };
 
@@ -1155,7 +1160,14 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kb_total = int((K + 63) / 64);
-  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  // tile width: 64 / 128 for narrow N; above, whichever of 128 / 256 pads N
+  // less (N = 784: 7 x 128 = 896 columns of tensor work instead of 4 x 256 =
+  // 1024), ties to 256 (more B reuse per tile).  HHB_GEMM_BN overrides (tests).
+  int bn = N <= 64 ? 64 : (N <= 128 ? 128 : ((N + 127) / 128 * 128 < (N + 255) / 256 * 256 ? 128 : 256));
+  if (const char* e = getenv("HHB_GEMM_BN")) {
+    const int v = atoi(e);
+    if (v == 64 || v == 128 || v == 256) bn = v;
+  }
   if (splits < 1) {
     // auto (splits <= 0): minimise a time model of the persistent grid --
     // waves x k-blocks per unit x ~0.28 us per 64-deep k-block of a tile
