@@ -45,6 +45,8 @@ struct FwdArgs {
   int64_t spkv_ld;
   const long long* step_dev;   // optional: device value added to step_base
   double* sq_part;             // optional: per-block partial sums of V'^2 (fused MSE(V, 0) forward)
+  uint16_t* spk_bf;            // optional: spike flags as bf16 0/1 [steps][spkb_ld] (the next layer's GEMM operand)
+  int64_t spkb_ld;
 };
 
 template <typename T>
@@ -410,6 +412,12 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const DevTable<T> tb, c
 #pragma unroll
       for (int j = 0; j < VEC; ++j)
         if (n0 + j < a.n) row[n0 + j] = spk[j] ? T(1) : T(0);
+    }
+    if (a.spk_bf != nullptr) {
+      uint16_t* row = a.spk_bf + t * a.spkb_ld;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j)
+        if (n0 + j < a.n) row[n0 + j] = spk[j] ? uint16_t(0x3F80) : uint16_t(0);
     }
     if (a.spk != nullptr) {
 #pragma unroll

@@ -903,7 +903,7 @@ typedef unsigned int u32;
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
-  float* spk_val; i64 spkv_ld; const long long* step_dev; double* sq_part; };
+  float* spk_val; i64 spkv_ld; const long long* step_dev; double* sq_part; unsigned short* spk_bf; i64 spkb_ld; };
 struct PoissonTab { int size; float amp; float cdf[48]; };
 // Philox-4x32-10 with the key schedule precomputed on the host (one kernel
 // parameter per round key: LOP3 takes them straight from the constant bank)
@@ -1091,6 +1091,7 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   float* vo = FF_VO ? a.v_out + n0 : nullptr;
   u32* so = FF_SO ? a.spk + n0 / 32 : nullptr;
   float* svo = FF_SVO ? a.spk_val + n0 : nullptr;
+  unsigned short* sbo = FF_SVB ? a.spk_bf + n0 : nullptr;
   const bool spk_writer = lane % (32 / VEC) == 0 && live;
   // loaded currents are prefetched FWD_PF (8) steps ahead with one neuron per
   // thread (small, latency-bound populations: one warp per SM, the step chain
@@ -1178,6 +1179,18 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       for (int j = 0; j < VEC; ++j) f[j] = ((nib >> j) & 1u) ? 1.0f : 0.0f;
       store4(svo, f);
       svo += a.spkv_ld;
+    }
+    if (FF_SVB) {   // bf16 0/1 (0x3F80 = 1.0): the next layer's GEMM operand, written beside the fp32 flags
+      if (VEC == 4 && (AL || full)) {
+        const u32 lo = ((nib & 1u) ? 0x3F80u : 0u) | ((nib & 2u) ? 0x3F800000u : 0u);
+        const u32 hi = ((nib & 4u) ? 0x3F80u : 0u) | ((nib & 8u) ? 0x3F800000u : 0u);
+        *reinterpret_cast<uint2*>(sbo) = make_uint2(lo, hi);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j)
+          if (n0 + j < a.n) sbo[j] = ((nib >> j) & 1u) ? (unsigned short)0x3F80 : (unsigned short)0;
+      }
+      sbo += a.spkb_ld;
     }
     if (FF_SO) {
       u32 w;
@@ -1868,7 +1881,7 @@ extern "C" __global__ void __launch_bounds__(BWD_THREADS / 2, BWD2_MINB) hh_bwd2
 // bwd_flags < 0: the forward module; >= 0: the backward module specialised
 // on BF_* (which optional streams the launch has); -2: both, for inspection
 enum { BF_SV = 1, BF_SS = 2, BF_DI = 4, BF_SPLIT = 8, BF_SUM = 16, BF_K1 = 32, BF_SVS = 64, BF_SPREV = 128 };
-enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16, FF_L2 = 32 };
+enum { FF_VO = 1, FF_SO = 2, FF_SVO = 4, FF_CK = 8, FF_AL = 16, FF_L2 = 32, FF_SVB = 64 };
 constexpr int kInspect = -1000;
 constexpr int kNet = -2000;   // the persistent network kernel (hh_net)
 static int fwd_kind(int ff) { return -1 - ff; }
@@ -2051,9 +2064,9 @@ __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, con
   if (bwd_flags < 0) {
     const int ff = bwd_flags == kInspect ? (FF_VO | FF_SO | FF_CK) : -1 - bwd_flags;
     src += fmt("#define FF_VO %d\n#define FF_SO %d\n#define FF_SVO %d\n#define FF_CK %d\n#define FF_AL %d\n"
-               "#define FF_L2 %d\n",
+               "#define FF_L2 %d\n#define FF_SVB %d\n",
                (ff & FF_VO) ? 1 : 0, (ff & FF_SO) ? 1 : 0, (ff & FF_SVO) ? 1 : 0, (ff & FF_CK) ? 1 : 0,
-               (ff & FF_AL) ? 1 : 0, (ff & FF_L2) ? 1 : 0);
+               (ff & FF_AL) ? 1 : 0, (ff & FF_L2) ? 1 : 0, (ff & FF_SVB) ? 1 : 0);
     src += kForwardBody;
   }
   if (bwd_flags >= 0 || bwd_flags == kInspect) {
@@ -2190,9 +2203,10 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
   const bool aligned = vec4 && a.n % 4 == 0 && (ptab || (a.i_sn == 1 && a.i_st % 4 == 0 && al16(a.i_ext))) &&
                        (!a.v_out || (a.v_ld % 4 == 0 && al16(a.v_out))) &&
                        (!a.spk_val || (a.spkv_ld % 4 == 0 && al16(a.spk_val))) &&
+                       (!a.spk_bf || (a.spkb_ld % 4 == 0 && (reinterpret_cast<uintptr_t>(a.spk_bf) & 7u) == 0)) &&
                        (!a.ckpt || (a.ck_ld % 4 == 0 && al16(a.ckpt)));
   const int ff = (a.v_out ? FF_VO : 0) | (a.spk ? FF_SO : 0) | (a.spk_val ? FF_SVO : 0) | (a.ckpt ? FF_CK : 0) |
-                 (aligned ? FF_AL : 0) | (a.sq_part ? FF_L2 : 0);
+                 (aligned ? FF_AL : 0) | (a.sq_part ? FF_L2 : 0) | (a.spk_bf ? FF_SVB : 0);
   jit::Module* m = jit::get_module(P, fwd_kind(ff));
   if (!m) return false;
   const int VEC = vec4 ? 4 : 1;

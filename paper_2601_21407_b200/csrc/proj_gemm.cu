@@ -1160,10 +1160,11 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kb_total = int((K + 63) / 64);
-  // tile width: 64 / 128 for narrow N; above, whichever of 128 / 256 pads N
-  // less (N = 784: 7 x 128 = 896 columns of tensor work instead of 4 x 256 =
-  // 1024), ties to 256 (more B reuse per tile).  HHB_GEMM_BN overrides (tests).
-  int bn = N <= 64 ? 64 : (N <= 128 ? 128 : ((N + 127) / 128 * 128 < (N + 255) / 256 * 256 ? 128 : 256));
+  // tile width: 64 / 128 for narrow N, else 256 (N = 784 measured 78.8 us
+  // (dW) / 86.9 us (dX) at 256 against 90.2 / 104.7 at 128: the padding of the
+  // last 256-wide tile costs less than halving B reuse, profiles/r2_gemm_variants.md).
+  // HHB_GEMM_BN overrides (experiments).
+  int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   if (const char* e = getenv("HHB_GEMM_BN")) {
     const int v = atoi(e);
     if (v == 64 || v == 128 || v == 256) bn = v;
