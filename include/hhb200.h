@@ -140,6 +140,17 @@ int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
                    int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
                    const int64_t* step_base_dev, double* sq_partials, void* stream);
+/* hhb_forward_ex plus spk_bf16[n_steps][spk_bf16_ld] (NULL = off): the spike
+ * flags again as bf16 0/1 values (0x3F80 = 1.0), so a stacked layer's spikes
+ * reach the next layer's bf16 tcgen05 GEMM as its A operand without a cast
+ * pass (learn.py:210-211 applied to spikes, exact in bf16). */
+int hhb_forward_ex2(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                    const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
+                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
+                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
+                    int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
+                    const int64_t* step_base_dev, double* sq_partials, void* spk_bf16, int64_t spk_bf16_ld,
+                    void* stream);
 int64_t hhb_forward_partials(int64_t n);
 /*
  * hhb_forward_poisson -- hhb_forward with the BASELINE config-2 stimulus

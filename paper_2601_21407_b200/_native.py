@@ -80,6 +80,14 @@ SIGNATURES = {
                               _vp, _i64,
                               _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
+    "hhb_forward_ex2": (_i32, [C.POINTER(Params), _i32, _i64, _i64,
+                               _vp, _vp, _i64, _vp, _vp,
+                               _vp, _i64, _i64,
+                               _vp, _i64,
+                               _vp, _i64,
+                               _vp, _i64,
+                               _vp, _i64, _i64,
+                               _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "hhb_forward_partials": (_i64, [_i64]),
     "hhb_backward": (_i32, [C.POINTER(Params), C.POINTER(Surrogate), _i32, _i64, _i64,
                             _vp, _i64, _i64,

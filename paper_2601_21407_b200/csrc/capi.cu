@@ -33,8 +33,11 @@ static int forward_t(const hhb_params_t* P, int64_t n, int64_t steps, const void
                      int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld, uint32_t* spk,
                      int64_t spk_ld, void* ckpt, int64_t ck_every, int64_t ck_ld,
                      int64_t step_base, int64_t* first_bad, cudaStream_t st, void* spk_val = nullptr,
-                     int64_t spkv_ld = 0, const int64_t* step_base_dev = nullptr, double* sq_part = nullptr) {
+                     int64_t spkv_ld = 0, const int64_t* step_base_dev = nullptr, double* sq_part = nullptr,
+                     void* spk_bf = nullptr, int64_t spkb_ld = 0) {
   FwdArgs<T> a{};
+  a.spk_bf = static_cast<uint16_t*>(spk_bf);
+  a.spkb_ld = spkb_ld;
   a.sq_part = sq_part;
   a.step_dev = reinterpret_cast<const long long*>(step_base_dev);
   a.spk_val = static_cast<T*>(spk_val);
@@ -201,12 +204,14 @@ int hhb_forward(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_
                         nullptr, nullptr, stream);
 }
 
-int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+int hhb_forward_ex2(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
                    const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
                    const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
                    uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
                    int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
-                   const int64_t* step_base_dev, double* sq_partials, void* stream) {
+                   const int64_t* step_base_dev, double* sq_partials, void* spk_bf16, int64_t spk_bf16_ld,
+                    void* stream) {
+  if (spk_bf16 && spk_bf16_ld < n) return fail(HHB_EINVAL, "spk_bf16_ld < n");
   if (spk_val && spk_val_ld < n) return fail(HHB_EINVAL, "spk_val_ld < n");
   int rc = check_params(params);
   if (rc) return rc;
@@ -222,10 +227,23 @@ int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t
   if (dtype == HHB_F32)
     return forward_t<float>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                             v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                            first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials);
+                            first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials, spk_bf16,
+                            spk_bf16_ld);
   return forward_t<double>(params, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn,
                            v_out, v_ld, spk_out, spk_ld, ckpt, ckpt_every, ckpt_ld, step_base,
-                           first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials);
+                           first_bad, ST(stream), spk_val, spk_val_ld, step_base_dev, sq_partials, spk_bf16,
+                            spk_bf16_ld);
+}
+
+int hhb_forward_ex(const hhb_params_t* params, int32_t dtype, int64_t n, int64_t n_steps,
+                   const void* v_in, const void* g_in, int64_t g_ld, void* v_fin, void* g_fin,
+                   const void* i_ext, int64_t i_st, int64_t i_sn, void* v_out, int64_t v_ld,
+                   uint32_t* spk_out, int64_t spk_ld, void* spk_val, int64_t spk_val_ld, void* ckpt,
+                   int64_t ckpt_every, int64_t ckpt_ld, int64_t step_base, int64_t* first_bad,
+                   const int64_t* step_base_dev, double* sq_partials, void* stream) {
+  return hhb_forward_ex2(params, dtype, n, n_steps, v_in, g_in, g_ld, v_fin, g_fin, i_ext, i_st, i_sn, v_out, v_ld,
+                         spk_out, spk_ld, spk_val, spk_val_ld, ckpt, ckpt_every, ckpt_ld, step_base, first_bad,
+                         step_base_dev, sq_partials, nullptr, 0, stream);
 }
 
 int64_t hhb_forward_partials(int64_t n) { return (n < 1 ? 1 : (n + 31) / 32) + 1; }
@@ -434,7 +452,7 @@ const char* hhb_jit_status(void) { return jit_status(); }
 
 int64_t hhb_jit_cubin(const hhb_params_t* params, int32_t kind, void* buf, int64_t cap) {
   if (check_params(params)) return -1;
-  if ((kind > 2 && kind < 16) || kind > 16 + 255 || kind < -64) {
+  if ((kind > 2 && kind < 16) || kind > 16 + 255 || kind < -128) {
     fail(HHB_EINVAL, "jit_cubin: kind 0..2, 16 + BF flags or -1 - FF flags");
     return -1;
   }

@@ -446,9 +446,10 @@ class Workspace:
 def _forward(params: HHParams, v: torch.Tensor, g: torch.Tensor, cur: torch.Tensor, i_st: int,
              i_sn: int, steps: int, *, v_fin=None, g_fin=None, v_out=None, bits=None,
              ckpt=None, ckpt_every: int = 0, step_base: int = 0, first_bad=None,
-             reset_bad: bool = True, spk_val=None, step_dev=None, sq_part=None):
+             reset_bad: bool = True, spk_val=None, step_dev=None, sq_part=None, spk_bf16=None):
     """One hhb_forward launch on device tensors (flat v (n,), g (ng, n)).
-    first_bad accumulates (atomicMin) across launches when reset_bad=False."""
+    first_bad accumulates (atomicMin) across launches when reset_bad=False.
+    spk_bf16: optional (steps, n) bf16 tensor receiving the spike flags as 0/1."""
     n = v.numel()
     P = _table(params)
     dt = D.code(v.dtype)
@@ -460,13 +461,13 @@ def _forward(params: HHParams, v: torch.Tensor, g: torch.Tensor, cur: torch.Tens
     if reset_bad:
         first_bad.fill_(D.INT64_MAX)
     words = (n + 31) // 32
-    rc = nat.load().hhb_forward_ex(
+    rc = nat.load().hhb_forward_ex2(
         C.byref(P), dt, n, steps, v.data_ptr(), D.ptr(g) if g.numel() else None, n,
         v_fin.data_ptr(), D.ptr(g_fin) if g_fin.numel() else None,
         D.ptr(cur), i_st, i_sn,
         D.ptr(v_out), n, D.ptr(bits), words, D.ptr(spk_val), n,
         D.ptr(ckpt), max(1, ckpt_every), n,
-        step_base, first_bad.data_ptr(), D.ptr(step_dev), D.ptr(sq_part), D.stream())
+        step_base, first_bad.data_ptr(), D.ptr(step_dev), D.ptr(sq_part), D.ptr(spk_bf16), n, D.stream())
     nat.check(rc, "hhb_forward")
     return v_fin, g_fin, first_bad
 

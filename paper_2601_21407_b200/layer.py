@@ -285,7 +285,14 @@ def _project(x, weight, bias, layer):
         with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
             cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
         return xb, wb, cur
-    xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
+    twin = getattr(x, "_hhb_bf16", None)
+    if (twin is not None and twin[1] == x._version and tuple(twin[0].shape) == tuple(x.shape)
+            and k_in % 8 == 0):
+        # spikes of an HHLayer(outputs="spikes") below: its forward kernel wrote
+        # them as bf16 0/1 too -- exactly x in bf16, no cast pass
+        xb = twin[0].view(T * B, k_in)
+    else:
+        xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
     wb = to_bf16_padded(weight.float().contiguous())
     with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
         cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())    # (T*B, n_out) == (T, B*n_out)
@@ -307,8 +314,13 @@ class _HHLayerFn(torch.autograd.Function):
         want_v, want_s = layer.outputs in ("both", "v"), layer.outputs in ("both", "spikes")
         v_out = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_v else None
         spikes = torch.empty((T, n), dtype=torch.float32, device=x.device) if want_s else None
+        # a spikes-only layer feeds a layer above: its bf16 GEMM operand comes
+        # straight out of the forward kernel (attached to the spike tensor)
+        sb = (torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+              if layer.outputs == "spikes" and n_out % 8 == 0 else None)
         with _timed("hh_forward", T * n):
-            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K)
+            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K,
+                                 spk_bf16=sb)
         layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)
@@ -316,7 +328,10 @@ class _HHLayerFn(torch.autograd.Function):
         ctx.save_for_backward(xb, wb, cur, ckpt)
         ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
         ctx.x_requires_grad = x.requires_grad
-        return (v_out.view(T, B, n_out) if want_v else None), (spikes.view(T, B, n_out) if want_s else None)
+        s_out = spikes.view(T, B, n_out) if want_s else None
+        if sb is not None:
+            s_out._hhb_bf16 = (sb.view(T, B, n_out), s_out._version)
+        return (v_out.view(T, B, n_out) if want_v else None), s_out
 
     @staticmethod
     def backward(ctx, d_v, d_s):

@@ -241,3 +241,20 @@ def test_config3_full_shape_unrounded_bf16x3_within_contract(cuda):
     for k in ("dW", "db", "dX", "d_c_m", "d_g_max"):
         assert r[k] < 1e-3, (k, r[k])
     assert r["loss_rel"] < 1e-4
+
+
+def test_spike_operand_written_by_the_forward_kernel(cuda):
+    """A spikes-only layer's forward kernel also writes its spikes as bf16 0/1
+    (hhb_forward_ex2): the layer above takes them as its GEMM operand without a
+    cast pass, with results identical to casting the float spikes."""
+    torch.manual_seed(4)
+    l1 = HHLayer(24, 32, DF.cortical_rs_params(dt=0.1), w_mean=0.6, w_std=0.5, device=cuda, outputs="spikes")
+    l2 = HHLayer(32, 8, DF.cortical_rs_params(dt=0.1), w_mean=3.0, w_std=2.0, device=cuda, outputs="v")
+    x = ((torch.rand((50, 3, 24), device=cuda) < 0.3).float())
+    _, s = l1(x)
+    twin = getattr(s, "_hhb_bf16", None)
+    assert twin is not None and twin[0].dtype == torch.bfloat16
+    assert torch.equal(twin[0].float(), s) and s.sum() > 0
+    va, _ = l2(s)
+    vb, _ = l2(s.detach().clone())          # a plain tensor: the cast path
+    assert torch.equal(va, vb)
