@@ -138,6 +138,8 @@ def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True):
                                "share_of_step": f.get("ms_per_step", 0) / step_ms},
             "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kern.items()}}
     if "xu_inst_per_neuron_step" in prof:
+        roof["mufu_check"] = {"source_count": mb, "ncu_sass_count": prof["xu_inst_per_neuron_step"],
+                              "agree": abs(prof["xu_inst_per_neuron_step"] - mb) <= 0.05 * mb}
         roof["ncu"] = {k: prof[k] for k in ("xu_inst_per_neuron_step", "inst_per_neuron_step", "issue_active_pct",
                                             "xu_pipe_pct", "fma_pipe_pct", "source") if k in prof}
     if g.get("units_per_s"):
@@ -789,6 +791,11 @@ def main():
             "hbm": {"achieved_gbs": bpn * ns_per_launch / fwd_avg_s / 1e9,
                     "peak_gbs": hbm_peak, "frac": bpn * ns_per_launch / fwd_avg_s / 1e9 / hbm_peak,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}}
+    if "xu_inst_per_neuron_step" in prof and not args.no_fuse:
+        # the numerator's MUFU count (generated source) against the executed MUFU
+        # instructions per neuron-step of an ncu capture of the same kernel
+        roof["mufu_check"] = {"source_count": mufu, "ncu_sass_count": prof["xu_inst_per_neuron_step"],
+                              "agree": abs(prof["xu_inst_per_neuron_step"] - mufu) <= 0.05 * mufu}
     if "inst_per_neuron_step" in prof and not args.no_fuse:
         # instruction-issue view: 4 warp-instructions / clk / SM = 128 thread-instructions
         sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
