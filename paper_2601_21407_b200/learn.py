@@ -245,7 +245,8 @@ def split_dataset(n_samples: int, rng: np.random.Generator, ratio=(3, 1)):
 @dataclass
 class DenseLayer:
     """y = x @ W.T + b over the trailing axis (learn.py:203-216).  numpy in ->
-    numpy out (computed on the device); CUDA tensors in -> tensors out."""
+    numpy out (computed on the device, float64 as the reference); CUDA tensors
+    in -> tensors out, float32 ones through the tcgen05 GEMM (bf16x3)."""
 
     weights: object   # (out, in)
     bias: object      # (out,)
@@ -253,9 +254,22 @@ class DenseLayer:
     def __call__(self, x):
         on_dev = D.is_dev(x)
         xd = _dev(x)
-        w = _dev(self.weights).to(xd.dtype)
-        b = _dev(self.bias).to(xd.dtype)
-        y = torch.matmul(xd, w.t()) + b
+        if xd.dtype == torch.float32:
+            # float32 device operands: the tcgen05 GEMM in its fp32-class bf16x3
+            # form (x and W split into bf16 hi + lo, three tensor-core products)
+            from .layer import gemm, split3_padded
+            k = xd.shape[-1]
+            x2 = xd.reshape(-1, k).contiguous()
+            xa, kp = split3_padded(x2, 0)
+            wa, _ = split3_padded(_dev(self.weights).float().reshape(-1, k).contiguous(), 1)
+            y = gemm(xa, wa, 3 * kp, bias=_dev(self.bias).float().contiguous())
+            y = y.reshape(*xd.shape[:-1], y.shape[-1])
+        else:
+            # float64 (the reference's own precision, learn.py:210-211): a plain
+            # library DGEMM -- no tensor-core form keeps 53 mantissa bits
+            w = _dev(self.weights).to(xd.dtype)
+            b = _dev(self.bias).to(xd.dtype)
+            y = torch.matmul(xd, w.t()) + b
         return y if on_dev else y.cpu().numpy()
 
     @staticmethod

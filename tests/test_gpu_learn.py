@@ -237,3 +237,29 @@ def test_readout_kernels_float32(cuda):
     with pytest.raises(Exception):   # workspace too small
         nat.check(lib.hhb_readout_grad(nat.F32, B, T, C, x.data_ptr(), x.stride(0), x.stride(1), dd.data_ptr(),
                                        d_w.data_ptr(), d_b.data_ptr(), ws.data_ptr(), 8, D.stream()), "grad")
+
+
+def test_dense_layer_float32_runs_on_the_tcgen05_gemm(cuda):
+    """learn.DenseLayer on float32 device tensors goes through hhb_gemm in the
+    bf16x3 form: within 4e-5 (relative to |x||W| scale) of the float64
+    x @ W.T + b of learn.py:210-211, for a batched (T, B, C) input and an
+    input width that is not a multiple of 8."""
+    import numpy as np
+    import torch
+    from paper_2601_21407_b200 import learn as L
+    rng = np.random.default_rng(0)
+    layer = L.DenseLayer(rng.normal(0.05, 0.1, (96, 37)), rng.normal(0, 1, 96))
+    x = rng.normal(0.5, 1.0, (10, 4, 37))
+    ref = x @ layer.weights.T + layer.bias
+    got = layer(torch.tensor(x, dtype=torch.float32, device=cuda))
+    assert got.dtype == torch.float32 and tuple(got.shape) == (10, 4, 96)
+    xr = torch.tensor(x, dtype=torch.float32).double().numpy()        # the float32 x exactly
+    wr = torch.tensor(layer.weights, dtype=torch.float32).double().numpy()
+    br = torch.tensor(layer.bias, dtype=torch.float32).double().numpy()
+    ref32 = xr @ wr.T + br
+    scale = np.abs(xr) @ np.abs(wr).T + np.abs(br)
+    assert np.max(np.abs(got.cpu().numpy() - ref32) / scale) < 4e-5    # hi/lo residuals: <= 2 x 2^-16
+    assert np.allclose(got.cpu().numpy(), ref, rtol=1e-3, atol=1e-3)
+    # numpy in -> numpy out, float64 (the reference's precision)
+    out = layer(x)
+    assert isinstance(out, np.ndarray) and np.allclose(out, ref, rtol=1e-12, atol=1e-12)
