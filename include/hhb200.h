@@ -286,6 +286,14 @@ enum hhb_gemm_flags { HHB_GEMM_A_MN = 1, HHB_GEMM_B_MN = 2 };
 int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
                 const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
                 float* workspace, void* stream);
+/* hhb_gemm_ex with k_switch > 0 (a multiple of 64 below K, K-major A): A2 is
+ * not a second addend but the A source for k >= k_switch, read at
+ * k - k_switch -- the K-concatenation [A | A2] of two operands without a
+ * copy.  The fp32-class input gradient uses it: [dI_hi | dI_lo] then dI_hi
+ * against [W_hi; W_hi; W_lo], three products in one GEMM. */
+int hhb_gemm_ex2(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
+                 const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
+                 float* workspace, int64_t k_switch, void* stream);
 /* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16,
  * 3: fp32 -> bf16 hi at [c][r] and lo = x - hi at [c][rows + r] (bf16x2 split),
  * 4: bf16 -> bf16 written to [c][r] and [c][rows + r].  Kinds 3 + 4 turn a

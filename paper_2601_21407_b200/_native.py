@@ -128,6 +128,8 @@ SIGNATURES = {
     "hhb_gemm": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp]),
     "hhb_gemm_workspace": (_i64, [_i64, _i64, _i32]),
     "hhb_gemm_ex": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "hhb_gemm_ex2": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64,
+                             _vp]),
     "hhb_transpose": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "hhb_cast_bf16": (_i32, [_i64, _vp, _vp, _vp]),
     "hhb_split_rows_bf16": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),

@@ -48,6 +48,7 @@ struct Args {
   int kb_per_split;
   int kb_total;
   uint32_t idesc;
+  int kb_switch;        // > 0 (K-major A, not DUAL): k-blocks >= kb_switch read A2 at k - kb_switch * 64
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -221,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
             if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
           }
+        } else if (!DUAL && args.kb_switch > 0 && kb0 + i >= args.kb_switch) {
+          tma_load_2d(&ta2, &full[s], a_dst, kx - args.kb_switch * kBK, int32_t(m0));
         } else {
           tma_load_2d(&ta, &full[s], a_dst, kx, int32_t(m0));
           if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
@@ -330,6 +333,7 @@ struct PArgs {
   int kb_per_split, kb_total;
   uint32_t idesc;
   const float* bias;   // only when splits == 1
+  int kb_switch;       // > 0 (K-major A, not DUAL): k-blocks >= kb_switch read A2 at k - kb_switch * 64
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
@@ -406,6 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
               if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
             }
+          } else if (!DUAL && args.kb_switch > 0 && kb >= args.kb_switch) {
+            tma_load_2d(&ta2, &full[s], a_dst, kx - args.kb_switch * 64, int32_t(m0));
           } else {
             tma_load_2d(&ta, &full[s], a_dst, kx, int32_t(m0));
             if (DUAL) tma_load_2d(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
@@ -669,6 +675,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               tma_load_2d_2sm(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
               if (DUAL) tma_load_2d_2sm(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
             }
+          } else if (!DUAL && args.kb_switch > 0 && kb >= args.kb_switch) {
+            tma_load_2d_2sm(&ta2, &full[s], a_dst, kx - args.kb_switch * 64, int32_t(m0));
           } else {
             tma_load_2d_2sm(&ta, &full[s], a_dst, kx, int32_t(m0));
             if (DUAL) tma_load_2d_2sm(&ta2, &full[s], a_dst + kStageA, kx, int32_t(m0));
@@ -867,6 +875,30 @@ __global__ void k_split3_rows(int64_t rows, int64_t cols, const float* src, int6
     d[0] = hi;
     d[slot] = order == 0 ? lo : hi;
     d[2 * slot] = order == 0 ? hi : lo;
+  }
+}
+
+// vectorised form (cols % 8 == 0, 16-byte aligned rows and slots): 8 columns
+// per thread, two 16-byte loads and three 16-byte stores
+__global__ void k_split3_rows_v8(int64_t rows, int64_t cols8, const float* src, int64_t lds, __nv_bfloat16* dst,
+                                 int64_t ldd, int64_t slot, int order) {
+  const int64_t total = rows * cols8;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = q / cols8, c = (q % cols8) * 8;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(src + r * lds + c));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(src + r * lds + c + 4));
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hi[j] = __float2bfloat16_rn(x[j]);
+      lo[j] = __float2bfloat16_rn(x[j] - __bfloat162float(hi[j]));
+    }
+    const uint4 h = *reinterpret_cast<const uint4*>(hi), l = *reinterpret_cast<const uint4*>(lo);
+    uint4* d = reinterpret_cast<uint4*>(dst + r * ldd + c);
+    d[0] = h;
+    *reinterpret_cast<uint4*>(dst + r * ldd + slot + c) = order == 0 ? l : h;
+    *reinterpret_cast<uint4*>(dst + r * ldd + 2 * slot + c) = order == 0 ? h : l;
   }
 }
 
@@ -1146,11 +1178,32 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
   return cuda_check("k_gemm_reduce launch");
 }
 
+static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2,
+                        int64_t lda, const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
+                        int32_t splits, float* workspace, int64_t k_switch, void* stream);
+
 int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
                 const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
                 float* workspace, void* stream) {
+  return gemm_ex_impl(flags, M, N, K, A, A2, lda, B, ldb, bias, D, ldd, splits, workspace, 0, stream);
+}
+
+int hhb_gemm_ex2(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
+                 const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
+                 float* workspace, int64_t k_switch, void* stream) {
+  return gemm_ex_impl(flags, M, N, K, A, A2, lda, B, ldb, bias, D, ldd, splits, workspace, k_switch, stream);
+}
+
+static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2,
+                        int64_t lda, const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
+                        int32_t splits, float* workspace, int64_t k_switch, void* stream) {
   using namespace hhb::gemm;
-  const bool a_mn = flags & HHB_GEMM_A_MN, b_mn = flags & HHB_GEMM_B_MN, dual = A2 != nullptr;
+  const bool a_mn = flags & HHB_GEMM_A_MN, b_mn = flags & HHB_GEMM_B_MN;
+  // k_switch > 0: A2 is not a second addend but the A source for k >= k_switch
+  // (K-concatenation of two K-major operands, e.g. [dI_hi | dI_lo] then dI_hi)
+  const bool dual = A2 != nullptr && k_switch <= 0;
+  if (k_switch > 0 && (a_mn || !A2 || k_switch % 64 || k_switch >= K))
+    return fail(HHB_EINVAL, "k_switch needs a K-major A2, a multiple of 64 below K");
   if (flags & ~(HHB_GEMM_A_MN | HHB_GEMM_B_MN)) return fail(HHB_EINVAL, "gemm flags");
   if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
   if (M == 0 || N == 0) return HHB_OK;
@@ -1178,7 +1231,7 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
     const bool pairs = bn >= 128 && M >= 512;
     const int64_t tiles = ((M + (pairs ? 2 * BM : BM) - 1) / (pairs ? 2 * BM : BM)) * ((N + bn - 1) / bn);
     const int64_t P = pairs ? hhb::gemm::num_sms() / 2 : hhb::gemm::num_sms();
-    const double t_kb = 0.28 * (A2 != nullptr ? 2.0 : 1.0) * (pairs ? 1.0 : 0.5) * (double(bn) / 256.0);
+    const double t_kb = 0.28 * (dual ? 2.0 : 1.0) * (pairs ? 1.0 : 0.5) * (double(bn) / 256.0);
     const double t_mn = double(M) * double(N) * 4.0 / 5e12 * 1e6;
     double best = 1e300;
     splits = 1;
@@ -1198,8 +1251,12 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   int rc = a_mn ? make_map_mn(&ta, A, M, K, lda) : make_map(&ta, false, A, M, K, lda, BM);
   if (rc) return rc;
   if (dual && (rc = a_mn ? make_map_mn(&ta2, A2, M, K, lda) : make_map(&ta2, false, A2, M, K, lda, BM))) return rc;
+  if (k_switch > 0) {
+    if ((rc = make_map(&ta, false, A, M, k_switch, lda, BM))) return rc;
+    if ((rc = make_map(&ta2, false, A2, M, K - k_switch, lda, BM))) return rc;
+  }
   if ((rc = b_mn ? make_map_mn(&tb, B, N, K, ldb) : make_map(&tb, false, B, N, K, ldb, bn))) return rc;
-  if (!dual) ta2 = ta;
+  if (!dual && k_switch <= 0) ta2 = ta;
   float* dst = splits > 1 ? workspace : D;
   const int64_t dld = splits > 1 ? N : ldd;
   if (dld % 4 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && !getenv("HHB_GEMM_NONPERSISTENT")) {
@@ -1221,6 +1278,7 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
       pa.tiles = pa.m_tiles * pa.n_tiles * splits;
       pa.idesc = instr_desc(false, bn, a_mn, b_mn, 2 * BM);
       pa.bias = splits > 1 ? nullptr : bias;
+      pa.kb_switch = k_switch > 0 ? int(k_switch / 64) : 0;
 #define HHB_GEMM_2CASE(AM, BMN, DU)                                                              \
   if (a_mn == AM && b_mn == BMN && dual == DU)                                                   \
     rc = bn == 128 ? launch_2sm<128, AM, BMN, DU>(ta, ta2, tb2, td, pa, st)                      \
@@ -1249,6 +1307,7 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
     pa.tiles = pa.m_tiles * pa.n_tiles * splits;
     pa.idesc = instr_desc(false, bn, a_mn, b_mn);
     pa.bias = splits > 1 ? nullptr : bias;
+    pa.kb_switch = k_switch > 0 ? int(k_switch / 64) : 0;
 #define HHB_GEMM_PCASE(AM, BMN, DU)                                   \
   if (a_mn == AM && b_mn == BMN && dual == DU)                        \
     rc = launch_p_bn<AM, BMN, DU>(bn, ta, ta2, tb, td, pa, st);
@@ -1272,6 +1331,7 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
   a.kb_total = kb_total;
   a.kb_per_split = (kb_total + splits - 1) / splits;
   a.idesc = instr_desc(false, bn, a_mn, b_mn);
+  a.kb_switch = k_switch > 0 ? int(k_switch / 64) : 0;
   if (splits > 1) {
     a.D = workspace;
     a.ldd = N;
@@ -1335,6 +1395,14 @@ int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, v
                     int64_t slot, int32_t order, void* stream) {
   if (rows <= 0 || cols <= 0) return HHB_OK;
   if (slot < cols || ldd < 3 * slot || (order != 0 && order != 1)) return fail(HHB_EINVAL, "split3 shape/order");
+  const bool vec = cols % 8 == 0 && lds % 4 == 0 && ldd % 8 == 0 && slot % 8 == 0 &&
+                   reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0;
+  if (vec) {
+    const int64_t total = rows * (cols / 8);
+    hhb::gemm::k_split3_rows_v8<<<grid_1d(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        rows, cols / 8, src, lds, static_cast<__nv_bfloat16*>(dst), ldd, slot, order);
+    return cuda_check("k_split3_rows_v8 launch");
+  }
   const dim3 grid{unsigned((cols + 255) / 256), unsigned(rows < 65535 ? rows : 65535), 1u};
   hhb::gemm::k_split3_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd, slot, order);

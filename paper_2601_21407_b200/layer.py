@@ -153,6 +153,21 @@ def gemm_ex(flags: int, M: int, N: int, K: int, A: torch.Tensor, A2, lda: int, B
     return out
 
 
+def gemm_ex2(flags: int, M: int, N: int, K: int, A: torch.Tensor, A2: torch.Tensor, lda: int, B: torch.Tensor,
+             ldb: int, k_switch: int, splits: int | None = None) -> torch.Tensor:
+    """out[M][N] = [A | A2] . B^T: K-major A for k < k_switch, A2 (same lda) at
+    k - k_switch above (hhb_gemm_ex2)."""
+    out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    lib = nat.load()
+    if splits is None:
+        splits = 0
+    ws_n = int(lib.hhb_gemm_workspace(M, N, splits if splits > 0 else 32))
+    ws = _workspace(ws_n, A.device) if ws_n else None
+    nat.check(lib.hhb_gemm_ex2(flags, M, N, K, A.data_ptr(), A2.data_ptr(), lda, B.data_ptr(), ldb, None,
+                               out.data_ptr(), N, splits, D.ptr(ws), k_switch, _stream()), "hhb_gemm_ex2")
+    return out
+
+
 _WS = {}
 
 
@@ -190,17 +205,18 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
     zb = torch.zeros((2 + p.n_gates) * n, dtype=torch.float32, device=cur.device)
     adj_v = zb[:n]
     adj_g = zb[n:(1 + p.n_gates) * n].view(p.n_gates, n)
-    # dI leaves the BPTT kernel as bf16 hi/lo planes [T*B][P] (P = n_out padded
-    # to 8 for TMA pitches) + per-neuron sums; the gradient GEMMs read them (and
-    # X, W) in place, MN-major
+    # dI leaves the BPTT kernel as bf16 hi/lo halves in one buffer, row (t, b) =
+    # [hi (P) | lo (P)] (P = n_out padded to 8 for TMA pitches), + per-neuron
+    # sums; the gradient GEMMs read it (and X, W) in place: MN-major hi / lo
+    # planes at lda = 2P for dW, K-major [hi | lo] rows for dX
     P = _pad8(n_out)
-    hi = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
-    lo = torch.empty((T, B * P), dtype=torch.bfloat16, device=cur.device)
+    H = torch.empty((T, B * 2 * P), dtype=torch.bfloat16, device=cur.device)
+    hi, lo = H, H.view(-1)[P:]
     dsum = zb[(1 + p.n_gates) * n:]
     with _timed("hh_bptt", T * n):
         _, d_params, gbad = _backward(p, layer.surrogate, cur, n, 1, T, n, ckpt, K, sv, ss, adj_v, adj_g,
-                                      want_d_i=False, split=(hi, lo, n_out, P), d_sum=dsum, ck_ld=n, sv_ld=sv_ld,
-                                      sv_scale=sv_scale)
+                                      want_d_i=False, split=(hi, lo, n_out, 2 * P), d_sum=dsum, ck_ld=n,
+                                      sv_ld=sv_ld, sv_scale=sv_scale)
     layer._last_gbad = gbad
     if layer.check_finite:
         b = int(gbad.item())
@@ -208,15 +224,15 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
             raise GradientOverflowError("adjoint state became non-finite", b)
     layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
     x3 = layer.proj == "bf16x3"
-    kp = xb.shape[1] // 3 if x3 else 0
+    kp = xb.shape[1] // 3 if x3 else 0      # slot width of the [x_hi | x_lo | x_hi] rows
 
     def weight_grad():
         # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views;
         # bf16x3: (dI_hi + dI_lo) . x_hi + dI_hi . x_lo (slots 0 and 1 of xb)
         with _timed("grad_w", 2.0 * M * n_out * k_in):
-            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, P, xb, xb.stride(0))
+            dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, 2 * P, xb, xb.stride(0))
             if x3:
-                dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, P, xb[:, kp:], xb.stride(0))
+                dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, 2 * P, xb[:, kp:], xb.stride(0))
         return dW
 
     if layer.overlap_weight_grad:
@@ -259,9 +275,15 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W);
         # bf16x3: (dI_hi + dI_lo) . W_hi + dI_hi . W_lo (slots 0 and 2 of wb)
         with _timed("grad_x", 2.0 * M * n_out * k_in):
-            dX = gemm_ex(B_MN, M, k_in, n_out, hi, lo, P, wb, wb.stride(0))
-            if x3:
-                dX += gemm_ex(B_MN, M, k_in, n_out, hi, None, P, wb[:, 2 * kp:], wb.stride(0))
+            if x3 and (2 * P) % 64 == 0:
+                # one GEMM over K = 3P: [dI_hi | dI_lo] (the buffer's rows), then
+                # dI_hi again (k_switch), against the stacked [W_hi; W_hi; W_lo]
+                dX = gemm_ex2(B_MN, M, k_in, 3 * P, hi, hi, 2 * P, wb, wb.stride(0), 2 * P)
+            elif x3:
+                dX = gemm_ex(B_MN, M, k_in, 2 * P, hi, None, 2 * P, wb, wb.stride(0))
+                dX += gemm_ex(B_MN, M, k_in, n_out, hi, None, 2 * P, wb[2 * P:], wb.stride(0))
+            else:
+                dX = gemm_ex(B_MN, M, k_in, n_out, hi, lo, 2 * P, wb, wb.stride(0))
         dX = dX.view(T, B, k_in)
     return dX, dW, db
 
@@ -280,11 +302,20 @@ def _project(x, weight, bias, layer):
     T, B, k_in = x.shape
     if layer.proj == "bf16x3":
         # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
-        xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
-        wb, _ = split3_padded(weight.float().contiguous(), 1)
-        with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
+        n_out = weight.shape[0]
+        with _timed("operand_prep", T * B * k_in):
+            xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
+            wb, _ = split3_padded(weight.float().contiguous(), 1)
+            # the input gradient's B operand: rows [W_hi; W_hi; W_lo], each block
+            # n_out rows padded to P (MN-major over the reduction index j)
+            P = _pad8(n_out)
+            w3 = torch.zeros((3 * P, kp), dtype=torch.bfloat16, device=x.device)
+            w3[:n_out] = wb[:, :kp]
+            w3[P:P + n_out] = wb[:, :kp]
+            w3[2 * P:2 * P + n_out] = wb[:, 2 * kp:]
+        with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
             cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
-        return xb, wb, cur
+        return xb, w3, cur
     twin = getattr(x, "_hhb_bf16", None)
     if (twin is not None and twin[1] == x._version and tuple(twin[0].shape) == tuple(x.shape)
             and k_in % 8 == 0):
@@ -292,8 +323,10 @@ def _project(x, weight, bias, layer):
         # them as bf16 0/1 too -- exactly x in bf16, no cast pass
         xb = twin[0].view(T * B, k_in)
     else:
-        xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
-    wb = to_bf16_padded(weight.float().contiguous())
+        with _timed("operand_prep", T * B * k_in):
+            xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
+    with _timed("operand_prep", weight.numel()):
+        wb = to_bf16_padded(weight.float().contiguous())
     with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
         cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())    # (T*B, n_out) == (T, B*n_out)
     return xb, wb, cur

@@ -148,3 +148,41 @@ def test_gemm_ex_layouts_and_dual_operand(cuda, a_mn, b_mn, dual, M, N, K, split
     if dual:   # the pair carries ~16 mantissa bits of the fp32 operand
         full = Am.double() @ Bm.double().T + bias.double()
         assert float((D.double() - full).norm() / full.norm()) < 5e-5
+
+
+@pytest.mark.parametrize("rows,cols", [(300, 784), (33, 20), (64, 24)])
+def test_split3_slots(cuda, rows, cols):
+    """hhb_split3_bf16 (vectorised when cols % 8 == 0, scalar otherwise):
+    slots [hi | lo | hi] (order 0) and [hi | hi | lo] (order 1), hi = bf16(x),
+    lo = bf16(x - hi), pad columns untouched (zero)."""
+    from paper_2601_21407_b200.layer import split3_padded
+    x = torch.randn((rows, cols), device=cuda) * 3.0
+    hi = x.to(torch.bfloat16)
+    lo = (x - hi.float()).to(torch.bfloat16)
+    for order in (0, 1):
+        out, kp = split3_padded(x, order)
+        assert out.shape == (rows, 3 * kp) and kp % 8 == 0 and kp >= cols
+        s0, s1, s2 = out[:, :cols], out[:, kp:kp + cols], out[:, 2 * kp:2 * kp + cols]
+        assert torch.equal(s0, hi)
+        assert torch.equal(s1, lo if order == 0 else hi)
+        assert torch.equal(s2, hi if order == 0 else lo)
+        if kp > cols:
+            assert not out[:, cols:kp].float().any()
+
+
+@pytest.mark.parametrize("M,N,P", [(1024, 784, 1024), (512, 96, 32), (256, 40, 64)])
+def test_gemm_k_switch_concatenates_a(cuda, M, N, P):
+    """hhb_gemm_ex2: K-major A for k < k_switch, A2 (same pitch) at k - k_switch
+    above -- here the layer's dX: A rows [hi | lo] (2P), then hi again, against
+    MN-major B rows [B0; B1; B2] (3P x N); equal to the explicit concatenation."""
+    from paper_2601_21407_b200.layer import B_MN, gemm_ex, gemm_ex2
+    torch.manual_seed(1)
+    H = torch.randn((M, 2 * P), device=cuda).to(torch.bfloat16)
+    Bm = torch.randn((3 * P, N), device=cuda).to(torch.bfloat16).contiguous()
+    got = gemm_ex2(B_MN, M, N, 3 * P, H, H, 2 * P, Bm, N, 2 * P)
+    a_cat = torch.cat([H, H[:, :P]], dim=1).float()
+    ref = a_cat @ Bm.float()
+    assert torch.allclose(got, ref, rtol=1e-4, atol=1e-3), float((got - ref).abs().max())
+    # the explicit concatenation through the plain GEMM agrees bit for bit
+    explicit = gemm_ex(B_MN, M, N, 3 * P, torch.cat([H, H[:, :P]], dim=1).contiguous(), None, 3 * P, Bm, N)
+    assert torch.equal(got, explicit)

@@ -193,7 +193,7 @@ def test_overlapped_weight_grads_match(cuda):
         assert torch.allclose(a, b, rtol=1e-6, atol=1e-9)
 
 
-@pytest.mark.parametrize("budget,n_out", [(None, 8), (4, 10), (None, 16)])
+@pytest.mark.parametrize("budget,n_out", [(None, 8), (4, 10), (None, 16), (None, 32), (3, 64)])
 def test_layer_bf16x3_matches_unrounded_oracle(cuda, budget, n_out):
     """proj="bf16x3" against the reference composition on the UNROUNDED
     operands (the float32 x and W taken exactly into float64, learn.py:210-211
