@@ -1210,7 +1210,9 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
   if ((lda * 2) % 16 || (ldb * 2) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
       reinterpret_cast<uintptr_t>(A2) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
     return fail(HHB_EINVAL, "gemm operands need 16-byte aligned base and row pitch");
-  if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
+  // K-switched A: each source spans only its own K range
+  const int64_t ka = k_switch > 0 ? (k_switch > K - k_switch ? k_switch : K - k_switch) : K;
+  if (lda < (a_mn ? M : ka) || ldb < (b_mn ? N : K)) return fail(HHB_EINVAL, "lda/ldb too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kb_total = int((K + 63) / 64);
   // tile width: 64 / 128 for narrow N, else 256 (N = 784 measured 78.8 us
