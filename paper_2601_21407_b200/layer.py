@@ -210,7 +210,8 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
     # sums; the gradient GEMMs read it (and X, W) in place: MN-major hi / lo
     # planes at lda = 2P for dW, K-major [hi | lo] rows for dX
     P = _pad8(n_out)
-    H = torch.empty((T, B * 2 * P), dtype=torch.bfloat16, device=cur.device)
+    # (pad columns n_out..P of each half are read by the K-concatenated dX GEMMs: zeros)
+    H = (torch.empty if P == n_out else torch.zeros)((T, B * 2 * P), dtype=torch.bfloat16, device=cur.device)
     hi, lo = H, H.view(-1)[P:]
     dsum = zb[(1 + p.n_gates) * n:]
     with _timed("hh_bptt", T * n):
