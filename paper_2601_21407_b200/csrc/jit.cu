@@ -1181,7 +1181,7 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
       svo += a.spkv_ld;
     }
     if (FF_SVB) {   // bf16 0/1 (0x3F80 = 1.0): the next layer's GEMM operand, written beside the fp32 flags
-      if (VEC == 4 && (AL || full)) {
+      if (VEC == 4 && AL) {           // AL: the host checked 8-byte alignment of every row (spkb_ld % 4 == 0)
         const u32 lo = ((nib & 1u) ? 0x3F80u : 0u) | ((nib & 2u) ? 0x3F800000u : 0u);
         const u32 hi = ((nib & 4u) ? 0x3F80u : 0u) | ((nib & 8u) ? 0x3F800000u : 0u);
         *reinterpret_cast<uint2*>(sbo) = make_uint2(lo, hi);
