@@ -439,10 +439,14 @@ def c5_leg(torch, dev, steps=1000, with_cpu=False, scale=0.5):
     build_s = time.perf_counter() - t0
     ex, ex_kind = None, None
     if world > 1:
-        if dist.get_backend() == "nccl":
+        if dist.get_backend() == "nccl" and os.environ.get("HHB_BENCH_C5_EXCHANGE", "library") == "library":
             # the library exchange (hhb_spk_step: ncclAllGather + delivery), captured into
-            # the 64-step CUDA graphs with the step kernels
-            ex, ex_kind = N.LibraryExchange(topo.n_neurons), "library ncclAllGather in CUDA graphs"
+            # the 64-step CUDA graphs with the step kernels; a hung or failed peer
+            # surfaces as ExchangeError after 120 s (the communicator is aborted)
+            ex = N.LibraryExchange(topo.n_neurons, timeout_s=120.0)
+            ex_kind = "library ncclAllGather in CUDA graphs"
+        elif dist.get_backend() == "nccl":
+            ex, ex_kind = N.allgather_exchange(topo.n_neurons), "torch.distributed all-gather (NCCL, eager)"
         else:
             ex, ex_kind = N.allgather_exchange(topo.n_neurons), "torch.distributed all-gather (gloo, host-staged)"
     net = N.CortexNetwork(topo, N.REST_CONFIG, device=dev, dtype=np.float32, rank=rank, world=world,
