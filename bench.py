@@ -460,11 +460,13 @@ def c5_leg(torch, dev, steps=1000, with_cpu=False, scale=0.5):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if graphs:
-        net.advance(steps)       # one persistent cooperative kernel (graph replay if unavailable)
+        net.advance(steps, wait=False)   # one persistent cooperative kernel (graph replay if unavailable)
     else:
         for _ in range(steps):
             net.step()
     e1.record()
+    if hasattr(ex, "wait"):
+        ex.wait()                # NCCL error / timeout check, outside the timed events
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     m = torch.tensor([ms], dtype=torch.float64, device=dev)

@@ -614,7 +614,8 @@ class CortexNetwork:
         self.t_dev.fill_(self.t)
         return record
 
-    def advance(self, n_steps: int, steps_per_graph: int = 64, record: torch.Tensor | None = None):
+    def advance(self, n_steps: int, steps_per_graph: int = 64, record: torch.Tensor | None = None,
+                wait: bool = True):
         """Advance n_steps.  One rank with float32 neurons runs them in ONE
         persistent cooperative kernel (hhb_cortex_run: the phases of each step
         separated by grid barriers); otherwise a CUDA graph of
@@ -624,7 +625,9 @@ class CortexNetwork:
         bit-identical to `step()`.  record: optional int32
         [n_steps][words_global] device buffer receiving each step's global
         spike words.  Host-RNG background cannot run on the device (use
-        step())."""
+        step()).  With a LibraryExchange the call ends by waiting for the
+        steps (NCCL error / timeout check) unless wait=False (then call
+        exchange.wait() yourself)."""
         if self.bg_mode == "host":
             raise UsageError("advance(): the host background is drawn per step; use step()")
         if n_steps > 0 and self.persistent_ok() and not getattr(self, "_no_persist", False):
@@ -669,7 +672,7 @@ class CortexNetwork:
                 record[done].copy_(gw[:self.words_global])
             done += 1
         self.t += n_steps
-        if hasattr(self.exchange, "wait"):
+        if wait and hasattr(self.exchange, "wait"):
             self.exchange.wait()        # NCCL async errors / a hung peer surface here (ExchangeError)
         return record
 
