@@ -494,7 +494,7 @@ static bool disabled() {
 }
 
 // shared exponentials (independent MUFU ops, issued back to back)
-static std::string emit_exps(const Plan& M, std::vector<std::string>* names = nullptr) {
+static std::string emit_exps(const Plan& M) {
   std::string o;
   std::vector<int> direct_only(M.groups.size(), 1);
   for (const auto& g : M.gates)
@@ -505,7 +505,6 @@ static std::string emit_exps(const Plan& M, std::vector<std::string>* names = nu
     const double K2 = -kLog2e / M.groups[i].b;
     o += fmt("  const float E%d = ex2f_(__fmaf_rn(v, %s, %s));\n", int(i), F(K2).c_str(),
              F(-M.groups[i].vc * K2).c_str());
-    if (names) names->push_back(fmt("E%d", int(i)));
   }
   return o;
 }
@@ -519,8 +518,7 @@ static std::string emit_exps(const Plan& M, std::vector<std::string>* names = nu
 // (measured: 36 % of config-2 forward warp-steps and 40 % of config-3 BPTT
 // warp-steps have a lane inside the series window).
 static std::string linoid_name(int g, int w) { return fmt("g%d%s", g, w ? "b" : "a"); }
-static std::string emit_linoid_pre(const Plan& M, std::string& anysg, std::vector<std::string>* names = nullptr,
-                                   std::string* sgdefs = nullptr) {
+static std::string emit_linoid_pre(const Plan& M, std::string& anysg) {
   std::string o;
   anysg.clear();
   for (size_t g = 0; g < M.gates.size(); ++g)
@@ -537,36 +535,8 @@ static std::string emit_linoid_pre(const Plan& M, std::string& anysg, std::vecto
       const double thr = r.sigma > 0 ? kSingThr : kSingThr * r.c;
       o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm.c_str(), nm.c_str(), F(thr).c_str());
       anysg += (anysg.empty() ? "" : " || ") + nm + "sg";
-      if (names) {
-        names->push_back(nm + "x");
-        names->push_back(nm + "d0");
-      }
-      if (sgdefs) *sgdefs += fmt("  const bool %ssg = SING && fabsf(%sd0) < %s;\n", nm.c_str(), nm.c_str(), F(thr).c_str());
     }
   return o;
-}
-
-
-// Split of a merged step into pre_<tag>(v) -> struct (the rate exponentials,
-// linoid x / d0 and the any-lane-in-a-series-window flag) and
-// body_<tag><SING>(..., const Pre<tag>&): callers vote ONCE over all the
-// neurons a thread steps (step_all / step_bwd_mv) and run straight-line bodies
-// (the per-neuron vote inside each step cost the 4-neuron interleaving: -9 %).
-static std::string emit_pre_fn(const char* tag, const std::string& pre, const std::vector<std::string>& names,
-                               const std::string& anysg) {
-  std::string o = fmt("struct Pre%s { ", tag);
-  for (const auto& n : names) o += "float " + n + "; ";
-  o += "bool any; };\n";
-  o += fmt("__device__ __forceinline__ Pre%s pre_%s(const float v) {\n", tag, tag) + pre;
-  o += fmt("  Pre%s q;\n", tag);
-  for (const auto& n : names) o += "  q." + n + " = " + n + ";\n";
-  o += "  q.any = " + (anysg.empty() ? std::string("false") : anysg) + ";\n  return q;\n}\n";
-  return o;
-}
-static std::string emit_pre_unpack(const std::vector<std::string>& names, const std::string& sgdefs) {
-  std::string o;
-  for (const auto& n : names) o += "  const float " + n + " = q." + n + ";\n";
-  return o + sgdefs;
 }
 
 // symbolic float expression that knows when it is identically zero (the
@@ -740,14 +710,12 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
   const int NG = L.ng;
   o += fmt("__device__ __forceinline__ bool regular(const float v) { return fabsf(__fsub_rn(v, %s)) < %s; }\n",
            F(0.5 * (M.lo + M.hi)).c_str(), F(0.5 * (M.hi - M.lo)).c_str());
-  std::string anysg, sgdefs;
-  std::vector<std::string> names;
-  std::string pre = emit_exps(M, &names);
-  pre += emit_linoid_pre(M, anysg, &names, &sgdefs);
-  o += emit_pre_fn("F", pre, names, anysg);
-  o += fmt("template <bool SING>\n__device__ __forceinline__ float body_F(const float v, float (&p)[%d], "
-           "const float cur, const PreF& q) {\n", NG > 0 ? NG : 1);
-  o += emit_pre_unpack(names, sgdefs);
+  o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
+           NG > 0 ? NG : 1);
+  o += emit_exps(M);
+  std::string anysg;
+  o += emit_linoid_pre(M, anysg);
+  o += "  auto body = [&](auto S_) -> float {\n  constexpr bool SING = decltype(S_)::value;\n";
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += "  float eta = 1.0f;\n";
@@ -840,11 +808,11 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
                F(-C.g_max * C.e_rev).c_str());
     o += "  }\n";
   }
-  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n}\n", F(P->dt / P->c_m).c_str());
-  o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n"
-           "  const PreF q = pre_F(v);\n"
-           "  if (__any_sync(0xffffffffu, q.any)) return body_F<true>(v, p, cur, q);\n"
-           "  return body_F<false>(v, p, cur, q);\n}\n", NG > 0 ? NG : 1);
+  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n  };\n", F(P->dt / P->c_m).c_str());
+  if (anysg.empty()) o += "  return body(BoolC<false>());\n}\n";
+  else
+    o += fmt("  if (__any_sync(0xffffffffu, %s)) return body(BoolC<true>());\n  return body(BoolC<false>());\n}\n",
+             anysg.c_str());
   return o;
 }
 
@@ -861,24 +829,15 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
   std::string o;
   const int NG = L.ng, NGX = NG > 0 ? NG : 1;
   const double dtcm = P->dt / P->c_m;
-  std::string anysg, sgdefs;
-  std::vector<std::string> names;
+  o += fmt(
+      "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
+      "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
+      "float (&acc)[%d]) {\n",
+      M ? "m" : (mode == kFast ? "f" : "s"), NGX, NGX, kSlots);
+  std::string anysg;
   if (M) {
-    std::string pre = mg::emit_exps(*M, &names);
-    pre += mg::emit_linoid_pre(*M, anysg, &names, &sgdefs);
-    o += mg::emit_pre_fn("B", pre, names, anysg);
-    o += fmt(
-        "template <bool SING>\n__device__ __forceinline__ float body_B(const Sur& sur, const float v, "
-        "const float (&p)[%d], const float cur, float& d_v, float (&d_p)[%d], const float d_spike, "
-        "const bool has_s, float (&acc)[%d], const PreB& q) {\n",
-        NGX, NGX, kSlots);
-    o += mg::emit_pre_unpack(names, sgdefs);
-  } else {
-    o += fmt(
-        "__device__ __forceinline__ float step_bwd_%s(const Sur& sur, const float v, const float (&p)[%d], "
-        "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
-        "float (&acc)[%d]) {\n",
-        mode == kFast ? "f" : "s", NGX, NGX, kSlots);
+    o += mg::emit_exps(*M);
+    o += mg::emit_linoid_pre(*M, anysg);
   }
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
@@ -916,6 +875,7 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
              F(P->channels[L.leak_ch[j]].e_rev).c_str(), k);
   }
   o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
+  if (M) o += "  auto gates = [&](auto S_) {\n  constexpr bool SING = decltype(S_)::value;\n";
   for (int g = 0; g < NG; ++g) {
     const hhb_gate_t& G = P->gates[g];
     const hhb_channel_t& C = P->channels[L.chan[g]];
@@ -956,31 +916,14 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
     }
     o += fmt("  d_p[%d] = dp;\n  }\n", g);
   }
+  if (M) {
+    o += "  };\n";
+    if (anysg.empty()) o += "  gates(BoolC<false>());\n";
+    else o += fmt("  if (__any_sync(0xffffffffu, %s)) gates(BoolC<true>());\n  else gates(BoolC<false>());\n",
+                  anysg.c_str());
+  }
   o += "  d_v = dv_in;\n";
   o += fmt("  return __fmul_rn(g_vp, %s);\n}\n", F(dtcm).c_str());
-  if (M) {
-    o += fmt(
-        "__device__ __forceinline__ float step_bwd_m(const Sur& sur, const float v, const float (&p)[%d], "
-        "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
-        "float (&acc)[%d]) {\n"
-        "  const PreB q = pre_B(v);\n"
-        "  if (__any_sync(0xffffffffu, q.any)) return body_B<true>(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc, q);\n"
-        "  return body_B<false>(sur, v, p, cur, d_v, d_p, d_spike, has_s, acc, q);\n}\n",
-        NGX, NGX, kSlots);
-    // all VEC neurons of a thread under one vote (the BPTT kernel's regular path)
-    o += fmt(
-        "template <int VEC>\n__device__ __forceinline__ void step_bwd_mv(const Sur& sur, const float (&v)[VEC], "
-        "const float (&p)[VEC][%d], const float (&cur)[VEC], float (&d_v)[VEC], float (&d_p)[VEC][%d], "
-        "const float (&ds)[VEC], const bool has_s, float (&acc)[%d], float (&di)[VEC]) {\n"
-        "  PreB q[VEC];\n  bool any = false;\n"
-        "#pragma unroll\n  for (int j = 0; j < VEC; ++j) { q[j] = pre_B(v[j]); any = any || q[j].any; }\n"
-        "  if (__any_sync(0xffffffffu, any)) {\n"
-        "#pragma unroll\n    for (int j = 0; j < VEC; ++j) di[j] = body_B<true>(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], has_s, acc, q[j]);\n"
-        "  } else {\n"
-        "#pragma unroll\n    for (int j = 0; j < VEC; ++j) di[j] = body_B<false>(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], has_s, acc, q[j]);\n"
-        "  }\n}\n",
-        NGX, NGX, kSlots);
-  }
   return o;
 }
 
@@ -1879,7 +1822,8 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #if HAS_MERGED
       // one warp vote per step for all VEC neurons of every lane
       if (__all_sync(0xffffffffu, reg)) {
-        step_bwd_mv<VEC>(sur, v, p, cur, d_v, d_p, ds, BF_SS, accf, di);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) di[j] = step_bwd_m(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) di[j] = step_bwd_irr(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
@@ -2036,19 +1980,8 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
       for (int g = 0; g < NGX; ++g) p[j][g] = reg ? pm[g] : p[j][g];
     }
   } else {
-    // every neuron regular: one more vote, over all VEC neurons, picks the
-    // body with or without the linoid series (straight-line bodies interleave)
-    PreF q[VEC];
-    bool any = false;
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) { q[j] = pre_F(v[j]); any = any || q[j].any; }
-    if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) vn[j] = body_F<true>(v[j], p[j], cur[j], q[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) vn[j] = body_F<false>(v[j], p[j], cur[j], q[j]);
-    }
+    for (int j = 0; j < VEC; ++j) vn[j] = step_fwd_m(v[j], p[j], cur[j]);
   }
 }
 )";
