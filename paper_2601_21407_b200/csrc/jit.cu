@@ -509,36 +509,6 @@ static std::string emit_exps(const Plan& M) {
   return o;
 }
 
-// The linoid rates' removable-singularity tests, hoisted out of the gate code:
-// x = v - v0, the fraction denominator d0 and the series flag sg for every
-// linoid rate of the table (names g<gate><a|b>x / d0 / sg).  The step body is
-// a generic lambda over SING: one warp vote (any lane near a singularity?)
-// picks the body with the series selects or the one without them -- the
-// selected values are identical, so the result does not depend on the path
-// (measured: 36 % of config-2 forward warp-steps and 40 % of config-3 BPTT
-// warp-steps have a lane inside the series window).
-static std::string linoid_name(int g, int w) { return fmt("g%d%s", g, w ? "b" : "a"); }
-static std::string emit_linoid_pre(const Plan& M, std::string& anysg) {
-  std::string o;
-  anysg.clear();
-  for (size_t g = 0; g < M.gates.size(); ++g)
-    for (int w = 0; w < 2; ++w) {
-      const RatePlan& r = w ? M.gates[g].b : M.gates[g].a;
-      if (r.kind != HHB_RATE_LINOID) continue;
-      const std::string nm = linoid_name(int(g), w);
-      const std::string E = fmt("E%d", r.group);
-      o += fmt("  const float %sx = __fsub_rn(v, %s);\n", nm.c_str(), F(r.v0).c_str());
-      if (r.sigma > 0)
-        o += fmt("  const float %sd0 = __fmaf_rn(%s, %s, 1.0f);\n", nm.c_str(), F(-r.c).c_str(), E.c_str());
-      else
-        o += fmt("  const float %sd0 = __fsub_rn(%s, %s);\n", nm.c_str(), E.c_str(), F(r.c).c_str());
-      const double thr = r.sigma > 0 ? kSingThr : kSingThr * r.c;
-      o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm.c_str(), nm.c_str(), F(thr).c_str());
-      anysg += (anysg.empty() ? "" : " || ") + nm + "sg";
-    }
-  return o;
-}
-
 // symbolic float expression that knows when it is identically zero (the
 // compiler may not fold x * 0.0f: x could be inf or NaN)
 struct X {
@@ -572,8 +542,7 @@ struct RateX {
   bool rat;
   X v, v1, n, d, n1, d1;
 };
-static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<Group>& G, const char* nm,
-                           int gidx) {
+static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<Group>& G, const char* nm) {
   RateX R;
   const double l2 = 1.0;   // slope scale (the decay term applies ln2 to s' itself)
   const std::string E = fmt("E%d", r.group);
@@ -613,26 +582,31 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
       }
       break;
     default: {
-      // x, d0 and the series flag are hoisted (emit_linoid_pre, names h*)
-      const std::string h = linoid_name(gidx, std::string(nm) == "b" ? 1 : 0);
-      std::string n0, n10, d10;
+      o += fmt("  const float %sx = __fsub_rn(v, %s);\n", nm, F(r.v0).c_str());
+      std::string n0, d0, n10, d10;
+      double thr;
       if (r.sigma > 0) {
-        n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), h.c_str());
+        n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), nm);
+        d0 = fmt("__fmaf_rn(%s, %s, 1.0f)", F(-r.c).c_str(), E.c_str());
         n10 = F(l2 * r.Sa);
         d10 = fmt("__fmul_rn(%s, %s)", F(l2 * r.c / bg).c_str(), E.c_str());
+        thr = kSingThr;
       } else {
-        n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), h.c_str(), E.c_str());
-        n10 = fmt("__fmul_rn(__fmaf_rn(%sx, %s, %s), %s)", h.c_str(), F(-l2 * r.Sa / bg).c_str(),
-                  F(l2 * r.Sa).c_str(), E.c_str());
+        n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), nm, E.c_str());
+        d0 = fmt("__fsub_rn(%s, %s)", E.c_str(), F(r.c).c_str());
+        n10 = fmt("__fmul_rn(__fmaf_rn(%sx, %s, %s), %s)", nm, F(-l2 * r.Sa / bg).c_str(), F(l2 * r.Sa).c_str(),
+                  E.c_str());
         d10 = fmt("__fmul_rn(%s, %s)", E.c_str(), F(-l2 / bg).c_str());
+        thr = kSingThr * r.c;
       }
-      o += fmt("  const bool %ssg = SING && %ssg;\n", nm, h.c_str());
-      o += fmt("  const float %sns = SING ? __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s) : 0.0f;\n", nm, h.c_str(),
-               h.c_str(), F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), F(r.Sa * r.b).c_str());
+      o += fmt("  const float %sd0 = %s;\n", nm, d0.c_str());
+      o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm, nm, F(thr).c_str());
+      o += fmt("  const float %sns = __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s);\n", nm, nm, nm,
+               F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), F(r.Sa * r.b).c_str());
       o += fmt("  const float %sn = %ssg ? %sns : %s;\n", nm, nm, nm, n0.c_str());
-      o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, h.c_str());
+      o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, nm);
       // slopes: d/dx of a b (1 + u/2 + u^2/12) = a (1/2 + u/6) in the series region
-      o += fmt("  const float %sn1 = %ssg ? __fmaf_rn(%sx, %s, %s) : %s;\n", nm, nm, h.c_str(),
+      o += fmt("  const float %sn1 = %ssg ? __fmaf_rn(%sx, %s, %s) : %s;\n", nm, nm, nm,
                F(l2 * r.Sa / (6.0 * r.b)).c_str(), F(l2 * 0.5 * r.Sa).c_str(), n10.c_str());
       o += fmt("  const float %sd1 = %ssg ? 0.0f : %s;\n", nm, nm, d10.c_str());
       R.n = V(w + "n");
@@ -649,8 +623,8 @@ static RateX emit_rate_bwd(std::string& o, const RatePlan& r, const std::vector<
 // (adjoint.py:155-164); with s~ = -dt log2(e) s, (-dt)(a' + b') = ln2 s~'.
 static std::string emit_gate_bwd(const GatePlan& gp, const std::vector<Group>& G, int g) {
   std::string o;
-  const RateX a = emit_rate_bwd(o, gp.a, G, "a", g);
-  const RateX b = emit_rate_bwd(o, gp.b, G, "b", g);
+  const RateX a = emit_rate_bwd(o, gp.a, G, "a");
+  const RateX b = emit_rate_bwd(o, gp.b, G, "b");
   X s, s1, pinf, dpinf;
   if (!a.rat && !b.rat) {
     s = bind(o, "s", addx(a.v, b.v));
@@ -713,9 +687,6 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
   o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
            NG > 0 ? NG : 1);
   o += emit_exps(M);
-  std::string anysg;
-  o += emit_linoid_pre(M, anysg);
-  o += "  auto body = [&](auto S_) -> float {\n  constexpr bool SING = decltype(S_)::value;\n";
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += "  float eta = 1.0f;\n";
@@ -758,18 +729,25 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
                      F(r.Sa).c_str(), E.c_str(), nm, E.c_str(), F(r.c).c_str());
           break;
         default: {
-          // x, d0 and the series flag are hoisted (emit_linoid_pre)
-          const std::string h = linoid_name(g, w);
-          std::string n0;
-          if (r.sigma > 0) n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), h.c_str());
-          else n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), h.c_str(), E.c_str());
-          o += fmt("  const bool %ssg = SING && %ssg;\n", nm, h.c_str());
+          o += fmt("  const float %sx = __fsub_rn(v, %s);\n", nm, F(r.v0).c_str());
+          std::string n0, d0;
+          double thr;
+          if (r.sigma > 0) {
+            n0 = fmt("__fmul_rn(%s, %sx)", F(r.Sa).c_str(), nm);
+            d0 = fmt("__fmaf_rn(%s, %s, 1.0f)", F(-r.c).c_str(), E.c_str());
+            thr = kSingThr;
+          } else {
+            n0 = fmt("__fmul_rn(__fmul_rn(%s, %sx), %s)", F(r.Sa).c_str(), nm, E.c_str());
+            d0 = fmt("__fsub_rn(%s, %s)", E.c_str(), F(r.c).c_str());
+            thr = kSingThr * r.c;
+          }
+          o += fmt("  const float %sd0 = %s;\n", nm, d0.c_str());
+          o += fmt("  const bool %ssg = fabsf(%sd0) < %s;\n", nm, nm, F(thr).c_str());
           // a b (1 + u/2 + u^2/12), u = x / b, as a Horner form in x
-          o += fmt("  const float %sns = SING ? __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s) : 0.0f;\n", nm,
-                   h.c_str(), h.c_str(), F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(),
-                   F(r.Sa * r.b).c_str());
+          o += fmt("  const float %sns = __fmaf_rn(%sx, __fmaf_rn(%sx, %s, %s), %s);\n", nm, nm, nm,
+                   F(r.Sa / (12.0 * r.b)).c_str(), F(0.5 * r.Sa).c_str(), F(r.Sa * r.b).c_str());
           o += fmt("  const float %sn = %ssg ? %sns : %s;\n", nm, nm, nm, n0.c_str());
-          o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, h.c_str());
+          o += fmt("  const float %sd = %ssg ? 1.0f : %sd0;\n", nm, nm, nm);
         }
       }
     }
@@ -808,11 +786,7 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
                F(-C.g_max * C.e_rev).c_str());
     o += "  }\n";
   }
-  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n  };\n", F(P->dt / P->c_m).c_str());
-  if (anysg.empty()) o += "  return body(BoolC<false>());\n}\n";
-  else
-    o += fmt("  if (__any_sync(0xffffffffu, %s)) return body(BoolC<true>());\n  return body(BoolC<false>());\n}\n",
-             anysg.c_str());
+  o += fmt("  return __fmaf_rn(__fsub_rn(cur, ion), %s, v);\n}\n", F(P->dt / P->c_m).c_str());
   return o;
 }
 
@@ -834,11 +808,7 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
       "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, "
       "float (&acc)[%d]) {\n",
       M ? "m" : (mode == kFast ? "f" : "s"), NGX, NGX, kSlots);
-  std::string anysg;
-  if (M) {
-    o += mg::emit_exps(*M);
-    o += mg::emit_linoid_pre(*M, anysg);
-  }
+  if (M) o += mg::emit_exps(*M);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += fmt("  float gsum = %s;\n", F(L.gl).c_str());
@@ -875,7 +845,6 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
              F(P->channels[L.leak_ch[j]].e_rev).c_str(), k);
   }
   o += fmt("  float dv_in = __fmul_rn(g_vp, __fmaf_rn(%s, gsum, 1.0f));\n", F(-dtcm).c_str());
-  if (M) o += "  auto gates = [&](auto S_) {\n  constexpr bool SING = decltype(S_)::value;\n";
   for (int g = 0; g < NG; ++g) {
     const hhb_gate_t& G = P->gates[g];
     const hhb_channel_t& C = P->channels[L.chan[g]];
@@ -916,12 +885,6 @@ static std::string emit_backward_step(const hhb_params_t* P, const Layout& L, Se
     }
     o += fmt("  d_p[%d] = dp;\n  }\n", g);
   }
-  if (M) {
-    o += "  };\n";
-    if (anysg.empty()) o += "  gates(BoolC<false>());\n";
-    else o += fmt("  if (__any_sync(0xffffffffu, %s)) gates(BoolC<true>());\n  else gates(BoolC<false>());\n",
-                  anysg.c_str());
-  }
   o += "  d_v = dv_in;\n";
   o += fmt("  return __fmul_rn(g_vp, %s);\n}\n", F(dtcm).c_str());
   return o;
@@ -937,7 +900,6 @@ static const char* kPrelude = R"(
 #endif
 typedef long long i64;
 typedef unsigned int u32;
-template <bool B> struct BoolC { static constexpr bool value = B; };
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
