@@ -347,8 +347,7 @@ struct Flavour {
          (a.v_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.v_out) % (sizeof(T) * (VECW)) == 0)) && \
         (a.ckpt == nullptr ||                                                                    \
          (a.ck_ld % (VECW) == 0 && reinterpret_cast<uintptr_t>(a.ckpt) % (sizeof(T) * (VECW)) == 0)); \
-    const bool wide = vec_ok && a.n >= int64_t(kNumSMs) * 32 * (VECW) &&                          \
-                      !(a.ckpt != nullptr && getenv("HHB_FWD_CK_VEC1"));   /* experiment knob */        \
+    const bool wide = vec_ok && a.n >= int64_t(kNumSMs) * 32 * (VECW);                            \
     int jrc = HHB_OK;                                                                            \
     if (try_jit_fwd<T>(P, a, ptab, wide && (VECW) == 4, st, jrc)) return jrc;                    \
     if (pois)                                                                                    \
