@@ -137,6 +137,14 @@ def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True):
                                "reference_tau_frac": TAU_RS_F * fw / mufu_peak,
                                "share_of_step": f.get("ms_per_step", 0) / step_ms},
             "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kern.items()}}
+    if "inst_per_neuron_step" in prof and bw:
+        # instruction-issue view (4 warp-instructions / clk / SM = 128 thread-instructions):
+        # the bound that binds this kernel (ncu: issue active 78 %, MUFU 39 %, FMA 47 %)
+        sm_hz = 1965.0e6
+        issue_bound = 148 * 128 * sm_hz / prof["inst_per_neuron_step"]
+        roof["issue"] = {"inst_per_neuron_step": prof["inst_per_neuron_step"],
+                         "bound_neuron_steps_per_s": issue_bound, "frac": bw / issue_bound,
+                         "source": prof.get("source")}
     if "xu_inst_per_neuron_step" in prof:
         roof["mufu_check"] = {"source_count": mb, "ncu_sass_count": prof["xu_inst_per_neuron_step"],
                               "agree": abs(prof["xu_inst_per_neuron_step"] - mb) <= 0.05 * mb}
