@@ -22,6 +22,13 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); calls the C-ABI kernels")
 
 
+# features that exist only in the NVRTC-generated kernels (the persistent
+# network kernel, the specialised modules): skipped when the generic
+# table-driven kernels are forced (HHB_NO_JIT=1 runs of the GPU suite)
+requires_jit = pytest.mark.skipif(os.environ.get("HHB_NO_JIT", "0") not in ("", "0"),
+                                  reason="JIT-only feature (HHB_NO_JIT set)")
+
+
 def golden(name):
     return np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
 

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden
+from conftest import golden, requires_jit
 from oracle import hh_oracle as O
 from paper_2601_21407_b200 import adjoint as A
 from paper_2601_21407_b200 import defaults as DF
@@ -341,6 +341,7 @@ def test_pipelined_host_path_equals_device_path(cuda, chunk_bytes, monkeypatch):
     assert e.value.step_index == 150
 
 
+@requires_jit
 def test_jit_specialised_kernels_are_active(cuda):
     from paper_2601_21407_b200 import _native as nat
     p = DF.cortical_rs_params(dt=0.1).with_(dtype=np.float32)

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden
+from conftest import golden, requires_jit
 from paper_2601_21407_b200 import network as N
 
 pytestmark = pytest.mark.gpu
@@ -198,6 +198,7 @@ def test_replicas_reproduce_single_network_runs(cuda):
         assert torch.equal(single.v, rep.v[r * rep.n_pad:r * rep.n_pad + topo.n_neurons])
 
 
+@requires_jit
 @pytest.mark.parametrize("cap,nopair", [(None, False), ("3", False), (None, True)])
 def test_persistent_kernel_equals_graph_path(cuda, monkeypatch, cap, nopair):
     """advance() on one rank with float32 neurons runs the persistent
@@ -301,6 +302,7 @@ def test_non_finite_state_is_reported_with_its_step(cuda, monkeypatch, graph):
         N._raise_if_bad(net.first_bad)
 
 
+@requires_jit
 def test_persistent_replicas_equal_graph_replicas(cuda, monkeypatch):
     """CortexReplicas in persistent launches (groups of <= 16 replicas) equal
     the graph path bit for bit, across a group boundary (R = 19)."""
@@ -340,6 +342,7 @@ def test_record_buffer_shape_is_checked(cuda):
     assert not tall[10:].any()
 
 
+@requires_jit
 def test_graphs_captured_before_segment_sort_are_dropped(cuda, monkeypatch):
     """A graph captured on the unsorted synapse arrays must not be replayed
     after the persistent path re-sorted them (the old buffers are freed)."""
@@ -463,6 +466,7 @@ def test_device_thalamic_drive_matches_restated_philox(cuda):
         assert np.array_equal(got, want), t
 
 
+@requires_jit
 def test_thalamic_persistent_graph_eager_and_shards_agree(cuda, monkeypatch):
     """With the device thalamic drive, the persistent kernel, the CUDA-graph
     path and eager steps give the same rasters and state bit for bit, and so
