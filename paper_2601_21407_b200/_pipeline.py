@@ -62,6 +62,7 @@ def pinned_empty(shape, dtype) -> np.ndarray:
 
 
 CHUNK_BYTES = int(os.environ.get("HHB_PIPE_CHUNK_MB", "64")) << 20   # input bytes per pipelined chunk
+MIN_CHUNKS = int(os.environ.get("HHB_PIPE_MIN_CHUNKS", "12"))         # chunks of a long, narrow call (measured: 12-16 best for config 1)
 
 
 def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forward, unpack,
@@ -78,6 +79,11 @@ def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forw
     cdt = D.np_dtype(params.dtype)
     tdt = D.torch_dtype(cdt)
     tc_max = int(max(1, min(T, chunk_bytes // max(1, n * cdt.itemsize))))
+    # small populations over long horizons (config 1: 1,024 x 10,000) fit one
+    # chunk: cut them into >= MIN_CHUNKS so the copies overlap the
+    # (latency-bound) compute
+    if T >= 4 * 64 and tc_max * MIN_CHUNKS > T:
+        tc_max = max(64, (T + MIN_CHUNKS - 1) // MIN_CHUNKS)
     nbuf = 2
     stage = [torch.empty((tc_max, n), dtype=tdt, pin_memory=True) for _ in range(nbuf)]
     d_in = [torch.empty((tc_max, n), dtype=tdt, device=dev) for _ in range(nbuf)]
