@@ -85,7 +85,8 @@ def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forw
     if T >= 4 * 64 and tc_max * MIN_CHUNKS > T:
         tc_max = max(64, (T + MIN_CHUNKS - 1) // MIN_CHUNKS)
     nbuf = 2
-    stage = [torch.empty((tc_max, n), dtype=tdt, pin_memory=True) for _ in range(nbuf)]
+    stage = [torch.empty((tc_max, n), dtype=tdt, pin_memory=True) for _ in range(nbuf)] \
+        if not (i2.dtype == cdt and i2.flags.c_contiguous and torch.from_numpy(i2).is_pinned()) else None
     d_in = [torch.empty((tc_max, n), dtype=tdt, device=dev) for _ in range(nbuf)]
     d_v = [torch.empty((tc_max, n), dtype=tdt, device=dev) for _ in range(nbuf)]
     d_v64 = [torch.empty((tc_max, n), dtype=torch.float64, device=dev) for _ in range(nbuf)]
@@ -106,16 +107,22 @@ def simulate_host(params, i2: np.ndarray, v: torch.Tensor, g: torch.Tensor, forw
 
     chunks = [(t0, min(T, t0 + tc_max)) for t0 in range(0, T, tc_max)]
 
+    # a caller's array already in page-locked memory (and of the compute dtype)
+    # is DMA'd as it is: no staging copy through host memory
+    src_t = torch.from_numpy(i2) if (i2.dtype == cdt and i2.flags.c_contiguous) else None
+    direct = src_t is not None and src_t.is_pinned()
+
     def stage_and_load(k):
         t0, t1 = chunks[k]
         b = k % nbuf
-        if ev_staged[b] is not None:
-            ev_staged[b].synchronize()          # stage[b] free again
-        _par_copy(stage[b][:t1 - t0].numpy(), i2[t0:t1])
+        if not direct:
+            if ev_staged[b] is not None:
+                ev_staged[b].synchronize()      # stage[b] free again
+            _par_copy(stage[b][:t1 - t0].numpy(), i2[t0:t1])
         with torch.cuda.stream(h2d):
             if ev_computed[b] is not None:
                 h2d.wait_event(ev_computed[b])  # d_in[b] consumed by the forward
-            d_in[b][:t1 - t0].copy_(stage[b][:t1 - t0], non_blocking=True)
+            d_in[b][:t1 - t0].copy_(src_t[t0:t1] if direct else stage[b][:t1 - t0], non_blocking=True)
             ev_staged[b] = torch.cuda.Event()
             ev_staged[b].record(h2d)
             ev_loaded[b] = ev_staged[b]

@@ -488,3 +488,20 @@ def test_state0_dtype_selects_the_arithmetic(cuda):
     assert not np.array_equal(tr.v_series, ref64.v_series)
     v_o, _ = O.simulate(p64, i, v0=s32.v, g0=s32.gates, dtype=np.float32)
     assert np.max(np.abs(tr.v_series - v_o)) < 0.05
+
+
+def test_simulate_reads_pinned_host_input_directly(cuda):
+    """simulate(numpy) with the current already in page-locked memory DMAs it
+    as it is (no staging copy); the results equal those of a pageable copy of
+    the same array, for one-chunk and many-chunk calls."""
+    from paper_2601_21407_b200._pipeline import pinned_empty
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    rng = np.random.default_rng(3)
+    for T, n in ((40, 3000), (1200, 256)):
+        pageable = (2.0 * rng.poisson(2.0, size=(T, n))).astype(np.float32)
+        pinned = pinned_empty((T, n), np.float32)
+        pinned[...] = pageable
+        assert torch.from_numpy(pinned).is_pinned()
+        a = Dy.simulate(p, pageable)
+        b = Dy.simulate(p, pinned)
+        assert np.array_equal(a.v_series, b.v_series) and np.array_equal(a.spike_series, b.spike_series)
