@@ -135,3 +135,22 @@ def test_config4_oracle_problem_is_well_posed():
         assert np.array_equal(s64, s32) and s64.sum() > 0
         h64 = s64.reshape(T, B, -1).astype(np.float64)
         h32 = s32.reshape(T, B, -1).astype(np.float64)
+
+
+@pytest.mark.gpu
+def test_config4_full_shape_gradients_within_contract(cuda):
+    """The benchmarked config-4 step at its full shape against the float64
+    composition (tools/parity_c4.py, profiles/r2_parity_c4.md)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tools/parity_c4.py"], cwd=root, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["loss_rel"] < 1e-4
+    for l in (1, 2, 3):
+        for k in ("dW", "db", "d_c_m", "d_g_max"):
+            assert r[f"layer{l}"][k] < 1e-3, (l, k, r[f"layer{l}"][k])

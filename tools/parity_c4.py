@@ -1,0 +1,97 @@
+"""Config-4 gradient parity at the full shape: the benchmarked stacked step
+(784 -> 2048 -> 2048 -> 10 RS layers, B 256, T 100, bf16 tcgen05 projections,
+float32 HH kernels, hidden layers handing on spikes, CE on the time-mean output
+V, side-stream weight gradients) against the same composition in float64
+kernels (the reference's operation order, pinned to the oracle within 1e-9)
+and float64 matmuls on the same bf16-rounded operands (config 4 states bf16
+projections): per layer dW, db, d_c_m, d_g_max normwise relative errors
+(contract 1e-3), the loss, and how many neurons of each hidden
+layer spike differently.
+
+    python tools/parity_c4.py [--batch B] [--steps T]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2601_21407_b200 import adjoint as A
+from paper_2601_21407_b200 import dynamics as Dy
+from paper_2601_21407_b200.defaults import cortical_rs_params
+from paper_2601_21407_b200.layer import HHLayer
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=256)
+ap.add_argument("--steps", type=int, default=100)
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+B, T = a.batch, a.steps
+sizes = [784, 2048, 2048, 10]
+torch.manual_seed(1)
+net = [HHLayer(784, 2048, w_mean=0.05, w_std=0.1, device=dev, outputs="spikes", overlap_weight_grad=True),
+       HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, device=dev, outputs="spikes", overlap_weight_grad=True),
+       HHLayer(2048, 10, w_mean=0.02, w_std=0.05, device=dev, outputs="v", overlap_weight_grad=True)]
+g = torch.Generator(device=dev).manual_seed(1)
+x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() + 0.1 * torch.randn((T, B, 784), device=dev,
+                                                                                        generator=g)
+y = torch.randint(0, 10, (B,), device=dev, generator=g)
+h, hidden = x, []
+for lyr in net[:-1]:
+    _, h = lyr(h)
+    hidden.append(h)
+v, _ = net[-1](h)
+loss = torch.nn.functional.cross_entropy(v.mean(0), y)
+loss.backward()
+torch.cuda.synchronize()
+
+# float64 composition on the bf16-rounded operands
+p64 = cortical_rs_params(dt=0.1)
+h64 = x.to(torch.bfloat16).double()
+Ws = [lyr.weight.detach().to(torch.bfloat16).double() for lyr in net]
+bs = [lyr.bias.detach().double() for lyr in net]
+drives, ins, spk, v3 = [], [], [], None
+for l in range(3):
+    ins.append(h64)
+    d = (h64.reshape(T * B, -1) @ Ws[l].t() + bs[l]).reshape(T, B * sizes[l + 1]).contiguous()
+    tr = Dy.simulate(p64, d)
+    drives.append(d)
+    spk.append(tr.spike_series)
+    v3 = tr.v_series
+    h64 = tr.spike_series.double().reshape(T, B, -1)
+logits = v3.reshape(T, B, 10).mean(0)
+loss64 = torch.nn.functional.cross_entropy(logits, y)
+dl = torch.softmax(logits, dim=1)
+dl[torch.arange(B, device=dev), y] -= 1.0
+dl = dl / B
+seed_v = (dl / T).expand(T, B, 10).reshape(T, -1).contiguous()
+seed_s = None
+ref = [None] * 3
+for l in (2, 1, 0):
+    n = B * sizes[l + 1]
+    sv = seed_v if seed_v is not None else torch.zeros((T, n), dtype=torch.float64, device=dev)
+    res = A.backward_through_time(p64, Dy.init_state(p64, (n,), device=dev), drives[l], sv, seed_s)
+    dd = res.d_i.reshape(T * B, sizes[l + 1])
+    xin = ins[l].reshape(T * B, sizes[l])
+    ref[l] = {"dW": dd.t() @ xin, "db": dd.sum(0), "d_c_m": res.d_c_m, "d_g_max": np.asarray(res.d_g_max)}
+    seed_s = (dd @ Ws[l]).reshape(T, -1).contiguous()
+    seed_v = None
+
+
+def nrel(a_, b_):
+    return float((a_.double() - b_).norm() / b_.norm())
+
+
+out = {"batch": B, "steps": T, "loss_rel": abs(loss.item() - loss64.item()) / abs(loss64.item()),
+       "spike_mismatch_neurons": [int((hidden[l].reshape(T, -1).bool() != spk[l]).any(0).sum().item())
+                                  for l in range(2)]}
+for l, lyr in enumerate(net):
+    pg = lyr.param_grads.cpu().numpy()
+    out[f"layer{l + 1}"] = {"dW": nrel(lyr.weight.grad, ref[l]["dW"]), "db": nrel(lyr.bias.grad, ref[l]["db"]),
+                            "d_c_m": abs(pg[0] - ref[l]["d_c_m"]) / abs(ref[l]["d_c_m"]),
+                            "d_g_max": float(np.linalg.norm(pg[1:] - ref[l]["d_g_max"]) /
+                                             np.linalg.norm(ref[l]["d_g_max"]))}
+print(json.dumps(out))
