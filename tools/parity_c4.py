@@ -33,8 +33,8 @@ B, T = a.batch, a.steps
 sizes = [784, 2048, 2048, 10]
 torch.manual_seed(1)
 net = [HHLayer(784, 2048, w_mean=0.05, w_std=0.1, device=dev, outputs="spikes", overlap_weight_grad=True),
-       HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, device=dev, outputs="spikes", overlap_weight_grad=True),
-       HHLayer(2048, 10, w_mean=0.02, w_std=0.05, device=dev, outputs="v", overlap_weight_grad=True)]
+       HHLayer(2048, 2048, w_mean=0.3, w_std=0.1, device=dev, outputs="spikes", overlap_weight_grad=True),
+       HHLayer(2048, 10, w_mean=0.3, w_std=0.1, device=dev, outputs="v", overlap_weight_grad=True)]
 g = torch.Generator(device=dev).manual_seed(1)
 x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() + 0.1 * torch.randn((T, B, 784), device=dev,
                                                                                         generator=g)

@@ -16,8 +16,8 @@ torch.manual_seed(1)
 ov = os.environ.get("OVERLAP", "1") == "1"
 net = torch.nn.ModuleList([
     HHLayer(784, 2048, w_mean=0.05, w_std=0.1, check_finite=False, device=dev, outputs="spikes", overlap_weight_grad=ov),
-    HHLayer(2048, 2048, w_mean=0.02, w_std=0.05, check_finite=False, device=dev, outputs="spikes", overlap_weight_grad=ov),
-    HHLayer(2048, 10, w_mean=0.02, w_std=0.05, check_finite=False, device=dev, outputs="v", overlap_weight_grad=ov)])
+    HHLayer(2048, 2048, w_mean=0.3, w_std=0.1, check_finite=False, device=dev, outputs="spikes", overlap_weight_grad=ov),
+    HHLayer(2048, 10, w_mean=0.3, w_std=0.1, check_finite=False, device=dev, outputs="v", overlap_weight_grad=ov)])
 g = torch.Generator(device=dev).manual_seed(1)
 x = (torch.rand((T, B, 784), device=dev, generator=g) < 0.2).float() + 0.1 * torch.randn((T, B, 784), device=dev, generator=g)
 y = torch.randint(0, 10, (B,), device=dev, generator=g)
