@@ -1098,7 +1098,7 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   // is shorter than an HBM load) and one step ahead with four (throughput-
   // bound, registers are the limit); the drawn stimulus is made at the top of
   // its own step (no registers held across it)
-  constexpr int PF = (VEC == 1 && !POIS) ? FWD_PF : 1;
+  constexpr int PF = POIS ? 1 : (VEC == 1 ? FWD_PF : FWD_PF4);
   float cur[VEC];
   float pre[PF][VEC];
   auto load_in = [&](float (&c)[VEC]) {
@@ -1125,7 +1125,16 @@ __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& 
   // the load and undoes the prefetch
   const float* ib1 = (n0 < a.n) ? a.i_ext + n0 * a.i_sn : a.i_ext;
   auto load_row = [&](i64 r, float (&c)[VEC]) {
-    c[0] = __ldg(ib1 + (r < a.steps ? r : a.steps - 1) * a.i_st);
+    const float* q = ib1 + (r < a.steps ? r : a.steps - 1) * a.i_st;
+    if (VEC == 1) {
+      c[0] = __ldg(q);
+    } else if (vec_in) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(q));     // live lanes only (vec_in: n % 4 == 0 or full)
+      c[0] = w.x; c[VEC > 1 ? 1 : 0] = w.y; c[VEC > 2 ? 2 : 0] = w.z; c[VEC > 3 ? 3 : 0] = w.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) c[j] = __ldg(q + (((valid >> j) & 1u) ? j : 0) * a.i_sn);
+    }
   };
   if (!POIS && a.steps > 0) {
 #pragma unroll
@@ -1903,6 +1912,8 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   src += fmt("#define FWD_MINB %d\n", mb ? atoi(mb) : 2);
   const char* pf = getenv("HHB_JIT_FWD_PF");
   src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 8);
+  const char* pf4 = getenv("HHB_JIT_FWD_PF4");
+  src += fmt("#define FWD_PF4 %d\n", pf4 && atoi(pf4) > 0 ? atoi(pf4) : 1);
   // 2-neuron BPTT: 8 resident 64-thread blocks (128 registers, no spills; the
   // operand ring holds only the launch's streams, 21.8 KB): 212 us vs 220 us
   // at 6 blocks for the config-3 step (profiles/r2_bptt.md)
@@ -2118,6 +2129,8 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += bmb2 ? std::string("c") + bmb2 : "";
   const char* pf = getenv("HHB_JIT_FWD_PF");
   k += pf ? std::string("p") + pf : "";
+  const char* pf4 = getenv("HHB_JIT_FWD_PF4");
+  k += pf4 ? std::string("q") + pf4 : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
   for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK"}) {
