@@ -1913,7 +1913,9 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   const char* pf = getenv("HHB_JIT_FWD_PF");
   src += fmt("#define FWD_PF %d\n", pf && atoi(pf) > 0 ? atoi(pf) : 8);
   const char* pf4 = getenv("HHB_JIT_FWD_PF4");
-  src += fmt("#define FWD_PF4 %d\n", pf4 && atoi(pf4) > 0 ? atoi(pf4) : 1);
+  // 4-neuron threads reading a current: 2 rows in flight (config-3 training
+  // forward 128 -> 122 us, config 4 270 -> 261 us per hidden layer; 3-4: same)
+  src += fmt("#define FWD_PF4 %d\n", pf4 && atoi(pf4) > 0 ? atoi(pf4) : 2);
   // 2-neuron BPTT: 8 resident 64-thread blocks (128 registers, no spills; the
   // operand ring holds only the launch's streams, 21.8 KB): 212 us vs 220 us
   // at 6 blocks for the config-3 step (profiles/r2_bptt.md)
