@@ -306,7 +306,8 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
                         int64_t ldd, void* stream);
 /* row-wise three-slot bf16 split (the fp32-class "bf16x3" projection):
  * slots of `slot` (>= cols) elements per row; order 0: [hi | lo | hi],
- * order 1: [hi | hi | lo].  A bf16 GEMM over K = 3 slot of an order-0 A and
+ * order 1: [hi | hi | lo]; order 2: three row blocks [hi; hi; lo] of `slot`
+ * (>= rows) rows of pitch ldd (the input gradient's stacked B operand).  A bf16 GEMM over K = 3 slot of an order-0 A and
  * an order-1 B is x_h.W_h + x_l.W_h + x_h.W_l (~16 mantissa bits of both
  * operands; replaces the float64 x @ W.T of DenseLayer, learn.py:210-211). */
 int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst,

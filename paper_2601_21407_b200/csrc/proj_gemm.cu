@@ -871,10 +871,12 @@ __global__ void k_split3_rows(int64_t rows, int64_t cols, const float* src, int6
     const float x = __ldg(src + r * lds + c);
     const __nv_bfloat16 hi = __float2bfloat16_rn(x);
     const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    // orders 0 / 1: three column slots of one row; 2: three row blocks of `slot` rows
+    const int64_t step = order == 2 ? slot * ldd : slot;
     __nv_bfloat16* d = dst + r * ldd + c;
     d[0] = hi;
-    d[slot] = order == 0 ? lo : hi;
-    d[2 * slot] = order == 0 ? hi : lo;
+    d[step] = order == 0 ? lo : hi;
+    d[2 * step] = order == 0 ? hi : lo;
   }
 }
 
@@ -895,10 +897,11 @@ __global__ void k_split3_rows_v8(int64_t rows, int64_t cols8, const float* src, 
       lo[j] = __float2bfloat16_rn(x[j] - __bfloat162float(hi[j]));
     }
     const uint4 h = *reinterpret_cast<const uint4*>(hi), l = *reinterpret_cast<const uint4*>(lo);
-    uint4* d = reinterpret_cast<uint4*>(dst + r * ldd + c);
-    d[0] = h;
-    *reinterpret_cast<uint4*>(dst + r * ldd + slot + c) = order == 0 ? l : h;
-    *reinterpret_cast<uint4*>(dst + r * ldd + 2 * slot + c) = order == 0 ? h : l;
+    const int64_t step = order == 2 ? slot * ldd : slot;
+    __nv_bfloat16* d = dst + r * ldd + c;
+    *reinterpret_cast<uint4*>(d) = h;
+    *reinterpret_cast<uint4*>(d + step) = order == 0 ? l : h;
+    *reinterpret_cast<uint4*>(d + 2 * step) = order == 0 ? h : l;
   }
 }
 
@@ -1396,7 +1399,8 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
 int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, void* dst, int64_t ldd,
                     int64_t slot, int32_t order, void* stream) {
   if (rows <= 0 || cols <= 0) return HHB_OK;
-  if (slot < cols || ldd < 3 * slot || (order != 0 && order != 1)) return fail(HHB_EINVAL, "split3 shape/order");
+  if (order == 2 ? (slot < rows || ldd < cols) : (order != 0 && order != 1) || slot < cols || ldd < 3 * slot)
+    return fail(HHB_EINVAL, "split3 shape/order");
   const bool vec = cols % 8 == 0 && lds % 4 == 0 && ldd % 8 == 0 && slot % 8 == 0 &&
                    reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0;
   if (vec) {

@@ -310,10 +310,11 @@ def _project(x, weight, bias, layer):
             # the input gradient's B operand: rows [W_hi; W_hi; W_lo], each block
             # n_out rows padded to P (MN-major over the reduction index j)
             P = _pad8(n_out)
-            w3 = torch.zeros((3 * P, kp), dtype=torch.bfloat16, device=x.device)
-            w3[:n_out] = wb[:, :kp]
-            w3[P:P + n_out] = wb[:, :kp]
-            w3[2 * P:2 * P + n_out] = wb[:, 2 * kp:]
+            w3 = (torch.empty if (P == n_out and kp == k_in) else torch.zeros)(
+                (3 * P, kp), dtype=torch.bfloat16, device=x.device)
+            wf = weight.float().contiguous()
+            nat.check(nat.load().hhb_split3_bf16(n_out, k_in, wf.data_ptr(), k_in, w3.data_ptr(), kp, P, 2,
+                                                 _stream()), "split3 stacked")
         with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
             cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
         return xb, w3, cur

@@ -186,3 +186,19 @@ def test_gemm_k_switch_concatenates_a(cuda, M, N, P):
     # the explicit concatenation through the plain GEMM agrees bit for bit
     explicit = gemm_ex(B_MN, M, N, 3 * P, torch.cat([H, H[:, :P]], dim=1).contiguous(), None, 3 * P, Bm, N)
     assert torch.equal(got, explicit)
+
+
+
+def test_split3_stacked_rows(cuda):
+    """order 2: three row blocks [hi; hi; lo] of `slot` rows (the dX B operand)."""
+    from paper_2601_21407_b200 import _native as nat
+    for rows, cols, P, ld in ((10, 20, 16, 24), (64, 784, 64, 784)):
+        x = torch.randn((rows, cols), device=cuda)
+        out = torch.zeros((3 * P, ld), dtype=torch.bfloat16, device=cuda)
+        nat.check(nat.load().hhb_split3_bf16(rows, cols, x.data_ptr(), cols, out.data_ptr(), ld, P, 2,
+                                             torch.cuda.current_stream().cuda_stream), "split3")
+        hi = x.to(torch.bfloat16)
+        lo = (x - hi.float()).to(torch.bfloat16)
+        assert torch.equal(out[:rows, :cols], hi) and torch.equal(out[P:P + rows, :cols], hi)
+        assert torch.equal(out[2 * P:2 * P + rows, :cols], lo)
+        assert not out[rows:P].float().any() and not out[:, cols:].float().any()
