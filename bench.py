@@ -52,10 +52,14 @@ def mufu_per_step(nat, params, which="fwd"):
     (forward or backward), counted in the generated source; the ncu-measured
     XU instruction count of the same kernel is reported beside it."""
     src = nat.jit_source(params)
-    fn = f"step_{which}_m(" if f"step_{which}_m(" in src else f"step_{which}_s("
-    body = src[src.index("__device__ __forceinline__ float " + fn):]
+    # the paired (f32x2) merged step when generated: one ex2v / rcpv per neuron
+    for head in (f"F2 step_{which}_m2(", f"float step_{which}_m(", f"float step_{which}_s("):
+        if head in src:
+            break
+    body = src[src.index(head):]
     body = body[:body.index("\n}\n")]
-    return body.count("ex2f_(") + body.count("rcpf_("), fn[:-1]
+    n = sum(body.count(k) for k in ("ex2f_(", "rcpf_(", "ex2v<H>(", "rcpv<H>("))
+    return n, head.split()[1][:-1]
 
 
 def load_json(*parts):

@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <cctype>
 #include <cmath>
 #include <cstdarg>
 #include <cstdlib>
@@ -790,6 +791,106 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
   return o;
 }
 
+
+// Paired (f32x2) form of a merged step.  sm_100a issues FFMA2 / FMUL2 / FADD2:
+// one warp instruction does the float op of two neurons (the FMA pipe's fp32
+// rate is unchanged, the issue slots halve -- the merged steps are issue-bound,
+// profiles/r2_fwdp.md, r2_bptt.md).  pair() rewrites the emitted scalar
+// function into template <bool H> ...2(F2 ...): every float becomes an F2 (x =
+// neuron j, y = neuron j + 1), selects become per-half sel2, MUFU ops stay one
+// per half (H: the y half is a copy of x and its MUFU ops are skipped -- the
+// one-neuron callers).  All callers, paired or not, run this one function, so
+// every kernel reproduces the same states bit for bit (ptxas contracts
+// FMUL2 + FADD2 into FFMA2 regardless of .rn; the scalar form would round
+// differently).
+static const char* kPairPrelude = R"(
+struct __align__(8) F2 {
+  float x, y;
+  __device__ __forceinline__ F2() {}
+  __device__ __forceinline__ F2(float a) : x(a), y(a) {}
+  __device__ __forceinline__ F2(float a, float b) : x(a), y(b) {}
+};
+struct B2 { bool x, y; };
+__device__ __forceinline__ float2 f2_(const F2 a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ F2 F2_(const float2 a) { return F2(a.x, a.y); }
+__device__ __forceinline__ F2 mul2(const F2 a, const F2 b) { return F2_(__fmul2_rn(f2_(a), f2_(b))); }
+__device__ __forceinline__ F2 add2(const F2 a, const F2 b) { return F2_(__fadd2_rn(f2_(a), f2_(b))); }
+__device__ __forceinline__ F2 sub2(const F2 a, const F2 b) { return F2_(__fadd2_rn(f2_(a), make_float2(-b.x, -b.y))); }
+__device__ __forceinline__ F2 fma2(const F2 a, const F2 b, const F2 c) { return F2_(__ffma2_rn(f2_(a), f2_(b), f2_(c))); }
+__device__ __forceinline__ F2 operator-(const F2 a) { return F2(-a.x, -a.y); }   // folds into operand modifiers
+__device__ __forceinline__ F2 abs2(const F2 a) { return F2(fabsf(a.x), fabsf(a.y)); }
+__device__ __forceinline__ B2 operator<(const F2 a, const float c) { return B2{a.x < c, a.y < c}; }
+__device__ __forceinline__ F2 sel2(const B2 c, const F2 a, const F2 b) { return F2(c.x ? a.x : b.x, c.y ? a.y : b.y); }
+// the y half's MUFU op is volatile: with duplicated halves (one-neuron callers)
+// the compiler would merge the two and then copy x into y with a MOV on the chain
+__device__ __forceinline__ float ex2y_(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rcpy_(float x) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+template <bool H> __device__ __forceinline__ F2 ex2v(const F2 a) { const float x = ex2f_(a.x); return F2(x, H ? x : ex2y_(a.y)); }
+template <bool H> __device__ __forceinline__ F2 rcpv(const F2 a) { const float x = rcpf_(a.x); return F2(x, H ? x : rcpy_(a.y)); }
+template <bool H> __device__ __forceinline__ F2 surrogate2(const Sur& s, const F2 u) {
+  const float x = surrogate(s, u.x);
+  return F2(x, H ? x : surrogate(s, u.y));
+}
+)";
+
+static void replace_all(std::string& s, const std::string& a, const std::string& b) {
+  for (size_t i = s.find(a); i != std::string::npos; i = s.find(a, i + b.size())) s.replace(i, a.size(), b);
+}
+static bool ident(char c) { return std::isalnum(static_cast<unsigned char>(c)) || c == '_'; }
+// whole-word replacement (a is an identifier)
+static void replace_word(std::string& s, const std::string& a, const std::string& b) {
+  for (size_t i = s.find(a); i != std::string::npos;) {
+    const bool l = i == 0 || !ident(s[i - 1]);
+    const bool r = i + a.size() >= s.size() || !ident(s[i + a.size()]);
+    if (l && r) {
+      s.replace(i, a.size(), b);
+      i = s.find(a, i + b.size());
+    } else {
+      i = s.find(a, i + a.size());
+    }
+  }
+}
+// "  const float x = c ? a : b;" -> "  const F2 x = sel2(c, a, b);" (the merged
+// steps' only selects: one condition name, no nested ternaries)
+static std::string pair_line(std::string ln) {
+  const size_t q = ln.find(" ? ");
+  if (q != std::string::npos) {
+    const size_t eq = ln.rfind(" = ", q);
+    const size_t c = ln.find(" : ", q);
+    const size_t end = ln.rfind(';');
+    if (eq == std::string::npos || c == std::string::npos || end == std::string::npos || end < c) return "#error pair";
+    ln = ln.substr(0, eq + 3) + "sel2(" + ln.substr(eq + 3, q - eq - 3) + ", " + ln.substr(q + 3, c - q - 3) + ", " +
+         ln.substr(c + 3, end - c - 3) + ")" + ln.substr(end);
+  }
+  return ln;
+}
+// scalar merged function (signature line + body) -> its paired template
+static std::string pair(const std::string& fn, const std::string& name) {
+  const size_t nl = fn.find('\n');
+  std::string sig = fn.substr(0, nl), body = fn.substr(nl + 1);
+  replace_word(sig, "float", "F2");
+  replace_word(sig, name, name + "2");
+  replace_all(sig, "__device__ __forceinline__", "template <bool H> __device__ __forceinline__");
+  replace_word(body, "float", "F2");
+  replace_word(body, "bool", "B2");
+  replace_all(body, "__fmul_rn(", "mul2(");
+  replace_all(body, "__fadd_rn(", "add2(");
+  replace_all(body, "__fsub_rn(", "sub2(");
+  replace_all(body, "__fmaf_rn(", "fma2(");
+  replace_all(body, "ex2f_(", "ex2v<H>(");
+  replace_all(body, "rcpf_(", "rcpv<H>(");
+  replace_all(body, "fabsf(", "abs2(");
+  replace_all(body, "surrogate(", "surrogate2<H>(");
+  std::string out = sig + "\n";
+  size_t i = 0;
+  while (i < body.size()) {
+    size_t j = body.find('\n', i);
+    if (j == std::string::npos) j = body.size();
+    out += pair_line(body.substr(i, j - i)) + "\n";
+    i = j + 1;
+  }
+  return out;
+}
 }  // namespace mg
 
 // adjoint of step_fwd (hh_step_backward, adjoint.py:116-188).  The parameter-
@@ -1793,11 +1894,42 @@ __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
 #if HAS_MERGED
       // one warp vote per step for all VEC neurons of every lane
       if (__all_sync(0xffffffffu, reg)) {
+#if BWD_PAIR
+        if (VEC == 2) {   // both neurons per f32x2 op
+          constexpr int k = VEC - 1;
+          F2 q[NGX], dq[NGX], ac[SLOTS];
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) di[j] = step_bwd_m(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+          for (int g = 0; g < NGX; ++g) {
+            q[g] = F2(p[0][g], p[k][g]);
+            dq[g] = F2(d_p[0][g], d_p[k][g]);
+          }
+#pragma unroll
+          for (int s = 0; s < SLOTS; ++s) ac[s] = F2(accf[s], 0.0f);   // y: this step's second neuron
+          F2 dv(d_v[0], d_v[k]);
+          const F2 r = step_bwd_m2<false>(sur, F2(v[0], v[k]), q, F2(cur[0], cur[k]), dv, dq, F2(ds[0], ds[k]),
+                                          BF_SS, ac);
+          di[0] = r.x;
+          di[k] = r.y;
+          d_v[0] = dv.x;
+          d_v[k] = dv.y;
+#pragma unroll
+          for (int g = 0; g < NGX; ++g) {
+            d_p[0][g] = dq[g].x;
+            d_p[k][g] = dq[g].y;
+          }
+#pragma unroll
+          for (int s = 0; s < SLOTS; ++s) accf[s] = __fadd_rn(ac[s].x, ac[s].y);
+        } else
+#endif
+        {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j)
+            di[j] = step_bwd_m(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+        }
       } else {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) di[j] = step_bwd_irr(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
+        for (int j = 0; j < VEC; ++j)
+          di[j] = step_bwd_irr(sur, v[j], p[j], cur[j], d_v[j], d_p[j], ds[j], BF_SS, accf);
       }
 #else
 #pragma unroll
@@ -1916,6 +2048,10 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   // 4-neuron threads reading a current: 2 rows in flight (config-3 training
   // forward 128 -> 122 us, config 4 270 -> 261 us per hidden layer; 3-4: same)
   src += fmt("#define FWD_PF4 %d\n", pf4 && atoi(pf4) > 0 ? atoi(pf4) : 2);
+  // one-neuron callers of the paired step: both halves' MUFU ops (0) or the x
+  // half's only, the y half copied (1: a MOV after every MUFU op on the chain)
+  const char* fh = getenv("HHB_JIT_FWD_HALF");
+  src += fmt("#define FWD_HALF %d\n", fh && atoi(fh) > 0 ? 1 : 0);
   // 2-neuron BPTT: 8 resident 64-thread blocks (128 registers, no spills; the
   // operand ring holds only the launch's streams, 21.8 KB): 212 us vs 220 us
   // at 6 blocks for the config-3 step (profiles/r2_bptt.md)
@@ -1934,7 +2070,26 @@ static std::string generate(const hhb_params_t* P, int bwd_flags = kInspect) {
   if (M.ok) {
     // merged form on every regular lane; one warp vote per step sends the
     // warp through the per-lane select only when some lane left the window
-    src += mg::emit_step(P, L, M);
+    {
+      // regular(), then the paired merged step and its one-neuron wrapper
+      const std::string st = mg::emit_step(P, L, M);
+      const size_t k = st.find("__device__ __forceinline__ float step_fwd_m(");
+      src += st.substr(0, k);
+      src += mg::kPairPrelude;
+      src += mg::pair(st.substr(k), "step_fwd_m");
+      // the network kernel (one neuron per thread, its own module: nothing
+      // else reproduces its states) keeps the scalar merged step
+      src += fmt("#define FWD_PAIR %d\n", bwd_flags <= kNet ? 0 : 1);
+      if (bwd_flags <= kNet) src += st.substr(k);
+      else src += fmt(
+          "__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n"
+          "  F2 q[NGX];\n"
+          "#pragma unroll\n  for (int g = 0; g < NGX; ++g) q[g] = F2(p[g]);\n"
+          "  const F2 r = step_fwd_m2<FWD_HALF>(F2(v), q, F2(cur));\n"
+          "#pragma unroll\n  for (int g = 0; g < NGX; ++g) p[g] = q[g].x;\n"
+          "  return r.x;\n}\n",
+          L.ng > 0 ? L.ng : 1);
+    }
     src += R"(template <int VEC>
 __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][NGX], const float (&cur)[VEC],
                                          float (&vn)[VEC]) {
@@ -1942,17 +2097,56 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
 #pragma unroll
   for (int j = 0; j < VEC; ++j) irr = irr || !regular(v[j]);
   if (__any_sync(0xffffffffu, irr)) {
+    if (FWD_PAIR && VEC % 2 == 0) {
+      // merged form for both neurons of a pair, the series form per neuron
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) {
-      float pm[NGX];
+      for (int j = 0; j < VEC; j += 2) {
+        const int k = VEC > 1 ? j + 1 : 0;
+        F2 q[NGX];
 #pragma unroll
-      for (int g = 0; g < NGX; ++g) pm[g] = p[j][g];
-      const float vm = step_fwd_m(v[j], pm, cur[j]);
-      const bool reg = regular(v[j]);
-      const float vs = step_fwd_s(v[j], p[j], cur[j]);
-      vn[j] = reg ? vm : vs;
+        for (int g = 0; g < NGX; ++g) q[g] = F2(p[j][g], p[k][g]);
+        const F2 r = step_fwd_m2<false>(F2(v[j], v[k]), q, F2(cur[j], cur[k]));
+        const bool rj = regular(v[j]), rk = regular(v[k]);
+        const float sj = step_fwd_s(v[j], p[j], cur[j]);
+        const float sk = step_fwd_s(v[k], p[k], cur[k]);
+        vn[j] = rj ? r.x : sj;
+        vn[k] = rk ? r.y : sk;
 #pragma unroll
-      for (int g = 0; g < NGX; ++g) p[j][g] = reg ? pm[g] : p[j][g];
+        for (int g = 0; g < NGX; ++g) {
+          p[j][g] = rj ? q[g].x : p[j][g];
+          p[k][g] = rk ? q[g].y : p[k][g];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        float pm[NGX];
+#pragma unroll
+        for (int g = 0; g < NGX; ++g) pm[g] = p[j][g];
+        const float vm = step_fwd_m(v[j], pm, cur[j]);
+        const bool reg = regular(v[j]);
+        const float vs = step_fwd_s(v[j], p[j], cur[j]);
+        vn[j] = reg ? vm : vs;
+#pragma unroll
+        for (int g = 0; g < NGX; ++g) p[j][g] = reg ? pm[g] : p[j][g];
+      }
+    }
+  } else if (FWD_PAIR && VEC % 2 == 0) {
+    // two neurons per f32x2 op
+#pragma unroll
+    for (int j = 0; j < VEC; j += 2) {
+      const int k = VEC > 1 ? j + 1 : 0;
+      F2 q[NGX];
+#pragma unroll
+      for (int g = 0; g < NGX; ++g) q[g] = F2(p[j][g], p[k][g]);
+      const F2 r = step_fwd_m2<false>(F2(v[j], v[k]), q, F2(cur[j], cur[k]));
+      vn[j] = r.x;
+      vn[k] = r.y;
+#pragma unroll
+      for (int g = 0; g < NGX; ++g) {
+        p[j][g] = q[g].x;
+        p[k][g] = q[g].y;
+      }
     }
   } else {
 #pragma unroll
@@ -2017,7 +2211,32 @@ __device__ __forceinline__ void step_all(const float (&v)[VEC], float (&p)[VEC][
       "__device__ __forceinline__ float step_bwd(const Sur& sur, const float v, const float (&p)[NGX], "
       "const float cur, float& d_v, float (&d_p)[NGX], const float d_spike, const bool has_s, float (&cb)[SLOTS])";
   if (M.ok) {
-    src += emit_backward_step(P, L, kSeries, &M);
+    // the adjoint step stays scalar by default: paired, the BPTT kernel lost
+    // ILP at its register budget (config 3: 203 -> 219 us, spills; DESIGN.md
+    // section 8); HHB_JIT_BWD_PAIR=1 selects the paired form.  Either way the
+    // segment recompute runs the forward's own (paired) step.
+    const char* bp = getenv("HHB_JIT_BWD_PAIR");
+    const bool bwd_pair = bp && atoi(bp) > 0;
+    src += fmt("#define BWD_PAIR %d\n", bwd_pair ? 1 : 0);
+    if (!bwd_pair) {
+      src += emit_backward_step(P, L, kSeries, &M);
+    } else {
+      const std::string bm = emit_backward_step(P, L, kSeries, &M);
+      src += mg::pair(bm, "step_bwd_m");
+      src += fmt(
+          "__device__ __forceinline__ float step_bwd_m(const Sur& sur, const float v, const float (&p)[%d], "
+          "const float cur, float& d_v, float (&d_p)[%d], const float d_spike, const bool has_s, float (&acc)[SLOTS]) {\n"
+          "  F2 q[NGX], dq[NGX], ac[SLOTS];\n"
+          "#pragma unroll\n  for (int g = 0; g < NGX; ++g) { q[g] = F2(p[g]); dq[g] = F2(d_p[g]); }\n"
+          "#pragma unroll\n  for (int s = 0; s < SLOTS; ++s) ac[s] = F2(acc[s]);\n"
+          "  F2 dv(d_v);\n"
+          "  const F2 r = step_bwd_m2<true>(sur, F2(v), q, F2(cur), dv, dq, F2(d_spike), has_s, ac);\n"
+          "  d_v = dv.x;\n"
+          "#pragma unroll\n  for (int g = 0; g < NGX; ++g) d_p[g] = dq[g].x;\n"
+          "#pragma unroll\n  for (int s = 0; s < SLOTS; ++s) acc[s] = ac[s].x;\n"
+          "  return r.x;\n}\n",
+          L.ng > 0 ? L.ng : 1, L.ng > 0 ? L.ng : 1);
+    }
     src += "#define HAS_MERGED 1\n";
     src += R"(// some lane of the warp left the merged form's window: both forms, per lane
 __device__ __forceinline__ float step_bwd_irr(const Sur& sur, const float v, const float (&p)[NGX], const float cur,
@@ -2135,7 +2354,7 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += pf4 ? std::string("q") + pf4 : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
-  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK"}) {
+  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK", "HHB_JIT_BWD_PAIR", "HHB_JIT_FWD_HALF"}) {
     const char* x = getenv(e);
     k += x ? std::string("|") + e + x : "";
   }

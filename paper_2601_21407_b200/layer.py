@@ -299,7 +299,10 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[key]
 
 
-def _project(x, weight, bias, layer):
+def _operands(x, weight, layer):
+    """bf16 GEMM operands of the projection: (xb, wb_proj, wb_grad, K) --
+    wb_grad is the input gradient's B operand (the stacked [W_hi; W_hi; W_lo]
+    for bf16x3, W itself for bf16)."""
     T, B, k_in = x.shape
     if layer.proj == "bf16x3":
         # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
@@ -315,9 +318,7 @@ def _project(x, weight, bias, layer):
             wf = weight.float().contiguous()
             nat.check(nat.load().hhb_split3_bf16(n_out, k_in, wf.data_ptr(), k_in, w3.data_ptr(), kp, P, 2,
                                                  _stream()), "split3 stacked")
-        with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
-            cur = gemm(xb, wb, 3 * kp, bias=bias.float().contiguous())
-        return xb, w3, cur
+        return xb, wb, w3, 3 * kp
     twin = getattr(x, "_hhb_bf16", None)
     if (twin is not None and twin[1] == x._version and tuple(twin[0].shape) == tuple(x.shape)
             and k_in % 8 == 0):
@@ -329,9 +330,69 @@ def _project(x, weight, bias, layer):
             xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
     with _timed("operand_prep", weight.numel()):
         wb = to_bf16_padded(weight.float().contiguous())
-    with _timed("proj_gemm", 2.0 * T * B * k_in * weight.shape[0]):
-        cur = gemm(xb, wb, k_in, bias=bias.float().contiguous())    # (T*B, n_out) == (T, B*n_out)
-    return xb, wb, cur
+    return xb, wb, wb, k_in
+
+
+def _time_chunks(T: int, K: int, work: int):
+    """Time chunks of the pipelined projection + forward: HHB_LAYER_CHUNKS
+    (default 1: measured slower) pieces, each a multiple of the checkpoint segment K; one chunk
+    for small problems (the GEMM tiles would not fill the GPU)."""
+    import os
+    C = int(os.environ.get("HHB_LAYER_CHUNKS", "1"))
+    if C <= 1 or T < 2 * C or work < (1 << 24):
+        return [(0, T)]
+    tc = -(-T // C)
+    tc = -(-tc // K) * K
+    return [(t0, min(T, t0 + tc)) for t0 in range(0, T, tc)]
+
+
+_PROJ: dict = {}
+
+
+def _proj_stream(dev) -> torch.cuda.Stream:
+    key = str(dev)
+    if key not in _PROJ:
+        _PROJ[key] = torch.cuda.Stream(dev)
+    return _PROJ[key]
+
+
+def _project_forward(x, weight, bias, layer, K, run_forward):
+    """Projection GEMM I = x W^T + b followed by the HH forward, pipelined over
+    time chunks: the GEMM of chunk c + 1 (a side stream) runs while the
+    forward of chunk c (the current stream) consumes the rows of chunk c --
+    the forward is sequential in time, so it can start as soon as its first
+    steps' currents exist.  run_forward(cur, t0, t1) launches the forward of
+    steps [t0, t1).  Returns (xb, wb_grad, cur)."""
+    T, B, k_in = x.shape
+    n_out = weight.shape[0]
+    xb, wb, wg, kk = _operands(x, weight, layer)
+    b32 = bias.float().contiguous()
+    cur = torch.empty((T * B, n_out), dtype=torch.float32, device=x.device)
+    chunks = _time_chunks(T, K, T * B * n_out)
+    if len(chunks) == 1:
+        with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
+            gemm(xb, wb, kk, bias=b32, out=cur)
+        run_forward(cur, 0, T)
+        return xb, wg, cur
+    main = torch.cuda.current_stream(x.device)
+    side = _proj_stream(x.device)
+    fork = torch.cuda.Event()
+    fork.record(main)
+    side.wait_event(fork)
+    evs = []
+    with torch.cuda.stream(side):
+        for t0, t1 in chunks:
+            with _timed("proj_gemm", 2.0 * (t1 - t0) * B * k_in * n_out):
+                gemm(xb[t0 * B:t1 * B], wb, kk, bias=b32, out=cur[t0 * B:t1 * B])
+            ev = torch.cuda.Event()
+            ev.record(side)
+            evs.append(ev)
+    for t in (xb, wb, b32, cur):
+        t.record_stream(side)
+    for (t0, t1), ev in zip(chunks, evs):
+        main.wait_event(ev)
+        run_forward(cur, t0, t1)
+    return xb, wg, cur
 
 
 class _HHLayerFn(torch.autograd.Function):
@@ -341,7 +402,6 @@ class _HHLayerFn(torch.autograd.Function):
         n_out = weight.shape[0]
         n = B * n_out
         p = layer.params
-        xb, wb, cur = _project(x, weight, bias, layer)
         v0, g0 = layer.rest_state(n, x.device)
         K = layer.segment(T)
         nck = (T + K - 1) // K
@@ -353,9 +413,27 @@ class _HHLayerFn(torch.autograd.Function):
         # straight out of the forward kernel (attached to the spike tensor)
         sb = (torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
               if layer.outputs == "spikes" and n_out % 8 == 0 else None)
-        with _timed("hh_forward", T * n):
-            _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, spk_val=spikes, ckpt=ckpt, ckpt_every=K,
-                                 spk_bf16=sb)
+        bad = torch.empty(1, dtype=torch.int64, device=x.device)
+        state = {}
+
+        def run_forward(cur, t0, t1):
+            full = t0 == 0 and t1 == T
+            if full:
+                vi, gi, vf, gf = v0, g0, None, None
+            else:
+                if t0 == 0:
+                    state["v"], state["g"] = v0.clone(), g0.clone()
+                vi = vf = state["v"]
+                gi = gf = state["g"]
+            with _timed("hh_forward", (t1 - t0) * n):
+                _forward(p, vi, gi, cur[t0 * B:t1 * B].view(t1 - t0, n), n, 1, t1 - t0, v_fin=vf, g_fin=gf,
+                         v_out=None if v_out is None else v_out[t0:t1],
+                         spk_val=None if spikes is None else spikes[t0:t1],
+                         ckpt=ckpt[t0 // K:(t1 + K - 1) // K], ckpt_every=K,
+                         spk_bf16=None if sb is None else sb[t0:t1], step_base=t0, first_bad=bad,
+                         reset_bad=t0 == 0)
+
+        xb, wb, cur = _project_forward(x, weight, bias, layer, K, run_forward)
         layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)
@@ -395,21 +473,37 @@ class _HHLayerMSEFn(torch.autograd.Function):
         n = B * n_out
         p = layer.params
         ng = p.n_gates
-        xb, wb, cur = _project(x, weight, bias, layer)
         v0, g0 = layer.rest_state(n, x.device)
         K = layer.segment(T)
-        sq = torch.zeros(int(nat.load().hhb_forward_partials(n)), dtype=torch.float64, device=x.device)
+        chunks = _time_chunks(T, K, T * B * n_out)
+        npart = int(nat.load().hhb_forward_partials(n))
+        # one row of fp64 partials per time chunk (each launch writes its own)
+        sq = torch.zeros((len(chunks), npart), dtype=torch.float64, device=x.device)
         if K == 1:
             ckpt = torch.empty((T + 1, 1 + ng, n), dtype=torch.float32, device=x.device)
             v_out = None
-            with _timed("hh_forward", T * n):
-                _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_fin=ckpt[T, 0], g_fin=ckpt[T, 1:], ckpt=ckpt,
-                                     ckpt_every=1, sq_part=sq)
         else:
             ckpt = torch.empty(((T + K - 1) // K, 1 + ng, n), dtype=torch.float32, device=x.device)
             v_out = torch.empty((T, n), dtype=torch.float32, device=x.device)
-            with _timed("hh_forward", T * n):
-                _, _, bad = _forward(p, v0, g0, cur, n, 1, T, v_out=v_out, ckpt=ckpt, ckpt_every=K, sq_part=sq)
+        bad = torch.empty(1, dtype=torch.int64, device=x.device)
+        state = {}
+
+        def run_forward(cur, t0, t1):
+            c = [i for i, ch in enumerate(chunks) if ch[0] == t0][0] if len(chunks) > 1 else 0
+            if t0 == 0:
+                state["v"], state["g"] = (v0, g0) if t1 == T else (v0.clone(), g0.clone())
+            vi, gi = state["v"], state["g"]
+            if K == 1 and t1 == T:
+                vf, gf = ckpt[T, 0], ckpt[T, 1:]        # the final state goes to the extra slot
+            else:
+                vf, gf = vi, gi
+            with _timed("hh_forward", (t1 - t0) * n):
+                _forward(p, vi, gi, cur[t0 * B:t1 * B].view(t1 - t0, n), n, 1, t1 - t0, v_fin=vf, g_fin=gf,
+                         v_out=None if v_out is None else v_out[t0:t1],
+                         ckpt=ckpt[t0 // K:(t1 + K - 1) // K], ckpt_every=K, sq_part=sq[c], step_base=t0,
+                         first_bad=bad, reset_bad=t0 == 0)
+
+        xb, wb, cur = _project_forward(x, weight, bias, layer, K, run_forward)
         layer._last_bad = bad
         if layer.check_finite:
             _raise_if_bad(bad)

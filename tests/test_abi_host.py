@@ -181,9 +181,12 @@ def test_jit_source_compiles_for_sm100a(mk, tmp_path):
 
 
 def _mufu_ops(src: str, fn: str) -> int:
-    body = src[src.index("__device__ __forceinline__ float " + fn + "("):]
+    # the merged forward is generated in paired (f32x2) form: ex2v / rcpv = one
+    # MUFU op per neuron
+    head = "F2 " + fn + "2(" if "F2 " + fn + "2(" in src else "float " + fn + "("
+    body = src[src.index(head):]
     body = body[:body.index("\n}\n")]
-    return body.count("ex2f_(") + body.count("rcpf_(")
+    return sum(body.count(k) for k in ("ex2f_(", "rcpf_(", "ex2v<H>(", "rcpv<H>("))
 
 
 @pytest.mark.parametrize("mk,tau,merged", [(lambda: DF.na_kdr_cal_kca_params(), 31, 20),
@@ -275,3 +278,25 @@ def test_generated_modules_compile_for_sm100a_without_a_gpu(which):
     for kind in ((0, 1, 2) if which == "rs" else (0,)):
         cubin = nat.jit_cubin(p, kind)
         assert cubin[:4] == b"\x7fELF" and len(cubin) > 10000
+
+
+def test_forward_module_issues_paired_fp32_ops(tmp_path):
+    """The merged forward step is generated in f32x2 form (jit.cu mg::pair):
+    the 4-neurons/thread config-2 kernel issues FFMA2 / FMUL2 (two neurons per
+    instruction) with at most a token spill (one slot, outside the step); the network module keeps the
+    scalar step (FWD_PAIR 0)."""
+    import shutil
+    import subprocess
+    import numpy as np
+    from paper_2601_21407_b200 import defaults as DF
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    p = DF.na_kdr_cal_kca_params(dt=0.01).with_(dtype=np.float32)
+    f = tmp_path / "fwd.cubin"
+    f.write_bytes(nat.jit_cubin(p, -1 - (1 | 2 | 16)))        # FF_VO | FF_SO | FF_AL: the bench stream set
+    sass = subprocess.run([tool, "-sass", "-fun", "hh_fwdp_v4", str(f)], capture_output=True, text=True).stdout
+    assert sass.count("FFMA2 ") > 50 and sass.count("FMUL2 ") > 50
+    assert sass.count("STL") + sass.count("LDL") <= 4
+    src = nat.jit_source(p)
+    assert "F2 step_fwd_m2(" in src and "#define FWD_PAIR 1" in src
