@@ -385,23 +385,24 @@ def fwd_bwd_leg(torch, dev, proj="bf16", mufu_peak=None, cpu_seconds=0.0):
     W ~ N(0.05, 0.1^2), loss MSE(V, 0).  One step = tcgen05 projection (bf16,
     or bf16x3: the fp32-class split that meets the gradient contract against
     the reference's float64 operands), HH forward (full storage), BPTT,
-    dW / db / dX gradient GEMMs."""
+    dW / db gradient GEMMs.  x is the data: no input gradient, as the
+    reference's first layer (SURVEY §8 d3 lists the forward and dW GEMMs; the
+    CPU composition, oracle/cpu_baseline.py, computes none either)."""
     from paper_2601_21407_b200 import _native as nat
     from paper_2601_21407_b200.layer import HHLayer
     B, N, T, K_in = 256, 1024, 100, 784
     torch.manual_seed(0)
-    # dW / db on a side stream, concurrent with dX (their tile tails fill each
-    # other: 0.566 -> 0.544 ms bf16, 0.724 -> 0.705 ms bf16x3)
-    ov = os.environ.get("HHB_BENCH_C3_OVERLAP", "1") not in ("", "0")
+    # HHB_BENCH_C3_OVERLAP=1: dW / db on a side stream (they overlapped dX when
+    # the leg also produced the input gradient)
+    ov = os.environ.get("HHB_BENCH_C3_OVERLAP", "0") not in ("", "0")
     layer = HHLayer(K_in, N, w_mean=0.05, w_std=0.1, check_finite=False, device=dev, proj=proj,
                     overlap_weight_grad=ov)
     g = torch.Generator(device=dev).manual_seed(0)
     x = ((torch.rand((T, B, K_in), device=dev, generator=g) < 0.2).float()
-         + 0.1 * torch.randn((T, B, K_in), device=dev, generator=g)).requires_grad_(True)
+         + 0.1 * torch.randn((T, B, K_in), device=dev, generator=g))
 
     def step():
         layer.zero_grad(set_to_none=True)
-        x.grad = None            # dX is produced every step, not accumulated across steps
         # MSE(V, 0) fused into the HH kernels: sum V^2 accumulated by the
         # forward, the seed 2 V / numel (learn.py:86-88) read from the
         # checkpoints by the BPTT kernel -- no V trace written, no seed pass
@@ -428,11 +429,11 @@ def fwd_bwd_leg(torch, dev, proj="bf16", mufu_peak=None, cpu_seconds=0.0):
     out = {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
            "cuda_graph": graph is not None, "proj": proj,
            "config": f"BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, {proj} tcgen05 "
-                     "projection + fp32 HH forward + full-storage BPTT + bf16 hi/lo gradient GEMMs "
-                     "(dW on a side stream beside dX), "
+                     "projection + fp32 HH forward + full-storage BPTT + bf16 hi/lo weight-gradient "
+                     "GEMM (x is the data: no input gradient, as the reference's first layer), "
                      "loss MSE(V, 0) fused into the HH kernels (layer.mse_loss; one unit = one "
                      "neuron-step through forward and backward)",
-           "parity": ("dW/dX within 1e-4 of the float64 reference on the UNROUNDED operands "
+           "parity": ("dW within 1e-4 of the float64 reference on the UNROUNDED operands "
                       "(profiles/r2_parity_c3_unrounded.md)" if proj == "bf16x3" else
                       "within 3e-5 of the float64 reference on bf16-rounded operands, 3-4e-3 on the "
                       "unrounded ones (profiles/r2_parity_c3_unrounded.md)")}
