@@ -318,6 +318,16 @@ int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream);
 int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out,
                 double* scratch, void* stream);
 int64_t hhb_col_sum_scratch(int64_t rows, int64_t cols);
+/* out64[c] / out32[c] = sum_r src[r][c] (assigned, either output may be NULL):
+ * the bias gradient of an HH layer (learn.py:273, db = d_i.sum over (t, b)) in
+ * one launch when rows <= 512 (the per-neuron BPTT sums of a batch), else two
+ * through hhb_col_sum_scratch doubles of scratch; fixed order (deterministic). */
+int hhb_col_sum_ex(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out64, float* out32,
+                   double* scratch, void* stream);
+/* out64[0] / out32[0] = scale * sum of x[0..n) in a fixed order (one block):
+ * the fused MSE(V, 0) loss of an HH layer from the forward kernel's per-block
+ * partials (learn.py:80-84, mean of V^2) -- replaces sum + divide + cast. */
+int hhb_sum_f64(int64_t n, const double* x, double scale, double* out64, float* out32, void* stream);
 
 /* ---- LIF baseline (dynamics.py:227-244, :532-538; adjoint.py:197-227) ------ */
 

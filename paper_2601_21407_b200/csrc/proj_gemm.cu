@@ -942,6 +942,52 @@ __global__ void __launch_bounds__(256) k_col_sum_part(int64_t rows, int64_t cols
     part[int64_t(blockIdx.y) * cols + c] = s;
   }
 }
+// one-pass form (rows <= kColOnePass: one row chunk) and the assigning final
+// pass of hhb_col_sum_ex: out64 / out32 receive the sums (either may be null)
+constexpr int64_t kColOnePass = 512;
+__global__ void __launch_bounds__(256) k_col_sum_one(int64_t rows, int64_t cols, const float* src, int64_t ld,
+                                                     double* out64, float* out32) {
+  __shared__ double red[8][33];
+  const int64_t c = int64_t(blockIdx.x) * 32 + threadIdx.x;
+  double acc = 0.0;
+  if (c < cols)
+    for (int64_t r = threadIdx.y; r < rows; r += 8) acc += double(src[r * ld + c]);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    if (out64) out64[c] = s;
+    if (out32) out32[c] = float(s);
+  }
+}
+__global__ void k_col_sum_final_set(int64_t cols, int chunks, const double* part, double* out64, float* out32) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int k = 0; k < chunks; ++k) s += part[int64_t(k) * cols + c];
+  if (out64) out64[c] = s;
+  if (out32) out32[c] = float(s);
+}
+// fixed-order sum of n doubles (one block: strided per-thread sums in order,
+// then a fixed shared-memory tree), times scale -> out64[0] / out32[0]
+__global__ void __launch_bounds__(1024) k_sum_f64(int64_t n, const double* x, double scale, double* out64,
+                                                  float* out32) {
+  __shared__ double red[1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double s = red[0] * scale;
+    if (out64) out64[0] = s;
+    if (out32) out32[0] = float(s);
+  }
+}
 __global__ void k_col_sum_final(int64_t cols, int chunks, const double* part, double* out) {
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
@@ -1449,6 +1495,29 @@ int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double
   k_col_sum_part<<<grid, block, 0, st>>>(rows, cols, src, ld, scratch);
   k_col_sum_final<<<unsigned((cols + 127) / 128), 128, 0, st>>>(cols, chunks, scratch, out);
   return cuda_check("k_col_sum launch");
+}
+
+int hhb_col_sum_ex(int64_t rows, int64_t cols, const float* src, int64_t ld, double* out64, float* out32,
+                   double* scratch, void* stream) {
+  if (cols <= 0) return HHB_OK;
+  using namespace hhb::gemm;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows <= kColOnePass) {
+    k_col_sum_one<<<unsigned((cols + 31) / 32), dim3(32u, 8u, 1u), 0, st>>>(rows, cols, src, ld, out64, out32);
+    return cuda_check("k_col_sum_one launch");
+  }
+  if (!scratch) return fail(HHB_EINVAL, "col_sum_ex needs hhb_col_sum_scratch doubles of scratch");
+  const int chunks = col_chunks(rows);
+  const dim3 grid{unsigned((cols + 31) / 32), unsigned(chunks), 1u};
+  k_col_sum_part<<<grid, dim3(32u, 8u, 1u), 0, st>>>(rows, cols, src, ld, scratch);
+  k_col_sum_final_set<<<unsigned((cols + 127) / 128), 128, 0, st>>>(cols, chunks, scratch, out64, out32);
+  return cuda_check("k_col_sum_ex launch");
+}
+
+int hhb_sum_f64(int64_t n, const double* x, double scale, double* out64, float* out32, void* stream) {
+  if (n < 0 || (n > 0 && !x)) return fail(HHB_EINVAL, "sum_f64: bad input");
+  hhb::gemm::k_sum_f64<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, scale, out64, out32);
+  return cuda_check("k_sum_f64 launch");
 }
 
 }  // extern "C"

@@ -185,6 +185,19 @@ def _workspace(n: int, dev) -> torch.Tensor:
 A_MN, B_MN = 1, 2
 
 
+def col_sum_f32(src: torch.Tensor) -> torch.Tensor:
+    """Column sums of a (rows, cols) fp32 matrix as fp32, fixed order, one
+    launch for rows <= 512 (hhb_col_sum_ex)."""
+    M, N = src.shape
+    lib = nat.load()
+    out = torch.empty(N, dtype=torch.float32, device=src.device)
+    scratch = (torch.empty(max(1, int(lib.hhb_col_sum_scratch(M, N))), dtype=torch.float64, device=src.device)
+               if M > 512 else None)
+    nat.check(lib.hhb_col_sum_ex(M, N, src.data_ptr(), src.stride(0), None, out.data_ptr(), D.ptr(scratch),
+                                 _stream()), "colsum")
+    return out
+
+
 def col_sum(dI: torch.Tensor) -> torch.Tensor:
     M, N = dI.shape
     lib = nat.load()
@@ -248,7 +261,7 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         side.wait_event(fork)
         with torch.cuda.stream(side):
             dW = weight_grad()
-            db = col_sum(dsum.view(B, n_out)).float()
+            db = col_sum_f32(dsum.view(B, n_out))
             done = torch.cuda.Event()
             done.record(side)
         for t in (hi, lo, zb, xb):
@@ -270,7 +283,7 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         dW = db = None
     else:
         dW = weight_grad()
-        db = col_sum(dsum.view(B, n_out)).float()
+        db = col_sum_f32(dsum.view(B, n_out))
     dX = None
     if x_requires_grad:
         # dX[m][k] = sum_j dI[m][j] W[j][k]: A = dI (K-major), B = W^T (MN-major view of W);
@@ -510,7 +523,10 @@ class _HHLayerMSEFn(torch.autograd.Function):
         ctx.save_for_backward(xb, wb, cur, ckpt, v_out)
         ctx.layer, ctx.K, ctx.shape = layer, K, (T, B, k_in, n_out)
         ctx.x_requires_grad = x.requires_grad
-        return (sq.sum() / (T * n)).float()
+        loss = torch.empty((), dtype=torch.float32, device=x.device)
+        nat.check(nat.load().hhb_sum_f64(sq.numel(), sq.data_ptr(), 1.0 / (T * n), None, loss.data_ptr(), _stream()),
+                  "loss")
+        return loss
 
     @staticmethod
     def backward(ctx, g):

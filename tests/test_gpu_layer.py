@@ -258,3 +258,26 @@ def test_spike_operand_written_by_the_forward_kernel(cuda):
     va, _ = l2(s)
     vb, _ = l2(s.detach().clone())          # a plain tensor: the cast path
     assert torch.equal(va, vb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols", [(1, 5), (256, 1024), (300, 10), (513, 37), (4096, 130)])
+def test_column_sums_and_loss_reduction(cuda, rows, cols):
+    """hhb_col_sum_ex (the bias gradient: one launch for rows <= 512, two
+    beyond) and hhb_sum_f64 (the fused loss) against float64 sums; both are
+    fixed-order, so repeated calls give identical bits."""
+    from paper_2601_21407_b200 import _native as nat
+    from paper_2601_21407_b200.layer import col_sum_f32
+    g = torch.Generator(device=cuda).manual_seed(rows * 7 + cols)
+    src = torch.randn((rows, cols), device=cuda, generator=g)
+    out = col_sum_f32(src)
+    ref = src.double().sum(0)
+    assert torch.allclose(out.double(), ref, rtol=1e-6, atol=1e-6)
+    assert torch.equal(out, col_sum_f32(src))
+    x = torch.rand(rows * cols, dtype=torch.float64, device=cuda, generator=g)
+    o64 = torch.empty(1, dtype=torch.float64, device=cuda)
+    o32 = torch.empty(1, dtype=torch.float32, device=cuda)
+    nat.check(nat.load().hhb_sum_f64(x.numel(), x.data_ptr(), 0.5, o64.data_ptr(), o32.data_ptr(), None), "sum")
+    torch.cuda.synchronize()
+    assert abs(o64.item() - 0.5 * x.sum().item()) <= 1e-12 * x.numel()
+    assert o32.item() == np.float32(o64.item())
