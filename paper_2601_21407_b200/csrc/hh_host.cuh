@@ -224,7 +224,7 @@ int launch_backward(const DevTable<T>& tb, const DevSur<T>& sur, const BwdArgs<T
   }
   int rc = cuda_check("k_backward launch");
   if (rc) return rc;
-  k_reduce<T><<<kSlots, 256, 0, st>>>(tb, a.partials, blocks, d_params);
+  launch_pdl(k_reduce<T>, dim3(kSlots), dim3(256), 0, st, tb, (const double*)a.partials, int64_t(blocks), d_params);
   return cuda_check("k_reduce launch");
 }
 
@@ -364,7 +364,8 @@ struct Flavour {
     int jrc = HHB_OK;                                                                            \
     if (try_jit_bwd<T>(P, sur, a, st, jrc)) {                                                    \
       if (jrc) return jrc;                                                                       \
-      k_reduce<T><<<kSlots, 256, 0, st>>>(tb, a.partials, bwd_blocks(a.n), d_params);            \
+      launch_pdl(k_reduce<T>, dim3(kSlots), dim3(256), 0, st, tb, (const double*)a.partials,        \
+                 int64_t(bwd_blocks(a.n)), d_params);                                                \
       return cuda_check("k_reduce launch");                                                      \
     }                                                                                            \
     return launch_backward<T>(tb, sur, a, d_params, st);                                         \

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "hh_device.cuh"
+#include "pdl.cuh"
 
 namespace hhb {
 
@@ -566,6 +567,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward(const DevTable<T> tb, 
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce(const DevTable<T> tb, const double* partials,
                                                 int64_t nblocks, double* d_params) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x;
   double x = 0.0;
   for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x) x += partials[b * kSlots + s];

@@ -53,6 +53,7 @@ struct Driver {
   decltype(&cuLaunchCooperativeKernel) coop = nullptr;                        // optional
   decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;  // optional
   decltype(&cuFuncSetAttribute) set_attr = nullptr;                           // optional
+  decltype(&cuLaunchKernelEx) launch_ex = nullptr;                            // optional (PDL)
   bool ok = false;
   std::string why;
 };
@@ -62,6 +63,24 @@ static Nvrtc g_nv;
 static Driver g_drv;
 static bool g_loaded = false;
 static std::string g_status = "not initialised";
+
+// cuLaunchKernel with the programmatic-stream-serialization attribute (pdl.cuh)
+static CUresult launch_pdl_drv(CUfunction f, unsigned gx, unsigned bx, CUstream st, void** params) {
+  if (!g_drv.launch_ex || !hhb::pdl_enabled()) return g_drv.launch(f, gx, 1, 1, bx, 1, 1, 0, st, params, nullptr);
+  CUlaunchConfig cfg{};
+  cfg.gridDimX = gx;
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = bx;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = 0;
+  cfg.hStream = st;
+  CUlaunchAttribute attr[1];
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return g_drv.launch_ex(&cfg, f, params, nullptr);
+}
 
 template <typename F>
 static bool sym(void* h, const char* name, F& out) {
@@ -104,6 +123,8 @@ static void load_libs() {
     g_drv.occupancy = reinterpret_cast<decltype(g_drv.occupancy)>(p);
   if (cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess && p)
     g_drv.set_attr = reinterpret_cast<decltype(g_drv.set_attr)>(p);
+  if (cudaGetDriverEntryPoint("cuLaunchKernelEx", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+    g_drv.launch_ex = reinterpret_cast<decltype(g_drv.launch_ex)>(p);
   g_drv.ok = ok;
   if (!ok) g_drv.why = "driver entry points unavailable";
 }
@@ -1001,6 +1022,12 @@ static const char* kPrelude = R"(
 #endif
 typedef long long i64;
 typedef unsigned int u32;
+// programmatic dependent launch (pdl.cuh): wait for the predecessor grid before
+// touching global memory, then let the successor's CTAs be scheduled
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 struct FwdArgs { i64 n, steps; const float* v_in; const float* g_in; i64 g_ld; float* v_fin; float* g_fin;
   const float* i_ext; i64 i_st, i_sn; float* v_out; i64 v_ld; u32* spk; i64 spk_ld; float* ckpt;
   i64 ck_every, ck_ld; i64 step_base; i64* first_bad; unsigned long long seed; i64 nbase;
@@ -1155,6 +1182,7 @@ struct Stimulus {
 // per-neuron tails in the loop).
 template <int VEC, bool POIS>
 __device__ __forceinline__ void fwd_body(const FwdArgs& a_in, const PoissonTab& tab, const Keys& ks) {
+  pdl_begin();
   FwdArgs a = a_in;
   if (a.step_dev != nullptr) a.step_base += *a.step_dev;
   const int lane = threadIdx.x & 31;
@@ -1760,6 +1788,7 @@ __device__ __forceinline__ void cpa(float* dst, const float* src) {
 
 template <int VEC>
 __device__ __forceinline__ void bwd_body(const Sur& sur, const BwdArgs& a) {
+  pdl_begin();
   constexpr int TPB = BWD_THREADS / VEC;
   __shared__ __align__(16) float ring[DEPTH * RING_STRIDE];
   const i64 i0 = i64(blockIdx.x) * BWD_THREADS + i64(threadIdx.x) * VEC;
@@ -2457,8 +2486,7 @@ bool jit_forward(const hhb_params_t* P, const FwdArgs<float>& a, const PoissonTa
   }
   void* params[] = {&args, &tab, keys};
   CUfunction f = ptab ? (vec4 ? m->fwdp4 : m->fwdp1) : (vec4 ? m->fwd4 : m->fwd1);
-  const CUresult r = jit::g_drv.launch(f, unsigned(blocks), 1, 1, unsigned(tpb), 1, 1, 0,
-                                       reinterpret_cast<CUstream>(st), params, nullptr);
+  const CUresult r = jit::launch_pdl_drv(f, unsigned(blocks), unsigned(tpb), reinterpret_cast<CUstream>(st), params);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit forward launch failed");
   return true;
 }
@@ -2491,9 +2519,9 @@ bool jit_backward(const hhb_params_t* P, const DevSur<float>& sur, const BwdArgs
                     (!a.di_hi || (even(a.dh_ld) && (a.dh_grp == 0 || (even(a.dh_grp) && even(a.dh_pitch))) &&
                                   (reinterpret_cast<uintptr_t>(a.di_hi) & 3) == 0 &&
                                   (reinterpret_cast<uintptr_t>(a.di_lo) & 3) == 0));
-  const CUresult r = jit::g_drv.launch(vec2 ? m->bwd2 : m->bwd, unsigned(blocks), 1, 1,
-                                       unsigned(vec2 ? kBwdThreads / 2 : kBwdThreads), 1, 1, 0,
-                                       reinterpret_cast<CUstream>(st), params, nullptr);
+  const CUresult r = jit::launch_pdl_drv(vec2 ? m->bwd2 : m->bwd, unsigned(blocks),
+                                         unsigned(vec2 ? kBwdThreads / 2 : kBwdThreads), reinterpret_cast<CUstream>(st),
+                                         params);
   rc = (r == CUDA_SUCCESS) ? HHB_OK : fail(HHB_ECUDA, "jit backward launch failed");
   return true;
 }

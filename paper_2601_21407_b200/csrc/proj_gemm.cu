@@ -206,6 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
+  pdl_wait();       // the prologue above overlaps the predecessor's tail (pdl.cuh)
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
@@ -388,6 +390,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
+  pdl_wait();       // the prologue above overlaps the predecessor's tail (pdl.cuh)
+  pdl_trigger();
   const int per_split = args.m_tiles * args.n_tiles;
 
   if (warp == 0) {
@@ -650,6 +654,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
+  pdl_wait();       // the prologue above overlaps the predecessor's tail (pdl.cuh)
+  pdl_trigger();
   const int per_split = args.m_tiles * args.n_tiles;      // m_tiles counts 256-row pair tiles
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
@@ -805,6 +811,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 // fixed-order split-K reduction (+ bias)
 __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits, int64_t split_stride,
                               const float* bias, float* D, int64_t ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = M * N;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t m = i / N, n = i % N;
@@ -821,6 +829,8 @@ __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits,
 enum { TR_PLAIN = 0, TR_SPLIT = 1, TR_DUP = 2 };
 template <typename S, typename Dt, int MODE>
 __global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t lds, Dt* dst, int64_t ldd) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float tile[32][33];
   const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -849,6 +859,8 @@ __global__ void k_transpose(int64_t rows, int64_t cols, const S* src, int64_t ld
 // row-wise bf16x2 split without transposing: dst[r][c] = hi, dst[r][cols + c] = lo
 __global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64_t lds, __nv_bfloat16* dst,
                              int64_t ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
@@ -865,6 +877,8 @@ __global__ void k_split_rows(int64_t rows, int64_t cols, const float* src, int64
 // ~2^-16 relative, is dropped).  Pad columns are left to the caller (zeros).
 __global__ void k_split3_rows(int64_t rows, int64_t cols, const float* src, int64_t lds, __nv_bfloat16* dst,
                               int64_t ldd, int64_t slot, int order) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
@@ -884,6 +898,8 @@ __global__ void k_split3_rows(int64_t rows, int64_t cols, const float* src, int6
 // per thread, two 16-byte loads and three 16-byte stores
 __global__ void k_split3_rows_v8(int64_t rows, int64_t cols8, const float* src, int64_t lds, __nv_bfloat16* dst,
                                  int64_t ldd, int64_t slot, int order) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = rows * cols8;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = q / cols8, c = (q % cols8) * 8;
@@ -908,6 +924,8 @@ __global__ void k_split3_rows_v8(int64_t rows, int64_t cols8, const float* src, 
 // 8 elements per thread: two 16-byte loads, one 16-byte store (16-byte aligned
 // src/dst, checked by the caller); the scalar kernel takes the rest
 __global__ void k_cast_bf16_v8(int64_t n8, const float4* src, uint4* dst) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
     const float4 a = __ldg(src + 2 * i), b = __ldg(src + 2 * i + 1);
     __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
@@ -916,6 +934,8 @@ __global__ void k_cast_bf16_v8(int64_t n8, const float4* src, uint4* dst) {
   }
 }
 __global__ void k_cast_bf16(int64_t n, const float* src, __nv_bfloat16* dst) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
 }
@@ -927,6 +947,8 @@ __global__ void k_cast_bf16(int64_t n, const float* src, __nv_bfloat16* dst) {
 constexpr int kColChunks = 64;
 __global__ void __launch_bounds__(256) k_col_sum_part(int64_t rows, int64_t cols, const float* src, int64_t ld,
                                                       double* part) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[8][33];
   const int64_t c = int64_t(blockIdx.x) * 32 + threadIdx.x;
   const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
@@ -947,6 +969,8 @@ __global__ void __launch_bounds__(256) k_col_sum_part(int64_t rows, int64_t cols
 constexpr int64_t kColOnePass = 512;
 __global__ void __launch_bounds__(256) k_col_sum_one(int64_t rows, int64_t cols, const float* src, int64_t ld,
                                                      double* out64, float* out32) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[8][33];
   const int64_t c = int64_t(blockIdx.x) * 32 + threadIdx.x;
   double acc = 0.0;
@@ -962,6 +986,8 @@ __global__ void __launch_bounds__(256) k_col_sum_one(int64_t rows, int64_t cols,
   }
 }
 __global__ void k_col_sum_final_set(int64_t cols, int chunks, const double* part, double* out64, float* out32) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   double s = 0.0;
@@ -973,6 +999,8 @@ __global__ void k_col_sum_final_set(int64_t cols, int chunks, const double* part
 // then a fixed shared-memory tree), times scale -> out64[0] / out32[0]
 __global__ void __launch_bounds__(1024) k_sum_f64(int64_t n, const double* x, double scale, double* out64,
                                                   float* out32) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[1024];
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
@@ -989,6 +1017,8 @@ __global__ void __launch_bounds__(1024) k_sum_f64(int64_t n, const double* x, do
   }
 }
 __global__ void k_col_sum_final(int64_t cols, int chunks, const double* part, double* out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   double s = 0.0;
@@ -1057,7 +1087,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorM
   });
   if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
   const dim3 grid{unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(splits)};
-  k_umma_gemm<BN, TF32, A_MN, B_MN, DUAL><<<grid, kThreads, smem, st>>>(ta, ta2, tb, a);
+  launch_pdl(k_umma_gemm<BN, TF32, A_MN, B_MN, DUAL>, dim3(grid), dim3(kThreads), smem, st, ta, ta2, tb, a);
   return cuda_check("k_umma_gemm launch");
 }
 
@@ -1108,7 +1138,7 @@ static int launch_p(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtenso
   });
   if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed");
   const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
-  k_umma_gemm_p<BN, A_MN, B_MN, DUAL><<<grid, kThreads, smem, st>>>(ta, ta2, tb, td, a);
+  launch_pdl(k_umma_gemm_p<BN, A_MN, B_MN, DUAL>, dim3(grid), dim3(kThreads), smem, st, ta, ta2, tb, td, a);
   return cuda_check("k_umma_gemm_p launch");
 }
 
@@ -1155,7 +1185,7 @@ static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUten
   int pairs = max_pairs;
   if (a.tiles < pairs) pairs = a.tiles;
   if (getenv("HHB_GEMM_PAIRS_DEBUG")) fprintf(stderr, "k_umma_gemm_2sm: %d co-resident pairs\n", max_pairs);
-  k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL><<<2 * pairs, kThreads2, smem, st>>>(ta, ta2, tb, td, a);
+  launch_pdl(k_umma_gemm_2sm<BN, A_MN, B_MN, DUAL>, dim3(2 * pairs), dim3(kThreads2), smem, st, ta, ta2, tb, td, a);
   return cuda_check("k_umma_gemm_2sm launch");
 }
 
@@ -1223,7 +1253,7 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
   rc = tf32 ? launch_bn<true, false, false, false>(bn, ta, ta, tb, a, splits, st)
             : launch_bn<false, false, false, false>(bn, ta, ta, tb, a, splits, st);
   if (rc || splits == 1) return rc;
-  k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+  launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits, int64_t(M * N), bias, D, ldd);
   return cuda_check("k_gemm_reduce launch");
 }
 
@@ -1344,7 +1374,7 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
       HHB_GEMM_2CASE(true, true, true)
 #undef HHB_GEMM_2CASE
       if (rc || splits == 1) return rc;
-      k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+      launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits, int64_t(M * N), bias, D, ldd);
       return cuda_check("k_gemm_reduce launch");
     }
     PArgs pa{};
@@ -1372,7 +1402,7 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
     HHB_GEMM_PCASE(true, true, true)
 #undef HHB_GEMM_PCASE
     if (rc || splits == 1) return rc;
-    k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+    launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits, int64_t(M * N), bias, D, ldd);
     return cuda_check("k_gemm_reduce launch");
   }
   Args a{};
@@ -1407,7 +1437,7 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
   HHB_GEMM_CASE(true, true, true)
 #undef HHB_GEMM_CASE
   if (rc || splits == 1) return rc;
-  k_gemm_reduce<<<grid_1d(M * N, 256), 256, 0, st>>>(M, N, workspace, splits, M * N, bias, D, ldd);
+  launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits, int64_t(M * N), bias, D, ldd);
   return cuda_check("k_gemm_reduce launch");
 }
 
@@ -1422,11 +1452,11 @@ int hhb_transpose(int32_t kind, int64_t rows, int64_t cols, const void* src, int
   const float* sf = static_cast<const float*>(src);
   const bf* sb = static_cast<const bf*>(src);
   switch (kind) {
-    case 0: k_transpose<float, float, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sf, lds, (float*)dst, ldd); break;
-    case 1: k_transpose<float, bf, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sf, lds, (bf*)dst, ldd); break;
-    case 2: k_transpose<bf, bf, TR_PLAIN><<<grid, block, 0, st>>>(rows, cols, sb, lds, (bf*)dst, ldd); break;
-    case 3: k_transpose<float, bf, TR_SPLIT><<<grid, block, 0, st>>>(rows, cols, sf, lds, (bf*)dst, ldd); break;
-    case 4: k_transpose<bf, bf, TR_DUP><<<grid, block, 0, st>>>(rows, cols, sb, lds, (bf*)dst, ldd); break;
+    case 0: launch_pdl(k_transpose<float, float, TR_PLAIN>, dim3(grid), dim3(block), 0, st, rows, cols, sf, lds, (float*)dst, ldd); break;
+    case 1: launch_pdl(k_transpose<float, bf, TR_PLAIN>, dim3(grid), dim3(block), 0, st, rows, cols, sf, lds, (bf*)dst, ldd); break;
+    case 2: launch_pdl(k_transpose<bf, bf, TR_PLAIN>, dim3(grid), dim3(block), 0, st, rows, cols, sb, lds, (bf*)dst, ldd); break;
+    case 3: launch_pdl(k_transpose<float, bf, TR_SPLIT>, dim3(grid), dim3(block), 0, st, rows, cols, sf, lds, (bf*)dst, ldd); break;
+    case 4: launch_pdl(k_transpose<bf, bf, TR_DUP>, dim3(grid), dim3(block), 0, st, rows, cols, sb, lds, (bf*)dst, ldd); break;
     default: return fail(HHB_EINVAL, "transpose kind");
   }
   return cuda_check("k_transpose launch");
@@ -1437,7 +1467,7 @@ int hhb_split_rows_bf16(int64_t rows, int64_t cols, const float* src, int64_t ld
   if (rows <= 0 || cols <= 0) return HHB_OK;
   if (ldd < 2 * cols) return fail(HHB_EINVAL, "ldd < 2*cols");
   const dim3 grid{unsigned((cols + 255) / 256), unsigned(rows < 65535 ? rows : 65535), 1u};
-  hhb::gemm::k_split_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_pdl(hhb::gemm::k_split_rows, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
   return cuda_check("k_split_rows launch");
 }
@@ -1451,12 +1481,12 @@ int hhb_split3_bf16(int64_t rows, int64_t cols, const float* src, int64_t lds, v
                    reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0;
   if (vec) {
     const int64_t total = rows * (cols / 8);
-    hhb::gemm::k_split3_rows_v8<<<grid_1d(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    launch_pdl(hhb::gemm::k_split3_rows_v8, dim3(grid_1d(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
         rows, cols / 8, src, lds, static_cast<__nv_bfloat16*>(dst), ldd, slot, order);
     return cuda_check("k_split3_rows_v8 launch");
   }
   const dim3 grid{unsigned((cols + 255) / 256), unsigned(rows < 65535 ? rows : 65535), 1u};
-  hhb::gemm::k_split3_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_pdl(hhb::gemm::k_split3_rows, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd, slot, order);
   return cuda_check("k_split3_rows launch");
 }
@@ -1467,12 +1497,12 @@ int hhb_cast_bf16(int64_t n, const float* src, void* dst, void* stream) {
   int64_t done = 0;
   if (reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && n >= 8) {
     const int64_t n8 = n / 8;
-    hhb::gemm::k_cast_bf16_v8<<<grid_1d(n8, 256), 256, 0, st>>>(n8, reinterpret_cast<const float4*>(src),
+    launch_pdl(hhb::gemm::k_cast_bf16_v8, dim3(grid_1d(n8, 256)), dim3(256), 0, st, n8, reinterpret_cast<const float4*>(src),
                                                                   static_cast<uint4*>(dst));
     done = n8 * 8;
   }
   if (done < n)
-    hhb::gemm::k_cast_bf16<<<grid_1d(n - done, 256), 256, 0, st>>>(n - done, src + done,
+    launch_pdl(hhb::gemm::k_cast_bf16, dim3(grid_1d(n - done, 256)), dim3(256), 0, st, n - done, src + done,
                                                                     static_cast<__nv_bfloat16*>(dst) + done);
   return cuda_check("k_cast_bf16 launch");
 }
@@ -1492,8 +1522,8 @@ int hhb_col_sum(int64_t rows, int64_t cols, const float* src, int64_t ld, double
   const int chunks = col_chunks(rows);
   const dim3 grid{unsigned((cols + 31) / 32), unsigned(chunks), 1u};
   const dim3 block{32u, 8u, 1u};
-  k_col_sum_part<<<grid, block, 0, st>>>(rows, cols, src, ld, scratch);
-  k_col_sum_final<<<unsigned((cols + 127) / 128), 128, 0, st>>>(cols, chunks, scratch, out);
+  launch_pdl(k_col_sum_part, dim3(grid), dim3(block), 0, st, rows, cols, src, ld, scratch);
+  launch_pdl(k_col_sum_final, dim3(unsigned((cols + 127) / 128)), dim3(128), 0, st, cols, chunks, scratch, out);
   return cuda_check("k_col_sum launch");
 }
 
@@ -1503,20 +1533,20 @@ int hhb_col_sum_ex(int64_t rows, int64_t cols, const float* src, int64_t ld, dou
   using namespace hhb::gemm;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows <= kColOnePass) {
-    k_col_sum_one<<<unsigned((cols + 31) / 32), dim3(32u, 8u, 1u), 0, st>>>(rows, cols, src, ld, out64, out32);
+    launch_pdl(k_col_sum_one, dim3(unsigned((cols + 31) / 32)), dim3(dim3(32u, 8u, 1u)), 0, st, rows, cols, src, ld, out64, out32);
     return cuda_check("k_col_sum_one launch");
   }
   if (!scratch) return fail(HHB_EINVAL, "col_sum_ex needs hhb_col_sum_scratch doubles of scratch");
   const int chunks = col_chunks(rows);
   const dim3 grid{unsigned((cols + 31) / 32), unsigned(chunks), 1u};
-  k_col_sum_part<<<grid, dim3(32u, 8u, 1u), 0, st>>>(rows, cols, src, ld, scratch);
-  k_col_sum_final_set<<<unsigned((cols + 127) / 128), 128, 0, st>>>(cols, chunks, scratch, out64, out32);
+  launch_pdl(k_col_sum_part, dim3(grid), dim3(dim3(32u, 8u, 1u)), 0, st, rows, cols, src, ld, scratch);
+  launch_pdl(k_col_sum_final_set, dim3(unsigned((cols + 127) / 128)), dim3(128), 0, st, cols, chunks, scratch, out64, out32);
   return cuda_check("k_col_sum_ex launch");
 }
 
 int hhb_sum_f64(int64_t n, const double* x, double scale, double* out64, float* out32, void* stream) {
   if (n < 0 || (n > 0 && !x)) return fail(HHB_EINVAL, "sum_f64: bad input");
-  hhb::gemm::k_sum_f64<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, scale, out64, out32);
+  launch_pdl(hhb::gemm::k_sum_f64, dim3(1), dim3(1024), 0, static_cast<cudaStream_t>(stream), n, x, scale, out64, out32);
   return cuda_check("k_sum_f64 launch");
 }
 
