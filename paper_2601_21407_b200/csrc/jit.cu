@@ -516,7 +516,10 @@ static bool disabled() {
 }
 
 // shared exponentials (independent MUFU ops, issued back to back)
-static std::string emit_exps(const Plan& M) {
+// poly: the first `poly` shared exponentials go to the FMA pipe (ex2p_, a
+// degree-6 polynomial, 1.3 ulp -- below MUFU.EX2's ~2) instead of MUFU; the
+// forward step only, where MUFU is the binding pipe (HHB_JIT_POLY_EXP)
+static std::string emit_exps(const Plan& M, int poly = 0) {
   std::string o;
   std::vector<int> direct_only(M.groups.size(), 1);
   for (const auto& g : M.gates)
@@ -525,7 +528,7 @@ static std::string emit_exps(const Plan& M) {
   for (size_t i = 0; i < M.groups.size(); ++i) {
     if (direct_only[i]) continue;
     const double K2 = -kLog2e / M.groups[i].b;
-    o += fmt("  const float E%d = ex2f_(__fmaf_rn(v, %s, %s));\n", int(i), F(K2).c_str(),
+    o += fmt("  const float E%d = %s(__fmaf_rn(v, %s, %s));\n", int(i), poly-- > 0 ? "ex2p_" : "ex2f_", F(K2).c_str(),
              F(-M.groups[i].vc * K2).c_str());
   }
   return o;
@@ -708,7 +711,8 @@ static std::string emit_step(const hhb_params_t* P, const Layout& L, const Plan&
            F(0.5 * (M.lo + M.hi)).c_str(), F(0.5 * (M.hi - M.lo)).c_str());
   o += fmt("__device__ __forceinline__ float step_fwd_m(const float v, float (&p)[%d], const float cur) {\n",
            NG > 0 ? NG : 1);
-  o += emit_exps(M);
+  const char* pe = getenv("HHB_JIT_POLY_EXP");
+  o += emit_exps(M, pe ? atoi(pe) : 0);
   o += L.leak_ch.empty() ? "  float ion = 0.0f;\n"
                          : fmt("  float ion = __fmaf_rn(%s, v, %s);\n", F(L.gl).c_str(), F(-L.gle).c_str());
   o += "  float eta = 1.0f;\n";
@@ -848,6 +852,18 @@ __device__ __forceinline__ float ex2y_(float x) { float y; asm volatile("ex2.app
 __device__ __forceinline__ float rcpy_(float x) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 template <bool H> __device__ __forceinline__ F2 ex2v(const F2 a) { const float x = ex2f_(a.x); return F2(x, H ? x : ex2y_(a.y)); }
 template <bool H> __device__ __forceinline__ F2 rcpv(const F2 a) { const float x = rcpf_(a.x); return F2(x, H ? x : rcpy_(a.y)); }
+__device__ __forceinline__ F2 ex2p2(const F2 x) {   // paired ex2p_ (same operations per half)
+  const F2 t = add2(x, 12582912.0f);
+  const F2 f = sub2(x, sub2(t, 12582912.0f));
+  F2 p = fma2(0x1.41d332p-13f, f, 0x1.5f456ap-10f);
+  p = fma2(p, f, 0x1.3b2dbcp-7f);
+  p = fma2(p, f, 0x1.c6aed4p-5f);
+  p = fma2(p, f, 0x1.ebfbdap-3f);
+  p = fma2(p, f, 0x1.62e430p-1f);
+  p = fma2(p, f, 1.0f);
+  return F2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+            __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 template <bool H> __device__ __forceinline__ F2 surrogate2(const Sur& s, const F2 u) {
   const float x = surrogate(s, u.x);
   return F2(x, H ? x : surrogate(s, u.y));
@@ -899,6 +915,7 @@ static std::string pair(const std::string& fn, const std::string& name) {
   replace_all(body, "__fsub_rn(", "sub2(");
   replace_all(body, "__fmaf_rn(", "fma2(");
   replace_all(body, "ex2f_(", "ex2v<H>(");
+  replace_all(body, "ex2p_(", "ex2p2(");
   replace_all(body, "rcpf_(", "rcpv<H>(");
   replace_all(body, "fabsf(", "abs2(");
   replace_all(body, "surrogate(", "surrogate2<H>(");
@@ -1110,6 +1127,20 @@ struct Sur { int kind; float w, inv_w, k2, half_inv_w; };
 #define LLMAX 0x7fffffffffffffffLL
 __device__ __forceinline__ float ex2f_(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float rcpf_(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+// 2^x on the FMA pipe: x = j + f (j = round(x) via the 1.5 * 2^23 shifter, |f| <= 1/2),
+// a degree-6 polynomial for 2^f (max rel. error 7.9e-8 = 1.3 ulp over the interval;
+// MUFU.EX2 is ~2 ulp), then j added to the exponent field.  For |x| < 126.
+__device__ __forceinline__ float ex2p_(float x) {
+  const float t = __fadd_rn(x, 12582912.0f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  float p = __fmaf_rn(0x1.41d332p-13f, f, 0x1.5f456ap-10f);
+  p = __fmaf_rn(p, f, 0x1.3b2dbcp-7f);
+  p = __fmaf_rn(p, f, 0x1.c6aed4p-5f);
+  p = __fmaf_rn(p, f, 0x1.ebfbdap-3f);
+  p = __fmaf_rn(p, f, 0x1.62e430p-1f);
+  p = __fmaf_rn(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ bool finitef_(float x) { return fabsf(x) < __int_as_float(0x7f800000); }
 __device__ __forceinline__ float surrogate(const Sur& s, float u) {
   if (s.kind == 1) return (fabsf(u) <= s.w) ? s.half_inv_w : 0.0f;
@@ -2383,7 +2414,7 @@ static std::string key_of(const hhb_params_t* P, int dev) {
   k += pf4 ? std::string("q") + pf4 : "";
   const char* b1 = getenv("HHB_JIT_BWD_ONE_RCP");
   k += b1 ? std::string("o") + b1 : "";
-  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK", "HHB_JIT_BWD_PAIR", "HHB_JIT_FWD_HALF"}) {
+  for (const char* e : {"HHB_NET_CAP", "HHB_NET_UNROLL", "HHB_NET_NOPAIR", "HHB_JIT_CHECK", "HHB_JIT_BWD_PAIR", "HHB_JIT_FWD_HALF", "HHB_JIT_POLY_EXP"}) {
     const char* x = getenv(e);
     k += x ? std::string("|") + e + x : "";
   }
