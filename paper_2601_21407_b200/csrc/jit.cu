@@ -1515,7 +1515,29 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
   }
   __syncthreads();
 }
+// the same barrier split in two, so that work can run between the arrival and
+// the wait: grid_arrive after the block's writes, grid_wait before reading the
+// other blocks' writes
+__device__ __forceinline__ void grid_arrive(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned target) {
+  if (threadIdx.x == 0) {
+    unsigned seen;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while (seen < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
 #define NET_THREADS 256
+// deliveries with delay >= 3 of one step, parked until the next step's barrier
+// wait (they land in ring rows >= t + 3: nothing reads them sooner)
+#ifndef NET_PEND
+#define NET_PEND 2048
+#endif
 // exclusive block scan of one value per thread (warp shuffles + one smem pass)
 __device__ __forceinline__ i64 block_scan(i64 x, i64* s_w, i64& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1552,6 +1574,12 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   unsigned long long (*s_next)[NET_THREADS] = reinterpret_cast<unsigned long long (*)[NET_THREADS]>(s_dyn);
   long long (*s_ahead)[NET_THREADS] = reinterpret_cast<long long (*)[NET_THREADS]>(s_dyn + R * NET_THREADS);
+  // step t's delay-2 deliveries (ring row t + 2), shifted into s_next when step t + 1 starts
+  unsigned long long (*s_next2)[NET_THREADS] =
+      reinterpret_cast<unsigned long long (*)[NET_THREADS]>(s_dyn + 2 * R * NET_THREADS);
+  __shared__ int s_poff[NET_PEND];                        // parked deliveries: ring offset, weight
+  __shared__ int s_pw[NET_PEND];
+  __shared__ int s_np;
   __shared__ int s_src[NET_CAP];                          // spiking sources, replica in bits 20+
   __shared__ int s_beg[NET_CAP];                          // (synapse indices < 2^31)
   __shared__ int s_pre[NET_CAP + 1];
@@ -1589,8 +1617,10 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     s_next[r][tid] = 0ull;
+    s_next2[r][tid] = 0ull;
     s_ahead[r][tid] = (on && a.steps > 0) ? __ldcg(a.ring + r * rring + i64(row) * a.ld + i) : 0ll;
   }
+  if (tid == 0) s_np = 0;
   unsigned long long* tm = a.timing ? a.timing + blockIdx.x * 4 : nullptr;
   for (i64 s = 0; s < a.steps; ++s) {
     const i64 t = a.t0 + s;
@@ -1604,7 +1634,8 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
     for (int r = 0; r < R; ++r) {
       arr[r] = (pair ? s_ahead[r][tid] : (on ? __ldcg(a.ring + r * rring + i64(row) * a.ld + i) : 0ll)) +
                (long long)s_next[r][tid];
-      s_next[r][tid] = 0ull;                        // (next written after this block's barriers)
+      s_next[r][tid] = s_next2[r][tid];             // step t - 1's delay-2 deliveries: row t + 1
+      s_next2[r][tid] = 0ull;                       // (both written after this block's barriers)
     }
     const int row1 = row + 1 == depth ? 0 : row + 1;
     NET_CHK(row >= 0 && row < depth && i64(row) == (t % a.depth));
@@ -1656,7 +1687,16 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
       __syncthreads();
       if (tid == 0) tm[s * nb * 4 + 1] = gtimer();
     }
-    grid_sync(a.bar, ++phase * nb);
+    grid_arrive(a.bar);
+    // between arrival and wait: the previous step's parked (delay >= 3) deliveries
+    {
+      const int np = min(s_np, NET_PEND);
+      for (int k = tid; k < np; k += NET_THREADS)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + s_poff[k]),
+                  (unsigned long long)(long long)s_pw[k]);
+    }
+    grid_wait(a.bar, ++phase * nb);
+    if (tid == 0) s_np = 0;                         // (read above, before grid_wait's bar.sync)
     if (tm && tid == 0) tm[s * nb * 4 + 2] = gtimer();
     // ---- delivery into this tile: list the spiking sources of every replica ...
     // this thread's (<= 8) words of every replica, loaded together (one L2 round trip)
@@ -1745,11 +1785,18 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
           const unsigned long long wq = (unsigned long long)(long long)wv[u];
           if (d[u] == 1) {
             atomicAdd(&s_next[R == 1 ? 0 : rr[u]][tg[u] - tlo], wq);
+          } else if (d[u] == 2) {
+            atomicAdd(&s_next2[R == 1 ? 0 : rr[u]][tg[u] - tlo], wq);
           } else {
             const int q = row + d[u] >= depth ? row + d[u] - depth : row + d[u];   // (t + d) % depth, d < depth
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + (R == 1 ? 0 : rr[u]) * rring + i64(q) * a.ld +
-                                                            tg[u]),
-                      wq);
+            const i64 off = (R == 1 ? 0 : rr[u]) * rring + i64(q) * a.ld + tg[u];
+            const int k = atomicAdd(&s_np, 1);
+            if (k < NET_PEND && off <= 0x7fffffffLL) {   // parked until the next barrier wait
+              s_poff[k] = int(off);
+              s_pw[k] = wv[u];
+            } else {
+              atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + off), wq);
+            }
           }
         }
       }
@@ -1759,11 +1806,19 @@ extern "C" __global__ void __launch_bounds__(NET_THREADS) hh_net(const NetArgs a
     row = row1;
   }
   __syncthreads();
+  {   // the last step's parked deliveries
+    const int np = min(s_np, NET_PEND);
+    for (int k = tid; k < np; k += NET_THREADS)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.ring + s_poff[k]), (unsigned long long)(long long)s_pw[k]);
+  }
+  __syncthreads();
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (on && a.steps > 0) {   // the last step's delay-1 deliveries back into the ring
+    if (on && a.steps > 0) {   // the last step's delay-1 and delay-2 deliveries back into the ring
       long long* slot = a.ring + r * rring + ((a.t0 + a.steps) % a.depth) * a.ld + i;
       *slot = *slot + (long long)s_next[r][tid];
+      long long* slot2 = a.ring + r * rring + ((a.t0 + a.steps + 1) % a.depth) * a.ld + i;
+      *slot2 = *slot2 + (long long)s_next2[r][tid];
     }
     if (on) {
       a.v[r * a.ld + i] = vv[r];
@@ -2465,8 +2520,8 @@ static Module* get_module(const hhb_params_t* P, int bwd_flags) {
   CUmodule mod;
   bool loaded = g_drv.load(&mod, cubin.data()) == CUDA_SUCCESS;
   if (loaded && bwd_flags <= kNet) {
-    // dynamic shared memory: s_next + s_ahead, 2 x replicas x 256 x 8 bytes
-    const int dyn = 2 * (kNet - bwd_flags + 1) * 256 * 8;
+    // dynamic shared memory: s_next + s_ahead + s_next2, 3 x replicas x 256 x 8 bytes
+    const int dyn = 3 * (kNet - bwd_flags + 1) * 256 * 8;
     loaded = g_drv.get(&m.net, mod, "hh_net") == CUDA_SUCCESS && g_drv.occupancy && g_drv.set_attr &&
              g_drv.set_attr(m.net, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, dyn) == CUDA_SUCCESS &&
              g_drv.occupancy(&m.net_blocks_per_sm, m.net, 256, size_t(dyn)) == CUDA_SUCCESS &&
