@@ -10,7 +10,24 @@ xb = torch.randn((M, K_in), device=dev).to(torch.bfloat16)
 wb = torch.randn((N_out, K_in), device=dev).to(torch.bfloat16)
 hi = torch.randn((M, N_out), device=dev).to(torch.bfloat16)
 lo = (torch.randn((M, N_out), device=dev) * 1e-3).to(torch.bfloat16)
+from paper_2601_21407_b200 import _native as nat
+from paper_2601_21407_b200.layer import _workspace
+x32 = torch.randn((M, K_in), device=dev)
+w32 = torch.randn((N_out, K_in), device=dev)
+out32 = torch.empty((M, N_out), device=dev)
+
+
+def tf32_fwd():
+    lib = nat.load()
+    ws_n = int(lib.hhb_gemm_workspace(M, N_out, 32))
+    ws = _workspace(ws_n, dev) if ws_n else None
+    nat.check(lib.hhb_gemm(1, M, N_out, K_in, x32.data_ptr(), K_in, w32.data_ptr(), K_in, None, out32.data_ptr(),
+                           N_out, 0, None if ws is None else ws.data_ptr(), torch.cuda.current_stream().cuda_stream),
+              "tf32")
+
+
 cases = {"fwd  I=X W^T": lambda: gemm_ex(0, M, N_out, K_in, xb, None, K_in, wb, K_in),
+         "fwd  tf32 (fp32 X, W read directly)": tf32_fwd,
          "dW = dI^T X ": lambda: gemm_ex(A_MN | B_MN, N_out, K_in, M, hi, lo, N_out, xb, K_in),
          "dX = dI W   ": lambda: gemm_ex(B_MN, M, K_in, N_out, hi, lo, N_out, wb, K_in)}
 for name, f in cases.items():
