@@ -429,7 +429,9 @@ def fwd_bwd_leg(torch, dev, proj="bf16", mufu_peak=None, cpu_seconds=0.0):
     out = {"value": B * N * T / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "eager_ms_per_step": eager_ms,
            "cuda_graph": graph is not None, "proj": proj,
            "config": f"BASELINE config 3: HH SNN layer 784->1024, batch 256, 100 steps, {proj} tcgen05 "
-                     "projection + fp32 HH forward + full-storage BPTT + bf16 hi/lo weight-gradient "
+                     + ("projection (fp32 x rounded and hi/lo-split on chip inside the GEMM) " if proj == "bf16x3"
+                        else "projection ") +
+                     "+ fp32 HH forward + full-storage BPTT + bf16 hi/lo weight-gradient "
                      "GEMM (x is the data: no input gradient, as the reference's first layer), "
                      "loss MSE(V, 0) fused into the HH kernels (layer.mse_loss; one unit = one "
                      "neuron-step through forward and backward)",

@@ -282,7 +282,13 @@ int64_t hhb_gemm_workspace(int64_t M, int64_t N, int32_t splits);
  * A/A2 the bf16 hi/lo halves of an fp32 operand the product carries ~16
  * mantissa bits of it.  So dW = dI^T X and dX = dI W read dI, X and W in
  * their natural row-major layouts, without transposed or split copies. */
-enum hhb_gemm_flags { HHB_GEMM_A_MN = 1, HHB_GEMM_B_MN = 2 };
+enum hhb_gemm_flags { HHB_GEMM_A_MN = 1, HHB_GEMM_B_MN = 2, HHB_GEMM_A_F32 = 4, HHB_GEMM_A_SPLIT = 8 };
+/* HHB_GEMM_A_F32: A is fp32 (K-major, lda in floats), rounded to bf16 on chip
+ * inside the GEMM (TMA -> converter warps -> tensor cores): D = bf16(A) . B^T
+ * (+ bias), bit-identical to casting A first; with HHB_GEMM_A_SPLIT, A2 is
+ * B_lo (bf16, B's layout) and D = A_hi.B + A_lo.B + A_hi.B_lo, A_hi/A_lo the
+ * bf16 hi/lo split of A (the fp32-class projection of DenseLayer, learn.py:
+ * 210-211, without the separate split pass).  K-major B, M >= 512. */
 int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
                 const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
                 float* workspace, void* stream);
@@ -294,6 +300,14 @@ int hhb_gemm_ex(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, c
 int hhb_gemm_ex2(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2, int64_t lda,
                  const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits,
                  float* workspace, int64_t k_switch, void* stream);
+/* The fp32-A GEMM of hhb_gemm_ex (HHB_GEMM_A_F32 [| HHB_GEMM_A_SPLIT with
+ * B_lo]) that also writes the operand it converted on chip: xs[m][k] = bf16
+ * hi of A, xs[m][xs_slot + k] = lo (B_lo given) -- the layer's weight gradient
+ * reads them, so the fp32-class projection needs no separate split pass.
+ * xs NULL: not written.  K, xs_ld, xs_slot multiples of 8. */
+int hhb_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const void* B, const void* B_lo,
+                  int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
+                  void* xs, int64_t xs_ld, int64_t xs_slot, void* stream);
 /* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16,
  * 3: fp32 -> bf16 hi at [c][r] and lo = x - hi at [c][rows + r] (bf16x2 split),
  * 4: bf16 -> bf16 written to [c][r] and [c][rows + r].  Kinds 3 + 4 turn a

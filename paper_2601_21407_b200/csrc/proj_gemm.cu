@@ -336,6 +336,10 @@ struct PArgs {
   uint32_t idesc;
   const float* bias;   // only when splits == 1
   int kb_switch;       // > 0 (K-major A, not DUAL): k-blocks >= kb_switch read A2 at k - kb_switch * 64
+  // fp32-A GEMM only: the on-chip bf16 conversion of A also written out (hi at
+  // xs[m][k], lo at xs[m][xs_slot + k]; null = not written)
+  uint16_t* xs;
+  int64_t xs_ld, xs_slot, K;
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
@@ -808,6 +812,281 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   }
 }
 
+// ---------------------------------------------------------------- fp32 A, converted on chip
+// CTA-pair GEMM whose A operand is fp32 in global memory (the layer input x):
+// TMA brings each CTA's 128 x 64 fp32 tile (two 128B-swizzled boxes of 32
+// columns) into shared memory, four converter warps round it to bf16 in place
+// (SPLIT: bf16 hi into the first half and lo = x - hi into the second), in the
+// K-major 128B-swizzled layout the MMA reads, and signal the pair leader; the
+// leader's MMAs are then those of the bf16 kernel (SPLIT: hi.B + lo.B + hi.B2,
+// B = W_hi, B2 = W_lo -- the fp32-class product of proj="bf16x3").  Replaces the
+// separate cast / split pass over x (read 4 B + write 2-6 B per element) by the
+// GEMM's own 4-byte read; the products and their order are those of the
+// unfused path, so D is bit-identical to it.
+template <int BN, bool SPLIT>
+struct PCvtCfg {
+  static constexpr uint32_t kStageF = BM * 64 * 4;           // 128 rows x 64 fp32 (-> bf16 hi [+ lo] in place)
+  static constexpr uint32_t kStageB = (BN / 2) * 128;        // half of B (and of B2)
+  static constexpr uint32_t kStage = kStageF + kStageB * (SPLIT ? 2 : 1);
+  static constexpr int kEpiWarps = EPI2_WARPS;
+  static constexpr int kCvtWarps = 4;
+  static constexpr int kThreads = 64 + 32 * (kEpiWarps + kCvtWarps);
+  static constexpr uint32_t kStaging = kEpiWarps * 32 * 32 * 4;
+  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 6 ? 6 : int((225 * 1024 - kStaging) / kStage);
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 512;
+};
+
+__device__ __forceinline__ void cvt_bar_sync() {   // the converter warps only (named barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * 4) : "memory");
+}
+
+template <int BN, bool SPLIT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::kThreads, 1)
+    k_umma_gemm_2sm_cvt(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                        const __grid_constant__ CUtensorMap tb2, const __grid_constant__ CUtensorMap td,
+                        const PArgs args) {
+  using C = PCvtCfg<BN, SPLIT>;
+  constexpr int ST = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sF = smem;                                   // [ST][kStageF]
+  uint8_t* sB = smem + ST * C::kStageF;                 // [ST][kStageB (x2 with SPLIT)]
+  constexpr uint32_t kBStride = C::kStageB * (SPLIT ? 2 : 1);
+  float* stg = reinterpret_cast<float*>(sB + ST * kBStride);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::kStaging);
+  uint64_t* afull = full + ST;
+  uint64_t* cfull = afull + ST;
+  uint64_t* empty = cfull + ST;
+  uint64_t* tfull = empty + ST;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    if (SPLIT) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&td)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 2);      // B: the leader's expect_tx + the peer's arrival
+      mbar_init(&afull[s], 1);     // this CTA's fp32 A tile
+      mbar_init(&cfull[s], 2);     // both CTAs' converted A tiles
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * C::kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(uint32_t(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+  pdl_wait();
+  pdl_trigger();
+  const int per_split = args.m_tiles * args.n_tiles;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr int kCvt0 = 2 + C::kEpiWarps;               // first converter warp
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own fp32 A rows, own half of B (and B2)
+      int it = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs) {
+        const int z = tile / per_split, r = tile % per_split;
+        const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+        const int64_t n0 = int64_t(r / args.m_tiles) * BN + int64_t(rank) * (BN / 2);
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          const int32_t kx = kb * 64;
+          uint8_t* f_dst = sF + s * C::kStageF;
+          mbar_expect_tx(&afull[s], C::kStageF);
+          tma_load_2d(&ta, &afull[s], f_dst, kx, int32_t(m0));
+          tma_load_2d(&ta, &afull[s], f_dst + C::kStageF / 2, kx + 32, int32_t(m0));
+          if (leader) mbar_expect_tx_only(&full[s], 2 * kBStride);
+          else mbar_arrive_leader(&full[s]);
+          uint8_t* b_dst = sB + s * kBStride;
+          tma_load_2d_2sm(&tb, &full[s], b_dst, kx, int32_t(n0));
+          if (SPLIT) tma_load_2d_2sm(&tb2, &full[s], b_dst + C::kStageB, kx, int32_t(n0));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer: the pair leader only
+      int it = 0, local = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+        const int z = tile / per_split;
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        const int b = local & 1;
+        mbar_wait(&tempty[b], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + uint32_t(b * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          mbar_wait(&cfull[s], (it / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* a_src = sF + s * C::kStageF;
+          const uint8_t* b_src = sB + s * kBStride;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = smem_desc(a_src + k * 32);
+            const uint64_t bd = smem_desc(b_src + k * 32);
+            umma2(acc, ad, bd, args.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (SPLIT) {
+              umma2(acc, smem_desc(a_src + C::kStageF / 2 + k * 32), bd, args.idesc, 1u);     // lo . W_hi
+              umma2(acc, ad, smem_desc(b_src + C::kStageB + k * 32), args.idesc, 1u);         // hi . W_lo
+            }
+          }
+          umma2_commit(&empty[s]);
+        }
+        umma2_commit(&tfull[b]);
+      }
+    }
+  } else if (warp >= kCvt0) {  // converter warps: fp32 tile -> bf16 (hi [, lo]) in place
+    const int ct = threadIdx.x - kCvt0 * 32;            // 0..127
+    int it = 0;
+    for (int tile = pair; tile < args.tiles; tile += npairs) {
+      const int z = tile / per_split, rt = tile % per_split;
+      const bool xs_out = args.xs != nullptr && rt / args.m_tiles == 0;
+      const int64_t xm0 = int64_t(rt % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int kb0 = z * args.kb_per_split;
+      const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % ST;
+        uint8_t* f = sF + s * C::kStageF;
+        mbar_wait(&afull[s], (it / ST) & 1);
+        // job q: row r = j / 8, 8-column chunk c = j % 8 (8 lanes per row: each
+        // quarter-warp reads one 128 B row of a swizzled box, conflict-free)
+        float x[8][8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = ct + 128 * q, r = j >> 3, c = j & 7;
+          const uint8_t* box = f + (c >> 2) * (C::kStageF / 2) + r * 128;
+          const int j0 = (2 * (c & 3)) ^ (r & 7), j1 = (2 * (c & 3) + 1) ^ (r & 7);
+          const float4 u = *reinterpret_cast<const float4*>(box + j0 * 16);
+          const float4 w = *reinterpret_cast<const float4*>(box + j1 * 16);
+          x[q][0] = u.x; x[q][1] = u.y; x[q][2] = u.z; x[q][3] = u.w;
+          x[q][4] = w.x; x[q][5] = w.y; x[q][6] = w.z; x[q][7] = w.w;
+        }
+        cvt_bar_sync();                                  // every fp32 value read before the tile is overwritten
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = ct + 128 * q, r = j >> 3, c = j & 7;
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(x[q][2 * e], x[q][2 * e + 1]);
+            h[e] = *reinterpret_cast<const uint32_t*>(&hb);
+            if (SPLIT) {
+              const float2 hf = __bfloat1622float2(hb);
+              const __nv_bfloat162 lb =
+                  __floats2bfloat162_rn(__fsub_rn(x[q][2 * e], hf.x), __fsub_rn(x[q][2 * e + 1], hf.y));
+              l[e] = *reinterpret_cast<const uint32_t*>(&lb);
+            }
+          }
+          const int off = r * 128 + ((c ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(f + off) = make_uint4(h[0], h[1], h[2], h[3]);
+          if (SPLIT) *reinterpret_cast<uint4*>(f + C::kStageF / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+          if (xs_out) {   // the converted operand for the layer's weight gradient (first column tile only)
+            const int64_t gk = int64_t(kb) * 64 + 8 * c, gm = xm0 + r;
+            if (gm < args.M && gk < args.K) {
+              uint16_t* d = args.xs + gm * args.xs_ld + gk;
+              *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+              if (SPLIT) *reinterpret_cast<uint4*>(d + args.xs_slot) = make_uint4(l[0], l[1], l[2], l[3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> the MMA's async reads
+        cvt_bar_sync();
+        if (ct == 0) mbar_arrive_leader(&cfull[s]);
+      }
+    }
+  } else {  // epilogue warps of both CTAs (as k_umma_gemm_2sm)
+    const int q = warp & 3;
+    const int half = C::kEpiWarps == 8 ? (warp - 2) >> 2 : 0;
+    constexpr int kCols = C::kEpiWarps == 8 ? BN / 2 : BN;
+    float* my_stg = stg + (warp - 2) * 1024;
+    int local = 0;
+    for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+      const int z = tile / per_split, r = tile % per_split;
+      const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int64_t n0 = int64_t(r / args.m_tiles) * BN;
+      const int kb0 = z * args.kb_per_split;
+      const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
+      const int b = local & 1;
+      mbar_wait(&tfull[b], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int32_t row0 = int32_t(m0 + q * 32);
+#pragma unroll 1
+      for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
+        if (n0 + c0 >= args.N) break;
+        uint32_t rr[32];
+        if (any_k) {
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(b * BN + c0), rr);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = 0u;
+        }
+        float* buf = my_stg;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        const bool bvec = args.bias != nullptr && n0 + c0 + 32 <= args.N &&
+                          (reinterpret_cast<uintptr_t>(args.bias + n0 + c0) & 15) == 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o;
+          const int64_t cb = n0 + c0 + 4 * j;
+          o.x = __uint_as_float(rr[4 * j + 0]);
+          o.y = __uint_as_float(rr[4 * j + 1]);
+          o.z = __uint_as_float(rr[4 * j + 2]);
+          o.w = __uint_as_float(rr[4 * j + 3]);
+          if (bvec) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(args.bias + cb));
+            o.x += bb.x;
+            o.y += bb.y;
+            o.z += bb.z;
+            o.w += bb.w;
+          } else if (args.bias != nullptr) {
+            o.x += cb + 0 < args.N ? __ldg(args.bias + cb + 0) : 0.f;
+            o.y += cb + 1 < args.N ? __ldg(args.bias + cb + 1) : 0.f;
+            o.z += cb + 2 < args.N ? __ldg(args.bias + cb + 2) : 0.f;
+            o.w += cb + 3 < args.N ? __ldg(args.bias + cb + 3) : 0.f;
+          }
+          *reinterpret_cast<float4*>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&td, buf, int32_t(n0 + c0), row0, z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[b]);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(2 * BN)));
+  }
+}
+
 // fixed-order split-K reduction (+ bias)
 __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits, int64_t split_stride,
                               const float* bias, float* D, int64_t ldd) {
@@ -1189,6 +1468,43 @@ static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUten
   return cuda_check("k_umma_gemm_2sm launch");
 }
 
+template <int BN, bool SPLIT>
+static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
+                          const CUtensorMap& td, const PArgs& a, cudaStream_t st) {
+  using C = PCvtCfg<BN, SPLIT>;
+  const size_t smem = C::kSmem;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_umma_gemm_2sm_cvt<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem));
+  });
+  if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed (cvt)");
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+    cfg.blockDim = dim3(C::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_umma_gemm_2sm_cvt<BN, SPLIT>, &cfg) != cudaSuccess || n <= 0)
+      n = num_sms() / 2;
+    (void)cudaGetLastError();
+    max_pairs = n;
+  }
+  int pairs = max_pairs;
+  if (a.tiles < pairs) pairs = a.tiles;
+  launch_pdl(k_umma_gemm_2sm_cvt<BN, SPLIT>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, tb, tb2, td, a);
+  return cuda_check("k_umma_gemm_2sm_cvt launch");
+}
+
 static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false, int m = BM) {
   const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
@@ -1257,6 +1573,9 @@ int hhb_gemm(int32_t in_kind, int64_t M, int64_t N, int64_t K, const void* A, in
   return cuda_check("k_gemm_reduce launch");
 }
 
+static int gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const void* B, const void* Blo,
+                     int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
+                     void* stream, void* xs = nullptr, int64_t xs_ld = 0, int64_t xs_slot = 0);
 static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2,
                         int64_t lda, const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
                         int32_t splits, float* workspace, int64_t k_switch, void* stream);
@@ -1273,11 +1592,100 @@ int hhb_gemm_ex2(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, 
   return gemm_ex_impl(flags, M, N, K, A, A2, lda, B, ldb, bias, D, ldd, splits, workspace, k_switch, stream);
 }
 
+int hhb_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const void* B, const void* B_lo,
+                  int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
+                  void* xs, int64_t xs_ld, int64_t xs_slot, void* stream) {
+  return gemm_f32a(M, N, K, A, lda, B, B_lo, ldb, bias, D, ldd, splits, workspace, stream, xs, xs_ld, xs_slot);
+}
+
+// fp32-A CTA-pair GEMM (k_umma_gemm_2sm_cvt): D = bf16(A) . B^T, or with B_lo
+// the three-product hi.B + lo.B + hi.B_lo of proj="bf16x3"; 2-SM tiles only
+static int gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const void* B, const void* Blo,
+                     int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
+                     void* stream, void* xs, int64_t xs_ld, int64_t xs_slot) {
+  using namespace hhb::gemm;
+  if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
+  if (M == 0 || N == 0) return HHB_OK;
+  if ((lda * 4) % 16 || (ldb * 2) % 16 || reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16 ||
+      reinterpret_cast<uintptr_t>(Blo) % 16)
+    return fail(HHB_EINVAL, "gemm operands need 16-byte aligned base and row pitch");
+  if (lda < K || ldb < K) return fail(HHB_EINVAL, "lda/ldb too small");
+  const int bn = N <= 128 ? 128 : 256;
+  if (M < 512) return fail(HHB_EINVAL, "fp32-A GEMM needs M >= 512 (CTA-pair tiles)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int kb_total = int((K + 63) / 64);
+  if (splits < 1) {   // the bf16 path's time model (CTA pairs), the three-product form counted 3x
+    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
+    const int64_t P = num_sms() / 2;
+    const double t_kb = 0.28 * (Blo ? 3.0 : 1.0) * (double(bn) / 256.0);
+    const double t_mn = double(M) * double(N) * 4.0 / 5e12 * 1e6;
+    double best = 1e300;
+    splits = 1;
+    for (int sp = 1; sp <= (kb_total >= 8 ? kb_total / 4 : 1) && sp <= 32; ++sp) {
+      const int64_t units = tiles * sp;
+      const double cost = double((units + P - 1) / P) * double((kb_total + sp - 1) / sp) * t_kb +
+                          (sp > 1 ? double(2 * sp + 1) * t_mn : 0.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = sp;
+      }
+    }
+  }
+  if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
+  if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
+  float* dst = splits > 1 ? workspace : D;
+  const int64_t dld = splits > 1 ? N : ldd;
+  if (dld % 4 != 0 || reinterpret_cast<uintptr_t>(dst) % 16 != 0)
+    return fail(HHB_EINVAL, "fp32-A GEMM needs a 16-byte aligned output pitch");
+  CUtensorMap ta, tb, tb2, td;
+  int rc = make_map(&ta, true, A, M, K, lda, BM);
+  if (rc) return rc;
+  if ((rc = make_map(&tb, false, B, N, K, ldb, bn / 2))) return rc;
+  if (Blo && (rc = make_map(&tb2, false, Blo, N, K, ldb, bn / 2))) return rc;
+  if (!Blo) tb2 = tb;
+  if ((rc = make_map_d(&td, dst, M, N, dld, splits))) return rc;
+  PArgs pa{};
+  pa.M = M;
+  pa.N = N;
+  pa.m_tiles = int((M + 2 * BM - 1) / (2 * BM));
+  pa.n_tiles = int((N + bn - 1) / bn);
+  pa.kb_total = kb_total;
+  pa.kb_per_split = (kb_total + splits - 1) / splits;
+  pa.splits = splits;
+  pa.tiles = pa.m_tiles * pa.n_tiles * splits;
+  pa.idesc = instr_desc(false, bn, false, false, 2 * BM);
+  pa.bias = splits > 1 ? nullptr : bias;
+  pa.kb_switch = 0;
+  pa.K = K;
+  if (xs) {
+    if (K % 8 || xs_ld % 8 || xs_slot % 8 || reinterpret_cast<uintptr_t>(xs) % 16 || xs_ld < (Blo ? xs_slot + K : K) ||
+        (Blo && xs_slot < K))
+      return fail(HHB_EINVAL, "converted-operand output: K, pitch and slot multiples of 8, 16-byte aligned");
+    pa.xs = static_cast<uint16_t*>(xs);
+    pa.xs_ld = xs_ld;
+    pa.xs_slot = xs_slot;
+  }
+  if (Blo) rc = bn == 128 ? launch_2sm_cvt<128, true>(ta, tb, tb2, td, pa, st) : launch_2sm_cvt<256, true>(ta, tb, tb2, td, pa, st);
+  else rc = bn == 128 ? launch_2sm_cvt<128, false>(ta, tb, tb2, td, pa, st) : launch_2sm_cvt<256, false>(ta, tb, tb2, td, pa, st);
+  if (rc || splits == 1) return rc;
+  launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits,
+             int64_t(M * N), bias, D, ldd);
+  return cuda_check("k_gemm_reduce launch");
+}
+
 static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, const void* A2,
                         int64_t lda, const void* B, int64_t ldb, const float* bias, float* D, int64_t ldd,
                         int32_t splits, float* workspace, int64_t k_switch, void* stream) {
   using namespace hhb::gemm;
   const bool a_mn = flags & HHB_GEMM_A_MN, b_mn = flags & HHB_GEMM_B_MN;
+  // fp32 A converted on chip (HHB_GEMM_A_F32; + HHB_GEMM_A_SPLIT: hi/lo with A2 = B_lo)
+  const bool a_f32 = flags & HHB_GEMM_A_F32, a_split = flags & HHB_GEMM_A_SPLIT;
+  if (a_f32 || a_split) {
+    if (!a_f32 || a_mn || b_mn || k_switch > 0 || (a_split != (A2 != nullptr)))
+      return fail(HHB_EINVAL, "fp32-A GEMM: K-major A and B, no k_switch, A2 (= B_lo) iff HHB_GEMM_A_SPLIT");
+    return gemm_f32a(M, N, K, static_cast<const float*>(A), lda, B, a_split ? A2 : nullptr, ldb, bias, D, ldd,
+                     splits, workspace, stream);
+  }
   // k_switch > 0: A2 is not a second addend but the A source for k >= k_switch
   // (K-concatenation of two K-major operands, e.g. [dI_hi | dI_lo] then dI_hi)
   const bool dual = A2 != nullptr && k_switch <= 0;

@@ -238,7 +238,7 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
             raise GradientOverflowError("adjoint state became non-finite", b)
     layer.param_grads = d_params                       # {d_c_m, d_g_max[...]} (fp64, device)
     x3 = layer.proj == "bf16x3"
-    kp = xb.shape[1] // 3 if x3 else 0      # slot width of the [x_hi | x_lo | x_hi] rows
+    kp = _pad8(k_in) if x3 else 0           # slot width of the [x_hi | x_lo (| x_hi)] rows
 
     def weight_grad():
         # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views;
@@ -312,16 +312,30 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[key]
 
 
+def _fused_split(x, layer) -> bool:
+    """bf16x3 projection with x converted and split on chip (hhb_gemm_f32a):
+    CTA-pair tiles (>= 512 rows) and 8-aligned k_in."""
+    import os
+    T, B, k_in = x.shape
+    return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0
+            and os.environ.get("HHB_LAYER_FUSED_SPLIT", "1") != "0")
+
+
 def _operands(x, weight, layer):
     """bf16 GEMM operands of the projection: (xb, wb_proj, wb_grad, K) --
     wb_grad is the input gradient's B operand (the stacked [W_hi; W_hi; W_lo]
-    for bf16x3, W itself for bf16)."""
+    for bf16x3, W itself for bf16).  Fused bf16x3 (_fused_split): xb is the
+    empty [x_hi | x_lo] buffer the projection GEMM fills while it converts x."""
     T, B, k_in = x.shape
     if layer.proj == "bf16x3":
         # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
         n_out = weight.shape[0]
         with _timed("operand_prep", T * B * k_in):
-            xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
+            if _fused_split(x, layer):
+                kp = _pad8(k_in)
+                xb = torch.empty((T * B, 2 * kp), dtype=torch.bfloat16, device=x.device)
+            else:
+                xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
             wb, _ = split3_padded(weight.float().contiguous(), 1)
             # the input gradient's B operand: rows [W_hi; W_hi; W_lo], each block
             # n_out rows padded to P (MN-major over the reduction index j)
@@ -382,9 +396,27 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
     b32 = bias.float().contiguous()
     cur = torch.empty((T * B, n_out), dtype=torch.float32, device=x.device)
     chunks = _time_chunks(T, K, T * B * n_out)
+    x32 = x.reshape(T * B, k_in).float().contiguous() if _fused_split(x, layer) else None
+
+    def project(r0, r1):
+        if x32 is None:
+            gemm(xb[r0:r1], wb, kk, bias=b32, out=cur[r0:r1])
+            return
+        # fp32 x rounded and split on chip; the GEMM also writes x_hi / x_lo
+        # into xb for the weight gradient (B = W_hi, B_lo = W_lo: slots 0 / 2 of wb)
+        lib = nat.load()
+        M = r1 - r0
+        kp = xb.shape[1] // 2
+        ws_n = int(lib.hhb_gemm_workspace(M, n_out, 32))
+        ws = _workspace(ws_n, x.device) if ws_n else None
+        nat.check(lib.hhb_gemm_f32a(M, n_out, k_in, x32[r0:].data_ptr(), k_in, wb.data_ptr(),
+                                    wb[:, 2 * kp:].data_ptr(), wb.stride(0), b32.data_ptr(), cur[r0:].data_ptr(),
+                                    n_out, 0, D.ptr(ws), xb[r0:].data_ptr(), xb.stride(0), kp, _stream()),
+                  "hhb_gemm_f32a")
+
     if len(chunks) == 1:
         with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
-            gemm(xb, wb, kk, bias=b32, out=cur)
+            project(0, T * B)
         run_forward(cur, 0, T)
         return xb, wg, cur
     main = torch.cuda.current_stream(x.device)
@@ -396,11 +428,11 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
     with torch.cuda.stream(side):
         for t0, t1 in chunks:
             with _timed("proj_gemm", 2.0 * (t1 - t0) * B * k_in * n_out):
-                gemm(xb[t0 * B:t1 * B], wb, kk, bias=b32, out=cur[t0 * B:t1 * B])
+                project(t0 * B, t1 * B)
             ev = torch.cuda.Event()
             ev.record(side)
             evs.append(ev)
-    for t in (xb, wb, b32, cur):
+    for t in (xb, wb, b32, cur) + (() if x32 is None else (x32,)):
         t.record_stream(side)
     for (t0, t1), ev in zip(chunks, evs):
         main.wait_event(ev)

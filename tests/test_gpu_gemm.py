@@ -202,3 +202,42 @@ def test_split3_stacked_rows(cuda):
         assert torch.equal(out[:rows, :cols], hi) and torch.equal(out[P:P + rows, :cols], hi)
         assert torch.equal(out[2 * P:2 * P + rows, :cols], lo)
         assert not out[rows:P].float().any() and not out[:, cols:].float().any()
+
+
+@pytest.mark.parametrize("M,N,K,bias,splits", [(512, 256, 784, False, 0), (1000, 300, 96, True, 0),
+                                               (25600, 1024, 784, True, 0), (4096, 784, 784, False, 0),
+                                               (512, 256, 8192, False, 4), (2048, 2048, 2048, True, 0)])
+def test_fp32_a_gemm_converts_on_chip(cuda, M, N, K, bias, splits):
+    """hhb_gemm_f32a / HHB_GEMM_A_F32: fp32 x rounded to bf16 inside the GEMM
+    gives the cast-then-GEMM result bit for bit; with B_lo it is the fp32-class
+    three-product form (hi.W_hi + lo.W_hi + hi.W_lo) within the error of the
+    unfused one against float64, and the hi / lo operand it writes out equals
+    the split pass's (hhb_split3_bf16) slots."""
+    from paper_2601_21407_b200.layer import _stream, _workspace, gemm, split3_padded, to_bf16_padded
+    lib = nat.load()
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    x = torch.randn((M, K), device=cuda, generator=g)
+    w = torch.randn((N, K), device=cuda, generator=g) * 0.05
+    b = torch.randn(N, device=cuda, generator=g) if bias else None
+    ws = _workspace(int(lib.hhb_gemm_workspace(M, N, max(splits, 32))), cuda)
+    wb = to_bf16_padded(w)
+
+    def f32a(B, Blo, ldb, xs=None, xs_ld=0, slot=0):
+        out = torch.empty((M, N), device=cuda)
+        nat.check(lib.hhb_gemm_f32a(M, N, K, x.data_ptr(), K, B.data_ptr(), None if Blo is None else Blo.data_ptr(),
+                                    ldb, None if b is None else b.data_ptr(), out.data_ptr(), N, splits,
+                                    ws.data_ptr(), None if xs is None else xs.data_ptr(), xs_ld, slot, _stream()),
+                  "f32a")
+        return out
+
+    ref = gemm(to_bf16_padded(x), wb, K, bias=b, splits=splits if splits > 0 else None)
+    assert torch.equal(f32a(wb, None, wb.stride(0)), ref)
+    w3, kp = split3_padded(w, 1)                      # [W_hi | W_hi | W_lo]
+    xs = torch.zeros((M, 2 * kp), dtype=torch.bfloat16, device=cuda)
+    got3 = f32a(w3, w3[:, 2 * kp:], w3.stride(0), xs, xs.stride(0), kp)
+    xb3, _ = split3_padded(x, 0)                      # [x_hi | x_lo | x_hi]
+    ref3 = gemm(xb3, w3, 3 * kp, bias=b)
+    exact = x.double() @ w.double().T + (b.double() if b is not None else 0)
+    scale = exact.abs().max()
+    assert (got3.double() - exact).abs().max() / scale < 4 * (ref3.double() - exact).abs().max() / scale + 1e-6
+    assert torch.equal(xs[:, :K], xb3[:, :K]) and torch.equal(xs[:, kp:kp + K], xb3[:, kp:kp + K])
