@@ -337,6 +337,8 @@ def _operands(x, weight, layer):
             else:
                 xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
             wb, _ = split3_padded(weight.float().contiguous(), 1)
+            if not x.requires_grad:
+                return xb, wb, wb, 3 * kp        # no input gradient: its stacked operand is not built
             # the input gradient's B operand: rows [W_hi; W_hi; W_lo], each block
             # n_out rows padded to P (MN-major over the reduction index j)
             P = _pad8(n_out)
