@@ -257,12 +257,25 @@ class DenseLayer:
         if xd.dtype == torch.float32:
             # float32 device operands: the tcgen05 GEMM in its fp32-class bf16x3
             # form (x and W split into bf16 hi + lo, three tensor-core products)
-            from .layer import gemm, split3_padded
+            from .layer import _stream, _workspace, gemm, split3_padded
+            from . import _native as nat
             k = xd.shape[-1]
             x2 = xd.reshape(-1, k).contiguous()
-            xa, kp = split3_padded(x2, 0)
-            wa, _ = split3_padded(_dev(self.weights).float().reshape(-1, k).contiguous(), 1)
-            y = gemm(xa, wa, 3 * kp, bias=_dev(self.bias).float().contiguous())
+            wa, kp = split3_padded(_dev(self.weights).float().reshape(-1, k).contiguous(), 1)   # [W_hi|W_hi|W_lo]
+            b32 = _dev(self.bias).float().contiguous()
+            M, N = x2.shape[0], wa.shape[0]
+            if M >= 512 and k % 4 == 0:
+                # x split into hi / lo on chip inside the GEMM (hhb_gemm_f32a)
+                lib = nat.load()
+                y = torch.empty((M, N), dtype=torch.float32, device=x2.device)
+                ws_n = int(lib.hhb_gemm_workspace(M, N, 32))
+                ws = _workspace(ws_n, x2.device) if ws_n else None
+                nat.check(lib.hhb_gemm_f32a(M, N, k, x2.data_ptr(), k, wa.data_ptr(), wa[:, 2 * kp:].data_ptr(),
+                                            wa.stride(0), b32.data_ptr(), y.data_ptr(), N, 0, D.ptr(ws), None, 0, 0,
+                                            _stream()), "DenseLayer")
+            else:
+                xa, _ = split3_padded(x2, 0)
+                y = gemm(xa, wa, 3 * kp, bias=b32)
             y = y.reshape(*xd.shape[:-1], y.shape[-1])
         else:
             # float64 (the reference's own precision, learn.py:210-211): a plain

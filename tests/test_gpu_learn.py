@@ -248,18 +248,20 @@ def test_dense_layer_float32_runs_on_the_tcgen05_gemm(cuda):
     import torch
     from paper_2601_21407_b200 import learn as L
     rng = np.random.default_rng(0)
-    layer = L.DenseLayer(rng.normal(0.05, 0.1, (96, 37)), rng.normal(0, 1, 96))
-    x = rng.normal(0.5, 1.0, (10, 4, 37))
-    ref = x @ layer.weights.T + layer.bias
-    got = layer(torch.tensor(x, dtype=torch.float32, device=cuda))
-    assert got.dtype == torch.float32 and tuple(got.shape) == (10, 4, 96)
-    xr = torch.tensor(x, dtype=torch.float32).double().numpy()        # the float32 x exactly
-    wr = torch.tensor(layer.weights, dtype=torch.float32).double().numpy()
-    br = torch.tensor(layer.bias, dtype=torch.float32).double().numpy()
-    ref32 = xr @ wr.T + br
-    scale = np.abs(xr) @ np.abs(wr).T + np.abs(br)
-    assert np.max(np.abs(got.cpu().numpy() - ref32) / scale) < 4e-5    # hi/lo residuals: <= 2 x 2^-16
-    assert np.allclose(got.cpu().numpy(), ref, rtol=1e-3, atol=1e-3)
+    # (10, 4, 37): the split pass + GEMM; (64, 16, 784): >= 512 rows, x split on chip (hhb_gemm_f32a)
+    for shape, n_out in (((10, 4, 37), 96), ((64, 16, 784), 300)):
+        layer = L.DenseLayer(rng.normal(0.05, 0.1, (n_out, shape[-1])), rng.normal(0, 1, n_out))
+        x = rng.normal(0.5, 1.0, shape)
+        ref = x @ layer.weights.T + layer.bias
+        got = layer(torch.tensor(x, dtype=torch.float32, device=cuda))
+        assert got.dtype == torch.float32 and tuple(got.shape) == shape[:-1] + (n_out,)
+        xr = torch.tensor(x, dtype=torch.float32).double().numpy()        # the float32 x exactly
+        wr = torch.tensor(layer.weights, dtype=torch.float32).double().numpy()
+        br = torch.tensor(layer.bias, dtype=torch.float32).double().numpy()
+        ref32 = xr @ wr.T + br
+        scale = np.abs(xr) @ np.abs(wr).T + np.abs(br)
+        assert np.max(np.abs(got.cpu().numpy() - ref32) / scale) < 4e-5    # hi/lo residuals: <= 2 x 2^-16
+        assert np.allclose(got.cpu().numpy(), ref, rtol=1e-3, atol=1e-3)
     # numpy in -> numpy out, float64 (the reference's precision)
     out = layer(x)
     assert isinstance(out, np.ndarray) and np.allclose(out, ref, rtol=1e-12, atol=1e-12)
