@@ -62,11 +62,11 @@ def test_paired_adjoint_step_matches_scalar(cuda, env):
     assert abs(got.d_c_m - ref.d_c_m) <= 1e-4 * abs(ref.d_c_m) + 1e-12
 
 
-def _layer_grads(cuda, chunks, env):
+def _layer_grads(cuda, chunks, env, proj="bf16"):
     from paper_2601_21407_b200.layer import HHLayer
     env.setenv("HHB_LAYER_CHUNKS", str(chunks))
     torch.manual_seed(0)
-    layer = HHLayer(784, 1024, w_mean=0.05, w_std=0.1, device=cuda)
+    layer = HHLayer(784, 1024, w_mean=0.05, w_std=0.1, device=cuda, proj=proj)
     g = torch.Generator(device=cuda).manual_seed(0)
     x = ((torch.rand((100, 256, 784), device=cuda, generator=g) < 0.2).float()
          + 0.1 * torch.randn((100, 256, 784), device=cuda, generator=g))
@@ -76,9 +76,11 @@ def _layer_grads(cuda, chunks, env):
     return float(loss.detach()), layer.weight.grad.clone(), layer.bias.grad.clone()
 
 
-def test_time_chunked_layer_pipeline_matches(cuda, env):
-    l1, w1, b1 = _layer_grads(cuda, 1, env)
-    l4, w4, b4 = _layer_grads(cuda, 4, env)
+@pytest.mark.parametrize("proj", ["bf16", "bf16x3"])
+def test_time_chunked_layer_pipeline_matches(cuda, env, proj):
+    # bf16x3: the on-chip split GEMM (hhb_gemm_f32a) on row chunks of x
+    l1, w1, b1 = _layer_grads(cuda, 1, env, proj)
+    l4, w4, b4 = _layer_grads(cuda, 4, env, proj)
     # the forward states are the same launches' states, chunk by chunk: the
     # gradients are identical; the loss's fp64 partial sums regroup per chunk
     assert torch.equal(w1, w4) and torch.equal(b1, b4)
