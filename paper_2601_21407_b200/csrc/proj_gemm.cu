@@ -892,6 +892,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
   const uint32_t tmem = *tmem_holder;
   pdl_wait();
   pdl_trigger();
+  // tile order: column tiles fastest -- the pairs on one 256-row block of x run
+  // together, so its fp32 tile comes from HBM once and from L2 for the others
   const int per_split = args.m_tiles * args.n_tiles;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   constexpr int kCvt0 = 2 + C::kEpiWarps;               // first converter warp
@@ -901,8 +903,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
       int it = 0;
       for (int tile = pair; tile < args.tiles; tile += npairs) {
         const int z = tile / per_split, r = tile % per_split;
-        const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
-        const int64_t n0 = int64_t(r / args.m_tiles) * BN + int64_t(rank) * (BN / 2);
+        const int64_t m0 = int64_t(r / args.n_tiles) * (2 * BM) + int64_t(rank) * BM;
+        const int64_t n0 = int64_t(r % args.n_tiles) * BN + int64_t(rank) * (BN / 2);
         const int kb0 = z * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -959,8 +961,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
     int it = 0;
     for (int tile = pair; tile < args.tiles; tile += npairs) {
       const int z = tile / per_split, rt = tile % per_split;
-      const bool xs_out = args.xs != nullptr && rt / args.m_tiles == 0;
-      const int64_t xm0 = int64_t(rt % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const bool xs_out = args.xs != nullptr && rt % args.n_tiles == 0;
+      const int64_t xm0 = int64_t(rt / args.n_tiles) * (2 * BM) + int64_t(rank) * BM;
       const int kb0 = z * args.kb_per_split;
       const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -1021,8 +1023,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
     int local = 0;
     for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
       const int z = tile / per_split, r = tile % per_split;
-      const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
-      const int64_t n0 = int64_t(r / args.m_tiles) * BN;
+      const int64_t m0 = int64_t(r / args.n_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int64_t n0 = int64_t(r % args.n_tiles) * BN;
       const int kb0 = z * args.kb_per_split;
       const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
       const int b = local & 1;
