@@ -340,6 +340,7 @@ struct PArgs {
   // xs[m][k], lo at xs[m][xs_slot + k]; null = not written)
   uint16_t* xs;
   int64_t xs_ld, xs_slot, K;
+  int n_fast;          // tile order: 1 = column tiles fastest (pairs on one row block run together), 0 = rows fastest
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
@@ -403,7 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
         const int z = tile / per_split, r = tile % per_split;
-        const int64_t m0 = int64_t(r % args.m_tiles) * BM, n0 = int64_t(r / args.m_tiles) * BN;
+        const int64_t m0 = int64_t(args.n_fast ? r / args.n_tiles : r % args.m_tiles) * BM;
+        const int64_t n0 = int64_t(args.n_fast ? r % args.n_tiles : r / args.m_tiles) * BN;
         const int kb0 = z * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -473,7 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0, nstore = 0;
     for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x, ++local) {
       const int z = tile / per_split, r = tile % per_split;
-      const int64_t m0 = int64_t(r % args.m_tiles) * BM, n0 = int64_t(r / args.m_tiles) * BN;
+      const int64_t m0 = int64_t(args.n_fast ? r / args.n_tiles : r % args.m_tiles) * BM;
+      const int64_t n0 = int64_t(args.n_fast ? r % args.n_tiles : r / args.m_tiles) * BN;
       const int kb0 = z * args.kb_per_split;
       const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
       const int b = local & 1;
@@ -668,8 +671,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       int it = 0;
       for (int tile = pair; tile < args.tiles; tile += npairs) {
         const int z = tile / per_split, r = tile % per_split;
-        const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
-        const int64_t n0 = int64_t(r / args.m_tiles) * BN + int64_t(rank) * (BN / 2);
+        const int64_t m0 = int64_t(args.n_fast ? r / args.n_tiles : r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+        const int64_t n0 = int64_t(args.n_fast ? r % args.n_tiles : r / args.m_tiles) * BN + int64_t(rank) * (BN / 2);
         const int kb0 = z * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -742,8 +745,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     int local = 0, nstore = 0;
     for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
       const int z = tile / per_split, r = tile % per_split;
-      const int64_t m0 = int64_t(r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
-      const int64_t n0 = int64_t(r / args.m_tiles) * BN;
+      const int64_t m0 = int64_t(args.n_fast ? r / args.n_tiles : r % args.m_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int64_t n0 = int64_t(args.n_fast ? r % args.n_tiles : r / args.m_tiles) * BN;
       const int kb0 = z * args.kb_per_split;
       const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
       const int b = local & 1;
@@ -1507,6 +1510,15 @@ static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   return cuda_check("k_umma_gemm_2sm_cvt launch");
 }
 
+// tile order of the persistent GEMMs: column tiles fastest unless HHB_GEMM_RASTER=m
+static int gemm_n_fast() {
+  static const int v = [] {
+    const char* e = getenv("HHB_GEMM_RASTER");
+    return (e && e[0] == 'm') ? 0 : 1;
+  }();
+  return v;
+}
+
 static uint32_t instr_desc(bool tf32, int bn, bool a_mn = false, bool b_mn = false, int m = BM) {
   const uint32_t fmt = tf32 ? 2u : 1u;  // TF32 : BF16
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
@@ -1658,6 +1670,7 @@ static int gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
   pa.idesc = instr_desc(false, bn, false, false, 2 * BM);
   pa.bias = splits > 1 ? nullptr : bias;
   pa.kb_switch = 0;
+  pa.n_fast = gemm_n_fast();
   pa.K = K;
   if (xs) {
     if (K % 8 || xs_ld % 8 || xs_slot % 8 || reinterpret_cast<uintptr_t>(xs) % 16 || xs_ld < (Blo ? xs_slot + K : K) ||
@@ -1770,6 +1783,7 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
       pa.idesc = instr_desc(false, bn, a_mn, b_mn, 2 * BM);
       pa.bias = splits > 1 ? nullptr : bias;
       pa.kb_switch = k_switch > 0 ? int(k_switch / 64) : 0;
+      pa.n_fast = gemm_n_fast();
 #define HHB_GEMM_2CASE(AM, BMN, DU)                                                              \
   if (a_mn == AM && b_mn == BMN && dual == DU)                                                   \
     rc = bn == 128 ? launch_2sm<128, AM, BMN, DU>(ta, ta2, tb2, td, pa, st)                      \
@@ -1799,6 +1813,7 @@ static int gemm_ex_impl(int32_t flags, int64_t M, int64_t N, int64_t K, const vo
     pa.idesc = instr_desc(false, bn, a_mn, b_mn);
     pa.bias = splits > 1 ? nullptr : bias;
     pa.kb_switch = k_switch > 0 ? int(k_switch / 64) : 0;
+    pa.n_fast = gemm_n_fast();
 #define HHB_GEMM_PCASE(AM, BMN, DU)                                   \
   if (a_mn == AM && b_mn == BMN && dual == DU)                        \
     rc = launch_p_bn<AM, BMN, DU>(bn, ta, ta2, tb, td, pa, st);
