@@ -115,7 +115,7 @@ def layer_kernels(torch, step, reps=7):
 TAU_RS_F, TAU_RS_B = 16, 18
 
 
-def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True):
+def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True, proj_products=1):
     """Roofline of an HH-layer training step: the dominant kernel (the BPTT
     kernel hh_bwd2) against the live MUFU peak, with the forward kernel and the
     projection GEMM beside it (GEMM against MEASURED_PEAKS bf16_tflops)."""
@@ -156,9 +156,14 @@ def layer_roofline(nat, params, kern, step_ms, mufu_peak, dual_grads=True):
                                             "xu_pipe_pct", "fma_pipe_pct", "source") if k in prof}
     if g.get("units_per_s"):
         pk = peaks.get("bf16_tflops", 1648.7)
-        roof["gemm"] = {"kernel": "k_umma_gemm_2sm (tcgen05 cta_group::2, projection x W^T)",
-                        "achieved_tflops": g["units_per_s"] / 1e12, "peak_tflops": pk,
-                        "frac": g["units_per_s"] / 1e12 / pk,
+        # tensor work issued: the bf16x3 projection runs three products per
+        # algorithmic MAC (x_hi.W_hi + x_lo.W_hi + x_hi.W_lo)
+        roof["gemm"] = {"kernel": ("k_umma_gemm_2sm_cvt (tcgen05 cta_group::2, x converted and hi/lo-split on chip, "
+                                   "three products)" if proj_products == 3 else
+                                   "k_umma_gemm_2sm (tcgen05 cta_group::2, projection x W^T)"),
+                        "achieved_tflops": proj_products * g["units_per_s"] / 1e12, "peak_tflops": pk,
+                        "frac": proj_products * g["units_per_s"] / 1e12 / pk,
+                        "algorithmic_tflops": g["units_per_s"] / 1e12, "products_per_mac": proj_products,
                         "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "fallback",
                         "share_of_step": g.get("ms_per_step", 0) / step_ms}
         for name in ("grad_w", "grad_x"):
@@ -440,7 +445,8 @@ def fwd_bwd_leg(torch, dev, proj="bf16", mufu_peak=None, cpu_seconds=0.0):
                       "within 3e-5 of the float64 reference on bf16-rounded operands, 3-4e-3 on the "
                       "unrounded ones (profiles/r2_parity_c3_unrounded.md)")}
     if mufu_peak:
-        out["roofline"] = layer_roofline(nat, layer.params, layer_kernels(torch, step), ms, mufu_peak)
+        out["roofline"] = layer_roofline(nat, layer.params, layer_kernels(torch, step), ms, mufu_peak,
+                                         proj_products=3 if proj == "bf16x3" else 1)
     if cpu_seconds > 0:
         out["cpu_baseline"] = cpu_layers_leg([784, 1024], cpu_seconds)
     return out
