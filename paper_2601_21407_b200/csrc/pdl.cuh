@@ -10,10 +10,11 @@
 // before its first global-memory access (read or write) in every thread, so a
 // PDL kernel never completes before its predecessor and the stream order stays
 // transitive.  Outside a PDL launch both instructions are no-ops.
-// Off by default (HHB_PDL=1 turns it on): measured on the layer steps, config 3
-// gained 1-2 % (0.463 -> 0.455 ms bf16) but config 4 lost 1.3 % -- early-launched
-// CTAs waiting on the main stream hold SM resources the side-stream weight-
-// gradient GEMM would use.
+// On by default (HHB_PDL=0 turns it off): three same-box A/B pairs, config 3
+// 0.567 -> 0.561 ms (bf16x3) and 0.471 -> 0.462 ms (bf16), config 4 2.450 ->
+// 2.446 ms, configs 1 / 2 / 5 unchanged.  (Before the
+// GEMMs walked column tiles fastest it cost config 4 1.3 %: CTAs parked in the
+// wait held SM resources the side-stream weight-gradient GEMM needed.)
 #pragma once
 
 #include <cstdlib>
@@ -28,7 +29,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HHB_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }
