@@ -832,15 +832,20 @@ struct PCvtCfg {
   static constexpr uint32_t kStageB = (BN / 2) * 128;        // half of B (and of B2)
   static constexpr uint32_t kStage = kStageF + kStageB * (SPLIT ? 2 : 1);
   static constexpr int kEpiWarps = EPI2_WARPS;
-  static constexpr int kCvtWarps = 4;
+#ifndef CVT_WARPS
+#define CVT_WARPS 8   // single-product form: 8 converter warps (66.7 vs 77.6 us at config 3; tools/cvt_check.py)
+#endif
+  static constexpr int kCvtWarps = SPLIT ? 4 : CVT_WARPS;
+  static constexpr int kJobs = 1024 / (32 * kCvtWarps);    // 16-byte output chunks per converter thread
   static constexpr int kThreads = 64 + 32 * (kEpiWarps + kCvtWarps);
   static constexpr uint32_t kStaging = kEpiWarps * 32 * 32 * 4;
   static constexpr int kStages = int((225 * 1024 - kStaging) / kStage) > 6 ? 6 : int((225 * 1024 - kStaging) / kStage);
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 512;
 };
 
+template <int W>
 __device__ __forceinline__ void cvt_bar_sync() {   // the converter warps only (named barrier 1)
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * 4) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * W) : "memory");
 }
 
 template <int BN, bool SPLIT>
@@ -974,10 +979,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
         mbar_wait(&afull[s], (it / ST) & 1);
         // job q: row r = j / 8, 8-column chunk c = j % 8 (8 lanes per row: each
         // quarter-warp reads one 128 B row of a swizzled box, conflict-free)
-        float x[8][8];
+        float x[C::kJobs][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int j = ct + 128 * q, r = j >> 3, c = j & 7;
+        for (int q = 0; q < C::kJobs; ++q) {
+          const int j = ct + 32 * C::kCvtWarps * q, r = j >> 3, c = j & 7;
           const uint8_t* box = f + (c >> 2) * (C::kStageF / 2) + r * 128;
           const int j0 = (2 * (c & 3)) ^ (r & 7), j1 = (2 * (c & 3) + 1) ^ (r & 7);
           const float4 u = *reinterpret_cast<const float4*>(box + j0 * 16);
@@ -985,10 +990,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
           x[q][0] = u.x; x[q][1] = u.y; x[q][2] = u.z; x[q][3] = u.w;
           x[q][4] = w.x; x[q][5] = w.y; x[q][6] = w.z; x[q][7] = w.w;
         }
-        cvt_bar_sync();                                  // every fp32 value read before the tile is overwritten
+        cvt_bar_sync<C::kCvtWarps>();                    // every fp32 value read before the tile is overwritten
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int j = ct + 128 * q, r = j >> 3, c = j & 7;
+        for (int q = 0; q < C::kJobs; ++q) {
+          const int j = ct + 32 * C::kCvtWarps * q, r = j >> 3, c = j & 7;
           uint32_t h[4], l[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -1014,7 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> the MMA's async reads
-        cvt_bar_sync();
+        cvt_bar_sync<C::kCvtWarps>();
         if (ct == 0) mbar_arrive_leader(&cfull[s]);
       }
     }
