@@ -312,9 +312,23 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[key]
 
 
-def _fused_split(x, layer) -> bool:
-    """bf16x3 projection with x converted and split on chip (hhb_gemm_f32a):
-    CTA-pair tiles (>= 512 rows) and 8-aligned k_in."""
+def _twin(x):
+    """The bf16 copy of x an HHLayer(outputs="spikes") below wrote beside its
+    fp32 spikes (exactly x in bf16), if it is still current."""
+    T, B, k_in = x.shape
+    twin = getattr(x, "_hhb_bf16", None)
+    if (twin is not None and twin[1] == x._version and tuple(twin[0].shape) == tuple(x.shape)
+            and k_in % 8 == 0):
+        return twin[0].view(T * B, k_in)
+    return None
+
+
+def _fused_convert(x, layer) -> bool:
+    """bf16x3 projection with fp32 x converted and split on chip inside the
+    GEMM (hhb_gemm_f32a): CTA-pair tiles (>= 512 rows), 8-aligned k_in.  The
+    GEMM also writes x_hi / x_lo for the weight gradient.  (The same fusion for
+    the bf16 projection measured slower in the step -- config 3 0.461 -> 0.475
+    ms, config 4 2.437 -> 2.463 ms -- so bf16 keeps the separate cast.)"""
     import os
     T, B, k_in = x.shape
     return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0
@@ -324,14 +338,14 @@ def _fused_split(x, layer) -> bool:
 def _operands(x, weight, layer):
     """bf16 GEMM operands of the projection: (xb, wb_proj, wb_grad, K) --
     wb_grad is the input gradient's B operand (the stacked [W_hi; W_hi; W_lo]
-    for bf16x3, W itself for bf16).  Fused bf16x3 (_fused_split): xb is the
+    for bf16x3, W itself for bf16).  Fused (_fused_convert): xb is the
     empty [x_hi | x_lo] buffer the projection GEMM fills while it converts x."""
     T, B, k_in = x.shape
     if layer.proj == "bf16x3":
         # fp32-class projection: I = x_h.W_h + x_l.W_h + x_h.W_l in one bf16 GEMM over 3 kp
         n_out = weight.shape[0]
         with _timed("operand_prep", T * B * k_in):
-            if _fused_split(x, layer):
+            if _fused_convert(x, layer):
                 kp = _pad8(k_in)
                 xb = torch.empty((T * B, 2 * kp), dtype=torch.bfloat16, device=x.device)
             else:
@@ -348,12 +362,9 @@ def _operands(x, weight, layer):
             nat.check(nat.load().hhb_split3_bf16(n_out, k_in, wf.data_ptr(), k_in, w3.data_ptr(), kp, P, 2,
                                                  _stream()), "split3 stacked")
         return xb, wb, w3, 3 * kp
-    twin = getattr(x, "_hhb_bf16", None)
-    if (twin is not None and twin[1] == x._version and tuple(twin[0].shape) == tuple(x.shape)
-            and k_in % 8 == 0):
-        # spikes of an HHLayer(outputs="spikes") below: its forward kernel wrote
-        # them as bf16 0/1 too -- exactly x in bf16, no cast pass
-        xb = twin[0].view(T * B, k_in)
+    xb = _twin(x)
+    if xb is not None:
+        pass      # spikes of an HHLayer(outputs="spikes") below: exactly x in bf16, no cast pass
     else:
         with _timed("operand_prep", T * B * k_in):
             xb = to_bf16_padded(x.reshape(T * B, k_in).float().contiguous())
@@ -398,7 +409,8 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
     b32 = bias.float().contiguous()
     cur = torch.empty((T * B, n_out), dtype=torch.float32, device=x.device)
     chunks = _time_chunks(T, K, T * B * n_out)
-    x32 = x.reshape(T * B, k_in).float().contiguous() if _fused_split(x, layer) else None
+    x32 = x.reshape(T * B, k_in).float().contiguous() if _fused_convert(x, layer) else None
+    x3 = layer.proj == "bf16x3"
 
     def project(r0, r1):
         if x32 is None:
@@ -408,12 +420,13 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
         # into xb for the weight gradient (B = W_hi, B_lo = W_lo: slots 0 / 2 of wb)
         lib = nat.load()
         M = r1 - r0
-        kp = xb.shape[1] // 2
+        kp = xb.shape[1] // 2 if x3 else 0
         ws_n = int(lib.hhb_gemm_workspace(M, n_out, 32))
         ws = _workspace(ws_n, x.device) if ws_n else None
         nat.check(lib.hhb_gemm_f32a(M, n_out, k_in, x32[r0:].data_ptr(), k_in, wb.data_ptr(),
-                                    wb[:, 2 * kp:].data_ptr(), wb.stride(0), b32.data_ptr(), cur[r0:].data_ptr(),
-                                    n_out, 0, D.ptr(ws), xb[r0:].data_ptr(), xb.stride(0), kp, _stream()),
+                                    wb[:, 2 * kp:].data_ptr() if x3 else None, wb.stride(0), b32.data_ptr(),
+                                    cur[r0:].data_ptr(), n_out, 0, D.ptr(ws), xb[r0:].data_ptr(), xb.stride(0), kp,
+                                    _stream()),
                   "hhb_gemm_f32a")
 
     if len(chunks) == 1:
