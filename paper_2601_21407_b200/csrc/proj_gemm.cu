@@ -835,7 +835,10 @@ struct PCvtCfg {
 #ifndef CVT_WARPS
 #define CVT_WARPS 8   // single-product form: 8 converter warps (66.7 vs 77.6 us at config 3; tools/cvt_check.py)
 #endif
-  static constexpr int kCvtWarps = SPLIT ? 4 : CVT_WARPS;
+#ifndef CVT_SPLIT_WARPS
+#define CVT_SPLIT_WARPS 4   // three-product form: 8 measured the same (107.2 vs 106.9 us)
+#endif
+  static constexpr int kCvtWarps = SPLIT ? CVT_SPLIT_WARPS : CVT_WARPS;
   static constexpr int kJobs = 1024 / (32 * kCvtWarps);    // 16-byte output chunks per converter thread
   static constexpr int kThreads = 64 + 32 * (kEpiWarps + kCvtWarps);
   static constexpr uint32_t kStaging = kEpiWarps * 32 * 32 * 4;
