@@ -343,6 +343,15 @@ struct PArgs {
   int n_fast;          // tile order: 1 = column tiles fastest (pairs on one row block run together), 0 = rows fastest
 };
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
                                              int32_t z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
@@ -855,6 +864,7 @@ template <int BN, bool SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::kThreads, 1)
     k_umma_gemm_2sm_cvt(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                         const __grid_constant__ CUtensorMap tb2, const __grid_constant__ CUtensorMap td,
+                        const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl,
                         const PArgs args) {
   using C = PCvtCfg<BN, SPLIT>;
   constexpr int ST = C::kStages;
@@ -884,7 +894,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
       mbar_init(&full[s], 2);      // B: the leader's expect_tx + the peer's arrival
       mbar_init(&afull[s], 1);     // this CTA's fp32 A tile
       mbar_init(&cfull[s], 2);     // both CTAs' converted A tiles
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);     // the MMA's commit + this CTA's converter (its x store has read the stage)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -969,7 +979,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
     }
   } else if (warp >= kCvt0) {  // converter warps: fp32 tile -> bf16 (hi [, lo]) in place
     const int ct = threadIdx.x - kCvt0 * 32;            // 0..127
-    int it = 0;
+    int it = 0, pend = -1;                              // pend: stage whose x store may still be reading
     for (int tile = pair; tile < args.tiles; tile += npairs) {
       const int z = tile / per_split, rt = tile % per_split;
       const bool xs_out = args.xs != nullptr && rt % args.n_tiles == 0;
@@ -1012,19 +1022,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
           const int off = r * 128 + ((c ^ (r & 7)) << 4);
           *reinterpret_cast<uint4*>(f + off) = make_uint4(h[0], h[1], h[2], h[3]);
           if (SPLIT) *reinterpret_cast<uint4*>(f + C::kStageF / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
-          if (xs_out) {   // the converted operand for the layer's weight gradient (first column tile only)
-            const int64_t gk = int64_t(kb) * 64 + 8 * c, gm = xm0 + r;
-            if (gm < args.M && gk < args.K) {
-              uint16_t* d = args.xs + gm * args.xs_ld + gk;
-              *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
-              if (SPLIT) *reinterpret_cast<uint4*>(d + args.xs_slot) = make_uint4(l[0], l[1], l[2], l[3]);
-            }
-          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> the MMA's async reads
         cvt_bar_sync<C::kCvtWarps>();
-        if (ct == 0) mbar_arrive_leader(&cfull[s]);
+        if (ct == 0) {
+          mbar_arrive_leader(&cfull[s]);
+          // the previous stage's x store (if any) has had a whole conversion to read
+          // its tile: release that stage now, then start this stage's store
+          if (pend >= 0) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            mbar_arrive_local(&empty[pend]);
+            pend = -1;
+          }
+          if (xs_out) {   // the converted operand for the weight gradient (first column tile only), by TMA
+            tma_store_2d(&txh, f, kb * 64, int32_t(xm0));
+            if (SPLIT) tma_store_2d(&txl, f + C::kStageF / 2, kb * 64, int32_t(xm0));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            pend = s;
+          } else {
+            mbar_arrive_local(&empty[s]);   // the stage may be reloaded once the MMA has also committed
+          }
+        }
       }
+    }
+    if (ct == 0 && pend >= 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      mbar_arrive_local(&empty[pend]);
     }
   } else {  // epilogue warps of both CTAs (as k_umma_gemm_2sm)
     const int q = warp & 3;
@@ -1483,7 +1506,8 @@ static int launch_2sm(const CUtensorMap& ta, const CUtensorMap& ta2, const CUten
 
 template <int BN, bool SPLIT>
 static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                          const CUtensorMap& td, const PArgs& a, cudaStream_t st) {
+                          const CUtensorMap& td, const CUtensorMap& txh, const CUtensorMap& txl, const PArgs& a,
+                          cudaStream_t st) {
   using C = PCvtCfg<BN, SPLIT>;
   const size_t smem = C::kSmem;
   static std::once_flag once;
@@ -1514,7 +1538,8 @@ static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   }
   int pairs = max_pairs;
   if (a.tiles < pairs) pairs = a.tiles;
-  launch_pdl(k_umma_gemm_2sm_cvt<BN, SPLIT>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, tb, tb2, td, a);
+  launch_pdl(k_umma_gemm_2sm_cvt<BN, SPLIT>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, tb, tb2, td, txh, txl,
+             a);
   return cuda_check("k_umma_gemm_2sm_cvt launch");
 }
 
@@ -1659,7 +1684,7 @@ static int gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
   const int64_t dld = splits > 1 ? N : ldd;
   if (dld % 4 != 0 || reinterpret_cast<uintptr_t>(dst) % 16 != 0)
     return fail(HHB_EINVAL, "fp32-A GEMM needs a 16-byte aligned output pitch");
-  CUtensorMap ta, tb, tb2, td;
+  CUtensorMap ta, tb, tb2, td, txh, txl;
   int rc = make_map(&ta, true, A, M, K, lda, BM);
   if (rc) return rc;
   if ((rc = make_map(&tb, false, B, N, K, ldb, bn / 2))) return rc;
@@ -1687,9 +1712,15 @@ static int gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
     pa.xs = static_cast<uint16_t*>(xs);
     pa.xs_ld = xs_ld;
     pa.xs_slot = xs_slot;
+    // hi / lo slots as separate K-wide tensors (the store of a partial last
+    // k-block is clipped at K, not spilled into the next slot)
+    if ((rc = make_map(&txh, false, xs, M, K, xs_ld, BM))) return rc;
+    if (Blo && (rc = make_map(&txl, false, static_cast<uint16_t*>(xs) + xs_slot, M, K, xs_ld, BM))) return rc;
   }
-  if (Blo) rc = bn == 128 ? launch_2sm_cvt<128, true>(ta, tb, tb2, td, pa, st) : launch_2sm_cvt<256, true>(ta, tb, tb2, td, pa, st);
-  else rc = bn == 128 ? launch_2sm_cvt<128, false>(ta, tb, tb2, td, pa, st) : launch_2sm_cvt<256, false>(ta, tb, tb2, td, pa, st);
+  if (!xs) txh = ta;
+  if (!xs || !Blo) txl = xs ? txh : ta;
+  if (Blo) rc = bn == 128 ? launch_2sm_cvt<128, true>(ta, tb, tb2, td, txh, txl, pa, st) : launch_2sm_cvt<256, true>(ta, tb, tb2, td, txh, txl, pa, st);
+  else rc = bn == 128 ? launch_2sm_cvt<128, false>(ta, tb, tb2, td, txh, txl, pa, st) : launch_2sm_cvt<256, false>(ta, tb, tb2, td, txh, txl, pa, st);
   if (rc || splits == 1) return rc;
   launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits,
              int64_t(M * N), bias, D, ldd);

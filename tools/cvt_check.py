@@ -103,4 +103,15 @@ print(" cast + bf16 GEMM   %.1f" % timeit(lambda: gemm(to_bf16_padded(x), wb, K,
 print(" fused bf16         %.1f" % timeit(lambda: fused(x, wb, b)))
 print(" split3 + GEMM(3K)  %.1f" % timeit(lambda: gemm(split3_padded(x, 0)[0], split3_padded(w, 1)[0], 3 * K, bias=b)))
 print(" fused 3-product    %.1f" % timeit(lambda: fused(x, whi, b, wlo=wlo)))
+kp3 = K
+xs3 = torch.empty((M, 2 * kp3), dtype=torch.bfloat16, device=dev)
+out3 = torch.empty((M, N), device=dev)
+
+
+def fused_xs():
+    nat.check(lib.hhb_gemm_f32a(M, N, K, x.data_ptr(), K, whi.data_ptr(), wlo.data_ptr(), whi.stride(0), b.data_ptr(),
+                                out3.data_ptr(), N, 0, None, xs3.data_ptr(), xs3.stride(0), kp3, _stream()), "xs")
+
+
+print(" fused 3-product + x_hi/x_lo written  %.1f" % timeit(fused_xs))
 print("OK" if ok else "MISMATCH")
