@@ -325,13 +325,14 @@ def _twin(x):
 
 def _fused_convert(x, layer) -> bool:
     """bf16x3 projection with fp32 x converted and split on chip inside the
-    GEMM (hhb_gemm_f32a): CTA-pair tiles (>= 512 rows), 8-aligned k_in.  The
+    GEMM (hhb_gemm_f32a): CTA-pair tiles (>= 512 rows), 8-aligned k_in, n_out a
+    multiple of 4 (16-byte output rows).  The
     GEMM also writes x_hi / x_lo for the weight gradient.  (The same fusion for
     the bf16 projection measured slower in the step -- config 3 0.461 -> 0.475
     ms, config 4 2.437 -> 2.463 ms -- so bf16 keeps the separate cast.)"""
     import os
     T, B, k_in = x.shape
-    return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0
+    return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0 and layer.weight.shape[0] % 4 == 0
             and os.environ.get("HHB_LAYER_FUSED_SPLIT", "1") != "0")
 
 

@@ -264,7 +264,7 @@ class DenseLayer:
             wa, kp = split3_padded(_dev(self.weights).float().reshape(-1, k).contiguous(), 1)   # [W_hi|W_hi|W_lo]
             b32 = _dev(self.bias).float().contiguous()
             M, N = x2.shape[0], wa.shape[0]
-            if M >= 512 and k % 4 == 0:
+            if M >= 512 and k % 4 == 0 and N % 4 == 0:      # (CTA-pair tiles, 16-byte row pitches)
                 # x split into hi / lo on chip inside the GEMM (hhb_gemm_f32a)
                 lib = nat.load()
                 y = torch.empty((M, N), dtype=torch.float32, device=x2.device)

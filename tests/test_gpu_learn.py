@@ -249,7 +249,8 @@ def test_dense_layer_float32_runs_on_the_tcgen05_gemm(cuda):
     from paper_2601_21407_b200 import learn as L
     rng = np.random.default_rng(0)
     # (10, 4, 37): the split pass + GEMM; (64, 16, 784): >= 512 rows, x split on chip (hhb_gemm_f32a)
-    for shape, n_out in (((10, 4, 37), 96), ((64, 16, 784), 300)):
+    # (64, 16, 784) -> 1: the readout width (output rows not 16-byte aligned: the split-pass path)
+    for shape, n_out in (((10, 4, 37), 96), ((64, 16, 784), 300), ((64, 16, 784), 1)):
         layer = L.DenseLayer(rng.normal(0.05, 0.1, (n_out, shape[-1])), rng.normal(0, 1, n_out))
         x = rng.normal(0.5, 1.0, shape)
         ref = x @ layer.weights.T + layer.bias

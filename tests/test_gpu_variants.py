@@ -114,3 +114,28 @@ def test_programmatic_dependent_launch_is_bit_identical(cuda, proj):
         assert r.returncode == 0, r.stderr[-2000:]
         out[pdl] = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["0"] == out["1"]
+
+
+@pytest.mark.parametrize("n_out", [12, 10])
+def test_onchip_split_projection_matches_split_pass(cuda, env, n_out):
+    """bf16x3 layer with >= 512 rows: the on-chip split GEMM (n_out a multiple
+    of 4) against HHB_LAYER_FUSED_SPLIT=0 (the split pass + K = 3k GEMM): the
+    same three products, accumulated in another order -- gradients agree to
+    float32 rounding; n_out = 10 (unaligned output rows) takes the split pass."""
+    from paper_2601_21407_b200.layer import HHLayer
+
+    def run():
+        torch.manual_seed(0)
+        layer = HHLayer(64, n_out, w_mean=0.3, w_std=0.2, device=cuda, proj="bf16x3")
+        g = torch.Generator(device=cuda).manual_seed(1)
+        x = ((torch.rand((40, 16, 64), device=cuda, generator=g) < 0.3).float()
+             + 0.1 * torch.randn((40, 16, 64), device=cuda, generator=g))
+        layer.mse_loss(x).backward()
+        torch.cuda.synchronize()
+        return layer.weight.grad.double(), layer.bias.grad.double()
+
+    w1, b1 = run()
+    env.setenv("HHB_LAYER_FUSED_SPLIT", "0")
+    w0, b0 = run()
+    assert torch.allclose(w1, w0, rtol=1e-4, atol=1e-6 * float(w0.abs().max()))
+    assert torch.allclose(b1, b0, rtol=1e-4, atol=1e-6 * float(b0.abs().max()))
