@@ -1123,6 +1123,236 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
   }
 }
 
+// Weight-gradient form of the on-chip split: D[m][n] = sum_k (A + A2)[k][m] . B_hi[k][n]
+// + A[k][m] . B_lo[k][n] with A / A2 the bf16 hi / lo halves of dI (MN-major)
+// and B the fp32 layer input x, MN-major (x[k][n], k = the (t, b) row), rounded
+// and split into bf16 hi / lo on chip by the converter warps in the MN-major
+// 128B-swizzled layout (64-column chunks of 64 k-rows x 128 B).  The
+// three-product fp32-class dW of proj="bf16x3" in one GEMM, reading x in fp32
+// -- so the forward projection need not write x_hi / x_lo.
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, true>::kThreads, 1)
+    k_umma_gemm_2sm_cvtb(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
+                         const __grid_constant__ CUtensorMap tbf, const __grid_constant__ CUtensorMap td,
+                         const PArgs args) {
+  using C = PCvtCfg<BN, true>;
+  constexpr int ST = C::kStages;
+  constexpr uint32_t kStageF = 64 * (BN / 2) * 4;        // this CTA's 64 k-rows x BN/2 columns of fp32 x
+  constexpr uint32_t kStageA = BM * 128;                 // 128 rows of A (hi; lo after it)
+  static_assert(kStageF == C::kStageF && 2 * kStageA == C::kStage - C::kStageF, "cvtb stage layout");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sF = smem;                                   // [ST][kStageF]: x fp32 -> B_hi | B_lo in place
+  uint8_t* sA = smem + ST * kStageF;                    // [ST][2 * kStageA]: A hi | A lo
+  float* stg = reinterpret_cast<float*>(sA + ST * 2 * kStageA);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::kStaging);
+  uint64_t* afull = full + ST;
+  uint64_t* cfull = afull + ST;
+  uint64_t* empty = cfull + ST;
+  uint64_t* tfull = empty + ST;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tbf)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&td)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 2);      // A: the leader's expect_tx + the peer's arrival
+      mbar_init(&afull[s], 1);     // this CTA's fp32 x tile
+      mbar_init(&cfull[s], 2);     // both CTAs' converted B tiles
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * C::kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(uint32_t(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+  pdl_wait();
+  pdl_trigger();
+  const int per_split = args.m_tiles * args.n_tiles;    // column tiles fastest
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr int kCvt0 = 2 + C::kEpiWarps;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own A rows (hi, lo), own half of the x columns (fp32)
+      int it = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs) {
+        const int z = tile / per_split, r = tile % per_split;
+        const int64_t m0 = int64_t(r / args.n_tiles) * (2 * BM) + int64_t(rank) * BM;
+        const int64_t n0 = int64_t(r % args.n_tiles) * BN + int64_t(rank) * (BN / 2);
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          const int32_t kx = kb * 64;
+          uint8_t* f_dst = sF + s * kStageF;
+          mbar_expect_tx(&afull[s], kStageF);
+#pragma unroll
+          for (int c = 0; c < (BN / 2) / 32; ++c) tma_load_2d(&tbf, &afull[s], f_dst + c * 8192, int32_t(n0) + 32 * c, kx);
+          if (leader) mbar_expect_tx_only(&full[s], 2 * 2 * kStageA);
+          else mbar_arrive_leader(&full[s]);
+          uint8_t* a_dst = sA + s * 2 * kStageA;
+#pragma unroll
+          for (int c = 0; c < BM / 64; ++c) {
+            tma_load_2d_2sm(&ta, &full[s], a_dst + c * 8192, int32_t(m0) + 64 * c, kx);
+            tma_load_2d_2sm(&ta2, &full[s], a_dst + kStageA + c * 8192, int32_t(m0) + 64 * c, kx);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer
+      int it = 0, local = 0;
+      for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+        const int z = tile / per_split;
+        const int kb0 = z * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        const int b = local & 1;
+        mbar_wait(&tempty[b], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + uint32_t(b * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          mbar_wait(&cfull[s], (it / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* a_src = sA + s * 2 * kStageA;
+          const uint8_t* f_src = sF + s * kStageF;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ah = smem_desc_mn(a_src + k * 2048), al = smem_desc_mn(a_src + kStageA + k * 2048);
+            const uint64_t bh = smem_desc_mn(f_src + k * 2048), bl = smem_desc_mn(f_src + kStageF / 2 + k * 2048);
+            umma2(acc, ah, bh, args.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma2(acc, al, bh, args.idesc, 1u);
+            umma2(acc, ah, bl, args.idesc, 1u);
+          }
+          umma2_commit(&empty[s]);
+        }
+        umma2_commit(&tfull[b]);
+      }
+    }
+  } else if (warp >= kCvt0) {  // converter warps: fp32 x (MN-major) -> bf16 hi | lo in place
+    const int ct = threadIdx.x - kCvt0 * 32;
+    int it = 0;
+    for (int tile = pair; tile < args.tiles; tile += npairs) {
+      const int z = tile / per_split;
+      const int kb0 = z * args.kb_per_split;
+      const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % ST;
+        uint8_t* f = sF + s * kStageF;
+        mbar_wait(&afull[s], (it / ST) & 1);
+        // job: k-row r = j / 16, 8-column chunk c = j % 16 of this CTA's 128 columns
+        float x[C::kJobs][8];
+#pragma unroll
+        for (int q = 0; q < C::kJobs; ++q) {
+          const int j = ct + 32 * C::kCvtWarps * q, r = j >> 4, c = j & 15;
+          const uint8_t* box = f + (c >> 2) * 8192 + r * 128;
+          const int j0 = (2 * (c & 3)) ^ (r & 7), j1 = (2 * (c & 3) + 1) ^ (r & 7);
+          const float4 u = *reinterpret_cast<const float4*>(box + j0 * 16);
+          const float4 w = *reinterpret_cast<const float4*>(box + j1 * 16);
+          x[q][0] = u.x; x[q][1] = u.y; x[q][2] = u.z; x[q][3] = u.w;
+          x[q][4] = w.x; x[q][5] = w.y; x[q][6] = w.z; x[q][7] = w.w;
+        }
+        cvt_bar_sync<C::kCvtWarps>();
+#pragma unroll
+        for (int q = 0; q < C::kJobs; ++q) {
+          const int j = ct + 32 * C::kCvtWarps * q, r = j >> 4, c = j & 15;
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(x[q][2 * e], x[q][2 * e + 1]);
+            h[e] = *reinterpret_cast<const uint32_t*>(&hb);
+            const float2 hf = __bfloat1622float2(hb);
+            const __nv_bfloat162 lb =
+                __floats2bfloat162_rn(__fsub_rn(x[q][2 * e], hf.x), __fsub_rn(x[q][2 * e + 1], hf.y));
+            l[e] = *reinterpret_cast<const uint32_t*>(&lb);
+          }
+          // MN-major bf16: 64-column chunk c / 8 (8 KB), k-row r, 16-byte chunk (c % 8) ^ (r % 8)
+          const int off = (c >> 3) * 8192 + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(f + off) = make_uint4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<uint4*>(f + kStageF / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        cvt_bar_sync<C::kCvtWarps>();
+        if (ct == 0) mbar_arrive_leader(&cfull[s]);
+      }
+    }
+  } else {  // epilogue warps (as k_umma_gemm_2sm)
+    const int q = warp & 3;
+    const int half = C::kEpiWarps == 8 ? (warp - 2) >> 2 : 0;
+    constexpr int kCols = C::kEpiWarps == 8 ? BN / 2 : BN;
+    float* my_stg = stg + (warp - 2) * 1024;
+    int local = 0;
+    for (int tile = pair; tile < args.tiles; tile += npairs, ++local) {
+      const int z = tile / per_split, r = tile % per_split;
+      const int64_t m0 = int64_t(r / args.n_tiles) * (2 * BM) + int64_t(rank) * BM;
+      const int64_t n0 = int64_t(r % args.n_tiles) * BN;
+      const int kb0 = z * args.kb_per_split;
+      const bool any_k = min(args.kb_total, kb0 + args.kb_per_split) > kb0;
+      const int b = local & 1;
+      mbar_wait(&tfull[b], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int32_t row0 = int32_t(m0 + q * 32);
+#pragma unroll 1
+      for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
+        if (n0 + c0 >= args.N) break;
+        uint32_t rr[32];
+        if (any_k) {
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(b * BN + c0), rr);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = 0u;
+        }
+        float* buf = my_stg;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o;
+          o.x = __uint_as_float(rr[4 * j + 0]);
+          o.y = __uint_as_float(rr[4 * j + 1]);
+          o.z = __uint_as_float(rr[4 * j + 2]);
+          o.w = __uint_as_float(rr[4 * j + 3]);
+          *reinterpret_cast<float4*>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&td, buf, int32_t(n0 + c0), row0, z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[b]);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(2 * BN)));
+  }
+}
+
 // fixed-order split-K reduction (+ bias)
 __global__ void k_gemm_reduce(int64_t M, int64_t N, const float* ws, int splits, int64_t split_stride,
                               const float* bias, float* D, int64_t ldd) {
@@ -1375,6 +1605,21 @@ static int make_map(CUtensorMap* map, bool tf32, const void* base, int64_t rows,
   return HHB_OK;
 }
 
+// MN-major fp32 operand (converted on chip): global [K][ld] floats, boxes of 32 x 64
+static int make_map_mn_f32(CUtensorMap* map, const float* base, int64_t mn, int64_t k, int64_t ld) {
+  EncodeFn enc = encoder();
+  if (!enc) return fail(HHB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cuuint64_t(mn), cuuint64_t(k)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  const cuuint32_t box[2] = {32u, 64u};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HHB_EINVAL, "cuTensorMapEncodeTiled rejected the fp32 MN-major operand");
+  return HHB_OK;
+}
+
 // MN-major bf16 operand: global [K][ld] (MN contiguous), boxes of 64 x 64
 static int make_map_mn(CUtensorMap* map, const void* base, int64_t mn, int64_t k, int64_t ld) {
   EncodeFn enc = encoder();
@@ -1543,6 +1788,41 @@ static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   return cuda_check("k_umma_gemm_2sm_cvt launch");
 }
 
+static int launch_2sm_cvtb(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tbf,
+                           const CUtensorMap& td, const PArgs& a, cudaStream_t st) {
+  using C = PCvtCfg<256, true>;
+  const size_t smem = C::kSmem;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_umma_gemm_2sm_cvtb<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  });
+  if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed (cvtb)");
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+    cfg.blockDim = dim3(C::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_umma_gemm_2sm_cvtb<256>, &cfg) != cudaSuccess || n <= 0)
+      n = num_sms() / 2;
+    (void)cudaGetLastError();
+    max_pairs = n;
+  }
+  int pairs = max_pairs;
+  if (a.tiles < pairs) pairs = a.tiles;
+  launch_pdl(k_umma_gemm_2sm_cvtb<256>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, ta2, tbf, td, a);
+  return cuda_check("k_umma_gemm_2sm_cvtb launch");
+}
+
 // tile order of the persistent GEMMs: column tiles fastest unless HHB_GEMM_RASTER=m
 static int gemm_n_fast() {
   static const int v = [] {
@@ -1643,6 +1923,66 @@ int hhb_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, 
                   int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
                   void* xs, int64_t xs_ld, int64_t xs_slot, void* stream) {
   return gemm_f32a(M, N, K, A, lda, B, B_lo, ldb, bias, D, ldd, splits, workspace, stream, xs, xs_ld, xs_slot);
+}
+
+int hhb_gemm_f32b(int64_t M, int64_t N, int64_t K, const void* A, const void* A_lo, int64_t lda, const float* B,
+                  int64_t ldb, float* D, int64_t ldd, int32_t splits, float* workspace, void* stream) {
+  using namespace hhb::gemm;
+  if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !A_lo || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
+  if (M == 0 || N == 0) return HHB_OK;
+  if ((lda * 2) % 16 || (ldb * 4) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
+      reinterpret_cast<uintptr_t>(A_lo) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
+    return fail(HHB_EINVAL, "gemm operands need 16-byte aligned base and row pitch");
+  if (lda < M || ldb < N) return fail(HHB_EINVAL, "lda/ldb too small");
+  if (M < 512 || N <= 128) return fail(HHB_EINVAL, "fp32-B GEMM: M >= 512 rows and N > 128 columns (256-wide pair tiles)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int bn = 256;
+  const int kb_total = int((K + 63) / 64);
+  if (splits < 1) {
+    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
+    const int64_t P = num_sms() / 2;
+    const double t_kb = 0.28 * 3.0;
+    const double t_mn = double(M) * double(N) * 4.0 / 5e12 * 1e6;
+    double best = 1e300;
+    splits = 1;
+    for (int sp = 1; sp <= (kb_total >= 8 ? kb_total / 4 : 1) && sp <= 32; ++sp) {
+      const int64_t units = tiles * sp;
+      const double cost = double((units + P - 1) / P) * double((kb_total + sp - 1) / sp) * t_kb +
+                          (sp > 1 ? double(2 * sp + 1) * t_mn : 0.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = sp;
+      }
+    }
+  }
+  if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
+  if (splits > 1 && !workspace) return fail(HHB_EINVAL, "split-K needs workspace");
+  float* dst = splits > 1 ? workspace : D;
+  const int64_t dld = splits > 1 ? N : ldd;
+  if (dld % 4 != 0 || reinterpret_cast<uintptr_t>(dst) % 16 != 0)
+    return fail(HHB_EINVAL, "fp32-B GEMM needs a 16-byte aligned output pitch");
+  CUtensorMap ta, ta2, tbf, td;
+  int rc = make_map_mn(&ta, A, M, K, lda);
+  if (rc) return rc;
+  if ((rc = make_map_mn(&ta2, A_lo, M, K, lda))) return rc;
+  if ((rc = make_map_mn_f32(&tbf, B, N, K, ldb))) return rc;
+  if ((rc = make_map_d(&td, dst, M, N, dld, splits))) return rc;
+  PArgs pa{};
+  pa.M = M;
+  pa.N = N;
+  pa.m_tiles = int((M + 2 * BM - 1) / (2 * BM));
+  pa.n_tiles = int((N + bn - 1) / bn);
+  pa.kb_total = kb_total;
+  pa.kb_per_split = (kb_total + splits - 1) / splits;
+  pa.splits = splits;
+  pa.tiles = pa.m_tiles * pa.n_tiles * splits;
+  pa.idesc = instr_desc(false, bn, true, true, 2 * BM);
+  pa.bias = nullptr;
+  pa.K = K;
+  if ((rc = launch_2sm_cvtb(ta, ta2, tbf, td, pa, st)) || splits == 1) return rc;
+  launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits,
+             int64_t(M * N), (const float*)nullptr, D, ldd);
+  return cuda_check("k_gemm_reduce launch");
 }
 
 // fp32-A CTA-pair GEMM (k_umma_gemm_2sm_cvt): D = bf16(A) . B^T, or with B_lo

@@ -244,6 +244,16 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         # dW[j][k] = sum_m dI[m][j] X[m][k]: A = dI^T, B = X^T, both MN-major views;
         # bf16x3: (dI_hi + dI_lo) . x_hi + dI_hi . x_lo (slots 0 and 1 of xb)
         with _timed("grad_w", 2.0 * M * n_out * k_in):
+            if xb.dtype == torch.float32:
+                # the fp32 x itself (_fused_dw): split on chip, three products in one GEMM
+                lib = nat.load()
+                dW = torch.empty((n_out, k_in), dtype=torch.float32, device=xb.device)
+                ws_n = int(lib.hhb_gemm_workspace(n_out, k_in, 32))
+                ws = _workspace(ws_n, xb.device) if ws_n else None
+                nat.check(lib.hhb_gemm_f32b(n_out, k_in, M, hi.data_ptr(), lo.data_ptr(), 2 * P, xb.data_ptr(),
+                                            xb.stride(0), dW.data_ptr(), k_in, 0, D.ptr(ws), _stream()),
+                          "hhb_gemm_f32b")
+                return dW
             dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, 2 * P, xb, xb.stride(0))
             if x3:
                 dW += gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, None, 2 * P, xb[:, kp:], xb.stride(0))
@@ -336,6 +346,16 @@ def _fused_convert(x, layer) -> bool:
             and os.environ.get("HHB_LAYER_FUSED_SPLIT", "1") != "0")
 
 
+def _fused_dw(x, layer) -> bool:
+    """With the on-chip split projection, the weight gradient also reads the
+    fp32 x and splits it on chip (hhb_gemm_f32b), so the projection need not
+    write x_hi / x_lo: 256-wide CTA-pair tiles (n_out >= 512, k_in > 128)."""
+    import os
+    T, B, k_in = x.shape
+    return (_fused_convert(x, layer) and layer.weight.shape[0] >= 512 and k_in > 128
+            and os.environ.get("HHB_LAYER_FUSED_DW", "1") != "0")
+
+
 def _operands(x, weight, layer):
     """bf16 GEMM operands of the projection: (xb, wb_proj, wb_grad, K) --
     wb_grad is the input gradient's B operand (the stacked [W_hi; W_hi; W_lo]
@@ -348,7 +368,10 @@ def _operands(x, weight, layer):
         with _timed("operand_prep", T * B * k_in):
             if _fused_convert(x, layer):
                 kp = _pad8(k_in)
-                xb = torch.empty((T * B, 2 * kp), dtype=torch.bfloat16, device=x.device)
+                # the [x_hi | x_lo] the projection GEMM writes for the weight
+                # gradient -- none when that GEMM splits the fp32 x itself
+                xb = None if _fused_dw(x, layer) else torch.empty((T * B, 2 * kp), dtype=torch.bfloat16,
+                                                                    device=x.device)
             else:
                 xb, kp = split3_padded(x.reshape(T * B, k_in).float().contiguous(), 0)
             wb, _ = split3_padded(weight.float().contiguous(), 1)
@@ -421,20 +444,21 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
         # into xb for the weight gradient (B = W_hi, B_lo = W_lo: slots 0 / 2 of wb)
         lib = nat.load()
         M = r1 - r0
-        kp = xb.shape[1] // 2 if x3 else 0
+        kp = _pad8(k_in) if x3 else 0
         ws_n = int(lib.hhb_gemm_workspace(M, n_out, 32))
         ws = _workspace(ws_n, x.device) if ws_n else None
         nat.check(lib.hhb_gemm_f32a(M, n_out, k_in, x32[r0:].data_ptr(), k_in, wb.data_ptr(),
                                     wb[:, 2 * kp:].data_ptr() if x3 else None, wb.stride(0), b32.data_ptr(),
-                                    cur[r0:].data_ptr(), n_out, 0, D.ptr(ws), xb[r0:].data_ptr(), xb.stride(0), kp,
-                                    _stream()),
+                                    cur[r0:].data_ptr(), n_out, 0, D.ptr(ws),
+                                    None if xb is None else xb[r0:].data_ptr(), 0 if xb is None else xb.stride(0),
+                                    kp, _stream()),
                   "hhb_gemm_f32a")
 
     if len(chunks) == 1:
         with _timed("proj_gemm", 2.0 * T * B * k_in * n_out):
             project(0, T * B)
         run_forward(cur, 0, T)
-        return xb, wg, cur
+        return (x32 if xb is None else xb), wg, cur
     main = torch.cuda.current_stream(x.device)
     side = _proj_stream(x.device)
     fork = torch.cuda.Event()
@@ -448,12 +472,12 @@ def _project_forward(x, weight, bias, layer, K, run_forward):
             ev = torch.cuda.Event()
             ev.record(side)
             evs.append(ev)
-    for t in (xb, wb, b32, cur) + (() if x32 is None else (x32,)):
+    for t in (wb, b32, cur) + (() if xb is None else (xb,)) + (() if x32 is None else (x32,)):
         t.record_stream(side)
     for (t0, t1), ev in zip(chunks, evs):
         main.wait_event(ev)
         run_forward(cur, t0, t1)
-    return xb, wg, cur
+    return (x32 if xb is None else xb), wg, cur
 
 
 class _HHLayerFn(torch.autograd.Function):

@@ -114,4 +114,36 @@ def fused_xs():
 
 
 print(" fused 3-product + x_hi/x_lo written  %.1f" % timeit(fused_xs))
+
+# weight-gradient form (hhb_gemm_f32b): dW = (dI_hi + dI_lo)^T x_hi + dI_hi^T x_lo with x fp32
+from paper_2601_21407_b200.layer import gemm_ex, A_MN, B_MN
+
+
+def check_f32b(R, n_out, k_in, splits=0):
+    g = torch.Generator(device=dev).manual_seed(R + n_out)
+    dI = torch.randn((R, n_out), device=dev, generator=g) * 1e-3
+    xf = torch.randn((R, k_in), device=dev, generator=g)
+    hi = dI.to(torch.bfloat16)
+    lo = (dI - hi.float()).to(torch.bfloat16)
+    xs3, kp = split3_padded(xf, 0)
+    ref = gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, lo, n_out, xs3, xs3.stride(0))
+    ref += gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, None, n_out, xs3[:, kp:], xs3.stride(0))
+    out = torch.empty((n_out, k_in), device=dev)
+    ws = _workspace(int(lib.hhb_gemm_workspace(n_out, k_in, 32)), dev)
+    fn = lambda: nat.check(lib.hhb_gemm_f32b(n_out, k_in, R, hi.data_ptr(), lo.data_ptr(), n_out, xf.data_ptr(),
+                                             k_in, out.data_ptr(), k_in, splits, ws.data_ptr(), _stream()), "f32b")
+    fn()
+    exact = dI.double().T @ xf.double()
+    torch.cuda.synchronize()
+    e = ((out.double() - exact).abs().max() / exact.abs().max()).item()
+    r = ((ref.double() - exact).abs().max() / exact.abs().max()).item()
+    print(f"f32b R={R} n_out={n_out} k_in={k_in}: rel err {e:.2e} (two-GEMM path {r:.2e})", flush=True)
+    return e < 4 * r + 1e-6, fn, lambda: (gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, lo, n_out, xs3, xs3.stride(0)),
+                                          gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, None, n_out, xs3[:, kp:], xs3.stride(0)))
+
+
+for case in [(1024, 512, 384), (4096, 600, 200), (25600, 1024, 784)]:
+    good, fn, two = check_f32b(*case)
+    ok = good and ok
+print("config-3 weight gradient: f32b %.1f us, two GEMMs %.1f us" % (timeit(fn), timeit(two)))
 print("OK" if ok else "MISMATCH")
