@@ -308,13 +308,15 @@ int hhb_gemm_ex2(int32_t flags, int64_t M, int64_t N, int64_t K, const void* A, 
 int hhb_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const void* B, const void* B_lo,
                   int64_t ldb, const float* bias, float* D, int64_t ldd, int32_t splits, float* workspace,
                   void* xs, int64_t xs_ld, int64_t xs_slot, void* stream);
-/* Weight-gradient form: D[m][n] = sum_k (A + A_lo)[k][m] . B_hi[k][n] + A[k][m] .
- * B_lo[k][n], A / A_lo bf16 MN-major (A[k][m] at A + k*lda + m: the hi / lo halves
- * of the layer's dI), B fp32 MN-major (B[k][n] at B + k*ldb + n: the layer input
- * x), rounded and split into bf16 hi / lo on chip -- the three-product dW of
- * proj="bf16x3" (learn.py:272) in one GEMM over the fp32 x.  M >= 512, N > 128. */
+/* Weight-gradient form: D[m][n] = sum_k (A + A_lo)[k][m] . B_hi[k][n] (+ A[k][m] .
+ * B_lo[k][n] when split_b), A / A_lo bf16 MN-major (A[k][m] at A + k*lda + m: the
+ * hi / lo halves of the layer's dI), B fp32 MN-major (B[k][n] at B + k*ldb + n:
+ * the layer input x), rounded (split_b: and split into bf16 hi / lo) on chip --
+ * the dW of proj="bf16x3" (three products) or proj="bf16" (two) (learn.py:272)
+ * in one GEMM over the fp32 x.  M >= 512, N > 128. */
 int hhb_gemm_f32b(int64_t M, int64_t N, int64_t K, const void* A, const void* A_lo, int64_t lda, const float* B,
-                  int64_t ldb, float* D, int64_t ldd, int32_t splits, float* workspace, void* stream);
+                  int64_t ldb, int32_t split_b, float* D, int64_t ldd, int32_t splits, float* workspace,
+                  void* stream);
 /* dst[c][r] = src[r][c]; kind 0: fp32->fp32, 1: fp32->bf16, 2: bf16->bf16,
  * 3: fp32 -> bf16 hi at [c][r] and lo = x - hi at [c][rows + r] (bf16x2 split),
  * 4: bf16 -> bf16 written to [c][r] and [c][rows + r].  Kinds 3 + 4 turn a

@@ -147,7 +147,7 @@ SIGNATURES = {
     "hhb_col_sum_ex": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hhb_gemm_f32a": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _i64,
                              _i64, _vp]),
-    "hhb_gemm_f32b": (_i32, [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _vp]),
+    "hhb_gemm_f32b": (_i32, [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _vp]),
     "hhb_sum_f64": (_i32, [_i64, _vp, C.c_double, _vp, _vp, _vp]),
     "hhb_cortex_input": (_i32, [_i32, _i64, _i64, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _dbl, _dbl,
                                 C.c_uint64, _i64, _vp, _vp, _dbl, _vp]),

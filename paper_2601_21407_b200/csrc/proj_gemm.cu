@@ -1130,16 +1130,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, SPLIT>::
 // 128B-swizzled layout (64-column chunks of 64 k-rows x 128 B).  The
 // three-product fp32-class dW of proj="bf16x3" in one GEMM, reading x in fp32
 // -- so the forward projection need not write x_hi / x_lo.
-template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, true>::kThreads, 1)
+// SPLIT = false: x rounded to bf16 only, D = sum_k (A + A2)[k][m] . bf16(B)[k][n]
+// (the dW of proj="bf16", two products per k-step).
+template <bool SPLIT>
+struct PCvtbCfg {
+  static constexpr int kEpiWarps = EPI2_WARPS;
+  static constexpr int kCvtWarps = SPLIT ? CVT_SPLIT_WARPS : CVT_WARPS;
+  static constexpr int kThreads = 64 + 32 * (kEpiWarps + kCvtWarps);
+  static constexpr int kJobs = 1024 / (32 * kCvtWarps);
+  static constexpr uint32_t kStage = 64 * 1024;           // fp32 x (32 KB) + A hi / lo (2 x 16 KB)
+  static constexpr uint32_t kStaging = kEpiWarps * 32 * 32 * 4;
+  static constexpr int kStages = int((225 * 1024 - kStaging) / kStage);
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStaging + 512;
+};
+
+template <int BN, bool SPLIT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtbCfg<SPLIT>::kThreads, 1)
     k_umma_gemm_2sm_cvtb(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                          const __grid_constant__ CUtensorMap tbf, const __grid_constant__ CUtensorMap td,
                          const PArgs args) {
-  using C = PCvtCfg<BN, true>;
+  using C = PCvtbCfg<SPLIT>;
   constexpr int ST = C::kStages;
   constexpr uint32_t kStageF = 64 * (BN / 2) * 4;        // this CTA's 64 k-rows x BN/2 columns of fp32 x
   constexpr uint32_t kStageA = BM * 128;                 // 128 rows of A (hi; lo after it)
-  static_assert(kStageF == C::kStageF && 2 * kStageA == C::kStage - C::kStageF, "cvtb stage layout");
+  static_assert(BN == 256 && kStageF + 2 * kStageA == C::kStage, "cvtb stage layout");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sF = smem;                                   // [ST][kStageF]: x fp32 -> B_hi | B_lo in place
@@ -1240,7 +1254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, true>::k
             const uint64_t bh = smem_desc_mn(f_src + k * 2048), bl = smem_desc_mn(f_src + kStageF / 2 + k * 2048);
             umma2(acc, ah, bh, args.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             umma2(acc, al, bh, args.idesc, 1u);
-            umma2(acc, ah, bl, args.idesc, 1u);
+            if (SPLIT) umma2(acc, ah, bl, args.idesc, 1u);
           }
           umma2_commit(&empty[s]);
         }
@@ -1279,15 +1293,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PCvtCfg<BN, true>::k
           for (int e = 0; e < 4; ++e) {
             const __nv_bfloat162 hb = __floats2bfloat162_rn(x[q][2 * e], x[q][2 * e + 1]);
             h[e] = *reinterpret_cast<const uint32_t*>(&hb);
-            const float2 hf = __bfloat1622float2(hb);
-            const __nv_bfloat162 lb =
-                __floats2bfloat162_rn(__fsub_rn(x[q][2 * e], hf.x), __fsub_rn(x[q][2 * e + 1], hf.y));
-            l[e] = *reinterpret_cast<const uint32_t*>(&lb);
+            if (SPLIT) {
+              const float2 hf = __bfloat1622float2(hb);
+              const __nv_bfloat162 lb =
+                  __floats2bfloat162_rn(__fsub_rn(x[q][2 * e], hf.x), __fsub_rn(x[q][2 * e + 1], hf.y));
+              l[e] = *reinterpret_cast<const uint32_t*>(&lb);
+            }
           }
           // MN-major bf16: 64-column chunk c / 8 (8 KB), k-row r, 16-byte chunk (c % 8) ^ (r % 8)
           const int off = (c >> 3) * 8192 + r * 128 + (((c & 7) ^ (r & 7)) << 4);
           *reinterpret_cast<uint4*>(f + off) = make_uint4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<uint4*>(f + kStageF / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+          if (SPLIT) *reinterpret_cast<uint4*>(f + kStageF / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         cvt_bar_sync<C::kCvtWarps>();
@@ -1788,14 +1804,15 @@ static int launch_2sm_cvt(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   return cuda_check("k_umma_gemm_2sm_cvt launch");
 }
 
+template <bool SPLIT>
 static int launch_2sm_cvtb(const CUtensorMap& ta, const CUtensorMap& ta2, const CUtensorMap& tbf,
                            const CUtensorMap& td, const PArgs& a, cudaStream_t st) {
-  using C = PCvtCfg<256, true>;
+  using C = PCvtbCfg<SPLIT>;
   const size_t smem = C::kSmem;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(k_umma_gemm_2sm_cvtb<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr_err = cudaFuncSetAttribute(k_umma_gemm_2sm_cvtb<256, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   });
   if (attr_err != cudaSuccess) return fail(HHB_ECUDA, "cudaFuncSetAttribute(smem) failed (cvtb)");
   static int max_pairs = 0;
@@ -1812,14 +1829,14 @@ static int launch_2sm_cvtb(const CUtensorMap& ta, const CUtensorMap& ta2, const 
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_umma_gemm_2sm_cvtb<256>, &cfg) != cudaSuccess || n <= 0)
+    if (cudaOccupancyMaxActiveClusters(&n, k_umma_gemm_2sm_cvtb<256, SPLIT>, &cfg) != cudaSuccess || n <= 0)
       n = num_sms() / 2;
     (void)cudaGetLastError();
     max_pairs = n;
   }
   int pairs = max_pairs;
   if (a.tiles < pairs) pairs = a.tiles;
-  launch_pdl(k_umma_gemm_2sm_cvtb<256>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, ta2, tbf, td, a);
+  launch_pdl(k_umma_gemm_2sm_cvtb<256, SPLIT>, dim3(2 * pairs), dim3(C::kThreads), smem, st, ta, ta2, tbf, td, a);
   return cuda_check("k_umma_gemm_2sm_cvtb launch");
 }
 
@@ -1926,7 +1943,8 @@ int hhb_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, 
 }
 
 int hhb_gemm_f32b(int64_t M, int64_t N, int64_t K, const void* A, const void* A_lo, int64_t lda, const float* B,
-                  int64_t ldb, float* D, int64_t ldd, int32_t splits, float* workspace, void* stream) {
+                  int64_t ldb, int32_t split_b, float* D, int64_t ldd, int32_t splits, float* workspace,
+                  void* stream) {
   using namespace hhb::gemm;
   if (M < 0 || N < 0 || K < 0 || (M && N && (!A || !A_lo || !B || !D)) || ldd < N) return fail(HHB_EINVAL, "gemm shape");
   if (M == 0 || N == 0) return HHB_OK;
@@ -1941,7 +1959,7 @@ int hhb_gemm_f32b(int64_t M, int64_t N, int64_t K, const void* A, const void* A_
   if (splits < 1) {
     const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
     const int64_t P = num_sms() / 2;
-    const double t_kb = 0.28 * 3.0;
+    const double t_kb = 0.28 * (split_b ? 3.0 : 2.0);
     const double t_mn = double(M) * double(N) * 4.0 / 5e12 * 1e6;
     double best = 1e300;
     splits = 1;
@@ -1979,7 +1997,9 @@ int hhb_gemm_f32b(int64_t M, int64_t N, int64_t K, const void* A, const void* A_
   pa.idesc = instr_desc(false, bn, true, true, 2 * BM);
   pa.bias = nullptr;
   pa.K = K;
-  if ((rc = launch_2sm_cvtb(ta, ta2, tbf, td, pa, st)) || splits == 1) return rc;
+  if ((rc = split_b ? launch_2sm_cvtb<true>(ta, ta2, tbf, td, pa, st) : launch_2sm_cvtb<false>(ta, ta2, tbf, td, pa, st)) ||
+      splits == 1)
+    return rc;
   launch_pdl(k_gemm_reduce, dim3(grid_1d(M * N, 256)), dim3(256), 0, st, M, N, (const float*)workspace, splits,
              int64_t(M * N), (const float*)nullptr, D, ldd);
   return cuda_check("k_gemm_reduce launch");

@@ -245,13 +245,14 @@ def _layer_grads(layer, xb, wb, cur, ckpt, K, shape, x_requires_grad, sv, ss, sv
         # bf16x3: (dI_hi + dI_lo) . x_hi + dI_hi . x_lo (slots 0 and 1 of xb)
         with _timed("grad_w", 2.0 * M * n_out * k_in):
             if xb.dtype == torch.float32:
-                # the fp32 x itself (_fused_dw): split on chip, three products in one GEMM
+                # the fp32 x itself (_fused_dw): rounded (bf16x3: and split) on chip, one GEMM
                 lib = nat.load()
                 dW = torch.empty((n_out, k_in), dtype=torch.float32, device=xb.device)
                 ws_n = int(lib.hhb_gemm_workspace(n_out, k_in, 32))
                 ws = _workspace(ws_n, xb.device) if ws_n else None
                 nat.check(lib.hhb_gemm_f32b(n_out, k_in, M, hi.data_ptr(), lo.data_ptr(), 2 * P, xb.data_ptr(),
-                                            xb.stride(0), dW.data_ptr(), k_in, 0, D.ptr(ws), _stream()),
+                                            xb.stride(0), 1 if x3 else 0, dW.data_ptr(), k_in, 0, D.ptr(ws),
+                                            _stream()),
                           "hhb_gemm_f32b")
                 return dW
             dW = gemm_ex(A_MN | B_MN, n_out, k_in, M, hi, lo, 2 * P, xb, xb.stride(0))
@@ -334,26 +335,32 @@ def _twin(x):
 
 
 def _fused_convert(x, layer) -> bool:
-    """bf16x3 projection with fp32 x converted and split on chip inside the
+    """bf16x3 projection with the fp32 x converted and split on chip inside the
     GEMM (hhb_gemm_f32a): CTA-pair tiles (>= 512 rows), 8-aligned k_in, n_out a
-    multiple of 4 (16-byte output rows).  The
-    GEMM also writes x_hi / x_lo for the weight gradient.  (The same fusion for
-    the bf16 projection measured slower in the step -- config 3 0.461 -> 0.475
-    ms, config 4 2.437 -> 2.463 ms -- so bf16 keeps the separate cast.)"""
+    multiple of 4 (16-byte output rows).  The bf16 projection keeps the separate
+    cast: with one (forward) or two (weight gradient) products per k-step the
+    conversion is not hidden -- config 3 0.461 -> 0.483 ms, config 4 2.435 ->
+    2.48 ms with both GEMMs converting on chip, 0.475 / 2.463 ms with the
+    projection writing the converted x back."""
     import os
     T, B, k_in = x.shape
-    return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0 and layer.weight.shape[0] % 4 == 0
+    n_out = layer.weight.shape[0]
+    return (layer.proj == "bf16x3" and T * B >= 512 and k_in % 8 == 0 and n_out % 4 == 0
             and os.environ.get("HHB_LAYER_FUSED_SPLIT", "1") != "0")
 
 
-def _fused_dw(x, layer) -> bool:
-    """With the on-chip split projection, the weight gradient also reads the
-    fp32 x and splits it on chip (hhb_gemm_f32b), so the projection need not
-    write x_hi / x_lo: 256-wide CTA-pair tiles (n_out >= 512, k_in > 128)."""
+def _dw_shape_ok(x, layer) -> bool:
     import os
-    T, B, k_in = x.shape
-    return (_fused_convert(x, layer) and layer.weight.shape[0] >= 512 and k_in > 128
+    return (layer.weight.shape[0] >= 512 and x.shape[2] > 128
             and os.environ.get("HHB_LAYER_FUSED_DW", "1") != "0")
+
+
+def _fused_dw(x, layer) -> bool:
+    """With the on-chip conversion in the projection, the weight gradient also
+    reads the fp32 x and converts it on chip (hhb_gemm_f32b), so the projection
+    need not write the converted x: 256-wide CTA-pair tiles (n_out >= 512,
+    k_in > 128)."""
+    return _fused_convert(x, layer) and _dw_shape_ok(x, layer)
 
 
 def _operands(x, weight, layer):

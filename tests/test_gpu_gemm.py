@@ -245,6 +245,31 @@ def test_fp32_a_gemm_converts_on_chip(cuda, M, N, K, bias, splits):
 
 @pytest.mark.parametrize("R,n_out,k_in,splits", [(1024, 512, 384, 0), (4096, 600, 200, 0), (25600, 1024, 784, 0),
                                                  (2048, 512, 784, 3)])
+def test_fp32_b_weight_gradient_gemm_bf16(cuda, R, n_out, k_in, splits):
+    """hhb_gemm_f32b with split_b = 0 (proj="bf16"): (dI_hi + dI_lo)^T bf16(x)
+    equals the dual GEMM over the cast x bit for bit (the same products, in
+    the same k order)."""
+    from paper_2601_21407_b200.layer import A_MN, B_MN, _stream, _workspace, gemm_ex, to_bf16_padded
+    lib = nat.load()
+    g = torch.Generator(device=cuda).manual_seed(R + n_out + 1)
+    dI = torch.randn((R, n_out), device=cuda, generator=g) * 1e-3
+    x = torch.randn((R, k_in), device=cuda, generator=g)
+    hi = dI.to(torch.bfloat16)
+    lo = (dI - hi.float()).to(torch.bfloat16)
+    xb = to_bf16_padded(x)
+    ws = _workspace(int(lib.hhb_gemm_workspace(n_out, k_in, max(splits, 32))), cuda)
+    ref = gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, lo, n_out, xb, xb.stride(0), splits=splits if splits else None)
+    out = torch.empty((n_out, k_in), device=cuda)
+    nat.check(lib.hhb_gemm_f32b(n_out, k_in, R, hi.data_ptr(), lo.data_ptr(), n_out, x.data_ptr(), k_in, 0,
+                                out.data_ptr(), k_in, splits, ws.data_ptr(), _stream()), "f32b")
+    torch.cuda.synchronize()
+    exact = dI.double().T @ x.double()
+    scale = exact.abs().max()
+    assert (out.double() - exact).abs().max() / scale <= 1.01 * (ref.double() - exact).abs().max() / scale + 1e-7
+
+
+@pytest.mark.parametrize("R,n_out,k_in,splits", [(1024, 512, 384, 0), (4096, 600, 200, 0), (25600, 1024, 784, 0),
+                                                 (2048, 512, 784, 3)])
 def test_fp32_b_weight_gradient_gemm(cuda, R, n_out, k_in, splits):
     """hhb_gemm_f32b: dW = (dI_hi + dI_lo)^T x_hi + dI_hi^T x_lo with the fp32 x
     split on chip (MN-major) -- within the error of the two-GEMM composition
@@ -261,7 +286,7 @@ def test_fp32_b_weight_gradient_gemm(cuda, R, n_out, k_in, splits):
     ref += gemm_ex(A_MN | B_MN, n_out, k_in, R, hi, None, n_out, xs3[:, kp:], xs3.stride(0))
     out = torch.empty((n_out, k_in), device=cuda)
     ws = _workspace(int(lib.hhb_gemm_workspace(n_out, k_in, max(splits, 32))), cuda)
-    nat.check(lib.hhb_gemm_f32b(n_out, k_in, R, hi.data_ptr(), lo.data_ptr(), n_out, x.data_ptr(), k_in,
+    nat.check(lib.hhb_gemm_f32b(n_out, k_in, R, hi.data_ptr(), lo.data_ptr(), n_out, x.data_ptr(), k_in, 1,
                                 out.data_ptr(), k_in, splits, ws.data_ptr(), _stream()), "f32b")
     exact = dI.double().T @ x.double()
     scale = exact.abs().max()

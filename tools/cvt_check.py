@@ -131,7 +131,7 @@ def check_f32b(R, n_out, k_in, splits=0):
     out = torch.empty((n_out, k_in), device=dev)
     ws = _workspace(int(lib.hhb_gemm_workspace(n_out, k_in, 32)), dev)
     fn = lambda: nat.check(lib.hhb_gemm_f32b(n_out, k_in, R, hi.data_ptr(), lo.data_ptr(), n_out, xf.data_ptr(),
-                                             k_in, out.data_ptr(), k_in, splits, ws.data_ptr(), _stream()), "f32b")
+                                             k_in, 1, out.data_ptr(), k_in, splits, ws.data_ptr(), _stream()), "f32b")
     fn()
     exact = dI.double().T @ xf.double()
     torch.cuda.synchronize()
