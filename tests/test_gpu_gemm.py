@@ -269,7 +269,7 @@ def test_fp32_b_weight_gradient_gemm_bf16(cuda, R, n_out, k_in, splits):
 
 
 @pytest.mark.parametrize("R,n_out,k_in,splits", [(1024, 512, 384, 0), (4096, 600, 200, 0), (25600, 1024, 784, 0),
-                                                 (2048, 512, 784, 3)])
+                                                 (2048, 512, 784, 3), (1000, 520, 136, 0)])
 def test_fp32_b_weight_gradient_gemm(cuda, R, n_out, k_in, splits):
     """hhb_gemm_f32b: dW = (dI_hi + dI_lo)^T x_hi + dI_hi^T x_lo with the fp32 x
     split on chip (MN-major) -- within the error of the two-GEMM composition
